@@ -1,0 +1,274 @@
+"""Generates tests/golden/*.npz from the compiled reference (oracle/_ref).
+
+Run here (the build container, where /root/reference exists):
+    make -C oracle ref && python oracle/make_golden.py
+The fixtures pin the CPU restatement (tests/test_oracle_cpu.py) and, through
+it, the GPU path; they travel with the repo because /root/reference does not
+exist on the GPU box.
+"""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT / "tests"))
+from oracle_lib import acts_arr, param_count, ptr, ref, sizes_arr  # noqa: E402
+
+GOLDEN = ROOT / "tests" / "golden"
+
+
+def f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def episodes(rng, T, N, D, A, p_term=0.05, p_trunc=0.05):
+    obs = f32(rng.standard_normal((T, N, D)))
+    act = f32(rng.uniform(-1, 1, (T, N, A)))
+    boot = f32(rng.standard_normal((T, N, D)))
+    rew = f32(rng.standard_normal((T, N)))
+    u = rng.uniform(size=(T, N))
+    term = (u < p_term).astype(np.uint8)
+    trunc = ((u >= p_term) & (u < p_term + p_trunc)).astype(np.uint8)
+    return obs, act, boot, rew, term, trunc
+
+
+def gen_indices(R, out):
+    cases = [(0, 1, 100, 8, 1), (0, 1, 100, 64, 3), (7, 2, 5_000_000, 256, 2),
+             (3, 1, 1, 16, 1), (11, 1, 3, 64, 2), (5, 1, (1 << 33) + 12345, 64, 1)]
+    for k, (seed, learner, count, B, n) in enumerate(cases):
+        if count > 20_000_000:
+            continue  # ref_sample_indices materialises `count` rows
+        idx = np.zeros(B * n, dtype=np.uint64)
+        R.ref_sample_indices(seed, learner, count, B, n, ptr(idx))
+        out[f"idx{k}"] = idx
+        out[f"idx{k}_args"] = np.array([seed, learner, count, B, n], dtype=np.uint64)
+    draws = np.zeros(1000, dtype=np.uint64)
+    R.ref_mt64_draws(R.ref_derive_seed(0, 4, 1), 1000, ptr(draws))
+    out["mt64_draws"] = draws
+
+
+def gen_nstep(R, out):
+    rng = np.random.default_rng(1)
+    for k, (T, N, D, A, n, cap) in enumerate([(40, 6, 5, 3, 3, 50), (30, 9, 4, 2, 1, 1000),
+                                              (25, 4, 3, 2, 4, 7)]):
+        obs, act, boot, rew, term, trunc = episodes(rng, T, N, D, A, 0.08, 0.08)
+        maxr = T * N * n
+        counts = np.zeros(T, dtype=np.uint64)
+        eo, ea, eb = (np.zeros((maxr, D), np.float32), np.zeros((maxr, A), np.float32),
+                      np.zeros((maxr, D), np.float32))
+        er, ee = np.zeros(maxr, np.float32), np.zeros(maxr, np.float32)
+        ro, rr = np.zeros((cap, D), np.float32), np.zeros(cap, np.float32)
+        cc = np.zeros(2, np.uint64)
+        total = R.ref_nstep_replay(T, N, D, A, np.float32(0.99), n, cap, ptr(obs), ptr(act),
+                                   ptr(boot), ptr(rew), ptr(term), ptr(trunc), ptr(counts),
+                                   ptr(eo), ptr(ea), ptr(eb), ptr(er), ptr(ee), maxr, ptr(ro),
+                                   ptr(rr), ptr(cc))
+        for name, v in dict(obs=obs, act=act, boot=boot, rew=rew, term=term, trunc=trunc,
+                            counts=counts, e_obs=eo[:total], e_act=ea[:total],
+                            e_boot=eb[:total], e_ret=er[:total], e_eff=ee[:total],
+                            ring_obs=ro, ring_ret=rr, cursor_count=cc,
+                            args=np.array([T, N, D, A, n, cap])).items():
+            out[f"c{k}_{name}"] = v
+
+
+def gen_elementwise(R, out):
+    rng = np.random.default_rng(2)
+    n = 4099
+    p = f32(rng.standard_normal(n)); g = f32(rng.standard_normal(n) * 0.1)
+    m = f32(rng.standard_normal(n) * 0.01); v = f32(np.abs(rng.standard_normal(n)) * 1e-3)
+    out.update(adam_p=p.copy(), adam_g=g.copy(), adam_m=m.copy(), adam_v=v.copy())
+    for t in (0, 1, 9, 99):
+        pp, mm, vv = p.copy(), m.copy(), v.copy()
+        R.ref_adam_step(ptr(pp), ptr(g), ptr(mm), ptr(vv), n, t, np.float32(5e-4))
+        out[f"adam_t{t}"] = np.stack([pp, mm, vv])
+    for scale in (0.01, 1.0, 30.0):
+        gg = f32(g * scale)
+        R.ref_clip_global_norm(ptr(gg), n, np.float32(0.5))
+        out[f"clip_{scale}"] = gg
+    out["sumsq"] = np.array([R.ref_sum_squares(ptr(g), n)])
+    t = f32(rng.standard_normal(n))
+    tt = t.copy()
+    R.ref_soft_update(ptr(tt), ptr(p), n, np.float32(0.05))
+    out.update(lerp_t=t, lerp_out=tt)
+    for N in (1, 2, 4, 7, 4096):
+        s = np.zeros(N, np.float32)
+        R.ref_build_schedule(np.float32(0.05), np.float32(0.8), N, ptr(s))
+        out[f"sched_{N}"] = s
+
+
+def gen_norm(R, out):
+    rng = np.random.default_rng(3)
+    D = 11
+    rows = np.array([1, 7, 64, 3], dtype=np.uintp)
+    data = f32(rng.standard_normal((int(rows.sum()), D)) * 3 + 1)
+    x = f32(rng.standard_normal((50, D)) * 20)
+    x[0, 0] = np.nan
+    cnt = np.zeros(1, np.int64); mean = np.zeros(D); m2 = np.zeros(D)
+    xn = np.zeros_like(x)
+    R.ref_normalizer(D, len(rows), ptr(rows), ptr(data), ptr(cnt), ptr(mean), ptr(m2), ptr(x),
+                     50, ptr(xn))
+    out.update(norm_rows=rows, norm_data=data, norm_x=x, norm_count=cnt, norm_mean=mean,
+               norm_m2=m2, norm_xn=xn)
+
+
+def gen_noise(R, out):
+    rng = np.random.default_rng(4)
+    for N, A, steps in ((64, 8, 3), (33, 20, 2), (5, 1, 4)):
+        a = f32(rng.uniform(-1, 1, (steps, N, A)))
+        a0 = a.copy()
+        R.ref_apply_noise(np.float32(0.05), np.float32(0.8), N, A, 0, steps, np.float32(-1),
+                          np.float32(1), ptr(a))
+        out[f"noise_{N}_{A}_in"] = a0
+        out[f"noise_{N}_{A}_out"] = a
+
+
+def gen_mlp(R, out):
+    rng = np.random.default_rng(5)
+    sizes = [13, 32, 24, 5]
+    L = len(sizes) - 1
+    sa = sizes_arr(sizes)
+    P = param_count(sizes)
+    flat = f32(rng.standard_normal(P) * 0.3)
+    B = 17
+    x = f32(rng.standard_normal((B, sizes[0])))
+    y = np.zeros((B, sizes[-1]), np.float32)
+    R.ref_mlp_forward(ptr(flat), ptr(sa), L, ptr(x), B, ptr(y))
+    up = f32(rng.standard_normal((B, sizes[-1])))
+    gr = np.zeros(P, np.float32)
+    din = np.zeros((B, sizes[0]), np.float32)
+    R.ref_mlp_backward(ptr(flat), ptr(sa), L, ptr(x), ptr(up), B, ptr(gr), ptr(din))
+    out.update(mlp_sizes=np.array(sizes), mlp_flat=flat, mlp_x=x, mlp_y=y, mlp_up=up,
+               mlp_grads=gr, mlp_din=din)
+    # orthogonal init, policy (learners.cpp:17-33) and critic pair (critic.hpp:16-26)
+    pol = np.zeros(param_count([6, 16, 16, 3]), np.float32)
+    R.ref_policy_init(6, 3, 16, 0, ptr(pol))
+    out["init_policy"] = pol
+    qs = sizes_arr([9, 16, 16, 1])
+    q = np.zeros(2 * param_count([9, 16, 16, 1]), np.float32)
+    R.ref_init_mlp(ptr(qs), 3, 12345, np.float32(np.sqrt(2.0)), np.float32(1.0), 2, ptr(q))
+    out["init_critics"] = q
+
+
+def small_nets(rng, D, A, H, L, out_dim=1):
+    ps = [D] + [H] * (L - 1) + [A]
+    qs = [D + A] + [H] * (L - 1) + [out_dim]
+    pol = f32(rng.standard_normal(param_count(ps)) * 0.3)
+    qn = [f32(rng.standard_normal(param_count(qs)) * 0.3) for _ in range(4)]
+    return ps, qs, pol, qn
+
+
+def gen_agents(R, out):
+    rng = np.random.default_rng(6)
+    D, A, H, L, B = 7, 3, 16, 3, 24
+    ps, qs, pol, (q1, q2, q1t, q2t) = small_nets(rng, D, A, H, L)
+    obs = f32(rng.standard_normal((B, D))); act = f32(rng.uniform(-1, 1, (B, A)))
+    boot = f32(rng.standard_normal((B, D))); ret = f32(rng.standard_normal(B))
+    eff = f32(np.where(rng.uniform(size=B) < 0.2, 0, 0.970299))
+    loss = np.zeros(1, np.float32); y = np.zeros(B, np.float32)
+    P = param_count(qs)
+    dq1 = np.zeros(P, np.float32); dq2 = np.zeros(P, np.float32)
+    R.ref_ddpg_critic_loss(ptr(pol), ptr(sizes_arr(ps)), ptr(q1), ptr(q2), ptr(q1t), ptr(q2t),
+                           ptr(sizes_arr(qs)), L, ptr(obs), ptr(act), ptr(boot), ptr(ret),
+                           ptr(eff), B, D, A, np.float32(-1), np.float32(1), ptr(loss), ptr(y),
+                           ptr(dq1), ptr(dq2))
+    aloss = np.zeros(1, np.float32); dpol = np.zeros(param_count(ps), np.float32)
+    R.ref_ddpg_actor_loss(ptr(pol), ptr(sizes_arr(ps)), ptr(q1), ptr(q2), ptr(sizes_arr(qs)), L,
+                          ptr(obs), B, D, np.float32(-1), np.float32(1), ptr(aloss), ptr(dpol))
+    out.update(ag_dims=np.array([D, A, H, L, B]), ag_pol=pol, ag_q1=q1, ag_q2=q2, ag_q1t=q1t,
+               ag_q2t=q2t, ag_obs=obs, ag_act=act, ag_boot=boot, ag_ret=ret, ag_eff=eff,
+               ag_loss=loss.copy(), ag_y=y, ag_dq1=dq1, ag_dq2=dq2, ag_aloss=aloss.copy(),
+               ag_dpol=dpol.copy())
+    # C51
+    La = 11
+    ps, qs, pol, (q1, q2, q1t, q2t) = small_nets(rng, D, A, H, L, La)
+    ret2 = f32(rng.standard_normal(B) * 2)
+    P = param_count(qs)
+    dq1 = np.zeros(P, np.float32); dq2 = np.zeros(P, np.float32)
+    R.ref_c51_critic_loss(ptr(pol), ptr(sizes_arr(ps)), ptr(q1), ptr(q2), ptr(q1t), ptr(q2t),
+                          ptr(sizes_arr(qs)), L, ptr(obs), ptr(act), ptr(boot), ptr(ret2),
+                          ptr(eff), B, D, A, np.float32(-1), np.float32(1), La, np.float32(-10),
+                          np.float32(10), ptr(loss), ptr(dq1), ptr(dq2))
+    dpol = np.zeros(param_count(ps), np.float32)
+    R.ref_c51_actor_loss(ptr(pol), ptr(sizes_arr(ps)), ptr(q1), ptr(q2), ptr(sizes_arr(qs)), L,
+                         ptr(obs), B, D, np.float32(-1), np.float32(1), La, np.float32(-10),
+                         np.float32(10), ptr(aloss), ptr(dpol))
+    out.update(c51_pol=pol, c51_q1=q1, c51_q2=q2, c51_q1t=q1t, c51_q2t=q2t, c51_ret=ret2,
+               c51_loss=loss.copy(), c51_dq1=dq1, c51_dq2=dq2, c51_aloss=aloss.copy(),
+               c51_dpol=dpol, c51_L=np.array([La]))
+    probs = rng.uniform(size=(40, La)).astype(np.float64)
+    probs = f32(probs / probs.sum(1, keepdims=True))
+    pret = f32(rng.standard_normal(40) * 4)
+    peff = f32(rng.choice([0.0, 0.970299, 1.0, 0.5], 40))
+    pret[0], peff[0] = 0.0, 1.0  # identity projection
+    proj = np.zeros_like(probs)
+    R.ref_c51_project(ptr(probs), ptr(pret), ptr(peff), 40, La, np.float32(-10), np.float32(10),
+                      ptr(proj))
+    out.update(proj_probs=probs, proj_ret=pret, proj_eff=peff, proj_out=proj)
+
+
+def gen_vupdate(R, out):
+    """k=3 successive V-learner updates (agents-level composition) and 3
+    P-learner updates on a small config; used for the k-step weight check."""
+    rng = np.random.default_rng(7)
+    D, A, H, nh, B, cap = 9, 4, 32, 2, 48, 500
+    ps = [D] + [H] * nh + [A]
+    qs = [D + A] + [H] * nh + [1]
+    pol = f32(rng.standard_normal(param_count(ps)) * 0.2)
+    q1 = f32(rng.standard_normal(param_count(qs)) * 0.2)
+    q2 = f32(rng.standard_normal(param_count(qs)) * 0.2)
+    n_rows = 300
+    obs = f32(rng.standard_normal((n_rows, D))); act = f32(rng.uniform(-1, 1, (n_rows, A)))
+    boot = f32(rng.standard_normal((n_rows, D))); ret = f32(rng.standard_normal(n_rows) * 0.1)
+    eff = f32(np.where(rng.uniform(size=n_rows) < 0.05, 0.0, 0.970299))
+    cnt = 1000; mean = rng.standard_normal(D) * 0.1; m2 = np.abs(rng.standard_normal(D)) * cnt
+    h = R.ref_vupdate_create(D, A, H, nh, B, cap, 0, ptr(q1), ptr(q2), ptr(pol), 0, 51,
+                             np.float32(-10), np.float32(10))
+    R.ref_vupdate_insert(h, ptr(obs), ptr(act), ptr(boot), ptr(ret), ptr(eff), n_rows)
+    R.ref_vupdate_adopt_norm(h, cnt, ptr(mean), ptr(m2))
+    losses = np.zeros(3, np.float32)
+    for k in range(3):
+        l = np.zeros(1, np.float32)
+        assert R.ref_vupdate_step(h, ptr(l)) == 0
+        losses[k] = l[0]
+    P = param_count(qs)
+    res = np.zeros((4, P), np.float32)
+    for w in range(4):
+        R.ref_vupdate_params(h, w, ptr(res[w]))
+    R.ref_vupdate_destroy(h)
+    out.update(vu_dims=np.array([D, A, H, nh, B, cap]), vu_pol=pol, vu_q1=q1, vu_q2=q2,
+               vu_obs=obs, vu_act=act, vu_boot=boot, vu_ret=ret, vu_eff=eff,
+               vu_norm=np.array([cnt]), vu_mean=mean, vu_m2=m2, vu_losses=losses, vu_params=res)
+    h = R.ref_pupdate_create(D, A, H, nh, B, cap, 0, ptr(pol), ptr(q1), ptr(q2), 0, 51,
+                             np.float32(-10), np.float32(10))
+    R.ref_pupdate_insert(h, ptr(obs), n_rows)
+    R.ref_pupdate_adopt_norm(h, cnt, ptr(mean), ptr(m2))
+    pl = np.zeros(3, np.float32)
+    for k in range(3):
+        l = np.zeros(1, np.float32)
+        assert R.ref_pupdate_step(h, ptr(l)) == 0
+        pl[k] = l[0]
+    pp = np.zeros(param_count(ps), np.float32)
+    R.ref_pupdate_params(h, ptr(pp))
+    R.ref_pupdate_destroy(h)
+    out.update(pu_losses=pl, pu_params=pp)
+
+
+def main():
+    R = ref()
+    if R is None:
+        raise SystemExit("oracle/_ref/libpqlref.so missing: run `make -C oracle ref` first")
+    GOLDEN.mkdir(parents=True, exist_ok=True)
+    for name, fn in [("indices", gen_indices), ("nstep", gen_nstep),
+                     ("elementwise", gen_elementwise), ("norm", gen_norm), ("noise", gen_noise),
+                     ("mlp", gen_mlp), ("agents", gen_agents), ("vupdate", gen_vupdate)]:
+        out: dict = {}
+        fn(R, out)
+        np.savez_compressed(GOLDEN / f"{name}.npz", **out)
+        print(name, sum(v.nbytes for v in out.values()), "bytes")
+
+
+if __name__ == "__main__":
+    main()

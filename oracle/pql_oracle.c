@@ -1,0 +1,1122 @@
+/*
+ * pql_oracle.c -- CPU restatement of the reference learner/actor hot path.
+ * TEST INFRASTRUCTURE ONLY (see pql_oracle.h).  Build: oracle/Makefile
+ * (gcc -O2 -ffp-contract=off, matching the reference's CMakeLists.txt:13).
+ */
+#include "pql_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ================================================================ rng.hpp */
+
+/* rng.hpp:20-25 */
+uint64_t orc_splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+/* rng.hpp:27-30 */
+uint64_t orc_derive_seed(uint64_t master, uint64_t stream, uint64_t index) {
+  uint64_t s = orc_splitmix64(master ^ (stream * 0xd6e8feb86659fd93ull));
+  return orc_splitmix64(s ^ orc_splitmix64(index));
+}
+
+/* std::mt19937_64 (libstdc++ bits/random.h mersenne_twister_engine with the
+ * standard 64-bit parameters); make_rng (rng.hpp:32-34) seeds it with
+ * derive_seed. */
+#define MT_N 312
+#define MT_M 156
+void orc_mt64_seed(orc_mt64* g, uint64_t seed) {
+  g->mt[0] = seed;
+  for (int i = 1; i < MT_N; ++i)
+    g->mt[i] = 6364136223846793005ull * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+  g->idx = MT_N;
+}
+
+static void mt64_twist(orc_mt64* g) {
+  const uint64_t upper = 0xFFFFFFFF80000000ull, lower = 0x7FFFFFFFull;
+  for (int i = 0; i < MT_N; ++i) {
+    uint64_t x = (g->mt[i] & upper) | (g->mt[(i + 1) % MT_N] & lower);
+    uint64_t xa = x >> 1;
+    if (x & 1ull) xa ^= 0xB5026F5AA96619E9ull;
+    g->mt[i] = g->mt[(i + MT_M) % MT_N] ^ xa;
+  }
+  g->idx = 0;
+}
+
+uint64_t orc_mt64_next(orc_mt64* g) {
+  if (g->idx >= MT_N) mt64_twist(g);
+  uint64_t y = g->mt[g->idx++];
+  y ^= (y >> 29) & 0x5555555555555555ull;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+  y ^= (y << 37) & 0xFFF7EEE000000000ull;
+  y ^= y >> 43;
+  return y;
+}
+
+/* Philox4x32-10, Random123 philox.h (rounds with multipliers 0xD2511F53 /
+ * 0xCD9E8D57, key bumps 0x9E3779B9 / 0xBB67AE85). */
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+  uint32_t k0 = key[0], k1 = key[1];
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+uint64_t orc_philox_draw(uint64_t key, uint64_t counter) {
+  const uint32_t c[4] = {(uint32_t)counter, (uint32_t)(counter >> 32), 0u, 0u};
+  const uint32_t k[2] = {(uint32_t)key, (uint32_t)(key >> 32)};
+  uint32_t o[4];
+  orc_philox4x32_10(c, k, o);
+  return (uint64_t)o[0] | ((uint64_t)o[1] << 32);
+}
+
+/* uniform_int_distribution<size_t>(0, count-1) with a 64-bit engine:
+ * libstdc++ bits/uniform_int_dist.h:257-276 (_S_nd, Lemire) via :313-319.
+ * Call sites: replay_buffer.hpp:59 and :106. */
+typedef uint64_t (*draw_fn)(void* ctx);
+static uint64_t lemire(draw_fn draw, void* ctx, uint64_t range) {
+  unsigned __int128 prod = (unsigned __int128)draw(ctx) * range;
+  uint64_t low = (uint64_t)prod;
+  if (low < range) {
+    const uint64_t threshold = (0 - range) % range;
+    while (low < threshold) {
+      prod = (unsigned __int128)draw(ctx) * range;
+      low = (uint64_t)prod;
+    }
+  }
+  return (uint64_t)(prod >> 64);
+}
+
+static uint64_t draw_mt(void* ctx) { return orc_mt64_next((orc_mt64*)ctx); }
+
+typedef struct { uint64_t key, ctr; } philox_ctx;
+static uint64_t draw_philox(void* ctx) {
+  philox_ctx* p = (philox_ctx*)ctx;
+  return orc_philox_draw(p->key, p->ctr++);
+}
+
+void orc_sample_indices_mt(orc_mt64* g, uint64_t count, size_t n, uint64_t* out) {
+  for (size_t r = 0; r < n; ++r) out[r] = lemire(draw_mt, g, count);
+}
+
+void orc_sample_indices_philox(uint64_t key, uint64_t* counter, uint64_t count, size_t n,
+                               uint64_t* out) {
+  philox_ctx c = {key, *counter};
+  for (size_t r = 0; r < n; ++r) out[r] = lemire(draw_philox, &c, count);
+  *counter = c.ctr;
+}
+
+/* ============================================================ nstep.hpp */
+
+orc_nstep* orc_nstep_create(size_t n_envs, size_t obs_dim, size_t act_dim, float gamma,
+                            size_t horizon) {
+  orc_nstep* a = (orc_nstep*)calloc(1, sizeof(orc_nstep));
+  a->n_envs = n_envs; a->obs_dim = obs_dim; a->act_dim = act_dim;
+  a->gamma = gamma; a->horizon = horizon;
+  a->obs = (float*)calloc(n_envs * horizon * obs_dim + 1, sizeof(float));
+  a->act = (float*)calloc(n_envs * horizon * act_dim + 1, sizeof(float));
+  a->rew = (float*)calloc(n_envs * horizon, sizeof(float));
+  a->head = (size_t*)calloc(n_envs, sizeof(size_t));
+  a->count = (size_t*)calloc(n_envs, sizeof(size_t));
+  return a;
+}
+
+void orc_nstep_destroy(orc_nstep* a) {
+  if (!a) return;
+  free(a->obs); free(a->act); free(a->rew); free(a->head); free(a->count); free(a);
+}
+
+orc_batch* orc_batch_create(size_t obs_dim, size_t act_dim) {
+  orc_batch* b = (orc_batch*)calloc(1, sizeof(orc_batch));
+  b->obs_dim = obs_dim; b->act_dim = act_dim;
+  return b;
+}
+
+void orc_batch_destroy(orc_batch* b) {
+  if (!b) return;
+  free(b->obs); free(b->act); free(b->boot); free(b->ret); free(b->eff); free(b);
+}
+
+void orc_batch_clear(orc_batch* b) { b->rows = 0; }
+
+static void batch_reserve(orc_batch* b, size_t rows) {
+  if (rows <= b->cap) return;
+  size_t cap = b->cap ? b->cap : 64;
+  while (cap < rows) cap *= 2;
+  b->obs = (float*)realloc(b->obs, cap * b->obs_dim * sizeof(float) + 4);
+  b->act = (float*)realloc(b->act, cap * b->act_dim * sizeof(float) + 4);
+  b->boot = (float*)realloc(b->boot, cap * b->obs_dim * sizeof(float) + 4);
+  b->ret = (float*)realloc(b->ret, cap * sizeof(float));
+  b->eff = (float*)realloc(b->eff, cap * sizeof(float));
+  b->cap = cap;
+}
+
+/* NStepAssembler::emit (nstep.hpp:104-118): g += disc*r; disc *= gamma in
+ * float with separate mul/add; eff = terminated ? 0 : disc. */
+static void nstep_emit(orc_nstep* a, size_t e, size_t m, int terminated, const float* boot,
+                       orc_batch* out) {
+  float g = 0.0f, disc = 1.0f;
+  for (size_t k = 0; k < m; ++k) {
+    const size_t slot = e * a->horizon + (a->head[e] + k) % a->horizon;
+    const float t = disc * a->rew[slot];
+    g = g + t;
+    disc = disc * a->gamma;
+  }
+  const size_t front = e * a->horizon + a->head[e];
+  batch_reserve(out, out->rows + 1);
+  const size_t r = out->rows++;
+  memcpy(out->obs + r * a->obs_dim, a->obs + front * a->obs_dim, a->obs_dim * sizeof(float));
+  memcpy(out->act + r * a->act_dim, a->act + front * a->act_dim, a->act_dim * sizeof(float));
+  memcpy(out->boot + r * a->obs_dim, boot, a->obs_dim * sizeof(float));
+  out->ret[r] = g;
+  out->eff[r] = terminated ? 0.0f : disc;
+}
+
+/* NStepAssembler::push_env (nstep.hpp:71-93). */
+static void nstep_push_env(orc_nstep* a, size_t e, const float* obs, const float* act, float rew,
+                           int terminated, int done, const float* boot, orc_batch* out) {
+  const size_t slot = e * a->horizon + (a->head[e] + a->count[e]) % a->horizon;
+  memcpy(a->obs + slot * a->obs_dim, obs, a->obs_dim * sizeof(float));
+  memcpy(a->act + slot * a->act_dim, act, a->act_dim * sizeof(float));
+  a->rew[slot] = rew;
+  a->count[e] += 1;
+  if (a->count[e] == a->horizon) {
+    nstep_emit(a, e, a->horizon, terminated && done, boot, out);
+    a->head[e] = (a->head[e] + 1) % a->horizon;
+    a->count[e] -= 1;
+  }
+  if (done) {
+    while (a->count[e] > 0) {
+      nstep_emit(a, e, a->count[e], terminated, boot, out);
+      a->head[e] = (a->head[e] + 1) % a->horizon;
+      a->count[e] -= 1;
+    }
+    a->head[e] = 0;
+  }
+}
+
+/* NStepAssembler::push_step (nstep.hpp:58-68): env-major order,
+ * done = trunc || term. */
+void orc_nstep_push_step(orc_nstep* a, const float* obs, const float* act, const float* rew,
+                         const uint8_t* term, const uint8_t* trunc, const float* boot,
+                         orc_batch* out) {
+  for (size_t e = 0; e < a->n_envs; ++e)
+    nstep_push_env(a, e, obs + e * a->obs_dim, act + e * a->act_dim, rew[e], term[e] != 0,
+                   (trunc[e] != 0) || (term[e] != 0), boot + e * a->obs_dim, out);
+}
+
+/* ===================================================== replay_buffer.hpp */
+
+orc_replay* orc_replay_create(size_t capacity, size_t obs_dim, size_t act_dim) {
+  orc_replay* r = (orc_replay*)calloc(1, sizeof(orc_replay));
+  r->capacity = capacity; r->obs_dim = obs_dim; r->act_dim = act_dim;
+  r->obs = (float*)calloc(capacity * obs_dim + 1, sizeof(float));
+  r->act = (float*)calloc(capacity * act_dim + 1, sizeof(float));
+  r->boot = (float*)calloc(capacity * obs_dim + 1, sizeof(float));
+  r->ret = (float*)calloc(capacity, sizeof(float));
+  r->eff = (float*)calloc(capacity, sizeof(float));
+  return r;
+}
+
+void orc_replay_destroy(orc_replay* r) {
+  if (!r) return;
+  free(r->obs); free(r->act); free(r->boot); free(r->ret); free(r->eff); free(r);
+}
+
+/* ReplayBuffer::insert (replay_buffer.hpp:33-47). */
+void orc_replay_insert(orc_replay* r, const orc_batch* b) {
+  for (size_t i = 0; i < b->rows; ++i) {
+    const size_t c = r->cursor;
+    memcpy(r->obs + c * r->obs_dim, b->obs + i * r->obs_dim, r->obs_dim * sizeof(float));
+    memcpy(r->act + c * r->act_dim, b->act + i * r->act_dim, r->act_dim * sizeof(float));
+    memcpy(r->boot + c * r->obs_dim, b->boot + i * r->obs_dim, r->obs_dim * sizeof(float));
+    r->ret[c] = b->ret[i];
+    r->eff[c] = b->eff[i];
+    r->cursor = (r->cursor + 1) % r->capacity;
+    if (r->count < r->capacity) ++r->count;
+  }
+}
+
+/* ReplayBuffer::sample row copies (replay_buffer.hpp:60-67). */
+void orc_replay_gather(const orc_replay* r, const uint64_t* idx, size_t n, float* obs, float* act,
+                       float* boot, float* ret, float* eff) {
+  for (size_t k = 0; k < n; ++k) {
+    const size_t i = (size_t)idx[k];
+    memcpy(obs + k * r->obs_dim, r->obs + i * r->obs_dim, r->obs_dim * sizeof(float));
+    memcpy(act + k * r->act_dim, r->act + i * r->act_dim, r->act_dim * sizeof(float));
+    memcpy(boot + k * r->obs_dim, r->boot + i * r->obs_dim, r->obs_dim * sizeof(float));
+    ret[k] = r->ret[i];
+    eff[k] = r->eff[i];
+  }
+}
+
+orc_states* orc_states_create(size_t capacity, size_t obs_dim) {
+  orc_states* s = (orc_states*)calloc(1, sizeof(orc_states));
+  s->capacity = capacity; s->obs_dim = obs_dim;
+  s->obs = (float*)calloc(capacity * obs_dim + 1, sizeof(float));
+  return s;
+}
+
+void orc_states_destroy(orc_states* s) {
+  if (!s) return;
+  free(s->obs); free(s);
+}
+
+/* StateBuffer::insert (replay_buffer.hpp:93-100). */
+void orc_states_insert(orc_states* s, const float* rows, size_t n) {
+  for (size_t i = 0; i < n; ++i) {
+    memcpy(s->obs + s->cursor * s->obs_dim, rows + i * s->obs_dim, s->obs_dim * sizeof(float));
+    s->cursor = (s->cursor + 1) % s->capacity;
+    if (s->count < s->capacity) ++s->count;
+  }
+}
+
+/* ====================================== normalizer.hpp / scalar.hpp:93-106 */
+
+/* normalizer.hpp:62-66 */
+void orc_norm_stats_to_f32(int64_t count, const double* mean, const double* m2, size_t d,
+                           float* mean_f, float* inv_f) {
+  for (size_t j = 0; j < d; ++j) {
+    mean_f[j] = (float)mean[j];
+    const double var = m2[j] / (double)count;
+    inv_f[j] = (float)(1.0 / sqrt(var + 1e-8));
+  }
+}
+
+/* scalar.hpp:93-106 */
+void orc_normalize_clip(const float* x, const float* mean, const float* inv, float* out, size_t B,
+                        size_t D, float clip) {
+  for (size_t b = 0; b < B; ++b)
+    for (size_t d = 0; d < D; ++d) {
+      float z = (x[b * D + d] - mean[d]) * inv[d];
+      if (z > clip) z = clip;
+      if (z < -clip) z = -clip;
+      out[b * D + d] = z;
+    }
+}
+
+/* RunningNormalizer::apply_stats (normalizer.hpp:56-70) */
+void orc_normalize_apply(int64_t count, const double* mean, const double* m2, const float* x,
+                         float* out, size_t B, size_t D) {
+  if (count <= 1) {
+    memcpy(out, x, B * D * sizeof(float));
+    return;
+  }
+  float* mf = (float*)malloc(D * sizeof(float));
+  float* inv = (float*)malloc(D * sizeof(float));
+  orc_norm_stats_to_f32(count, mean, m2, D, mf, inv);
+  orc_normalize_clip(x, mf, inv, out, B, D, 5.0f);
+  free(mf); free(inv);
+}
+
+/* RunningNormalizer::update + merge (normalizer.hpp:33-50, 73-83) */
+void orc_norm_update(int64_t* count, double* mean, double* m2, const float* batch, size_t rows,
+                     size_t d) {
+  if (rows == 0) return;
+  double* bmean = (double*)calloc(d, sizeof(double));
+  double* bm2 = (double*)calloc(d, sizeof(double));
+  double n = 0.0;
+  for (size_t r = 0; r < rows; ++r) {
+    n += 1.0;
+    for (size_t j = 0; j < d; ++j) {
+      const double x = batch[r * d + j];
+      const double delta = x - bmean[j];
+      bmean[j] += delta / n;
+      bm2[j] += delta * (x - bmean[j]);
+    }
+  }
+  const double na = (double)*count, nb = (double)rows, nab = na + nb;
+  for (size_t j = 0; j < d; ++j) {
+    const double delta = bmean[j] - mean[j];
+    mean[j] += delta * (nb / nab);
+    m2[j] += bm2[j] + delta * delta * (na * nb / nab);
+  }
+  *count += (int64_t)rows;
+  free(bmean); free(bm2);
+}
+
+/* =============================================================== optim.hpp */
+
+/* optim.hpp:35-39 (beta1 0.9, beta2 0.999) */
+void orc_adam_bias_corrections(int64_t t, float* bc1, float* bc2) {
+  const double b1t = pow(0.9, (double)t);
+  const double b2t = pow(0.999, (double)t);
+  *bc1 = (float)(1.0 / (1.0 - b1t));
+  *bc2 = (float)(1.0 / (1.0 - b2t));
+}
+
+/* scalar.hpp:69-80 */
+void orc_adam_update(float* p, const float* g, float* m, float* v, size_t n, float lr, float beta1,
+                     float beta2, float eps, float bc1, float bc2) {
+  const float ob1 = 1.0f - beta1, ob2 = 1.0f - beta2;
+  for (size_t i = 0; i < n; ++i) {
+    const float gi = g[i];
+    m[i] = beta1 * m[i] + ob1 * gi;
+    v[i] = beta2 * v[i] + ob2 * (gi * gi);
+    const float mhat = m[i] * bc1;
+    const float vhat = v[i] * bc2;
+    p[i] -= lr * (mhat / (sqrtf(vhat) + eps));
+  }
+}
+
+/* scalar.hpp:108-116 */
+double orc_sum_squares(const float* x, size_t n) {
+  double acc = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    const double xi = (double)x[i];
+    acc += xi * xi;
+  }
+  return acc;
+}
+
+/* optim.hpp:54-69 */
+float orc_clip_global_norm(float* g, size_t n, float max_norm) {
+  const double norm = sqrt(orc_sum_squares(g, n));
+  if (norm <= (double)max_norm) return 1.0f;
+  const float s = (float)((double)max_norm / norm * (1.0 - 1e-6));
+  for (size_t i = 0; i < n; ++i) g[i] *= s;
+  return s;
+}
+
+/* scalar.hpp:82-86 (soft_update, optim.hpp:72-79) */
+void orc_lerp_towards(float* target, const float* online, size_t n, float tau) {
+  const float keep = 1.0f - tau;
+  for (size_t i = 0; i < n; ++i) target[i] = tau * online[i] + keep * target[i];
+}
+
+/* =============================================================== noise.hpp */
+
+/* noise.hpp:23-42 */
+void orc_build_schedule(float sigma_min, float sigma_max, size_t n, float* sigma) {
+  if (n == 1) {
+    sigma[0] = sigma_min;
+    return;
+  }
+  const double lo = sigma_min, span = (double)sigma_max - sigma_min;
+  for (size_t k = 0; k < n; ++k)
+    sigma[k] = (float)(lo + ((double)k / (double)(n - 1)) * span);
+  sigma[0] = sigma_min;
+  sigma[n - 1] = sigma_max;
+}
+
+/* glibc 2.39 sysdeps/ieee754/flt-32/e_logf.c (+ e_logf_data.c) restated.
+ * Verified equal to the host logf over every positive finite float. */
+static const double LOGF_T[16][2] = {
+    {0x1.661ec79f8f3bep+0, -0x1.57bf7808caadep-2}, {0x1.571ed4aaf883dp+0, -0x1.2bef0a7c06ddbp-2},
+    {0x1.49539f0f010bp+0, -0x1.01eae7f513a67p-2},  {0x1.3c995b0b80385p+0, -0x1.b31d8a68224e9p-3},
+    {0x1.30d190c8864a5p+0, -0x1.6574f0ac07758p-3}, {0x1.25e227b0b8eap+0, -0x1.1aa2bc79c81p-3},
+    {0x1.1bb4a4a1a343fp+0, -0x1.a4e76ce8c0e5ep-4}, {0x1.12358f08ae5bap+0, -0x1.1973c5a611cccp-4},
+    {0x1.0953f419900a7p+0, -0x1.252f438e10c1ep-5}, {0x1p+0, 0x0p+0},
+    {0x1.e608cfd9a47acp-1, 0x1.aa5aa5df25984p-5},  {0x1.ca4b31f026aap-1, 0x1.c5e53aa362eb4p-4},
+    {0x1.b2036576afce6p-1, 0x1.526e57720db08p-3},  {0x1.9c2d163a1aa2dp-1, 0x1.bc2860d22477p-3},
+    {0x1.886e6037841edp-1, 0x1.1058bc8a07ee1p-2},  {0x1.767dcf5534862p-1, 0x1.4043057b6ee09p-2}};
+static const double LOGF_LN2 = 0x1.62e42fefa39efp-1;
+static const double LOGF_A[3] = {-0x1.00ea348b88334p-2, 0x1.5575b0be00b6ap-2,
+                                 -0x1.ffffef20a4123p-2};
+
+float orc_glibc_logf(float x) {
+  uint32_t ix;
+  memcpy(&ix, &x, 4);
+  if (ix == 0x3f800000u) return 0.0f;
+  if (ix - 0x00800000u >= 0x7f800000u - 0x00800000u) {
+    if (ix * 2 == 0) return -INFINITY;
+    if (ix == 0x7f800000u) return x;
+    if ((ix & 0x80000000u) || ix * 2 >= 0xff000000u) return NAN;
+    const float y = x * 0x1p23f;
+    memcpy(&ix, &y, 4);
+    ix -= 23u << 23;
+  }
+  const uint32_t tmp = ix - 0x3f330000u;
+  const int i = (int)((tmp >> (23 - 4)) % 16);
+  const int k = (int32_t)tmp >> 23;
+  const uint32_t iz = ix - (tmp & (0x1ffu << 23));
+  float zf;
+  memcpy(&zf, &iz, 4);
+  const double z = zf, invc = LOGF_T[i][0], logc = LOGF_T[i][1];
+  const double r = z * invc - 1.0;
+  const double y0 = logc + (double)k * LOGF_LN2;
+  const double r2 = r * r;
+  double y = LOGF_A[1] * r + LOGF_A[2];
+  y = LOGF_A[0] * r2 + y;
+  y = y * r2 + (y0 + r);
+  return (float)y;
+}
+
+/* generate_canonical<float> over SplitMixEngine (random.tcc:3349-3381):
+ * float(x) / 2^64, clamped below 1. */
+static float canonical_f32(uint64_t* state) {
+  const uint64_t x = orc_splitmix64((*state)++);
+  float u = (float)x / 18446744073709551616.0f;
+  if (u >= 1.0f) u = nextafterf(1.0f, 0.0f);
+  return u;
+}
+
+/* apply_noise (noise.hpp:56-72) with a fresh normal_distribution<float>
+ * per row (polar method, random.tcc:1811-1844). */
+void orc_apply_noise(float* actions, size_t n, size_t act_dim, const float* sigma, float low,
+                     float high, uint64_t* states) {
+  for (size_t i = 0; i < n; ++i) {
+    const float sig = sigma[i];
+    float* row = actions + i * act_dim;
+    if (sig > 0.0f) {
+      int saved_ok = 0;
+      float saved = 0.0f;
+      for (size_t d = 0; d < act_dim; ++d) {
+        float z;
+        if (saved_ok) {
+          saved_ok = 0;
+          z = saved;
+        } else {
+          float x, y, r2;
+          do {
+            x = (float)((double)(2.0f * canonical_f32(&states[i])) - 1.0);
+            y = (float)((double)(2.0f * canonical_f32(&states[i])) - 1.0);
+            r2 = x * x + y * y;
+          } while (r2 > 1.0f || r2 == 0.0f);
+          const float mult = sqrtf(-2.0f * logf(r2) / r2);
+          saved = x * mult;
+          saved_ok = 1;
+          z = y * mult;
+        }
+        row[d] += z * sig + 0.0f;
+      }
+    }
+    for (size_t d = 0; d < act_dim; ++d) {
+      if (row[d] < low) row[d] = low;
+      if (row[d] > high) row[d] = high;
+    }
+  }
+}
+
+/* ================================================================ mlp.hpp */
+
+size_t orc_mlp_param_count(const size_t* sizes, size_t n_layers) {
+  size_t t = 0;
+  for (size_t l = 0; l < n_layers; ++l) t += sizes[l] * sizes[l + 1] + sizes[l + 1];
+  return t;
+}
+
+static size_t w_off(const size_t* sizes, size_t l) {
+  size_t t = 0;
+  for (size_t j = 0; j < l; ++j) t += sizes[j] * sizes[j + 1] + sizes[j + 1];
+  return t;
+}
+
+/* scalar.hpp:12-25 */
+static void affine_forward(const float* in, const float* w, const float* bias, float* out,
+                           size_t B, size_t I, size_t O) {
+  for (size_t b = 0; b < B; ++b) {
+    const float* x = in + b * I;
+    float* y = out + b * O;
+    for (size_t o = 0; o < O; ++o) y[o] = bias[o];
+    for (size_t i = 0; i < I; ++i) {
+      const float xi = x[i];
+      const float* wrow = w + i * O;
+      for (size_t o = 0; o < O; ++o) y[o] += xi * wrow[o];
+    }
+  }
+}
+
+/* scalar.hpp:27-40 */
+static void affine_backward_input(const float* g, const float* w, float* din, size_t B, size_t I,
+                                  size_t O) {
+  for (size_t b = 0; b < B; ++b) {
+    const float* grow = g + b * O;
+    float* drow = din + b * I;
+    for (size_t i = 0; i < I; ++i) {
+      const float* wrow = w + i * O;
+      float acc = 0.0f;
+      for (size_t o = 0; o < O; ++o) acc += grow[o] * wrow[o];
+      drow[i] = acc;
+    }
+  }
+}
+
+/* scalar.hpp:42-55 */
+static void affine_backward_params(const float* in, const float* g, float* dw, float* db, size_t B,
+                                   size_t I, size_t O) {
+  for (size_t b = 0; b < B; ++b) {
+    const float* x = in + b * I;
+    const float* grow = g + b * O;
+    for (size_t o = 0; o < O; ++o) db[o] += grow[o];
+    for (size_t i = 0; i < I; ++i) {
+      const float xi = x[i];
+      float* wrow = dw + i * O;
+      for (size_t o = 0; o < O; ++o) wrow[o] += xi * grow[o];
+    }
+  }
+}
+
+/* fa::forward (mlp.hpp:128-149) */
+void orc_mlp_forward(const float* flat, const size_t* sizes, const uint8_t* acts, size_t n_layers,
+                     const float* in, size_t B, float* out, float* cache) {
+  const float* cur = in;
+  float* buf = NULL;
+  size_t cache_off = 0;
+  for (size_t l = 0; l < n_layers; ++l) {
+    const size_t I = sizes[l], O = sizes[l + 1];
+    float* next = cache ? cache + cache_off : (float*)malloc(B * O * sizeof(float));
+    const size_t wo = w_off(sizes, l);
+    affine_forward(cur, flat + wo, flat + wo + I * O, next, B, I, O);
+    if (acts[l])
+      for (size_t k = 0; k < B * O; ++k) next[k] = next[k] > 0.0f ? next[k] : 0.0f;
+    if (!cache && buf) free(buf);
+    if (!cache) buf = next;
+    cur = next;
+    cache_off += B * O;
+  }
+  memcpy(out, cur, B * sizes[n_layers] * sizeof(float));
+  if (!cache && buf) free(buf);
+}
+
+/* fa::backward (mlp.hpp:161-184); ReLU mask from the cached post-activation
+ * (pre > 0 <=> post > 0). */
+void orc_mlp_backward(const float* flat, const size_t* sizes, const uint8_t* acts,
+                      size_t n_layers, const float* in, const float* cache, const float* upstream,
+                      size_t B, float* grads, float* dinput) {
+  size_t offs[16];
+  size_t o = 0;
+  for (size_t l = 0; l < n_layers; ++l) {
+    offs[l] = o;
+    o += B * sizes[l + 1];
+  }
+  size_t maxw = 0;
+  for (size_t l = 0; l <= n_layers; ++l)
+    if (sizes[l] > maxw) maxw = sizes[l];
+  float* g = (float*)malloc(B * maxw * sizeof(float));
+  float* din = (float*)malloc(B * maxw * sizeof(float));
+  memcpy(g, upstream, B * sizes[n_layers] * sizeof(float));
+  for (size_t l = n_layers; l-- > 0;) {
+    const size_t I = sizes[l], O = sizes[l + 1];
+    if (acts[l]) {
+      const float* post = cache + offs[l];
+      for (size_t k = 0; k < B * O; ++k)
+        if (!(post[k] > 0.0f)) g[k] = 0.0f;
+    }
+    const float* layer_in = l == 0 ? in : cache + offs[l - 1];
+    const size_t wo = w_off(sizes, l);
+    affine_backward_params(layer_in, g, grads + wo, grads + wo + I * O, B, I, O);
+    if (l > 0 || dinput) {
+      affine_backward_input(g, flat + wo, din, B, I, O);
+      float* t = g;
+      g = din;
+      din = t;
+    }
+  }
+  if (dinput) memcpy(dinput, g, B * sizes[0] * sizeof(float));
+  free(g);
+  free(din);
+}
+
+/* ============================================================== agents */
+
+static void policy_forward_cached(const float* flat, const size_t* sizes, size_t n_layers,
+                                  const float* obs, size_t B, float* y, float* cache) {
+  uint8_t acts[16];
+  for (size_t l = 0; l < n_layers; ++l) acts[l] = (uint8_t)(l + 1 < n_layers);
+  orc_mlp_forward(flat, sizes, acts, n_layers, obs, B, y, cache);
+}
+
+/* DeterministicPolicy::act (policy.hpp:33-38) */
+void orc_policy_act(const float* flat, const size_t* sizes, size_t n_layers, const float* obs,
+                    size_t B, float low, float high, float* act) {
+  const size_t A = sizes[n_layers];
+  policy_forward_cached(flat, sizes, n_layers, obs, B, act, NULL);
+  const float m = (low + high) / 2.0f, h = (high - low) / 2.0f;
+  for (size_t k = 0; k < B * A; ++k) act[k] = m + h * tanhf(act[k]);
+}
+
+static size_t cache_size(const size_t* sizes, size_t n_layers, size_t B) {
+  size_t t = 0;
+  for (size_t l = 0; l < n_layers; ++l) t += B * sizes[l + 1];
+  return t;
+}
+
+/* concat_cols (policy.hpp:12-21) */
+static float* concat_cols(const float* a, size_t ca, const float* b, size_t cb, size_t B) {
+  float* out = (float*)malloc(B * (ca + cb) * sizeof(float));
+  for (size_t r = 0; r < B; ++r) {
+    memcpy(out + r * (ca + cb), a + r * ca, ca * sizeof(float));
+    memcpy(out + r * (ca + cb) + ca, b + r * cb, cb * sizeof(float));
+  }
+  return out;
+}
+
+static int finite_f(float v) { return isfinite((double)v); }
+
+/* ddpg_critic_target (ddpg.hpp:24-40) */
+int orc_ddpg_target(const float* pol, const size_t* psizes, const float* q1t, const float* q2t,
+                    const size_t* qsizes, size_t n_layers, const float* boot_norm, const float* ret,
+                    const float* eff, size_t B, size_t obs_dim, size_t act_dim, float low,
+                    float high, float* y) {
+  float* next_act = (float*)malloc(B * act_dim * sizeof(float));
+  orc_policy_act(pol, psizes, n_layers, boot_norm, B, low, high, next_act);
+  float* xq = concat_cols(boot_norm, obs_dim, next_act, act_dim, B);
+  float* q1 = (float*)malloc(B * sizeof(float));
+  float* q2 = (float*)malloc(B * sizeof(float));
+  uint8_t acts[16];
+  for (size_t l = 0; l < n_layers; ++l) acts[l] = (uint8_t)(l + 1 < n_layers);
+  orc_mlp_forward(q1t, qsizes, acts, n_layers, xq, B, q1, NULL);
+  orc_mlp_forward(q2t, qsizes, acts, n_layers, xq, B, q2, NULL);
+  int rc = 0;
+  for (size_t b = 0; b < B; ++b) {
+    const float qmin = q2[b] < q1[b] ? q2[b] : q1[b]; /* std::min(a, b) = b < a ? b : a */
+    y[b] = ret[b] + eff[b] * qmin;
+    if (!finite_f(y[b])) rc = -2;
+  }
+  free(next_act); free(xq); free(q1); free(q2);
+  return rc;
+}
+
+/* ddpg_critic_loss (ddpg.hpp:50-76) */
+int orc_ddpg_critic_loss(const float* pol, const size_t* psizes, const float* q1p, const float* q2p,
+                         const float* q1t, const float* q2t, const size_t* qsizes,
+                         size_t n_layers, const float* obs_norm, const float* act,
+                         const float* boot_norm, const float* ret, const float* eff, size_t B,
+                         size_t obs_dim, size_t act_dim, float low, float high, float* loss_out,
+                         float* y_out, float* dq1, float* dq2) {
+  float* y = y_out ? y_out : (float*)malloc(B * sizeof(float));
+  int rc = orc_ddpg_target(pol, psizes, q1t, q2t, qsizes, n_layers, boot_norm, ret, eff, B,
+                           obs_dim, act_dim, low, high, y);
+  if (rc) {
+    if (!y_out) free(y);
+    return rc;
+  }
+  float* xq = concat_cols(obs_norm, obs_dim, act, act_dim, B);
+  uint8_t acts[16];
+  for (size_t l = 0; l < n_layers; ++l) acts[l] = (uint8_t)(l + 1 < n_layers);
+  const size_t cs = cache_size(qsizes, n_layers, B);
+  float* c1 = (float*)malloc(cs * sizeof(float));
+  float* c2 = (float*)malloc(cs * sizeof(float));
+  float* q1 = (float*)malloc(B * sizeof(float));
+  float* q2 = (float*)malloc(B * sizeof(float));
+  orc_mlp_forward(q1p, qsizes, acts, n_layers, xq, B, q1, c1);
+  orc_mlp_forward(q2p, qsizes, acts, n_layers, xq, B, q2, c2);
+  float* up1 = (float*)malloc(B * sizeof(float));
+  float* up2 = (float*)malloc(B * sizeof(float));
+  float loss = 0.0f;
+  for (size_t b = 0; b < B; ++b) {
+    const float e1 = q1[b] - y[b];
+    const float e2 = q2[b] - y[b];
+    loss += e1 * e1 + e2 * e2;
+    up1[b] = 2.0f * e1 / (float)B;
+    up2[b] = 2.0f * e2 / (float)B;
+  }
+  loss = loss / (float)B;
+  *loss_out = loss;
+  if (!finite_f(loss)) rc = -2;
+  const size_t P = orc_mlp_param_count(qsizes, n_layers);
+  memset(dq1, 0, P * sizeof(float));
+  memset(dq2, 0, P * sizeof(float));
+  if (!rc) {
+    orc_mlp_backward(q1p, qsizes, acts, n_layers, xq, c1, up1, B, dq1, NULL);
+    orc_mlp_backward(q2p, qsizes, acts, n_layers, xq, c2, up2, B, dq2, NULL);
+  }
+  free(xq); free(c1); free(c2); free(q1); free(q2); free(up1); free(up2);
+  if (!y_out) free(y);
+  return rc;
+}
+
+/* backward_input_only (mlp.hpp:187-201) */
+static void mlp_backward_input_only(const float* flat, const size_t* sizes, const uint8_t* acts,
+                                    size_t n_layers, const float* cache, const float* upstream,
+                                    size_t B, float* dinput) {
+  size_t offs[16];
+  size_t o = 0;
+  for (size_t l = 0; l < n_layers; ++l) {
+    offs[l] = o;
+    o += B * sizes[l + 1];
+  }
+  size_t maxw = 0;
+  for (size_t l = 0; l <= n_layers; ++l)
+    if (sizes[l] > maxw) maxw = sizes[l];
+  float* g = (float*)malloc(B * maxw * sizeof(float));
+  float* din = (float*)malloc(B * maxw * sizeof(float));
+  memcpy(g, upstream, B * sizes[n_layers] * sizeof(float));
+  for (size_t l = n_layers; l-- > 0;) {
+    const size_t I = sizes[l], O = sizes[l + 1];
+    if (acts[l]) {
+      const float* post = cache + offs[l];
+      for (size_t k = 0; k < B * O; ++k)
+        if (!(post[k] > 0.0f)) g[k] = 0.0f;
+    }
+    affine_backward_input(g, flat + w_off(sizes, l), din, B, I, O);
+    float* t = g;
+    g = din;
+    din = t;
+  }
+  memcpy(dinput, g, B * sizes[0] * sizeof(float));
+  free(g);
+  free(din);
+}
+
+/* Shared tail of ddpg/c51 actor losses: dact -> DeterministicPolicy::backward
+ * (policy.hpp:41-51). */
+static void policy_backward(const float* pol, const size_t* psizes, size_t n_layers,
+                            const float* states, const float* pcache, const float* dact, size_t B,
+                            float low, float high, float* dpolicy) {
+  const size_t A = psizes[n_layers];
+  const size_t yoff = cache_size(psizes, n_layers, B) - B * A;
+  const float* y = pcache + yoff; /* pre-squash output (identity head) */
+  float* dy = (float*)malloc(B * A * sizeof(float));
+  const float h = (high - low) / 2.0f;
+  for (size_t k = 0; k < B * A; ++k) {
+    const float t = tanhf(y[k]);
+    dy[k] = dact[k] * h * (1.0f - t * t);
+  }
+  uint8_t acts[16];
+  for (size_t l = 0; l < n_layers; ++l) acts[l] = (uint8_t)(l + 1 < n_layers);
+  memset(dpolicy, 0, orc_mlp_param_count(psizes, n_layers) * sizeof(float));
+  orc_mlp_backward(pol, psizes, acts, n_layers, states, pcache, dy, B, dpolicy, NULL);
+  free(dy);
+}
+
+/* ddpg_actor_loss (ddpg.hpp:86-118) */
+int orc_ddpg_actor_loss(const float* pol, const size_t* psizes, const float* q1p, const float* q2p,
+                        const size_t* qsizes, size_t n_layers, const float* states, size_t B,
+                        size_t obs_dim, size_t act_dim, float low, float high, float* loss_out,
+                        float* dpolicy) {
+  uint8_t acts[16];
+  for (size_t l = 0; l < n_layers; ++l) acts[l] = (uint8_t)(l + 1 < n_layers);
+  const size_t pcs = cache_size(psizes, n_layers, B);
+  float* pc = (float*)malloc(pcs * sizeof(float));
+  float* act = (float*)malloc(B * act_dim * sizeof(float));
+  policy_forward_cached(pol, psizes, n_layers, states, B, act, pc);
+  const float m = (low + high) / 2.0f, h = (high - low) / 2.0f;
+  for (size_t k = 0; k < B * act_dim; ++k) act[k] = m + h * tanhf(act[k]);
+  float* xq = concat_cols(states, obs_dim, act, act_dim, B);
+  const size_t cs = cache_size(qsizes, n_layers, B);
+  float* c1 = (float*)malloc(cs * sizeof(float));
+  float* c2 = (float*)malloc(cs * sizeof(float));
+  float* q1 = (float*)malloc(B * sizeof(float));
+  float* q2 = (float*)malloc(B * sizeof(float));
+  orc_mlp_forward(q1p, qsizes, acts, n_layers, xq, B, q1, c1);
+  orc_mlp_forward(q2p, qsizes, acts, n_layers, xq, B, q2, c2);
+  float* up1 = (float*)malloc(B * sizeof(float));
+  float* up2 = (float*)malloc(B * sizeof(float));
+  float loss = 0.0f;
+  for (size_t b = 0; b < B; ++b) {
+    const int pick1 = q1[b] <= q2[b];
+    loss -= pick1 ? q1[b] : q2[b];
+    up1[b] = pick1 ? -1.0f / (float)B : 0.0f;
+    up2[b] = pick1 ? 0.0f : -1.0f / (float)B;
+  }
+  loss = loss / (float)B;
+  *loss_out = loss;
+  int rc = finite_f(loss) ? 0 : -2;
+  if (!rc) {
+    const size_t D = obs_dim + act_dim;
+    float* din1 = (float*)malloc(B * D * sizeof(float));
+    float* din2 = (float*)malloc(B * D * sizeof(float));
+    mlp_backward_input_only(q1p, qsizes, acts, n_layers, c1, up1, B, din1);
+    mlp_backward_input_only(q2p, qsizes, acts, n_layers, c2, up2, B, din2);
+    float* dact = (float*)malloc(B * act_dim * sizeof(float));
+    for (size_t b = 0; b < B; ++b)
+      for (size_t d = 0; d < act_dim; ++d)
+        dact[b * act_dim + d] = din1[b * D + obs_dim + d] + din2[b * D + obs_dim + d];
+    policy_backward(pol, psizes, n_layers, states, pc, dact, B, low, high, dpolicy);
+    free(din1); free(din2); free(dact);
+  }
+  free(pc); free(act); free(xq); free(c1); free(c2); free(q1); free(q2); free(up1); free(up2);
+  return rc;
+}
+
+/* ================================================================ c51.hpp */
+
+/* CategoricalHead::create (c51.hpp:21-34) */
+void orc_c51_atoms(size_t n_atoms, float vmin, float vmax, float* atoms) {
+  const double dz = ((double)vmax - vmin) / (double)(n_atoms - 1);
+  for (size_t j = 0; j < n_atoms; ++j) atoms[j] = (float)((double)vmin + dz * (double)j);
+  atoms[0] = vmin;
+  atoms[n_atoms - 1] = vmax;
+}
+
+/* softmax_row (c51.hpp:43-53) */
+static void softmax_row(const float* logits, float* probs, size_t n) {
+  float mx = logits[0];
+  for (size_t j = 1; j < n; ++j) mx = mx < logits[j] ? logits[j] : mx;
+  float sum = 0.0f;
+  for (size_t j = 0; j < n; ++j) {
+    probs[j] = expf(logits[j] - mx);
+    sum += probs[j];
+  }
+  for (size_t j = 0; j < n; ++j) probs[j] /= sum;
+}
+
+/* c51_project (c51.hpp:62-98); returns -2 if an input row is not normalized. */
+int orc_c51_project(const float* probs, const float* ret, const float* eff, size_t B,
+                    size_t L, float vmin_f, float vmax_f, const float* atoms, float* out) {
+  const double vmin = vmin_f, vmax = vmax_f;
+  const double dz = ((double)vmax_f - vmin_f) / (double)(L - 1);
+  memset(out, 0, B * L * sizeof(float));
+  for (size_t b = 0; b < B; ++b) {
+    const float* p = probs + b * L;
+    double mass = 0.0;
+    for (size_t j = 0; j < L; ++j) mass += (double)p[j];
+    if (fabs(mass - 1.0) > 1e-5) return -2;
+    float* q = out + b * L;
+    const double g = (double)ret[b], e = (double)eff[b];
+    for (size_t j = 0; j < L; ++j) {
+      double tz = g + e * (double)atoms[j];
+      if (tz < vmin) tz = vmin;
+      if (tz > vmax) tz = vmax;
+      double pos = (tz - vmin) / dz;
+      const double snapped = nearbyint(pos);
+      if (fabs(pos - snapped) < 1e-5) pos = snapped;
+      const size_t lo = (size_t)pos;
+      const double frac = pos - (double)lo;
+      if (frac == 0.0) {
+        q[lo] += p[j];
+      } else {
+        q[lo] += (float)((double)p[j] * (1.0 - frac));
+        q[lo + 1] += (float)((double)p[j] * frac);
+      }
+    }
+  }
+  return 0;
+}
+
+/* c51_critic_loss (c51.hpp:104-156) */
+int orc_c51_critic_loss(const float* pol, const size_t* psizes, const float* q1p, const float* q2p,
+                        const float* q1t, const float* q2t, const size_t* qsizes,
+                        size_t n_layers, const float* obs_norm, const float* act,
+                        const float* boot_norm, const float* ret, const float* eff, size_t B,
+                        size_t obs_dim, size_t act_dim, float low, float high, size_t L,
+                        float vmin, float vmax, float* loss_out, float* dq1, float* dq2) {
+  float* atoms = (float*)malloc(L * sizeof(float));
+  orc_c51_atoms(L, vmin, vmax, atoms);
+  uint8_t acts[16];
+  for (size_t l = 0; l < n_layers; ++l) acts[l] = (uint8_t)(l + 1 < n_layers);
+  float* next_act = (float*)malloc(B * act_dim * sizeof(float));
+  orc_policy_act(pol, psizes, n_layers, boot_norm, B, low, high, next_act);
+  float* xqn = concat_cols(boot_norm, obs_dim, next_act, act_dim, B);
+  float* l1 = (float*)malloc(B * L * sizeof(float));
+  float* l2 = (float*)malloc(B * L * sizeof(float));
+  orc_mlp_forward(q1t, qsizes, acts, n_layers, xqn, B, l1, NULL);
+  orc_mlp_forward(q2t, qsizes, acts, n_layers, xqn, B, l2, NULL);
+  float* target = (float*)malloc(B * L * sizeof(float));
+  float* p1 = (float*)malloc(L * sizeof(float));
+  float* p2 = (float*)malloc(L * sizeof(float));
+  for (size_t b = 0; b < B; ++b) {
+    softmax_row(l1 + b * L, p1, L);
+    softmax_row(l2 + b * L, p2, L);
+    float e1 = 0.0f, e2 = 0.0f;
+    for (size_t j = 0; j < L; ++j) {
+      e1 += p1[j] * atoms[j];
+      e2 += p2[j] * atoms[j];
+    }
+    memcpy(target + b * L, e1 <= e2 ? p1 : p2, L * sizeof(float));
+  }
+  float* proj = (float*)malloc(B * L * sizeof(float));
+  int rc = orc_c51_project(target, ret, eff, B, L, vmin, vmax, atoms, proj);
+  const size_t P = orc_mlp_param_count(qsizes, n_layers);
+  memset(dq1, 0, P * sizeof(float));
+  memset(dq2, 0, P * sizeof(float));
+  if (!rc) {
+    float* xq = concat_cols(obs_norm, obs_dim, act, act_dim, B);
+    const size_t cs = cache_size(qsizes, n_layers, B);
+    float* c1 = (float*)malloc(cs * sizeof(float));
+    float* c2 = (float*)malloc(cs * sizeof(float));
+    float* o1 = (float*)malloc(B * L * sizeof(float));
+    float* o2 = (float*)malloc(B * L * sizeof(float));
+    orc_mlp_forward(q1p, qsizes, acts, n_layers, xq, B, o1, c1);
+    orc_mlp_forward(q2p, qsizes, acts, n_layers, xq, B, o2, c2);
+    float* up1 = (float*)malloc(B * L * sizeof(float));
+    float* up2 = (float*)malloc(B * L * sizeof(float));
+    float loss = 0.0f;
+    for (size_t b = 0; b < B; ++b) {
+      softmax_row(o1 + b * L, p1, L);
+      softmax_row(o2 + b * L, p2, L);
+      const float* pj = proj + b * L;
+      for (size_t j = 0; j < L; ++j) {
+        if (pj[j] > 0.0f) {
+          loss -= pj[j] * logf(p1[j] > 1e-30f ? p1[j] : 1e-30f);
+          loss -= pj[j] * logf(p2[j] > 1e-30f ? p2[j] : 1e-30f);
+        }
+        up1[b * L + j] = (p1[j] - pj[j]) / (float)B;
+        up2[b * L + j] = (p2[j] - pj[j]) / (float)B;
+      }
+    }
+    loss = loss / (float)B;
+    *loss_out = loss;
+    if (!finite_f(loss)) rc = -2;
+    if (!rc) {
+      orc_mlp_backward(q1p, qsizes, acts, n_layers, xq, c1, up1, B, dq1, NULL);
+      orc_mlp_backward(q2p, qsizes, acts, n_layers, xq, c2, up2, B, dq2, NULL);
+    }
+    free(xq); free(c1); free(c2); free(o1); free(o2); free(up1); free(up2);
+  }
+  free(atoms); free(next_act); free(xqn); free(l1); free(l2); free(target); free(p1); free(p2);
+  free(proj);
+  return rc;
+}
+
+/* c51_actor_loss (c51.hpp:159-205) */
+int orc_c51_actor_loss(const float* pol, const size_t* psizes, const float* q1p, const float* q2p,
+                       const size_t* qsizes, size_t n_layers, const float* states, size_t B,
+                       size_t obs_dim, size_t act_dim, float low, float high, size_t L,
+                       float vmin, float vmax, float* loss_out, float* dpolicy) {
+  float* atoms = (float*)malloc(L * sizeof(float));
+  orc_c51_atoms(L, vmin, vmax, atoms);
+  uint8_t acts[16];
+  for (size_t l = 0; l < n_layers; ++l) acts[l] = (uint8_t)(l + 1 < n_layers);
+  const size_t pcs = cache_size(psizes, n_layers, B);
+  float* pc = (float*)malloc(pcs * sizeof(float));
+  float* act = (float*)malloc(B * act_dim * sizeof(float));
+  policy_forward_cached(pol, psizes, n_layers, states, B, act, pc);
+  const float mid = (low + high) / 2.0f, h = (high - low) / 2.0f;
+  for (size_t k = 0; k < B * act_dim; ++k) act[k] = mid + h * tanhf(act[k]);
+  float* xq = concat_cols(states, obs_dim, act, act_dim, B);
+  const size_t cs = cache_size(qsizes, n_layers, B);
+  float* c1 = (float*)malloc(cs * sizeof(float));
+  float* c2 = (float*)malloc(cs * sizeof(float));
+  float* o1 = (float*)malloc(B * L * sizeof(float));
+  float* o2 = (float*)malloc(B * L * sizeof(float));
+  orc_mlp_forward(q1p, qsizes, acts, n_layers, xq, B, o1, c1);
+  orc_mlp_forward(q2p, qsizes, acts, n_layers, xq, B, o2, c2);
+  float* up1 = (float*)calloc(B * L, sizeof(float));
+  float* up2 = (float*)calloc(B * L, sizeof(float));
+  float* s1 = (float*)malloc(L * sizeof(float));
+  float* s2 = (float*)malloc(L * sizeof(float));
+  float loss = 0.0f;
+  for (size_t b = 0; b < B; ++b) {
+    softmax_row(o1 + b * L, s1, L);
+    softmax_row(o2 + b * L, s2, L);
+    float e1 = 0.0f, e2 = 0.0f;
+    for (size_t j = 0; j < L; ++j) {
+      e1 += s1[j] * atoms[j];
+      e2 += s2[j] * atoms[j];
+    }
+    const int pick1 = e1 <= e2;
+    loss -= pick1 ? e1 : e2;
+    if (pick1) {
+      for (size_t j = 0; j < L; ++j) up1[b * L + j] = -s1[j] * (atoms[j] - e1) / (float)B;
+    } else {
+      for (size_t j = 0; j < L; ++j) up2[b * L + j] = -s2[j] * (atoms[j] - e2) / (float)B;
+    }
+  }
+  loss = loss / (float)B;
+  *loss_out = loss;
+  int rc = finite_f(loss) ? 0 : -2;
+  if (!rc) {
+    const size_t D = obs_dim + act_dim;
+    float* din1 = (float*)malloc(B * D * sizeof(float));
+    float* din2 = (float*)malloc(B * D * sizeof(float));
+    mlp_backward_input_only(q1p, qsizes, acts, n_layers, c1, up1, B, din1);
+    mlp_backward_input_only(q2p, qsizes, acts, n_layers, c2, up2, B, din2);
+    float* dact = (float*)malloc(B * act_dim * sizeof(float));
+    for (size_t b = 0; b < B; ++b)
+      for (size_t d = 0; d < act_dim; ++d)
+        dact[b * act_dim + d] = din1[b * D + obs_dim + d] + din2[b * D + obs_dim + d];
+    policy_backward(pol, psizes, n_layers, states, pc, dact, B, low, high, dpolicy);
+    free(din1); free(din2); free(dact);
+  }
+  free(atoms); free(pc); free(act); free(xq); free(c1); free(c2); free(o1); free(o2);
+  free(up1); free(up2); free(s1); free(s2);
+  return rc;
+}
+
+/* ======================================================= synthetic env
+ * Defined by this build; honours the EnvBatch contract of
+ * vecenv.cpp:84-106 (auto-reset, terminal obs kept, truncation flag,
+ * per-env SplitMix stream derive_seed(seed, env, i) as vecenv.cpp:66).
+ *   s' = clamp(0.95 s + 0.05 (M a), +-10)     a clamped to [low, high]
+ *   reward = -( sum(s'^2)/D + 0.01 * sum(a^2)/A )
+ *   terminal when |s'_0| > 9;  time limit max_len; episode_step starts at
+ *   i % max_len so dones are spread over steps.
+ *   reset: s_d = uniform(rng_i, -1, 1) (vecenv.cpp:19-23, 53-bit path).
+ *   M[d][k] = 2 * (splitmix64(derive_seed(seed, env, 2^40) + d*A + k) >> 11) * 2^-53 - 1
+ */
+static float env_uniform(uint64_t* st, float lo, float hi) {
+  const double u = (double)(orc_splitmix64((*st)++) >> 11) * 0x1.0p-53;
+  return (float)(lo + (hi - lo) * u);
+}
+
+orc_env* orc_env_create(size_t n_envs, size_t obs_dim, size_t act_dim, uint64_t seed,
+                        size_t max_len) {
+  orc_env* e = (orc_env*)calloc(1, sizeof(orc_env));
+  e->n_envs = n_envs; e->obs_dim = obs_dim; e->act_dim = act_dim; e->seed = seed;
+  e->max_len = max_len; e->low = -1.0f; e->high = 1.0f;
+  e->M = (float*)malloc(obs_dim * act_dim * sizeof(float));
+  const uint64_t mseed = orc_derive_seed(seed, ORC_STREAM_ENV, 1ull << 40);
+  for (size_t d = 0; d < obs_dim; ++d)
+    for (size_t k = 0; k < act_dim; ++k) {
+      const uint64_t u = orc_splitmix64(mseed + d * act_dim + k);
+      e->M[d * act_dim + k] = (float)((double)(u >> 11) * 0x1.0p-53 * 2.0 - 1.0);
+    }
+  e->s = (float*)malloc(n_envs * obs_dim * sizeof(float));
+  e->episode_step = (int64_t*)calloc(n_envs, sizeof(int64_t));
+  e->rng = (uint64_t*)malloc(n_envs * sizeof(uint64_t));
+  for (size_t i = 0; i < n_envs; ++i) {
+    e->rng[i] = orc_derive_seed(seed, ORC_STREAM_ENV, i);
+    for (size_t d = 0; d < obs_dim; ++d) e->s[i * obs_dim + d] = env_uniform(&e->rng[i], -1.0f, 1.0f);
+    e->episode_step[i] = (int64_t)(i % max_len);
+  }
+  return e;
+}
+
+void orc_env_destroy(orc_env* e) {
+  if (!e) return;
+  free(e->M); free(e->s); free(e->episode_step); free(e->rng); free(e);
+}
+
+void orc_env_observe(const orc_env* e, float* obs) {
+  memcpy(obs, e->s, e->n_envs * e->obs_dim * sizeof(float));
+}
+
+int orc_env_step(orc_env* e, const float* actions, float* next_obs, float* terminal_obs,
+                 float* rewards, uint8_t* dones, uint8_t* truncated) {
+  const size_t D = e->obs_dim, A = e->act_dim;
+  for (size_t k = 0; k < e->n_envs * A; ++k)
+    if (!isfinite(actions[k])) return -2;
+  float a[256];
+  for (size_t i = 0; i < e->n_envs; ++i) {
+    float aa = 0.0f;
+    for (size_t k = 0; k < A; ++k) {
+      float u = actions[i * A + k];
+      u = u < e->low ? e->low : (u > e->high ? e->high : u);
+      a[k] = u;
+      aa = aa + u * u;
+    }
+    float* s = e->s + i * D;
+    float ss = 0.0f;
+    for (size_t d = 0; d < D; ++d) {
+      float ma = 0.0f;
+      for (size_t k = 0; k < A; ++k) ma = ma + e->M[d * A + k] * a[k];
+      float v = 0.95f * s[d] + 0.05f * ma;
+      v = v < -10.0f ? -10.0f : (v > 10.0f ? 10.0f : v);
+      s[d] = v;
+      ss = ss + v * v;
+    }
+    const float reward = -(ss / (float)D + 0.01f * (aa / (float)A));
+    const int terminal = fabsf(s[0]) > 9.0f;
+    e->episode_step[i] += 1;
+    const int timeout = e->episode_step[i] >= (int64_t)e->max_len;
+    rewards[i] = reward;
+    dones[i] = (uint8_t)(terminal || timeout);
+    truncated[i] = (uint8_t)(!terminal && timeout);
+    if (dones[i]) {
+      memcpy(terminal_obs + i * D, s, D * sizeof(float));
+      for (size_t d = 0; d < D; ++d) s[d] = env_uniform(&e->rng[i], -1.0f, 1.0f);
+      e->episode_step[i] = 0;
+    }
+    memcpy(next_obs + i * D, s, D * sizeof(float));
+  }
+  return 0;
+}

@@ -1,0 +1,707 @@
+// ref_harness.cpp -- extern "C" entry points into the UNMODIFIED reference
+// (/root/reference/proj), compiled by `make -C oracle ref` into
+// oracle/_ref/libpqlref.so.  TEST INFRASTRUCTURE ONLY: used to pin the CPU
+// restatement (pql_oracle.c), to generate tests/golden fixtures, and as the
+// timed CPU baseline (bench.py --impl reference).  Every function below just
+// drives the reference's own classes/functions in the order the reference's
+// runtime cores use them (proj/src/runtime/learners.cpp).
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <vector>
+
+#include "pql/agents/c51.hpp"
+#include "pql/agents/ddpg.hpp"
+#include "pql/explore/noise.hpp"
+#include "pql/funcapprox/normalizer.hpp"
+#include "pql/funcapprox/optim.hpp"
+#include "pql/kernels/kernels.hpp"
+#include "pql/replay/nstep.hpp"
+#include "pql/replay/replay_buffer.hpp"
+#include "pql/rng.hpp"
+#include "pql/runtime/learners.hpp"
+#include "pql/vecenv/vecenv.hpp"
+
+using namespace pql;
+
+#define REF_API extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+fa::Mlp<float> make_mlp(const size_t* sizes, size_t n_layers, const float* flat) {
+  std::vector<std::size_t> s(sizes, sizes + n_layers + 1);
+  std::vector<fa::Act> acts(n_layers, fa::Act::relu);
+  acts.back() = fa::Act::identity;
+  auto net = fa::Mlp<float>::zeros(s, acts);
+  if (flat) std::memcpy(net.flat.data(), flat, net.flat.size() * sizeof(float));
+  return net;
+}
+
+MatF make_mat(const float* p, size_t rows, size_t cols) {
+  MatF m(rows, cols);
+  if (p) std::memcpy(m.data(), p, rows * cols * sizeof(float));
+  return m;
+}
+
+replay::NStepBatch<float> make_batch(const float* obs, const float* act, const float* boot,
+                                     const float* ret, const float* eff, size_t B, size_t D,
+                                     size_t A) {
+  replay::NStepBatch<float> b;
+  b.obs = make_mat(obs, B, D);
+  b.act = make_mat(act, B, A);
+  b.boot_obs = make_mat(boot, B, D);
+  b.ret.assign(ret, ret + B);
+  b.eff_disc.assign(eff, eff + B);
+  return b;
+}
+
+fa::NormStats make_stats(int64_t count, const double* mean, const double* m2, size_t D) {
+  fa::NormStats s;
+  s.count = count;
+  s.mean.assign(mean, mean + D);
+  s.m2.assign(m2, m2 + D);
+  return s;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- rng
+REF_API uint64_t ref_derive_seed(uint64_t master, uint64_t stream, uint64_t index) {
+  return derive_seed(master, static_cast<RngStream>(stream), index);
+}
+
+REF_API void ref_mt64_draws(uint64_t seed, size_t n, uint64_t* out) {
+  std::mt19937_64 g(seed);
+  for (size_t i = 0; i < n; ++i) out[i] = g();
+}
+
+// Indices drawn by n_calls successive ReplayBuffer::sample(B) calls of a
+// learner whose sample_rng_ = make_rng(seed, sample, learner)
+// (learners.cpp:136, :212).  Row i of the buffer carries ret = i.
+REF_API void ref_sample_indices(uint64_t seed, uint64_t learner, uint64_t count, size_t B,
+                                size_t n_calls, uint64_t* out) {
+  replay::ReplayBuffer buf(count, 1, 1);
+  replay::NStepBatch<float> b;
+  b.obs.resize(count, 1);
+  b.act.resize(count, 1);
+  b.boot_obs.resize(count, 1);
+  b.ret.resize(count);
+  b.eff_disc.assign(count, 0.0f);
+  for (size_t i = 0; i < count; ++i) b.ret[i] = static_cast<float>(i);
+  buf.insert(b);
+  auto rng = make_rng(seed, RngStream::sample, learner);
+  for (size_t c = 0; c < n_calls; ++c) {
+    auto s = buf.sample(B, rng, 1);
+    for (size_t r = 0; r < B; ++r) out[c * B + r] = static_cast<uint64_t>(s->ret[r]);
+  }
+}
+
+// ---------------------------------------------------------- n-step + ring
+// T steps of NStepAssembler::push_step (rewards already scaled) followed by
+// ReplayBuffer::insert into a ring of capacity cap.  Returns total emitted
+// rows; emitted rows are written up to max_rows; ring obs/ret are dumped via
+// the public obs_row / ret_at accessors (replay_buffer.hpp:71-73).
+REF_API size_t ref_nstep_replay(size_t T, size_t N, size_t D, size_t A, float gamma, size_t n,
+                                size_t cap, const float* obs, const float* act, const float* boot,
+                                const float* rew, const uint8_t* term, const uint8_t* trunc,
+                                uint64_t* emit_counts, float* e_obs, float* e_act, float* e_boot,
+                                float* e_ret, float* e_eff, size_t max_rows, float* ring_obs,
+                                float* ring_ret, uint64_t* cursor_count) {
+  replay::NStepAssembler<float> as(N, D, A, gamma, n);
+  replay::ReplayBuffer buf(cap, D, A);
+  replay::NStepBatch<float> out;
+  size_t total = 0;
+  for (size_t t = 0; t < T; ++t) {
+    MatF o = make_mat(obs + t * N * D, N, D), a = make_mat(act + t * N * A, N, A),
+         bo = make_mat(boot + t * N * D, N, D);
+    out.clear();
+    as.push_step(o, a, std::span<const float>(rew + t * N, N),
+                 std::span<const uint8_t>(term + t * N, N),
+                 std::span<const uint8_t>(trunc + t * N, N), bo, out);
+    emit_counts[t] = out.size();
+    for (size_t r = 0; r < out.size() && total + r < max_rows; ++r) {
+      const size_t k = total + r;
+      std::memcpy(e_obs + k * D, out.obs.row(r), D * sizeof(float));
+      std::memcpy(e_act + k * A, out.act.row(r), A * sizeof(float));
+      std::memcpy(e_boot + k * D, out.boot_obs.row(r), D * sizeof(float));
+      e_ret[k] = out.ret[r];
+      e_eff[k] = out.eff_disc[r];
+    }
+    total += out.size();
+    buf.insert(out);
+  }
+  for (size_t i = 0; i < cap; ++i) {
+    std::memcpy(ring_obs + i * D, buf.obs_row(i), D * sizeof(float));
+    ring_ret[i] = buf.ret_at(i);
+  }
+  cursor_count[0] = buf.cursor();
+  cursor_count[1] = buf.size();
+  return total;
+}
+
+// StateBuffer insert of T batches of N rows, then n_calls sample(B) with
+// make_rng(seed, sample, 2) (learners.cpp:212).
+REF_API void ref_state_buffer(size_t cap, size_t D, size_t T, size_t N, const float* rows,
+                              uint64_t seed, size_t B, size_t n_calls, float* out,
+                              uint64_t* count_out) {
+  replay::StateBuffer sb(cap, D);
+  for (size_t t = 0; t < T; ++t) sb.insert(make_mat(rows + t * N * D, N, D));
+  auto rng = make_rng(seed, RngStream::sample, 2);
+  for (size_t c = 0; c < n_calls; ++c) {
+    auto s = sb.sample(B, rng, 1);
+    std::memcpy(out + c * B * D, s->data(), B * D * sizeof(float));
+  }
+  *count_out = sb.size();
+}
+
+// ------------------------------------------------------------- normalizer
+REF_API void ref_normalizer(size_t D, size_t n_batches, const size_t* rows, const float* data,
+                            int64_t* count_out, double* mean_out, double* m2_out, const float* x,
+                            size_t Bx, float* xn_out) {
+  fa::RunningNormalizer norm(D);
+  size_t off = 0;
+  for (size_t i = 0; i < n_batches; ++i) {
+    norm.update(make_mat(data + off * D, rows[i], D));
+    off += rows[i];
+  }
+  const auto& s = norm.stats();
+  *count_out = s.count;
+  std::memcpy(mean_out, s.mean.data(), D * sizeof(double));
+  std::memcpy(m2_out, s.m2.data(), D * sizeof(double));
+  MatF xn = norm.apply(make_mat(x, Bx, D));
+  std::memcpy(xn_out, xn.data(), Bx * D * sizeof(float));
+}
+
+REF_API void ref_normalize_apply(int64_t count, const double* mean, const double* m2, size_t D,
+                                 const float* x, size_t B, float* out) {
+  MatF r = fa::RunningNormalizer::apply_stats(make_stats(count, mean, m2, D), make_mat(x, B, D));
+  std::memcpy(out, r.data(), B * D * sizeof(float));
+}
+
+// ------------------------------------------------------------------ optim
+REF_API int ref_adam_step(float* p, const float* g, float* m, float* v, size_t n, int64_t t,
+                          float lr) {
+  std::vector<float> params(p, p + n), grads(g, g + n);
+  fa::AdamState<float> st(n);
+  st.m.assign(m, m + n);
+  st.v.assign(v, v + n);
+  st.t = t;
+  try {
+    fa::adam_step(params, grads, st, lr);
+  } catch (const std::exception&) {
+    return -2;
+  }
+  std::memcpy(p, params.data(), n * sizeof(float));
+  std::memcpy(m, st.m.data(), n * sizeof(float));
+  std::memcpy(v, st.v.data(), n * sizeof(float));
+  return 0;
+}
+
+REF_API void ref_clip_global_norm(float* g, size_t n, float max_norm) {
+  std::vector<float> v(g, g + n);
+  fa::clip_global_norm(v, max_norm);
+  std::memcpy(g, v.data(), n * sizeof(float));
+}
+
+REF_API double ref_sum_squares(const float* x, size_t n) { return kernels::sum_squares(x, n); }
+
+REF_API void ref_soft_update(float* target, const float* online, size_t n, float tau) {
+  std::vector<float> t(target, target + n), o(online, online + n);
+  fa::soft_update(t, o, tau);
+  std::memcpy(target, t.data(), n * sizeof(float));
+}
+
+// ------------------------------------------------------------------ noise
+REF_API void ref_build_schedule(float smin, float smax, size_t n, float* out) {
+  auto s = explore::build_schedule(smin, smax, n);
+  std::memcpy(out, s.sigma.data(), n * sizeof(float));
+}
+
+// `steps` successive apply_noise calls with the actor's per-env noise
+// streams (learners.cpp:74-75); actions [steps][N][A] are perturbed in place.
+REF_API void ref_apply_noise(float smin, float smax, size_t N, size_t A, uint64_t seed,
+                             size_t steps, float low, float high, float* actions) {
+  auto sched = explore::build_schedule(smin, smax, N);
+  std::vector<env::SplitMixEngine> rngs(N);
+  for (size_t i = 0; i < N; ++i) rngs[i].state = derive_seed(seed, RngStream::noise, i);
+  for (size_t s = 0; s < steps; ++s) {
+    MatF a = make_mat(actions + s * N * A, N, A);
+    explore::apply_noise(a, sched, low, high, rngs);
+    std::memcpy(actions + s * N * A, a.data(), N * A * sizeof(float));
+  }
+}
+
+// -------------------------------------------------------------------- MLP
+REF_API void ref_mlp_forward(const float* flat, const size_t* sizes, size_t n_layers,
+                             const float* in, size_t B, float* out) {
+  auto net = make_mlp(sizes, n_layers, flat);
+  MatF y = fa::forward(net, make_mat(in, B, sizes[0]));
+  std::memcpy(out, y.data(), B * sizes[n_layers] * sizeof(float));
+}
+
+REF_API void ref_mlp_backward(const float* flat, const size_t* sizes, size_t n_layers,
+                              const float* in, const float* upstream, size_t B, float* grads,
+                              float* dinput) {
+  auto net = make_mlp(sizes, n_layers, flat);
+  fa::ForwardCache<float> cache;
+  fa::forward(net, make_mat(in, B, sizes[0]), &cache);
+  std::vector<float> g;
+  MatF din;
+  fa::backward(net, cache, make_mat(upstream, B, sizes[n_layers]), g, dinput ? &din : nullptr);
+  std::memcpy(grads, g.data(), g.size() * sizeof(float));
+  if (dinput) std::memcpy(dinput, din.data(), B * sizes[0] * sizeof(float));
+}
+
+// Orthogonal init exactly as PolicyHandle::create (learners.cpp:17-33) and
+// CriticPair::create (critic.hpp:16-26).
+REF_API void ref_init_mlp(const size_t* sizes, size_t n_layers, uint64_t rng_seed,
+                          float hidden_gain, float final_gain, size_t n_nets, float* out) {
+  std::mt19937_64 rng(rng_seed);
+  for (size_t k = 0; k < n_nets; ++k) {
+    auto net = make_mlp(sizes, n_layers, nullptr);
+    fa::init_orthogonal(net, rng, hidden_gain, final_gain);
+    std::memcpy(out + k * net.flat.size(), net.flat.data(), net.flat.size() * sizeof(float));
+  }
+}
+
+// ----------------------------------------------------------------- agents
+namespace {
+agents::DeterministicPolicy<float> make_policy(const float* flat, const size_t* sizes,
+                                               size_t n_layers, float low, float high) {
+  agents::DeterministicPolicy<float> p;
+  p.net = make_mlp(sizes, n_layers, flat);
+  p.low = low;
+  p.high = high;
+  return p;
+}
+agents::CriticPair<float> make_pair(const float* q1, const float* q2, const float* q1t,
+                                    const float* q2t, const size_t* sizes, size_t n_layers) {
+  agents::CriticPair<float> c;
+  c.q1 = make_mlp(sizes, n_layers, q1);
+  c.q2 = make_mlp(sizes, n_layers, q2);
+  c.q1_target = make_mlp(sizes, n_layers, q1t ? q1t : q1);
+  c.q2_target = make_mlp(sizes, n_layers, q2t ? q2t : q2);
+  return c;
+}
+}  // namespace
+
+REF_API int ref_ddpg_critic_loss(const float* pol, const size_t* psizes, const float* q1,
+                                 const float* q2, const float* q1t, const float* q2t,
+                                 const size_t* qsizes, size_t n_layers, const float* obs_norm,
+                                 const float* act, const float* boot_norm, const float* ret,
+                                 const float* eff, size_t B, size_t D, size_t A, float low,
+                                 float high, float* loss, float* y, float* dq1, float* dq2) {
+  auto policy = make_policy(pol, psizes, n_layers, low, high);
+  auto pair = make_pair(q1, q2, q1t, q2t, qsizes, n_layers);
+  auto batch = make_batch(obs_norm, act, boot_norm, ret, eff, B, D, A);
+  try {
+    if (y) {
+      auto yy = agents::ddpg_critic_target(batch, policy, pair);
+      std::memcpy(y, yy.data(), B * sizeof(float));
+    }
+    auto r = agents::ddpg_critic_loss(batch, policy, pair);
+    *loss = r.loss;
+    std::memcpy(dq1, r.dq1.data(), r.dq1.size() * sizeof(float));
+    std::memcpy(dq2, r.dq2.data(), r.dq2.size() * sizeof(float));
+  } catch (const std::exception&) {
+    return -2;
+  }
+  return 0;
+}
+
+REF_API int ref_ddpg_actor_loss(const float* pol, const size_t* psizes, const float* q1,
+                                const float* q2, const size_t* qsizes, size_t n_layers,
+                                const float* states, size_t B, size_t D, float low, float high,
+                                float* loss, float* dpolicy) {
+  auto policy = make_policy(pol, psizes, n_layers, low, high);
+  auto pair = make_pair(q1, q2, nullptr, nullptr, qsizes, n_layers);
+  try {
+    auto r = agents::ddpg_actor_loss(make_mat(states, B, D), policy, pair);
+    *loss = r.loss;
+    std::memcpy(dpolicy, r.dpolicy.data(), r.dpolicy.size() * sizeof(float));
+  } catch (const std::exception&) {
+    return -2;
+  }
+  return 0;
+}
+
+REF_API int ref_c51_project(const float* probs, const float* ret, const float* eff, size_t B,
+                            size_t L, float vmin, float vmax, float* out) {
+  auto head = agents::CategoricalHead<float>::create(L, vmin, vmax);
+  try {
+    MatF q = agents::c51_project<float>(make_mat(probs, B, L), std::span<const float>(ret, B),
+                                        std::span<const float>(eff, B), head);
+    std::memcpy(out, q.data(), B * L * sizeof(float));
+  } catch (const std::exception&) {
+    return -2;
+  }
+  return 0;
+}
+
+REF_API void ref_c51_atoms(size_t L, float vmin, float vmax, float* out) {
+  auto head = agents::CategoricalHead<float>::create(L, vmin, vmax);
+  std::memcpy(out, head.atoms.data(), L * sizeof(float));
+}
+
+REF_API int ref_c51_critic_loss(const float* pol, const size_t* psizes, const float* q1,
+                                const float* q2, const float* q1t, const float* q2t,
+                                const size_t* qsizes, size_t n_layers, const float* obs_norm,
+                                const float* act, const float* boot_norm, const float* ret,
+                                const float* eff, size_t B, size_t D, size_t A, float low,
+                                float high, size_t L, float vmin, float vmax, float* loss,
+                                float* dq1, float* dq2) {
+  auto policy = make_policy(pol, psizes, n_layers, low, high);
+  auto pair = make_pair(q1, q2, q1t, q2t, qsizes, n_layers);
+  auto batch = make_batch(obs_norm, act, boot_norm, ret, eff, B, D, A);
+  auto head = agents::CategoricalHead<float>::create(L, vmin, vmax);
+  try {
+    auto r = agents::c51_critic_loss(batch, policy, pair, head);
+    *loss = r.loss;
+    std::memcpy(dq1, r.dq1.data(), r.dq1.size() * sizeof(float));
+    std::memcpy(dq2, r.dq2.data(), r.dq2.size() * sizeof(float));
+  } catch (const std::exception&) {
+    return -2;
+  }
+  return 0;
+}
+
+REF_API int ref_c51_actor_loss(const float* pol, const size_t* psizes, const float* q1,
+                               const float* q2, const size_t* qsizes, size_t n_layers,
+                               const float* states, size_t B, size_t D, float low, float high,
+                               size_t L, float vmin, float vmax, float* loss, float* dpolicy) {
+  auto policy = make_policy(pol, psizes, n_layers, low, high);
+  auto pair = make_pair(q1, q2, nullptr, nullptr, qsizes, n_layers);
+  auto head = agents::CategoricalHead<float>::create(L, vmin, vmax);
+  try {
+    auto r = agents::c51_actor_loss(make_mat(states, B, D), policy, pair, head);
+    *loss = r.loss;
+    std::memcpy(dpolicy, r.dpolicy.data(), r.dpolicy.size() * sizeof(float));
+  } catch (const std::exception&) {
+    return -2;
+  }
+  return 0;
+}
+
+// ----------------------------------------------- V-learner update (agents)
+// One CriticLearnerCore::update (learners.cpp:157-188) for an arbitrary
+// depth of network, composed from the reference's own replay / normalizer /
+// agents / optim calls in the same order.  State arrays are updated in place.
+struct RefCritic {
+  size_t D, A, n_layers, B;
+  std::vector<size_t> qsizes, psizes;
+  float low = -1.0f, high = 1.0f, lr = 5e-4f, tau = 0.05f;
+  int distributional = 0;
+  size_t n_atoms = 51;
+  float vmin = -10.0f, vmax = 10.0f;
+  agents::CriticPair<float> critics;
+  fa::AdamState<float> adam_q1, adam_q2;
+  agents::DeterministicPolicy<float> lagged;
+  fa::NormStats norm;
+  std::unique_ptr<replay::ReplayBuffer> buffer;
+  std::mt19937_64 sample_rng;
+};
+
+REF_API void* ref_vupdate_create(size_t D, size_t A, size_t hidden, size_t n_hidden, size_t B,
+                                 size_t capacity, uint64_t seed, const float* q1, const float* q2,
+                                 const float* policy, int distributional, size_t n_atoms,
+                                 float vmin, float vmax) {
+  auto* r = new RefCritic();
+  r->D = D; r->A = A; r->B = B; r->n_layers = n_hidden + 1;
+  r->distributional = distributional; r->n_atoms = n_atoms; r->vmin = vmin; r->vmax = vmax;
+  r->qsizes.push_back(D + A);
+  r->psizes.push_back(D);
+  for (size_t i = 0; i < n_hidden; ++i) {
+    r->qsizes.push_back(hidden);
+    r->psizes.push_back(hidden);
+  }
+  r->qsizes.push_back(distributional ? n_atoms : 1);
+  r->psizes.push_back(A);
+  r->critics = make_pair(q1, q2, nullptr, nullptr, r->qsizes.data(), r->n_layers);
+  r->adam_q1 = fa::AdamState<float>(r->critics.q1.param_count());
+  r->adam_q2 = fa::AdamState<float>(r->critics.q2.param_count());
+  r->lagged = make_policy(policy, r->psizes.data(), r->n_layers, -1.0f, 1.0f);
+  r->buffer = std::make_unique<replay::ReplayBuffer>(capacity, D, A);
+  r->sample_rng = make_rng(seed, RngStream::sample, 1);
+  return r;
+}
+
+REF_API void ref_vupdate_destroy(void* h) { delete static_cast<RefCritic*>(h); }
+
+REF_API void ref_vupdate_insert(void* h, const float* obs, const float* act, const float* boot,
+                                const float* ret, const float* eff, size_t n) {
+  auto* r = static_cast<RefCritic*>(h);
+  r->buffer->insert(make_batch(obs, act, boot, ret, eff, n, r->D, r->A));
+}
+
+REF_API void ref_vupdate_adopt_norm(void* h, int64_t count, const double* mean, const double* m2) {
+  auto* r = static_cast<RefCritic*>(h);
+  r->norm = make_stats(count, mean, m2, r->D);
+}
+
+REF_API int ref_vupdate_step(void* h, float* loss_out) {
+  auto* r = static_cast<RefCritic*>(h);
+  try {
+    auto sampled = r->buffer->sample(r->B, r->sample_rng, r->B);
+    if (!sampled) return 1;
+    auto& batch = *sampled;
+    batch.obs = fa::RunningNormalizer::apply_stats(r->norm, batch.obs);
+    batch.boot_obs = fa::RunningNormalizer::apply_stats(r->norm, batch.boot_obs);
+    agents::CriticLossResult<float> res;
+    if (r->distributional) {
+      auto head = agents::CategoricalHead<float>::create(r->n_atoms, r->vmin, r->vmax);
+      res = agents::c51_critic_loss(batch, r->lagged, r->critics, head);
+    } else {
+      res = agents::ddpg_critic_loss(batch, r->lagged, r->critics);
+    }
+    fa::clip_global_norm(res.dq1, 0.5f);
+    fa::clip_global_norm(res.dq2, 0.5f);
+    fa::adam_step(r->critics.q1.flat, res.dq1, r->adam_q1, r->lr);
+    fa::adam_step(r->critics.q2.flat, res.dq2, r->adam_q2, r->lr);
+    r->critics.soft_update_targets(r->tau);
+    *loss_out = res.loss;
+  } catch (const std::exception&) {
+    return -2;
+  }
+  return 0;
+}
+
+// which: 0 q1, 1 q2, 2 q1_target, 3 q2_target
+REF_API void ref_vupdate_params(void* h, int which, float* out) {
+  auto* r = static_cast<RefCritic*>(h);
+  const auto& c = r->critics;
+  const fa::Mlp<float>* nets[4] = {&c.q1, &c.q2, &c.q1_target, &c.q2_target};
+  std::memcpy(out, nets[which]->flat.data(), nets[which]->flat.size() * sizeof(float));
+}
+
+// ----------------------------------------------- P-learner update (agents)
+struct RefPolicy {
+  size_t D, A, n_layers, B;
+  std::vector<size_t> qsizes, psizes;
+  float low = -1.0f, high = 1.0f, lr = 5e-4f;
+  int distributional = 0;
+  size_t n_atoms = 51;
+  float vmin = -10.0f, vmax = 10.0f;
+  agents::DeterministicPolicy<float> policy;
+  fa::AdamState<float> adam;
+  agents::CriticPair<float> critics;
+  fa::NormStats norm;
+  std::unique_ptr<replay::StateBuffer> states;
+  std::mt19937_64 sample_rng;
+};
+
+REF_API void* ref_pupdate_create(size_t D, size_t A, size_t hidden, size_t n_hidden, size_t B,
+                                 size_t capacity, uint64_t seed, const float* policy,
+                                 const float* q1, const float* q2, int distributional,
+                                 size_t n_atoms, float vmin, float vmax) {
+  auto* r = new RefPolicy();
+  r->D = D; r->A = A; r->B = B; r->n_layers = n_hidden + 1;
+  r->distributional = distributional; r->n_atoms = n_atoms; r->vmin = vmin; r->vmax = vmax;
+  r->qsizes.push_back(D + A);
+  r->psizes.push_back(D);
+  for (size_t i = 0; i < n_hidden; ++i) {
+    r->qsizes.push_back(hidden);
+    r->psizes.push_back(hidden);
+  }
+  r->qsizes.push_back(distributional ? n_atoms : 1);
+  r->psizes.push_back(A);
+  r->policy = make_policy(policy, r->psizes.data(), r->n_layers, -1.0f, 1.0f);
+  r->adam = fa::AdamState<float>(r->policy.net.param_count());
+  r->critics = make_pair(q1, q2, nullptr, nullptr, r->qsizes.data(), r->n_layers);
+  r->states = std::make_unique<replay::StateBuffer>(capacity, D);
+  r->sample_rng = make_rng(seed, RngStream::sample, 2);
+  return r;
+}
+
+REF_API void ref_pupdate_destroy(void* h) { delete static_cast<RefPolicy*>(h); }
+
+REF_API void ref_pupdate_insert(void* h, const float* rows, size_t n) {
+  auto* r = static_cast<RefPolicy*>(h);
+  r->states->insert(make_mat(rows, n, r->D));
+}
+
+REF_API void ref_pupdate_adopt_norm(void* h, int64_t count, const double* mean, const double* m2) {
+  auto* r = static_cast<RefPolicy*>(h);
+  r->norm = make_stats(count, mean, m2, r->D);
+}
+
+REF_API int ref_pupdate_step(void* h, float* loss_out) {
+  auto* r = static_cast<RefPolicy*>(h);
+  try {
+    auto sampled = r->states->sample(r->B, r->sample_rng, r->B);
+    if (!sampled) return 1;
+    MatF states = fa::RunningNormalizer::apply_stats(r->norm, *sampled);
+    float loss;
+    std::vector<float> dpolicy;
+    if (r->distributional) {
+      auto head = agents::CategoricalHead<float>::create(r->n_atoms, r->vmin, r->vmax);
+      auto res = agents::c51_actor_loss(states, r->policy, r->critics, head);
+      loss = res.loss;
+      dpolicy = std::move(res.dpolicy);
+    } else {
+      auto res = agents::ddpg_actor_loss(states, r->policy, r->critics);
+      loss = res.loss;
+      dpolicy = std::move(res.dpolicy);
+    }
+    fa::clip_global_norm(dpolicy, 0.5f);
+    fa::adam_step(r->policy.net.flat, dpolicy, r->adam, r->lr);
+    *loss_out = loss;
+  } catch (const std::exception&) {
+    return -2;
+  }
+  return 0;
+}
+
+REF_API void ref_pupdate_params(void* h, float* out) {
+  auto* r = static_cast<RefPolicy*>(h);
+  std::memcpy(out, r->policy.net.flat.data(), r->policy.net.flat.size() * sizeof(float));
+}
+
+// --------------------------------------------------- actor step (agents)
+// ActorCore::rollout_step (learners.cpp:80-116) composed from the
+// reference's normalizer / DeterministicPolicy / apply_noise, with the
+// environment step supplied by the caller (the synthetic env lives in the
+// restatement; EnvBatch's tasks have other dims).  Phase 1: raw obs ->
+// noisy actions (+ normalizer update after acting is phase 2).
+struct RefActor {
+  size_t N, D, A, n_layers;
+  std::vector<size_t> psizes;
+  agents::DeterministicPolicy<float> policy;
+  fa::RunningNormalizer normalizer;
+  explore::NoiseSchedule schedule;
+  std::vector<env::SplitMixEngine> noise_rng;
+};
+
+REF_API void* ref_actor_create(size_t N, size_t D, size_t A, size_t hidden, size_t n_hidden,
+                               uint64_t seed, const float* policy, float smin, float smax) {
+  auto* r = new RefActor();
+  r->N = N; r->D = D; r->A = A; r->n_layers = n_hidden + 1;
+  r->psizes.push_back(D);
+  for (size_t i = 0; i < n_hidden; ++i) r->psizes.push_back(hidden);
+  r->psizes.push_back(A);
+  r->policy = make_policy(policy, r->psizes.data(), r->n_layers, -1.0f, 1.0f);
+  r->normalizer = fa::RunningNormalizer(D);
+  r->schedule = explore::build_schedule(smin, smax, N);
+  r->noise_rng.resize(N);
+  for (size_t i = 0; i < N; ++i) r->noise_rng[i].state = derive_seed(seed, RngStream::noise, i);
+  return r;
+}
+
+REF_API void ref_actor_destroy(void* h) { delete static_cast<RefActor*>(h); }
+
+REF_API void ref_actor_act(void* h, const float* obs, float* actions) {
+  auto* r = static_cast<RefActor*>(h);
+  MatF o = make_mat(obs, r->N, r->D);
+  MatF obs_norm = r->normalizer.apply(o);
+  MatF a = r->policy.act(obs_norm);
+  explore::apply_noise(a, r->schedule, r->policy.low, r->policy.high, r->noise_rng);
+  std::memcpy(actions, a.data(), r->N * r->A * sizeof(float));
+}
+
+REF_API void ref_actor_observe(void* h, const float* obs) {
+  auto* r = static_cast<RefActor*>(h);
+  r->normalizer.update(make_mat(obs, r->N, r->D));
+}
+
+REF_API void ref_actor_stats(void* h, int64_t* count, double* mean, double* m2) {
+  auto* r = static_cast<RefActor*>(h);
+  const auto& s = r->normalizer.stats();
+  *count = s.count;
+  std::memcpy(mean, s.mean.data(), r->D * sizeof(double));
+  std::memcpy(m2, s.m2.data(), r->D * sizeof(double));
+}
+
+// --------------------------------------------------- CriticLearnerCore
+// The reference's own runtime core (2 hidden layers of cfg.hidden), used for
+// config 1 end to end: ingest (n-step + insert, learners.cpp:144-151) and
+// update (learners.cpp:157-188).
+struct RefVCore {
+  RunConfig cfg;
+  size_t D = 0, A = 0;
+  std::unique_ptr<rt::CriticLearnerCore> core;
+};
+
+REF_API void* ref_vcore_create(size_t n_envs, size_t batch, size_t capacity, size_t hidden,
+                               size_t D, size_t A, uint64_t seed, uint64_t init_seed,
+                               float reward_scale, int distributional) {
+  auto* r = new RefVCore();
+  r->cfg.n_envs = n_envs;
+  r->cfg.batch_size = batch;
+  r->cfg.buffer_capacity = capacity;
+  r->cfg.hidden = hidden;
+  r->cfg.seed = seed;
+  r->cfg.reward_scale = reward_scale;
+  r->cfg.algo = distributional ? agents::Algo::pql_d : agents::Algo::pql_ddpg;
+  r->D = D;
+  r->A = A;
+  rt::TaskDims dims{D, A, -1.0f, 1.0f};
+  r->core = std::make_unique<rt::CriticLearnerCore>(r->cfg, dims, std::mt19937_64(init_seed));
+  return r;
+}
+
+REF_API void ref_vcore_destroy(void* h) { delete static_cast<RefVCore*>(h); }
+
+REF_API void ref_vcore_ingest(void* h, const float* obs, const float* act, const float* boot,
+                              const float* rew, const uint8_t* term, const uint8_t* trunc) {
+  auto* r = static_cast<RefVCore*>(h);
+  const size_t N = r->cfg.n_envs;
+  rt::StepSlice s;
+  s.obs = make_mat(obs, N, r->D);
+  s.act = make_mat(act, N, r->A);
+  s.boot_obs = make_mat(boot, N, r->D);
+  s.rew.assign(rew, rew + N);
+  s.term.assign(term, term + N);
+  s.trunc.assign(trunc, trunc + N);
+  r->core->ingest(s);
+}
+
+REF_API int ref_vcore_ready(void* h, int64_t c_a) {
+  return static_cast<RefVCore*>(h)->core->ready(c_a) ? 1 : 0;
+}
+
+REF_API size_t ref_vcore_buffer_size(void* h) {
+  return static_cast<RefVCore*>(h)->core->buffer_size();
+}
+
+REF_API void ref_vcore_adopt_norm(void* h, int64_t count, const double* mean, const double* m2) {
+  auto* r = static_cast<RefVCore*>(h);
+  r->core->adopt_norm(make_stats(count, mean, m2, r->D));
+}
+
+REF_API void ref_vcore_adopt_policy(void* h, const float* flat, int64_t version) {
+  auto* r = static_cast<RefVCore*>(h);
+  rt::PolicySnapshot snap;
+  snap.version = version;
+  const size_t sizes[4] = {r->D, r->cfg.hidden, r->cfg.hidden, r->A};
+  snap.net = make_mlp(sizes, 3, flat);
+  r->core->adopt_policy(snap);
+}
+
+REF_API int ref_vcore_update(void* h, float* loss) {
+  auto* r = static_cast<RefVCore*>(h);
+  try {
+    *loss = r->core->update();
+  } catch (const std::exception&) {
+    return -2;
+  }
+  return 0;
+}
+
+// which: 0 q1, 1 q2, 2 q1_target, 3 q2_target
+REF_API void ref_vcore_params(void* h, int which, float* out) {
+  auto* r = static_cast<RefVCore*>(h);
+  const auto& c = r->core->critics();
+  const fa::Mlp<float>* nets[4] = {&c.q1, &c.q2, &c.q1_target, &c.q2_target};
+  std::memcpy(out, nets[which]->flat.data(), nets[which]->flat.size() * sizeof(float));
+}
+
+REF_API void ref_policy_init(size_t D, size_t A, size_t hidden, uint64_t seed, float* out) {
+  RunConfig cfg;
+  cfg.hidden = hidden;
+  cfg.seed = seed;
+  rt::TaskDims dims{D, A, -1.0f, 1.0f};
+  auto rng = make_rng(seed, RngStream::init, 0);
+  auto p = rt::PolicyHandle::create(cfg, dims, rng);
+  std::memcpy(out, p.net().flat.data(), p.net().flat.size() * sizeof(float));
+}

@@ -1,0 +1,82 @@
+"""ctypes binding of libpqlg.so (the C ABI in include/pqlg.h).
+
+There is deliberately no fallback: if the library or a CUDA device is
+missing, the first call raises.  Signatures are declared once here so the
+Python mirror classes and the tests call through the exact C ABI.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libpqlg.so"
+
+PQLG_OK, PQLG_NOT_READY = 0, 1
+PQLG_EINVAL, PQLG_ENONFINITE, PQLG_ECUDA, PQLG_ENCCL = -1, -2, -3, -4
+
+vp, i32, i64, u64, f32, f64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_float, C.c_double
+
+# name -> (restype, argtypes)
+SIGNATURES: dict[str, tuple] = {
+    "pqlg_last_error": (C.c_char_p, []),
+    "pqlg_abi_version": (i32, []),
+    "pqlg_launch_count": (u64, []),
+    "pqlg_k_gemm_tf32": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32,
+                               i32, vp]),
+}
+
+
+class PqlgError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[{status}] {msg}")
+        self.status = status
+
+
+class NotReady(PqlgError):
+    pass
+
+
+class NonFinite(PqlgError):
+    pass
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: run `python -m paper_2307_12983_b200.build` "
+                "(there is no CPU fallback)")
+        handle = C.CDLL(str(LIB_PATH), mode=C.RTLD_GLOBAL)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def last_error() -> str:
+    return lib().pqlg_last_error().decode()
+
+
+def check(status: int) -> int:
+    """Maps a PQLG status to the reference's exception convention."""
+    if status == PQLG_OK:
+        return status
+    msg = last_error()
+    if status == PQLG_NOT_READY:
+        raise NotReady(status, msg)
+    if status == PQLG_EINVAL:
+        raise ValueError(msg)
+    if status == PQLG_ENONFINITE:
+        raise NonFinite(status, msg)
+    raise PqlgError(status, msg)
+
+
+def call(name: str, *args) -> int:
+    return check(getattr(lib(), name)(*args))

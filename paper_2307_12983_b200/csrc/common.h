@@ -1,0 +1,67 @@
+// Host-side plumbing shared by every translation unit of libpqlg: status
+// codes, the thread-local last-error string, CUDA error checking and TMA
+// tensor-map construction.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/pqlg.h"
+
+namespace pqlg {
+
+// Exceptions carry the C status they map to at the ABI boundary.
+struct Error : std::runtime_error {
+  int status;
+  Error(int s, const std::string& msg) : std::runtime_error(msg), status(s) {}
+};
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
+
+#define PQLG_CUDA(expr)                                                   \
+  do {                                                                    \
+    cudaError_t _e = (expr);                                              \
+    if (_e != cudaSuccess) ::pqlg::throw_cuda(_e, #expr, __FILE__, __LINE__); \
+  } while (0)
+
+#define PQLG_CHECK_LAUNCH() PQLG_CUDA(cudaGetLastError())
+
+inline void require(bool ok, const std::string& msg) {
+  if (!ok) throw Error(PQLG_EINVAL, msg);
+}
+
+void set_last_error(const std::string& msg);
+
+// Kernel launches issued by this library (reported through pqlg_launch_count).
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Wraps an ABI entry point: converts exceptions to status codes.
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PQLG_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.status;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return PQLG_EINVAL;
+  }
+}
+
+// ----------------------------------------------------------------- TMA maps
+enum class Swz { k128, k128a32 };
+
+// 2-D fp32 tensor map: `inner` contiguous elements per row, `outer` rows at
+// `row_stride` elements; box = box_inner x box_outer elements.
+CUtensorMap make_tmap_2d(const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride,
+                         uint32_t box_inner, uint32_t box_outer, Swz swz, bool tf32_type = false);
+
+}  // namespace pqlg

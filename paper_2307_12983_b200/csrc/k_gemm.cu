@@ -1,0 +1,111 @@
+// Operator-level GEMM entry point (pqlg_k_gemm_tf32): the affine kernels of
+// pql::kernels (kernels.hpp:25-43) restated as one tcgen05 TF32 GEMM with an
+// optional bias + ReLU epilogue.  Used by the per-op parity tests.
+#include "gemm_host.cuh"
+
+namespace pqlg {
+namespace {
+
+struct StoreEpi {
+  float* D;
+  const float* bias;
+  int ldd, M, N, relu;
+  struct Row {};
+  __device__ void begin(Row&, int, int, int, int) const {}
+  __device__ void end(Row&, int, int, int, int) const {}
+  __device__ void chunk(Row&, int, int, int m, int n0, const float (&v)[32]) const {
+    if (m >= M) return;
+    float* d = D + static_cast<size_t>(m) * ldd;
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+      const int n = n0 + t;
+      if (n < N) {
+        float x = v[t];
+        if (bias) x = __fadd_rn(x, bias[n]);
+        if (relu) x = x > 0.0f ? x : 0.0f;
+        d[n] = x;
+      }
+    }
+  }
+};
+
+// Split-K partial tiles: W[split][M][N], summed later in split order.
+struct PartialEpi {
+  float* W;
+  int M, N;
+  struct Row {};
+  __device__ void begin(Row&, int, int, int, int) const {}
+  __device__ void end(Row&, int, int, int, int) const {}
+  __device__ void chunk(Row&, int, int split, int m, int n0, const float (&v)[32]) const {
+    if (m >= M) return;
+    float* d = W + (static_cast<size_t>(split) * M + m) * N;
+#pragma unroll
+    for (int t = 0; t < 32; ++t)
+      if (n0 + t < N) d[n0 + t] = v[t];
+  }
+};
+
+__global__ void reduce_splits(const float* W, int splits, int M, int N, float* D, int ldd,
+                              const float* bias, int relu) {
+  const size_t total = static_cast<size_t>(M) * N;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float acc = W[i];
+    for (int s = 1; s < splits; ++s) acc = __fadd_rn(acc, W[s * total + i]);
+    const int m = static_cast<int>(i / N), n = static_cast<int>(i % N);
+    if (bias) acc = __fadd_rn(acc, bias[n]);
+    if (relu) acc = acc > 0.0f ? acc : 0.0f;
+    D[static_cast<size_t>(m) * ldd + n] = acc;
+  }
+}
+
+template <int BN, bool AMN, bool BMN>
+void run(const float* A, const float* B, float* D, const float* bias, int M, int N, int K,
+         int lda, int ldb, int ldd, int relu, int splits, bool tf32, cudaStream_t st) {
+  gemm::Operands ops;
+  ops.a[0] = ops.a[1] = gemm::map_a(A, M, K, lda, AMN, tf32);
+  ops.b[0] = ops.b[1] = gemm::map_b(B, N, K, ldb, BMN, BN, tf32);
+  gemm::Problem p = gemm::make_problem(M, N, K, splits);
+  if (p.splits == 1) {
+    gemm::launch<BN, AMN, BMN>(ops, p, 1, StoreEpi{D, bias, ldd, M, N, relu}, st);
+    return;
+  }
+  float* W = nullptr;
+  PQLG_CUDA(cudaMallocAsync(&W, sizeof(float) * p.splits * M * N, st));
+  gemm::launch<BN, AMN, BMN>(ops, p, 1, PartialEpi{W, M, N}, st);
+  reduce_splits<<<296, 256, 0, st>>>(W, p.splits, M, N, D, ldd, bias, relu);
+  PQLG_CHECK_LAUNCH();
+  count_launch();
+  PQLG_CUDA(cudaFreeAsync(W, st));
+}
+
+template <int BN>
+void dispatch_major(int a_mn, int b_mn, const float* A, const float* B, float* D,
+                    const float* bias, int M, int N, int K, int lda, int ldb, int ldd, int relu,
+                    int splits, bool tf32, cudaStream_t st) {
+  if (!a_mn && !b_mn) run<BN, false, false>(A, B, D, bias, M, N, K, lda, ldb, ldd, relu, splits, tf32, st);
+  else if (!a_mn && b_mn) run<BN, false, true>(A, B, D, bias, M, N, K, lda, ldb, ldd, relu, splits, tf32, st);
+  else if (a_mn && !b_mn) run<BN, true, false>(A, B, D, bias, M, N, K, lda, ldb, ldd, relu, splits, tf32, st);
+  else run<BN, true, true>(A, B, D, bias, M, N, K, lda, ldb, ldd, relu, splits, tf32, st);
+}
+
+}  // namespace
+}  // namespace pqlg
+
+extern "C" int pqlg_k_gemm_tf32(const float* A, const float* B, float* D, const float* bias, int M,
+                                int N, int K, int a_mn, int b_mn, int lda, int ldb, int ldd,
+                                int relu, int splits, int round_mode, void* stream) {
+  return pqlg::guarded([&] {
+    pqlg::require(M > 0 && N > 0 && K > 0, "gemm: empty shape");
+    auto st = static_cast<cudaStream_t>(stream);
+    const bool tf32 = round_mode == 1;
+    if (N > 128)
+      pqlg::dispatch_major<256>(a_mn, b_mn, A, B, D, bias, M, N, K, lda, ldb, ldd, relu, splits, tf32, st);
+    else if (N > 64)
+      pqlg::dispatch_major<128>(a_mn, b_mn, A, B, D, bias, M, N, K, lda, ldb, ldd, relu, splits, tf32, st);
+    else if (N > 32)
+      pqlg::dispatch_major<64>(a_mn, b_mn, A, B, D, bias, M, N, K, lda, ldb, ldd, relu, splits, tf32, st);
+    else
+      pqlg::dispatch_major<32>(a_mn, b_mn, A, B, D, bias, M, N, K, lda, ldb, ldd, relu, splits, tf32, st);
+  });
+}

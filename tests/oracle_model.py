@@ -1,0 +1,170 @@
+"""Composition of the oracle restatement into the reference's runtime-core
+steps (tests only).  The arithmetic is in oracle/pql_oracle.c; this file only
+sequences the calls the way proj/src/runtime/learners.cpp does."""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle_lib import (MT64, STREAM_SAMPLE, acts_arr, derive_seed, orc, param_count, ptr,
+                        sizes_arr)
+
+
+def f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def normalize(count, mean, m2, x):
+    x = f32(x)
+    out = np.empty_like(x)
+    orc().orc_normalize_apply(int(count), ptr(np.ascontiguousarray(mean, np.float64)),
+                              ptr(np.ascontiguousarray(m2, np.float64)), ptr(x), ptr(out),
+                              x.shape[0], x.shape[1])
+    return out
+
+
+def mlp_forward(flat, sizes, x):
+    L = len(sizes) - 1
+    y = np.zeros((x.shape[0], sizes[-1]), np.float32)
+    orc().orc_mlp_forward(ptr(f32(flat)), ptr(sizes_arr(sizes)), ptr(acts_arr(L)), L,
+                          ptr(f32(x)), x.shape[0], ptr(y), None)
+    return y
+
+
+def policy_act(flat, sizes, x, low=-1.0, high=1.0):
+    y = np.zeros((x.shape[0], sizes[-1]), np.float32)
+    orc().orc_policy_act(ptr(f32(flat)), ptr(sizes_arr(sizes)), len(sizes) - 1, ptr(f32(x)),
+                         x.shape[0], np.float32(low), np.float32(high), ptr(y))
+    return y
+
+
+def adam(p, g, m, v, t, lr):
+    bc1 = np.zeros(1, np.float32)
+    bc2 = np.zeros(1, np.float32)
+    orc().orc_adam_bias_corrections(t, ptr(bc1), ptr(bc2))
+    orc().orc_adam_update(ptr(p), ptr(g), ptr(m), ptr(v), p.size, np.float32(lr), np.float32(0.9),
+                          np.float32(0.999), np.float32(1e-8), bc1[0], bc2[0])
+
+
+class OracleVUpdate:
+    """CriticLearnerCore::update (learners.cpp:157-188) on explicit state,
+    sampling with mt19937_64 (make_rng(seed, sample, 1)) or Philox."""
+
+    def __init__(self, D, A, hidden, n_hidden, B, q1, q2, policy, seed=0, lr=5e-4, tau=0.05,
+                 philox=False, distributional=False, n_atoms=51, vmin=-10.0, vmax=10.0):
+        self.D, self.A, self.B = D, A, B
+        self.ps = [D] + [hidden] * n_hidden + [A]
+        self.qs = [D + A] + [hidden] * n_hidden + [n_atoms if distributional else 1]
+        self.L = n_hidden + 1
+        self.q = [f32(q1).copy(), f32(q2).copy()]
+        self.qt = [self.q[0].copy(), self.q[1].copy()]
+        self.pol = f32(policy).copy()
+        P = param_count(self.qs)
+        self.m = [np.zeros(P, np.float32) for _ in range(2)]
+        self.v = [np.zeros(P, np.float32) for _ in range(2)]
+        self.t = 0
+        self.lr, self.tau = lr, tau
+        self.philox = philox
+        self.key = derive_seed(seed, STREAM_SAMPLE, 1)
+        self.ctr = np.zeros(1, np.uint64)
+        self.mt = MT64(self.key)
+        self.rows = None
+        self.norm = (0, np.zeros(D), np.zeros(D))
+        self.distributional = distributional
+        self.n_atoms, self.vmin, self.vmax = n_atoms, vmin, vmax
+
+    def set_rows(self, obs, act, boot, ret, eff):
+        self.rows = [f32(obs), f32(act), f32(boot), f32(ret), f32(eff)]
+
+    def sample(self):
+        count = self.rows[3].shape[0]
+        idx = np.zeros(self.B, np.uint64)
+        if self.philox:
+            orc().orc_sample_indices_philox(self.key, ptr(self.ctr), count, self.B, ptr(idx))
+        else:
+            orc().orc_sample_indices_mt(self.mt.handle, count, self.B, ptr(idx))
+        return idx
+
+    def step(self):
+        idx = self.sample().astype(np.int64)
+        obs, act, boot, ret, eff = (r[idx] for r in self.rows)
+        c, mean, m2 = self.norm
+        obs_n = normalize(c, mean, m2, obs)
+        boot_n = normalize(c, mean, m2, boot)
+        P = param_count(self.qs)
+        dq = [np.zeros(P, np.float32), np.zeros(P, np.float32)]
+        loss = np.zeros(1, np.float32)
+        y = np.zeros(self.B, np.float32)
+        args = (ptr(self.pol), ptr(sizes_arr(self.ps)), ptr(self.q[0]), ptr(self.q[1]),
+                ptr(self.qt[0]), ptr(self.qt[1]), ptr(sizes_arr(self.qs)), self.L, ptr(obs_n),
+                ptr(f32(act)), ptr(boot_n), ptr(f32(ret)), ptr(f32(eff)), self.B, self.D, self.A,
+                np.float32(-1), np.float32(1))
+        if self.distributional:
+            rc = orc().orc_c51_critic_loss(*args, self.n_atoms, np.float32(self.vmin),
+                                           np.float32(self.vmax), ptr(loss), ptr(dq[0]),
+                                           ptr(dq[1]))
+        else:
+            rc = orc().orc_ddpg_critic_loss(*args, ptr(loss), ptr(y), ptr(dq[0]), ptr(dq[1]))
+        if rc != 0:
+            raise FloatingPointError("non-finite target/loss")
+        scales = []
+        for k in range(2):
+            scales.append(orc().orc_clip_global_norm(ptr(dq[k]), P, np.float32(0.5)))
+        self.t += 1
+        for k in range(2):
+            adam(self.q[k], dq[k], self.m[k], self.v[k], self.t, self.lr)
+        for k in range(2):
+            orc().orc_lerp_towards(ptr(self.qt[k]), ptr(self.q[k]), P, np.float32(self.tau))
+        return float(loss[0]), dict(idx=idx, y=y, dq=dq, scales=scales)
+
+
+class OraclePUpdate:
+    """PolicyLearnerCore::update (learners.cpp:239-270) on explicit state."""
+
+    def __init__(self, D, A, hidden, n_hidden, B, policy, q1, q2, seed=0, lr=5e-4, philox=False,
+                 distributional=False, n_atoms=51, vmin=-10.0, vmax=10.0):
+        self.D, self.A, self.B = D, A, B
+        self.ps = [D] + [hidden] * n_hidden + [A]
+        self.qs = [D + A] + [hidden] * n_hidden + [n_atoms if distributional else 1]
+        self.L = n_hidden + 1
+        self.pol = f32(policy).copy()
+        self.q = [f32(q1).copy(), f32(q2).copy()]
+        P = param_count(self.ps)
+        self.m = np.zeros(P, np.float32)
+        self.v = np.zeros(P, np.float32)
+        self.t = 0
+        self.lr = lr
+        self.philox = philox
+        self.key = derive_seed(seed, STREAM_SAMPLE, 2)
+        self.ctr = np.zeros(1, np.uint64)
+        self.mt = MT64(self.key)
+        self.states = None
+        self.norm = (0, np.zeros(D), np.zeros(D))
+        self.distributional = distributional
+        self.n_atoms, self.vmin, self.vmax = n_atoms, vmin, vmax
+
+    def step(self):
+        count = self.states.shape[0]
+        idx = np.zeros(self.B, np.uint64)
+        if self.philox:
+            orc().orc_sample_indices_philox(self.key, ptr(self.ctr), count, self.B, ptr(idx))
+        else:
+            orc().orc_sample_indices_mt(self.mt.handle, count, self.B, ptr(idx))
+        c, mean, m2 = self.norm
+        s = normalize(c, mean, m2, self.states[idx.astype(np.int64)])
+        P = param_count(self.ps)
+        dp = np.zeros(P, np.float32)
+        loss = np.zeros(1, np.float32)
+        args = (ptr(self.pol), ptr(sizes_arr(self.ps)), ptr(self.q[0]), ptr(self.q[1]),
+                ptr(sizes_arr(self.qs)), self.L, ptr(s), self.B, self.D, self.A, np.float32(-1),
+                np.float32(1))
+        if self.distributional:
+            rc = orc().orc_c51_actor_loss(*args, self.n_atoms, np.float32(self.vmin),
+                                          np.float32(self.vmax), ptr(loss), ptr(dp))
+        else:
+            rc = orc().orc_ddpg_actor_loss(*args, ptr(loss), ptr(dp))
+        if rc != 0:
+            raise FloatingPointError("non-finite actor loss")
+        orc().orc_clip_global_norm(ptr(dp), P, np.float32(0.5))
+        self.t += 1
+        adam(self.pol, dp, self.m, self.v, self.t, self.lr)
+        return float(loss[0]), dict(idx=idx, dp=dp)
