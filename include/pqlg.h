@@ -66,6 +66,93 @@ PQLG_API int pqlg_k_gemm_tf32(const float* A_dev, const float* B_dev, float* D_d
                      int M, int N, int K, int a_mn, int b_mn, int lda, int ldb, int ldd, int relu,
                      int splits, int round_mode, void* stream);
 
+/* ------------------------------------------------------------ data views */
+
+/* StepSlice (proj/include/pql/runtime/messages.hpp:31-35) as device views.
+ * ld_* are row strides in floats (0 = dense). */
+typedef struct {
+  const float* obs;      /* [N x obs_dim] raw observations s_t            */
+  const float* act;      /* [N x act_dim] actions a_t                     */
+  const float* boot_obs; /* [N x obs_dim] next obs, terminal obs on done  */
+  const float* rew;      /* [N] unscaled task rewards                     */
+  const uint8_t* term;   /* [N] terminated (done && !truncated)           */
+  const uint8_t* trunc;  /* [N] time-limit truncation                     */
+  int64_t ld_obs, ld_act;
+} pqlg_step_slice;
+
+/* NStepBatch (proj/include/pql/replay/nstep.hpp:15-29) as device views. */
+typedef struct {
+  float* obs;
+  float* act;
+  float* boot_obs;
+  float* ret;
+  float* eff_disc;
+  int64_t ld_obs, ld_act;
+} pqlg_nstep_batch;
+
+/* NormStats (proj/include/pql/funcapprox/normalizer.hpp:14-21), host. */
+typedef struct {
+  int64_t count;
+  const double* mean;
+  const double* m2;
+} pqlg_norm_stats;
+
+/* Sampling generator.  PQLG_RNG_PHILOX: counter-based Philox4x32-10 draws
+ * (key, counter), bit-exact against the reference's sample() driven by the
+ * same URBG; the counter advances by the draws consumed.
+ * PQLG_RNG_INDICES: explicit host indices (the reference's own
+ * std::mt19937_64 stream generated on the host) -- the mt19937-compat mode. */
+enum { PQLG_RNG_PHILOX = 0, PQLG_RNG_INDICES = 1 };
+typedef struct {
+  int mode;
+  uint64_t key;
+  uint64_t counter;
+  const uint64_t* host_indices; /* [batch] when mode == PQLG_RNG_INDICES */
+} pqlg_rng;
+
+/* ------------------------------------------------------- replay buffers */
+typedef struct pqlg_replay_s* pqlg_replay;
+typedef struct pqlg_nstep_s* pqlg_nstep;
+typedef struct pqlg_states_s* pqlg_states;
+
+/* ReplayBuffer(capacity, obs_dim, act_dim)   replay_buffer.hpp:19-27 */
+PQLG_API int pqlg_replay_create(uint64_t capacity, int obs_dim, int act_dim, void* stream,
+                                pqlg_replay* out);
+PQLG_API int pqlg_replay_destroy(pqlg_replay h);
+/* size() / cursor() (replay_buffer.hpp:29-31); synchronize the stream. */
+PQLG_API int pqlg_replay_size(pqlg_replay h, uint64_t* out);
+PQLG_API int pqlg_replay_cursor(pqlg_replay h, uint64_t* out);
+/* insert(batch)   replay_buffer.hpp:33-47 (n rows, device views) */
+PQLG_API int pqlg_replay_insert(pqlg_replay h, const pqlg_nstep_batch* dev, uint64_t n);
+/* sample(batch, rng, min_live)   replay_buffer.hpp:50-69.  Returns
+ * PQLG_NOT_READY (empty optional) when size < min_live.  `norm` (nullable)
+ * fuses RunningNormalizer::apply_stats on obs and boot_obs.  Synchronizes
+ * and writes the advanced Philox counter back into *rng. */
+PQLG_API int pqlg_replay_sample(pqlg_replay h, uint64_t batch, pqlg_rng* rng, uint64_t min_live,
+                                const pqlg_norm_stats* norm, pqlg_nstep_batch* dev_out);
+/* Ring rows [i0, i0+n) to host (obs_row / ret_at, replay_buffer.hpp:71-73);
+ * any output pointer may be NULL. */
+PQLG_API int pqlg_replay_read_rows(pqlg_replay h, uint64_t i0, uint64_t n, float* obs, float* act,
+                                   float* boot_obs, float* ret, float* eff_disc);
+
+/* NStepAssembler(n_envs, obs_dim, act_dim, gamma, horizon)  nstep.hpp:39-52 */
+PQLG_API int pqlg_nstep_create(int n_envs, int obs_dim, int act_dim, float gamma, int horizon,
+                               void* stream, pqlg_nstep* out);
+PQLG_API int pqlg_nstep_destroy(pqlg_nstep h);
+/* push_step fused with ReplayBuffer::insert (learners.cpp:144-151): rewards
+ * are scaled by reward_scale first; the emitted records go straight into
+ * `dst` in the reference's env-major order. */
+PQLG_API int pqlg_nstep_push_step(pqlg_nstep h, const pqlg_step_slice* dev, float reward_scale,
+                                  pqlg_replay dst);
+
+/* StateBuffer(capacity, obs_dim)   replay_buffer.hpp:84-91 */
+PQLG_API int pqlg_states_create(uint64_t capacity, int obs_dim, void* stream, pqlg_states* out);
+PQLG_API int pqlg_states_destroy(pqlg_states h);
+PQLG_API int pqlg_states_size(pqlg_states h, uint64_t* out);
+PQLG_API int pqlg_states_insert(pqlg_states h, const float* rows_dev, int64_t ld, uint64_t n);
+PQLG_API int pqlg_states_sample(pqlg_states h, uint64_t batch, pqlg_rng* rng, uint64_t min_live,
+                                const pqlg_norm_stats* norm, float* out_dev, int64_t ld_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,6 +17,32 @@ PQLG_EINVAL, PQLG_ENONFINITE, PQLG_ECUDA, PQLG_ENCCL = -1, -2, -3, -4
 
 vp, i32, i64, u64, f32, f64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_float, C.c_double
 
+
+class StepSlice(C.Structure):
+    """pqlg_step_slice (device views of a StepSlice)."""
+    _fields_ = [("obs", vp), ("act", vp), ("boot_obs", vp), ("rew", vp), ("term", vp),
+                ("trunc", vp), ("ld_obs", i64), ("ld_act", i64)]
+
+
+class NStepBatch(C.Structure):
+    """pqlg_nstep_batch (device views of an NStepBatch)."""
+    _fields_ = [("obs", vp), ("act", vp), ("boot_obs", vp), ("ret", vp), ("eff_disc", vp),
+                ("ld_obs", i64), ("ld_act", i64)]
+
+
+class NormStats(C.Structure):
+    """pqlg_norm_stats (host NormStats)."""
+    _fields_ = [("count", i64), ("mean", vp), ("m2", vp)]
+
+
+class Rng(C.Structure):
+    """pqlg_rng: Philox (key, counter) or explicit host indices."""
+    _fields_ = [("mode", i32), ("key", u64), ("counter", u64), ("host_indices", vp)]
+
+
+RNG_PHILOX, RNG_INDICES = 0, 1
+P = C.POINTER
+
 # name -> (restype, argtypes)
 SIGNATURES: dict[str, tuple] = {
     "pqlg_last_error": (C.c_char_p, []),
@@ -24,6 +50,21 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_launch_count": (u64, []),
     "pqlg_k_gemm_tf32": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32,
                                i32, vp]),
+    "pqlg_replay_create": (i32, [u64, i32, i32, vp, P(vp)]),
+    "pqlg_replay_destroy": (i32, [vp]),
+    "pqlg_replay_size": (i32, [vp, P(u64)]),
+    "pqlg_replay_cursor": (i32, [vp, P(u64)]),
+    "pqlg_replay_insert": (i32, [vp, P(NStepBatch), u64]),
+    "pqlg_replay_sample": (i32, [vp, u64, P(Rng), u64, P(NormStats), P(NStepBatch)]),
+    "pqlg_replay_read_rows": (i32, [vp, u64, u64, vp, vp, vp, vp, vp]),
+    "pqlg_nstep_create": (i32, [i32, i32, i32, f32, i32, vp, P(vp)]),
+    "pqlg_nstep_destroy": (i32, [vp]),
+    "pqlg_nstep_push_step": (i32, [vp, P(StepSlice), f32, vp]),
+    "pqlg_states_create": (i32, [u64, i32, vp, P(vp)]),
+    "pqlg_states_destroy": (i32, [vp]),
+    "pqlg_states_size": (i32, [vp, P(u64)]),
+    "pqlg_states_insert": (i32, [vp, vp, i64, u64]),
+    "pqlg_states_sample": (i32, [vp, u64, P(Rng), u64, P(NormStats), vp, i64]),
 }
 
 

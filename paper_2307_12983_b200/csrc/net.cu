@@ -1,0 +1,45 @@
+#include "net.h"
+
+namespace pqlg {
+
+namespace {
+// detail::orthogonalize (mlp.hpp:209-225), T = float.
+void orthogonalize(std::vector<float>& a, size_t rows, size_t cols) {
+  for (size_t c = 0; c < cols; ++c) {
+    for (size_t p = 0; p < c; ++p) {
+      float dot = 0.0f;
+      for (size_t r = 0; r < rows; ++r) dot += a[r * cols + c] * a[r * cols + p];
+      for (size_t r = 0; r < rows; ++r) a[r * cols + c] -= dot * a[r * cols + p];
+    }
+    float norm = 0.0f;
+    for (size_t r = 0; r < rows; ++r) norm += a[r * cols + c] * a[r * cols + c];
+    norm = std::sqrt(norm);
+    if (norm < 1e-12f) norm = 1.0f;
+    for (size_t r = 0; r < rows; ++r) a[r * cols + c] /= norm;
+  }
+}
+}  // namespace
+
+void init_orthogonal(const NetShape& net, std::vector<float>& flat, std::mt19937_64& rng,
+                     float hidden_gain, float final_gain) {
+  flat.assign(net.params, 0.0f);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  for (int l = 0; l < net.layers(); ++l) {
+    const size_t in = net.sizes[l], out = net.sizes[l + 1];
+    const size_t big = std::max(in, out), small = std::min(in, out);
+    std::vector<float> m(big * small);
+    for (auto& x : m) x = static_cast<float>(gauss(rng));
+    orthogonalize(m, big, small);
+    const float gain = (l + 1 == net.layers()) ? final_gain : hidden_gain;
+    float* w = flat.data() + net.w_off[l];
+    for (size_t i = 0; i < in; ++i)
+      for (size_t o = 0; o < out; ++o) {
+        const float v = (in >= out) ? m[i * small + o] : m[o * small + i];
+        w[i * out + o] = gain * v;
+      }
+    float* b = flat.data() + net.b_off[l];
+    for (size_t o = 0; o < out; ++o) b[o] = 0.0f;
+  }
+}
+
+}  // namespace pqlg

@@ -1,0 +1,407 @@
+// Device replay path: n-step assembly fused with the ring insert, the state
+// ring, and Philox-driven minibatch sampling fused with observation
+// normalization.  All are HBM-bound copy kernels: one warp per row, lanes
+// stride the row so every access is a coalesced 128-byte segment.
+//
+// Reference semantics (bit-exact):
+//   NStepAssembler::push_step / push_env / emit   nstep.hpp:58-118
+//   ReplayBuffer::insert / sample                 replay_buffer.hpp:33-69
+//   StateBuffer::insert / sample                  replay_buffer.hpp:93-112
+//   RunningNormalizer::apply_stats + normalize_clip  normalizer.hpp:56-70,
+//                                                 scalar.hpp:93-106
+#pragma once
+
+#include <cstdint>
+
+#include "rng.cuh"
+
+namespace pqlg::replay {
+
+// SoA ring on device (replay_buffer.hpp:79-80); rows padded to `ld_*`.
+struct Ring {
+  float* obs;
+  float* act;
+  float* boot;
+  float* ret;
+  float* eff;
+  int64_t ld_obs, ld_act;
+  int D, A;
+  uint64_t capacity;
+  uint64_t* state;  // device: [0] cursor, [1] count
+};
+
+struct StateRing {
+  float* obs;
+  int64_t ld;
+  int D;
+  uint64_t capacity;
+  uint64_t* state;  // [0] cursor, [1] count
+};
+
+// Per-env n-step windows (nstep.hpp:120-125).
+struct Window {
+  float* obs;  // [N*n x ld_obs]
+  float* act;  // [N*n x ld_act]
+  float* rew;  // [N*n]
+  uint32_t* head;
+  uint32_t* count;
+  int64_t ld_obs, ld_act;
+  int N, n;
+  float gamma;
+};
+
+// StepSlice (messages.hpp:31-35) on device.
+struct Slice {
+  const float* obs;
+  const float* act;
+  const float* boot;
+  const float* rew;
+  const uint8_t* term;
+  const uint8_t* trunc;
+  int64_t ld_obs, ld_act;
+};
+
+// Normalization constants in fp32 (normalizer.hpp:62-66), identity flag.
+struct Norm {
+  const float* mean;
+  const float* inv;
+  int identity;  // count <= 1
+};
+
+// Destination of a gathered minibatch.  obs/boot rows are normalized.
+struct Gather {
+  float* obs;
+  int64_t ld_obs;
+  float* act;  // may alias obs + D (critic input [obs | act])
+  int64_t ld_act;
+  float* boot;
+  int64_t ld_boot;
+  float* ret;
+  float* eff;
+};
+
+constexpr int kScanBlock = 1024;
+constexpr int kWarpsPerBlock = 8;
+
+__device__ __forceinline__ float normalize1(float x, float mean, float inv) {
+  float z = __fmul_rn(__fsub_rn(x, mean), inv);
+  if (z > 5.0f) z = 5.0f;
+  if (z < -5.0f) z = -5.0f;
+  return z;
+}
+
+// Emit count of env e for this step (0..n): nstep.hpp:78-92.
+__device__ __forceinline__ int emit_count(uint32_t count, int n, bool done) {
+  int c = static_cast<int>(count) + 1;
+  int emits = 0;
+  if (c == n) {
+    emits = 1;
+    c -= 1;
+  }
+  if (done) emits += c;
+  return emits;
+}
+
+// K1: per-env emit counts, block-exclusive offsets and block totals.
+__global__ void nstep_count_kernel(Window w, Slice s, uint32_t* offs, uint32_t* block_sums) {
+  __shared__ uint32_t warp_tot[kScanBlock / 32];
+  const int e = blockIdx.x * kScanBlock + threadIdx.x;
+  uint32_t c = 0;
+  if (e < w.N) {
+    const bool done = (s.term[e] != 0) || (s.trunc[e] != 0);
+    c = static_cast<uint32_t>(emit_count(w.count[e], w.n, done));
+  }
+  // warp-inclusive scan
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t v = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v += t;
+  }
+  if (lane == 31) warp_tot[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t t = warp_tot[lane];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, t, d);
+      if (lane >= d) t += u;
+    }
+    warp_tot[lane] = t;  // inclusive over warps
+  }
+  __syncthreads();
+  const uint32_t warp_prefix = wid ? warp_tot[wid - 1] : 0u;
+  if (e < w.N) offs[e] = warp_prefix + v - c;
+  if (threadIdx.x == kScanBlock - 1) block_sums[blockIdx.x] = warp_tot[31];
+}
+
+// K2: one warp per env.  Writes the new window slot, then emits this step's
+// records in reference order straight into the ring.
+__global__ void nstep_emit_kernel(Window w, Slice s, float reward_scale, Ring ring,
+                                  const uint32_t* offs, const uint32_t* block_sums,
+                                  int n_blocks) {
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (e >= w.N) return;
+  // global offset of this env's first record and the step total
+  uint32_t before = 0, total = 0;
+  const int my_block = e / kScanBlock;
+  for (int b = lane; b < n_blocks; b += 32) {
+    const uint32_t v = block_sums[b];
+    total += v;
+    if (b < my_block) before += v;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    total += __shfl_xor_sync(0xffffffffu, total, d);
+    before += __shfl_xor_sync(0xffffffffu, before, d);
+  }
+  const uint64_t base = static_cast<uint64_t>(before) + offs[e];
+  const uint64_t cursor0 = ring.state[0];
+  const int n = w.n, D = ring.D, A = ring.A;
+
+  uint32_t h = w.head[e];
+  uint32_t c = w.count[e];
+  // push: window slot (head + count) % n
+  {
+    const uint32_t slot = (h + c) % n;
+    const size_t wrow = static_cast<size_t>(e) * n + slot;
+    const float* so = s.obs + static_cast<size_t>(e) * s.ld_obs;
+    float* wo = w.obs + wrow * w.ld_obs;
+    for (int d = lane; d < D; d += 32) wo[d] = so[d];
+    const float* sa = s.act + static_cast<size_t>(e) * s.ld_act;
+    float* wa = w.act + wrow * w.ld_act;
+    for (int d = lane; d < A; d += 32) wa[d] = sa[d];
+    if (lane == 0) w.rew[wrow] = __fmul_rn(s.rew[e], reward_scale);
+  }
+  __syncwarp();
+  c += 1;
+  const bool term = s.term[e] != 0;
+  const bool done = term || (s.trunc[e] != 0);
+
+  uint32_t j = 0;
+  auto emit = [&](uint32_t m, bool terminated) {
+    float g = 0.0f, disc = 1.0f;
+    for (uint32_t k = 0; k < m; ++k) {
+      const float r = w.rew[static_cast<size_t>(e) * n + (h + k) % n];
+      g = __fadd_rn(g, __fmul_rn(disc, r));
+      disc = __fmul_rn(disc, w.gamma);
+    }
+    const uint64_t rec = base + j++;
+    // records overwritten within this same insert are skipped (ring order)
+    if (rec + ring.capacity < total) return;
+    const uint64_t p = (cursor0 + rec) % ring.capacity;
+    const size_t front = static_cast<size_t>(e) * n + h;
+    const float* wo = w.obs + front * w.ld_obs;
+    float* ro = ring.obs + p * ring.ld_obs;
+    for (int d = lane; d < D; d += 32) ro[d] = wo[d];
+    const float* wa = w.act + front * w.ld_act;
+    float* ra = ring.act + p * ring.ld_act;
+    for (int d = lane; d < A; d += 32) ra[d] = wa[d];
+    const float* sb = s.boot + static_cast<size_t>(e) * s.ld_obs;
+    float* rb = ring.boot + p * ring.ld_obs;
+    for (int d = lane; d < D; d += 32) rb[d] = sb[d];
+    if (lane == 0) {
+      ring.ret[p] = g;
+      ring.eff[p] = terminated ? 0.0f : disc;
+    }
+  };
+
+  if (c == static_cast<uint32_t>(n)) {
+    emit(n, term);  // terminated && done == terminated
+    h = (h + 1) % n;
+    c -= 1;
+  }
+  if (done) {
+    while (c > 0) {
+      emit(c, term);
+      h = (h + 1) % n;
+      c -= 1;
+    }
+    h = 0;
+  }
+  if (lane == 0) {
+    w.head[e] = h;
+    w.count[e] = c;
+  }
+}
+
+// K3: cursor = (cursor + total) % cap; count = min(count + total, cap).
+__global__ void ring_advance_kernel(uint64_t* state, uint64_t capacity, const uint32_t* sums,
+                                    int n_sums, uint64_t extra) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  uint64_t total = extra;
+  for (int b = 0; b < n_sums; ++b) total += sums[b];
+  state[0] = (state[0] + total) % capacity;
+  const uint64_t c = state[1] + total;
+  state[1] = c < capacity ? c : capacity;
+}
+
+// Direct insert of an assembled batch (ReplayBuffer::insert).  One warp per
+// row; rows that a later row of the same batch overwrites are skipped.
+__global__ void ring_insert_kernel(Ring ring, const float* obs, const float* act,
+                                   const float* boot, const float* ret, const float* eff,
+                                   int64_t ld_obs, int64_t ld_act, uint64_t n) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (r >= n || r + ring.capacity < n) return;
+  const uint64_t p = (ring.state[0] + r) % ring.capacity;
+  for (int d = lane; d < ring.D; d += 32) {
+    ring.obs[p * ring.ld_obs + d] = obs[r * ld_obs + d];
+    ring.boot[p * ring.ld_obs + d] = boot[r * ld_obs + d];
+  }
+  for (int d = lane; d < ring.A; d += 32) ring.act[p * ring.ld_act + d] = act[r * ld_act + d];
+  if (lane == 0) {
+    ring.ret[p] = ret[r];
+    ring.eff[p] = eff[r];
+  }
+}
+
+__global__ void state_insert_kernel(StateRing ring, const float* rows, int64_t ld, uint64_t n) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (r >= n || r + ring.capacity < n) return;
+  const uint64_t p = (ring.state[0] + r) % ring.capacity;
+  for (int d = lane; d < ring.D; d += 32) ring.obs[p * ring.ld + d] = rows[r * ld + d];
+}
+
+// ---------------------------------------------------------------- sampling
+// Sampler state on device: Philox key, counter, rejection flag.
+struct SamplerState {
+  uint64_t key;
+  uint64_t counter;
+  uint32_t reject;
+  uint32_t pad;
+};
+
+// idx for row r: host_idx (mt19937-compat mode) or Philox + Lemire.
+__device__ __forceinline__ uint64_t sample_index(const SamplerState* ss, const uint64_t* host_idx,
+                                                 uint64_t count, uint64_t r, bool& reject) {
+  reject = false;
+  if (host_idx) return host_idx[r];
+  return rng::lemire_step(rng::philox_draw(ss->key, ss->counter + r), count, reject);
+}
+
+__device__ __forceinline__ void gather_row(const Ring& ring, const Norm& norm, const Gather& g,
+                                           uint64_t i, uint64_t r, int lane) {
+  const float* so = ring.obs + i * ring.ld_obs;
+  const float* sb = ring.boot + i * ring.ld_obs;
+  float* dobs = g.obs + r * g.ld_obs;
+  float* dboot = g.boot + r * g.ld_boot;
+  for (int d = lane; d < ring.D; d += 32) {
+    float x = so[d], y = sb[d];
+    if (!norm.identity) {
+      const float mu = norm.mean[d], iv = norm.inv[d];
+      x = normalize1(x, mu, iv);
+      y = normalize1(y, mu, iv);
+    }
+    dobs[d] = x;
+    dboot[d] = y;
+  }
+  const float* sa = ring.act + i * ring.ld_act;
+  float* da = g.act + r * g.ld_act;
+  for (int d = lane; d < ring.A; d += 32) da[d] = sa[d];
+  if (lane == 0) {
+    g.ret[r] = ring.ret[i];
+    g.eff[r] = ring.eff[i];
+  }
+}
+
+// ReplayBuffer::sample fused with apply_stats on obs and boot_obs.
+__global__ void replay_sample_kernel(Ring ring, Norm norm, Gather g, SamplerState* ss,
+                                     const uint64_t* host_idx, uint64_t B) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (r >= B) return;
+  const uint64_t count = ring.state[1];
+  bool reject = false;
+  uint64_t i = 0;
+  if (lane == 0) i = sample_index(ss, host_idx, count, r, reject);
+  i = __shfl_sync(0xffffffffu, i, 0);
+  if (lane == 0 && reject) atomicOr(&ss->reject, 1u);
+  gather_row(ring, norm, g, i, r, lane);
+}
+
+// Sequential fix-up when any draw hit Lemire's rejection zone (probability
+// ~count/2^64 per draw): redo the whole batch with libstdc++'s redraw loop,
+// then advance the counter by the draws consumed.  Always launched (1 warp).
+__global__ void replay_sample_finalize_kernel(Ring ring, Norm norm, Gather g, SamplerState* ss,
+                                              const uint64_t* host_idx, uint64_t B) {
+  const int lane = threadIdx.x & 31;
+  if (host_idx) return;
+  if (ss->reject == 0) {
+    if (lane == 0) ss->counter += B;
+    return;
+  }
+  const uint64_t count = ring.state[1];
+  uint64_t ctr = ss->counter;
+  for (uint64_t r = 0; r < B; ++r) {
+    uint64_t i = 0;
+    if (lane == 0) {
+      bool reject = true;
+      while (reject) i = rng::lemire_step(rng::philox_draw(ss->key, ctr++), count, reject);
+    }
+    i = __shfl_sync(0xffffffffu, i, 0);
+    gather_row(ring, norm, g, i, r, lane);
+  }
+  if (lane == 0) {
+    ss->counter = ctr;
+    ss->reject = 0;
+  }
+}
+
+// StateBuffer::sample fused with apply_stats.
+__global__ void state_sample_kernel(StateRing ring, Norm norm, float* out, int64_t ld_out,
+                                    SamplerState* ss, const uint64_t* host_idx, uint64_t B) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (r >= B) return;
+  const uint64_t count = ring.state[1];
+  bool reject = false;
+  uint64_t i = 0;
+  if (lane == 0) i = sample_index(ss, host_idx, count, r, reject);
+  i = __shfl_sync(0xffffffffu, i, 0);
+  if (lane == 0 && reject) atomicOr(&ss->reject, 1u);
+  const float* so = ring.obs + i * ring.ld;
+  float* d = out + r * ld_out;
+  for (int k = lane; k < ring.D; k += 32) {
+    float x = so[k];
+    if (!norm.identity) x = normalize1(x, norm.mean[k], norm.inv[k]);
+    d[k] = x;
+  }
+}
+
+__global__ void state_sample_finalize_kernel(StateRing ring, Norm norm, float* out,
+                                             int64_t ld_out, SamplerState* ss,
+                                             const uint64_t* host_idx, uint64_t B) {
+  const int lane = threadIdx.x & 31;
+  if (host_idx) return;
+  if (ss->reject == 0) {
+    if (lane == 0) ss->counter += B;
+    return;
+  }
+  const uint64_t count = ring.state[1];
+  uint64_t ctr = ss->counter;
+  for (uint64_t r = 0; r < B; ++r) {
+    uint64_t i = 0;
+    if (lane == 0) {
+      bool reject = true;
+      while (reject) i = rng::lemire_step(rng::philox_draw(ss->key, ctr++), count, reject);
+    }
+    i = __shfl_sync(0xffffffffu, i, 0);
+    const float* so = ring.obs + i * ring.ld;
+    float* d = out + r * ld_out;
+    for (int k = lane; k < ring.D; k += 32) {
+      float x = so[k];
+      if (!norm.identity) x = normalize1(x, norm.mean[k], norm.inv[k]);
+      d[k] = x;
+    }
+  }
+  if (lane == 0) {
+    ss->counter = ctr;
+    ss->reject = 0;
+  }
+}
+
+}  // namespace pqlg::replay
