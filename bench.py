@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""bench.py -- PQL learner/actor hot path on B200 (one JSON line on rank 0).
+
+Metric (BASELINE.json): critic updates/s at batch 8192 (headline `value`)
+and actor transitions/s at 16384 envs (reported under "actor" when built),
+config 3 (Shadow-Hand-like dims: obs 211 / act 20, 3x512 MLPs, B=8192,
+5M-record replay, mixed exploration noise).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one CriticLearnerCore::update (sample -> TD target -> twin critic
+loss/backward -> clip/Adam/Polyak) replayed from a CUDA graph.  Inputs are
+sampled from a 5M-record ring (8.9 GB >> the 126 MB L2), so every step
+reads fresh rows from HBM.  Under torchrun (N>1) every rank runs its own
+learner on its own replay shard (weak scaling) and rank 0 reports the
+device time as the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (obs_dim, act_dim, hidden, hidden_layers, batch, n_envs, capacity)
+    "c1": (32, 8, 256, 2, 1024, 256, 100_000),
+    "c2": (60, 8, 512, 3, 8192, 4096, 5_000_000),
+    "c3": (211, 20, 512, 3, 8192, 16384, 5_000_000),
+}
+METRIC = "critic updates/s (batch 8192) and actor transitions/s at 16384 envs"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# --------------------------------------------------------------- plumbing
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    mx = max(mx, float(f[2]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, f[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        except OSError:
+            pass
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except OSError:
+        return {}
+
+
+def tf32_peak_tflops():
+    """cuBLAS TF32 GEMM 8192^3 (the TF32 denominator MEASURED_PEAKS lacks)."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = True
+    n = 8192
+    a = torch.randn(n, n, device="cuda")
+    b = torch.randn(n, n, device="cuda")
+    for _ in range(3):
+        a @ b
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(10):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        a @ b
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e))
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return 2 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def traffic_from_profiles(kernel_key):
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        return json.loads(p.read_text()).get(kernel_key)
+    except (OSError, ValueError):
+        return None
+
+
+# ------------------------------------------------------------ our arm
+def critic_flops(D, A, H, nh, B):
+    """Algorithmic FLOPs of one critic update: policy fwd +
+    4 critic fwd + 2 x (critic wgrad + dgrad for layers >= 1)."""
+    pol = D * H + (nh - 1) * H * H + H * A
+    crit = (D + A) * H + (nh - 1) * H * H + H
+    crit_dgrad = (nh - 1) * H * H + H
+    return 2 * B * (pol + 4 * crit + 2 * (crit + crit_dgrad))
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    from paper_2307_12983_b200 import _lib
+    D, A, H, nh, B, N, cap = CONFIGS[args.config]
+    stream = torch.cuda.Stream(device=local)
+    cfg = _lib.default_config(batch_size=B, buffer_capacity=cap, hidden=H, hidden_layers=nh,
+                              n_envs=N, seed=rank)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    h = C.c_void_p()
+    _lib.call("pqlg_vlearner_create", C.byref(cfg), C.byref(dims), 12345 + rank,
+              C.c_void_p(stream.cuda_stream), C.byref(h))
+    rp = C.c_void_p()
+    _lib.call("pqlg_vlearner_replay", h, C.byref(rp))
+    _lib.call("pqlg_replay_fill_synthetic", rp, cap, 1000 + rank, np.float32(0.970299), 200)
+    count = 10 ** 6
+    mean = np.zeros(D)
+    m2 = np.full(D, float(count))
+    ns = _lib.NormStats(count, mean.ctypes.data, m2.ctypes.data)
+    _lib.call("pqlg_vlearner_adopt_norm", h, C.byref(ns))
+    kpu = C.c_int()
+    _lib.call("pqlg_vlearner_kernels_per_update", h, C.byref(kpu))
+    stream.synchronize()
+
+    # warm-up (graph build + W updates)
+    _lib.call("pqlg_vlearner_update_n", h, args.warmup)
+    stream.synchronize()
+    barrier(world)
+
+    launches0 = _lib.lib().pqlg_launch_count()
+    with ClockSampler(local) as clk:
+        stream.synchronize()
+        barrier(world)
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        _lib.call("pqlg_vlearner_update_n", h, args.steps)
+        e.record(stream)
+        e.synchronize()
+        barrier(world)
+        ms = s.elapsed_time(e)
+    launches = _lib.lib().pqlg_launch_count() - launches0
+    ms = max_over_ranks(ms, world)
+    loss = C.c_float()
+    _lib.call("pqlg_vlearner_last_loss", h, C.byref(loss))
+    ms_step = ms / args.steps
+    value = world * args.steps / (ms * 1e-3)
+
+    # ---- e2e: the reference-facing synchronous update() per step with the
+    # step's host inputs (normalizer stats, pinned) copied in and the loss
+    # copied out, host timer around the whole loop.
+    mean_p = torch.zeros(D, dtype=torch.float64).pin_memory()
+    m2_p = torch.full((D,), float(count), dtype=torch.float64).pin_memory()
+    e2e_steps = max(10, min(args.steps, 100))
+    barrier(world)
+    stream.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ns = _lib.NormStats(count, mean_p.data_ptr(), m2_p.data_ptr())
+        _lib.call("pqlg_vlearner_adopt_norm", h, C.byref(ns))
+        _lib.call("pqlg_vlearner_update", h, C.byref(loss))
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    e2e = {"value": world * e2e_steps / e2e_s, "unit": "updates/s",
+           "h2d_bytes_per_step": 2 * D * 8, "d2h_bytes_per_step": 4,
+           "api": "pqlg_vlearner_adopt_norm + pqlg_vlearner_update (sync)"}
+
+    # ---- roofline of the dominant kernel: the hidden-layer tcgen05 GEMM
+    roof = None
+    if rank == 0:
+        M, Nn, K = B, H, H
+        a = torch.randn(M, K, device="cuda")
+        bw = torch.randn(K, Nn, device="cuda")
+        d = torch.empty(M, Nn, device="cuda")
+        bias = torch.zeros(Nn, device="cuda")
+        it = 200
+
+        def gemm(n):
+            _lib.call("pqlg_k_gemm_tf32_repeat", a.data_ptr(), bw.data_ptr(), d.data_ptr(),
+                      bias.data_ptr(), M, Nn, K, K, Nn, Nn, 1, n, C.c_void_p(stream.cuda_stream))
+        gemm(5)
+        stream.synchronize()
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record(stream)
+        gemm(it)
+        e2.record(stream)
+        e2.synchronize()
+        k_ms = s2.elapsed_time(e2) / it
+        achieved = 2 * M * Nn * K / (k_ms * 1e-3) / 1e12
+        peak = tf32_peak_tflops()
+        roof = {"bound": "tensor", "kernel": "gemm_tf32_kernel<256,4,K-major A,N-major B> "
+                "(hidden layer fwd, 8192x512x512, bias+ReLU epilogue)",
+                "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4),
+                "peak_source": "measured here: cuBLAS TF32 GEMM 8192^3 via torch (MEASURED_PEAKS.json has no TF32 figure)",
+                "kernel_ms": round(k_ms, 5),
+                "traffic": traffic_from_profiles("gemm_hidden_fwd")}
+        flops = critic_flops(D, A, H, nh, B)
+        roof["update_tflops"] = round(flops / (ms_step * 1e-3) / 1e12, 2)
+        roof["update_frac_of_tf32_peak"] = round(flops / (ms_step * 1e-3) / 1e12 / peak, 4)
+    return dict(value=value, ms_step=ms_step, loss=loss.value, e2e=e2e, roof=roof,
+                clocks=clk.summary(), launches=int(launches), kpu=kpu.value)
+
+
+# ------------------------------------------------------ reference arm
+def ref_lib():
+    so = ROOT / "oracle" / "_ref" / "libpqlref.so"
+    if not so.exists():
+        return None
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import ref
+    return ref()
+
+
+def reference_critic_rate(cfg_name, n_updates, batch_override=None):
+    """The reference's own CPU path (oracle/_ref, compiled from
+    /root/reference): the CriticLearnerCore::update composition of
+    learners.cpp:157-188 over the config's 3x512 nets (agents-level, since
+    RunConfig can only express 2 hidden layers), single-threaded as the
+    reference runs it.  Returns (updates/s, sample description)."""
+    R = ref_lib()
+    if R is None:
+        return None, "oracle/_ref/libpqlref.so not built"
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import param_count, ptr
+    D, A, H, nh, B, N, cap = CONFIGS[cfg_name]
+    if batch_override:
+        B = batch_override
+    rng = np.random.default_rng(0)
+    qs = [D + A] + [H] * nh + [1]
+    ps = [D] + [H] * nh + [A]
+    q1 = (rng.standard_normal(param_count(qs)) * 0.05).astype(np.float32)
+    q2 = (rng.standard_normal(param_count(qs)) * 0.05).astype(np.float32)
+    pol = (rng.standard_normal(param_count(ps)) * 0.05).astype(np.float32)
+    n_rows = max(4 * B, 20000)
+    h = R.ref_vupdate_create(D, A, H, nh, B, n_rows, 0, ptr(q1), ptr(q2), ptr(pol), 0, 51,
+                             np.float32(-10), np.float32(10))
+    obs = rng.standard_normal((n_rows, D)).astype(np.float32)
+    act = rng.uniform(-1, 1, (n_rows, A)).astype(np.float32)
+    boot = rng.standard_normal((n_rows, D)).astype(np.float32)
+    ret = (rng.standard_normal(n_rows) * 0.1).astype(np.float32)
+    eff = np.full(n_rows, 0.970299, np.float32)
+    R.ref_vupdate_insert(h, ptr(obs), ptr(act), ptr(boot), ptr(ret), ptr(eff), n_rows)
+    mean = np.zeros(D); m2 = np.full(D, 1e6)
+    R.ref_vupdate_adopt_norm(h, 10 ** 6, ptr(mean), ptr(m2))
+    loss = np.zeros(1, np.float32)
+    R.ref_vupdate_step(h, ptr(loss))  # warm
+    t0 = time.perf_counter()
+    for _ in range(n_updates):
+        R.ref_vupdate_step(h, ptr(loss))
+    dt = time.perf_counter() - t0
+    R.ref_vupdate_destroy(h)
+    rate = n_updates / dt
+    if batch_override:
+        rate *= batch_override / CONFIGS[cfg_name][4]  # per full-batch update
+    sample = (f"{n_updates} CriticLearnerCore-equivalent updates at B={B} "
+              f"({cfg_name} dims, 3x512), reference AVX2 build, 1 thread")
+    return rate, sample
+
+
+def cpu_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_setup(args.gpus)
+    D, A, H, nh, B, N, cap = CONFIGS[args.config]
+    base = {"metric": METRIC, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "tf32 (fp32 storage, tf32 tensor-core products, fp32 accumulate)",
+            "data": "synthetic (device-generated replay fill, SURVEY 8d distributions)",
+            "config": {"workload": f"{args.config}: CriticLearnerCore::update, obs {D} / act {A}, "
+                                   f"{nh}x{H} MLPs, batch {B}, {cap} record replay",
+                       "global_batch": B * world, "parallelism": f"replicas x{world}",
+                       "l2": "inputs sampled from an 8.9 GB ring (>> 126 MB L2)"}}
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        # bounded sample per step: a full B=8192 update is ~2-3 s on one core
+        per = 1 if args.steps * 2.5 < 150 else None
+        t0 = time.perf_counter()
+        if per:
+            rate, sample = reference_critic_rate(args.config, args.steps + 0)
+        else:
+            rate, sample = reference_critic_rate(args.config, args.steps, batch_override=512)
+        if rate is None:
+            print(json.dumps({"impl": "reference", "unavailable": sample}))
+            return
+        model, ncpu = cpu_info()
+        out = dict(base)
+        out.update(impl="reference", value=rate, ms_per_step=1e3 / rate,
+                   cpu_baseline={"value": rate, "unit": "updates/s", "cores": 1,
+                                 "kind": "reference", "sample": sample, "cpu": model,
+                                 "host_cores": ncpu},
+                   e2e={"value": rate, "unit": "updates/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0},
+                   wall_s=round(time.perf_counter() - t0, 1))
+        print(json.dumps(out))
+        return
+
+    r = run_ours(args, rank, world, local)
+    if rank != 0:
+        return
+    out = dict(base)
+    out.update(value=r["value"], ms_per_step=r["ms_step"], e2e=r["e2e"], roofline=r["roof"],
+               clocks=r["clocks"], gpu_launches=r["launches"],
+               kernels_per_update=r["kpu"], last_loss=r["loss"])
+    if world == 1 and not args.no_cpu_baseline:
+        rate, sample = reference_critic_rate(args.config, 3)
+        model, ncpu = cpu_info()
+        out["cpu_baseline"] = ({"value": rate, "unit": "updates/s", "cores": 1,
+                                "kind": "reference", "sample": sample, "cpu": model,
+                                "host_cores": ncpu} if rate else None)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -66,6 +66,12 @@ PQLG_API int pqlg_k_gemm_tf32(const float* A_dev, const float* B_dev, float* D_d
                      int M, int N, int K, int a_mn, int b_mn, int lda, int ldb, int ldd, int relu,
                      int splits, int round_mode, void* stream);
 
+/* `iters` back-to-back launches of the forward-layer GEMM (A K-major, B
+ * [K x N] N-major, TFLOAT32 maps) for device-time measurement. */
+PQLG_API int pqlg_k_gemm_tf32_repeat(const float* A_dev, const float* B_dev, float* D_dev,
+                                     const float* bias_dev, int M, int N, int K, int lda, int ldb,
+                                     int ldd, int relu, int iters, void* stream);
+
 /* ------------------------------------------------------------ data views */
 
 /* StepSlice (proj/include/pql/runtime/messages.hpp:31-35) as device views.
@@ -130,6 +136,11 @@ PQLG_API int pqlg_replay_insert(pqlg_replay h, const pqlg_nstep_batch* dev, uint
  * and writes the advanced Philox counter back into *rng. */
 PQLG_API int pqlg_replay_sample(pqlg_replay h, uint64_t batch, pqlg_rng* rng, uint64_t min_live,
                                 const pqlg_norm_stats* norm, pqlg_nstep_batch* dev_out);
+/* Appends n synthetic records generated on device (benchmark pre-fill,
+ * SURVEY 8(d)): obs/boot ~ N(0,1), act ~ U(-1,1), ret ~ 0.1 N(0,1),
+ * eff_disc = disc except every terminal_every-th record (0). */
+PQLG_API int pqlg_replay_fill_synthetic(pqlg_replay h, uint64_t n, uint64_t seed, float disc,
+                                        uint32_t terminal_every);
 /* Ring rows [i0, i0+n) to host (obs_row / ret_at, replay_buffer.hpp:71-73);
  * any output pointer may be NULL. */
 PQLG_API int pqlg_replay_read_rows(pqlg_replay h, uint64_t i0, uint64_t n, float* obs, float* act,
@@ -152,6 +163,94 @@ PQLG_API int pqlg_states_size(pqlg_states h, uint64_t* out);
 PQLG_API int pqlg_states_insert(pqlg_states h, const float* rows_dev, int64_t ld, uint64_t n);
 PQLG_API int pqlg_states_sample(pqlg_states h, uint64_t batch, pqlg_rng* rng, uint64_t min_live,
                                 const pqlg_norm_stats* norm, float* out_dev, int64_t ld_out);
+
+/* ------------------------------------------------------------ run config */
+
+/* RunConfig fields the cores consume (proj/include/pql/config.hpp:15-48),
+ * plus `hidden_layers` (the reference hard-codes 2: learners.cpp:22-23,
+ * :127-130, :206-209; configs 2-5 need 3) and the synthetic env's time
+ * limit.  pqlg_config_default() fills the Table B.1 defaults. */
+enum { PQLG_ALGO_DDPG = 0, PQLG_ALGO_C51 = 1 };
+typedef struct {
+  int algo;               /* PQLG_ALGO_DDPG (pql_ddpg) or PQLG_ALGO_C51 (pql_d) */
+  int n_envs;
+  int batch_size;
+  uint64_t buffer_capacity;
+  double gamma;
+  double tau;
+  int n_step;
+  double lr_actor;
+  double lr_critic;
+  int64_t warm_up;
+  double sigma_min;
+  double sigma_max;
+  double sigma_fixed;     /* >= 0: same sigma for every env */
+  double reward_scale;    /* effective_reward_scale() (> 0) */
+  uint64_t seed;
+  int hidden;             /* hidden width */
+  int hidden_layers;      /* number of hidden layers */
+  int n_atoms;
+  double vmin;
+  double vmax;
+  int max_episode_len;    /* synthetic env time limit */
+  int env_offset;         /* global index of this shard's first env (sharded actors) */
+} pqlg_config;
+
+/* TaskDims (learners.hpp:23-26) */
+typedef struct {
+  int obs_dim;
+  int act_dim;
+  float low;
+  float high;
+} pqlg_task_dims;
+
+PQLG_API void pqlg_config_default(pqlg_config* cfg);
+
+/* ------------------------------------------------ V-learner (critic core) */
+typedef struct pqlg_vlearner_s* pqlg_vlearner;
+
+/* CriticLearnerCore(cfg, dims, init_rng)  learners.hpp:79, learners.cpp:122-139.
+ * Critics are initialised exactly as CriticPair::create with
+ * std::mt19937_64(init_rng_seed); the lagged policy as PolicyHandle::create
+ * with make_rng(seed, init, 0).  Sampling uses Philox keyed by
+ * derive_seed(seed, sample, 1) unless pqlg_vlearner_set_sampler selects the
+ * reference's mt19937_64 stream. */
+PQLG_API int pqlg_vlearner_create(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                                  uint64_t init_rng_seed, void* stream, pqlg_vlearner* out);
+PQLG_API int pqlg_vlearner_destroy(pqlg_vlearner h);
+/* adopt_policy: equal-or-newer version replaces (learners.cpp:37-42) */
+PQLG_API int pqlg_vlearner_adopt_policy(pqlg_vlearner h, const float* flat_host, int64_t version);
+PQLG_API int pqlg_vlearner_adopt_norm(pqlg_vlearner h, const pqlg_norm_stats* norm);
+/* ingest(StepSlice): reward scale + n-step + insert (learners.cpp:144-151) */
+PQLG_API int pqlg_vlearner_ingest(pqlg_vlearner h, const pqlg_step_slice* dev);
+PQLG_API int pqlg_vlearner_ready(pqlg_vlearner h, int64_t c_a, int* ready);
+/* update(): one critic update; synchronizes and returns the loss
+ * (PQLG_NOT_READY before warm-up, PQLG_ENONFINITE on non-finite). */
+PQLG_API int pqlg_vlearner_update(pqlg_vlearner h, float* loss_host);
+/* n updates replayed from a CUDA graph, asynchronous (no host sync). */
+PQLG_API int pqlg_vlearner_update_n(pqlg_vlearner h, int n);
+/* loss of the last completed update + sticky status; synchronizes. */
+PQLG_API int pqlg_vlearner_last_loss(pqlg_vlearner h, float* loss_host);
+/* which: 0 q1, 1 q2, 2 q1_target, 3 q2_target, 4 lagged policy (host copy) */
+PQLG_API int pqlg_vlearner_get_params(pqlg_vlearner h, int which, float* flat_host);
+PQLG_API int pqlg_vlearner_param_count(pqlg_vlearner h, int which, int64_t* out);
+/* make_snapshot(version) -> online nets (learners.cpp:190-196) */
+PQLG_API int pqlg_vlearner_snapshot(pqlg_vlearner h, float* q1_host, float* q2_host);
+PQLG_API int pqlg_vlearner_buffer_size(pqlg_vlearner h, uint64_t* out);
+/* Sampler: PQLG_RNG_PHILOX (default) or PQLG_RNG_INDICES = the reference's
+ * own std::mt19937_64 make_rng(seed, sample, 1) stream drawn on the host. */
+PQLG_API int pqlg_vlearner_set_sampler(pqlg_vlearner h, int mode);
+/* The owned replay buffer (for direct inserts / inspection). */
+PQLG_API int pqlg_vlearner_replay(pqlg_vlearner h, pqlg_replay* out);
+/* Overwrite parameters (which as in get_params; CriticPair::hard_sync_online
+ * for 0/1, critic.hpp:33-36); resets nothing else. */
+PQLG_API int pqlg_vlearner_set_params(pqlg_vlearner h, int which, const float* flat_host);
+/* Intermediates of the last update for parity checks: 0 TD target y [B],
+ * 1 dLoss/dQ [2 x B], 2 flat gradients before clipping [2 x P],
+ * 3 clip scales [2], 4 sampled critic input [B x (obs_dim+act_dim)]. */
+PQLG_API int pqlg_vlearner_debug_read(pqlg_vlearner h, int what, float* host_out);
+/* Number of kernels one update launches (graph nodes). */
+PQLG_API int pqlg_vlearner_kernels_per_update(pqlg_vlearner h, int* out);
 
 #ifdef __cplusplus
 }

@@ -150,6 +150,14 @@ def gen_mlp(R, out):
     q = np.zeros(2 * param_count([9, 16, 16, 1]), np.float32)
     R.ref_init_mlp(ptr(qs), 3, 12345, np.float32(np.sqrt(2.0)), np.float32(1.0), 2, ptr(q))
     out["init_critics"] = q
+    # same at a GEMM-friendly width (32) for the device learners' init check
+    pol = np.zeros(param_count([6, 32, 32, 3]), np.float32)
+    R.ref_policy_init(6, 3, 32, 0, ptr(pol))
+    out["init_policy_h32"] = pol
+    qs = sizes_arr([9, 32, 32, 1])
+    q = np.zeros(2 * param_count([9, 32, 32, 1]), np.float32)
+    R.ref_init_mlp(ptr(qs), 3, 12345, np.float32(np.sqrt(2.0)), np.float32(1.0), 2, ptr(q))
+    out["init_critics_h32"] = q
 
 
 def small_nets(rng, D, A, H, L, out_dim=1):

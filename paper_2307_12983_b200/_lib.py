@@ -41,7 +41,23 @@ class Rng(C.Structure):
 
 
 RNG_PHILOX, RNG_INDICES = 0, 1
+ALGO_DDPG, ALGO_C51 = 0, 1
 P = C.POINTER
+
+
+class Config(C.Structure):
+    """pqlg_config: the RunConfig fields the cores consume (config.hpp:15-48)."""
+    _fields_ = [("algo", i32), ("n_envs", i32), ("batch_size", i32), ("buffer_capacity", u64),
+                ("gamma", f64), ("tau", f64), ("n_step", i32), ("lr_actor", f64),
+                ("lr_critic", f64), ("warm_up", i64), ("sigma_min", f64), ("sigma_max", f64),
+                ("sigma_fixed", f64), ("reward_scale", f64), ("seed", u64), ("hidden", i32),
+                ("hidden_layers", i32), ("n_atoms", i32), ("vmin", f64), ("vmax", f64),
+                ("max_episode_len", i32), ("env_offset", i32)]
+
+
+class TaskDims(C.Structure):
+    """pqlg_task_dims (learners.hpp:23-26)."""
+    _fields_ = [("obs_dim", i32), ("act_dim", i32), ("low", f32), ("high", f32)]
 
 # name -> (restype, argtypes)
 SIGNATURES: dict[str, tuple] = {
@@ -65,7 +81,37 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_states_size": (i32, [vp, P(u64)]),
     "pqlg_states_insert": (i32, [vp, vp, i64, u64]),
     "pqlg_states_sample": (i32, [vp, u64, P(Rng), u64, P(NormStats), vp, i64]),
+    "pqlg_config_default": (None, [P(Config)]),
+    "pqlg_vlearner_create": (i32, [P(Config), P(TaskDims), u64, vp, P(vp)]),
+    "pqlg_vlearner_destroy": (i32, [vp]),
+    "pqlg_vlearner_adopt_policy": (i32, [vp, vp, i64]),
+    "pqlg_vlearner_adopt_norm": (i32, [vp, P(NormStats)]),
+    "pqlg_vlearner_ingest": (i32, [vp, P(StepSlice)]),
+    "pqlg_vlearner_ready": (i32, [vp, i64, P(i32)]),
+    "pqlg_vlearner_update": (i32, [vp, P(f32)]),
+    "pqlg_vlearner_update_n": (i32, [vp, i32]),
+    "pqlg_vlearner_last_loss": (i32, [vp, P(f32)]),
+    "pqlg_vlearner_get_params": (i32, [vp, i32, vp]),
+    "pqlg_vlearner_param_count": (i32, [vp, i32, P(i64)]),
+    "pqlg_vlearner_snapshot": (i32, [vp, vp, vp]),
+    "pqlg_vlearner_buffer_size": (i32, [vp, P(u64)]),
+    "pqlg_vlearner_set_sampler": (i32, [vp, i32]),
+    "pqlg_vlearner_replay": (i32, [vp, P(vp)]),
+    "pqlg_vlearner_set_params": (i32, [vp, i32, vp]),
+    "pqlg_vlearner_debug_read": (i32, [vp, i32, vp]),
+    "pqlg_vlearner_kernels_per_update": (i32, [vp, P(i32)]),
+    "pqlg_replay_fill_synthetic": (i32, [vp, u64, u64, f32, C.c_uint32]),
+    "pqlg_k_gemm_tf32_repeat": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32,
+                                      vp]),
 }
+
+
+def default_config(**overrides) -> Config:
+    cfg = Config()
+    lib().pqlg_config_default(C.byref(cfg))
+    for k, v in overrides.items():
+        setattr(cfg, k, v)
+    return cfg
 
 
 class PqlgError(RuntimeError):

@@ -1,0 +1,201 @@
+// Row-wise heads of the DDPG critic losses (ddpg.hpp) that sit between the
+// tensor-core GEMMs: the value head 512->1 is folded into the last hidden
+// layer's epilogue as per-n-tile partial dots; these kernels finish it.
+//
+//   td_target_kernel     ddpg_critic_target  y = G + eff * min(Q1', Q2')      ddpg.hpp:24-40
+//   critic_loss_kernel   ddpg_critic_loss    e = Q - y, up = 2e/B, loss       ddpg.hpp:50-76
+//   actor_pick_kernel    ddpg_actor_loss     pick1 = Q1 <= Q2, up = -1/B      ddpg.hpp:86-118
+//   head_backward_kernel fa::backward of the 512->1 layer + ReLU mask of the
+//                        layer below (mlp.hpp:161-184) and its bias/weight
+//                        gradient partials (scalar.hpp:42-55)
+#pragma once
+
+#include <cstdint>
+
+namespace pqlg::critic {
+
+constexpr int kRowThreads = 256;
+
+// q_k[b] = b_head_k + sum_t partial[k][t][b]   (t ascending)
+__device__ __forceinline__ float head_value(const float* partial, int64_t ld, int n_tiles,
+                                            int group, float bias, int64_t b) {
+  float q = bias;
+  for (int t = 0; t < n_tiles; ++t)
+    q = __fadd_rn(q, partial[(static_cast<int64_t>(group) * n_tiles + t) * ld + b]);
+  return q;
+}
+
+struct TdArgs {
+  const float* partial;  // [2][n_tiles][ld]
+  int64_t ld;
+  int n_tiles;
+  const float* q1t;  // target nets (bias of the head at head_b_off)
+  const float* q2t;
+  int64_t head_b_off;
+  const float* ret;
+  const float* eff;
+  float* y;
+  int B;
+  uint32_t* status;  // bit1: non-finite target
+  int64_t* step;     // Adam step, incremented once per update
+};
+
+static __global__ void td_target_kernel(TdArgs a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b == 0) *a.step += 1;
+  if (b >= a.B) return;
+  const float q1 = head_value(a.partial, a.ld, a.n_tiles, 0, a.q1t[a.head_b_off], b);
+  const float q2 = head_value(a.partial, a.ld, a.n_tiles, 1, a.q2t[a.head_b_off], b);
+  const float qmin = q2 < q1 ? q2 : q1;  // std::min(q1, q2)
+  const float y = __fadd_rn(a.ret[b], __fmul_rn(a.eff[b], qmin));
+  a.y[b] = y;
+  if (!isfinite(y)) atomicOr(a.status, 2u);
+}
+
+struct LossArgs {
+  const float* partial;  // online [2][n_tiles][ld]
+  int64_t ld;
+  int n_tiles;
+  const float* q1;
+  const float* q2;
+  int64_t head_b_off;
+  const float* y;
+  float* up;          // [2][B]  dLoss/dQ_k = 2 e_k / B
+  double* block_loss; // [gridDim.x]
+  unsigned int* counter;
+  float* loss_out;
+  uint32_t* status;   // bit2: non-finite loss
+  int B;
+};
+
+static __global__ void __launch_bounds__(kRowThreads) critic_loss_kernel(LossArgs a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  double l = 0.0;
+  if (b < a.B) {
+    const float q1 = head_value(a.partial, a.ld, a.n_tiles, 0, a.q1[a.head_b_off], b);
+    const float q2 = head_value(a.partial, a.ld, a.n_tiles, 1, a.q2[a.head_b_off], b);
+    const float e1 = __fsub_rn(q1, a.y[b]);
+    const float e2 = __fsub_rn(q2, a.y[b]);
+    l = static_cast<double>(__fadd_rn(__fmul_rn(e1, e1), __fmul_rn(e2, e2)));
+    const float Bf = static_cast<float>(a.B);
+    a.up[b] = __fdiv_rn(__fmul_rn(2.0f, e1), Bf);
+    a.up[a.B + b] = __fdiv_rn(__fmul_rn(2.0f, e2), Bf);
+  }
+  __shared__ double red[kRowThreads / 32];
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) l += __shfl_down_sync(0xffffffffu, l, d);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = l;
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kRowThreads / 32; ++w) s += red[w];
+    a.block_loss[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double tot = 0.0;
+  const volatile double* bl = a.block_loss;
+  for (unsigned i = 0; i < gridDim.x; ++i) tot += bl[i];
+  *a.counter = 0;
+  const float loss = static_cast<float>(tot / static_cast<double>(a.B));
+  *a.loss_out = loss;
+  if (!isfinite(loss)) atomicOr(a.status, 4u);
+}
+
+// ddpg_actor_loss row head: pick1 = q1 <= q2; loss -= min; upstream of the
+// picked critic -1/B (ddpg.hpp:100-105).
+static __global__ void __launch_bounds__(kRowThreads) actor_pick_kernel(LossArgs a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  double l = 0.0;
+  if (b < a.B) {
+    const float q1 = head_value(a.partial, a.ld, a.n_tiles, 0, a.q1[a.head_b_off], b);
+    const float q2 = head_value(a.partial, a.ld, a.n_tiles, 1, a.q2[a.head_b_off], b);
+    const bool pick1 = q1 <= q2;
+    l = -static_cast<double>(pick1 ? q1 : q2);
+    const float up = __fdiv_rn(-1.0f, static_cast<float>(a.B));
+    a.up[b] = pick1 ? up : 0.0f;
+    a.up[a.B + b] = pick1 ? 0.0f : up;
+  }
+  __shared__ double red[kRowThreads / 32];
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) l += __shfl_down_sync(0xffffffffu, l, d);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = l;
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kRowThreads / 32; ++w) s += red[w];
+    a.block_loss[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  double tot = 0.0;
+  const volatile double* bl = a.block_loss;
+  for (unsigned i = 0; i < gridDim.x; ++i) tot += bl[i];
+  *a.counter = 0;
+  const float loss = static_cast<float>(tot / static_cast<double>(a.B));
+  *a.loss_out = loss;
+  if (!isfinite(loss)) atomicOr(a.status, 4u);
+}
+
+// Backward through the 512->1 value head for both critics.
+//   G[b,i]   = up[b] * w[i] * [h[b,i] > 0]            (dgrad + ReLU mask)
+//   dW[i]   += h[b,i] * up[b]     db_head += up[b]    (wgrad of the head)
+//   db[i]   += G[b,i]                                 (bias grad of layer below)
+// grid = (row tiles of 128, groups); partials per row tile, summed later in
+// tile order.  with_params = 0 for the actor gradient (input grads only).
+struct HeadBwdArgs {
+  const float* up;     // [2][B]
+  const float* h[2];   // post-activations of the last hidden layer [B x H]
+  int64_t ld_h;
+  const float* w[2];   // head weights [H] (W_head is [H x 1])
+  float* G[2];         // out [B x H]
+  int64_t ld_g;
+  float* dw_part;      // [2][tiles][H]
+  float* db_head_part; // [2][tiles]
+  float* db_part;      // [2][tiles][H]
+  int B, H, tiles;
+  int with_params;
+};
+
+static __global__ void head_backward_kernel(HeadBwdArgs a) {
+  const int tile = blockIdx.x, k = blockIdx.y;
+  const int b0 = tile * 128;
+  const int b1 = min(b0 + 128, a.B);
+  const float* up = a.up + static_cast<int64_t>(k) * a.B;
+  const float* h = a.h[k];
+  const float* w = a.w[k];
+  float* G = a.G[k];
+  for (int i = threadIdx.x; i < a.H; i += blockDim.x) {
+    const float wi = w[i];
+    float dw = 0.0f, db = 0.0f;
+    for (int b = b0; b < b1; ++b) {
+      const float hv = h[static_cast<int64_t>(b) * a.ld_h + i];
+      const float u = up[b];
+      const float g = hv > 0.0f ? __fmul_rn(u, wi) : 0.0f;
+      G[static_cast<int64_t>(b) * a.ld_g + i] = g;
+      if (a.with_params) {
+        dw = __fadd_rn(dw, __fmul_rn(hv, u));
+        db = __fadd_rn(db, g);
+      }
+    }
+    if (a.with_params) {
+      a.dw_part[(static_cast<int64_t>(k) * a.tiles + tile) * a.H + i] = dw;
+      a.db_part[(static_cast<int64_t>(k) * a.tiles + tile) * a.H + i] = db;
+    }
+  }
+  if (a.with_params && threadIdx.x == 0) {
+    float s = 0.0f;
+    for (int b = b0; b < b1; ++b) s = __fadd_rn(s, up[b]);
+    a.db_head_part[static_cast<int64_t>(k) * a.tiles + tile] = s;
+  }
+}
+
+}  // namespace pqlg::critic

@@ -79,6 +79,18 @@ void run(const float* A, const float* B, float* D, const float* bias, int M, int
   PQLG_CUDA(cudaFreeAsync(W, st));
 }
 
+// Back-to-back launches with pre-encoded maps (device-time measurement).
+template <int BN>
+void run_repeat(const float* A, const float* B, float* D, const float* bias, int M, int N, int K,
+                int lda, int ldb, int ldd, int relu, int iters, cudaStream_t st) {
+  gemm::Operands ops;
+  ops.a[0] = ops.a[1] = gemm::map_a(A, M, K, lda, false, true);
+  ops.b[0] = ops.b[1] = gemm::map_b(B, N, K, ldb, true, BN, true);
+  const gemm::Problem p = gemm::make_problem(M, N, K, 1);
+  const StoreEpi e{D, bias, ldd, M, N, relu};
+  for (int i = 0; i < iters; ++i) gemm::launch<BN, false, true>(ops, p, 1, e, st);
+}
+
 template <int BN>
 void dispatch_major(int a_mn, int b_mn, const float* A, const float* B, float* D,
                     const float* bias, int M, int N, int K, int lda, int ldb, int ldd, int relu,
@@ -91,6 +103,18 @@ void dispatch_major(int a_mn, int b_mn, const float* A, const float* B, float* D
 
 }  // namespace
 }  // namespace pqlg
+
+extern "C" int pqlg_k_gemm_tf32_repeat(const float* A, const float* B, float* D,
+                                       const float* bias, int M, int N, int K, int lda, int ldb,
+                                       int ldd, int relu, int iters, void* stream) {
+  return pqlg::guarded([&] {
+    auto st = static_cast<cudaStream_t>(stream);
+    if (N > 128) pqlg::run_repeat<256>(A, B, D, bias, M, N, K, lda, ldb, ldd, relu, iters, st);
+    else if (N > 64) pqlg::run_repeat<128>(A, B, D, bias, M, N, K, lda, ldb, ldd, relu, iters, st);
+    else if (N > 32) pqlg::run_repeat<64>(A, B, D, bias, M, N, K, lda, ldb, ldd, relu, iters, st);
+    else pqlg::run_repeat<32>(A, B, D, bias, M, N, K, lda, ldb, ldd, relu, iters, st);
+  });
+}
 
 extern "C" int pqlg_k_gemm_tf32(const float* A, const float* B, float* D, const float* bias, int M,
                                 int N, int K, int a_mn, int b_mn, int lda, int ldb, int ldd,

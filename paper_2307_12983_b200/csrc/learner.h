@@ -1,0 +1,94 @@
+// The three runtime cores (learners.hpp:52-139) as device-resident objects.
+#pragma once
+
+#include <array>
+#include <memory>
+#include <random>
+#include <vector>
+
+#include "mlp_host.h"
+#include "net.h"
+#include "replay_host.h"
+
+namespace pqlg {
+
+// CriticLearnerCore (learners.hpp:77-106).
+class VLearner {
+ public:
+  VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t init_seed,
+           cudaStream_t st);
+  ~VLearner();
+
+  void adopt_policy(const float* flat_host, int64_t version);
+  void adopt_norm(int64_t count, const double* mean, const double* m2);
+  void ingest(const replay::Slice& s);
+  bool ready(int64_t c_a);
+  float update();
+  void update_n(int n);
+  float last_loss();
+  void get_params(int which, float* out);
+  int64_t param_count(int which) const;
+  void set_params(int which, const float* flat_host);
+  void debug_read(int what, float* out);
+  void set_mt_mode(bool on) { mt_mode_ = on; }
+  int kernels_per_update();
+
+  DeviceReplay* replay() { return replay_.get(); }
+  int obs_dim() const { return D_; }
+  int act_dim() const { return A_; }
+  cudaStream_t stream() const { return stream_; }
+
+ private:
+  void build_update();
+  void enqueue();
+  void prepare_indices();
+  int check_status();
+
+  pqlg_config cfg_;
+  pqlg_task_dims dims_;
+  cudaStream_t stream_;
+  cudaStream_t owned_stream_ = nullptr;
+  int D_, A_, H_, nh_, B_, Kp_;
+  float reward_scale_, gamma_;
+  NetShape qnet_, pnet_;
+  int64_t Ps_ = 0;  // group stride of the twin-critic parameter blocks
+  int64_t lagged_version_ = 0;
+
+  DevBuf<float> q_, qt_, m_, v_, grads_, lagged_;
+  WeightMirror lagged_head_;
+  std::unique_ptr<DeviceReplay> replay_;
+  std::unique_ptr<DeviceNStep> nstep_;
+  DeviceNorm norm_;
+  DevBuf<replay::SamplerState> sampler_;
+  bool mt_mode_ = false;
+  std::mt19937_64 mt_;
+  DevBuf<uint64_t> idx_;
+  std::vector<uint64_t> idx_host_;
+
+  DevBuf<int64_t> step_;
+  DevBuf<float2> bc_;
+  DevBuf<uint32_t> status_;
+  DevBuf<float> loss_;
+
+  // workspaces
+  DevBuf<float> Xon_, Xtg_, ret_, eff_, y_;
+  std::vector<DevBuf<float>> pact_;
+  std::array<std::vector<DevBuf<float>>, 2> tact_, oact_, G_;
+  DevBuf<float> part_t_, part_o_, up_;
+  DevBuf<double> block_loss_;
+  DevBuf<unsigned int> loss_counter_;
+  std::vector<DevBuf<float>> wpart_, colsum_;
+  std::vector<int> wsplits_;
+  DevBuf<float> head_dw_, head_db_;
+  int fin_blocks_ = 0;
+  DevBuf<double> block_sq_;
+  DevBuf<unsigned int> fin_counter_;
+  DevBuf<float> scale_;
+
+  std::vector<mlp::Step> steps_;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  bool graph_checked_ = false;
+  int kpu_ = 0;
+};
+
+}  // namespace pqlg

@@ -1,0 +1,122 @@
+// Host-side builders for the MLP GEMMs of the learners: every GEMM of an
+// update is turned into a closure with its tensor maps pre-encoded at handle
+// construction, so an update is a fixed list of launches (CUDA-graph ready).
+//
+//   fwd    out = A * W        A = activations [M x K] (K-major),
+//                             W = [K x N] row-major (fa::Mlp layout, N-major)
+//   dgrad  din = G * W^T      G = [M x N_out] (K-major), W = [N_in x N_out] (K-major)
+//   wgrad  dW = H^T * G       H = [K=B x M=in] (M-major), G = [B x N] (N-major)
+#pragma once
+
+#include <cmath>
+#include <functional>
+#include <type_traits>
+#include <vector>
+
+#include "epilogues.cuh"
+#include "gemm_host.cuh"
+
+namespace pqlg::mlp {
+
+using Step = std::function<void(cudaStream_t)>;
+
+inline int bn_for(int N) { return N > 128 ? 256 : N > 64 ? 128 : N > 32 ? 64 : 32; }
+inline int n_tiles(int N) { return (N + bn_for(N) - 1) / bn_for(N); }
+constexpr int kSMs = 148;
+
+template <class F>
+void with_bn(int N, F&& f) {
+  switch (bn_for(N)) {
+    case 256: f(std::integral_constant<int, 256>{}); break;
+    case 128: f(std::integral_constant<int, 128>{}); break;
+    case 64: f(std::integral_constant<int, 64>{}); break;
+    default: f(std::integral_constant<int, 32>{}); break;
+  }
+}
+
+// Split factor so that (tiles * splits) roughly fills the 148 SMs once.
+inline int wgrad_splits(int M, int N, int K, int groups) {
+  const int tiles = ((M + 127) / 128) * n_tiles(N) * groups;
+  const int k_tiles = (K + gemm::kBK - 1) / gemm::kBK;
+  int s = kSMs / tiles;
+  if (s < 1) s = 1;
+  if (s > k_tiles) s = k_tiles;
+  return s;
+}
+
+// ldw: row stride of W (N unless W is read from a padded WeightMirror).
+template <class Epi>
+Step fwd(const float* A0, const float* A1, int64_t lda, const float* W0, const float* W1, int M,
+         int N, int K, int groups, Epi epi, int64_t ldw = 0) {
+  Step step;
+  if (ldw == 0) ldw = N;
+  with_bn(N, [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    gemm::Operands ops;
+    ops.a[0] = gemm::map_a(A0, M, K, lda, false, true);
+    ops.a[1] = groups > 1 ? gemm::map_a(A1, M, K, lda, false, true) : ops.a[0];
+    ops.b[0] = gemm::map_b(W0, N, K, ldw, true, BN, true);
+    ops.b[1] = groups > 1 ? gemm::map_b(W1, N, K, ldw, true, BN, true) : ops.b[0];
+    const gemm::Problem p = gemm::make_problem(M, N, K, 1);
+    step = [ops, p, groups, epi](cudaStream_t st) {
+      gemm::launch<BN, false, true>(ops, p, groups, epi, st);
+    };
+  });
+  return step;
+}
+
+// din[M x N_in] = G[M x N_out] * W^T, W = [N_in x N_out] row-major (ld = ldw).
+template <class Epi>
+Step dgrad(const float* G0, const float* G1, int64_t ldg, const float* W0, const float* W1,
+           int64_t ldw, int M, int N_in, int N_out, int groups, Epi epi) {
+  Step step;
+  with_bn(N_in, [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    gemm::Operands ops;
+    ops.a[0] = gemm::map_a(G0, M, N_out, ldg, false, true);
+    ops.a[1] = groups > 1 ? gemm::map_a(G1, M, N_out, ldg, false, true) : ops.a[0];
+    ops.b[0] = gemm::map_b(W0, N_in, N_out, ldw, false, BN, true);
+    ops.b[1] = groups > 1 ? gemm::map_b(W1, N_in, N_out, ldw, false, BN, true) : ops.b[0];
+    const gemm::Problem p = gemm::make_problem(M, N_in, N_out, 1);
+    step = [ops, p, groups, epi](cudaStream_t st) {
+      gemm::launch<BN, false, false>(ops, p, groups, epi, st);
+    };
+  });
+  return step;
+}
+
+// dW[M=in x N=out] = H^T G over K = batch rows; split-K partials via Epi.
+template <class Epi>
+Step wgrad(const float* H0, const float* H1, int64_t ldh, const float* G0, const float* G1,
+           int64_t ldg, int M, int N, int K, int groups, int splits, Epi epi) {
+  Step step;
+  with_bn(N, [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    gemm::Operands ops;
+    ops.a[0] = gemm::map_a(H0, M, K, ldh, true, true);
+    ops.a[1] = groups > 1 ? gemm::map_a(H1, M, K, ldh, true, true) : ops.a[0];
+    ops.b[0] = gemm::map_b(G0, N, K, ldg, true, BN, true);
+    ops.b[1] = groups > 1 ? gemm::map_b(G1, N, K, ldg, true, BN, true) : ops.b[0];
+    const gemm::Problem p = gemm::make_problem(M, N, K, splits);
+    step = [ops, p, groups, epi](cudaStream_t st) {
+      gemm::launch<BN, true, true>(ops, p, groups, epi, st);
+    };
+  });
+  return step;
+}
+
+// Bias-correction table bc[t] = (float(1/(1-0.9^t)), float(1/(1-0.999^t)))
+// computed on the host with the same libm pow the reference uses
+// (optim.hpp:35-39).  Beyond t = 32767 both are exactly 1.0f.
+inline std::vector<float2> adam_bias_table(double beta1, double beta2, int len = 32768) {
+  std::vector<float2> t(len);
+  t[0] = make_float2(1.0f, 1.0f);
+  for (int i = 1; i < len; ++i) {
+    const double b1t = std::pow(beta1, static_cast<double>(i));
+    const double b2t = std::pow(beta2, static_cast<double>(i));
+    t[i] = make_float2(static_cast<float>(1.0 / (1.0 - b1t)), static_cast<float>(1.0 / (1.0 - b2t)));
+  }
+  return t;
+}
+
+}  // namespace pqlg::mlp

@@ -3,6 +3,25 @@
 namespace pqlg {
 
 namespace {
+__global__ void pad_rows_kernel(const float* src, float* dst, int rows, int cols, int ld) {
+  const int64_t n = static_cast<int64_t>(rows) * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    dst[r * ld + c] = src[i];
+  }
+}
+}  // namespace
+
+void launch_pad_rows(const float* src, float* dst, int rows, int cols, int ld, cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(rows) * cols;
+  const int blocks = static_cast<int>(std::min<int64_t>(592, (n + 255) / 256));
+  pad_rows_kernel<<<blocks, 256, 0, st>>>(src, dst, rows, cols, ld);
+  PQLG_CHECK_LAUNCH();
+  count_launch();
+}
+
+namespace {
 // detail::orthogonalize (mlp.hpp:209-225), T = float.
 void orthogonalize(std::vector<float>& a, size_t rows, size_t cols) {
   for (size_t c = 0; c < cols; ++c) {

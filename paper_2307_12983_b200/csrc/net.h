@@ -34,6 +34,32 @@ struct NetShape {
   int out() const { return sizes.back(); }
 };
 
+// dst[r * ld + c] = src[r * cols + c] (c < cols); padding columns stay zero.
+void launch_pad_rows(const float* src, float* dst, int rows, int cols, int ld, cudaStream_t st);
+
+// TMA needs 16-byte row strides: a weight matrix W [in x out] whose `out` is
+// not a multiple of 4 (policy heads with act_dim 1/2/3, the 51-atom C51
+// head) is read by the GEMMs from a padded mirror refreshed after every
+// parameter change.
+struct WeightMirror {
+  const float* src = nullptr;
+  int in = 0, out = 0, ld = 0;
+  DevBuf<float> buf;
+  void init(const float* w, int rows, int cols) {
+    src = w;
+    in = rows;
+    out = cols;
+    ld = static_cast<int>(round_up(cols, 4));
+    if (ld != cols) buf.alloc(static_cast<size_t>(rows) * ld);
+  }
+  bool needed() const { return buf.p != nullptr; }
+  const float* ptr() const { return needed() ? buf.p : src; }
+  int64_t stride() const { return needed() ? ld : out; }
+  void refresh(cudaStream_t st) const {
+    if (needed()) launch_pad_rows(src, buf.p, in, out, ld, st);
+  }
+};
+
 // Orthogonal init (mlp.hpp:230-249): modified Gram-Schmidt on a
 // normal_distribution<double> draw, in T = float, with -ffp-contract=off
 // semantics (this TU is compiled without contraction for host code).

@@ -31,8 +31,9 @@ struct Segment {
 struct FinalizeArgs {
   Segment seg[kMaxSegments];
   int n_seg;
-  int64_t total;  // elements per group (== params)
-  float* grads;   // [groups x total]
+  int64_t total;    // elements per group (== params)
+  int64_t gstride;  // group stride of grads (16-byte aligned groups)
+  float* grads;     // [groups x gstride]
   double* block_sq;         // [groups x gridDim.x]
   unsigned int* counter;    // [groups], self-resetting
   float* scale;             // [groups] clip scale (1 if not clipped)
@@ -40,7 +41,7 @@ struct FinalizeArgs {
   float max_norm;
 };
 
-__global__ void __launch_bounds__(kFinalizeThreads) finalize_kernel(FinalizeArgs a) {
+static __global__ void __launch_bounds__(kFinalizeThreads) finalize_kernel(FinalizeArgs a) {
   const int group = blockIdx.y;
   double sq = 0.0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < a.total;
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(kFinalizeThreads) finalize_kernel(FinalizeArgs
     const float* src = sg.src + group * sg.group_stride + j;
     float acc = src[0];
     for (int t = 1; t < sg.n_terms; ++t) acc = __fadd_rn(acc, src[t * sg.stride]);
-    a.grads[group * a.total + i] = acc;
+    a.grads[group * a.gstride + i] = acc;
     const double d = static_cast<double>(acc);
     sq += d * d;
   }
@@ -96,6 +97,7 @@ struct AdamArgs {
   float* v;
   float* target;   // nullable: Polyak target [groups x n]
   int64_t n;
+  int64_t gstride;      // group stride of p/g/m/v/target
   const float* scale;   // [groups], clip scale
   const uint32_t* status;
   const int64_t* step;  // device Adam step t (already incremented for this update)
@@ -104,8 +106,10 @@ struct AdamArgs {
   float lr, beta1, beta2, eps, tau;
 };
 
-__global__ void adam_polyak_kernel(AdamArgs a) {
-  if (*a.status & 1u) return;  // adam_step throws before touching params
+static __global__ void adam_polyak_kernel(AdamArgs a) {
+  // A non-finite target / loss / gradient makes the reference throw before
+  // adam_step modifies anything (ddpg.hpp:37,72; optim.hpp:33-34).
+  if (*a.status) return;
   const int group = blockIdx.y;
   int64_t t = *a.step;
   if (t >= a.bc_len) t = a.bc_len - 1;
@@ -114,7 +118,7 @@ __global__ void adam_polyak_kernel(AdamArgs a) {
   const bool clipped = s != 1.0f;
   const float ob1 = __fsub_rn(1.0f, a.beta1), ob2 = __fsub_rn(1.0f, a.beta2);
   const float keep = __fsub_rn(1.0f, a.tau);
-  const int64_t off = group * a.n;
+  const int64_t off = group * a.gstride;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < a.n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     float gi = a.g[off + i];

@@ -66,12 +66,6 @@ void launch_state_sample(const DeviceStates& r, const replay::Norm& norm, float*
 }  // namespace pqlg
 
 // ------------------------------------------------------------------ C ABI
-struct pqlg_replay_s {
-  std::unique_ptr<pqlg::DeviceReplay> r;
-  pqlg::DeviceNorm norm;
-  pqlg::DevBuf<pqlg::replay::SamplerState> ss;
-  pqlg::DevBuf<uint64_t> idx;
-};
 struct pqlg_nstep_s {
   std::unique_ptr<pqlg::DeviceNStep> a;
   cudaStream_t stream;
@@ -128,8 +122,9 @@ int pqlg_replay_create(uint64_t capacity, int obs_dim, int act_dim, void* stream
   return guarded([&] {
     require(out != nullptr, "replay_create: out is null");
     auto h = std::make_unique<pqlg_replay_s>();
-    h->r = std::make_unique<DeviceReplay>(capacity, obs_dim, act_dim,
-                                          static_cast<cudaStream_t>(stream));
+    h->owned = std::make_unique<DeviceReplay>(capacity, obs_dim, act_dim,
+                                              static_cast<cudaStream_t>(stream));
+    h->r = h->owned.get();
     h->norm.init(obs_dim);
     *out = h.release();
   });
@@ -182,6 +177,21 @@ int pqlg_replay_sample(pqlg_replay h, uint64_t batch, pqlg_rng* rng, uint64_t mi
     finish_rng(rng, h->ss, r.stream);
   });
   return rc;
+}
+
+int pqlg_replay_fill_synthetic(pqlg_replay h, uint64_t n, uint64_t seed, float disc,
+                               uint32_t terminal_every) {
+  return guarded([&] {
+    if (n == 0) return;
+    auto& r = *h->r;
+    const uint64_t blocks = (n + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    replay::ring_fill_kernel<<<static_cast<unsigned>(blocks), 32 * kWarpsPerBlock, 0,
+                               r.stream>>>(r.view(), n, seed, disc, terminal_every);
+    PQLG_CHECK_LAUNCH();
+    replay::ring_advance_kernel<<<1, 32, 0, r.stream>>>(r.state.p, r.capacity, nullptr, 0, n);
+    PQLG_CHECK_LAUNCH();
+    count_launch(2);
+  });
 }
 
 int pqlg_replay_read_rows(pqlg_replay h, uint64_t i0, uint64_t n, float* obs, float* act,

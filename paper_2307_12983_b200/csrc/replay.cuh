@@ -103,7 +103,7 @@ __device__ __forceinline__ int emit_count(uint32_t count, int n, bool done) {
 }
 
 // K1: per-env emit counts, block-exclusive offsets and block totals.
-__global__ void nstep_count_kernel(Window w, Slice s, uint32_t* offs, uint32_t* block_sums) {
+static __global__ void nstep_count_kernel(Window w, Slice s, uint32_t* offs, uint32_t* block_sums) {
   __shared__ uint32_t warp_tot[kScanBlock / 32];
   const int e = blockIdx.x * kScanBlock + threadIdx.x;
   uint32_t c = 0;
@@ -138,7 +138,7 @@ __global__ void nstep_count_kernel(Window w, Slice s, uint32_t* offs, uint32_t* 
 
 // K2: one warp per env.  Writes the new window slot, then emits this step's
 // records in reference order straight into the ring.
-__global__ void nstep_emit_kernel(Window w, Slice s, float reward_scale, Ring ring,
+static __global__ void nstep_emit_kernel(Window w, Slice s, float reward_scale, Ring ring,
                                   const uint32_t* offs, const uint32_t* block_sums,
                                   int n_blocks) {
   const int lane = threadIdx.x & 31;
@@ -228,7 +228,7 @@ __global__ void nstep_emit_kernel(Window w, Slice s, float reward_scale, Ring ri
 }
 
 // K3: cursor = (cursor + total) % cap; count = min(count + total, cap).
-__global__ void ring_advance_kernel(uint64_t* state, uint64_t capacity, const uint32_t* sums,
+static __global__ void ring_advance_kernel(uint64_t* state, uint64_t capacity, const uint32_t* sums,
                                     int n_sums, uint64_t extra) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   uint64_t total = extra;
@@ -240,7 +240,7 @@ __global__ void ring_advance_kernel(uint64_t* state, uint64_t capacity, const ui
 
 // Direct insert of an assembled batch (ReplayBuffer::insert).  One warp per
 // row; rows that a later row of the same batch overwrites are skipped.
-__global__ void ring_insert_kernel(Ring ring, const float* obs, const float* act,
+static __global__ void ring_insert_kernel(Ring ring, const float* obs, const float* act,
                                    const float* boot, const float* ret, const float* eff,
                                    int64_t ld_obs, int64_t ld_act, uint64_t n) {
   const int lane = threadIdx.x & 31;
@@ -258,12 +258,44 @@ __global__ void ring_insert_kernel(Ring ring, const float* obs, const float* act
   }
 }
 
-__global__ void state_insert_kernel(StateRing ring, const float* rows, int64_t ld, uint64_t n) {
+static __global__ void state_insert_kernel(StateRing ring, const float* rows, int64_t ld, uint64_t n) {
   const int lane = threadIdx.x & 31;
   const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
   if (r >= n || r + ring.capacity < n) return;
   const uint64_t p = (ring.state[0] + r) % ring.capacity;
   for (int d = lane; d < ring.D; d += 32) ring.obs[p * ring.ld + d] = rows[r * ld + d];
+}
+
+// Synthetic pre-fill: obs/boot ~ N(0,1), act ~ U(-1,1),
+// ret ~ 0.1 N(0,1), eff = disc except 1/terminal_every rows (terminal, 0).
+// Philox keyed by `seed`; one warp per row.  Used by the benchmarks to fill
+// a 5M-record ring without a host round trip.
+__device__ __forceinline__ float philox_normal(uint64_t key, uint64_t ctr) {
+  const uint64_t x = rng::philox_draw(key, ctr);
+  const float u1 = (static_cast<float>(x >> 40) + 0.5f) * 0x1p-24f;
+  const float u2 = static_cast<float>((x >> 16) & 0xFFFFFFu) * 0x1p-24f;
+  return sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+}
+
+static __global__ void ring_fill_kernel(Ring ring, uint64_t n, uint64_t seed, float disc,
+                                        uint32_t terminal_every) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (r >= n) return;
+  const uint64_t p = (ring.state[0] + r) % ring.capacity;
+  const uint64_t base = r * 1024;
+  for (int d = lane; d < ring.D; d += 32) {
+    ring.obs[p * ring.ld_obs + d] = philox_normal(seed, base + d);
+    ring.boot[p * ring.ld_obs + d] = philox_normal(seed, base + 512 + d);
+  }
+  for (int d = lane; d < ring.A; d += 32) {
+    const uint64_t x = rng::philox_draw(seed ^ 0x5bd1e995ull, base + d);
+    ring.act[p * ring.ld_act + d] = static_cast<float>(x >> 40) * 0x1p-23f - 1.0f;
+  }
+  if (lane == 0) {
+    ring.ret[p] = 0.1f * philox_normal(seed ^ 0x27d4eb2full, r);
+    ring.eff[p] = (terminal_every && (r % terminal_every) == 0) ? 0.0f : disc;
+  }
 }
 
 // ---------------------------------------------------------------- sampling
@@ -309,7 +341,7 @@ __device__ __forceinline__ void gather_row(const Ring& ring, const Norm& norm, c
 }
 
 // ReplayBuffer::sample fused with apply_stats on obs and boot_obs.
-__global__ void replay_sample_kernel(Ring ring, Norm norm, Gather g, SamplerState* ss,
+static __global__ void replay_sample_kernel(Ring ring, Norm norm, Gather g, SamplerState* ss,
                                      const uint64_t* host_idx, uint64_t B) {
   const int lane = threadIdx.x & 31;
   const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -326,7 +358,7 @@ __global__ void replay_sample_kernel(Ring ring, Norm norm, Gather g, SamplerStat
 // Sequential fix-up when any draw hit Lemire's rejection zone (probability
 // ~count/2^64 per draw): redo the whole batch with libstdc++'s redraw loop,
 // then advance the counter by the draws consumed.  Always launched (1 warp).
-__global__ void replay_sample_finalize_kernel(Ring ring, Norm norm, Gather g, SamplerState* ss,
+static __global__ void replay_sample_finalize_kernel(Ring ring, Norm norm, Gather g, SamplerState* ss,
                                               const uint64_t* host_idx, uint64_t B) {
   const int lane = threadIdx.x & 31;
   if (host_idx) return;
@@ -352,7 +384,7 @@ __global__ void replay_sample_finalize_kernel(Ring ring, Norm norm, Gather g, Sa
 }
 
 // StateBuffer::sample fused with apply_stats.
-__global__ void state_sample_kernel(StateRing ring, Norm norm, float* out, int64_t ld_out,
+static __global__ void state_sample_kernel(StateRing ring, Norm norm, float* out, int64_t ld_out,
                                     SamplerState* ss, const uint64_t* host_idx, uint64_t B) {
   const int lane = threadIdx.x & 31;
   const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -372,7 +404,7 @@ __global__ void state_sample_kernel(StateRing ring, Norm norm, float* out, int64
   }
 }
 
-__global__ void state_sample_finalize_kernel(StateRing ring, Norm norm, float* out,
+static __global__ void state_sample_finalize_kernel(StateRing ring, Norm norm, float* out,
                                              int64_t ld_out, SamplerState* ss,
                                              const uint64_t* host_idx, uint64_t B) {
   const int lane = threadIdx.x & 31;

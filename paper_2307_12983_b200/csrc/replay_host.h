@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cmath>
+#include <memory>
 #include <vector>
 
 #include "common.h"
@@ -142,3 +143,12 @@ void launch_state_sample(const DeviceStates& r, const replay::Norm& norm, float*
                          uint64_t B, cudaStream_t st);
 
 }  // namespace pqlg
+
+// ABI handle: owns its buffer, or views one owned by a learner core.
+struct pqlg_replay_s {
+  pqlg::DeviceReplay* r = nullptr;
+  std::unique_ptr<pqlg::DeviceReplay> owned;
+  pqlg::DeviceNorm norm;
+  pqlg::DevBuf<pqlg::replay::SamplerState> ss;
+  pqlg::DevBuf<uint64_t> idx;
+};

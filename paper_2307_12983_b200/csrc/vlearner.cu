@@ -1,0 +1,654 @@
+// V-learner: CriticLearnerCore (proj/include/pql/runtime/learners.hpp:77-106,
+// proj/src/runtime/learners.cpp:122-196) on one B200.
+//
+// One update = sample -> target policy -> twin target critics -> TD target ->
+// twin online critics -> loss -> backward (head, then wgrad/dgrad per layer)
+// -> fixed-order gradient reduction + fp64 norm -> fused clip/Adam/Polyak.
+// Every step is a pre-built launch; update_n() replays them from a CUDA graph.
+#include <memory>
+#include <random>
+#include <vector>
+
+#include "critic_kernels.cuh"
+#include "learner.h"
+#include "optim.cuh"
+
+namespace pqlg {
+
+using mlp::Step;
+
+VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t init_seed,
+                   cudaStream_t st)
+    : cfg_(cfg), dims_(dims), stream_(st) {
+  if (!stream_) {  // the legacy default stream cannot be graph-captured
+    PQLG_CUDA(cudaStreamCreateWithFlags(&owned_stream_, cudaStreamNonBlocking));
+    stream_ = owned_stream_;
+  }
+  st = stream_;
+  require(cfg.algo == PQLG_ALGO_DDPG || cfg.algo == PQLG_ALGO_C51, "vlearner: unknown algo");
+  require(cfg.algo == PQLG_ALGO_DDPG, "vlearner: the C51 critic is not built in this version");
+  require(cfg.hidden_layers >= 1 && cfg.hidden >= 32 && cfg.hidden % 32 == 0,
+          "vlearner: hidden width must be a multiple of 32");
+  require(cfg.batch_size >= 1, "vlearner: batch_size must be >= 1");
+  D_ = dims.obs_dim;
+  A_ = dims.act_dim;
+  H_ = cfg.hidden;
+  nh_ = cfg.hidden_layers;
+  B_ = cfg.batch_size;
+  Kp_ = static_cast<int>(round_up(D_ + A_, 4));
+  reward_scale_ = static_cast<float>(cfg.reward_scale);
+  gamma_ = static_cast<float>(cfg.gamma);
+
+  std::vector<int> qs{D_ + A_}, ps{D_};
+  for (int i = 0; i < nh_; ++i) {
+    qs.push_back(H_);
+    ps.push_back(H_);
+  }
+  qs.push_back(1);
+  ps.push_back(A_);
+  qnet_ = NetShape::make(qs);
+  pnet_ = NetShape::make(ps);
+  const int64_t P = qnet_.params;
+  Ps_ = round_up(P, 64);  // group stride: 16-byte aligned second critic for TMA
+  const int64_t Ps = Ps_;
+
+  // --- parameters: CriticPair::create (critic.hpp:16-26) and the lagged policy
+  std::mt19937_64 init_rng(init_seed);
+  std::vector<float> q1, q2, pol;
+  init_orthogonal(qnet_, q1, init_rng, static_cast<float>(std::sqrt(2.0)), 1.0f);
+  init_orthogonal(qnet_, q2, init_rng, static_cast<float>(std::sqrt(2.0)), 1.0f);
+  std::mt19937_64 prng(rng::derive_seed(cfg.seed, rng::kInit, 0));
+  init_orthogonal(pnet_, pol, prng, static_cast<float>(std::sqrt(2.0)), 1e-2f);
+  q_.alloc(2 * Ps);
+  qt_.alloc(2 * Ps);
+  m_.alloc(2 * Ps);
+  v_.alloc(2 * Ps);
+  grads_.alloc(2 * Ps);
+  lagged_.alloc(pnet_.params);
+  PQLG_CUDA(cudaMemcpy(q_.p, q1.data(), P * 4, cudaMemcpyHostToDevice));
+  PQLG_CUDA(cudaMemcpy(q_.p + Ps, q2.data(), P * 4, cudaMemcpyHostToDevice));
+  PQLG_CUDA(cudaMemcpy(qt_.p, q_.p, 2 * Ps * 4, cudaMemcpyDeviceToDevice));
+  PQLG_CUDA(cudaMemcpy(lagged_.p, pol.data(), pnet_.params * 4, cudaMemcpyHostToDevice));
+
+  // --- replay + n-step (learners.cpp:131-136)
+  replay_ = std::make_unique<DeviceReplay>(cfg.buffer_capacity, D_, A_, st);
+  nstep_ = std::make_unique<DeviceNStep>(cfg.n_envs, D_, A_, gamma_, cfg.n_step);
+  norm_.init(D_);
+  sampler_.alloc(1);
+  replay::SamplerState s0{rng::derive_seed(cfg.seed, rng::kSample, 1), 0, 0, 0};
+  PQLG_CUDA(cudaMemcpy(sampler_.p, &s0, sizeof(s0), cudaMemcpyHostToDevice));
+  mt_.seed(rng::derive_seed(cfg.seed, rng::kSample, 1));
+  idx_.alloc(B_);
+  idx_host_.resize(B_);
+
+  // --- optimizer state
+  step_.alloc(1);
+  auto tab = mlp::adam_bias_table(0.9, 0.999);
+  bc_.alloc(tab.size());
+  PQLG_CUDA(cudaMemcpy(bc_.p, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  status_.alloc(1);
+  loss_.alloc(1);
+
+  build_update();
+  PQLG_CUDA(cudaDeviceSynchronize());
+}
+
+VLearner::~VLearner() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (owned_stream_) {
+    cudaStreamSynchronize(owned_stream_);
+    cudaStreamDestroy(owned_stream_);
+  }
+}
+
+void VLearner::build_update() {
+  const int B = B_, D = D_, A = A_, H = H_, nh = nh_, K0 = D + A;
+  const int64_t P = qnet_.params;
+  const int nt = mlp::n_tiles(H);
+  const int mt = (B + 127) / 128;
+  float* q1 = q_.p;
+  float* q2 = q_.p + Ps_;
+  float* q1t = qt_.p;
+  float* q2t = qt_.p + Ps_;
+
+  Xon_.alloc(static_cast<size_t>(B) * Kp_);
+  Xtg_.alloc(static_cast<size_t>(B) * Kp_);
+  ret_.alloc(B);
+  eff_.alloc(B);
+  y_.alloc(B);
+  pact_.resize(nh);
+  for (auto& b : pact_) b.alloc(static_cast<size_t>(B) * H);
+  for (int k = 0; k < 2; ++k) {
+    tact_[k].resize(nh);
+    oact_[k].resize(nh);
+    G_[k].resize(nh);
+    for (int l = 0; l < nh; ++l) {
+      tact_[k][l].alloc(l + 1 < nh ? static_cast<size_t>(B) * H : 0);
+      oact_[k][l].alloc(static_cast<size_t>(B) * H);
+      G_[k][l].alloc(static_cast<size_t>(B) * H);
+    }
+  }
+  part_t_.alloc(2ull * nt * B);
+  part_o_.alloc(2ull * nt * B);
+  up_.alloc(2ull * B);
+  const int loss_blocks = (B + critic::kRowThreads - 1) / critic::kRowThreads;
+  block_loss_.alloc(loss_blocks);
+  loss_counter_.alloc(1);
+
+  // ---------------------------------------------------------------- sample
+  steps_.push_back([this, B](cudaStream_t st) {
+    const uint64_t* idx = mt_mode_ ? idx_.p : nullptr;
+    replay::Gather g{Xon_.p, Kp_, Xon_.p + D_, Kp_, Xtg_.p, Kp_, ret_.p, eff_.p};
+    launch_replay_sample(*replay_, norm_.view(), g, sampler_.p, idx, B, st);
+  });
+
+  // ------------------------------------------- target policy (lagged, 1 group)
+  {
+    const float* in = Xtg_.p;
+    int64_t ld = Kp_;
+    int K = D;
+    for (int l = 0; l < nh; ++l) {
+      epi::Hidden e{};
+      e.bias[0] = e.bias[1] = lagged_.p + pnet_.b_off[l];
+      e.out[0] = e.out[1] = pact_[l].p;
+      e.ld_out = H;
+      e.M = B;
+      e.N = H;
+      e.store = 1;
+      const float* W = lagged_.p + pnet_.w_off[l];
+      steps_.push_back(mlp::fwd(in, in, ld, W, W, B, H, K, 1, e));
+      in = pact_[l].p;
+      ld = H;
+      K = H;
+    }
+    epi::PolicyHead ph{};
+    ph.bias = lagged_.p + pnet_.b_off[nh];
+    ph.act = Xtg_.p + D;  // critic target input [norm(boot) | pi(boot)]
+    ph.ld_act = Kp_;
+    ph.M = B;
+    ph.A = A;
+    ph.mid = (dims_.low + dims_.high) / 2.0f;
+    ph.half = (dims_.high - dims_.low) / 2.0f;
+    lagged_head_.init(lagged_.p + pnet_.w_off[nh], H, A);
+    lagged_head_.refresh(stream_);
+    const float* W = lagged_head_.ptr();
+    steps_.push_back(mlp::fwd(in, in, ld, W, W, B, A, H, 1, ph, lagged_head_.stride()));
+  }
+
+  // --------------------------------------------- twin critics, shared helper
+  auto critic_fwd = [&](bool target) {
+    float* nets[2] = {target ? q1t : q1, target ? q2t : q2};
+    const float* X = target ? Xtg_.p : Xon_.p;
+    float* part = target ? part_t_.p : part_o_.p;
+    for (int l = 0; l < nh; ++l) {
+      epi::Hidden e{};
+      for (int k = 0; k < 2; ++k) {
+        e.bias[k] = nets[k] + qnet_.b_off[l];
+        e.out[k] = target ? tact_[k][l].p : oact_[k][l].p;
+      }
+      e.ld_out = H;
+      e.M = B;
+      e.N = H;
+      const bool last = l + 1 == nh;
+      e.store = (!target || !last) ? 1 : 0;
+      if (last) {
+        for (int k = 0; k < 2; ++k) e.w_head[k] = nets[k] + qnet_.w_off[nh];
+        e.partial = part;
+        e.ld_part = B;
+        e.n_tiles = nt;
+      }
+      const float* a0 = l == 0 ? X : (target ? tact_[0][l - 1].p : oact_[0][l - 1].p);
+      const float* a1 = l == 0 ? X : (target ? tact_[1][l - 1].p : oact_[1][l - 1].p);
+      const int64_t lda = l == 0 ? Kp_ : H;
+      const int K = l == 0 ? K0 : H;
+      steps_.push_back(mlp::fwd(a0, a1, lda, nets[0] + qnet_.w_off[l], nets[1] + qnet_.w_off[l],
+                                B, H, K, 2, e));
+    }
+  };
+
+  critic_fwd(true);
+  // ------------------------------------------------------------- TD target
+  {
+    critic::TdArgs a{part_t_.p, B, nt, q1t, q2t, qnet_.b_off[nh], ret_.p, eff_.p, y_.p, B,
+                     status_.p, step_.p};
+    steps_.push_back([a, B](cudaStream_t st) {
+      critic::td_target_kernel<<<(B + 255) / 256, 256, 0, st>>>(a);
+      PQLG_CHECK_LAUNCH();
+      count_launch();
+    });
+  }
+  critic_fwd(false);
+  // ------------------------------------------------------------------ loss
+  {
+    critic::LossArgs a{part_o_.p, B, nt, q1, q2, qnet_.b_off[nh], y_.p, up_.p,
+                       block_loss_.p, loss_counter_.p, loss_.p, status_.p, B};
+    steps_.push_back([a, loss_blocks](cudaStream_t st) {
+      critic::critic_loss_kernel<<<loss_blocks, critic::kRowThreads, 0, st>>>(a);
+      PQLG_CHECK_LAUNCH();
+      count_launch();
+    });
+  }
+
+  // -------------------------------------------------------------- backward
+  wpart_.resize(nh);
+  colsum_.resize(nh);
+  wsplits_.resize(nh);
+  for (int l = 0; l < nh; ++l) {
+    const int in = l == 0 ? K0 : H;
+    wsplits_[l] = mlp::wgrad_splits(in, H, B, 2);
+    wpart_[l].alloc(2ull * wsplits_[l] * in * H);
+    colsum_[l].alloc(2ull * mt * H);
+  }
+  head_dw_.alloc(2ull * mt * H);
+  head_db_.alloc(2ull * mt);
+  {
+    critic::HeadBwdArgs a{};
+    a.up = up_.p;
+    for (int k = 0; k < 2; ++k) {
+      a.h[k] = oact_[k][nh - 1].p;
+      a.w[k] = (k ? q2 : q1) + qnet_.w_off[nh];
+      a.G[k] = G_[k][nh - 1].p;
+    }
+    a.ld_h = H;
+    a.ld_g = H;
+    a.dw_part = head_dw_.p;
+    a.db_head_part = head_db_.p;
+    a.db_part = colsum_[nh - 1].p;
+    a.B = B;
+    a.H = H;
+    a.tiles = mt;
+    a.with_params = 1;
+    const int threads = H < 1024 ? H : 1024;
+    steps_.push_back([a, mt, threads](cudaStream_t st) {
+      critic::head_backward_kernel<<<dim3(mt, 2), threads, 0, st>>>(a);
+      PQLG_CHECK_LAUNCH();
+      count_launch();
+    });
+  }
+  for (int l = nh - 1; l >= 0; --l) {
+    const int in = l == 0 ? K0 : H;
+    // wgrad: dW_l = act_{l-1}^T G_l  (act_{-1} = the critic input)
+    epi::Partial pe{wpart_[l].p, wsplits_[l], in, H};
+    const float* h0 = l == 0 ? Xon_.p : oact_[0][l - 1].p;
+    const float* h1 = l == 0 ? Xon_.p : oact_[1][l - 1].p;
+    const int64_t ldh = l == 0 ? Kp_ : H;
+    steps_.push_back(mlp::wgrad(h0, h1, ldh, G_[0][l].p, G_[1][l].p, H, in, H, B, 2,
+                                wsplits_[l], pe));
+    if (l > 0) {
+      // dgrad: G_{l-1} = (G_l W_l^T) * [act_{l-1} > 0], + bias colsums of layer l-1
+      epi::DgradMask dm{};
+      for (int k = 0; k < 2; ++k) {
+        dm.post[k] = oact_[k][l - 1].p;
+        dm.out[k] = G_[k][l - 1].p;
+      }
+      dm.ld_post = H;
+      dm.ld_out = H;
+      dm.colsum = colsum_[l - 1].p;
+      dm.ld_cs = H;
+      dm.m_tiles = mt;
+      dm.M = B;
+      dm.N = H;
+      steps_.push_back(mlp::dgrad(G_[0][l].p, G_[1][l].p, H, q1 + qnet_.w_off[l],
+                                  q2 + qnet_.w_off[l], H, B, H, H, 2, dm));
+    }
+  }
+
+  // --------------------------------------- gradient reduction + clip scale
+  {
+    optim::FinalizeArgs f{};
+    int s = 0;
+    for (int l = 0; l < nh; ++l) {
+      const int in = l == 0 ? K0 : H;
+      f.seg[s++] = optim::Segment{qnet_.w_off[l], static_cast<int64_t>(in) * H, wpart_[l].p,
+                                  static_cast<int64_t>(wsplits_[l]) * in * H, wsplits_[l],
+                                  static_cast<int64_t>(in) * H};
+      f.seg[s++] = optim::Segment{qnet_.b_off[l], H, colsum_[l].p,
+                                  static_cast<int64_t>(mt) * H, mt, H};
+    }
+    f.seg[s++] = optim::Segment{qnet_.w_off[nh], H, head_dw_.p, static_cast<int64_t>(mt) * H,
+                                mt, H};
+    f.seg[s++] = optim::Segment{qnet_.b_off[nh], 1, head_db_.p, mt, mt, 1};
+    require(s <= optim::kMaxSegments, "vlearner: too many layers");
+    f.n_seg = s;
+    f.total = P;
+    f.gstride = Ps_;
+    f.grads = grads_.p;
+    fin_blocks_ = static_cast<int>(std::min<int64_t>(4 * mlp::kSMs, (P + 1023) / 1024));
+    block_sq_.alloc(2ull * fin_blocks_);
+    fin_counter_.alloc(2);
+    scale_.alloc(2);
+    f.block_sq = block_sq_.p;
+    f.counter = fin_counter_.p;
+    f.scale = scale_.p;
+    f.status = status_.p;
+    f.max_norm = 0.5f;
+    const int fb = fin_blocks_;
+    steps_.push_back([f, fb](cudaStream_t st) {
+      optim::finalize_kernel<<<dim3(fb, 2), optim::kFinalizeThreads, 0, st>>>(f);
+      PQLG_CHECK_LAUNCH();
+      count_launch();
+    });
+  }
+  // ------------------------------------------------ clip + Adam + Polyak
+  {
+    optim::AdamArgs a{};
+    a.p = q_.p;
+    a.g = grads_.p;
+    a.m = m_.p;
+    a.v = v_.p;
+    a.target = qt_.p;
+    a.n = P;
+    a.gstride = Ps_;
+    a.scale = scale_.p;
+    a.status = status_.p;
+    a.step = step_.p;
+    a.bc = bc_.p;
+    a.bc_len = static_cast<int64_t>(bc_.n);
+    a.lr = static_cast<float>(cfg_.lr_critic);
+    a.beta1 = 0.9f;
+    a.beta2 = 0.999f;
+    a.eps = 1e-8f;
+    a.tau = static_cast<float>(cfg_.tau);
+    const int blocks = static_cast<int>(std::min<int64_t>(4 * mlp::kSMs, (P + 255) / 256));
+    steps_.push_back([a, blocks](cudaStream_t st) {
+      optim::adam_polyak_kernel<<<dim3(blocks, 2), 256, 0, st>>>(a);
+      PQLG_CHECK_LAUNCH();
+      count_launch();
+    });
+  }
+}
+
+void VLearner::adopt_policy(const float* flat, int64_t version) {
+  if (version < lagged_version_) return;  // learners.cpp:37-42
+  PQLG_CUDA(cudaMemcpyAsync(lagged_.p, flat, pnet_.params * 4, cudaMemcpyHostToDevice, stream_));
+  lagged_head_.refresh(stream_);
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+  lagged_version_ = version;
+}
+
+void VLearner::adopt_norm(int64_t count, const double* mean, const double* m2) {
+  norm_.set(count, mean, m2, stream_);
+}
+
+void VLearner::ingest(const replay::Slice& s) { nstep_->push(s, reward_scale_, *replay_, stream_); }
+
+bool VLearner::ready(int64_t c_a) {
+  return c_a >= cfg_.warm_up && replay_->size() >= static_cast<uint64_t>(B_);
+}
+
+void VLearner::prepare_indices() {
+  // The reference's own generator: uniform_int_distribution over
+  // std::mt19937_64 make_rng(seed, sample, 1) (replay_buffer.hpp:58-59).
+  const uint64_t count = replay_->size();
+  std::uniform_int_distribution<std::size_t> pick(0, count - 1);
+  for (int r = 0; r < B_; ++r) idx_host_[r] = pick(mt_);
+  PQLG_CUDA(cudaMemcpyAsync(idx_.p, idx_host_.data(), B_ * sizeof(uint64_t),
+                            cudaMemcpyHostToDevice, stream_));
+}
+
+void VLearner::enqueue() {
+  for (auto& s : steps_) s(stream_);
+}
+
+int VLearner::check_status() {
+  uint32_t st = 0;
+  PQLG_CUDA(cudaMemcpyAsync(&st, status_.p, 4, cudaMemcpyDeviceToHost, stream_));
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+  if (st) {
+    PQLG_CUDA(cudaMemsetAsync(status_.p, 0, 4, stream_));
+    return PQLG_ENONFINITE;
+  }
+  return PQLG_OK;
+}
+
+float VLearner::update() {
+  if (replay_->size() < static_cast<uint64_t>(B_))
+    throw Error(PQLG_NOT_READY, "critic update before buffer warm-up");
+  if (mt_mode_) prepare_indices();
+  enqueue();
+  float loss = 0.0f;
+  PQLG_CUDA(cudaMemcpyAsync(&loss, loss_.p, 4, cudaMemcpyDeviceToHost, stream_));
+  if (check_status() != PQLG_OK) throw Error(PQLG_ENONFINITE, "ddpg critic update: non-finite");
+  return loss;
+}
+
+void VLearner::update_n(int n) {
+  require(!mt_mode_, "update_n: graph replay needs the Philox sampler");
+  if (!graph_checked_) {
+    if (replay_->size() < static_cast<uint64_t>(B_))
+      throw Error(PQLG_NOT_READY, "critic update before buffer warm-up");
+    graph_checked_ = true;
+  }
+  if (!graph_exec_) {
+    cudaGraph_t g;
+    const uint64_t before = g_launches.load();
+    PQLG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    enqueue();
+    PQLG_CUDA(cudaStreamEndCapture(stream_, &g));
+    kpu_ = static_cast<int>(g_launches.load() - before);
+    g_launches.fetch_sub(kpu_);  // captured, not launched
+    PQLG_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
+    cudaGraphDestroy(g);
+  }
+  for (int i = 0; i < n; ++i) PQLG_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+  count_launch(static_cast<uint64_t>(n) * kpu_);
+}
+
+int VLearner::kernels_per_update() {
+  if (kpu_ == 0) {
+    const uint64_t before = g_launches.load();
+    cudaGraph_t g;
+    PQLG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    enqueue();
+    PQLG_CUDA(cudaStreamEndCapture(stream_, &g));
+    cudaGraphDestroy(g);
+    kpu_ = static_cast<int>(g_launches.load() - before);
+    g_launches.fetch_sub(kpu_);
+  }
+  return kpu_;
+}
+
+float VLearner::last_loss() {
+  float loss = 0.0f;
+  PQLG_CUDA(cudaMemcpyAsync(&loss, loss_.p, 4, cudaMemcpyDeviceToHost, stream_));
+  if (check_status() != PQLG_OK) throw Error(PQLG_ENONFINITE, "ddpg critic update: non-finite");
+  return loss;
+}
+
+void VLearner::get_params(int which, float* out) {
+  const int64_t P = qnet_.params;
+  const float* src = nullptr;
+  int64_t n = P;
+  switch (which) {
+    case 0: src = q_.p; break;
+    case 1: src = q_.p + Ps_; break;
+    case 2: src = qt_.p; break;
+    case 3: src = qt_.p + Ps_; break;
+    case 4: src = lagged_.p; n = pnet_.params; break;
+    default: throw Error(PQLG_EINVAL, "get_params: which must be 0..4");
+  }
+  PQLG_CUDA(cudaMemcpyAsync(out, src, n * 4, cudaMemcpyDeviceToHost, stream_));
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+}
+
+int64_t VLearner::param_count(int which) const {
+  return which == 4 ? pnet_.params : qnet_.params;
+}
+
+void VLearner::set_params(int which, const float* flat) {
+  const int64_t P = qnet_.params;
+  float* dst = nullptr;
+  int64_t n = P;
+  switch (which) {
+    case 0: dst = q_.p; break;
+    case 1: dst = q_.p + Ps_; break;
+    case 2: dst = qt_.p; break;
+    case 3: dst = qt_.p + Ps_; break;
+    case 4: dst = lagged_.p; n = pnet_.params; break;
+    default: throw Error(PQLG_EINVAL, "set_params: which must be 0..4");
+  }
+  PQLG_CUDA(cudaMemcpyAsync(dst, flat, n * 4, cudaMemcpyHostToDevice, stream_));
+  if (which == 4) lagged_head_.refresh(stream_);
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void VLearner::debug_read(int what, float* out) {
+  const int64_t P = qnet_.params;
+  switch (what) {
+    case 0:
+      PQLG_CUDA(cudaMemcpyAsync(out, y_.p, B_ * 4, cudaMemcpyDeviceToHost, stream_));
+      break;
+    case 1:
+      PQLG_CUDA(cudaMemcpyAsync(out, up_.p, 2ull * B_ * 4, cudaMemcpyDeviceToHost, stream_));
+      break;
+    case 2:
+      PQLG_CUDA(cudaMemcpy2DAsync(out, P * 4, grads_.p, Ps_ * 4, P * 4, 2,
+                                  cudaMemcpyDeviceToHost, stream_));
+      break;
+    case 3:
+      PQLG_CUDA(cudaMemcpyAsync(out, scale_.p, 2 * 4, cudaMemcpyDeviceToHost, stream_));
+      break;
+    case 4:
+      PQLG_CUDA(cudaMemcpy2DAsync(out, (D_ + A_) * 4, Xon_.p, Kp_ * 4, (D_ + A_) * 4, B_,
+                                  cudaMemcpyDeviceToHost, stream_));
+      break;
+    default: throw Error(PQLG_EINVAL, "debug_read: what must be 0..4");
+  }
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+}
+
+}  // namespace pqlg
+
+// ------------------------------------------------------------------ C ABI
+struct pqlg_vlearner_s {
+  std::unique_ptr<pqlg::VLearner> v;
+  pqlg_replay_s replay_view;
+};
+
+using namespace pqlg;
+
+extern "C" {
+
+void pqlg_config_default(pqlg_config* c) {
+  // RunConfig defaults (config.hpp:15-48) with Table B.1 values.
+  *c = pqlg_config{};
+  c->algo = PQLG_ALGO_DDPG;
+  c->n_envs = 4096;
+  c->batch_size = 8192;
+  c->buffer_capacity = 5000000;
+  c->gamma = 0.99;
+  c->tau = 0.05;
+  c->n_step = 3;
+  c->lr_actor = 5e-4;
+  c->lr_critic = 5e-4;
+  c->warm_up = 32;
+  c->sigma_min = 0.05;
+  c->sigma_max = 0.8;
+  c->sigma_fixed = -1.0;
+  c->reward_scale = 1.0;
+  c->seed = 0;
+  c->hidden = 256;
+  c->hidden_layers = 2;
+  c->n_atoms = 51;
+  c->vmin = -10.0;
+  c->vmax = 10.0;
+  c->max_episode_len = 1000;
+  c->env_offset = 0;
+}
+
+int pqlg_vlearner_create(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                         uint64_t init_rng_seed, void* stream, pqlg_vlearner* out) {
+  return guarded([&] {
+    require(cfg && dims && out, "vlearner_create: null argument");
+    auto h = std::make_unique<pqlg_vlearner_s>();
+    h->v = std::make_unique<VLearner>(*cfg, *dims, init_rng_seed,
+                                      static_cast<cudaStream_t>(stream));
+    h->replay_view.r = h->v->replay();
+    h->replay_view.norm.init(dims->obs_dim);
+    *out = h.release();
+  });
+}
+
+int pqlg_vlearner_destroy(pqlg_vlearner h) {
+  return guarded([&] { delete h; });
+}
+
+int pqlg_vlearner_adopt_policy(pqlg_vlearner h, const float* flat, int64_t version) {
+  return guarded([&] { h->v->adopt_policy(flat, version); });
+}
+
+int pqlg_vlearner_adopt_norm(pqlg_vlearner h, const pqlg_norm_stats* n) {
+  return guarded([&] { h->v->adopt_norm(n->count, n->mean, n->m2); });
+}
+
+int pqlg_vlearner_ingest(pqlg_vlearner h, const pqlg_step_slice* s) {
+  return guarded([&] {
+    const int D = h->v->obs_dim(), A = h->v->act_dim();
+    replay::Slice sl{s->obs, s->act, s->boot_obs, s->rew, s->term, s->trunc,
+                     s->ld_obs > 0 ? s->ld_obs : D, s->ld_act > 0 ? s->ld_act : A};
+    h->v->ingest(sl);
+  });
+}
+
+int pqlg_vlearner_ready(pqlg_vlearner h, int64_t c_a, int* ready) {
+  return guarded([&] { *ready = h->v->ready(c_a) ? 1 : 0; });
+}
+
+int pqlg_vlearner_update(pqlg_vlearner h, float* loss) {
+  return guarded([&] {
+    const float l = h->v->update();
+    if (loss) *loss = l;
+  });
+}
+
+int pqlg_vlearner_update_n(pqlg_vlearner h, int n) {
+  return guarded([&] { h->v->update_n(n); });
+}
+
+int pqlg_vlearner_last_loss(pqlg_vlearner h, float* loss) {
+  return guarded([&] { *loss = h->v->last_loss(); });
+}
+
+int pqlg_vlearner_get_params(pqlg_vlearner h, int which, float* out) {
+  return guarded([&] { h->v->get_params(which, out); });
+}
+
+int pqlg_vlearner_param_count(pqlg_vlearner h, int which, int64_t* out) {
+  return guarded([&] { *out = h->v->param_count(which); });
+}
+
+int pqlg_vlearner_snapshot(pqlg_vlearner h, float* q1, float* q2) {
+  return guarded([&] {
+    h->v->get_params(0, q1);
+    h->v->get_params(1, q2);
+  });
+}
+
+int pqlg_vlearner_buffer_size(pqlg_vlearner h, uint64_t* out) {
+  return guarded([&] { *out = h->v->replay()->size(); });
+}
+
+int pqlg_vlearner_set_sampler(pqlg_vlearner h, int mode) {
+  return guarded([&] {
+    require(mode == PQLG_RNG_PHILOX || mode == PQLG_RNG_INDICES, "set_sampler: bad mode");
+    h->v->set_mt_mode(mode == PQLG_RNG_INDICES);
+  });
+}
+
+int pqlg_vlearner_replay(pqlg_vlearner h, pqlg_replay* out) {
+  return guarded([&] { *out = &h->replay_view; });
+}
+
+int pqlg_vlearner_set_params(pqlg_vlearner h, int which, const float* flat) {
+  return guarded([&] { h->v->set_params(which, flat); });
+}
+
+int pqlg_vlearner_debug_read(pqlg_vlearner h, int what, float* out) {
+  return guarded([&] { h->v->debug_read(what, out); });
+}
+
+int pqlg_vlearner_kernels_per_update(pqlg_vlearner h, int* out) {
+  return guarded([&] { *out = h->v->kernels_per_update(); });
+}
+
+}  // extern "C"
