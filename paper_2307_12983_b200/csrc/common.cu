@@ -64,6 +64,27 @@ CUtensorMap make_tmap_2d(const void* base, uint64_t inner, uint64_t outer, uint6
   return m;
 }
 
+CUtensorMap make_tmap_3d(const void* base, uint64_t inner, uint64_t mid, uint64_t outer,
+                         uint64_t stride_mid, uint64_t stride_outer, uint32_t box_inner,
+                         uint32_t box_mid, Swz swz) {
+  require((reinterpret_cast<uintptr_t>(base) & 15) == 0, "TMA base must be 16-byte aligned");
+  require((stride_mid * 4) % 16 == 0 && (stride_outer * 4) % 16 == 0,
+          "TMA strides must be multiples of 16 bytes");
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  cuuint64_t dims[3] = {inner, mid, outer};
+  cuuint64_t strides[2] = {stride_mid * 4, stride_outer * 4};
+  cuuint32_t box[3] = {box_inner, box_mid, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(
+      &m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE,
+      swz == Swz::k128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(PQLG_ECUDA, "cuTensorMapEncodeTiled (3d) failed");
+  return m;
+}
+
 std::atomic<uint64_t> g_launches{0};
 
 }  // namespace pqlg

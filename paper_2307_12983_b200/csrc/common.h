@@ -98,4 +98,14 @@ enum class Swz { k128, k128a32 };
 CUtensorMap make_tmap_2d(const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride,
                          uint32_t box_inner, uint32_t box_outer, Swz swz, bool tf32_type = false);
 
+// 3-D fp32 tensor map {inner, mid, outer}; strides in elements.
+CUtensorMap make_tmap_3d(const void* base, uint64_t inner, uint64_t mid, uint64_t outer,
+                         uint64_t stride_mid, uint64_t stride_outer, uint32_t box_inner,
+                         uint32_t box_mid, Swz swz);
+
+// Output map of a GEMM epilogue: rows x cols fp32, box 32 x 32, 128B swizzle.
+inline CUtensorMap make_store_map(const void* base, uint64_t rows, uint64_t cols, uint64_t ld) {
+  return make_tmap_2d(base, cols, rows, ld, 32, 32, Swz::k128, false);
+}
+
 }  // namespace pqlg

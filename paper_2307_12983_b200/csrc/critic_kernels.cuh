@@ -149,8 +149,12 @@ static __global__ void __launch_bounds__(kRowThreads) actor_pick_kernel(LossArgs
 //   G[b,i]   = up[b] * w[i] * [h[b,i] > 0]            (dgrad + ReLU mask)
 //   dW[i]   += h[b,i] * up[b]     db_head += up[b]    (wgrad of the head)
 //   db[i]   += G[b,i]                                 (bias grad of layer below)
-// grid = (row tiles of 128, groups); partials per row tile, summed later in
-// tile order.  with_params = 0 for the actor gradient (input grads only).
+// grid = (row tiles of kHeadRows, groups), one thread per column: loads and
+// stores are coalesced across the block; partials per row tile are summed
+// later in tile order.  with_params = 0 for the actor gradient.
+constexpr int kHeadRows = 64;
+constexpr int kHeadThreads = 512;
+
 struct HeadBwdArgs {
   const float* up;     // [2][B]
   const float* h[2];   // post-activations of the last hidden layer [B x H]
@@ -165,24 +169,33 @@ struct HeadBwdArgs {
   int with_params;
 };
 
-static __global__ void head_backward_kernel(HeadBwdArgs a) {
+static __global__ void __launch_bounds__(kHeadThreads)
+    head_backward_kernel(const __grid_constant__ HeadBwdArgs a) {
   const int tile = blockIdx.x, k = blockIdx.y;
-  const int b0 = tile * 128;
-  const int b1 = min(b0 + 128, a.B);
+  const int b0 = tile * kHeadRows;
+  const int b1 = min(b0 + kHeadRows, a.B);
   const float* up = a.up + static_cast<int64_t>(k) * a.B;
-  const float* h = a.h[k];
-  const float* w = a.w[k];
-  float* G = a.G[k];
+  __shared__ float sup[kHeadRows];
+  for (int b = threadIdx.x; b < b1 - b0; b += blockDim.x) sup[b] = up[b0 + b];
+  __syncthreads();
+  const float* __restrict__ h = a.h[k];
+  const float* __restrict__ w = a.w[k];
+  float* __restrict__ G = a.G[k];
   for (int i = threadIdx.x; i < a.H; i += blockDim.x) {
     const float wi = w[i];
     float dw = 0.0f, db = 0.0f;
-    for (int b = b0; b < b1; ++b) {
-      const float hv = h[static_cast<int64_t>(b) * a.ld_h + i];
-      const float u = up[b];
-      const float g = hv > 0.0f ? __fmul_rn(u, wi) : 0.0f;
-      G[static_cast<int64_t>(b) * a.ld_g + i] = g;
-      if (a.with_params) {
-        dw = __fadd_rn(dw, __fmul_rn(hv, u));
+    for (int bb = b0; bb < b1; bb += 8) {
+      float hv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        hv[u] = bb + u < b1 ? __ldg(h + static_cast<int64_t>(bb + u) * a.ld_h + i) : 0.0f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (bb + u >= b1) break;
+        const float uu = sup[bb + u - b0];
+        const float g = hv[u] > 0.0f ? __fmul_rn(uu, wi) : 0.0f;
+        G[static_cast<int64_t>(bb + u) * a.ld_g + i] = g;
+        dw = __fadd_rn(dw, __fmul_rn(hv[u], uu));
         db = __fadd_rn(db, g);
       }
     }
@@ -193,7 +206,7 @@ static __global__ void head_backward_kernel(HeadBwdArgs a) {
   }
   if (a.with_params && threadIdx.x == 0) {
     float s = 0.0f;
-    for (int b = b0; b < b1; ++b) s = __fadd_rn(s, up[b]);
+    for (int b = 0; b < b1 - b0; ++b) s = __fadd_rn(s, sup[b]);
     a.db_head_part[static_cast<int64_t>(k) * a.tiles + tile] = s;
   }
 }

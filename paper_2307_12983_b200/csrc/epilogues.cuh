@@ -1,7 +1,10 @@
 // GEMM epilogues of the MLP layers.  Each thread of the 4 epilogue warps owns
 // one output row (TMEM lane) and receives 32 consecutive accumulator columns
 // per call, so row-wise heads (DDPG value dot, policy squash + exploration
-// noise, C51 logits) fuse without a cross-thread reduction.
+// noise) fuse without a cross-thread reduction.  Per-tile constants (bias,
+// head weights, ReLU masks) are preloaded in prepare() while the mainloop
+// runs; results leave through 128B-swizzled smem + TMA stores
+// (kStoreRank > 0) or direct stores for narrow heads.
 //
 // Reference arithmetic they replace:
 //   affine_forward bias add + relu          scalar.hpp:12-25, :57-60
@@ -13,59 +16,58 @@
 
 #include <cstdint>
 
+#include "ptx.cuh"
 #include "rng.cuh"
 
 namespace pqlg::epi {
 
-// relu(acc + b), stored; optional head dot  sum_n relu(.)*w_head[n]  per
-// n-tile, written to partial[(group*n_tiles + n_tile)*ld_part + m].
+// relu(acc + b) -> TMA store (store = 1) and/or a ReLU bitmask (bit t of
+// word n/32 = post[m, n] > 0) used by the backward; optional head dot
+// sum_n relu(.)*w_head[n] per n-tile -> partial[(group*n_tiles + n_tile)*ld_part + m].
 struct Hidden {
+  static constexpr int kStoreRank = 2;
   const float* bias[2];
-  float* out[2];
-  int64_t ld_out;
   const float* w_head[2];  // null: no head dot
+  uint32_t* mask[2];       // null: no bitmask
+  int ld_mask;             // words per row (= N/32)
   float* partial;
   int64_t ld_part;
   int n_tiles;
+  int bn;
   int M, N;
-  int store;  // 0: skip storing the activation (target critics)
+  int store;  // 0: skip storing the activation (target critics' last layer)
   struct Row {
     float dot;
   };
-  __device__ void begin(Row& r, int, int, int, int) const { r.dot = 0.0f; }
-  __device__ void chunk(Row& r, int group, int, int m, int n0, const float (&v)[32]) const {
-    if (m >= M) return;
+  __device__ void prepare(Row& r, int group, int, int, int n_tile, float* scratch) const {
+    r.dot = 0.0f;
+    const int t = threadIdx.x - 64;  // epilogue threads 0..127
     const float* b = bias[group];
-    float* o = out[group] + static_cast<int64_t>(m) * ld_out;
     const float* wh = w_head[group];
-    if (n0 + 32 <= N) {
-      float x[32];
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        const float y = __fadd_rn(v[t], b[n0 + t]);
-        x[t] = y > 0.0f ? y : 0.0f;
-      }
-      if (store) {
-#pragma unroll
-        for (int t = 0; t < 32; t += 4)
-          *reinterpret_cast<float4*>(o + n0 + t) = make_float4(x[t], x[t + 1], x[t + 2], x[t + 3]);
-      }
-      if (wh) {
-#pragma unroll
-        for (int t = 0; t < 32; ++t) r.dot = __fadd_rn(r.dot, __fmul_rn(x[t], wh[n0 + t]));
-      }
-    } else {
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        const int n = n0 + t;
-        if (n < N) {
-          const float y = __fadd_rn(v[t], b[n]);
-          const float x = y > 0.0f ? y : 0.0f;
-          if (store) o[n] = x;
-          if (wh) r.dot = __fadd_rn(r.dot, __fmul_rn(x, wh[n]));
-        }
-      }
+    for (int i = t; i < bn; i += 128) {
+      const int n = n_tile * bn + i;
+      scratch[i] = n < N ? b[n] : 0.0f;
+      if (wh) scratch[bn + i] = n < N ? wh[n] : 0.0f;
     }
+    ptx::named_bar_sync(1, 128);
+  }
+  __device__ bool chunk(Row& r, int group, int, int m, int n0, float (&v)[32],
+                        const float* scratch) const {
+    const int c0 = n0 % bn;
+    uint32_t bits = 0;
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+      const float y = __fadd_rn(v[t], scratch[c0 + t]);
+      const float x = y > 0.0f ? y : 0.0f;
+      v[t] = x;
+      bits |= (x > 0.0f ? 1u : 0u) << t;
+    }
+    if (w_head[group]) {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) r.dot = __fadd_rn(r.dot, __fmul_rn(v[t], scratch[bn + c0 + t]));
+    }
+    if (mask[group] && m < M) mask[group][static_cast<int64_t>(m) * ld_mask + (n0 >> 5)] = bits;
+    return store != 0;
   }
   __device__ void end(Row& r, int group, int, int m, int n_tile) const {
     if (m < M && w_head[group])
@@ -80,6 +82,7 @@ struct Hidden {
 // stream.  Noise draws consume columns in order n = 0..A-1, so the row state
 // (stream position, cached polar value) persists across 32-column chunks.
 struct PolicyHead {
+  static constexpr int kStoreRank = 0;
   const float* bias;
   float* act;
   int64_t ld_act;
@@ -97,7 +100,9 @@ struct PolicyHead {
     int has_saved;
     float sig;
   };
-  __device__ void begin(Row& r, int, int, int m, int) const {
+  __device__ void prepare(Row& r, int, int, int m, int, float* scratch) const {
+    const int t = threadIdx.x - 64;
+    for (int i = t; i < A; i += 128) scratch[i] = bias[i];
     r.has_saved = 0;
     r.saved = 0.0f;
     if (noise_state && m < M) {
@@ -107,14 +112,16 @@ struct PolicyHead {
       r.st = 0;
       r.sig = 0.0f;
     }
+    ptx::named_bar_sync(1, 128);
   }
-  __device__ void chunk(Row& r, int, int, int m, int n0, const float (&v)[32]) const {
-    if (m >= M) return;
+  __device__ bool chunk(Row& r, int, int, int m, int n0, float (&v)[32],
+                        const float* scratch) const {
+    if (m >= M) return false;
 #pragma unroll 1
     for (int t = 0; t < 32; ++t) {
       const int n = n0 + t;
       if (n >= A) break;
-      const float y = __fadd_rn(v[t], bias[n]);
+      const float y = __fadd_rn(v[t], scratch[n]);
       const float th = tanhf(y);
       float a = __fadd_rn(mid, __fmul_rn(half, th));
       if (tanh_out) tanh_out[static_cast<int64_t>(m) * ld_tanh + n] = th;
@@ -135,125 +142,144 @@ struct PolicyHead {
       }
       act[static_cast<int64_t>(m) * ld_act + n] = a;
     }
+    return false;
   }
   __device__ void end(Row& r, int, int, int m, int) const {
     if (noise_state && m < M) noise_state[m] = r.st;
   }
 };
 
-// dgrad output with the ReLU mask of the layer below (pre > 0 <=> post > 0),
-// plus per-CTA column sums of the masked gradient (the bias gradient of that
-// layer) written to colsum[(group*m_tiles + m_tile)*ld_cs + n].
+// dgrad output with the ReLU mask of the layer below (from its bitmask),
+// TMA-stored, plus per-CTA column sums of the masked gradient (the bias
+// gradient of that layer) written to colsum[(group*m_tiles + m_tile)*ld_cs + n].
 struct DgradMask {
-  const float* post[2];  // activation whose ReLU mask applies (nullable: no mask)
-  int64_t ld_post;
-  float* out[2];
-  int64_t ld_out;
+  static constexpr int kStoreRank = 2;
+  const uint32_t* mask[2];  // nullable: no mask
+  int ld_mask;
   float* colsum;  // nullable
   int64_t ld_cs;
   int m_tiles;
+  int bn;
   int M, N;
-  struct Row {};
-  __device__ void begin(Row&, int, int, int, int) const {}
-  __device__ void end(Row&, int, int, int, int) const {}
-  __device__ void chunk(Row&, int group, int, int m, int n0, const float (&v)[32]) const {
-    float g[32];
+  struct Row {
+    uint32_t bits[8];  // mask words of this row for the n-tile (bn <= 256)
+  };
+  __device__ void prepare(Row& r, int group, int, int m, int n_tile, float*) const {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.bits[i] = 0xffffffffu;
+    if (mask[group] && m < M) {
+      const uint32_t* p = mask[group] + static_cast<int64_t>(m) * ld_mask + n_tile * (bn >> 5);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < (bn >> 5)) r.bits[i] = p[i];
+    }
+  }
+  __device__ bool chunk(Row& r, int group, int, int m, int n0, float (&v)[32],
+                        float* scratch) const {
+    const int c = (n0 % bn) >> 5;
+    uint32_t bits = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i == c) bits = r.bits[i];
     const bool row_ok = m < M;
-    if (row_ok) {
-      const float* pp = post[group] ? post[group] + static_cast<int64_t>(m) * ld_post : nullptr;
-      float* o = out[group] + static_cast<int64_t>(m) * ld_out;
 #pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        const int n = n0 + t;
-        float x = v[t];
-        if (n >= N) x = 0.0f;
-        else if (pp && !(pp[n] > 0.0f)) x = 0.0f;
-        g[t] = x;
-      }
-      if (n0 + 32 <= N) {
-#pragma unroll
-        for (int t = 0; t < 32; t += 4)
-          *reinterpret_cast<float4*>(o + n0 + t) = make_float4(g[t], g[t + 1], g[t + 2], g[t + 3]);
-      } else {
-#pragma unroll
-        for (int t = 0; t < 32; ++t)
-          if (n0 + t < N) o[n0 + t] = g[t];
-      }
-    } else {
-#pragma unroll
-      for (int t = 0; t < 32; ++t) g[t] = 0.0f;
+    for (int t = 0; t < 32; ++t) {
+      const bool keep = row_ok && (n0 + t < N) && ((bits >> t) & 1u);
+      v[t] = keep ? v[t] : 0.0f;
     }
-    if (!colsum) return;
-    // Column sums over the 32 rows of this warp: recursive halving leaves
-    // lane l with the sum of one column (fixed order -> deterministic).
-    const int lane = threadIdx.x & 31;
+    if (colsum) {
+      // Column sums over the 32 rows of this warp: recursive halving leaves
+      // lane l with the sum of column l (fixed order -> deterministic).
+      float g[32];
 #pragma unroll
-    for (int w = 16; w >= 1; w >>= 1) {
-      const bool upper = (lane & w) != 0;
+      for (int t = 0; t < 32; ++t) g[t] = v[t];
+      const int lane = threadIdx.x & 31;
 #pragma unroll
-      for (int t = 0; t < w; ++t) {
-        const float send = upper ? g[t] : g[t + w];
-        const float keep = upper ? g[t + w] : g[t];
-        const float recv = __shfl_xor_sync(0xffffffffu, send, w);
-        g[t] = __fadd_rn(keep, recv);
+      for (int w = 16; w >= 1; w >>= 1) {
+        const bool upper = (lane & w) != 0;
+#pragma unroll
+        for (int t = 0; t < w; ++t) {
+          const float send = upper ? g[t] : g[t + w];
+          const float keep = upper ? g[t + w] : g[t];
+          const float recv = __shfl_xor_sync(0xffffffffu, send, w);
+          g[t] = __fadd_rn(keep, recv);
+        }
       }
+      const int q = (threadIdx.x >> 5) & 3;
+      scratch[q * 32 + lane] = g[0];
+      ptx::named_bar_sync(2, 128);
+      if (q == 0 && n0 + lane < N) {
+        const float s = __fadd_rn(__fadd_rn(scratch[lane], scratch[32 + lane]),
+                                  __fadd_rn(scratch[64 + lane], scratch[96 + lane]));
+        const int m_tile = (m - lane) / 128;
+        colsum[(static_cast<int64_t>(group) * m_tiles + m_tile) * ld_cs + n0 + lane] = s;
+      }
+      ptx::named_bar_sync(2, 128);
     }
-    // lane l now holds column c(l) where c is the bit-reversal-free mapping:
-    // at each level the upper half of lanes kept the upper half of columns.
-    const int col = n0 + lane;
-    const int q = (threadIdx.x >> 5) & 3;  // TMEM lane quadrant of this warp
-    // Cross-warp combine through shared memory in quadrant order.
-    __shared__ float cs[4][32];
-    cs[q][lane] = g[0];
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (q == 0 && col < N) {
-      const float s = __fadd_rn(__fadd_rn(cs[0][lane], cs[1][lane]),
-                                __fadd_rn(cs[2][lane], cs[3][lane]));
-      const int m_tile = (m - lane) / 128;  // all rows of this CTA share the tile
-      colsum[(static_cast<int64_t>(group) * m_tiles + m_tile) * ld_cs + col] = s;
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
+    return true;
   }
-};
-
-// Split-K partial tiles: W[((group*splits + split)*M + m)*N + n].
-struct Partial {
-  float* W;
-  int splits;
-  int M, N;
-  struct Row {};
-  __device__ void begin(Row&, int, int, int, int) const {}
   __device__ void end(Row&, int, int, int, int) const {}
-  __device__ void chunk(Row&, int group, int split, int m, int n0, const float (&v)[32]) const {
-    if (m >= M) return;
-    float* d = W + ((static_cast<int64_t>(group) * splits + split) * M + m) * N;
-    if (n0 + 32 <= N && (N & 3) == 0) {
-#pragma unroll
-      for (int t = 0; t < 32; t += 4)
-        *reinterpret_cast<float4*>(d + n0 + t) = make_float4(v[t], v[t + 1], v[t + 2], v[t + 3]);
-    } else {
-#pragma unroll
-      for (int t = 0; t < 32; ++t)
-        if (n0 + t < N) d[n0 + t] = v[t];
-    }
-  }
 };
 
-// Raw store of the accumulator (identity layer without bias): din columns.
+// Split-K partial tiles, TMA-stored through a 3-D map
+// {N, M, groups*splits}: W[((group*splits + split)*M + m)*N + n].
+struct Partial {
+  static constexpr int kStoreRank = 3;
+  struct Row {};
+  __device__ void prepare(Row&, int, int, int, int, float*) const {}
+  __device__ bool chunk(Row&, int, int, int, int, float (&)[32], const float*) const {
+    return true;
+  }
+  __device__ void end(Row&, int, int, int, int) const {}
+};
+
+// out = acc (+ bias) (ReLU optional), TMA-stored: the plain affine layer.
+struct Linear {
+  static constexpr int kStoreRank = 2;
+  const float* bias;  // nullable
+  int relu;
+  int bn;
+  int N;
+  struct Row {};
+  __device__ void prepare(Row&, int, int, int, int n_tile, float* scratch) const {
+    const int t = threadIdx.x - 64;
+    for (int i = t; i < bn; i += 128) {
+      const int n = n_tile * bn + i;
+      scratch[i] = (bias && n < N) ? bias[n] : 0.0f;
+    }
+    ptx::named_bar_sync(1, 128);
+  }
+  __device__ bool chunk(Row&, int, int, int, int n0, float (&v)[32], const float* scratch) const {
+    const int c0 = n0 % bn;
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+      float x = bias ? __fadd_rn(v[t], scratch[c0 + t]) : v[t];
+      if (relu) x = x > 0.0f ? x : 0.0f;
+      v[t] = x;
+    }
+    return true;
+  }
+  __device__ void end(Row&, int, int, int, int) const {}
+};
+
+// Raw store of the accumulator (narrow outputs, e.g. the action columns of
+// the critic input gradient).
 struct Store {
+  static constexpr int kStoreRank = 0;
   float* out[2];
   int64_t ld_out;
   int M, N;
   struct Row {};
-  __device__ void begin(Row&, int, int, int, int) const {}
-  __device__ void end(Row&, int, int, int, int) const {}
-  __device__ void chunk(Row&, int group, int, int m, int n0, const float (&v)[32]) const {
-    if (m >= M) return;
+  __device__ void prepare(Row&, int, int, int, int, float*) const {}
+  __device__ bool chunk(Row&, int group, int, int m, int n0, float (&v)[32], const float*) const {
+    if (m >= M) return false;
     float* o = out[group] + static_cast<int64_t>(m) * ld_out;
 #pragma unroll
     for (int t = 0; t < 32; ++t)
       if (n0 + t < N) o[n0 + t] = v[t];
+    return false;
   }
+  __device__ void end(Row&, int, int, int, int) const {}
 };
 
 }  // namespace pqlg::epi

@@ -11,13 +11,18 @@
 // so one kernel template covers all three by choosing each operand's major
 // mode.  K-major operands use the 128B swizzle; MN-major tf32 operands must use
 // the 128B/32B-atom swizzle (the only MN-major tf32 smem layout UMMA accepts).
+// Operand tensor maps are typed TFLOAT32 so TMA rounds fp32 -> tf32 to
+// nearest on the way into shared memory (the MMA alone would truncate).
 //
 // Structure (one 128 x BN output tile per CTA, 192 threads):
 //   warp 0      TMA producer   (one elected lane, kStages-deep smem ring)
 //   warp 1      TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..5  epilogue: tcgen05.ld 32 columns at a time, hand to Epi
+//   warps 2..5  epilogue: Epi::prepare() preloads per-tile constants while the
+//               mainloop runs; then tcgen05.ld 32 columns at a time ->
+//               Epi::chunk() -> 128B-swizzled staging in the (now idle)
+//               pipeline smem -> TMA bulk tensor store (coalesced, async).
 // Split-K over blockIdx.z lets the K=8192 weight-gradient GEMMs fill 148 SMs;
-// the epilogue then writes partial tiles that a fixed-order reduction sums.
+// their epilogue stores partial tiles that a fixed-order reduction sums.
 #pragma once
 
 #include <cstdint>
@@ -30,10 +35,12 @@ constexpr int kBM = 128;       // UMMA M (cta_group::1)
 constexpr int kBK = 32;        // fp32 elements per 128-byte swizzle row
 constexpr int kUmmaK = 8;      // K per tcgen05.mma.kind::tf32
 constexpr int kThreads = 192;  // 6 warps
+constexpr int kScratchBytes = 4096;  // per-tile epilogue constants
 
 struct Operands {
   CUtensorMap a[2];  // one per group (twin critics share a launch)
   CUtensorMap b[2];
+  CUtensorMap d[2];  // output maps (Epi::kStoreRank > 0)
 };
 
 struct Problem {
@@ -48,7 +55,12 @@ struct SmemLayout {
   static constexpr int kABytes = kBM * kBK * 4;        // 16 KB
   static constexpr int kBBytes = BN * kBK * 4;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kBarOffset = kStages * kStageBytes;
+  static constexpr int kPipeBytes = kStages * kStageBytes;
+  // epilogue staging reuses the pipeline ring: 4 warps x (BN/32) x 4 KB
+  static constexpr int kStageOutBytes = 4 * (BN / 32) * 4096;
+  static_assert(kStageOutBytes <= kPipeBytes, "staging must fit in the pipeline smem");
+  static constexpr int kScratchOffset = kPipeBytes;
+  static constexpr int kBarOffset = kScratchOffset + kScratchBytes;
   // full[kStages], empty[kStages], tmem_full, tmem pointer
   static constexpr int kTotal = kBarOffset + (2 * kStages + 1) * 8 + 16;
   static constexpr int kDynamic = kTotal + 1024;  // slack for 1024B alignment
@@ -100,15 +112,35 @@ constexpr uint32_t make_idesc() {
   return d;
 }
 
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* smem, int32_t c0,
+                                             int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(ptx::smem_u32(smem)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* smem, int32_t c0,
+                                             int32_t c1, int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(ptx::smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 // Epi concept:
-//   struct Epi {
-//     struct Row;                                   // per-thread row state
-//     __device__ void begin(Row&, int group, int split, int m, int n_tile) const;
-//     __device__ void chunk(Row&, int group, int split, int m, int n0, const float (&v)[32]) const;
-//     __device__ void end(Row&, int group, int split, int m, int n_tile) const;
-//   };
-// `m` may be >= M (rows beyond the problem are zero-filled by TMA); the
-// epilogue masks its own stores.
+//   static constexpr int kStoreRank;   // 0: Epi stores itself; 2/3: TMA store of v
+//   struct Row;                        // per-thread row state
+//   __device__ void prepare(Row&, int group, int split, int m, int n_tile, float* scratch) const;
+//       called by all 128 epilogue threads before the accumulator is ready;
+//       must end with ptx::named_bar_sync(1, 128) if it writes `scratch`.
+//   __device__ bool chunk(Row&, int group, int split, int m, int n0, float (&v)[32],
+//                         const float* scratch) const;  // transforms v; true = store v
+//   __device__ void end(Row&, int group, int split, int m, int n_tile) const;
+// `m` may be >= M (rows beyond the problem are zero-filled by TMA; TMA stores
+// clip them); the epilogue masks its own direct stores.
 template <int BN, int kStages, bool kAMN, bool kBMN, class Epi>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ Operands ops, const Problem prob, const Epi epi) {
@@ -116,6 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
+  float* scratch = reinterpret_cast<float*>(smem + L::kScratchOffset);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
   uint64_t* empty = full + kStages;
   uint64_t* tmem_full = empty + kStages;
@@ -202,13 +235,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Epilogue warps 2..5: TMEM lane quadrant = warp % 4.
     const int q = warp & 3;
     const int lane = threadIdx.x & 31;
-    const int m = m_tile * kBM + q * 32 + lane;
+    const int row0 = m_tile * kBM + q * 32;
+    const int m = row0 + lane;
     typename Epi::Row row;
-    epi.begin(row, group, split, m, n_tile);
+    epi.prepare(row, group, split, m, n_tile, scratch);
     if (n_kt > 0) {
       ptx::mbar_wait(tmem_full, 0);
       ptx::tc_fence_after();
     }
+    // staging for this warp: (BN/32) buffers of 32 rows x 128 B (SW128)
+    uint8_t* stage = smem + q * (BN / 32) * 4096;
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       float v[32];
@@ -222,9 +258,34 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int t = 0; t < 32; ++t) v[t] = 0.0f;
       }
-      epi.chunk(row, group, split, m, n_tile * BN + c * 32, v);
+      const int n0 = n_tile * BN + c * 32;
+      const bool st = epi.chunk(row, group, split, m, n0, v, scratch);
+      if constexpr (Epi::kStoreRank > 0) {
+        if (st) {
+          uint8_t* buf = stage + c * 4096;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4* dst = reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4));
+            *dst = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (Epi::kStoreRank == 2) {
+              tma_store_2d(&ops.d[group], buf, n0, row0);
+            } else {
+              tma_store_3d(&ops.d[0], buf, n0, row0, group * prob.splits + split);
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+      }
     }
     epi.end(row, group, split, m, n_tile);
+    if constexpr (Epi::kStoreRank > 0) {
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      __syncwarp();
+    }
   }
 
   ptx::tc_fence_before();

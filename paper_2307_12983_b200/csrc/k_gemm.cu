@@ -1,49 +1,13 @@
-// Operator-level GEMM entry point (pqlg_k_gemm_tf32): the affine kernels of
-// pql::kernels (kernels.hpp:25-43) restated as one tcgen05 TF32 GEMM with an
-// optional bias + ReLU epilogue.  Used by the per-op parity tests.
+// Operator-level GEMM entry points (pqlg_k_gemm_tf32*): the affine kernels of
+// pql::kernels (kernels.hpp:25-43) restated as one tcgen05 TF32 GEMM with the
+// learners' epilogue path (bias + ReLU, TMA store, split-K partials + a
+// fixed-order reduction).  Used by the per-op parity tests and the bench's
+// roofline measurement.
+#include "epilogues.cuh"
 #include "gemm_host.cuh"
 
 namespace pqlg {
 namespace {
-
-struct StoreEpi {
-  float* D;
-  const float* bias;
-  int ldd, M, N, relu;
-  struct Row {};
-  __device__ void begin(Row&, int, int, int, int) const {}
-  __device__ void end(Row&, int, int, int, int) const {}
-  __device__ void chunk(Row&, int, int, int m, int n0, const float (&v)[32]) const {
-    if (m >= M) return;
-    float* d = D + static_cast<size_t>(m) * ldd;
-#pragma unroll
-    for (int t = 0; t < 32; ++t) {
-      const int n = n0 + t;
-      if (n < N) {
-        float x = v[t];
-        if (bias) x = __fadd_rn(x, bias[n]);
-        if (relu) x = x > 0.0f ? x : 0.0f;
-        d[n] = x;
-      }
-    }
-  }
-};
-
-// Split-K partial tiles: W[split][M][N], summed later in split order.
-struct PartialEpi {
-  float* W;
-  int M, N;
-  struct Row {};
-  __device__ void begin(Row&, int, int, int, int) const {}
-  __device__ void end(Row&, int, int, int, int) const {}
-  __device__ void chunk(Row&, int, int split, int m, int n0, const float (&v)[32]) const {
-    if (m >= M) return;
-    float* d = W + (static_cast<size_t>(split) * M + m) * N;
-#pragma unroll
-    for (int t = 0; t < 32; ++t)
-      if (n0 + t < N) d[n0 + t] = v[t];
-  }
-};
 
 __global__ void reduce_splits(const float* W, int splits, int M, int N, float* D, int ldd,
                               const float* bias, int relu) {
@@ -67,27 +31,33 @@ void run(const float* A, const float* B, float* D, const float* bias, int M, int
   ops.b[0] = ops.b[1] = gemm::map_b(B, N, K, ldb, BMN, BN, tf32);
   gemm::Problem p = gemm::make_problem(M, N, K, splits);
   if (p.splits == 1) {
-    gemm::launch<BN, AMN, BMN>(ops, p, 1, StoreEpi{D, bias, ldd, M, N, relu}, st);
+    ops.d[0] = ops.d[1] = make_store_map(D, M, N, ldd);
+    gemm::launch<BN, AMN, BMN>(ops, p, 1, epi::Linear{bias, relu, BN, N}, st);
     return;
   }
+  require(N % 4 == 0, "split-K partials need N % 4 == 0");
   float* W = nullptr;
   PQLG_CUDA(cudaMallocAsync(&W, sizeof(float) * p.splits * M * N, st));
-  gemm::launch<BN, AMN, BMN>(ops, p, 1, PartialEpi{W, M, N}, st);
+  ops.d[0] = ops.d[1] = make_tmap_3d(W, N, M, p.splits, N, static_cast<uint64_t>(M) * N, 32, 32,
+                                     Swz::k128);
+  gemm::launch<BN, AMN, BMN>(ops, p, 1, epi::Partial{}, st);
   reduce_splits<<<296, 256, 0, st>>>(W, p.splits, M, N, D, ldd, bias, relu);
   PQLG_CHECK_LAUNCH();
   count_launch();
   PQLG_CUDA(cudaFreeAsync(W, st));
 }
 
-// Back-to-back launches with pre-encoded maps (device-time measurement).
+// Back-to-back launches of the hidden-layer forward GEMM with the learners'
+// Hidden epilogue (bias + ReLU + bitmask + TMA store) and pre-encoded maps.
 template <int BN>
 void run_repeat(const float* A, const float* B, float* D, const float* bias, int M, int N, int K,
                 int lda, int ldb, int ldd, int relu, int iters, cudaStream_t st) {
   gemm::Operands ops;
   ops.a[0] = ops.a[1] = gemm::map_a(A, M, K, lda, false, true);
   ops.b[0] = ops.b[1] = gemm::map_b(B, N, K, ldb, true, BN, true);
+  ops.d[0] = ops.d[1] = make_store_map(D, M, N, ldd);
   const gemm::Problem p = gemm::make_problem(M, N, K, 1);
-  const StoreEpi e{D, bias, ldd, M, N, relu};
+  const epi::Linear e{bias, relu, BN, N};
   for (int i = 0; i < iters; ++i) gemm::launch<BN, false, true>(ops, p, 1, e, st);
 }
 

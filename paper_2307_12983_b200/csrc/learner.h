@@ -74,12 +74,13 @@ class VLearner {
   DevBuf<float> Xon_, Xtg_, ret_, eff_, y_;
   std::vector<DevBuf<float>> pact_;
   std::array<std::vector<DevBuf<float>>, 2> tact_, oact_, G_;
+  std::array<std::vector<DevBuf<uint32_t>>, 2> omask_;  // ReLU bitmasks of the online critics
   DevBuf<float> part_t_, part_o_, up_;
   DevBuf<double> block_loss_;
   DevBuf<unsigned int> loss_counter_;
   std::vector<DevBuf<float>> wpart_, colsum_;
   std::vector<int> wsplits_;
-  DevBuf<float> head_dw_, head_db_;
+  DevBuf<float> head_dw_, head_db_, head_cs_;
   int fin_blocks_ = 0;
   DevBuf<double> block_sq_;
   DevBuf<unsigned int> fin_counter_;

@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cmath>
+#include <cstring>
 #include <functional>
 #include <type_traits>
 #include <vector>
@@ -41,15 +42,28 @@ inline int wgrad_splits(int M, int N, int K, int groups) {
   int s = kSMs / tiles;
   if (s < 1) s = 1;
   if (s > k_tiles) s = k_tiles;
-  return s;
+  const int per = (k_tiles + s - 1) / s;  // effective count after even chunking
+  return (k_tiles + per - 1) / per;
 }
 
 // ldw: row stride of W (N unless W is read from a padded WeightMirror).
+// Output maps: D0/D1 [M x N] with row stride ldd (null: the epilogue stores
+// directly and no map is built).
+inline void set_out(gemm::Operands& ops, const float* D0, const float* D1, int M, int N,
+                    int64_t ldd, int groups) {
+  std::memset(&ops.d, 0, sizeof(ops.d));
+  if (!D0) return;
+  ops.d[0] = make_store_map(D0, M, N, ldd);
+  ops.d[1] = groups > 1 ? make_store_map(D1, M, N, ldd) : ops.d[0];
+}
+
 template <class Epi>
 Step fwd(const float* A0, const float* A1, int64_t lda, const float* W0, const float* W1, int M,
-         int N, int K, int groups, Epi epi, int64_t ldw = 0) {
+         int N, int K, int groups, Epi epi, int64_t ldw = 0, const float* D0 = nullptr,
+         const float* D1 = nullptr, int64_t ldd = 0) {
   Step step;
   if (ldw == 0) ldw = N;
+  if (ldd == 0) ldd = N;
   with_bn(N, [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
     gemm::Operands ops;
@@ -57,6 +71,7 @@ Step fwd(const float* A0, const float* A1, int64_t lda, const float* W0, const f
     ops.a[1] = groups > 1 ? gemm::map_a(A1, M, K, lda, false, true) : ops.a[0];
     ops.b[0] = gemm::map_b(W0, N, K, ldw, true, BN, true);
     ops.b[1] = groups > 1 ? gemm::map_b(W1, N, K, ldw, true, BN, true) : ops.b[0];
+    set_out(ops, D0, D1, M, N, ldd, groups);
     const gemm::Problem p = gemm::make_problem(M, N, K, 1);
     step = [ops, p, groups, epi](cudaStream_t st) {
       gemm::launch<BN, false, true>(ops, p, groups, epi, st);
@@ -68,7 +83,9 @@ Step fwd(const float* A0, const float* A1, int64_t lda, const float* W0, const f
 // din[M x N_in] = G[M x N_out] * W^T, W = [N_in x N_out] row-major (ld = ldw).
 template <class Epi>
 Step dgrad(const float* G0, const float* G1, int64_t ldg, const float* W0, const float* W1,
-           int64_t ldw, int M, int N_in, int N_out, int groups, Epi epi) {
+           int64_t ldw, int M, int N_in, int N_out, int groups, Epi epi,
+           const float* D0 = nullptr, const float* D1 = nullptr, int64_t ldd = 0) {
+  if (ldd == 0) ldd = N_in;
   Step step;
   with_bn(N_in, [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
@@ -77,6 +94,7 @@ Step dgrad(const float* G0, const float* G1, int64_t ldg, const float* W0, const
     ops.a[1] = groups > 1 ? gemm::map_a(G1, M, N_out, ldg, false, true) : ops.a[0];
     ops.b[0] = gemm::map_b(W0, N_in, N_out, ldw, false, BN, true);
     ops.b[1] = groups > 1 ? gemm::map_b(W1, N_in, N_out, ldw, false, BN, true) : ops.b[0];
+    set_out(ops, D0, D1, M, N_in, ldd, groups);
     const gemm::Problem p = gemm::make_problem(M, N_in, N_out, 1);
     step = [ops, p, groups, epi](cudaStream_t st) {
       gemm::launch<BN, false, false>(ops, p, groups, epi, st);
@@ -85,10 +103,11 @@ Step dgrad(const float* G0, const float* G1, int64_t ldg, const float* W0, const
   return step;
 }
 
-// dW[M=in x N=out] = H^T G over K = batch rows; split-K partials via Epi.
+// dW[M=in x N=out] = H^T G over K = batch rows; split-K partial tiles are
+// TMA-stored to W[(group*splits + split)][M][N] (N % 4 == 0).
 template <class Epi>
 Step wgrad(const float* H0, const float* H1, int64_t ldh, const float* G0, const float* G1,
-           int64_t ldg, int M, int N, int K, int groups, int splits, Epi epi) {
+           int64_t ldg, int M, int N, int K, int groups, int splits, Epi epi, float* W) {
   Step step;
   with_bn(N, [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
@@ -98,6 +117,9 @@ Step wgrad(const float* H0, const float* H1, int64_t ldh, const float* G0, const
     ops.b[0] = gemm::map_b(G0, N, K, ldg, true, BN, true);
     ops.b[1] = groups > 1 ? gemm::map_b(G1, N, K, ldg, true, BN, true) : ops.b[0];
     const gemm::Problem p = gemm::make_problem(M, N, K, splits);
+    require(p.splits == splits, "wgrad: split count must divide the k tiles evenly");
+    ops.d[0] = ops.d[1] = make_tmap_3d(W, N, M, static_cast<uint64_t>(groups) * splits, N,
+                                       static_cast<uint64_t>(M) * N, 32, 32, Swz::k128);
     step = [ops, p, groups, epi](cudaStream_t st) {
       gemm::launch<BN, true, true>(ops, p, groups, epi, st);
     };

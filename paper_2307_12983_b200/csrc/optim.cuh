@@ -41,7 +41,10 @@ struct FinalizeArgs {
   float max_norm;
 };
 
-static __global__ void __launch_bounds__(kFinalizeThreads) finalize_kernel(FinalizeArgs a) {
+// __grid_constant__: the segment table is indexed dynamically; without it
+// every thread would copy the whole argument block to local memory.
+static __global__ void __launch_bounds__(kFinalizeThreads)
+    finalize_kernel(const __grid_constant__ FinalizeArgs a) {
   const int group = blockIdx.y;
   double sq = 0.0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < a.total;
@@ -51,8 +54,18 @@ static __global__ void __launch_bounds__(kFinalizeThreads) finalize_kernel(Final
     const Segment& sg = a.seg[s];
     const int64_t j = i - sg.dst;
     const float* src = sg.src + group * sg.group_stride + j;
+    // terms summed in ascending order; loads issued 8 at a time so the
+    // latency of the (L2-resident) partials overlaps
     float acc = src[0];
-    for (int t = 1; t < sg.n_terms; ++t) acc = __fadd_rn(acc, src[t * sg.stride]);
+    int t = 1;
+    for (; t + 8 <= sg.n_terms; t += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = src[(t + u) * sg.stride];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = __fadd_rn(acc, v[u]);
+    }
+    for (; t < sg.n_terms; ++t) acc = __fadd_rn(acc, src[t * sg.stride]);
     a.grads[group * a.gstride + i] = acc;
     const double d = static_cast<double>(acc);
     sq += d * d;

@@ -317,11 +317,36 @@ __device__ __forceinline__ uint64_t sample_index(const SamplerState* ss, const u
 
 __device__ __forceinline__ void gather_row(const Ring& ring, const Norm& norm, const Gather& g,
                                            uint64_t i, uint64_t r, int lane) {
-  const float* so = ring.obs + i * ring.ld_obs;
-  const float* sb = ring.boot + i * ring.ld_obs;
-  float* dobs = g.obs + r * g.ld_obs;
-  float* dboot = g.boot + r * g.ld_boot;
-  for (int d = lane; d < ring.D; d += 32) {
+  const float* __restrict__ so = ring.obs + i * ring.ld_obs;
+  const float* __restrict__ sb = ring.boot + i * ring.ld_obs;
+  float* __restrict__ dobs = g.obs + r * g.ld_obs;
+  float* __restrict__ dboot = g.boot + r * g.ld_boot;
+  int d0 = 0;
+  if (ring.D <= 256) {  // all loads of the row in flight before any store
+    float x[8], y[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int d = lane + 32 * u;
+      x[u] = d < ring.D ? __ldg(so + d) : 0.0f;
+      y[u] = d < ring.D ? __ldg(sb + d) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int d = lane + 32 * u;
+      if (d < ring.D) {
+        float xx = x[u], yy = y[u];
+        if (!norm.identity) {
+          const float mu = norm.mean[d], iv = norm.inv[d];
+          xx = normalize1(xx, mu, iv);
+          yy = normalize1(yy, mu, iv);
+        }
+        dobs[d] = xx;
+        dboot[d] = yy;
+      }
+    }
+    d0 = ring.D;
+  }
+  for (int d = d0 + lane; d < ring.D; d += 32) {
     float x = so[d], y = sb[d];
     if (!norm.identity) {
       const float mu = norm.mean[d], iv = norm.inv[d];

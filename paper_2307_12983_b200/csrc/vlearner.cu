@@ -105,7 +105,9 @@ void VLearner::build_update() {
   const int B = B_, D = D_, A = A_, H = H_, nh = nh_, K0 = D + A;
   const int64_t P = qnet_.params;
   const int nt = mlp::n_tiles(H);
+  const int bnH = mlp::bn_for(H);
   const int mt = (B + 127) / 128;
+  const int wpr = H / 32;  // mask words per row
   float* q1 = q_.p;
   float* q2 = q_.p + Ps_;
   float* q1t = qt_.p;
@@ -121,10 +123,12 @@ void VLearner::build_update() {
   for (int k = 0; k < 2; ++k) {
     tact_[k].resize(nh);
     oact_[k].resize(nh);
+    omask_[k].resize(nh);
     G_[k].resize(nh);
     for (int l = 0; l < nh; ++l) {
       tact_[k][l].alloc(l + 1 < nh ? static_cast<size_t>(B) * H : 0);
       oact_[k][l].alloc(static_cast<size_t>(B) * H);
+      omask_[k][l].alloc(static_cast<size_t>(B) * wpr);
       G_[k][l].alloc(static_cast<size_t>(B) * H);
     }
   }
@@ -150,13 +154,12 @@ void VLearner::build_update() {
     for (int l = 0; l < nh; ++l) {
       epi::Hidden e{};
       e.bias[0] = e.bias[1] = lagged_.p + pnet_.b_off[l];
-      e.out[0] = e.out[1] = pact_[l].p;
-      e.ld_out = H;
+      e.bn = bnH;
       e.M = B;
       e.N = H;
       e.store = 1;
       const float* W = lagged_.p + pnet_.w_off[l];
-      steps_.push_back(mlp::fwd(in, in, ld, W, W, B, H, K, 1, e));
+      steps_.push_back(mlp::fwd(in, in, ld, W, W, B, H, K, 1, e, 0, pact_[l].p, pact_[l].p, H));
       in = pact_[l].p;
       ld = H;
       K = H;
@@ -184,9 +187,10 @@ void VLearner::build_update() {
       epi::Hidden e{};
       for (int k = 0; k < 2; ++k) {
         e.bias[k] = nets[k] + qnet_.b_off[l];
-        e.out[k] = target ? tact_[k][l].p : oact_[k][l].p;
+        e.mask[k] = target ? nullptr : omask_[k][l].p;
       }
-      e.ld_out = H;
+      e.ld_mask = wpr;
+      e.bn = bnH;
       e.M = B;
       e.N = H;
       const bool last = l + 1 == nh;
@@ -199,10 +203,13 @@ void VLearner::build_update() {
       }
       const float* a0 = l == 0 ? X : (target ? tact_[0][l - 1].p : oact_[0][l - 1].p);
       const float* a1 = l == 0 ? X : (target ? tact_[1][l - 1].p : oact_[1][l - 1].p);
+      const float* d0 = target ? tact_[0][l].p : oact_[0][l].p;
+      const float* d1 = target ? tact_[1][l].p : oact_[1][l].p;
+      if (!e.store) d0 = d1 = nullptr;
       const int64_t lda = l == 0 ? Kp_ : H;
       const int K = l == 0 ? K0 : H;
       steps_.push_back(mlp::fwd(a0, a1, lda, nets[0] + qnet_.w_off[l], nets[1] + qnet_.w_off[l],
-                                B, H, K, 2, e));
+                                B, H, K, 2, e, 0, d0, d1, H));
     }
   };
 
@@ -239,8 +246,10 @@ void VLearner::build_update() {
     wpart_[l].alloc(2ull * wsplits_[l] * in * H);
     colsum_[l].alloc(2ull * mt * H);
   }
-  head_dw_.alloc(2ull * mt * H);
-  head_db_.alloc(2ull * mt);
+  const int ht = (B + critic::kHeadRows - 1) / critic::kHeadRows;  // head-backward row tiles
+  head_dw_.alloc(2ull * ht * H);
+  head_db_.alloc(2ull * ht);
+  head_cs_.alloc(2ull * ht * H);
   {
     critic::HeadBwdArgs a{};
     a.up = up_.p;
@@ -253,14 +262,13 @@ void VLearner::build_update() {
     a.ld_g = H;
     a.dw_part = head_dw_.p;
     a.db_head_part = head_db_.p;
-    a.db_part = colsum_[nh - 1].p;
+    a.db_part = head_cs_.p;
     a.B = B;
     a.H = H;
-    a.tiles = mt;
+    a.tiles = ht;
     a.with_params = 1;
-    const int threads = H < 1024 ? H : 1024;
-    steps_.push_back([a, mt, threads](cudaStream_t st) {
-      critic::head_backward_kernel<<<dim3(mt, 2), threads, 0, st>>>(a);
+    steps_.push_back([a, ht](cudaStream_t st) {
+      critic::head_backward_kernel<<<dim3(ht, 2), critic::kHeadThreads, 0, st>>>(a);
       PQLG_CHECK_LAUNCH();
       count_launch();
     });
@@ -268,28 +276,25 @@ void VLearner::build_update() {
   for (int l = nh - 1; l >= 0; --l) {
     const int in = l == 0 ? K0 : H;
     // wgrad: dW_l = act_{l-1}^T G_l  (act_{-1} = the critic input)
-    epi::Partial pe{wpart_[l].p, wsplits_[l], in, H};
     const float* h0 = l == 0 ? Xon_.p : oact_[0][l - 1].p;
     const float* h1 = l == 0 ? Xon_.p : oact_[1][l - 1].p;
     const int64_t ldh = l == 0 ? Kp_ : H;
     steps_.push_back(mlp::wgrad(h0, h1, ldh, G_[0][l].p, G_[1][l].p, H, in, H, B, 2,
-                                wsplits_[l], pe));
+                                wsplits_[l], epi::Partial{}, wpart_[l].p));
     if (l > 0) {
       // dgrad: G_{l-1} = (G_l W_l^T) * [act_{l-1} > 0], + bias colsums of layer l-1
       epi::DgradMask dm{};
-      for (int k = 0; k < 2; ++k) {
-        dm.post[k] = oact_[k][l - 1].p;
-        dm.out[k] = G_[k][l - 1].p;
-      }
-      dm.ld_post = H;
-      dm.ld_out = H;
+      for (int k = 0; k < 2; ++k) dm.mask[k] = omask_[k][l - 1].p;
+      dm.ld_mask = wpr;
       dm.colsum = colsum_[l - 1].p;
       dm.ld_cs = H;
       dm.m_tiles = mt;
+      dm.bn = bnH;
       dm.M = B;
       dm.N = H;
       steps_.push_back(mlp::dgrad(G_[0][l].p, G_[1][l].p, H, q1 + qnet_.w_off[l],
-                                  q2 + qnet_.w_off[l], H, B, H, H, 2, dm));
+                                  q2 + qnet_.w_off[l], H, B, H, H, 2, dm, G_[0][l - 1].p,
+                                  G_[1][l - 1].p, H));
     }
   }
 
@@ -302,12 +307,16 @@ void VLearner::build_update() {
       f.seg[s++] = optim::Segment{qnet_.w_off[l], static_cast<int64_t>(in) * H, wpart_[l].p,
                                   static_cast<int64_t>(wsplits_[l]) * in * H, wsplits_[l],
                                   static_cast<int64_t>(in) * H};
-      f.seg[s++] = optim::Segment{qnet_.b_off[l], H, colsum_[l].p,
-                                  static_cast<int64_t>(mt) * H, mt, H};
+      if (l + 1 < nh)
+        f.seg[s++] = optim::Segment{qnet_.b_off[l], H, colsum_[l].p,
+                                    static_cast<int64_t>(mt) * H, mt, H};
+      else
+        f.seg[s++] = optim::Segment{qnet_.b_off[l], H, head_cs_.p, static_cast<int64_t>(ht) * H,
+                                    ht, H};
     }
-    f.seg[s++] = optim::Segment{qnet_.w_off[nh], H, head_dw_.p, static_cast<int64_t>(mt) * H,
-                                mt, H};
-    f.seg[s++] = optim::Segment{qnet_.b_off[nh], 1, head_db_.p, mt, mt, 1};
+    f.seg[s++] = optim::Segment{qnet_.w_off[nh], H, head_dw_.p, static_cast<int64_t>(ht) * H,
+                                ht, H};
+    f.seg[s++] = optim::Segment{qnet_.b_off[nh], 1, head_db_.p, ht, ht, 1};
     require(s <= optim::kMaxSegments, "vlearner: too many layers");
     f.n_seg = s;
     f.total = P;
