@@ -86,11 +86,21 @@ static __global__ void __launch_bounds__(kFinalizeThreads)
     last = prev == gridDim.x - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last) return;
+  // Last block: fixed-order tree over the block partials (all threads load,
+  // so the L2 latency is paid once, not gridDim.x times).
   __threadfence();
-  double tot = 0.0;
   const volatile double* bs = a.block_sq + group * gridDim.x;
-  for (unsigned b = 0; b < gridDim.x; ++b) tot += bs[b];
+  double part = 0.0;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) part += bs[b];
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) part += __shfl_down_sync(0xffffffffu, part, d);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double tot = 0.0;
+  for (int w = 0; w < kFinalizeThreads / 32; ++w) tot += red[w];
   a.counter[group] = 0;
   const double norm = sqrt(tot);
   float s = 1.0f;
