@@ -194,6 +194,7 @@ typedef struct {
   double vmax;
   int max_episode_len;    /* synthetic env time limit */
   int env_offset;         /* global index of this shard's first env (sharded actors) */
+  int envs_total;         /* global env count of a sharded actor (0: n_envs)          */
 } pqlg_config;
 
 /* TaskDims (learners.hpp:23-26) */
@@ -251,6 +252,87 @@ PQLG_API int pqlg_vlearner_set_params(pqlg_vlearner h, int which, const float* f
 PQLG_API int pqlg_vlearner_debug_read(pqlg_vlearner h, int what, float* host_out);
 /* Number of kernels one update launches (graph nodes). */
 PQLG_API int pqlg_vlearner_kernels_per_update(pqlg_vlearner h, int* out);
+
+/* ------------------------------------------------ P-learner (policy core) */
+typedef struct pqlg_plearner_s* pqlg_plearner;
+
+/* PolicyLearnerCore(cfg, dims, init_rng)  learners.hpp:112, learners.cpp:202-217.
+ * Critic replicas initialised as CriticPair::create(std::mt19937_64(init_rng_seed)),
+ * the policy as PolicyHandle::create(make_rng(seed, init, 0)); sampling keyed by
+ * derive_seed(seed, sample, 2). */
+PQLG_API int pqlg_plearner_create(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                                  uint64_t init_rng_seed, void* stream, pqlg_plearner* out);
+PQLG_API int pqlg_plearner_destroy(pqlg_plearner h);
+/* adopt_critics(snapshot): equal-or-newer version replaces (learners.cpp:222-227) */
+PQLG_API int pqlg_plearner_adopt_critics(pqlg_plearner h, const float* q1_host,
+                                         const float* q2_host, int64_t version);
+PQLG_API int pqlg_plearner_adopt_norm(pqlg_plearner h, const pqlg_norm_stats* norm);
+/* ingest(states) = StateBuffer::insert (learners.hpp:117) */
+PQLG_API int pqlg_plearner_ingest(pqlg_plearner h, const float* states_dev, int64_t ld,
+                                  uint64_t n);
+PQLG_API int pqlg_plearner_ready(pqlg_plearner h, int64_t c_a, int* ready);
+/* update(): one policy update; synchronizes and returns the actor loss. */
+PQLG_API int pqlg_plearner_update(pqlg_plearner h, float* loss_host);
+PQLG_API int pqlg_plearner_update_n(pqlg_plearner h, int n);
+PQLG_API int pqlg_plearner_last_loss(pqlg_plearner h, float* loss_host);
+/* make_snapshot(): the policy's flat parameters (host copy). */
+PQLG_API int pqlg_plearner_snapshot(pqlg_plearner h, float* flat_host);
+/* which: 0 policy, 1 critic replica q1, 2 critic replica q2 */
+PQLG_API int pqlg_plearner_get_params(pqlg_plearner h, int which, float* flat_host);
+PQLG_API int pqlg_plearner_set_params(pqlg_plearner h, int which, const float* flat_host);
+PQLG_API int pqlg_plearner_param_count(pqlg_plearner h, int which, int64_t* out);
+PQLG_API int pqlg_plearner_buffer_size(pqlg_plearner h, uint64_t* out);
+PQLG_API int pqlg_plearner_set_sampler(pqlg_plearner h, int mode);
+PQLG_API int pqlg_plearner_kernels_per_update(pqlg_plearner h, int* out);
+
+/* ------------------------------------------------------------ actor */
+typedef struct pqlg_actor_s* pqlg_actor;
+typedef struct pqlg_env_s* pqlg_env;
+
+/* ActorCore(cfg, dims)  learners.hpp:54, learners.cpp:62-76, with the
+ * synthetic vectorised environment of SURVEY 8(d) in place of make_env.
+ * Env/noise streams use global env indices env_offset + i. */
+PQLG_API int pqlg_actor_create(const pqlg_config* cfg, const pqlg_task_dims* dims, void* stream,
+                               pqlg_actor* out);
+PQLG_API int pqlg_actor_destroy(pqlg_actor h);
+/* adopt_policy: PolicyHandle::adopt, equal-or-newer (learners.cpp:37-42) */
+PQLG_API int pqlg_actor_adopt_policy(pqlg_actor h, const float* flat_host, int64_t version);
+/* rollout_step() (learners.cpp:80-116): enqueues one step; *out receives
+ * device views of the StepSlice, valid until the next rollout_step. */
+PQLG_API int pqlg_actor_rollout_step(pqlg_actor h, pqlg_step_slice* out);
+/* n steps replayed from CUDA graphs (no slices returned). */
+PQLG_API int pqlg_actor_rollout_n(pqlg_actor h, int n);
+/* norm(): the running NormStats (host copies); synchronizes. */
+PQLG_API int pqlg_actor_norm(pqlg_actor h, int64_t* count, double* mean_host, double* m2_host);
+PQLG_API int pqlg_actor_policy_version(pqlg_actor h, int64_t* out);
+/* what: 0 obs [N x D] f32, 1 actions [N x A] f32, 2 noise streams [N] u64,
+ * 3 episode steps [N] i64, 4 env streams [N] u64, 5 policy params, 6 status */
+PQLG_API int pqlg_actor_read(pqlg_actor h, int what, void* host_out);
+PQLG_API int pqlg_actor_kernels_per_step(pqlg_actor h, int* out);
+
+/* The synthetic EnvBatch on its own (vecenv.hpp:44-81 contract). */
+PQLG_API int pqlg_env_create(int n_envs, int obs_dim, int act_dim, uint64_t seed,
+                             int max_episode_len, int env_offset, float low, float high,
+                             void* stream, pqlg_env* out);
+PQLG_API int pqlg_env_destroy(pqlg_env h);
+/* reset_all() (vecenv.cpp:53-60); writes the observations. */
+PQLG_API int pqlg_env_reset_all(pqlg_env h, float* obs_dev, int64_t ld);
+/* step(actions) (vecenv.cpp:84-106): next obs, terminal obs (valid on done
+ * rows), rewards, dones, truncated.  Non-finite action -> PQLG_ENONFINITE. */
+PQLG_API int pqlg_env_step(pqlg_env h, const float* act_dev, int64_t ld_act, float* next_obs_dev,
+                           float* terminal_obs_dev, float* rew_dev, uint8_t* done_dev,
+                           uint8_t* trunc_dev, int64_t ld_obs);
+
+/* explore::apply_noise (noise.hpp:56-72) on device, bit-exact: per-row
+ * polar-method normals from the row's SplitMix state (advanced in place). */
+PQLG_API int pqlg_k_apply_noise(float* act_dev, int64_t ld, int n, int act_dim,
+                                const float* sigma_dev, float low, float high,
+                                uint64_t* states_dev, void* stream);
+/* RunningNormalizer::update (normalizer.hpp:33-50, :73-83) on device; also
+ * writes the fp32 apply constants.  Synchronizes. */
+PQLG_API int pqlg_k_normalizer_update(int64_t* count_dev, double* mean_dev, double* m2_dev,
+                                      const float* batch_dev, int64_t ld, int rows, int dim,
+                                      float* mean_f_dev, float* inv_f_dev, void* stream);
 
 #ifdef __cplusplus
 }

@@ -52,7 +52,7 @@ class Config(C.Structure):
                 ("lr_critic", f64), ("warm_up", i64), ("sigma_min", f64), ("sigma_max", f64),
                 ("sigma_fixed", f64), ("reward_scale", f64), ("seed", u64), ("hidden", i32),
                 ("hidden_layers", i32), ("n_atoms", i32), ("vmin", f64), ("vmax", f64),
-                ("max_episode_len", i32), ("env_offset", i32)]
+                ("max_episode_len", i32), ("env_offset", i32), ("envs_total", i32)]
 
 
 class TaskDims(C.Structure):
@@ -103,6 +103,37 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_replay_fill_synthetic": (i32, [vp, u64, u64, f32, C.c_uint32]),
     "pqlg_k_gemm_tf32_repeat": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32,
                                       vp]),
+    "pqlg_plearner_create": (i32, [P(Config), P(TaskDims), u64, vp, P(vp)]),
+    "pqlg_plearner_destroy": (i32, [vp]),
+    "pqlg_plearner_adopt_critics": (i32, [vp, vp, vp, i64]),
+    "pqlg_plearner_adopt_norm": (i32, [vp, P(NormStats)]),
+    "pqlg_plearner_ingest": (i32, [vp, vp, i64, u64]),
+    "pqlg_plearner_ready": (i32, [vp, i64, P(i32)]),
+    "pqlg_plearner_update": (i32, [vp, P(f32)]),
+    "pqlg_plearner_update_n": (i32, [vp, i32]),
+    "pqlg_plearner_last_loss": (i32, [vp, P(f32)]),
+    "pqlg_plearner_snapshot": (i32, [vp, vp]),
+    "pqlg_plearner_get_params": (i32, [vp, i32, vp]),
+    "pqlg_plearner_set_params": (i32, [vp, i32, vp]),
+    "pqlg_plearner_param_count": (i32, [vp, i32, P(i64)]),
+    "pqlg_plearner_buffer_size": (i32, [vp, P(u64)]),
+    "pqlg_plearner_set_sampler": (i32, [vp, i32]),
+    "pqlg_plearner_kernels_per_update": (i32, [vp, P(i32)]),
+    "pqlg_actor_create": (i32, [P(Config), P(TaskDims), vp, P(vp)]),
+    "pqlg_actor_destroy": (i32, [vp]),
+    "pqlg_actor_adopt_policy": (i32, [vp, vp, i64]),
+    "pqlg_actor_rollout_step": (i32, [vp, P(StepSlice)]),
+    "pqlg_actor_rollout_n": (i32, [vp, i32]),
+    "pqlg_actor_norm": (i32, [vp, P(i64), vp, vp]),
+    "pqlg_actor_policy_version": (i32, [vp, P(i64)]),
+    "pqlg_actor_read": (i32, [vp, i32, vp]),
+    "pqlg_actor_kernels_per_step": (i32, [vp, P(i32)]),
+    "pqlg_env_create": (i32, [i32, i32, i32, u64, i32, i32, f32, f32, vp, P(vp)]),
+    "pqlg_env_destroy": (i32, [vp]),
+    "pqlg_env_reset_all": (i32, [vp, vp, i64]),
+    "pqlg_env_step": (i32, [vp, vp, i64, vp, vp, vp, vp, vp, i64]),
+    "pqlg_k_apply_noise": (i32, [vp, i64, i32, i32, vp, f32, f32, vp, vp]),
+    "pqlg_k_normalizer_update": (i32, [vp, vp, vp, vp, i64, i32, i32, vp, vp, vp]),
 }
 
 

@@ -1,0 +1,499 @@
+// Actor: ActorCore::rollout_step (proj/include/pql/runtime/learners.hpp:52-73,
+// proj/src/runtime/learners.cpp:62-116) on one B200, with the synthetic GPU
+// environment behind the EnvBatch contract (vecenv.hpp:44-81).
+//
+// One step = normalize (stats of step t-1) -> policy (tcgen05 GEMMs) whose
+// head epilogue squashes, adds the per-env mixed exploration noise and clamps
+// -> env step kernel (auto-reset, terminal obs, truncation) -> StepSlice
+// views -> running-normalizer update over the step's observations.
+#include <cmath>
+#include <memory>
+#include <random>
+#include <vector>
+
+#include "actor_kernels.cuh"
+#include "learner.h"
+
+namespace pqlg {
+
+// Host copy of the synthetic task's fixed coupling matrix (pql_oracle.c
+// orc_env_create): M[d][k] = 2 * (splitmix64(derive_seed(seed, env, 2^40) +
+// d*A + k) >> 11) * 2^-53 - 1.
+static std::vector<float> coupling_matrix(uint64_t seed, int D, int A) {
+  std::vector<float> M(static_cast<size_t>(D) * A);
+  const uint64_t mseed = rng::derive_seed(seed, rng::kEnv, 1ull << 40);
+  for (int d = 0; d < D; ++d)
+    for (int k = 0; k < A; ++k) {
+      const uint64_t u = rng::splitmix64(mseed + static_cast<uint64_t>(d) * A + k);
+      M[static_cast<size_t>(d) * A + k] =
+          static_cast<float>(static_cast<double>(u >> 11) * 0x1.0p-53 * 2.0 - 1.0);
+    }
+  return M;
+}
+
+// Synthetic EnvBatch on device (also exposed through pqlg_env_*).
+struct DeviceEnv {
+  int N, D, A, max_len, offset;
+  int64_t ld;
+  float low, high;
+  DevBuf<float> s, M;
+  DevBuf<int64_t> ep;
+  DevBuf<uint64_t> rng;
+
+  DeviceEnv(int n, int obs_dim, int act_dim, uint64_t seed, int max_episode_len, int env_offset,
+            float lo, float hi)
+      : N(n), D(obs_dim), A(act_dim), max_len(max_episode_len), offset(env_offset), low(lo),
+        high(hi) {
+    require(n >= 1, "make_env: n_envs must be >= 1");  // vecenv.cpp:57
+    require(max_episode_len >= 1, "env: max_episode_len must be >= 1");
+    ld = round_up(D, 4);
+    s.alloc(static_cast<size_t>(N) * ld);
+    auto m = coupling_matrix(seed, D, A);
+    M.alloc(m.size());
+    PQLG_CUDA(cudaMemcpy(M.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice));
+    ep.alloc(N);
+    std::vector<uint64_t> r(N);
+    for (int i = 0; i < N; ++i) r[i] = rng::derive_seed(seed, rng::kEnv, offset + i);
+    rng.alloc(N);
+    PQLG_CUDA(cudaMemcpy(rng.p, r.data(), N * 8, cudaMemcpyHostToDevice));
+  }
+  actor::EnvState view() const {
+    return actor::EnvState{s.p, ld, M.p, ep.p, rng.p, N, D, A, max_len, low, high};
+  }
+  void reset(float* obs, int64_t ld_obs, cudaStream_t st) {
+    actor::env_reset_kernel<<<(N + actor::kEnvWarps - 1) / actor::kEnvWarps,
+                              32 * actor::kEnvWarps, 0, st>>>(view(), obs, ld_obs, offset);
+    PQLG_CHECK_LAUNCH();
+    count_launch();
+  }
+  void step(const float* act, int64_t ld_act, const actor::StepOut& o, cudaStream_t st) {
+    const size_t smem = static_cast<size_t>(actor::kEnvWarps) * (D + A) * sizeof(float);
+    actor::env_step_kernel<<<(N + actor::kEnvWarps - 1) / actor::kEnvWarps,
+                             32 * actor::kEnvWarps, smem, st>>>(view(), act, ld_act, o);
+    PQLG_CHECK_LAUNCH();
+    count_launch();
+  }
+};
+
+class Actor {
+ public:
+  Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st);
+  ~Actor();
+  void adopt_policy(const float* flat, int64_t version, bool device);
+  void rollout_step(pqlg_step_slice* out);
+  void rollout_n(int n);
+  void norm(int64_t* count, double* mean, double* m2);
+  void read_state(int what, void* out);
+  int64_t policy_version() const { return version_; }
+  cudaStream_t stream() const { return stream_; }
+  int kernels_per_step();
+  int n_envs() const { return N_; }
+
+ private:
+  void build();
+  void enqueue(int cur);
+
+  pqlg_config cfg_;
+  pqlg_task_dims dims_;
+  cudaStream_t stream_;
+  cudaStream_t owned_stream_ = nullptr;
+  int N_, D_, A_, Ap_, H_, nh_;
+  int64_t Dp_;
+  NetShape pnet_;
+  int64_t version_ = 0;
+  int cur_ = 0;
+
+  std::unique_ptr<DeviceEnv> env_;
+  DevBuf<float> obs_[2], boot_, rew_, act_, Xn_;
+  DevBuf<uint8_t> term_, trunc_;
+  DevBuf<float> pol_;
+  WeightMirror head_;
+  std::vector<DevBuf<float>> pact_;
+  DevBuf<uint64_t> noise_rng_;
+  DevBuf<float> sigma_;
+  DevBuf<int64_t> count_;
+  DevBuf<double> mean_, m2_, cmean_, cm2_, ccount_;
+  DevBuf<float> mean_f_, inv_f_;
+  DevBuf<int> identity_;
+  DevBuf<uint32_t> status_;
+  std::vector<mlp::Step> policy_steps_;
+  cudaGraphExec_t graph_[2] = {nullptr, nullptr};
+  int kps_ = 0;
+};
+
+Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st)
+    : cfg_(cfg), dims_(dims), stream_(st) {
+  if (!stream_) {
+    PQLG_CUDA(cudaStreamCreateWithFlags(&owned_stream_, cudaStreamNonBlocking));
+    stream_ = owned_stream_;
+  }
+  require(cfg.algo == PQLG_ALGO_DDPG || cfg.algo == PQLG_ALGO_C51, "actor: unknown algo");
+  require(cfg.hidden_layers >= 1 && cfg.hidden >= 32 && cfg.hidden % 32 == 0,
+          "actor: hidden width must be a multiple of 32");
+  N_ = cfg.n_envs;
+  D_ = dims.obs_dim;
+  A_ = dims.act_dim;
+  Ap_ = static_cast<int>(round_up(A_, 4));
+  H_ = cfg.hidden;
+  nh_ = cfg.hidden_layers;
+  Dp_ = round_up(D_, 4);
+  std::vector<int> ps{D_};
+  for (int i = 0; i < nh_; ++i) ps.push_back(H_);
+  ps.push_back(A_);
+  pnet_ = NetShape::make(ps);
+
+  // policy: PolicyHandle::create with make_rng(seed, init, 0) (learners.cpp:69)
+  std::mt19937_64 prng(rng::derive_seed(cfg.seed, rng::kInit, 0));
+  std::vector<float> pol;
+  init_orthogonal(pnet_, pol, prng, static_cast<float>(std::sqrt(2.0)), 1e-2f);
+  pol_.alloc(pnet_.params);
+  PQLG_CUDA(cudaMemcpy(pol_.p, pol.data(), pol.size() * 4, cudaMemcpyHostToDevice));
+
+  // exploration: build_schedule over the global env count (noise.hpp:23-42;
+  // a sharded actor takes its slice of the one global schedule), per-env
+  // SplitMix streams derive_seed(seed, noise, global i) (learners.cpp:74-75)
+  const int n_total = cfg.envs_total > 0 ? cfg.envs_total : N_;
+  require(cfg.env_offset + N_ <= n_total, "actor: env_offset + n_envs exceeds envs_total");
+  std::vector<float> sig(N_);
+  for (int i = 0; i < N_; ++i) {
+    const int gi = cfg.env_offset + i;
+    const float smin = static_cast<float>(cfg.sigma_min), smax = static_cast<float>(cfg.sigma_max);
+    float v;
+    if (cfg.sigma_fixed >= 0.0) v = static_cast<float>(cfg.sigma_fixed);  // build_fixed_schedule
+    else if (n_total == 1 || gi == 0) v = smin;
+    else if (gi == n_total - 1) v = smax;
+    else {
+      const double lo = smin, span = static_cast<double>(smax) - smin;
+      v = static_cast<float>(lo + (static_cast<double>(gi) / (n_total - 1)) * span);
+    }
+    sig[i] = v;
+  }
+  sigma_.alloc(N_);
+  PQLG_CUDA(cudaMemcpy(sigma_.p, sig.data(), N_ * 4, cudaMemcpyHostToDevice));
+  std::vector<uint64_t> nr(N_);
+  for (int i = 0; i < N_; ++i) nr[i] = rng::derive_seed(cfg.seed, rng::kNoise, cfg.env_offset + i);
+  noise_rng_.alloc(N_);
+  PQLG_CUDA(cudaMemcpy(noise_rng_.p, nr.data(), N_ * 8, cudaMemcpyHostToDevice));
+
+  // environment + initial observations (make_env -> reset_all, learners.cpp:66-68)
+  env_ = std::make_unique<DeviceEnv>(N_, D_, A_, cfg.seed, cfg.max_episode_len, cfg.env_offset,
+                                     dims.low, dims.high);
+  for (auto& o : obs_) o.alloc(static_cast<size_t>(N_) * Dp_);
+  boot_.alloc(static_cast<size_t>(N_) * Dp_);
+  rew_.alloc(N_);
+  term_.alloc(N_);
+  trunc_.alloc(N_);
+  act_.alloc(static_cast<size_t>(N_) * Ap_);
+  Xn_.alloc(static_cast<size_t>(N_) * Dp_);
+  env_->reset(obs_[0].p, Dp_, stream_);
+
+  // normalizer (count 0 -> identity)
+  count_.alloc(1);
+  mean_.alloc(D_);
+  m2_.alloc(D_);
+  mean_f_.alloc(D_);
+  inv_f_.alloc(D_);
+  identity_.alloc(1);
+  const int one = 1;
+  PQLG_CUDA(cudaMemcpy(identity_.p, &one, 4, cudaMemcpyHostToDevice));
+  const int chunks = (N_ + actor::kNormChunk - 1) / actor::kNormChunk;
+  cmean_.alloc(static_cast<size_t>(chunks) * D_);
+  cm2_.alloc(static_cast<size_t>(chunks) * D_);
+  ccount_.alloc(chunks);
+  status_.alloc(1);
+  build();
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+}
+
+Actor::~Actor() {
+  for (auto& g : graph_)
+    if (g) cudaGraphExecDestroy(g);
+  if (owned_stream_) {
+    cudaStreamSynchronize(owned_stream_);
+    cudaStreamDestroy(owned_stream_);
+  }
+}
+
+void Actor::build() {
+  const int N = N_, D = D_, A = A_, H = H_, nh = nh_;
+  const int bnH = mlp::bn_for(H);
+  pact_.resize(nh);
+  for (auto& b : pact_) b.alloc(static_cast<size_t>(N) * H);
+  const float* in = Xn_.p;
+  int64_t ld = Dp_;
+  int K = D;
+  for (int l = 0; l < nh; ++l) {
+    epi::Hidden e{};
+    e.bias[0] = e.bias[1] = pol_.p + pnet_.b_off[l];
+    e.bn = bnH;
+    e.M = N;
+    e.N = H;
+    e.store = 1;
+    const float* W = pol_.p + pnet_.w_off[l];
+    policy_steps_.push_back(mlp::fwd(in, in, ld, W, W, N, H, K, 1, e, 0, pact_[l].p, pact_[l].p, H));
+    in = pact_[l].p;
+    ld = H;
+    K = H;
+  }
+  // DeterministicPolicy::act + apply_noise (learners.cpp:96-98), fused
+  epi::PolicyHead ph{};
+  ph.bias = pol_.p + pnet_.b_off[nh];
+  ph.act = act_.p;
+  ph.ld_act = Ap_;
+  ph.M = N;
+  ph.A = A;
+  ph.mid = (dims_.low + dims_.high) / 2.0f;
+  ph.half = (dims_.high - dims_.low) / 2.0f;
+  ph.noise_state = noise_rng_.p;
+  ph.sigma = sigma_.p;
+  ph.low = dims_.low;
+  ph.high = dims_.high;
+  head_.init(pol_.p + pnet_.w_off[nh], H, A);
+  head_.refresh(stream_);
+  const float* W = head_.ptr();
+  policy_steps_.push_back(mlp::fwd(in, in, ld, W, W, N, A, H, 1, ph, head_.stride()));
+}
+
+void Actor::enqueue(int cur) {
+  cudaStream_t st = stream_;
+  const int N = N_, D = D_;
+  const float* obs = obs_[cur].p;
+  // obs_norm = normalizer_.apply(obs_)  (stats of previous steps)
+  actor::normalize_kernel<<<4 * mlp::kSMs, 256, 0, st>>>(obs, Dp_, Xn_.p, Dp_, mean_f_.p,
+                                                         inv_f_.p, identity_.p, N, D);
+  PQLG_CHECK_LAUNCH();
+  count_launch();
+  for (auto& s : policy_steps_) s(st);
+  // env_->step(actions)
+  actor::StepOut o{obs_[1 - cur].p, boot_.p, rew_.p, term_.p, trunc_.p, nullptr, Dp_, status_.p};
+  env_->step(act_.p, Ap_, o, st);
+  // normalizer_.update(obs_)  (after acting, learners.cpp:113)
+  const int chunks = (N + actor::kNormChunk - 1) / actor::kNormChunk;
+  actor::norm_chunk_kernel<<<chunks, 256, 0, st>>>(obs, Dp_, N, D, cmean_.p, cm2_.p, ccount_.p);
+  PQLG_CHECK_LAUNCH();
+  actor::NormState ns{count_.p, mean_.p, m2_.p, mean_f_.p, inv_f_.p, identity_.p};
+  actor::norm_merge_kernel<<<1, 256, 0, st>>>(cmean_.p, cm2_.p, ccount_.p, chunks, D, N, ns);
+  PQLG_CHECK_LAUNCH();
+  count_launch(2);
+}
+
+int Actor::kernels_per_step() {
+  if (kps_ == 0) {
+    const uint64_t before = g_launches.load();
+    cudaGraph_t g;
+    PQLG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    enqueue(0);
+    PQLG_CUDA(cudaStreamEndCapture(stream_, &g));
+    cudaGraphDestroy(g);
+    kps_ = static_cast<int>(g_launches.load() - before);
+    g_launches.fetch_sub(kps_);
+  }
+  return kps_;
+}
+
+void Actor::rollout_step(pqlg_step_slice* out) {
+  const int cur = cur_;
+  enqueue(cur);
+  if (out) {
+    out->obs = obs_[cur].p;
+    out->act = act_.p;
+    out->boot_obs = boot_.p;
+    out->rew = rew_.p;
+    out->term = term_.p;
+    out->trunc = trunc_.p;
+    out->ld_obs = Dp_;
+    out->ld_act = Ap_;
+  }
+  cur_ = 1 - cur;
+}
+
+void Actor::rollout_n(int n) {
+  for (int c = 0; c < 2; ++c) {
+    if (graph_[c]) continue;
+    kernels_per_step();
+    cudaGraph_t g;
+    PQLG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    enqueue(c);
+    PQLG_CUDA(cudaStreamEndCapture(stream_, &g));
+    g_launches.fetch_sub(kps_);
+    PQLG_CUDA(cudaGraphInstantiate(&graph_[c], g, 0));
+    cudaGraphDestroy(g);
+  }
+  for (int i = 0; i < n; ++i) {
+    PQLG_CUDA(cudaGraphLaunch(graph_[cur_], stream_));
+    cur_ = 1 - cur_;
+  }
+  count_launch(static_cast<uint64_t>(n) * kps_);
+}
+
+void Actor::adopt_policy(const float* flat, int64_t version, bool device) {
+  if (version < version_) return;  // PolicyHandle::adopt (learners.cpp:37-42)
+  PQLG_CUDA(cudaMemcpyAsync(pol_.p, flat, pnet_.params * 4,
+                            device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream_));
+  head_.refresh(stream_);
+  if (!device) PQLG_CUDA(cudaStreamSynchronize(stream_));
+  version_ = version;
+}
+
+void Actor::norm(int64_t* count, double* mean, double* m2) {
+  PQLG_CUDA(cudaMemcpyAsync(count, count_.p, 8, cudaMemcpyDeviceToHost, stream_));
+  if (mean) PQLG_CUDA(cudaMemcpyAsync(mean, mean_.p, D_ * 8, cudaMemcpyDeviceToHost, stream_));
+  if (m2) PQLG_CUDA(cudaMemcpyAsync(m2, m2_.p, D_ * 8, cudaMemcpyDeviceToHost, stream_));
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// what: 0 current obs [N x D] f32, 1 last actions [N x A] f32, 2 noise stream
+// states [N] u64, 3 env episode steps [N] i64, 4 env stream states [N] u64,
+// 5 policy params, 6 status word (u32)
+void Actor::read_state(int what, void* out) {
+  auto st = stream_;
+  switch (what) {
+    case 0:
+      PQLG_CUDA(cudaMemcpy2DAsync(out, D_ * 4, obs_[cur_].p, Dp_ * 4, D_ * 4, N_,
+                                  cudaMemcpyDeviceToHost, st));
+      break;
+    case 1:
+      PQLG_CUDA(cudaMemcpy2DAsync(out, A_ * 4, act_.p, Ap_ * 4, A_ * 4, N_,
+                                  cudaMemcpyDeviceToHost, st));
+      break;
+    case 2: PQLG_CUDA(cudaMemcpyAsync(out, noise_rng_.p, N_ * 8, cudaMemcpyDeviceToHost, st)); break;
+    case 3: PQLG_CUDA(cudaMemcpyAsync(out, env_->ep.p, N_ * 8, cudaMemcpyDeviceToHost, st)); break;
+    case 4: PQLG_CUDA(cudaMemcpyAsync(out, env_->rng.p, N_ * 8, cudaMemcpyDeviceToHost, st)); break;
+    case 5:
+      PQLG_CUDA(cudaMemcpyAsync(out, pol_.p, pnet_.params * 4, cudaMemcpyDeviceToHost, st));
+      break;
+    case 6: PQLG_CUDA(cudaMemcpyAsync(out, status_.p, 4, cudaMemcpyDeviceToHost, st)); break;
+    default: throw Error(PQLG_EINVAL, "actor_read: what must be 0..6");
+  }
+  PQLG_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace pqlg
+
+// ------------------------------------------------------------------ C ABI
+struct pqlg_actor_s {
+  std::unique_ptr<pqlg::Actor> a;
+};
+struct pqlg_env_s {
+  std::unique_ptr<pqlg::DeviceEnv> e;
+  pqlg::DevBuf<uint32_t> status;
+  cudaStream_t stream;
+};
+
+using namespace pqlg;
+
+extern "C" {
+
+int pqlg_actor_create(const pqlg_config* cfg, const pqlg_task_dims* dims, void* stream,
+                      pqlg_actor* out) {
+  return guarded([&] {
+    require(cfg && dims && out, "actor_create: null argument");
+    auto h = std::make_unique<pqlg_actor_s>();
+    h->a = std::make_unique<Actor>(*cfg, *dims, static_cast<cudaStream_t>(stream));
+    *out = h.release();
+  });
+}
+
+int pqlg_actor_destroy(pqlg_actor h) {
+  return guarded([&] { delete h; });
+}
+
+int pqlg_actor_adopt_policy(pqlg_actor h, const float* flat, int64_t version) {
+  return guarded([&] { h->a->adopt_policy(flat, version, false); });
+}
+
+int pqlg_actor_rollout_step(pqlg_actor h, pqlg_step_slice* out) {
+  return guarded([&] { h->a->rollout_step(out); });
+}
+
+int pqlg_actor_rollout_n(pqlg_actor h, int n) {
+  return guarded([&] { h->a->rollout_n(n); });
+}
+
+int pqlg_actor_norm(pqlg_actor h, int64_t* count, double* mean, double* m2) {
+  return guarded([&] { h->a->norm(count, mean, m2); });
+}
+
+int pqlg_actor_policy_version(pqlg_actor h, int64_t* out) {
+  return guarded([&] { *out = h->a->policy_version(); });
+}
+
+int pqlg_actor_read(pqlg_actor h, int what, void* out) {
+  return guarded([&] { h->a->read_state(what, out); });
+}
+
+int pqlg_actor_kernels_per_step(pqlg_actor h, int* out) {
+  return guarded([&] { *out = h->a->kernels_per_step(); });
+}
+
+int pqlg_env_create(int n_envs, int obs_dim, int act_dim, uint64_t seed, int max_episode_len,
+                    int env_offset, float low, float high, void* stream, pqlg_env* out) {
+  return guarded([&] {
+    auto h = std::make_unique<pqlg_env_s>();
+    h->e = std::make_unique<DeviceEnv>(n_envs, obs_dim, act_dim, seed, max_episode_len,
+                                       env_offset, low, high);
+    h->status.alloc(1);
+    h->stream = static_cast<cudaStream_t>(stream);
+    *out = h.release();
+  });
+}
+
+int pqlg_env_destroy(pqlg_env h) {
+  return guarded([&] { delete h; });
+}
+
+int pqlg_env_reset_all(pqlg_env h, float* obs_dev, int64_t ld) {
+  return guarded([&] { h->e->reset(obs_dev, ld > 0 ? ld : h->e->D, h->stream); });
+}
+
+int pqlg_env_step(pqlg_env h, const float* act_dev, int64_t ld_act, float* next_obs_dev,
+                  float* terminal_obs_dev, float* rew_dev, uint8_t* done_dev, uint8_t* trunc_dev,
+                  int64_t ld_obs) {
+  return guarded([&] {
+    auto& e = *h->e;
+    // term is (done && !trunc); the EnvBatch contract reports dones (vecenv.hpp:23-29)
+    DevBuf<uint8_t> term(e.N);
+    actor::StepOut o{next_obs_dev, terminal_obs_dev, rew_dev, term.p, trunc_dev, done_dev,
+                     ld_obs > 0 ? ld_obs : e.D, h->status.p};
+    e.step(act_dev, ld_act > 0 ? ld_act : e.A, o, h->stream);
+    uint32_t st = 0;
+    PQLG_CUDA(cudaMemcpyAsync(&st, h->status.p, 4, cudaMemcpyDeviceToHost, h->stream));
+    PQLG_CUDA(cudaStreamSynchronize(h->stream));
+    if (st) {
+      PQLG_CUDA(cudaMemset(h->status.p, 0, 4));
+      throw Error(PQLG_ENONFINITE, "step: non-finite action (upstream divergence)");
+    }
+  });
+}
+
+int pqlg_k_apply_noise(float* act_dev, int64_t ld, int n, int act_dim, const float* sigma_dev,
+                       float low, float high, uint64_t* states_dev, void* stream) {
+  return guarded([&] {
+    actor::noise_kernel<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        act_dev, ld > 0 ? ld : act_dim, n, act_dim, sigma_dev, low, high, states_dev);
+    PQLG_CHECK_LAUNCH();
+    count_launch();
+  });
+}
+
+int pqlg_k_normalizer_update(int64_t* count_dev, double* mean_dev, double* m2_dev,
+                             const float* batch_dev, int64_t ld, int rows, int dim,
+                             float* mean_f_dev, float* inv_f_dev, void* stream) {
+  return guarded([&] {
+    auto st = static_cast<cudaStream_t>(stream);
+    const int chunks = (rows + actor::kNormChunk - 1) / actor::kNormChunk;
+    DevBuf<double> cm(static_cast<size_t>(chunks) * dim), c2(static_cast<size_t>(chunks) * dim),
+        cc(chunks);
+    DevBuf<int> ident(1);
+    actor::norm_chunk_kernel<<<chunks, 256, 0, st>>>(batch_dev, ld > 0 ? ld : dim, rows, dim,
+                                                     cm.p, c2.p, cc.p);
+    PQLG_CHECK_LAUNCH();
+    actor::NormState ns{count_dev, mean_dev, m2_dev, mean_f_dev, inv_f_dev, ident.p};
+    actor::norm_merge_kernel<<<1, 256, 0, st>>>(cm.p, c2.p, cc.p, chunks, dim, rows, ns);
+    PQLG_CHECK_LAUNCH();
+    PQLG_CUDA(cudaStreamSynchronize(st));
+    count_launch(2);
+  });
+}
+
+}  // extern "C"

@@ -211,4 +211,63 @@ static __global__ void __launch_bounds__(kHeadThreads)
   }
 }
 
+// Input gradient through the value head only (ddpg_actor_loss, critics
+// frozen: mlp.hpp:187-201): G[b,i] = up[b] * w[i] * [post[b,i] > 0] with the
+// ReLU mask taken from the forward pass's bitmask.  One thread per element.
+struct HeadInputGradArgs {
+  const float* up;         // [2][B]
+  const uint32_t* mask[2]; // [B x H/32]
+  const float* w[2];       // [H]
+  float* G[2];             // [B x H]
+  int B, H;
+};
+
+static __global__ void head_input_grad_kernel(const __grid_constant__ HeadInputGradArgs a) {
+  const int k = blockIdx.y;
+  const int64_t n = static_cast<int64_t>(a.B) * a.H;
+  const int words = a.H >> 5;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = e / a.H;
+    const int i = static_cast<int>(e % a.H);
+    const uint32_t bits = a.mask[k][b * words + (i >> 5)];
+    a.G[k][e] = ((bits >> (i & 31)) & 1u) ? __fmul_rn(a.up[k * a.B + b], a.w[k][i]) : 0.0f;
+  }
+}
+
+// DeterministicPolicy::backward head (policy.hpp:41-51) fed by the actor
+// gradient: dact = din1[:, obs:] + din2[:, obs:] (ddpg.hpp:112-115), then
+// dy = dact * half * (1 - t^2) with t = tanh(y) from the forward; plus the
+// head-bias gradient partials db[tile][a] = sum over the tile's rows of dy.
+struct PolicyHeadBwdArgs {
+  const float* dact1;  // [B x lda]
+  const float* dact2;
+  int64_t ld_dact;
+  const float* t;      // tanh(y) [B x ld_t]
+  int64_t ld_t;
+  float* dy;           // [B x ld_dy]
+  int64_t ld_dy;
+  float* db_part;      // [tiles][A]
+  float half;
+  int B, A, rows_per_tile;
+};
+
+static __global__ void policy_head_backward_kernel(const __grid_constant__ PolicyHeadBwdArgs a) {
+  const int tile = blockIdx.x;
+  const int b0 = tile * a.rows_per_tile;
+  const int b1 = min(b0 + a.rows_per_tile, a.B);
+  for (int c = threadIdx.x; c < a.A; c += blockDim.x) {
+    float db = 0.0f;
+    for (int b = b0; b < b1; ++b) {
+      const float da = __fadd_rn(a.dact1[static_cast<int64_t>(b) * a.ld_dact + c],
+                                 a.dact2[static_cast<int64_t>(b) * a.ld_dact + c]);
+      const float t = a.t[static_cast<int64_t>(b) * a.ld_t + c];
+      const float g = __fmul_rn(__fmul_rn(da, a.half), __fsub_rn(1.0f, __fmul_rn(t, t)));
+      a.dy[static_cast<int64_t>(b) * a.ld_dy + c] = g;
+      db = __fadd_rn(db, g);
+    }
+    a.db_part[static_cast<int64_t>(tile) * a.A + c] = db;
+  }
+}
+
 }  // namespace pqlg::critic

@@ -92,4 +92,80 @@ class VLearner {
   int kpu_ = 0;
 };
 
+// PolicyLearnerCore (learners.hpp:110-139): the actor gradient through the
+// frozen online critic replicas (ddpg_actor_loss, ddpg.hpp:86-118), clip +
+// Adam on the policy (learners.cpp:239-270).
+class PLearner {
+ public:
+  PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t init_seed,
+           cudaStream_t st);
+  ~PLearner();
+
+  void adopt_critics(const float* q1_host, const float* q2_host, int64_t version);
+  void adopt_critics_device(const float* q1_dev, const float* q2_dev, int64_t version);
+  void adopt_norm(int64_t count, const double* mean, const double* m2);
+  void ingest(const float* states_dev, int64_t ld, uint64_t n);
+  bool ready(int64_t c_a);
+  float update();
+  void update_n(int n);
+  float last_loss();
+  void get_params(int which, float* out);
+  void set_params(int which, const float* flat_host);
+  int64_t param_count(int which) const;
+  void set_mt_mode(bool on) { mt_mode_ = on; }
+  int kernels_per_update();
+  uint64_t buffer_size() { return states_->size(); }
+  const float* policy_dev() const { return pol_.p; }
+  int obs_dim() const { return D_; }
+  cudaStream_t stream() const { return stream_; }
+  int64_t critic_version() const { return critic_version_; }
+
+ private:
+  void build_update();
+  void enqueue();
+  int check_status();
+
+  pqlg_config cfg_;
+  pqlg_task_dims dims_;
+  cudaStream_t stream_;
+  cudaStream_t owned_stream_ = nullptr;
+  int D_, A_, Ap_, H_, nh_, B_, Kp_;
+  NetShape qnet_, pnet_;
+  int64_t Ps_ = 0;
+  int64_t critic_version_ = 0;
+
+  DevBuf<float> pol_, m_, v_, grads_, q_;
+  WeightMirror head_;
+  std::unique_ptr<DeviceStates> states_;
+  DeviceNorm norm_;
+  DevBuf<replay::SamplerState> sampler_;
+  bool mt_mode_ = false;
+  std::mt19937_64 mt_;
+  DevBuf<uint64_t> idx_;
+  std::vector<uint64_t> idx_host_;
+  DevBuf<int64_t> step_;
+  DevBuf<float2> bc_;
+  DevBuf<uint32_t> status_;
+  DevBuf<float> loss_;
+
+  DevBuf<float> X_, T_, dy_, up_, part_;
+  std::vector<DevBuf<float>> pact_, Gp_;
+  std::vector<DevBuf<uint32_t>> pmask_;
+  std::array<std::vector<DevBuf<float>>, 2> cact_, Gc_;
+  std::array<std::vector<DevBuf<uint32_t>>, 2> cmask_;
+  std::array<DevBuf<float>, 2> dact_;
+  DevBuf<double> block_loss_;
+  DevBuf<unsigned int> loss_counter_;
+  std::vector<DevBuf<float>> wpart_, colsum_;
+  std::vector<int> wsplits_;
+  DevBuf<float> head_db_;
+  DevBuf<double> block_sq_;
+  DevBuf<unsigned int> fin_counter_;
+  DevBuf<float> scale_;
+
+  std::vector<mlp::Step> steps_;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  int kpu_ = 0;
+};
+
 }  // namespace pqlg

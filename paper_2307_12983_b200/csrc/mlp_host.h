@@ -107,7 +107,9 @@ Step dgrad(const float* G0, const float* G1, int64_t ldg, const float* W0, const
 // TMA-stored to W[(group*splits + split)][M][N] (N % 4 == 0).
 template <class Epi>
 Step wgrad(const float* H0, const float* H1, int64_t ldh, const float* G0, const float* G1,
-           int64_t ldg, int M, int N, int K, int groups, int splits, Epi epi, float* W) {
+           int64_t ldg, int M, int N, int K, int groups, int splits, Epi epi, float* W,
+           int64_t ldw_part = 0) {
+  if (ldw_part == 0) ldw_part = N;
   Step step;
   with_bn(N, [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
@@ -118,8 +120,9 @@ Step wgrad(const float* H0, const float* H1, int64_t ldh, const float* G0, const
     ops.b[1] = groups > 1 ? gemm::map_b(G1, N, K, ldg, true, BN, true) : ops.b[0];
     const gemm::Problem p = gemm::make_problem(M, N, K, splits);
     require(p.splits == splits, "wgrad: split count must divide the k tiles evenly");
-    ops.d[0] = ops.d[1] = make_tmap_3d(W, N, M, static_cast<uint64_t>(groups) * splits, N,
-                                       static_cast<uint64_t>(M) * N, 32, 32, Swz::k128);
+    ops.d[0] = ops.d[1] = make_tmap_3d(W, N, M, static_cast<uint64_t>(groups) * splits,
+                                       ldw_part, static_cast<uint64_t>(M) * ldw_part, 32, 32,
+                                       Swz::k128);
     step = [ops, p, groups, epi](cudaStream_t st) {
       gemm::launch<BN, true, true>(ops, p, groups, epi, st);
     };

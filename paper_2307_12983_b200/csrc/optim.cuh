@@ -26,6 +26,8 @@ struct Segment {
   int64_t group_stride;  // src advance per group
   int n_terms;
   int64_t stride;
+  int64_t cols = 0;      // > 0: src rows are padded, src = (j / cols) * ld_src + j % cols
+  int64_t ld_src = 0;
 };
 
 struct FinalizeArgs {
@@ -53,7 +55,8 @@ static __global__ void __launch_bounds__(kFinalizeThreads)
     while (s + 1 < a.n_seg && i >= a.seg[s + 1].dst) ++s;
     const Segment& sg = a.seg[s];
     const int64_t j = i - sg.dst;
-    const float* src = sg.src + group * sg.group_stride + j;
+    const int64_t js = sg.cols > 0 ? (j / sg.cols) * sg.ld_src + j % sg.cols : j;
+    const float* src = sg.src + group * sg.group_stride + js;
     // terms summed in ascending order; loads issued 8 at a time so the
     // latency of the (L2-resident) partials overlaps
     float acc = src[0];

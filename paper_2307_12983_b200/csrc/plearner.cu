@@ -1,0 +1,602 @@
+// P-learner: PolicyLearnerCore (proj/include/pql/runtime/learners.hpp:110-139,
+// proj/src/runtime/learners.cpp:202-274) on one B200.
+//
+// One update = state sample (+ normalize) -> policy forward (masks + tanh kept)
+// -> twin online critic replicas forward (masks only) -> pick min critic ->
+// input gradient back through the picked critic (dgrad chain; the layer-0
+// dgrad only for the action columns) -> policy head backward -> policy
+// wgrad/dgrad chain -> fixed-order gradient reduction + fp64 norm -> clip +
+// Adam (no Polyak for the policy).
+#include <memory>
+#include <random>
+#include <vector>
+
+#include "critic_kernels.cuh"
+#include "learner.h"
+#include "optim.cuh"
+
+namespace pqlg {
+
+PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t init_seed,
+                   cudaStream_t st)
+    : cfg_(cfg), dims_(dims), stream_(st) {
+  if (!stream_) {
+    PQLG_CUDA(cudaStreamCreateWithFlags(&owned_stream_, cudaStreamNonBlocking));
+    stream_ = owned_stream_;
+  }
+  require(cfg.algo == PQLG_ALGO_DDPG, "plearner: the C51 actor objective is not built yet");
+  require(cfg.hidden_layers >= 1 && cfg.hidden >= 32 && cfg.hidden % 32 == 0,
+          "plearner: hidden width must be a multiple of 32");
+  D_ = dims.obs_dim;
+  A_ = dims.act_dim;
+  Ap_ = static_cast<int>(round_up(A_, 4));
+  H_ = cfg.hidden;
+  nh_ = cfg.hidden_layers;
+  B_ = cfg.batch_size;
+  Kp_ = static_cast<int>(round_up(D_ + A_, 4));
+  require(A_ <= 32, "plearner: act_dim > 32 not supported by the policy head kernels");
+
+  std::vector<int> qs{D_ + A_}, ps{D_};
+  for (int i = 0; i < nh_; ++i) {
+    qs.push_back(H_);
+    ps.push_back(H_);
+  }
+  qs.push_back(1);
+  ps.push_back(A_);
+  qnet_ = NetShape::make(qs);
+  pnet_ = NetShape::make(ps);
+  Ps_ = round_up(qnet_.params, 64);
+
+  // critics_ (learners.cpp:202-205): CriticPair::create with the caller's
+  // init_rng; the policy from make_rng(seed, init, 0) (learners.cpp:214).
+  std::mt19937_64 init_rng(init_seed);
+  std::vector<float> q1, q2, pol;
+  init_orthogonal(qnet_, q1, init_rng, static_cast<float>(std::sqrt(2.0)), 1.0f);
+  init_orthogonal(qnet_, q2, init_rng, static_cast<float>(std::sqrt(2.0)), 1.0f);
+  std::mt19937_64 prng(rng::derive_seed(cfg.seed, rng::kInit, 0));
+  init_orthogonal(pnet_, pol, prng, static_cast<float>(std::sqrt(2.0)), 1e-2f);
+  q_.alloc(2 * Ps_);
+  pol_.alloc(pnet_.params);
+  m_.alloc(pnet_.params);
+  v_.alloc(pnet_.params);
+  grads_.alloc(pnet_.params);
+  PQLG_CUDA(cudaMemcpy(q_.p, q1.data(), q1.size() * 4, cudaMemcpyHostToDevice));
+  PQLG_CUDA(cudaMemcpy(q_.p + Ps_, q2.data(), q2.size() * 4, cudaMemcpyHostToDevice));
+  PQLG_CUDA(cudaMemcpy(pol_.p, pol.data(), pol.size() * 4, cudaMemcpyHostToDevice));
+
+  states_ = std::make_unique<DeviceStates>(cfg.buffer_capacity, D_, stream_);
+  norm_.init(D_);
+  sampler_.alloc(1);
+  replay::SamplerState s0{rng::derive_seed(cfg.seed, rng::kSample, 2), 0, 0, 0};
+  PQLG_CUDA(cudaMemcpy(sampler_.p, &s0, sizeof(s0), cudaMemcpyHostToDevice));
+  mt_.seed(rng::derive_seed(cfg.seed, rng::kSample, 2));
+  idx_.alloc(B_);
+  idx_host_.resize(B_);
+  step_.alloc(1);
+  auto tab = mlp::adam_bias_table(0.9, 0.999);
+  bc_.alloc(tab.size());
+  PQLG_CUDA(cudaMemcpy(bc_.p, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  status_.alloc(1);
+  loss_.alloc(1);
+  build_update();
+  PQLG_CUDA(cudaDeviceSynchronize());
+}
+
+PLearner::~PLearner() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (owned_stream_) {
+    cudaStreamSynchronize(owned_stream_);
+    cudaStreamDestroy(owned_stream_);
+  }
+}
+
+namespace {
+// Small row-wise kernels of the update (launched through closures).
+__global__ void step_increment_kernel(int64_t* step) { *step += 1; }
+}  // namespace
+
+void PLearner::build_update() {
+  const int B = B_, D = D_, A = A_, H = H_, nh = nh_, K0 = D + A;
+  const int nt = mlp::n_tiles(H);
+  const int bnH = mlp::bn_for(H);
+  const int mt = (B + 127) / 128;
+  const int wpr = H / 32;
+  const float* q[2] = {q_.p, q_.p + Ps_};
+
+  X_.alloc(static_cast<size_t>(B) * Kp_);
+  T_.alloc(static_cast<size_t>(B) * Ap_);
+  dy_.alloc(static_cast<size_t>(B) * Ap_);
+  up_.alloc(2ull * B);
+  part_.alloc(2ull * nt * B);
+  pact_.resize(nh);
+  pmask_.resize(nh);
+  Gp_.resize(nh);
+  for (int l = 0; l < nh; ++l) {
+    pact_[l].alloc(static_cast<size_t>(B) * H);
+    pmask_[l].alloc(static_cast<size_t>(B) * wpr);
+    Gp_[l].alloc(static_cast<size_t>(B) * H);
+  }
+  for (int k = 0; k < 2; ++k) {
+    cact_[k].resize(nh);
+    cmask_[k].resize(nh);
+    Gc_[k].resize(nh);
+    for (int l = 0; l < nh; ++l) {
+      cact_[k][l].alloc(l + 1 < nh ? static_cast<size_t>(B) * H : 0);
+      cmask_[k][l].alloc(static_cast<size_t>(B) * wpr);
+      Gc_[k][l].alloc(static_cast<size_t>(B) * H);
+    }
+    dact_[k].alloc(static_cast<size_t>(B) * Ap_);
+  }
+  const int loss_blocks = (B + critic::kRowThreads - 1) / critic::kRowThreads;
+  block_loss_.alloc(loss_blocks);
+  loss_counter_.alloc(1);
+
+  // ------------------------------------------------- sample + normalize
+  steps_.push_back([this, B](cudaStream_t st) {
+    const uint64_t* idx = mt_mode_ ? idx_.p : nullptr;
+    launch_state_sample(*states_, norm_.view(), X_.p, Kp_, sampler_.p, idx, B, st);
+    step_increment_kernel<<<1, 1, 0, st>>>(step_.p);
+    PQLG_CHECK_LAUNCH();
+    count_launch();
+  });
+
+  // -------------------------------------------------------- policy forward
+  {
+    const float* in = X_.p;
+    int64_t ld = Kp_;
+    int K = D;
+    for (int l = 0; l < nh; ++l) {
+      epi::Hidden e{};
+      e.bias[0] = e.bias[1] = pol_.p + pnet_.b_off[l];
+      e.mask[0] = e.mask[1] = pmask_[l].p;
+      e.ld_mask = wpr;
+      e.bn = bnH;
+      e.M = B;
+      e.N = H;
+      e.store = 1;
+      const float* W = pol_.p + pnet_.w_off[l];
+      steps_.push_back(mlp::fwd(in, in, ld, W, W, B, H, K, 1, e, 0, pact_[l].p, pact_[l].p, H));
+      in = pact_[l].p;
+      ld = H;
+      K = H;
+    }
+    epi::PolicyHead ph{};
+    ph.bias = pol_.p + pnet_.b_off[nh];
+    ph.act = X_.p + D;  // critic input [norm(s) | pi(s)]
+    ph.ld_act = Kp_;
+    ph.tanh_out = T_.p;
+    ph.ld_tanh = Ap_;
+    ph.M = B;
+    ph.A = A;
+    ph.mid = (dims_.low + dims_.high) / 2.0f;
+    ph.half = (dims_.high - dims_.low) / 2.0f;
+    head_.init(pol_.p + pnet_.w_off[nh], H, A);
+    head_.refresh(stream_);
+    const float* W = head_.ptr();
+    steps_.push_back(mlp::fwd(in, in, ld, W, W, B, A, H, 1, ph, head_.stride()));
+  }
+
+  // ------------------------------------------ twin critic replicas forward
+  for (int l = 0; l < nh; ++l) {
+    epi::Hidden e{};
+    for (int k = 0; k < 2; ++k) {
+      e.bias[k] = q[k] + qnet_.b_off[l];
+      e.mask[k] = cmask_[k][l].p;
+    }
+    e.ld_mask = wpr;
+    e.bn = bnH;
+    e.M = B;
+    e.N = H;
+    const bool last = l + 1 == nh;
+    e.store = last ? 0 : 1;
+    if (last) {
+      for (int k = 0; k < 2; ++k) e.w_head[k] = q[k] + qnet_.w_off[nh];
+      e.partial = part_.p;
+      e.ld_part = B;
+      e.n_tiles = nt;
+    }
+    const float* a0 = l == 0 ? X_.p : cact_[0][l - 1].p;
+    const float* a1 = l == 0 ? X_.p : cact_[1][l - 1].p;
+    const int64_t lda = l == 0 ? Kp_ : H;
+    const int K = l == 0 ? K0 : H;
+    steps_.push_back(mlp::fwd(a0, a1, lda, q[0] + qnet_.w_off[l], q[1] + qnet_.w_off[l], B, H, K,
+                              2, e, 0, last ? nullptr : cact_[0][l].p,
+                              last ? nullptr : cact_[1][l].p, H));
+  }
+  // ------------------------------------------------ min critic + upstream
+  {
+    critic::LossArgs a{part_.p, B, nt, q[0], q[1], qnet_.b_off[nh], nullptr, up_.p,
+                       block_loss_.p, loss_counter_.p, loss_.p, status_.p, B};
+    steps_.push_back([a, loss_blocks](cudaStream_t st) {
+      critic::actor_pick_kernel<<<loss_blocks, critic::kRowThreads, 0, st>>>(a);
+      PQLG_CHECK_LAUNCH();
+      count_launch();
+    });
+  }
+  // --------------------------------- input gradient through the critics
+  {
+    critic::HeadInputGradArgs a{};
+    a.up = up_.p;
+    for (int k = 0; k < 2; ++k) {
+      a.mask[k] = cmask_[k][nh - 1].p;
+      a.w[k] = q[k] + qnet_.w_off[nh];
+      a.G[k] = Gc_[k][nh - 1].p;
+    }
+    a.B = B;
+    a.H = H;
+    const int blocks = 4 * mlp::kSMs;
+    steps_.push_back([a, blocks](cudaStream_t st) {
+      critic::head_input_grad_kernel<<<dim3(blocks, 2), 256, 0, st>>>(a);
+      PQLG_CHECK_LAUNCH();
+      count_launch();
+    });
+  }
+  for (int l = nh - 1; l >= 1; --l) {
+    epi::DgradMask dm{};
+    for (int k = 0; k < 2; ++k) dm.mask[k] = cmask_[k][l - 1].p;
+    dm.ld_mask = wpr;
+    dm.bn = bnH;
+    dm.M = B;
+    dm.N = H;
+    steps_.push_back(mlp::dgrad(Gc_[0][l].p, Gc_[1][l].p, H, q[0] + qnet_.w_off[l],
+                                q[1] + qnet_.w_off[l], H, B, H, H, 2, dm, Gc_[0][l - 1].p,
+                                Gc_[1][l - 1].p, H));
+  }
+  {
+    // layer-0 dgrad restricted to the action columns: rows D..D+A-1 of W0
+    epi::Store s{};
+    s.out[0] = dact_[0].p;
+    s.out[1] = dact_[1].p;
+    s.ld_out = Ap_;
+    s.M = B;
+    s.N = A;
+    steps_.push_back(mlp::dgrad(Gc_[0][0].p, Gc_[1][0].p, H, q[0] + qnet_.w_off[0] + D * H,
+                                q[1] + qnet_.w_off[0] + D * H, H, B, A, H, 2, s));
+  }
+  // ------------------------------------------------- policy head backward
+  const int ptiles = (B + 63) / 64;
+  head_db_.alloc(static_cast<size_t>(ptiles) * A);
+  {
+    critic::PolicyHeadBwdArgs a{};
+    a.dact1 = dact_[0].p;
+    a.dact2 = dact_[1].p;
+    a.ld_dact = Ap_;
+    a.t = T_.p;
+    a.ld_t = Ap_;
+    a.dy = dy_.p;
+    a.ld_dy = Ap_;
+    a.db_part = head_db_.p;
+    a.half = (dims_.high - dims_.low) / 2.0f;
+    a.B = B;
+    a.A = A;
+    a.rows_per_tile = 64;
+    steps_.push_back([a, ptiles](cudaStream_t st) {
+      critic::policy_head_backward_kernel<<<ptiles, 32, 0, st>>>(a);
+      PQLG_CHECK_LAUNCH();
+      count_launch();
+    });
+  }
+  // ----------------------------------------------------- policy backward
+  wpart_.resize(nh + 1);
+  colsum_.resize(nh);
+  wsplits_.resize(nh + 1);
+  for (int l = 0; l <= nh; ++l) {
+    const int in = l == 0 ? D : H;
+    const int out = l == nh ? A : H;
+    const int ldo = l == nh ? Ap_ : H;
+    wsplits_[l] = mlp::wgrad_splits(in, out, B, 1);
+    wpart_[l].alloc(static_cast<size_t>(wsplits_[l]) * in * ldo);
+    if (l < nh) colsum_[l].alloc(static_cast<size_t>(mt) * H);
+  }
+  // head layer: dW_nh = act_{nh-1}^T dy ; G_{nh-1} = (dy W_nh^T) * mask
+  steps_.push_back(mlp::wgrad(pact_[nh - 1].p, pact_[nh - 1].p, H, dy_.p, dy_.p, Ap_, H, A, B, 1,
+                              wsplits_[nh], epi::Partial{}, wpart_[nh].p, Ap_));
+  {
+    epi::DgradMask dm{};
+    dm.mask[0] = dm.mask[1] = pmask_[nh - 1].p;
+    dm.ld_mask = wpr;
+    dm.colsum = colsum_[nh - 1].p;
+    dm.ld_cs = H;
+    dm.m_tiles = mt;
+    dm.bn = bnH;
+    dm.M = B;
+    dm.N = H;
+    steps_.push_back(mlp::dgrad(dy_.p, dy_.p, Ap_, head_.ptr(), head_.ptr(), head_.stride(), B,
+                                H, A, 1, dm, Gp_[nh - 1].p, Gp_[nh - 1].p, H));
+  }
+  for (int l = nh - 1; l >= 0; --l) {
+    const int in = l == 0 ? D : H;
+    const float* h = l == 0 ? X_.p : pact_[l - 1].p;
+    const int64_t ldh = l == 0 ? Kp_ : H;
+    steps_.push_back(mlp::wgrad(h, h, ldh, Gp_[l].p, Gp_[l].p, H, in, H, B, 1, wsplits_[l],
+                                epi::Partial{}, wpart_[l].p));
+    if (l > 0) {
+      epi::DgradMask dm{};
+      dm.mask[0] = dm.mask[1] = pmask_[l - 1].p;
+      dm.ld_mask = wpr;
+      dm.colsum = colsum_[l - 1].p;
+      dm.ld_cs = H;
+      dm.m_tiles = mt;
+      dm.bn = bnH;
+      dm.M = B;
+      dm.N = H;
+      const float* W = pol_.p + pnet_.w_off[l];
+      steps_.push_back(mlp::dgrad(Gp_[l].p, Gp_[l].p, H, W, W, H, B, H, H, 1, dm,
+                                  Gp_[l - 1].p, Gp_[l - 1].p, H));
+    }
+  }
+  // ------------------------------------- reduction + clip + Adam (policy)
+  {
+    optim::FinalizeArgs f{};
+    int s = 0;
+    for (int l = 0; l < nh; ++l) {
+      const int in = l == 0 ? D : H;
+      f.seg[s++] = optim::Segment{pnet_.w_off[l], static_cast<int64_t>(in) * H, wpart_[l].p, 0,
+                                  wsplits_[l], static_cast<int64_t>(in) * H};
+      f.seg[s++] = optim::Segment{pnet_.b_off[l], H, colsum_[l].p, 0, mt, H};
+    }
+    optim::Segment wh{pnet_.w_off[nh], static_cast<int64_t>(H) * A, wpart_[nh].p, 0,
+                      wsplits_[nh], static_cast<int64_t>(H) * Ap_};
+    wh.cols = A;
+    wh.ld_src = Ap_;
+    f.seg[s++] = wh;
+    f.seg[s++] = optim::Segment{pnet_.b_off[nh], A, head_db_.p, 0, ptiles, A};
+    require(s <= optim::kMaxSegments, "plearner: too many layers");
+    f.n_seg = s;
+    f.total = pnet_.params;
+    f.gstride = pnet_.params;
+    f.grads = grads_.p;
+    const int fb = static_cast<int>(std::min<int64_t>(4 * mlp::kSMs, (pnet_.params + 1023) / 1024));
+    block_sq_.alloc(fb);
+    fin_counter_.alloc(1);
+    scale_.alloc(1);
+    f.block_sq = block_sq_.p;
+    f.counter = fin_counter_.p;
+    f.scale = scale_.p;
+    f.status = status_.p;
+    f.max_norm = 0.5f;
+    steps_.push_back([f, fb](cudaStream_t st) {
+      optim::finalize_kernel<<<dim3(fb, 1), optim::kFinalizeThreads, 0, st>>>(f);
+      PQLG_CHECK_LAUNCH();
+      count_launch();
+    });
+    optim::AdamArgs a{};
+    a.p = pol_.p;
+    a.g = grads_.p;
+    a.m = m_.p;
+    a.v = v_.p;
+    a.target = nullptr;
+    a.n = pnet_.params;
+    a.gstride = pnet_.params;
+    a.scale = scale_.p;
+    a.status = status_.p;
+    a.step = step_.p;
+    a.bc = bc_.p;
+    a.bc_len = static_cast<int64_t>(bc_.n);
+    a.lr = static_cast<float>(cfg_.lr_actor);
+    a.beta1 = 0.9f;
+    a.beta2 = 0.999f;
+    a.eps = 1e-8f;
+    a.tau = 0.0f;
+    const int blocks = static_cast<int>(std::min<int64_t>(4 * mlp::kSMs, (pnet_.params + 255) / 256));
+    steps_.push_back([a, blocks](cudaStream_t st) {
+      optim::adam_polyak_kernel<<<dim3(blocks, 1), 256, 0, st>>>(a);
+      PQLG_CHECK_LAUNCH();
+      count_launch();
+    });
+  }
+  // the padded head mirror follows the updated policy
+  steps_.push_back([this](cudaStream_t st) { head_.refresh(st); });
+}
+
+void PLearner::adopt_critics(const float* q1, const float* q2, int64_t version) {
+  if (version < critic_version_) return;  // learners.cpp:222-227
+  const int64_t P = qnet_.params;
+  PQLG_CUDA(cudaMemcpyAsync(q_.p, q1, P * 4, cudaMemcpyHostToDevice, stream_));
+  PQLG_CUDA(cudaMemcpyAsync(q_.p + Ps_, q2, P * 4, cudaMemcpyHostToDevice, stream_));
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+  critic_version_ = version;
+}
+
+void PLearner::adopt_critics_device(const float* q1, const float* q2, int64_t version) {
+  if (version < critic_version_) return;
+  const int64_t P = qnet_.params;
+  PQLG_CUDA(cudaMemcpyAsync(q_.p, q1, P * 4, cudaMemcpyDeviceToDevice, stream_));
+  PQLG_CUDA(cudaMemcpyAsync(q_.p + Ps_, q2, P * 4, cudaMemcpyDeviceToDevice, stream_));
+  critic_version_ = version;
+}
+
+void PLearner::adopt_norm(int64_t count, const double* mean, const double* m2) {
+  norm_.set(count, mean, m2, stream_);
+}
+
+void PLearner::ingest(const float* states, int64_t ld, uint64_t n) {
+  states_->insert(states, ld, n, stream_);
+}
+
+bool PLearner::ready(int64_t c_a) {
+  return c_a >= cfg_.warm_up && states_->size() >= static_cast<uint64_t>(B_);
+}
+
+void PLearner::enqueue() {
+  for (auto& s : steps_) s(stream_);
+}
+
+int PLearner::check_status() {
+  uint32_t st = 0;
+  PQLG_CUDA(cudaMemcpyAsync(&st, status_.p, 4, cudaMemcpyDeviceToHost, stream_));
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+  if (st) {
+    PQLG_CUDA(cudaMemsetAsync(status_.p, 0, 4, stream_));
+    return PQLG_ENONFINITE;
+  }
+  return PQLG_OK;
+}
+
+float PLearner::update() {
+  if (states_->size() < static_cast<uint64_t>(B_))
+    throw Error(PQLG_NOT_READY, "policy update before state warm-up");
+  if (mt_mode_) {
+    const uint64_t count = states_->size();
+    std::uniform_int_distribution<std::size_t> pick(0, count - 1);
+    for (int r = 0; r < B_; ++r) idx_host_[r] = pick(mt_);
+    PQLG_CUDA(cudaMemcpyAsync(idx_.p, idx_host_.data(), B_ * sizeof(uint64_t),
+                              cudaMemcpyHostToDevice, stream_));
+  }
+  enqueue();
+  float loss = 0.0f;
+  PQLG_CUDA(cudaMemcpyAsync(&loss, loss_.p, 4, cudaMemcpyDeviceToHost, stream_));
+  if (check_status() != PQLG_OK) throw Error(PQLG_ENONFINITE, "ddpg actor update: non-finite");
+  return loss;
+}
+
+int PLearner::kernels_per_update() {
+  if (kpu_ == 0) {
+    const uint64_t before = g_launches.load();
+    cudaGraph_t g;
+    PQLG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    enqueue();
+    PQLG_CUDA(cudaStreamEndCapture(stream_, &g));
+    cudaGraphDestroy(g);
+    kpu_ = static_cast<int>(g_launches.load() - before);
+    g_launches.fetch_sub(kpu_);
+  }
+  return kpu_;
+}
+
+void PLearner::update_n(int n) {
+  require(!mt_mode_, "update_n: graph replay needs the Philox sampler");
+  if (states_->size() < static_cast<uint64_t>(B_))
+    throw Error(PQLG_NOT_READY, "policy update before state warm-up");
+  if (!graph_exec_) {
+    kernels_per_update();
+    cudaGraph_t g;
+    PQLG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    enqueue();
+    PQLG_CUDA(cudaStreamEndCapture(stream_, &g));
+    g_launches.fetch_sub(kpu_);
+    PQLG_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
+    cudaGraphDestroy(g);
+  }
+  for (int i = 0; i < n; ++i) PQLG_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+  count_launch(static_cast<uint64_t>(n) * kpu_);
+}
+
+float PLearner::last_loss() {
+  float loss = 0.0f;
+  PQLG_CUDA(cudaMemcpyAsync(&loss, loss_.p, 4, cudaMemcpyDeviceToHost, stream_));
+  if (check_status() != PQLG_OK) throw Error(PQLG_ENONFINITE, "ddpg actor update: non-finite");
+  return loss;
+}
+
+// which: 0 policy, 1 critic replica q1, 2 critic replica q2
+void PLearner::get_params(int which, float* out) {
+  const float* src = which == 0 ? pol_.p : (which == 1 ? q_.p : q_.p + Ps_);
+  const int64_t n = param_count(which);
+  require(which >= 0 && which <= 2, "get_params: which must be 0..2");
+  PQLG_CUDA(cudaMemcpyAsync(out, src, n * 4, cudaMemcpyDeviceToHost, stream_));
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void PLearner::set_params(int which, const float* flat) {
+  require(which >= 0 && which <= 2, "set_params: which must be 0..2");
+  float* dst = which == 0 ? pol_.p : (which == 1 ? q_.p : q_.p + Ps_);
+  PQLG_CUDA(cudaMemcpyAsync(dst, flat, param_count(which) * 4, cudaMemcpyHostToDevice, stream_));
+  if (which == 0) head_.refresh(stream_);
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+}
+
+int64_t PLearner::param_count(int which) const {
+  return which == 0 ? pnet_.params : qnet_.params;
+}
+
+}  // namespace pqlg
+
+// ------------------------------------------------------------------ C ABI
+struct pqlg_plearner_s {
+  std::unique_ptr<pqlg::PLearner> p;
+};
+
+using namespace pqlg;
+
+extern "C" {
+
+int pqlg_plearner_create(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                         uint64_t init_rng_seed, void* stream, pqlg_plearner* out) {
+  return guarded([&] {
+    require(cfg && dims && out, "plearner_create: null argument");
+    auto h = std::make_unique<pqlg_plearner_s>();
+    h->p = std::make_unique<PLearner>(*cfg, *dims, init_rng_seed,
+                                      static_cast<cudaStream_t>(stream));
+    *out = h.release();
+  });
+}
+
+int pqlg_plearner_destroy(pqlg_plearner h) {
+  return guarded([&] { delete h; });
+}
+
+int pqlg_plearner_adopt_critics(pqlg_plearner h, const float* q1, const float* q2,
+                                int64_t version) {
+  return guarded([&] { h->p->adopt_critics(q1, q2, version); });
+}
+
+int pqlg_plearner_adopt_norm(pqlg_plearner h, const pqlg_norm_stats* n) {
+  return guarded([&] { h->p->adopt_norm(n->count, n->mean, n->m2); });
+}
+
+int pqlg_plearner_ingest(pqlg_plearner h, const float* states_dev, int64_t ld, uint64_t n) {
+  return guarded([&] { h->p->ingest(states_dev, ld > 0 ? ld : h->p->obs_dim(), n); });
+}
+
+int pqlg_plearner_ready(pqlg_plearner h, int64_t c_a, int* ready) {
+  return guarded([&] { *ready = h->p->ready(c_a) ? 1 : 0; });
+}
+
+int pqlg_plearner_update(pqlg_plearner h, float* loss) {
+  return guarded([&] {
+    const float l = h->p->update();
+    if (loss) *loss = l;
+  });
+}
+
+int pqlg_plearner_update_n(pqlg_plearner h, int n) {
+  return guarded([&] { h->p->update_n(n); });
+}
+
+int pqlg_plearner_last_loss(pqlg_plearner h, float* loss) {
+  return guarded([&] { *loss = h->p->last_loss(); });
+}
+
+int pqlg_plearner_snapshot(pqlg_plearner h, float* flat) {
+  return guarded([&] { h->p->get_params(0, flat); });
+}
+
+int pqlg_plearner_get_params(pqlg_plearner h, int which, float* flat) {
+  return guarded([&] { h->p->get_params(which, flat); });
+}
+
+int pqlg_plearner_set_params(pqlg_plearner h, int which, const float* flat) {
+  return guarded([&] { h->p->set_params(which, flat); });
+}
+
+int pqlg_plearner_param_count(pqlg_plearner h, int which, int64_t* out) {
+  return guarded([&] { *out = h->p->param_count(which); });
+}
+
+int pqlg_plearner_buffer_size(pqlg_plearner h, uint64_t* out) {
+  return guarded([&] { *out = h->p->buffer_size(); });
+}
+
+int pqlg_plearner_set_sampler(pqlg_plearner h, int mode) {
+  return guarded([&] {
+    require(mode == PQLG_RNG_PHILOX || mode == PQLG_RNG_INDICES, "set_sampler: bad mode");
+    h->p->set_mt_mode(mode == PQLG_RNG_INDICES);
+  });
+}
+
+int pqlg_plearner_kernels_per_update(pqlg_plearner h, int* out) {
+  return guarded([&] { *out = h->p->kernels_per_update(); });
+}
+
+}  // extern "C"

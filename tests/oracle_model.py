@@ -164,7 +164,82 @@ class OraclePUpdate:
             rc = orc().orc_ddpg_actor_loss(*args, ptr(loss), ptr(dp))
         if rc != 0:
             raise FloatingPointError("non-finite actor loss")
+        # scale of the objective's terms: mean_b |min(Q1, Q2)(s, pi(s))| -- the
+        # loss itself is a mean of terms that largely cancel, so tolerances on
+        # it are stated relative to this scale
+        a = policy_act(self.pol, self.ps, s)
+        xq = np.concatenate([s, a], axis=1)
+        q1 = mlp_forward(self.q[0], self.qs, xq)
+        q2 = mlp_forward(self.q[1], self.qs, xq)
+        qscale = float(np.mean(np.abs(np.minimum(q1, q2)))) if not self.distributional else 1.0
         orc().orc_clip_global_norm(ptr(dp), P, np.float32(0.5))
         self.t += 1
         adam(self.pol, dp, self.m, self.v, self.t, self.lr)
-        return float(loss[0]), dict(idx=idx, dp=dp)
+        return float(loss[0]), dict(idx=idx, dp=dp, qscale=qscale)
+
+
+class OracleEnv:
+    """The synthetic EnvBatch of the restatement (pql_oracle.c orc_env_*)."""
+
+    def __init__(self, N, D, A, seed, max_len):
+        self.N, self.D, self.A = N, D, A
+        self.h = orc().orc_env_create(N, D, A, seed, max_len)
+
+    def observe(self):
+        o = np.zeros((self.N, self.D), np.float32)
+        orc().orc_env_observe(self.h, ptr(o))
+        return o
+
+    def step(self, act):
+        act = f32(act)
+        nxt = np.zeros((self.N, self.D), np.float32)
+        term_obs = np.zeros((self.N, self.D), np.float32)
+        rew = np.zeros(self.N, np.float32)
+        done = np.zeros(self.N, np.uint8)
+        trunc = np.zeros(self.N, np.uint8)
+        rc = orc().orc_env_step(self.h, ptr(act), ptr(nxt), ptr(term_obs), ptr(rew), ptr(done),
+                                ptr(trunc))
+        if rc:
+            raise FloatingPointError("non-finite action")
+        return nxt, term_obs, rew, done, trunc
+
+    def __del__(self):
+        try:
+            orc().orc_env_destroy(self.h)
+        except Exception:
+            pass
+
+
+class OracleActor:
+    """ActorCore::rollout_step (learners.cpp:80-116) over the synthetic env."""
+
+    def __init__(self, N, D, A, hidden, n_hidden, policy, seed=0, max_len=1000,
+                 sigma_min=0.05, sigma_max=0.8):
+        from oracle_lib import STREAM_NOISE
+        self.N, self.D, self.A = N, D, A
+        self.ps = [D] + [hidden] * n_hidden + [A]
+        self.pol = f32(policy).copy()
+        self.env = OracleEnv(N, D, A, seed, max_len)
+        self.obs = self.env.observe()
+        self.count = np.zeros(1, np.int64)
+        self.mean = np.zeros(D)
+        self.m2 = np.zeros(D)
+        self.sigma = np.zeros(N, np.float32)
+        orc().orc_build_schedule(np.float32(sigma_min), np.float32(sigma_max), N, ptr(self.sigma))
+        self.noise = np.array([derive_seed(seed, STREAM_NOISE, i) for i in range(N)], np.uint64)
+
+    def step(self):
+        obs_norm = normalize(int(self.count[0]), self.mean, self.m2, self.obs)
+        act = policy_act(self.pol, self.ps, obs_norm)
+        pre_noise = act.copy()
+        orc().orc_apply_noise(ptr(act), self.N, self.A, ptr(self.sigma), np.float32(-1),
+                              np.float32(1), ptr(self.noise))
+        nxt, term_obs, rew, done, trunc = self.env.step(act)
+        term = (done.astype(bool) & ~trunc.astype(bool)).astype(np.uint8)
+        boot = np.where(done[:, None].astype(bool), term_obs, nxt)
+        obs = self.obs
+        orc().orc_norm_update(ptr(self.count), ptr(self.mean), ptr(self.m2), ptr(obs), self.N,
+                              self.D)
+        self.obs = nxt
+        return dict(obs=obs, act=act, pre_noise=pre_noise, boot=f32(boot), rew=rew, term=term,
+                    trunc=trunc)

@@ -1,0 +1,181 @@
+"""Actor path on the GPU: the synthetic EnvBatch and the exploration noise
+bit-exact against the oracle (and the reference's noise fixtures), the
+normalizer update to 1e-10, and ActorCore::rollout_step end to end
+(actions within the TF32 tolerance, noise/env stream states exact)."""
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle_lib import STREAM_NOISE, derive_seed, orc, param_count, ptr
+from oracle_model import OracleActor, OracleEnv, f32
+from paper_2307_12983_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def u32(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+@pytest.mark.parametrize("N,D,A,max_len", [(64, 5, 2, 7), (96, 211, 20, 1000), (40, 60, 8, 13)])
+def test_env_bit_exact_vs_oracle(N, D, A, max_len):
+    import torch
+    seed = 3
+    h = C.c_void_p()
+    _lib.call("pqlg_env_create", N, D, A, seed, max_len, 0, np.float32(-1), np.float32(1), None,
+              C.byref(h))
+    o = OracleEnv(N, D, A, seed, max_len)
+    obs = torch.zeros(N, D, device="cuda")
+    _lib.call("pqlg_env_reset_all", h, obs.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert np.array_equal(u32(host(obs)), u32(o.observe()))
+    rng = np.random.default_rng(N + D)
+    # constant push on some envs so |s_0| crosses 9 (terminal) within the run
+    M = None
+    drive = np.sign(rng.standard_normal((N, A))).astype(np.float32)
+    saw_term = saw_trunc = False
+    for t in range(60):
+        a = f32(np.where(rng.uniform(size=(N, 1)) < 0.5, drive,
+                         rng.uniform(-1.5, 1.5, (N, A))))  # includes out-of-range actions
+        ad = dev(a)
+        nxt = torch.zeros(N, D, device="cuda"); term_obs = torch.zeros(N, D, device="cuda")
+        rew = torch.zeros(N, device="cuda")
+        done = torch.zeros(N, dtype=torch.uint8, device="cuda")
+        trunc = torch.zeros(N, dtype=torch.uint8, device="cuda")
+        _lib.call("pqlg_env_step", h, ad.data_ptr(), 0, nxt.data_ptr(), term_obs.data_ptr(),
+                  rew.data_ptr(), done.data_ptr(), trunc.data_ptr(), 0)
+        torch.cuda.synchronize()
+        w_nxt, w_term, w_rew, w_done, w_trunc = o.step(a)
+        assert np.array_equal(host(done), w_done) and np.array_equal(host(trunc), w_trunc)
+        assert np.array_equal(u32(host(nxt)), u32(w_nxt)), t
+        assert np.array_equal(u32(host(rew)), u32(w_rew)), t
+        d = w_done.astype(bool)
+        assert np.array_equal(u32(host(term_obs)[d]), u32(w_term[d]))
+        saw_term |= bool(np.any(d & ~w_trunc.astype(bool)))
+        saw_trunc |= bool(np.any(w_trunc))
+    if max_len <= 60:
+        assert saw_trunc
+    # non-finite action -> runtime_error (vecenv.cpp:87-89)
+    bad = dev(f32(np.full((N, A), np.nan)))
+    with pytest.raises(_lib.NonFinite):
+        _lib.call("pqlg_env_step", h, bad.data_ptr(), 0, nxt.data_ptr(), term_obs.data_ptr(),
+                  rew.data_ptr(), done.data_ptr(), trunc.data_ptr(), 0)
+    _lib.call("pqlg_env_destroy", h)
+
+
+def test_noise_bit_exact_vs_reference_golden():
+    G = np.load(GOLDEN / "noise.npz")
+    for N, A, steps in ((64, 8, 3), (33, 20, 2), (5, 1, 4)):
+        a = G[f"noise_{N}_{A}_in"].copy()
+        sig = np.zeros(N, np.float32)
+        orc().orc_build_schedule(np.float32(0.05), np.float32(0.8), N, ptr(sig))
+        st = dev(np.array([derive_seed(0, STREAM_NOISE, i) for i in range(N)], np.uint64))
+        sd = dev(sig)
+        out = []
+        for s in range(steps):
+            ad = dev(a[s])
+            _lib.call("pqlg_k_apply_noise", ad.data_ptr(), 0, N, A, sd.data_ptr(),
+                      np.float32(-1), np.float32(1), st.data_ptr(), None)
+            out.append(host(ad))
+        assert np.array_equal(u32(np.stack(out)), u32(G[f"noise_{N}_{A}_out"])), (N, A)
+
+
+def test_noise_bit_exact_wide_random_vs_oracle():
+    # many rows -> many glibc-logf evaluations, incl. 1-ulp-sensitive inputs
+    N, A = 20000, 20
+    rng = np.random.default_rng(1)
+    a = f32(rng.uniform(-1, 1, (N, A)))
+    sig = np.zeros(N, np.float32)
+    orc().orc_build_schedule(np.float32(0.05), np.float32(0.8), N, ptr(sig))
+    states = np.array([derive_seed(9, STREAM_NOISE, i) for i in range(N)], np.uint64)
+    ad, sd, st = dev(a), dev(sig), dev(states)
+    _lib.call("pqlg_k_apply_noise", ad.data_ptr(), 0, N, A, sd.data_ptr(), np.float32(-1),
+              np.float32(1), st.data_ptr(), None)
+    want = a.copy()
+    ws = states.copy()
+    orc().orc_apply_noise(ptr(want), N, A, ptr(sig), np.float32(-1), np.float32(1), ptr(ws))
+    assert np.array_equal(u32(host(ad)), u32(want))
+    assert np.array_equal(host(st), ws)
+
+
+def test_normalizer_update_vs_oracle():
+    import torch
+    rng = np.random.default_rng(2)
+    D = 211
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    mean = torch.zeros(D, dtype=torch.float64, device="cuda")
+    m2 = torch.zeros(D, dtype=torch.float64, device="cuda")
+    mf = torch.zeros(D, device="cuda"); inv = torch.zeros(D, device="cuda")
+    oc = np.zeros(1, np.int64); om = np.zeros(D); om2 = np.zeros(D)
+    for rows in (1, 300, 16384, 5):
+        x = f32(rng.standard_normal((rows, D)) * 3 + 2)
+        xd = dev(x)
+        _lib.call("pqlg_k_normalizer_update", cnt.data_ptr(), mean.data_ptr(), m2.data_ptr(),
+                  xd.data_ptr(), 0, rows, D, mf.data_ptr(), inv.data_ptr(), None)
+        orc().orc_norm_update(ptr(oc), ptr(om), ptr(om2), ptr(x), rows, D)
+        assert int(host(cnt)[0]) == oc[0]
+        np.testing.assert_allclose(host(mean), om, rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(host(m2), om2, rtol=1e-10)
+    mf_o = np.zeros(D, np.float32); inv_o = np.zeros(D, np.float32)
+    orc().orc_norm_stats_to_f32(int(oc[0]), ptr(om), ptr(om2), D, ptr(mf_o), ptr(inv_o))
+    np.testing.assert_allclose(host(mf), mf_o, rtol=1e-6)
+    np.testing.assert_allclose(host(inv), inv_o, rtol=1e-6)
+
+
+@pytest.mark.parametrize("cfg", ["small", "c3"])
+def test_rollout_steps_vs_oracle(cfg):
+    N, D, A, H, nh, T = {"small": (300, 13, 3, 64, 2, 6), "c3": (2048, 211, 20, 512, 3, 4)}[cfg]
+    conf = _lib.default_config(n_envs=N, hidden=H, hidden_layers=nh, seed=5, max_episode_len=50)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    h = C.c_void_p()
+    _lib.call("pqlg_actor_create", C.byref(conf), C.byref(dims), None, C.byref(h))
+    P = param_count([D] + [H] * nh + [A])
+    pol = np.zeros(P, np.float32)
+    _lib.call("pqlg_actor_read", h, 5, ptr(pol))
+    # a policy with visible actions (the orthogonal init's 1e-2 head is near zero)
+    rng = np.random.default_rng(3)
+    pol = f32(pol + rng.standard_normal(P).astype(np.float32) * 0.02)
+    _lib.call("pqlg_actor_adopt_policy", h, ptr(pol), 1)
+    o = OracleActor(N, D, A, H, nh, pol, seed=5, max_len=50)
+    obs0 = np.zeros((N, D), np.float32)
+    _lib.call("pqlg_actor_read", h, 0, ptr(obs0))
+    assert np.array_equal(u32(obs0), u32(o.obs))
+    for t in range(T):
+        s = _lib.StepSlice()
+        _lib.call("pqlg_actor_rollout_step", h, C.byref(s))
+        w = o.step()
+        act = np.zeros((N, A), np.float32)
+        _lib.call("pqlg_actor_read", h, 1, ptr(act))
+        ns = np.zeros(N, np.uint64)
+        _lib.call("pqlg_actor_read", h, 2, ptr(ns))
+        ep = np.zeros(N, np.int64)
+        _lib.call("pqlg_actor_read", h, 3, ptr(ep))
+        # noise streams advance identically (polar rejections depend only on the stream)
+        assert np.array_equal(ns, o.noise), t
+        rel = np.linalg.norm(act - w["act"]) / np.linalg.norm(w["act"])
+        print(f"\n{cfg} t={t}: actions rel={rel:.2e} max={np.max(np.abs(act - w['act'])):.2e}")
+        assert rel <= 2e-3
+        obs = np.zeros((N, D), np.float32)
+        _lib.call("pqlg_actor_read", h, 0, ptr(obs))  # next observation
+        # next obs = 0.95 s + 0.05 M a: inherits the TF32 action error
+        orel = np.linalg.norm(obs - o.obs) / np.linalg.norm(o.obs)
+        assert orel <= 1e-3, orel
+    cnt = C.c_int64()
+    mean = np.zeros(D); m2 = np.zeros(D)
+    _lib.call("pqlg_actor_norm", h, C.byref(cnt), ptr(mean), ptr(m2))
+    assert cnt.value == o.count[0] == N * T
+    np.testing.assert_allclose(mean, o.mean, rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(m2, o.m2, rtol=1e-4)
+    _lib.call("pqlg_actor_destroy", h)
