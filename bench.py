@@ -279,8 +279,104 @@ def run_ours(args, rank, world, local):
         flops = critic_flops(D, A, H, nh, B)
         roof["update_tflops"] = round(flops / (ms_step * 1e-3) / 1e12, 2)
         roof["update_frac_of_tf32_peak"] = round(flops / (ms_step * 1e-3) / 1e12 / peak, 4)
+    _lib.call("pqlg_vlearner_destroy", h)
     return dict(value=value, ms_step=ms_step, loss=loss.value, e2e=e2e, roof=roof,
                 clocks=clk.summary(), launches=int(launches), kpu=kpu.value)
+
+
+def run_actor(args, rank, world, local, steps, warmup):
+    """Actor transitions/s: one ActorCore::rollout_step over N envs (normalize
+    -> policy -> mixed noise -> synthetic env -> StepSlice -> normalizer
+    update) plus the V-learner ingest (n-step assemble + ring insert) and the
+    P-learner StateBuffer insert of that slice, all on the GPU."""
+    import torch
+    from paper_2307_12983_b200 import _lib
+    D, A, H, nh, B, N, cap = CONFIGS[args.config]
+    stream = torch.cuda.Stream(device=local)
+    sp = C.c_void_p(stream.cuda_stream)
+    cfg = _lib.default_config(batch_size=B, buffer_capacity=cap, hidden=H, hidden_layers=nh,
+                              n_envs=N, seed=rank, env_offset=rank * N, envs_total=world * N,
+                              max_episode_len=1000)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    act, vl, pl = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    _lib.call("pqlg_actor_create", C.byref(cfg), C.byref(dims), sp, C.byref(act))
+    _lib.call("pqlg_vlearner_create", C.byref(cfg), C.byref(dims), 1, sp, C.byref(vl))
+    _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 1, sp, C.byref(pl))
+    s = _lib.StepSlice()
+
+    def step():
+        _lib.call("pqlg_actor_rollout_step", act, C.byref(s))
+        _lib.call("pqlg_vlearner_ingest", vl, C.byref(s))
+        _lib.call("pqlg_plearner_ingest", pl, s.obs, s.ld_obs, N)
+
+    for _ in range(warmup):
+        step()
+    stream.synchronize()
+    barrier(world)
+    l0 = _lib.lib().pqlg_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        step()
+    ev1.record(stream)
+    ev1.synchronize()
+    barrier(world)
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world)
+    launches = _lib.lib().pqlg_launch_count() - l0
+    # policy-inference-only rate (graph replay of the actor step alone)
+    _lib.call("pqlg_actor_rollout_n", act, warmup)
+    stream.synchronize()
+    ev0.record(stream)
+    _lib.call("pqlg_actor_rollout_n", act, steps)
+    ev1.record(stream)
+    ev1.synchronize()
+    ms_actor_only = max_over_ranks(ev0.elapsed_time(ev1), world)
+    # e2e: the host-facing C-ABI calls per step, each step ending with a
+    # synchronous device->host read of its status word (4 B)
+    e2e_steps = max(5, min(steps, 50))
+    status = np.zeros(1, np.uint32)
+    stream.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        step()
+        _lib.call("pqlg_actor_read", act, 6, status.ctypes.data)
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    for h, fn in ((act, "pqlg_actor_destroy"), (vl, "pqlg_vlearner_destroy"),
+                  (pl, "pqlg_plearner_destroy")):
+        _lib.call(fn, h)
+    return {"value": world * N * steps / (ms * 1e-3), "unit": "transitions/s",
+            "n_envs_per_gpu": N, "ms_per_step": ms / steps,
+            "actor_step_only": {"value": world * N * steps / (ms_actor_only * 1e-3),
+                                "ms_per_step": ms_actor_only / steps},
+            "e2e": {"value": world * N * e2e_steps / e2e_s, "unit": "transitions/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4},
+            "gpu_launches": int(launches)}
+
+
+def run_policy(args, rank, world, local, steps, warmup):
+    """Policy (P-learner) updates/s at batch 8192."""
+    import torch
+    from paper_2307_12983_b200 import _lib
+    D, A, H, nh, B, N, cap = CONFIGS[args.config]
+    stream = torch.cuda.Stream(device=local)
+    cfg = _lib.default_config(batch_size=B, buffer_capacity=1_000_000, hidden=H,
+                              hidden_layers=nh, n_envs=N, seed=rank)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    pl = C.c_void_p()
+    _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 1,
+              C.c_void_p(stream.cuda_stream), C.byref(pl))
+    states = torch.randn(1_000_000, D, device="cuda")
+    _lib.call("pqlg_plearner_ingest", pl, states.data_ptr(), D, 1_000_000)
+    _lib.call("pqlg_plearner_update_n", pl, warmup)
+    stream.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    _lib.call("pqlg_plearner_update_n", pl, steps)
+    ev1.record(stream)
+    ev1.synchronize()
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world)
+    _lib.call("pqlg_plearner_destroy", pl)
+    return {"value": world * steps / (ms * 1e-3), "unit": "updates/s", "ms_per_step": ms / steps}
 
 
 # ------------------------------------------------------ reference arm
@@ -389,9 +485,13 @@ def main():
         return
 
     r = run_ours(args, rank, world, local)
+    actor = run_actor(args, rank, world, local, max(10, args.steps // 4), max(3, args.warmup // 4))
+    policy = run_policy(args, rank, world, local, args.steps, args.warmup)
     if rank != 0:
         return
     out = dict(base)
+    out["actor"] = actor
+    out["policy_updates"] = policy
     out.update(value=r["value"], ms_per_step=r["ms_step"], e2e=r["e2e"], roofline=r["roof"],
                clocks=r["clocks"], gpu_launches=r["launches"],
                kernels_per_update=r["kpu"], last_loss=r["loss"])
