@@ -66,10 +66,18 @@ struct DeviceEnv {
     PQLG_CHECK_LAUNCH();
     count_launch();
   }
-  void step(const float* act, int64_t ld_act, const actor::StepOut& o, cudaStream_t st) {
-    const size_t smem = static_cast<size_t>(actor::kEnvWarps) * (D + A) * sizeof(float);
+  void step(const float* act, int64_t ld_act, const actor::StepOut& o, cudaStream_t st,
+            const actor::NextNorm& nn = actor::NextNorm{}) {
+    require(A <= actor::kMaxA, "env: act_dim > 32 not supported");
+    const size_t smem = actor::env_step_smem(D, A);
+    static bool configured = false;
+    if (!configured) {
+      PQLG_CUDA(cudaFuncSetAttribute(actor::env_step_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      configured = true;
+    }
     actor::env_step_kernel<<<(N + actor::kEnvWarps - 1) / actor::kEnvWarps,
-                             32 * actor::kEnvWarps, smem, st>>>(view(), act, ld_act, o);
+                             32 * actor::kEnvWarps, smem, st>>>(view(), act, ld_act, o, nn);
     PQLG_CHECK_LAUNCH();
     count_launch();
   }
@@ -112,7 +120,7 @@ class Actor {
   DevBuf<uint64_t> noise_rng_;
   DevBuf<float> sigma_;
   DevBuf<int64_t> count_;
-  DevBuf<double> mean_, m2_, cmean_, cm2_, ccount_;
+  DevBuf<double> mean_, m2_, npart_;
   DevBuf<float> mean_f_, inv_f_;
   DevBuf<int> identity_;
   DevBuf<uint32_t> status_;
@@ -196,11 +204,14 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
   identity_.alloc(1);
   const int one = 1;
   PQLG_CUDA(cudaMemcpy(identity_.p, &one, 4, cudaMemcpyHostToDevice));
-  const int chunks = (N_ + actor::kNormChunk - 1) / actor::kNormChunk;
-  cmean_.alloc(static_cast<size_t>(chunks) * D_);
-  cm2_.alloc(static_cast<size_t>(chunks) * D_);
-  ccount_.alloc(chunks);
+  npart_.alloc(static_cast<size_t>(actor::kNormGroups) * D_ * 2);
   status_.alloc(1);
+  // first policy input: apply_stats with count 0 is the identity
+  actor::normalize_kernel<<<4 * mlp::kSMs, 256, 0, stream_>>>(obs_[0].p, Dp_, Xn_.p, Dp_,
+                                                               mean_f_.p, inv_f_.p, identity_.p,
+                                                               N_, D_);
+  PQLG_CHECK_LAUNCH();
+  count_launch();
   build();
   PQLG_CUDA(cudaStreamSynchronize(stream_));
 }
@@ -258,23 +269,22 @@ void Actor::enqueue(int cur) {
   cudaStream_t st = stream_;
   const int N = N_, D = D_;
   const float* obs = obs_[cur].p;
-  // obs_norm = normalizer_.apply(obs_)  (stats of previous steps)
-  actor::normalize_kernel<<<4 * mlp::kSMs, 256, 0, st>>>(obs, Dp_, Xn_.p, Dp_, mean_f_.p,
-                                                         inv_f_.p, identity_.p, N, D);
-  PQLG_CHECK_LAUNCH();
-  count_launch();
+  // actions = pi(obs_norm) + mixed noise; Xn_ holds apply(stats_{t-1}, obs_t)
   for (auto& s : policy_steps_) s(st);
-  // env_->step(actions)
-  actor::StepOut o{obs_[1 - cur].p, boot_.p, rew_.p, term_.p, trunc_.p, nullptr, Dp_, status_.p};
-  env_->step(act_.p, Ap_, o, st);
-  // normalizer_.update(obs_)  (after acting, learners.cpp:113)
-  const int chunks = (N + actor::kNormChunk - 1) / actor::kNormChunk;
-  actor::norm_chunk_kernel<<<chunks, 256, 0, st>>>(obs, Dp_, N, D, cmean_.p, cm2_.p, ccount_.p);
+  // normalizer_.update(obs_) (learners.cpp:113): it only reads this step's
+  // observations, so it runs before the env step and the env kernel can emit
+  // the next policy input apply(stats_t, obs_{t+1}) directly.
+  actor::norm_partial_kernel<<<dim3((D + 31) / 32, actor::kNormGroups), 256, 0, st>>>(
+      obs, Dp_, N, D, npart_.p);
   PQLG_CHECK_LAUNCH();
   actor::NormState ns{count_.p, mean_.p, m2_.p, mean_f_.p, inv_f_.p, identity_.p};
-  actor::norm_merge_kernel<<<1, 256, 0, st>>>(cmean_.p, cm2_.p, ccount_.p, chunks, D, N, ns);
+  actor::norm_finish_kernel<<<1, 256, 0, st>>>(obs, npart_.p, actor::kNormGroups, D, N, ns);
   PQLG_CHECK_LAUNCH();
   count_launch(2);
+  // env_->step(actions) + next-obs normalisation
+  actor::StepOut o{obs_[1 - cur].p, boot_.p, rew_.p, term_.p, trunc_.p, nullptr, Dp_, status_.p};
+  actor::NextNorm nn{Xn_.p, Dp_, mean_f_.p, inv_f_.p, identity_.p};
+  env_->step(act_.p, Ap_, o, st, nn);
 }
 
 int Actor::kernels_per_step() {
@@ -481,15 +491,16 @@ int pqlg_k_normalizer_update(int64_t* count_dev, double* mean_dev, double* m2_de
                              float* mean_f_dev, float* inv_f_dev, void* stream) {
   return guarded([&] {
     auto st = static_cast<cudaStream_t>(stream);
-    const int chunks = (rows + actor::kNormChunk - 1) / actor::kNormChunk;
-    DevBuf<double> cm(static_cast<size_t>(chunks) * dim), c2(static_cast<size_t>(chunks) * dim),
-        cc(chunks);
+    if (rows == 0) return;  // normalizer.hpp:34
+    DevBuf<double> part(static_cast<size_t>(actor::kNormGroups) * dim * 2);
     DevBuf<int> ident(1);
-    actor::norm_chunk_kernel<<<chunks, 256, 0, st>>>(batch_dev, ld > 0 ? ld : dim, rows, dim,
-                                                     cm.p, c2.p, cc.p);
+    const int64_t ldx = ld > 0 ? ld : dim;
+    actor::norm_partial_kernel<<<dim3((dim + 31) / 32, actor::kNormGroups), 256, 0, st>>>(
+        batch_dev, ldx, rows, dim, part.p);
     PQLG_CHECK_LAUNCH();
     actor::NormState ns{count_dev, mean_dev, m2_dev, mean_f_dev, inv_f_dev, ident.p};
-    actor::norm_merge_kernel<<<1, 256, 0, st>>>(cm.p, c2.p, cc.p, chunks, dim, rows, ns);
+    actor::norm_finish_kernel<<<1, 256, 0, st>>>(batch_dev, part.p, actor::kNormGroups, dim, rows,
+                                                 ns);
     PQLG_CHECK_LAUNCH();
     PQLG_CUDA(cudaStreamSynchronize(st));
     count_launch(2);

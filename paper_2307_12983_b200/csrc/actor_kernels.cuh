@@ -43,32 +43,67 @@ struct StepOut {
   uint32_t* status;  // bit3: non-finite action
 };
 
+// Optional fused observation normalisation of the next observation (the
+// actor's next policy input): the running stats are updated from this
+// step's observations before the env step, exactly the stats the reference
+// applies at the next rollout_step (learners.cpp:89, :113).
+struct NextNorm {
+  float* out;         // [N x ld_out] (null: not fused)
+  int64_t ld_out;
+  const float* mean;  // fp32 apply constants
+  const float* inv;
+  const int* identity;
+};
+
 // One warp per env.  Lane-parallel over state dims; the order-sensitive sums
 // (sum a^2, sum s'^2, the per-dim M a dot) are evaluated in the oracle's
-// ascending order.
-static __global__ void env_step_kernel(EnvState e, const float* __restrict__ act, int64_t ld_act,
-                                       StepOut o) {
-  extern __shared__ float sh[];  // [kEnvWarps][D + A]
+// ascending order.  M is staged in shared memory (padded rows, float4
+// loads) and the clamped action kept in registers.
+constexpr int kMaxA = 32;
+static __global__ void __launch_bounds__(32 * kEnvWarps)
+    env_step_kernel(EnvState e, const float* __restrict__ act, int64_t ld_act, StepOut o,
+                    NextNorm nn) {
+  extern __shared__ float4 sh4[];
+  const int Ap = (e.A + 3) & ~3;
+  float* sM = reinterpret_cast<float*>(sh4);             // [D x Ap]
+  float* sv_all = sM + static_cast<int64_t>(e.D) * Ap;  // [kEnvWarps][D]
+  for (int j = threadIdx.x; j < e.D * Ap; j += blockDim.x) {
+    const int d = j / Ap, k = j % Ap;
+    sM[j] = k < e.A ? e.M[static_cast<int64_t>(d) * e.A + k] : 0.0f;
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = blockIdx.x * kEnvWarps + w;
   if (i >= e.N) return;
-  float* sa = sh + w * (e.D + e.A);
-  float* sv = sa + e.A;
+  float* sv = sv_all + w * e.D;
   const float* a_in = act + static_cast<int64_t>(i) * ld_act;
+  float a[kMaxA];
   bool bad = false;
-  for (int k = lane; k < e.A; k += 32) {
-    float u = a_in[k];
-    if (!isfinite(u)) bad = true;
-    u = u < e.low ? e.low : (u > e.high ? e.high : u);
-    sa[k] = u;
+#pragma unroll
+  for (int k = 0; k < kMaxA; ++k) {
+    float u = 0.0f;
+    if (k < e.A) {
+      u = a_in[k];  // broadcast load (all lanes, same address)
+      if (!isfinite(u)) bad = true;
+      u = u < e.low ? e.low : (u > e.high ? e.high : u);
+    }
+    a[k] = u;
   }
-  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(o.status, 8u);
-  __syncwarp();
+  if (bad && lane == 0) atomicOr(o.status, 8u);
   float* s = e.s + static_cast<int64_t>(i) * e.ld;
   for (int d = lane; d < e.D; d += 32) {
     float ma = 0.0f;
-    const float* Mr = e.M + static_cast<int64_t>(d) * e.A;
-    for (int k = 0; k < e.A; ++k) ma = __fadd_rn(ma, __fmul_rn(Mr[k], sa[k]));
+    const float4* Mr = reinterpret_cast<const float4*>(sM + static_cast<int64_t>(d) * Ap);
+#pragma unroll
+    for (int k4 = 0; k4 < kMaxA / 4; ++k4) {
+      if (4 * k4 < e.A) {
+        const float4 m4 = Mr[k4];
+        const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (4 * k4 + u < e.A) ma = __fadd_rn(ma, __fmul_rn(mm[u], a[4 * k4 + u]));
+      }
+    }
     float v = __fadd_rn(__fmul_rn(0.95f, s[d]), __fmul_rn(0.05f, ma));
     v = v < -10.0f ? -10.0f : (v > 10.0f ? 10.0f : v);
     sv[d] = v;
@@ -78,8 +113,18 @@ static __global__ void env_step_kernel(EnvState e, const float* __restrict__ act
   int done_i = 0, trunc_i = 0;
   if (lane == 0) {
     float aa = 0.0f, ss = 0.0f;
-    for (int k = 0; k < e.A; ++k) aa = __fadd_rn(aa, __fmul_rn(sa[k], sa[k]));
-    for (int d = 0; d < e.D; ++d) ss = __fadd_rn(ss, __fmul_rn(sv[d], sv[d]));
+#pragma unroll
+    for (int k = 0; k < kMaxA; ++k)
+      if (k < e.A) aa = __fadd_rn(aa, __fmul_rn(a[k], a[k]));
+    int d = 0;
+    for (; d + 8 <= e.D; d += 8) {
+      float q[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) q[u] = sv[d + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) ss = __fadd_rn(ss, __fmul_rn(q[u], q[u]));
+    }
+    for (; d < e.D; ++d) ss = __fadd_rn(ss, __fmul_rn(sv[d], sv[d]));
     const float reward = -__fadd_rn(__fdiv_rn(ss, static_cast<float>(e.D)),
                                     __fmul_rn(0.01f, __fdiv_rn(aa, static_cast<float>(e.A))));
     const bool terminal = fabsf(sv[0]) > 9.0f;
@@ -97,6 +142,8 @@ static __global__ void env_step_kernel(EnvState e, const float* __restrict__ act
   const uint64_t st0 = e.rng[i];
   float* nxt = o.next_obs + static_cast<int64_t>(i) * o.ld_obs;
   float* bt = o.boot + static_cast<int64_t>(i) * o.ld_obs;
+  const bool id = nn.out ? (*nn.identity != 0) : true;
+  float* xn = nn.out ? nn.out + static_cast<int64_t>(i) * nn.ld_out : nullptr;
   for (int d = lane; d < e.D; d += 32) {
     const float v = sv[d];
     bt[d] = v;  // terminal observation on done, next observation otherwise
@@ -107,8 +154,22 @@ static __global__ void env_step_kernel(EnvState e, const float* __restrict__ act
     }
     s[d] = ns;
     nxt[d] = ns;
+    if (xn) {
+      float z = ns;
+      if (!id) {
+        z = __fmul_rn(__fsub_rn(ns, nn.mean[d]), nn.inv[d]);
+        if (z > 5.0f) z = 5.0f;
+        if (z < -5.0f) z = -5.0f;
+      }
+      xn[d] = z;
+    }
   }
   if (done_i && lane == 0) e.rng[i] = st0 + static_cast<uint64_t>(e.D);
+}
+
+inline size_t env_step_smem(int D, int A) {
+  const int Ap = (A + 3) & ~3;
+  return (static_cast<size_t>(D) * Ap + static_cast<size_t>(kEnvWarps) * D) * sizeof(float);
 }
 
 // reset_all (vecenv.cpp:53-60) + staggered episode_step = i % max_len.
@@ -150,23 +211,39 @@ static __global__ void normalize_kernel(const float* __restrict__ x, int64_t ldx
   }
 }
 
-// Welford over one chunk of rows (row order) for all columns: thread = column.
-static __global__ void norm_chunk_kernel(const float* __restrict__ x, int64_t ldx, int N, int D,
-                                         double* cmean, double* cm2, double* ccount) {
-  const int chunk = blockIdx.x;
-  const int r0 = chunk * kNormChunk, r1 = min(r0 + kNormChunk, N);
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
-    double mean = 0.0, m2 = 0.0, n = 0.0;
-    for (int r = r0; r < r1; ++r) {
-      n += 1.0;
-      const double v = x[static_cast<int64_t>(r) * ldx + d];
-      const double delta = v - mean;
-      mean += delta / n;
-      m2 += delta * (v - mean);
+// Batch moments, parallel and deterministic: warp lanes own columns, warps
+// stride rows; sums are shifted by the batch's first row (no cancellation
+// for offset data) and reduced in fixed order.  partial[(g*D + c)*2 + {0,1}]
+// = (sum (x - x0), sum (x - x0)^2) over row group g.
+constexpr int kNormGroups = 64;
+static __global__ void __launch_bounds__(256)
+    norm_partial_kernel(const float* __restrict__ x, int64_t ldx, int N, int D, double* partial) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  const int g = blockIdx.y;
+  const int per = (N + gridDim.y - 1) / gridDim.y;
+  const int r0 = g * per, r1 = min(r0 + per, N);
+  double s1 = 0.0, s2 = 0.0;
+  if (c < D) {
+    const double shift = x[c];
+    for (int r = r0 + w; r < r1; r += 8) {
+      const double v = static_cast<double>(x[static_cast<int64_t>(r) * ldx + c]) - shift;
+      s1 += v;
+      s2 += v * v;
     }
-    cmean[static_cast<int64_t>(chunk) * D + d] = mean;
-    cm2[static_cast<int64_t>(chunk) * D + d] = m2;
-    if (d == 0) ccount[chunk] = n;
+  }
+  __shared__ double red[8][32][2];
+  red[w][lane][0] = s1;
+  red[w][lane][1] = s2;
+  __syncthreads();
+  if (w == 0 && c < D) {
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      a += red[k][lane][0];
+      b += red[k][lane][1];
+    }
+    partial[(static_cast<int64_t>(g) * D + c) * 2] = a;
+    partial[(static_cast<int64_t>(g) * D + c) * 2 + 1] = b;
   }
 }
 
@@ -179,31 +256,29 @@ struct NormState {
   int* identity;
 };
 
-// Chan merge of the chunk statistics (left fold in chunk order) and of the
-// batch into the running stats; then the fp32 apply constants.  Launched as
-// one block so the count update follows every column's read of it.
-static __global__ void norm_merge_kernel(const double* cmean, const double* cm2,
-                                         const double* ccount, int chunks, int D, int64_t rows,
-                                         NormState s) {
+// Batch (mean, M2) from the partials (groups summed in order), then
+// merge(bcount, bmean, bm2) into the running stats (normalizer.hpp:73-83)
+// and the fp32 apply constants (normalizer.hpp:62-66).  One block, so the
+// count update follows every column's read of it.
+static __global__ void norm_finish_kernel(const float* __restrict__ x, const double* partial,
+                                          int groups, int D, int64_t rows, NormState s) {
   const int64_t n0i = *s.count;
   const int64_t cnt = n0i + rows;
+  const double nb = static_cast<double>(rows);
   for (int d = threadIdx.x; d < D; d += blockDim.x) {
-    double na = ccount[0], ma = cmean[d], m2a = cm2[d];
-    for (int c = 1; c < chunks; ++c) {
-      const double nb = ccount[c], mb = cmean[static_cast<int64_t>(c) * D + d],
-                   m2b = cm2[static_cast<int64_t>(c) * D + d];
-      const double nab = na + nb;
-      const double delta = mb - ma;
-      ma += delta * (nb / nab);
-      m2a += m2b + delta * delta * (na * nb / nab);
-      na = nab;
+    double s1 = 0.0, s2 = 0.0;
+    for (int g = 0; g < groups; ++g) {
+      s1 += partial[(static_cast<int64_t>(g) * D + d) * 2];
+      s2 += partial[(static_cast<int64_t>(g) * D + d) * 2 + 1];
     }
-    // merge(bcount, bmean, bm2) into the running stats (normalizer.hpp:73-83)
-    const double n0 = static_cast<double>(n0i);
-    const double nab = n0 + na;
-    const double delta = ma - s.mean[d];
-    const double mean = s.mean[d] + delta * (na / nab);
-    const double m2 = s.m2[d] + (m2a + delta * delta * (n0 * na / nab));
+    const double bmean = static_cast<double>(x[d]) + s1 / nb;
+    double bm2 = s2 - s1 * s1 / nb;
+    if (bm2 < 0.0) bm2 = 0.0;
+    const double na = static_cast<double>(n0i);
+    const double nab = na + nb;
+    const double delta = bmean - s.mean[d];
+    const double mean = s.mean[d] + delta * (nb / nab);
+    const double m2 = s.m2[d] + (bm2 + delta * delta * (na * nb / nab));
     s.mean[d] = mean;
     s.m2[d] = m2;
     s.mean_f[d] = static_cast<float>(mean);

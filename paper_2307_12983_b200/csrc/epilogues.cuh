@@ -94,59 +94,57 @@ struct PolicyHead {
   uint64_t* noise_state;  // nullable: per-env SplitMix state
   const float* sigma;     // per-env sigma_i
   float low, high;
+  // The normal draws depend only on the env's stream (not on the action
+  // values), so prepare() generates all A of them while the mainloop runs
+  // (A <= 32, one 32-column chunk); chunk() only squashes, adds and clamps.
   struct Row {
-    uint64_t st;
-    float saved;
-    int has_saved;
+    float z[32];
     float sig;
   };
   __device__ void prepare(Row& r, int, int, int m, int, float* scratch) const {
     const int t = threadIdx.x - 64;
     for (int i = t; i < A; i += 128) scratch[i] = bias[i];
-    r.has_saved = 0;
-    r.saved = 0.0f;
+    r.sig = 0.0f;
     if (noise_state && m < M) {
-      r.st = noise_state[m];
       r.sig = sigma[m];
-    } else {
-      r.st = 0;
-      r.sig = 0.0f;
+      if (r.sig > 0.0f) {
+        uint64_t st = noise_state[m];
+        float saved = 0.0f;
+#pragma unroll
+        for (int d = 0; d < 32; d += 2) {
+          if (d < A) {
+            r.z[d] = rng::polar_pair(st, saved);  // y*mult first, x*mult cached
+            r.z[d + 1] = saved;
+          }
+        }
+        noise_state[m] = st;
+      }
     }
     ptx::named_bar_sync(1, 128);
   }
   __device__ bool chunk(Row& r, int, int, int m, int n0, float (&v)[32],
                         const float* scratch) const {
     if (m >= M) return false;
-#pragma unroll 1
+    float* out = act + static_cast<int64_t>(m) * ld_act;
+#pragma unroll
     for (int t = 0; t < 32; ++t) {
       const int n = n0 + t;
-      if (n >= A) break;
-      const float y = __fadd_rn(v[t], scratch[n]);
-      const float th = tanhf(y);
-      float a = __fadd_rn(mid, __fmul_rn(half, th));
-      if (tanh_out) tanh_out[static_cast<int64_t>(m) * ld_tanh + n] = th;
-      if (noise_state) {
-        if (r.sig > 0.0f) {
-          float z;
-          if (r.has_saved) {
-            r.has_saved = 0;
-            z = r.saved;
-          } else {
-            z = rng::polar_pair(r.st, r.saved);
-            r.has_saved = 1;
-          }
-          a = __fadd_rn(a, __fadd_rn(__fmul_rn(z, r.sig), 0.0f));
+      if (n < A) {
+        const float y = __fadd_rn(v[t], scratch[n]);
+        const float th = tanhf(y);
+        float a = __fadd_rn(mid, __fmul_rn(half, th));
+        if (tanh_out) tanh_out[static_cast<int64_t>(m) * ld_tanh + n] = th;
+        if (noise_state) {
+          if (r.sig > 0.0f) a = __fadd_rn(a, __fadd_rn(__fmul_rn(r.z[t], r.sig), 0.0f));
+          if (a < low) a = low;
+          if (a > high) a = high;
         }
-        if (a < low) a = low;
-        if (a > high) a = high;
+        out[n] = a;
       }
-      act[static_cast<int64_t>(m) * ld_act + n] = a;
     }
     return false;
   }
-  __device__ void end(Row& r, int, int, int m, int) const {
-    if (noise_state && m < M) noise_state[m] = r.st;
-  }
+  __device__ void end(Row&, int, int, int, int) const {}
 };
 
 // dgrad output with the ReLU mask of the layer below (from its bitmask),

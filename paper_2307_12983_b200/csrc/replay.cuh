@@ -83,6 +83,25 @@ struct Gather {
 constexpr int kScanBlock = 1024;
 constexpr int kWarpsPerBlock = 8;
 
+// Warp-cooperative row copy.  With 16-byte aligned rows whose strides leave
+// room for the padded tail (wide = true), lanes move float4s; otherwise a
+// scalar loop.
+__device__ __forceinline__ void copy_row(float* __restrict__ dst, const float* __restrict__ src,
+                                         int n, bool wide, int lane) {
+  if (wide) {
+    const int n4 = (n + 3) >> 2;
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (int j = lane; j < n4; j += 32) d4[j] = s4[j];
+  } else {
+    for (int d = lane; d < n; d += 32) dst[d] = src[d];
+  }
+}
+
+__device__ __forceinline__ bool aligned16(const void* p, int64_t ld) {
+  return ((reinterpret_cast<uintptr_t>(p) & 15) == 0) && ((ld & 3) == 0);
+}
+
 __device__ __forceinline__ float normalize1(float x, float mean, float inv) {
   float z = __fmul_rn(__fsub_rn(x, mean), inv);
   if (z > 5.0f) z = 5.0f;
@@ -163,16 +182,16 @@ static __global__ void nstep_emit_kernel(Window w, Slice s, float reward_scale, 
 
   uint32_t h = w.head[e];
   uint32_t c = w.count[e];
+  // float4 paths when the slice rows are 16B aligned with padded strides
+  const bool wide_o = aligned16(s.obs, s.ld_obs) && aligned16(s.boot, s.ld_obs) &&
+                      s.ld_obs >= ((D + 3) & ~3);
+  const bool wide_a = aligned16(s.act, s.ld_act) && s.ld_act >= ((A + 3) & ~3);
   // push: window slot (head + count) % n
   {
     const uint32_t slot = (h + c) % n;
     const size_t wrow = static_cast<size_t>(e) * n + slot;
-    const float* so = s.obs + static_cast<size_t>(e) * s.ld_obs;
-    float* wo = w.obs + wrow * w.ld_obs;
-    for (int d = lane; d < D; d += 32) wo[d] = so[d];
-    const float* sa = s.act + static_cast<size_t>(e) * s.ld_act;
-    float* wa = w.act + wrow * w.ld_act;
-    for (int d = lane; d < A; d += 32) wa[d] = sa[d];
+    copy_row(w.obs + wrow * w.ld_obs, s.obs + static_cast<size_t>(e) * s.ld_obs, D, wide_o, lane);
+    copy_row(w.act + wrow * w.ld_act, s.act + static_cast<size_t>(e) * s.ld_act, A, wide_a, lane);
     if (lane == 0) w.rew[wrow] = __fmul_rn(s.rew[e], reward_scale);
   }
   __syncwarp();
@@ -193,15 +212,11 @@ static __global__ void nstep_emit_kernel(Window w, Slice s, float reward_scale, 
     if (rec + ring.capacity < total) return;
     const uint64_t p = (cursor0 + rec) % ring.capacity;
     const size_t front = static_cast<size_t>(e) * n + h;
-    const float* wo = w.obs + front * w.ld_obs;
-    float* ro = ring.obs + p * ring.ld_obs;
-    for (int d = lane; d < D; d += 32) ro[d] = wo[d];
-    const float* wa = w.act + front * w.ld_act;
-    float* ra = ring.act + p * ring.ld_act;
-    for (int d = lane; d < A; d += 32) ra[d] = wa[d];
-    const float* sb = s.boot + static_cast<size_t>(e) * s.ld_obs;
-    float* rb = ring.boot + p * ring.ld_obs;
-    for (int d = lane; d < D; d += 32) rb[d] = sb[d];
+    // window and ring rows are padded to 16 bytes by construction
+    copy_row(ring.obs + p * ring.ld_obs, w.obs + front * w.ld_obs, D, true, lane);
+    copy_row(ring.act + p * ring.ld_act, w.act + front * w.ld_act, A, true, lane);
+    copy_row(ring.boot + p * ring.ld_obs, s.boot + static_cast<size_t>(e) * s.ld_obs, D, wide_o,
+             lane);
     if (lane == 0) {
       ring.ret[p] = g;
       ring.eff[p] = terminated ? 0.0f : disc;
@@ -263,7 +278,8 @@ static __global__ void state_insert_kernel(StateRing ring, const float* rows, in
   const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
   if (r >= n || r + ring.capacity < n) return;
   const uint64_t p = (ring.state[0] + r) % ring.capacity;
-  for (int d = lane; d < ring.D; d += 32) ring.obs[p * ring.ld + d] = rows[r * ld + d];
+  const bool wide = aligned16(rows, ld) && ld >= ((ring.D + 3) & ~3);
+  copy_row(ring.obs + p * ring.ld, rows + r * ld, ring.D, wide, lane);
 }
 
 // Synthetic pre-fill: obs/boot ~ N(0,1), act ~ U(-1,1),
