@@ -224,6 +224,9 @@ PQLG_API int pqlg_vlearner_adopt_policy(pqlg_vlearner h, const float* flat_host,
 PQLG_API int pqlg_vlearner_adopt_norm(pqlg_vlearner h, const pqlg_norm_stats* norm);
 /* ingest(StepSlice): reward scale + n-step + insert (learners.cpp:144-151) */
 PQLG_API int pqlg_vlearner_ingest(pqlg_vlearner h, const pqlg_step_slice* dev);
+/* ingest from HOST buffers (a CPU-produced StepSlice): copied in on the
+ * learner's stream; returns once the slice may be reused. */
+PQLG_API int pqlg_vlearner_ingest_host(pqlg_vlearner h, const pqlg_step_slice* host);
 PQLG_API int pqlg_vlearner_ready(pqlg_vlearner h, int64_t c_a, int* ready);
 /* update(): one critic update; synchronizes and returns the loss
  * (PQLG_NOT_READY before warm-up, PQLG_ENONFINITE on non-finite). */
@@ -270,6 +273,8 @@ PQLG_API int pqlg_plearner_adopt_norm(pqlg_plearner h, const pqlg_norm_stats* no
 /* ingest(states) = StateBuffer::insert (learners.hpp:117) */
 PQLG_API int pqlg_plearner_ingest(pqlg_plearner h, const float* states_dev, int64_t ld,
                                   uint64_t n);
+PQLG_API int pqlg_plearner_ingest_host(pqlg_plearner h, const float* states_host, int64_t ld,
+                                       uint64_t n);
 PQLG_API int pqlg_plearner_ready(pqlg_plearner h, int64_t c_a, int* ready);
 /* update(): one policy update; synchronizes and returns the actor loss. */
 PQLG_API int pqlg_plearner_update(pqlg_plearner h, float* loss_host);

@@ -87,6 +87,7 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_vlearner_adopt_policy": (i32, [vp, vp, i64]),
     "pqlg_vlearner_adopt_norm": (i32, [vp, P(NormStats)]),
     "pqlg_vlearner_ingest": (i32, [vp, P(StepSlice)]),
+    "pqlg_vlearner_ingest_host": (i32, [vp, P(StepSlice)]),
     "pqlg_vlearner_ready": (i32, [vp, i64, P(i32)]),
     "pqlg_vlearner_update": (i32, [vp, P(f32)]),
     "pqlg_vlearner_update_n": (i32, [vp, i32]),
@@ -108,6 +109,7 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_plearner_adopt_critics": (i32, [vp, vp, vp, i64]),
     "pqlg_plearner_adopt_norm": (i32, [vp, P(NormStats)]),
     "pqlg_plearner_ingest": (i32, [vp, vp, i64, u64]),
+    "pqlg_plearner_ingest_host": (i32, [vp, vp, i64, u64]),
     "pqlg_plearner_ready": (i32, [vp, i64, P(i32)]),
     "pqlg_plearner_update": (i32, [vp, P(f32)]),
     "pqlg_plearner_update_n": (i32, [vp, i32]),

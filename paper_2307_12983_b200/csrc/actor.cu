@@ -16,8 +16,8 @@
 
 namespace pqlg {
 
-// Host copy of the synthetic task's fixed coupling matrix (pql_oracle.c
-// orc_env_create): M[d][k] = 2 * (splitmix64(derive_seed(seed, env, 2^40) +
+// Host copy of the synthetic task's fixed coupling matrix (SURVEY 8(d)
+// synthetic env): M[d][k] = 2 * (splitmix64(derive_seed(seed, env, 2^40) +
 // d*A + k) >> 11) * 2^-53 - 1.
 static std::vector<float> coupling_matrix(uint64_t seed, int D, int A) {
   std::vector<float> M(static_cast<size_t>(D) * A);
@@ -69,6 +69,7 @@ struct DeviceEnv {
   void step(const float* act, int64_t ld_act, const actor::StepOut& o, cudaStream_t st,
             const actor::NextNorm& nn = actor::NextNorm{}) {
     require(A <= actor::kMaxA, "env: act_dim > 32 not supported");
+    require(D <= 32 * actor::kMaxDChunks, "env: obs_dim > 256 not supported");
     const size_t smem = actor::env_step_smem(D, A);
     static bool configured = false;
     if (!configured) {
@@ -76,8 +77,10 @@ struct DeviceEnv {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       configured = true;
     }
-    actor::env_step_kernel<<<(N + actor::kEnvWarps - 1) / actor::kEnvWarps,
-                             32 * actor::kEnvWarps, smem, st>>>(view(), act, ld_act, o, nn);
+    const int tiles = (N + actor::kEnvTile - 1) / actor::kEnvTile;
+    const int blocks = std::min(tiles, 4 * mlp::kSMs);
+    actor::env_step_kernel<<<blocks, 32 * actor::kEnvWarps, smem, st>>>(view(), act, ld_act, o,
+                                                                       nn);
     PQLG_CHECK_LAUNCH();
     count_launch();
   }
@@ -121,6 +124,7 @@ class Actor {
   DevBuf<float> sigma_;
   DevBuf<int64_t> count_;
   DevBuf<double> mean_, m2_, npart_;
+  DevBuf<unsigned int> nticket_;
   DevBuf<float> mean_f_, inv_f_;
   DevBuf<int> identity_;
   DevBuf<uint32_t> status_;
@@ -205,6 +209,7 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
   const int one = 1;
   PQLG_CUDA(cudaMemcpy(identity_.p, &one, 4, cudaMemcpyHostToDevice));
   npart_.alloc(static_cast<size_t>(actor::kNormGroups) * D_ * 2);
+  nticket_.alloc(1);
   status_.alloc(1);
   // first policy input: apply_stats with count 0 is the identity
   actor::normalize_kernel<<<4 * mlp::kSMs, 256, 0, stream_>>>(obs_[0].p, Dp_, Xn_.p, Dp_,
@@ -274,13 +279,11 @@ void Actor::enqueue(int cur) {
   // normalizer_.update(obs_) (learners.cpp:113): it only reads this step's
   // observations, so it runs before the env step and the env kernel can emit
   // the next policy input apply(stats_t, obs_{t+1}) directly.
-  actor::norm_partial_kernel<<<dim3((D + 31) / 32, actor::kNormGroups), 256, 0, st>>>(
-      obs, Dp_, N, D, npart_.p);
-  PQLG_CHECK_LAUNCH();
   actor::NormState ns{count_.p, mean_.p, m2_.p, mean_f_.p, inv_f_.p, identity_.p};
-  actor::norm_finish_kernel<<<1, 256, 0, st>>>(obs, npart_.p, actor::kNormGroups, D, N, ns);
+  actor::norm_update_kernel<<<dim3((D + 31) / 32, actor::kNormGroups), 256, 0, st>>>(
+      obs, Dp_, N, D, npart_.p, nticket_.p, ns);
   PQLG_CHECK_LAUNCH();
-  count_launch(2);
+  count_launch();
   // env_->step(actions) + next-obs normalisation
   actor::StepOut o{obs_[1 - cur].p, boot_.p, rew_.p, term_.p, trunc_.p, nullptr, Dp_, status_.p};
   actor::NextNorm nn{Xn_.p, Dp_, mean_f_.p, inv_f_.p, identity_.p};
@@ -494,16 +497,14 @@ int pqlg_k_normalizer_update(int64_t* count_dev, double* mean_dev, double* m2_de
     if (rows == 0) return;  // normalizer.hpp:34
     DevBuf<double> part(static_cast<size_t>(actor::kNormGroups) * dim * 2);
     DevBuf<int> ident(1);
+    DevBuf<unsigned int> ticket(1);
     const int64_t ldx = ld > 0 ? ld : dim;
-    actor::norm_partial_kernel<<<dim3((dim + 31) / 32, actor::kNormGroups), 256, 0, st>>>(
-        batch_dev, ldx, rows, dim, part.p);
-    PQLG_CHECK_LAUNCH();
     actor::NormState ns{count_dev, mean_dev, m2_dev, mean_f_dev, inv_f_dev, ident.p};
-    actor::norm_finish_kernel<<<1, 256, 0, st>>>(batch_dev, part.p, actor::kNormGroups, dim, rows,
-                                                 ns);
+    actor::norm_update_kernel<<<dim3((dim + 31) / 32, actor::kNormGroups), 256, 0, st>>>(
+        batch_dev, ldx, rows, dim, part.p, ticket.p, ns);
     PQLG_CHECK_LAUNCH();
     PQLG_CUDA(cudaStreamSynchronize(st));
-    count_launch(2);
+    count_launch();
   });
 }
 

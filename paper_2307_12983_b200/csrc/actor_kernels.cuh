@@ -4,7 +4,7 @@
 //
 //   env step       EnvBatch::step contract (vecenv.cpp:84-106) with the
 //                  synthetic task of SURVEY 8(d); float mul/add only, in the
-//                  oracle's order, so states/rewards are bit-exact
+//                  d-ascending order, so states/rewards are bit-exact
 //   normalize      RunningNormalizer::apply_stats (normalizer.hpp:56-70)
 //   norm update    RunningNormalizer::update + merge (normalizer.hpp:33-50,
 //                  :73-83): Welford per 128-row chunk (row order), chunks
@@ -55,121 +55,178 @@ struct NextNorm {
   const int* identity;
 };
 
-// One warp per env.  Lane-parallel over state dims; the order-sensitive sums
-// (sum a^2, sum s'^2, the per-dim M a dot) are evaluated in the oracle's
-// ascending order.  M is staged in shared memory (padded rows, float4
-// loads) and the clamped action kept in registers.
+// Tiles of 32 envs per block iteration (persistent grid, M staged once per
+// block in shared memory):
+//   phase 1  warp per env: s' = clamp(0.95 s + 0.05 M a) lane-parallel over d,
+//            up to 8 independent k-ascending chains per lane; s' -> smem tile
+//   phase 2  thread per env (warp 0): the d-ascending sum of s'^2, reward,
+//            termination, time limit -- the order-sensitive serial sums run
+//            32 envs at a time instead of on one lane of a warp
+//   phase 3  warp per env: boot obs, auto-reset draws, next obs, state and
+//            the fused next-obs normalisation
+// All sums are float mul/add in d-ascending order, so states, rewards and
+// flags are bit-exact.
 constexpr int kMaxA = 32;
+constexpr int kEnvTile = 32;
+constexpr int kMaxDChunks = 8;  // obs_dim <= 256
+
+__device__ __forceinline__ int env_tile_ld(int D) { return D | 1; }  // odd: conflict-free rows
+
 static __global__ void __launch_bounds__(32 * kEnvWarps)
     env_step_kernel(EnvState e, const float* __restrict__ act, int64_t ld_act, StepOut o,
                     NextNorm nn) {
   extern __shared__ float4 sh4[];
-  const int Ap = (e.A + 3) & ~3;
+  const int D = e.D, A = e.A;
+  const int Ap = (A + 3) & ~3;
+  const int ldv = env_tile_ld(D);
   float* sM = reinterpret_cast<float*>(sh4);             // [D x Ap]
-  float* sv_all = sM + static_cast<int64_t>(e.D) * Ap;  // [kEnvWarps][D]
-  for (int j = threadIdx.x; j < e.D * Ap; j += blockDim.x) {
-    const int d = j / Ap, k = j % Ap;
-    sM[j] = k < e.A ? e.M[static_cast<int64_t>(d) * e.A + k] : 0.0f;
+  float* sv = sM + static_cast<int64_t>(D) * Ap;        // [kEnvTile x ldv]  s'
+  float* saa = sv + kEnvTile * ldv;                      // [kEnvTile]        sum a^2
+  int* sdone = reinterpret_cast<int*>(saa + kEnvTile);   // [kEnvTile]
+  for (int idx = threadIdx.x; idx < D * Ap; idx += blockDim.x) {
+    const int d = idx / Ap, k = idx - d * Ap;
+    sM[idx] = k < A ? e.M[static_cast<int64_t>(d) * A + k] : 0.0f;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int i = blockIdx.x * kEnvWarps + w;
-  if (i >= e.N) return;
-  float* sv = sv_all + w * e.D;
-  const float* a_in = act + static_cast<int64_t>(i) * ld_act;
-  float a[kMaxA];
-  bool bad = false;
-#pragma unroll
-  for (int k = 0; k < kMaxA; ++k) {
-    float u = 0.0f;
-    if (k < e.A) {
-      u = a_in[k];  // broadcast load (all lanes, same address)
-      if (!isfinite(u)) bad = true;
-      u = u < e.low ? e.low : (u > e.high ? e.high : u);
-    }
-    a[k] = u;
-  }
-  if (bad && lane == 0) atomicOr(o.status, 8u);
-  float* s = e.s + static_cast<int64_t>(i) * e.ld;
-  for (int d = lane; d < e.D; d += 32) {
-    float ma = 0.0f;
-    const float4* Mr = reinterpret_cast<const float4*>(sM + static_cast<int64_t>(d) * Ap);
-#pragma unroll
-    for (int k4 = 0; k4 < kMaxA / 4; ++k4) {
-      if (4 * k4 < e.A) {
-        const float4 m4 = Mr[k4];
-        const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (4 * k4 + u < e.A) ma = __fadd_rn(ma, __fmul_rn(mm[u], a[4 * k4 + u]));
-      }
-    }
-    float v = __fadd_rn(__fmul_rn(0.95f, s[d]), __fmul_rn(0.05f, ma));
-    v = v < -10.0f ? -10.0f : (v > 10.0f ? 10.0f : v);
-    sv[d] = v;
-  }
-  __syncwarp();
-  // reward / termination / time limit (lane 0, ascending sums)
-  int done_i = 0, trunc_i = 0;
-  if (lane == 0) {
-    float aa = 0.0f, ss = 0.0f;
-#pragma unroll
-    for (int k = 0; k < kMaxA; ++k)
-      if (k < e.A) aa = __fadd_rn(aa, __fmul_rn(a[k], a[k]));
-    int d = 0;
-    for (; d + 8 <= e.D; d += 8) {
-      float q[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) q[u] = sv[d + u];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) ss = __fadd_rn(ss, __fmul_rn(q[u], q[u]));
-    }
-    for (; d < e.D; ++d) ss = __fadd_rn(ss, __fmul_rn(sv[d], sv[d]));
-    const float reward = -__fadd_rn(__fdiv_rn(ss, static_cast<float>(e.D)),
-                                    __fmul_rn(0.01f, __fdiv_rn(aa, static_cast<float>(e.A))));
-    const bool terminal = fabsf(sv[0]) > 9.0f;
-    const int64_t ep = e.episode_step[i] + 1;
-    const bool timeout = ep >= e.max_len;
-    done_i = terminal || timeout;
-    trunc_i = !terminal && timeout;
-    e.episode_step[i] = done_i ? 0 : ep;
-    o.rew[i] = reward;
-    o.term[i] = static_cast<uint8_t>(done_i && !trunc_i);
-    o.trunc[i] = static_cast<uint8_t>(trunc_i);
-    if (o.done) o.done[i] = static_cast<uint8_t>(done_i);
-  }
-  done_i = __shfl_sync(0xffffffffu, done_i, 0);
-  const uint64_t st0 = e.rng[i];
-  float* nxt = o.next_obs + static_cast<int64_t>(i) * o.ld_obs;
-  float* bt = o.boot + static_cast<int64_t>(i) * o.ld_obs;
+  const int nch = (D + 31) >> 5;
   const bool id = nn.out ? (*nn.identity != 0) : true;
-  float* xn = nn.out ? nn.out + static_cast<int64_t>(i) * nn.ld_out : nullptr;
-  for (int d = lane; d < e.D; d += 32) {
-    const float v = sv[d];
-    bt[d] = v;  // terminal observation on done, next observation otherwise
-    float ns = v;
-    if (done_i) {
-      uint64_t st = st0 + static_cast<uint64_t>(d);  // draw d of the reset sequence
-      ns = rng::env_uniform(st, -1.0f, 1.0f);
-    }
-    s[d] = ns;
-    nxt[d] = ns;
-    if (xn) {
-      float z = ns;
-      if (!id) {
-        z = __fmul_rn(__fsub_rn(ns, nn.mean[d]), nn.inv[d]);
-        if (z > 5.0f) z = 5.0f;
-        if (z < -5.0f) z = -5.0f;
+  const int n_tiles = (e.N + kEnvTile - 1) / kEnvTile;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int i0 = tile * kEnvTile;
+    // ---- phase 1
+    for (int j = w; j < kEnvTile && i0 + j < e.N; j += kEnvWarps) {
+      const int i = i0 + j;
+      const float* s = e.s + static_cast<int64_t>(i) * e.ld;
+      float sd[kMaxDChunks];
+#pragma unroll
+      for (int c = 0; c < kMaxDChunks; ++c) {
+        const int d = lane + 32 * c;
+        sd[c] = (c < nch && d < D) ? s[d] : 0.0f;
       }
-      xn[d] = z;
+      const float* a_in = act + static_cast<int64_t>(i) * ld_act;
+      float a[kMaxA];
+      bool bad = false;
+#pragma unroll
+      for (int k = 0; k < kMaxA; ++k) {
+        float u = 0.0f;
+        if (k < A) {
+          u = a_in[k];  // broadcast load
+          if (!isfinite(u)) bad = true;
+          u = u < e.low ? e.low : (u > e.high ? e.high : u);
+        }
+        a[k] = u;
+      }
+      if (bad && lane == 0) atomicOr(o.status, 8u);
+      float acc[kMaxDChunks];
+#pragma unroll
+      for (int c = 0; c < kMaxDChunks; ++c) acc[c] = 0.0f;
+#pragma unroll
+      for (int k4 = 0; k4 < kMaxA / 4; ++k4) {
+        if (4 * k4 < A) {
+#pragma unroll
+          for (int c = 0; c < kMaxDChunks; ++c) {
+            const int d = lane + 32 * c;
+            if (c < nch && d < D) {
+              const float4 m4 = reinterpret_cast<const float4*>(sM + d * Ap)[k4];
+              const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (4 * k4 + u < A) acc[c] = __fadd_rn(acc[c], __fmul_rn(mm[u], a[4 * k4 + u]));
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < kMaxDChunks; ++c) {
+        const int d = lane + 32 * c;
+        if (c < nch && d < D) {
+          float v = __fadd_rn(__fmul_rn(0.95f, sd[c]), __fmul_rn(0.05f, acc[c]));
+          v = v < -10.0f ? -10.0f : (v > 10.0f ? 10.0f : v);
+          sv[j * ldv + d] = v;
+        }
+      }
+      if (lane == 0) {
+        float aa = 0.0f;
+#pragma unroll
+        for (int k = 0; k < kMaxA; ++k)
+          if (k < A) aa = __fadd_rn(aa, __fmul_rn(a[k], a[k]));
+        saa[j] = aa;
+      }
     }
+    __syncthreads();
+    // ---- phase 2
+    if (w == 0) {
+      const int i = i0 + lane;
+      int done_i = 0;
+      if (i < e.N) {
+        const float* row = sv + lane * ldv;
+        float ss = 0.0f;
+        int d = 0;
+        for (; d + 8 <= D; d += 8) {
+          float q[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) q[u] = row[d + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) ss = __fadd_rn(ss, __fmul_rn(q[u], q[u]));
+        }
+        for (; d < D; ++d) ss = __fadd_rn(ss, __fmul_rn(row[d], row[d]));
+        const float reward = -__fadd_rn(__fdiv_rn(ss, static_cast<float>(D)),
+                                        __fmul_rn(0.01f, __fdiv_rn(saa[lane], static_cast<float>(A))));
+        const bool terminal = fabsf(row[0]) > 9.0f;
+        const int64_t ep = e.episode_step[i] + 1;
+        const bool timeout = ep >= e.max_len;
+        done_i = terminal || timeout;
+        const int trunc_i = !terminal && timeout;
+        e.episode_step[i] = done_i ? 0 : ep;
+        o.rew[i] = reward;
+        o.term[i] = static_cast<uint8_t>(done_i && !trunc_i);
+        o.trunc[i] = static_cast<uint8_t>(trunc_i);
+        if (o.done) o.done[i] = static_cast<uint8_t>(done_i);
+      }
+      sdone[lane] = done_i;
+    }
+    __syncthreads();
+    // ---- phase 3
+    for (int j = w; j < kEnvTile && i0 + j < e.N; j += kEnvWarps) {
+      const int i = i0 + j;
+      const int done_i = sdone[j];
+      const uint64_t st0 = e.rng[i];
+      float* s = e.s + static_cast<int64_t>(i) * e.ld;
+      float* nxt = o.next_obs + static_cast<int64_t>(i) * o.ld_obs;
+      float* bt = o.boot + static_cast<int64_t>(i) * o.ld_obs;
+      float* xn = nn.out ? nn.out + static_cast<int64_t>(i) * nn.ld_out : nullptr;
+      for (int d = lane; d < D; d += 32) {
+        const float v = sv[j * ldv + d];
+        bt[d] = v;  // terminal observation on done, next observation otherwise
+        float ns = v;
+        if (done_i) {
+          uint64_t st = st0 + static_cast<uint64_t>(d);  // draw d of the reset sequence
+          ns = rng::env_uniform(st, -1.0f, 1.0f);
+        }
+        s[d] = ns;
+        nxt[d] = ns;
+        if (xn) {
+          float z = ns;
+          if (!id) {
+            z = __fmul_rn(__fsub_rn(ns, nn.mean[d]), nn.inv[d]);
+            if (z > 5.0f) z = 5.0f;
+            if (z < -5.0f) z = -5.0f;
+          }
+          xn[d] = z;
+        }
+      }
+      if (done_i && lane == 0) e.rng[i] = st0 + static_cast<uint64_t>(D);
+    }
+    // the next tile's phase 1 writes only rows owned by the same warp; saa /
+    // sdone are rewritten after the next barrier
   }
-  if (done_i && lane == 0) e.rng[i] = st0 + static_cast<uint64_t>(e.D);
 }
 
 inline size_t env_step_smem(int D, int A) {
   const int Ap = (A + 3) & ~3;
-  return (static_cast<size_t>(D) * Ap + static_cast<size_t>(kEnvWarps) * D) * sizeof(float);
+  return (static_cast<size_t>(D) * Ap + static_cast<size_t>(kEnvTile) * (D | 1) + 2 * kEnvTile) *
+         sizeof(float);
 }
 
 // reset_all (vecenv.cpp:53-60) + staggered episode_step = i % max_len.
@@ -211,13 +268,27 @@ static __global__ void normalize_kernel(const float* __restrict__ x, int64_t ldx
   }
 }
 
-// Batch moments, parallel and deterministic: warp lanes own columns, warps
-// stride rows; sums are shifted by the batch's first row (no cancellation
-// for offset data) and reduced in fixed order.  partial[(g*D + c)*2 + {0,1}]
-// = (sum (x - x0), sum (x - x0)^2) over row group g.
+struct NormState {
+  int64_t* count;
+  double* mean;
+  double* m2;
+  float* mean_f;
+  float* inv_f;
+  int* identity;
+};
+
+// RunningNormalizer::update (normalizer.hpp:33-50, :73-83) in one launch,
+// parallel and deterministic.  Grid (ceil(D/32), kNormGroups): warp lanes own
+// columns, warps stride the group's rows; sums are shifted by the batch's
+// first row (no cancellation for offset data).  The last block to finish
+// (atomic ticket) reduces the group partials per column in fixed order
+// (lane-strided sums + xor butterfly), forms the batch (mean, M2), merges it
+// into the running stats with Chan's formula and refreshes the fp32 apply
+// constants (normalizer.hpp:62-66).
 constexpr int kNormGroups = 64;
 static __global__ void __launch_bounds__(256)
-    norm_partial_kernel(const float* __restrict__ x, int64_t ldx, int N, int D, double* partial) {
+    norm_update_kernel(const float* __restrict__ x, int64_t ldx, int N, int D, double* partial,
+                       unsigned int* ticket, NormState s) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   const int g = blockIdx.y;
@@ -226,10 +297,22 @@ static __global__ void __launch_bounds__(256)
   double s1 = 0.0, s2 = 0.0;
   if (c < D) {
     const double shift = x[c];
-    for (int r = r0 + w; r < r1; r += 8) {
-      const double v = static_cast<double>(x[static_cast<int64_t>(r) * ldx + c]) - shift;
-      s1 += v;
-      s2 += v * v;
+    int r = r0 + w;
+    for (; r + 24 < r1; r += 32) {
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = x[static_cast<int64_t>(r + 8 * u) * ldx + c];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double t = static_cast<double>(v[u]) - shift;
+        s1 += t;
+        s2 += t * t;
+      }
+    }
+    for (; r < r1; r += 8) {
+      const double t = static_cast<double>(x[static_cast<int64_t>(r) * ldx + c]) - shift;
+      s1 += t;
+      s2 += t * t;
     }
   }
   __shared__ double red[8][32][2];
@@ -245,49 +328,48 @@ static __global__ void __launch_bounds__(256)
     partial[(static_cast<int64_t>(g) * D + c) * 2] = a;
     partial[(static_cast<int64_t>(g) * D + c) * 2 + 1] = b;
   }
-}
-
-struct NormState {
-  int64_t* count;
-  double* mean;
-  double* m2;
-  float* mean_f;
-  float* inv_f;
-  int* identity;
-};
-
-// Batch (mean, M2) from the partials (groups summed in order), then
-// merge(bcount, bmean, bm2) into the running stats (normalizer.hpp:73-83)
-// and the fp32 apply constants (normalizer.hpp:62-66).  One block, so the
-// count update follows every column's read of it.
-static __global__ void norm_finish_kernel(const float* __restrict__ x, const double* partial,
-                                          int groups, int D, int64_t rows, NormState s) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
   const int64_t n0i = *s.count;
-  const int64_t cnt = n0i + rows;
-  const double nb = static_cast<double>(rows);
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+  const int64_t cnt = n0i + N;
+  const double nb = static_cast<double>(N);
+  const double na = static_cast<double>(n0i);
+  const double nab = na + nb;
+  const int groups = gridDim.y;
+  for (int d = w; d < D; d += blockDim.x / 32) {
     double s1 = 0.0, s2 = 0.0;
-    for (int g = 0; g < groups; ++g) {
-      s1 += partial[(static_cast<int64_t>(g) * D + d) * 2];
-      s2 += partial[(static_cast<int64_t>(g) * D + d) * 2 + 1];
+    for (int k = lane; k < groups; k += 32) {
+      s1 += __ldcg(partial + (static_cast<int64_t>(k) * D + d) * 2);
+      s2 += __ldcg(partial + (static_cast<int64_t>(k) * D + d) * 2 + 1);
     }
-    const double bmean = static_cast<double>(x[d]) + s1 / nb;
-    double bm2 = s2 - s1 * s1 / nb;
-    if (bm2 < 0.0) bm2 = 0.0;
-    const double na = static_cast<double>(n0i);
-    const double nab = na + nb;
-    const double delta = bmean - s.mean[d];
-    const double mean = s.mean[d] + delta * (nb / nab);
-    const double m2 = s.m2[d] + (bm2 + delta * delta * (na * nb / nab));
-    s.mean[d] = mean;
-    s.m2[d] = m2;
-    s.mean_f[d] = static_cast<float>(mean);
-    s.inv_f[d] = static_cast<float>(1.0 / sqrt(m2 / static_cast<double>(cnt) + 1e-8));
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+      const double bmean = static_cast<double>(x[d]) + s1 / nb;
+      double bm2 = s2 - s1 * s1 / nb;
+      if (bm2 < 0.0) bm2 = 0.0;
+      const double delta = bmean - s.mean[d];
+      const double mean = s.mean[d] + delta * (nb / nab);
+      const double m2 = s.m2[d] + (bm2 + delta * delta * (na * nb / nab));
+      s.mean[d] = mean;
+      s.m2[d] = m2;
+      s.mean_f[d] = static_cast<float>(mean);
+      s.inv_f[d] = static_cast<float>(1.0 / sqrt(m2 / static_cast<double>(cnt) + 1e-8));
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     *s.count = cnt;
     *s.identity = cnt <= 1 ? 1 : 0;
+    *ticket = 0u;
   }
 }
 

@@ -22,6 +22,7 @@ class VLearner {
   void adopt_policy(const float* flat_host, int64_t version);
   void adopt_norm(int64_t count, const double* mean, const double* m2);
   void ingest(const replay::Slice& s);
+  void ingest_host(const pqlg_step_slice& host);  // copy-in path for a host StepSlice
   bool ready(int64_t c_a);
   float update();
   void update_n(int n);
@@ -58,6 +59,8 @@ class VLearner {
   WeightMirror lagged_head_;
   std::unique_ptr<DeviceReplay> replay_;
   std::unique_ptr<DeviceNStep> nstep_;
+  DevBuf<float> in_f_;     // host-ingest staging: obs | act | boot | rew
+  DevBuf<uint8_t> in_u8_;  // term | trunc
   DeviceNorm norm_;
   DevBuf<replay::SamplerState> sampler_;
   bool mt_mode_ = false;
@@ -105,6 +108,7 @@ class PLearner {
   void adopt_critics_device(const float* q1_dev, const float* q2_dev, int64_t version);
   void adopt_norm(int64_t count, const double* mean, const double* m2);
   void ingest(const float* states_dev, int64_t ld, uint64_t n);
+  void ingest_host(const float* states_host, int64_t ld, uint64_t n);
   bool ready(int64_t c_a);
   float update();
   void update_n(int n);
@@ -137,6 +141,7 @@ class PLearner {
   DevBuf<float> pol_, m_, v_, grads_, q_;
   WeightMirror head_;
   std::unique_ptr<DeviceStates> states_;
+  DevBuf<float> in_f_;  // host-ingest staging
   DeviceNorm norm_;
   DevBuf<replay::SamplerState> sampler_;
   bool mt_mode_ = false;

@@ -414,6 +414,18 @@ void PLearner::ingest(const float* states, int64_t ld, uint64_t n) {
   states_->insert(states, ld, n, stream_);
 }
 
+// PolicyLearnerCore::ingest(const MatF&) (learners.hpp:121) from host rows.
+void PLearner::ingest_host(const float* states, int64_t ld, uint64_t n) {
+  if (n == 0) return;
+  require(states != nullptr, "ingest: null states");
+  const int64_t Dp = round_up(D_, 4);
+  if (in_f_.n < n * Dp) in_f_.alloc(n * Dp);
+  PQLG_CUDA(cudaMemcpy2DAsync(in_f_.p, Dp * 4, states, ld * 4, D_ * 4, n, cudaMemcpyHostToDevice,
+                              stream_));
+  ingest(in_f_.p, Dp, n);
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+}
+
 bool PLearner::ready(int64_t c_a) {
   return c_a >= cfg_.warm_up && states_->size() >= static_cast<uint64_t>(B_);
 }
@@ -547,6 +559,10 @@ int pqlg_plearner_adopt_norm(pqlg_plearner h, const pqlg_norm_stats* n) {
 
 int pqlg_plearner_ingest(pqlg_plearner h, const float* states_dev, int64_t ld, uint64_t n) {
   return guarded([&] { h->p->ingest(states_dev, ld > 0 ? ld : h->p->obs_dim(), n); });
+}
+
+int pqlg_plearner_ingest_host(pqlg_plearner h, const float* states_host, int64_t ld, uint64_t n) {
+  return guarded([&] { h->p->ingest_host(states_host, ld > 0 ? ld : h->p->obs_dim(), n); });
 }
 
 int pqlg_plearner_ready(pqlg_plearner h, int64_t c_a, int* ready) {

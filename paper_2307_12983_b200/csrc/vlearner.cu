@@ -381,6 +381,34 @@ void VLearner::adopt_norm(int64_t count, const double* mean, const double* m2) {
 
 void VLearner::ingest(const replay::Slice& s) { nstep_->push(s, reward_scale_, *replay_, stream_); }
 
+// Host StepSlice (CriticLearnerCore::ingest takes host matrices,
+// learners.cpp:144-151): staged into device buffers on the learner's stream.
+void VLearner::ingest_host(const pqlg_step_slice& h) {
+  const int N = cfg_.n_envs, D = D_, A = A_;
+  const int64_t lo = h.ld_obs > 0 ? h.ld_obs : D, la = h.ld_act > 0 ? h.ld_act : A;
+  require(h.obs && h.act && h.boot_obs && h.rew && h.term && h.trunc, "ingest: null slice field");
+  const int Dp = static_cast<int>(round_up(D, 4)), Ap = static_cast<int>(round_up(A, 4));  // 16-byte rows: vector gathers
+  const size_t nf = static_cast<size_t>(N) * (2 * Dp + Ap + 1);
+  if (in_f_.n < nf) in_f_.alloc(nf);
+  if (in_u8_.n < 2u * N) in_u8_.alloc(2u * N);
+  float* obs = in_f_.p;
+  float* boot = obs + static_cast<size_t>(N) * Dp;
+  float* act = boot + static_cast<size_t>(N) * Dp;
+  float* rew = act + static_cast<size_t>(N) * Ap;
+  auto h2d2 = [&](float* dst, int64_t ldd, int w, const float* src, int64_t ld) {
+    PQLG_CUDA(cudaMemcpy2DAsync(dst, ldd * 4, src, ld * 4, w * 4, N, cudaMemcpyHostToDevice,
+                                stream_));
+  };
+  h2d2(obs, Dp, D, h.obs, lo);
+  h2d2(boot, Dp, D, h.boot_obs, lo);
+  h2d2(act, Ap, A, h.act, la);
+  PQLG_CUDA(cudaMemcpyAsync(rew, h.rew, N * 4, cudaMemcpyHostToDevice, stream_));
+  PQLG_CUDA(cudaMemcpyAsync(in_u8_.p, h.term, N, cudaMemcpyHostToDevice, stream_));
+  PQLG_CUDA(cudaMemcpyAsync(in_u8_.p + N, h.trunc, N, cudaMemcpyHostToDevice, stream_));
+  ingest(replay::Slice{obs, act, boot, rew, in_u8_.p, in_u8_.p + N, Dp, Ap});
+  PQLG_CUDA(cudaStreamSynchronize(stream_));  // the host slice may be reused on return
+}
+
 bool VLearner::ready(int64_t c_a) {
   return c_a >= cfg_.warm_up && replay_->size() >= static_cast<uint64_t>(B_);
 }
@@ -596,6 +624,13 @@ int pqlg_vlearner_ingest(pqlg_vlearner h, const pqlg_step_slice* s) {
     replay::Slice sl{s->obs, s->act, s->boot_obs, s->rew, s->term, s->trunc,
                      s->ld_obs > 0 ? s->ld_obs : D, s->ld_act > 0 ? s->ld_act : A};
     h->v->ingest(sl);
+  });
+}
+
+int pqlg_vlearner_ingest_host(pqlg_vlearner h, const pqlg_step_slice* s) {
+  return guarded([&] {
+    require(s != nullptr, "ingest_host: null slice");
+    h->v->ingest_host(*s);
   });
 }
 

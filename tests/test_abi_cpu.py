@@ -77,3 +77,36 @@ def test_product_does_not_touch_the_oracle():
         text = p.read_text()
         assert "oracle" not in text.lower().replace("oracle (", ""), p
         assert "libpqlref" not in text and "/root/reference" not in text, p
+
+
+def test_cpp_layer_compiles_and_maps_errors(tmp_path):
+    """include/pqlg.hpp (the C++ layer a reference build would include, see
+    INTEGRATION.md) compiles against the library and maps ABI statuses to the
+    reference's exception types; without a GPU, construction must throw
+    std::runtime_error (no CPU fallback)."""
+    import shutil
+    import subprocess
+    if shutil.which("g++") is None:
+        pytest.skip("no g++")
+    src = tmp_path / "t.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include "pqlg.hpp"
+int main(int argc, char**) {
+  if (pqlg_abi_version() <= 0) return 2;
+  pqlg_config cfg; pqlg_config_default(&cfg);
+  pqlg_task_dims dims{4, 2, -1.0f, 1.0f};
+  cfg.batch_size = -1;
+  try { pqlg::VLearner v(cfg, dims, 1); return 3; }
+  catch (const std::invalid_argument&) { std::puts("einval"); }
+  catch (const std::runtime_error&) { std::puts("runtime"); }
+  return 0;
+}
+''')
+    lib = ROOT / "paper_2307_12983_b200"
+    exe = tmp_path / "t"
+    subprocess.run(["g++", "-std=c++17", "-Wall", "-Werror", f"-I{ROOT / 'include'}", str(src),
+                    f"-L{lib}", "-lpqlg", f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out
+    assert out.stdout.strip() in ("einval", "runtime")

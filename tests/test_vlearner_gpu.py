@@ -202,3 +202,45 @@ def test_ingest_ready_and_not_ready():
     _lib.call("pqlg_vlearner_ready", h, 31, C.byref(r))
     assert r.value == 0  # warm_up = 32 (learners.cpp:153-155)
     _lib.call("pqlg_vlearner_destroy", h)
+
+
+def _replay_rows(h, D, A):
+    rp = C.c_void_p()
+    _lib.call("pqlg_vlearner_replay", h, C.byref(rp))
+    n = C.c_uint64()
+    _lib.call("pqlg_replay_size", rp, C.byref(n))
+    n = n.value
+    out = [np.zeros((n, D), np.float32), np.zeros((n, A), np.float32),
+           np.zeros((n, D), np.float32), np.zeros(n, np.float32), np.zeros(n, np.float32)]
+    _lib.call("pqlg_replay_read_rows", rp, 0, n, *(ptr(x) for x in out))
+    return out
+
+
+def test_ingest_host_equals_device_ingest():
+    """pqlg_vlearner_ingest_host (CriticLearnerCore::ingest on a host
+    StepSlice, learners.cpp:144-151) stores exactly what the device-view
+    ingest stores."""
+    import torch
+    D, A, N = 7, 3, 8
+    hd = make_vl(D, A, 32, 2, 8, 256, n_envs=N)
+    hh = make_vl(D, A, 32, 2, 8, 256, n_envs=N)
+    rng = np.random.default_rng(3)
+    for t in range(9):
+        obs = rng.standard_normal((N, D)).astype(np.float32)
+        act = rng.uniform(-1, 1, (N, A)).astype(np.float32)
+        boot = rng.standard_normal((N, D)).astype(np.float32)
+        rew = rng.standard_normal(N).astype(np.float32)
+        term = (rng.random(N) < 0.15).astype(np.uint8)
+        trunc = ((rng.random(N) < 0.1) & (term == 0)).astype(np.uint8)
+        hs = _lib.StepSlice(ptr(obs), ptr(act), ptr(boot), ptr(rew), ptr(term), ptr(trunc), 0, 0)
+        _lib.call("pqlg_vlearner_ingest_host", hh, C.byref(hs))
+        dev = [torch.from_numpy(x).cuda() for x in (obs, act, boot, rew, term, trunc)]
+        ds = _lib.StepSlice(*(x.data_ptr() for x in dev), 0, 0)
+        _lib.call("pqlg_vlearner_ingest", hd, C.byref(ds))
+        torch.cuda.synchronize()
+    a, b = _replay_rows(hd, D, A), _replay_rows(hh, D, A)
+    assert len(a[3]) > 0
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    for h in (hd, hh):
+        _lib.call("pqlg_vlearner_destroy", h)
