@@ -61,10 +61,7 @@ struct DeviceEnv {
     return actor::EnvState{s.p, ld, M.p, ep.p, rng.p, N, D, A, max_len, low, high};
   }
   void reset(float* obs, int64_t ld_obs, cudaStream_t st) {
-    actor::env_reset_kernel<<<(N + actor::kEnvWarps - 1) / actor::kEnvWarps,
-                              32 * actor::kEnvWarps, 0, st>>>(view(), obs, ld_obs, offset);
-    PQLG_CHECK_LAUNCH();
-    count_launch();
+    launch(actor::env_reset_kernel, dim3((N + actor::kEnvWarps - 1) / actor::kEnvWarps), dim3(32 * actor::kEnvWarps), 0, st, view(), obs, ld_obs, offset);
   }
   void step(const float* act, int64_t ld_act, const actor::StepOut& o, cudaStream_t st,
             const actor::NextNorm& nn = actor::NextNorm{}) {
@@ -79,10 +76,8 @@ struct DeviceEnv {
     }
     const int tiles = (N + actor::kEnvTile - 1) / actor::kEnvTile;
     const int blocks = std::min(tiles, 4 * mlp::kSMs);
-    actor::env_step_kernel<<<blocks, 32 * actor::kEnvWarps, smem, st>>>(view(), act, ld_act, o,
+    launch(actor::env_step_kernel, dim3(blocks), dim3(32 * actor::kEnvWarps), smem, st, view(), act, ld_act, o,
                                                                        nn);
-    PQLG_CHECK_LAUNCH();
-    count_launch();
   }
 };
 
@@ -212,11 +207,9 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
   nticket_.alloc(1);
   status_.alloc(1);
   // first policy input: apply_stats with count 0 is the identity
-  actor::normalize_kernel<<<4 * mlp::kSMs, 256, 0, stream_>>>(obs_[0].p, Dp_, Xn_.p, Dp_,
+  launch(actor::normalize_kernel, dim3(4 * mlp::kSMs), dim3(256), 0, stream_, obs_[0].p, Dp_, Xn_.p, Dp_,
                                                                mean_f_.p, inv_f_.p, identity_.p,
                                                                N_, D_);
-  PQLG_CHECK_LAUNCH();
-  count_launch();
   build();
   PQLG_CUDA(cudaStreamSynchronize(stream_));
 }
@@ -280,10 +273,7 @@ void Actor::enqueue(int cur) {
   // observations, so it runs before the env step and the env kernel can emit
   // the next policy input apply(stats_t, obs_{t+1}) directly.
   actor::NormState ns{count_.p, mean_.p, m2_.p, mean_f_.p, inv_f_.p, identity_.p};
-  actor::norm_update_kernel<<<dim3((D + 31) / 32, actor::kNormGroups), 256, 0, st>>>(
-      obs, Dp_, N, D, npart_.p, nticket_.p, ns);
-  PQLG_CHECK_LAUNCH();
-  count_launch();
+  launch(actor::norm_update_kernel, dim3(dim3((D + 31) / 32, actor::kNormGroups)), dim3(256), 0, st, obs, Dp_, N, D, npart_.p, nticket_.p, ns);
   // env_->step(actions) + next-obs normalisation
   actor::StepOut o{obs_[1 - cur].p, boot_.p, rew_.p, term_.p, trunc_.p, nullptr, Dp_, status_.p};
   actor::NextNorm nn{Xn_.p, Dp_, mean_f_.p, inv_f_.p, identity_.p};
@@ -482,10 +472,7 @@ int pqlg_env_step(pqlg_env h, const float* act_dev, int64_t ld_act, float* next_
 int pqlg_k_apply_noise(float* act_dev, int64_t ld, int n, int act_dim, const float* sigma_dev,
                        float low, float high, uint64_t* states_dev, void* stream) {
   return guarded([&] {
-    actor::noise_kernel<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-        act_dev, ld > 0 ? ld : act_dim, n, act_dim, sigma_dev, low, high, states_dev);
-    PQLG_CHECK_LAUNCH();
-    count_launch();
+    launch(actor::noise_kernel, dim3((n + 127) / 128), dim3(128), 0, static_cast<cudaStream_t>(stream), act_dev, ld > 0 ? ld : act_dim, n, act_dim, sigma_dev, low, high, states_dev);
   });
 }
 
@@ -500,11 +487,8 @@ int pqlg_k_normalizer_update(int64_t* count_dev, double* mean_dev, double* m2_de
     DevBuf<unsigned int> ticket(1);
     const int64_t ldx = ld > 0 ? ld : dim;
     actor::NormState ns{count_dev, mean_dev, m2_dev, mean_f_dev, inv_f_dev, ident.p};
-    actor::norm_update_kernel<<<dim3((dim + 31) / 32, actor::kNormGroups), 256, 0, st>>>(
-        batch_dev, ldx, rows, dim, part.p, ticket.p, ns);
-    PQLG_CHECK_LAUNCH();
+    launch(actor::norm_update_kernel, dim3(dim3((dim + 31) / 32, actor::kNormGroups)), dim3(256), 0, st, batch_dev, ldx, rows, dim, part.p, ticket.p, ns);
     PQLG_CUDA(cudaStreamSynchronize(st));
-    count_launch();
   });
 }
 

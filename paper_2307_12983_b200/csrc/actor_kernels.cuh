@@ -12,6 +12,7 @@
 //   noise          explore::apply_noise (noise.hpp:56-72), bit-exact
 #pragma once
 
+#include "pdl.cuh"
 #include <cstdint>
 
 #include "rng.cuh"
@@ -88,6 +89,7 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
     sM[idx] = k < A ? e.M[static_cast<int64_t>(d) * A + k] : 0.0f;
   }
   __syncthreads();
+  pdl::entry();  // M is constant: staged while the previous kernel drains
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nch = (D + 31) >> 5;
   const bool id = nn.out ? (*nn.identity != 0) : true;
@@ -231,6 +233,7 @@ inline size_t env_step_smem(int D, int A) {
 
 // reset_all (vecenv.cpp:53-60) + staggered episode_step = i % max_len.
 static __global__ void env_reset_kernel(EnvState e, float* obs, int64_t ld_obs, int env_offset) {
+  pdl::entry();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = blockIdx.x * kEnvWarps + w;
   if (i >= e.N) return;
@@ -252,6 +255,7 @@ static __global__ void env_reset_kernel(EnvState e, float* obs, int64_t ld_obs, 
 static __global__ void normalize_kernel(const float* __restrict__ x, int64_t ldx, float* out,
                                         int64_t ldo, const float* mean, const float* inv,
                                         const int* identity, int N, int D) {
+  pdl::entry();
   const int64_t n = static_cast<int64_t>(N) * D;
   const bool id = *identity != 0;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
@@ -289,6 +293,7 @@ constexpr int kNormGroups = 64;
 static __global__ void __launch_bounds__(256)
     norm_update_kernel(const float* __restrict__ x, int64_t ldx, int N, int D, double* partial,
                        unsigned int* ticket, NormState s) {
+  pdl::entry();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   const int g = blockIdx.y;
@@ -376,6 +381,7 @@ static __global__ void __launch_bounds__(256)
 // Standalone apply_noise (op-level hook): one thread per env row.
 static __global__ void noise_kernel(float* act, int64_t ld, int N, int A, const float* sigma,
                                     float low, float high, uint64_t* states) {
+  pdl::entry();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   float* row = act + static_cast<int64_t>(i) * ld;

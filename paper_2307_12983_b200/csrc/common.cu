@@ -1,5 +1,7 @@
 #include "common.h"
 
+#include <cstdlib>
+
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -86,6 +88,14 @@ CUtensorMap make_tmap_3d(const void* base, uint64_t inner, uint64_t mid, uint64_
 }
 
 std::atomic<uint64_t> g_launches{0};
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PQLG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 }  // namespace pqlg
 

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "../../include/pqlg.h"
 
@@ -40,6 +41,27 @@ void set_last_error(const std::string& msg);
 // Kernel launches issued by this library (reported through pqlg_launch_count).
 extern std::atomic<uint64_t> g_launches;
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Every library kernel is launched through launch(): with the programmatic
+// stream-serialisation attribute (PDL, see pdl.cuh) unless PQLG_PDL=0.
+bool pdl_enabled();
+
+template <class... KArgs, class... Args>
+void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+            Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PQLG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+  count_launch();
+}
 
 // Wraps an ABI entry point: converts exceptions to status codes.
 template <class F>

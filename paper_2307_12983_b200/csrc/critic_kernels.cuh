@@ -10,6 +10,7 @@
 //                        gradient partials (scalar.hpp:42-55)
 #pragma once
 
+#include "pdl.cuh"
 #include <cstdint>
 
 namespace pqlg::critic {
@@ -41,6 +42,7 @@ struct TdArgs {
 };
 
 static __global__ void td_target_kernel(TdArgs a) {
+  pdl::entry();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b == 0) *a.step += 1;
   if (b >= a.B) return;
@@ -69,6 +71,7 @@ struct LossArgs {
 };
 
 static __global__ void __launch_bounds__(kRowThreads) critic_loss_kernel(LossArgs a) {
+  pdl::entry();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   double l = 0.0;
   if (b < a.B) {
@@ -109,6 +112,7 @@ static __global__ void __launch_bounds__(kRowThreads) critic_loss_kernel(LossArg
 // ddpg_actor_loss row head: pick1 = q1 <= q2; loss -= min; upstream of the
 // picked critic -1/B (ddpg.hpp:100-105).
 static __global__ void __launch_bounds__(kRowThreads) actor_pick_kernel(LossArgs a) {
+  pdl::entry();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   double l = 0.0;
   if (b < a.B) {
@@ -171,6 +175,7 @@ struct HeadBwdArgs {
 
 static __global__ void __launch_bounds__(kHeadThreads)
     head_backward_kernel(const __grid_constant__ HeadBwdArgs a) {
+  pdl::entry();
   const int tile = blockIdx.x, k = blockIdx.y;
   const int b0 = tile * kHeadRows;
   const int b1 = min(b0 + kHeadRows, a.B);
@@ -223,6 +228,7 @@ struct HeadInputGradArgs {
 };
 
 static __global__ void head_input_grad_kernel(const __grid_constant__ HeadInputGradArgs a) {
+  pdl::entry();
   const int k = blockIdx.y;
   const int64_t n = static_cast<int64_t>(a.B) * a.H;
   const int words = a.H >> 5;
@@ -253,6 +259,7 @@ struct PolicyHeadBwdArgs {
 };
 
 static __global__ void policy_head_backward_kernel(const __grid_constant__ PolicyHeadBwdArgs a) {
+  pdl::entry();
   const int tile = blockIdx.x;
   const int b0 = tile * a.rows_per_tile;
   const int b1 = min(b0 + a.rows_per_tile, a.B);

@@ -50,9 +50,7 @@ void launch(const Operands& ops, const Problem& p, int groups, const Epi& epi, c
     configured = true;
   }
   dim3 grid((p.M + kBM - 1) / kBM, (p.N + BN - 1) / BN, p.splits * groups);
-  kern<<<grid, kThreads, L::kDynamic, st>>>(ops, p, epi);
-  PQLG_CHECK_LAUNCH();
-  count_launch();
+  ::pqlg::launch(kern, grid, dim3(kThreads), L::kDynamic, st, ops, p, epi);
 }
 
 }  // namespace pqlg::gemm

@@ -27,6 +27,7 @@
 
 #include <cstdint>
 
+#include "pdl.cuh"
 #include "ptx.cuh"
 
 namespace pqlg::gemm {
@@ -180,6 +181,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
+  // everything above overlapped the previous kernel's tail (PDL)
+  pdl::entry();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {

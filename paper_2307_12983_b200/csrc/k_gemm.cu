@@ -3,6 +3,7 @@
 // learners' epilogue path (bias + ReLU, TMA store, split-K partials + a
 // fixed-order reduction).  Used by the per-op parity tests and the bench's
 // roofline measurement.
+#include "pdl.cuh"
 #include "epilogues.cuh"
 #include "gemm_host.cuh"
 
@@ -11,6 +12,7 @@ namespace {
 
 __global__ void reduce_splits(const float* W, int splits, int M, int N, float* D, int ldd,
                               const float* bias, int relu) {
+  pdl::entry();
   const size_t total = static_cast<size_t>(M) * N;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -41,9 +43,7 @@ void run(const float* A, const float* B, float* D, const float* bias, int M, int
   ops.d[0] = ops.d[1] = make_tmap_3d(W, N, M, p.splits, N, static_cast<uint64_t>(M) * N, 32, 32,
                                      Swz::k128);
   gemm::launch<BN, AMN, BMN>(ops, p, 1, epi::Partial{}, st);
-  reduce_splits<<<296, 256, 0, st>>>(W, p.splits, M, N, D, ldd, bias, relu);
-  PQLG_CHECK_LAUNCH();
-  count_launch();
+  launch(reduce_splits, dim3(296), dim3(256), 0, st, W, p.splits, M, N, D, ldd, bias, relu);
   PQLG_CUDA(cudaFreeAsync(W, st));
 }
 

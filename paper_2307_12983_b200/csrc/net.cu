@@ -1,9 +1,11 @@
+#include "pdl.cuh"
 #include "net.h"
 
 namespace pqlg {
 
 namespace {
 __global__ void pad_rows_kernel(const float* src, float* dst, int rows, int cols, int ld) {
+  pdl::entry();
   const int64_t n = static_cast<int64_t>(rows) * cols;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -16,9 +18,7 @@ __global__ void pad_rows_kernel(const float* src, float* dst, int rows, int cols
 void launch_pad_rows(const float* src, float* dst, int rows, int cols, int ld, cudaStream_t st) {
   const int64_t n = static_cast<int64_t>(rows) * cols;
   const int blocks = static_cast<int>(std::min<int64_t>(592, (n + 255) / 256));
-  pad_rows_kernel<<<blocks, 256, 0, st>>>(src, dst, rows, cols, ld);
-  PQLG_CHECK_LAUNCH();
-  count_launch();
+  launch(pad_rows_kernel, dim3(blocks), dim3(256), 0, st, src, dst, rows, cols, ld);
 }
 
 namespace {

@@ -11,6 +11,7 @@
 // All are HBM-bound streaming kernels (grid = multiple of 148 SMs x 4).
 #pragma once
 
+#include "pdl.cuh"
 #include <cstdint>
 
 namespace pqlg::optim {
@@ -47,6 +48,7 @@ struct FinalizeArgs {
 // every thread would copy the whole argument block to local memory.
 static __global__ void __launch_bounds__(kFinalizeThreads)
     finalize_kernel(const __grid_constant__ FinalizeArgs a) {
+  pdl::entry();
   const int group = blockIdx.y;
   double sq = 0.0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < a.total;
@@ -133,6 +135,7 @@ struct AdamArgs {
 };
 
 static __global__ void adam_polyak_kernel(AdamArgs a) {
+  pdl::entry();
   // A non-finite target / loss / gradient makes the reference throw before
   // adam_step modifies anything (ddpg.hpp:37,72; optim.hpp:33-34).
   if (*a.status) return;

@@ -7,6 +7,7 @@
 // dgrad only for the action columns) -> policy head backward -> policy
 // wgrad/dgrad chain -> fixed-order gradient reduction + fp64 norm -> clip +
 // Adam (no Polyak for the policy).
+#include "pdl.cuh"
 #include <memory>
 #include <random>
 #include <vector>
@@ -92,7 +93,7 @@ PLearner::~PLearner() {
 
 namespace {
 // Small row-wise kernels of the update (launched through closures).
-__global__ void step_increment_kernel(int64_t* step) { *step += 1; }
+__global__ void step_increment_kernel(int64_t* step) { pdl::entry(); *step += 1; }
 }  // namespace
 
 void PLearner::build_update() {
@@ -135,9 +136,7 @@ void PLearner::build_update() {
   steps_.push_back([this, B](cudaStream_t st) {
     const uint64_t* idx = mt_mode_ ? idx_.p : nullptr;
     launch_state_sample(*states_, norm_.view(), X_.p, Kp_, sampler_.p, idx, B, st);
-    step_increment_kernel<<<1, 1, 0, st>>>(step_.p);
-    PQLG_CHECK_LAUNCH();
-    count_launch();
+    launch(step_increment_kernel, dim3(1), dim3(1), 0, st, step_.p);
   });
 
   // -------------------------------------------------------- policy forward
@@ -208,9 +207,7 @@ void PLearner::build_update() {
     critic::LossArgs a{part_.p, B, nt, q[0], q[1], qnet_.b_off[nh], nullptr, up_.p,
                        block_loss_.p, loss_counter_.p, loss_.p, status_.p, B};
     steps_.push_back([a, loss_blocks](cudaStream_t st) {
-      critic::actor_pick_kernel<<<loss_blocks, critic::kRowThreads, 0, st>>>(a);
-      PQLG_CHECK_LAUNCH();
-      count_launch();
+      launch(critic::actor_pick_kernel, dim3(loss_blocks), dim3(critic::kRowThreads), 0, st, a);
     });
   }
   // --------------------------------- input gradient through the critics
@@ -226,9 +223,7 @@ void PLearner::build_update() {
     a.H = H;
     const int blocks = 4 * mlp::kSMs;
     steps_.push_back([a, blocks](cudaStream_t st) {
-      critic::head_input_grad_kernel<<<dim3(blocks, 2), 256, 0, st>>>(a);
-      PQLG_CHECK_LAUNCH();
-      count_launch();
+      launch(critic::head_input_grad_kernel, dim3(dim3(blocks, 2)), dim3(256), 0, st, a);
     });
   }
   for (int l = nh - 1; l >= 1; --l) {
@@ -271,9 +266,7 @@ void PLearner::build_update() {
     a.A = A;
     a.rows_per_tile = 64;
     steps_.push_back([a, ptiles](cudaStream_t st) {
-      critic::policy_head_backward_kernel<<<ptiles, 32, 0, st>>>(a);
-      PQLG_CHECK_LAUNCH();
-      count_launch();
+      launch(critic::policy_head_backward_kernel, dim3(ptiles), dim3(32), 0, st, a);
     });
   }
   // ----------------------------------------------------- policy backward
@@ -356,9 +349,7 @@ void PLearner::build_update() {
     f.status = status_.p;
     f.max_norm = 0.5f;
     steps_.push_back([f, fb](cudaStream_t st) {
-      optim::finalize_kernel<<<dim3(fb, 1), optim::kFinalizeThreads, 0, st>>>(f);
-      PQLG_CHECK_LAUNCH();
-      count_launch();
+      launch(optim::finalize_kernel, dim3(dim3(fb, 1)), dim3(optim::kFinalizeThreads), 0, st, f);
     });
     optim::AdamArgs a{};
     a.p = pol_.p;
@@ -380,9 +371,7 @@ void PLearner::build_update() {
     a.tau = 0.0f;
     const int blocks = static_cast<int>(std::min<int64_t>(4 * mlp::kSMs, (pnet_.params + 255) / 256));
     steps_.push_back([a, blocks](cudaStream_t st) {
-      optim::adam_polyak_kernel<<<dim3(blocks, 1), 256, 0, st>>>(a);
-      PQLG_CHECK_LAUNCH();
-      count_launch();
+      launch(optim::adam_polyak_kernel, dim3(dim3(blocks, 1)), dim3(256), 0, st, a);
     });
   }
   // the padded head mirror follows the updated policy

@@ -13,54 +13,37 @@ using replay::kWarpsPerBlock;
 void DeviceNStep::push(const replay::Slice& s, float reward_scale, DeviceReplay& ring,
                        cudaStream_t st) {
   require(ring.D == D && ring.A == A, "nstep: replay schema mismatch");
-  replay::nstep_count_kernel<<<n_blocks, replay::kScanBlock, 0, st>>>(window(), s, offs.p,
+  launch(replay::nstep_count_kernel, dim3(n_blocks), dim3(replay::kScanBlock), 0, st, window(), s, offs.p,
                                                                       block_sums.p);
-  PQLG_CHECK_LAUNCH();
   const int warps = N;
-  replay::nstep_emit_kernel<<<(warps + kWarpsPerBlock - 1) / kWarpsPerBlock, 32 * kWarpsPerBlock,
-                              0, st>>>(window(), s, reward_scale, ring.view(), offs.p,
+  launch(replay::nstep_emit_kernel, dim3((warps + kWarpsPerBlock - 1) / kWarpsPerBlock), dim3(32 * kWarpsPerBlock), 0, st, window(), s, reward_scale, ring.view(), offs.p,
                                        block_sums.p, n_blocks);
-  PQLG_CHECK_LAUNCH();
-  replay::ring_advance_kernel<<<1, 32, 0, st>>>(ring.state.p, ring.capacity, block_sums.p,
+  launch(replay::ring_advance_kernel, dim3(1), dim3(32), 0, st, ring.state.p, ring.capacity, block_sums.p,
                                                 n_blocks, 0);
-  PQLG_CHECK_LAUNCH();
-  count_launch(3);
 }
 
 void DeviceStates::insert(const float* rows, int64_t ld_rows, uint64_t n, cudaStream_t st) {
   if (n == 0) return;
   const uint64_t blocks = (n + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  replay::state_insert_kernel<<<static_cast<unsigned>(blocks), 32 * kWarpsPerBlock, 0, st>>>(
-      view(), rows, ld_rows, n);
-  PQLG_CHECK_LAUNCH();
-  replay::ring_advance_kernel<<<1, 32, 0, st>>>(state.p, capacity, nullptr, 0, n);
-  PQLG_CHECK_LAUNCH();
-  count_launch(2);
+  launch(replay::state_insert_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kWarpsPerBlock), 0, st, view(), rows, ld_rows, n);
+  launch(replay::ring_advance_kernel, dim3(1), dim3(32), 0, st, state.p, capacity, nullptr, 0, n);
 }
 
 void launch_replay_sample(const DeviceReplay& r, const replay::Norm& norm, const replay::Gather& g,
                           replay::SamplerState* ss, const uint64_t* idx_dev, uint64_t B,
                           cudaStream_t st) {
   const uint64_t blocks = (B + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  replay::replay_sample_kernel<<<static_cast<unsigned>(blocks), 32 * kWarpsPerBlock, 0, st>>>(
-      r.view(), norm, g, ss, idx_dev, B);
-  PQLG_CHECK_LAUNCH();
-  replay::replay_sample_finalize_kernel<<<1, 32, 0, st>>>(r.view(), norm, g, ss, idx_dev, B);
-  PQLG_CHECK_LAUNCH();
-  count_launch(2);
+  launch(replay::replay_sample_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kWarpsPerBlock), 0, st, r.view(), norm, g, ss, idx_dev, B);
+  launch(replay::replay_sample_finalize_kernel, dim3(1), dim3(32), 0, st, r.view(), norm, g, ss, idx_dev, B);
 }
 
 void launch_state_sample(const DeviceStates& r, const replay::Norm& norm, float* out,
                          int64_t ld_out, replay::SamplerState* ss, const uint64_t* idx_dev,
                          uint64_t B, cudaStream_t st) {
   const uint64_t blocks = (B + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  replay::state_sample_kernel<<<static_cast<unsigned>(blocks), 32 * kWarpsPerBlock, 0, st>>>(
-      r.view(), norm, out, ld_out, ss, idx_dev, B);
-  PQLG_CHECK_LAUNCH();
-  replay::state_sample_finalize_kernel<<<1, 32, 0, st>>>(r.view(), norm, out, ld_out, ss, idx_dev,
+  launch(replay::state_sample_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kWarpsPerBlock), 0, st, r.view(), norm, out, ld_out, ss, idx_dev, B);
+  launch(replay::state_sample_finalize_kernel, dim3(1), dim3(32), 0, st, r.view(), norm, out, ld_out, ss, idx_dev,
                                                          B);
-  PQLG_CHECK_LAUNCH();
-  count_launch(2);
 }
 
 }  // namespace pqlg
@@ -152,13 +135,9 @@ int pqlg_replay_insert(pqlg_replay h, const pqlg_nstep_batch* b, uint64_t n) {
     auto& r = *h->r;
     const int64_t ldo = ld_or(b->ld_obs, r.D), lda = ld_or(b->ld_act, r.A);
     const uint64_t blocks = (n + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    replay::ring_insert_kernel<<<static_cast<unsigned>(blocks), 32 * kWarpsPerBlock, 0,
-                                 r.stream>>>(r.view(), b->obs, b->act, b->boot_obs, b->ret,
+    launch(replay::ring_insert_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kWarpsPerBlock), 0, r.stream, r.view(), b->obs, b->act, b->boot_obs, b->ret,
                                              b->eff_disc, ldo, lda, n);
-    PQLG_CHECK_LAUNCH();
-    replay::ring_advance_kernel<<<1, 32, 0, r.stream>>>(r.state.p, r.capacity, nullptr, 0, n);
-    PQLG_CHECK_LAUNCH();
-    count_launch(2);
+    launch(replay::ring_advance_kernel, dim3(1), dim3(32), 0, r.stream, r.state.p, r.capacity, nullptr, 0, n);
   });
 }
 
@@ -185,12 +164,8 @@ int pqlg_replay_fill_synthetic(pqlg_replay h, uint64_t n, uint64_t seed, float d
     if (n == 0) return;
     auto& r = *h->r;
     const uint64_t blocks = (n + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    replay::ring_fill_kernel<<<static_cast<unsigned>(blocks), 32 * kWarpsPerBlock, 0,
-                               r.stream>>>(r.view(), n, seed, disc, terminal_every);
-    PQLG_CHECK_LAUNCH();
-    replay::ring_advance_kernel<<<1, 32, 0, r.stream>>>(r.state.p, r.capacity, nullptr, 0, n);
-    PQLG_CHECK_LAUNCH();
-    count_launch(2);
+    launch(replay::ring_fill_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kWarpsPerBlock), 0, r.stream, r.view(), n, seed, disc, terminal_every);
+    launch(replay::ring_advance_kernel, dim3(1), dim3(32), 0, r.stream, r.state.p, r.capacity, nullptr, 0, n);
   });
 }
 

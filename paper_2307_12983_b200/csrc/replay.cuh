@@ -11,6 +11,7 @@
 //                                                 scalar.hpp:93-106
 #pragma once
 
+#include "pdl.cuh"
 #include <cstdint>
 
 #include "rng.cuh"
@@ -123,6 +124,7 @@ __device__ __forceinline__ int emit_count(uint32_t count, int n, bool done) {
 
 // K1: per-env emit counts, block-exclusive offsets and block totals.
 static __global__ void nstep_count_kernel(Window w, Slice s, uint32_t* offs, uint32_t* block_sums) {
+  pdl::entry();
   __shared__ uint32_t warp_tot[kScanBlock / 32];
   const int e = blockIdx.x * kScanBlock + threadIdx.x;
   uint32_t c = 0;
@@ -160,6 +162,7 @@ static __global__ void nstep_count_kernel(Window w, Slice s, uint32_t* offs, uin
 static __global__ void nstep_emit_kernel(Window w, Slice s, float reward_scale, Ring ring,
                                   const uint32_t* offs, const uint32_t* block_sums,
                                   int n_blocks) {
+  pdl::entry();
   const int lane = threadIdx.x & 31;
   const int e = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (e >= w.N) return;
@@ -245,6 +248,7 @@ static __global__ void nstep_emit_kernel(Window w, Slice s, float reward_scale, 
 // K3: cursor = (cursor + total) % cap; count = min(count + total, cap).
 static __global__ void ring_advance_kernel(uint64_t* state, uint64_t capacity, const uint32_t* sums,
                                     int n_sums, uint64_t extra) {
+  pdl::entry();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   uint64_t total = extra;
   for (int b = 0; b < n_sums; ++b) total += sums[b];
@@ -258,6 +262,7 @@ static __global__ void ring_advance_kernel(uint64_t* state, uint64_t capacity, c
 static __global__ void ring_insert_kernel(Ring ring, const float* obs, const float* act,
                                    const float* boot, const float* ret, const float* eff,
                                    int64_t ld_obs, int64_t ld_act, uint64_t n) {
+  pdl::entry();
   const int lane = threadIdx.x & 31;
   const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
   if (r >= n || r + ring.capacity < n) return;
@@ -274,6 +279,7 @@ static __global__ void ring_insert_kernel(Ring ring, const float* obs, const flo
 }
 
 static __global__ void state_insert_kernel(StateRing ring, const float* rows, int64_t ld, uint64_t n) {
+  pdl::entry();
   const int lane = threadIdx.x & 31;
   const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
   if (r >= n || r + ring.capacity < n) return;
@@ -295,6 +301,7 @@ __device__ __forceinline__ float philox_normal(uint64_t key, uint64_t ctr) {
 
 static __global__ void ring_fill_kernel(Ring ring, uint64_t n, uint64_t seed, float disc,
                                         uint32_t terminal_every) {
+  pdl::entry();
   const int lane = threadIdx.x & 31;
   const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
   if (r >= n) return;
@@ -384,6 +391,7 @@ __device__ __forceinline__ void gather_row(const Ring& ring, const Norm& norm, c
 // ReplayBuffer::sample fused with apply_stats on obs and boot_obs.
 static __global__ void replay_sample_kernel(Ring ring, Norm norm, Gather g, SamplerState* ss,
                                      const uint64_t* host_idx, uint64_t B) {
+  pdl::entry();
   const int lane = threadIdx.x & 31;
   const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
   if (r >= B) return;
@@ -401,6 +409,7 @@ static __global__ void replay_sample_kernel(Ring ring, Norm norm, Gather g, Samp
 // then advance the counter by the draws consumed.  Always launched (1 warp).
 static __global__ void replay_sample_finalize_kernel(Ring ring, Norm norm, Gather g, SamplerState* ss,
                                               const uint64_t* host_idx, uint64_t B) {
+  pdl::entry();
   const int lane = threadIdx.x & 31;
   if (host_idx) return;
   if (ss->reject == 0) {
@@ -427,6 +436,7 @@ static __global__ void replay_sample_finalize_kernel(Ring ring, Norm norm, Gathe
 // StateBuffer::sample fused with apply_stats.
 static __global__ void state_sample_kernel(StateRing ring, Norm norm, float* out, int64_t ld_out,
                                     SamplerState* ss, const uint64_t* host_idx, uint64_t B) {
+  pdl::entry();
   const int lane = threadIdx.x & 31;
   const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
   if (r >= B) return;
@@ -448,6 +458,7 @@ static __global__ void state_sample_kernel(StateRing ring, Norm norm, float* out
 static __global__ void state_sample_finalize_kernel(StateRing ring, Norm norm, float* out,
                                              int64_t ld_out, SamplerState* ss,
                                              const uint64_t* host_idx, uint64_t B) {
+  pdl::entry();
   const int lane = threadIdx.x & 31;
   if (host_idx) return;
   if (ss->reject == 0) {

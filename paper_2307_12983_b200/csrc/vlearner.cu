@@ -219,9 +219,7 @@ void VLearner::build_update() {
     critic::TdArgs a{part_t_.p, B, nt, q1t, q2t, qnet_.b_off[nh], ret_.p, eff_.p, y_.p, B,
                      status_.p, step_.p};
     steps_.push_back([a, B](cudaStream_t st) {
-      critic::td_target_kernel<<<(B + 255) / 256, 256, 0, st>>>(a);
-      PQLG_CHECK_LAUNCH();
-      count_launch();
+      launch(critic::td_target_kernel, dim3((B + 255) / 256), dim3(256), 0, st, a);
     });
   }
   critic_fwd(false);
@@ -230,9 +228,7 @@ void VLearner::build_update() {
     critic::LossArgs a{part_o_.p, B, nt, q1, q2, qnet_.b_off[nh], y_.p, up_.p,
                        block_loss_.p, loss_counter_.p, loss_.p, status_.p, B};
     steps_.push_back([a, loss_blocks](cudaStream_t st) {
-      critic::critic_loss_kernel<<<loss_blocks, critic::kRowThreads, 0, st>>>(a);
-      PQLG_CHECK_LAUNCH();
-      count_launch();
+      launch(critic::critic_loss_kernel, dim3(loss_blocks), dim3(critic::kRowThreads), 0, st, a);
     });
   }
 
@@ -268,9 +264,7 @@ void VLearner::build_update() {
     a.tiles = ht;
     a.with_params = 1;
     steps_.push_back([a, ht](cudaStream_t st) {
-      critic::head_backward_kernel<<<dim3(ht, 2), critic::kHeadThreads, 0, st>>>(a);
-      PQLG_CHECK_LAUNCH();
-      count_launch();
+      launch(critic::head_backward_kernel, dim3(dim3(ht, 2)), dim3(critic::kHeadThreads), 0, st, a);
     });
   }
   for (int l = nh - 1; l >= 0; --l) {
@@ -333,9 +327,7 @@ void VLearner::build_update() {
     f.max_norm = 0.5f;
     const int fb = fin_blocks_;
     steps_.push_back([f, fb](cudaStream_t st) {
-      optim::finalize_kernel<<<dim3(fb, 2), optim::kFinalizeThreads, 0, st>>>(f);
-      PQLG_CHECK_LAUNCH();
-      count_launch();
+      launch(optim::finalize_kernel, dim3(dim3(fb, 2)), dim3(optim::kFinalizeThreads), 0, st, f);
     });
   }
   // ------------------------------------------------ clip + Adam + Polyak
@@ -360,9 +352,7 @@ void VLearner::build_update() {
     a.tau = static_cast<float>(cfg_.tau);
     const int blocks = static_cast<int>(std::min<int64_t>(4 * mlp::kSMs, (P + 255) / 256));
     steps_.push_back([a, blocks](cudaStream_t st) {
-      optim::adam_polyak_kernel<<<dim3(blocks, 2), 256, 0, st>>>(a);
-      PQLG_CHECK_LAUNCH();
-      count_launch();
+      launch(optim::adam_polyak_kernel, dim3(dim3(blocks, 2)), dim3(256), 0, st, a);
     });
   }
 }
