@@ -58,26 +58,52 @@ struct DeviceEnv {
     PQLG_CUDA(cudaMemcpy(rng.p, r.data(), N * 8, cudaMemcpyHostToDevice));
   }
   actor::EnvState view() const {
-    return actor::EnvState{s.p, ld, M.p, ep.p, rng.p, N, D, A, max_len, low, high};
+    return actor::EnvState{s.p, ld, s.p, ld, M.p, ep.p, rng.p, N, D, A, max_len, low, high};
   }
   void reset(float* obs, int64_t ld_obs, cudaStream_t st) {
     launch(actor::env_reset_kernel, dim3((N + actor::kEnvWarps - 1) / actor::kEnvWarps), dim3(32 * actor::kEnvWarps), 0, st, view(), obs, ld_obs, offset);
   }
+  // persistent grid: as many blocks as fit (occupancy), at most one per tile
+  template <int kNch>
+  void step_as(const float* act, int64_t ld_act, const actor::StepOut& o, cudaStream_t st,
+               const actor::NextNorm& nn, size_t smem, const float* cur, int64_t ld_cur) {
+    auto kern = actor::env_step_kernel<kNch>;
+    static int per_sm = 0;
+    if (per_sm == 0) {
+      PQLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+      PQLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
+                                                              32 * actor::kEnvWarps, smem));
+      if (per_sm < 1) per_sm = 1;
+    }
+    const int tiles = (N + actor::kEnvTile - 1) / actor::kEnvTile;
+    const int blocks = std::min(tiles, per_sm * mlp::kSMs);
+    actor::EnvState v = view();
+    if (cur) {  // the caller's obs buffers hold the state: read cur, write next_obs only
+      v.s = nullptr;
+      v.s_in = cur;
+      v.ld_in = ld_cur;
+    }
+    launch(kern, dim3(blocks), dim3(32 * actor::kEnvWarps), smem, st, v, act, ld_act, o, nn);
+  }
+  // cur: optional obs buffer holding the current state (the actor's double
+  // buffer); then the internal state array is neither read nor written.
   void step(const float* act, int64_t ld_act, const actor::StepOut& o, cudaStream_t st,
-            const actor::NextNorm& nn = actor::NextNorm{}) {
+            const actor::NextNorm& nn = actor::NextNorm{}, const float* cur = nullptr,
+            int64_t ld_cur = 0) {
     require(A <= actor::kMaxA, "env: act_dim > 32 not supported");
     require(D <= 32 * actor::kMaxDChunks, "env: obs_dim > 256 not supported");
     const size_t smem = actor::env_step_smem(D, A);
-    static bool configured = false;
-    if (!configured) {
-      PQLG_CUDA(cudaFuncSetAttribute(actor::env_step_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      configured = true;
+    switch ((D + 31) / 32) {
+      case 1: step_as<1>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
+      case 2: step_as<2>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
+      case 3: step_as<3>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
+      case 4: step_as<4>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
+      case 5: step_as<5>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
+      case 6: step_as<6>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
+      case 7: step_as<7>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
+      default: step_as<8>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
     }
-    const int tiles = (N + actor::kEnvTile - 1) / actor::kEnvTile;
-    const int blocks = std::min(tiles, 4 * mlp::kSMs);
-    launch(actor::env_step_kernel, dim3(blocks), dim3(32 * actor::kEnvWarps), smem, st, view(), act, ld_act, o,
-                                                                       nn);
   }
 };
 
@@ -204,7 +230,7 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
   const int one = 1;
   PQLG_CUDA(cudaMemcpy(identity_.p, &one, 4, cudaMemcpyHostToDevice));
   npart_.alloc(static_cast<size_t>(actor::kNormGroups) * D_ * 2);
-  nticket_.alloc(1);
+  nticket_.alloc(actor::norm_tickets(D_));
   status_.alloc(1);
   // first policy input: apply_stats with count 0 is the identity
   launch(actor::normalize_kernel, dim3(4 * mlp::kSMs), dim3(256), 0, stream_, obs_[0].p, Dp_, Xn_.p, Dp_,
@@ -277,7 +303,7 @@ void Actor::enqueue(int cur) {
   // env_->step(actions) + next-obs normalisation
   actor::StepOut o{obs_[1 - cur].p, boot_.p, rew_.p, term_.p, trunc_.p, nullptr, Dp_, status_.p};
   actor::NextNorm nn{Xn_.p, Dp_, mean_f_.p, inv_f_.p, identity_.p};
-  env_->step(act_.p, Ap_, o, st, nn);
+  env_->step(act_.p, Ap_, o, st, nn, obs, Dp_);
 }
 
 int Actor::kernels_per_step() {
@@ -484,7 +510,7 @@ int pqlg_k_normalizer_update(int64_t* count_dev, double* mean_dev, double* m2_de
     if (rows == 0) return;  // normalizer.hpp:34
     DevBuf<double> part(static_cast<size_t>(actor::kNormGroups) * dim * 2);
     DevBuf<int> ident(1);
-    DevBuf<unsigned int> ticket(1);
+    DevBuf<unsigned int> ticket(actor::norm_tickets(dim));
     const int64_t ldx = ld > 0 ? ld : dim;
     actor::NormState ns{count_dev, mean_dev, m2_dev, mean_f_dev, inv_f_dev, ident.p};
     launch(actor::norm_update_kernel, dim3(dim3((dim + 31) / 32, actor::kNormGroups)), dim3(256), 0, st, batch_dev, ldx, rows, dim, part.p, ticket.p, ns);

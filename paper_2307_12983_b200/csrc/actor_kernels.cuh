@@ -23,8 +23,10 @@ constexpr int kEnvWarps = 8;
 constexpr int kNormChunk = 128;
 
 struct EnvState {
-  float* s;                // [N x ld] state (= observation)
-  int64_t ld;
+  float* s;                // [N x ld] state (= observation); null: the caller keeps the
+  int64_t ld;              //   state in its obs buffers (s_in = this step's obs)
+  const float* s_in;       // state read by the step (= s unless aliased)
+  int64_t ld_in;
   const float* M;          // [D x A] coupling
   int64_t* episode_step;   // [N]
   uint64_t* rng;           // [N] SplitMix state per env
@@ -73,6 +75,8 @@ constexpr int kMaxDChunks = 8;  // obs_dim <= 256
 
 __device__ __forceinline__ int env_tile_ld(int D) { return D | 1; }  // odd: conflict-free rows
 
+// kNch = number of 32-wide obs chunks per lane (ceil(D/32) rounded up to 1, 2, 4 or 8).
+template <int kNch>
 static __global__ void __launch_bounds__(32 * kEnvWarps)
     env_step_kernel(EnvState e, const float* __restrict__ act, int64_t ld_act, StepOut o,
                     NextNorm nn) {
@@ -84,65 +88,102 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
   float* sv = sM + static_cast<int64_t>(D) * Ap;        // [kEnvTile x ldv]  s'
   float* saa = sv + kEnvTile * ldv;                      // [kEnvTile]        sum a^2
   int* sdone = reinterpret_cast<int*>(saa + kEnvTile);   // [kEnvTile]
-  for (int idx = threadIdx.x; idx < D * Ap; idx += blockDim.x) {
-    const int d = idx / Ap, k = idx - d * Ap;
-    sM[idx] = k < A ? e.M[static_cast<int64_t>(d) * A + k] : 0.0f;
+  float* sa_all = saa + 2 * kEnvTile;                    // [kEnvWarps x 32]  clamped actions
+  {
+    // stage M (constant since env creation) before the PDL wait, under the
+    // previous kernel's tail
+    if ((A & 3) == 0) {  // rows are float4-aligned: straight vector copy
+      const int total4 = D * A / 4;
+      const float4* src = reinterpret_cast<const float4*>(e.M);
+      for (int idx = threadIdx.x; idx < total4; idx += blockDim.x) sh4[idx] = src[idx];
+    } else {
+      const int total = D * Ap;
+      for (int base = threadIdx.x; base < total; base += 8 * blockDim.x) {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int idx = base + q * blockDim.x;
+          v[q] = 0.0f;
+          if (idx < total) {
+            const int d = idx / Ap, k = idx - d * Ap;
+            if (k < A) v[q] = e.M[static_cast<int64_t>(d) * A + k];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int idx = base + q * blockDim.x;
+          if (idx < total) sM[idx] = v[q];
+        }
+      }
+    }
   }
   __syncthreads();
-  pdl::entry();  // M is constant: staged while the previous kernel drains
+  pdl::entry();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int nch = (D + 31) >> 5;
+  float* sa = sa_all + w * 32;
   const bool id = nn.out ? (*nn.identity != 0) : true;
   const int n_tiles = (e.N + kEnvTile - 1) / kEnvTile;
+  const int A4 = (A + 3) >> 2;
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int i0 = tile * kEnvTile;
     // ---- phase 1
     for (int j = w; j < kEnvTile && i0 + j < e.N; j += kEnvWarps) {
       const int i = i0 + j;
-      const float* s = e.s + static_cast<int64_t>(i) * e.ld;
-      float sd[kMaxDChunks];
+      const float* s = e.s_in + static_cast<int64_t>(i) * e.ld_in;
+      float sd[kNch];
 #pragma unroll
-      for (int c = 0; c < kMaxDChunks; ++c) {
+      for (int c = 0; c < kNch; ++c) {
         const int d = lane + 32 * c;
-        sd[c] = (c < nch && d < D) ? s[d] : 0.0f;
+        sd[c] = d < D ? s[d] : 0.0f;
       }
-      const float* a_in = act + static_cast<int64_t>(i) * ld_act;
-      float a[kMaxA];
+      float u = 0.0f;
       bool bad = false;
-#pragma unroll
-      for (int k = 0; k < kMaxA; ++k) {
-        float u = 0.0f;
-        if (k < A) {
-          u = a_in[k];  // broadcast load
-          if (!isfinite(u)) bad = true;
-          u = u < e.low ? e.low : (u > e.high ? e.high : u);
-        }
-        a[k] = u;
+      if (lane < A) {
+        u = act[static_cast<int64_t>(i) * ld_act + lane];
+        bad = !isfinite(u);
+        u = u < e.low ? e.low : (u > e.high ? e.high : u);
       }
-      if (bad && lane == 0) atomicOr(o.status, 8u);
-      float acc[kMaxDChunks];
+      sa[lane] = u;
+      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(o.status, 8u);
+      __syncwarp();
+      float acc[kNch];
 #pragma unroll
-      for (int c = 0; c < kMaxDChunks; ++c) acc[c] = 0.0f;
+      for (int c = 0; c < kNch; ++c) acc[c] = 0.0f;
+#pragma unroll 1
+      for (int k4 = 0; k4 < A4; ++k4) {
+        const float4 a4 = reinterpret_cast<const float4*>(sa)[k4];
+        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+        const int nu = A - 4 * k4;
+        if (nu >= 4) {  // full quad (always when A % 4 == 0)
 #pragma unroll
-      for (int k4 = 0; k4 < kMaxA / 4; ++k4) {
-        if (4 * k4 < A) {
-#pragma unroll
-          for (int c = 0; c < kMaxDChunks; ++c) {
+          for (int c = 0; c < kNch; ++c) {
             const int d = lane + 32 * c;
-            if (c < nch && d < D) {
+            if (c + 1 < kNch || d < D) {
+              const float4 m4 = reinterpret_cast<const float4*>(sM + d * Ap)[k4];
+              acc[c] = __fadd_rn(acc[c], __fmul_rn(m4.x, av[0]));
+              acc[c] = __fadd_rn(acc[c], __fmul_rn(m4.y, av[1]));
+              acc[c] = __fadd_rn(acc[c], __fmul_rn(m4.z, av[2]));
+              acc[c] = __fadd_rn(acc[c], __fmul_rn(m4.w, av[3]));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < kNch; ++c) {
+            const int d = lane + 32 * c;
+            if (d < D) {
               const float4 m4 = reinterpret_cast<const float4*>(sM + d * Ap)[k4];
               const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
 #pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (4 * k4 + u < A) acc[c] = __fadd_rn(acc[c], __fmul_rn(mm[u], a[4 * k4 + u]));
+              for (int q = 0; q < 4; ++q)
+                if (q < nu) acc[c] = __fadd_rn(acc[c], __fmul_rn(mm[q], av[q]));
             }
           }
         }
       }
 #pragma unroll
-      for (int c = 0; c < kMaxDChunks; ++c) {
+      for (int c = 0; c < kNch; ++c) {
         const int d = lane + 32 * c;
-        if (c < nch && d < D) {
+        if (d < D) {
           float v = __fadd_rn(__fmul_rn(0.95f, sd[c]), __fmul_rn(0.05f, acc[c]));
           v = v < -10.0f ? -10.0f : (v > 10.0f ? 10.0f : v);
           sv[j * ldv + d] = v;
@@ -150,11 +191,10 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
       }
       if (lane == 0) {
         float aa = 0.0f;
-#pragma unroll
-        for (int k = 0; k < kMaxA; ++k)
-          if (k < A) aa = __fadd_rn(aa, __fmul_rn(a[k], a[k]));
+        for (int k = 0; k < A; ++k) aa = __fadd_rn(aa, __fmul_rn(sa[k], sa[k]));
         saa[j] = aa;
       }
+      __syncwarp();
     }
     __syncthreads();
     // ---- phase 2
@@ -168,9 +208,9 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
         for (; d + 8 <= D; d += 8) {
           float q[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) q[u] = row[d + u];
+          for (int t = 0; t < 8; ++t) q[t] = row[d + t];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) ss = __fadd_rn(ss, __fmul_rn(q[u], q[u]));
+          for (int t = 0; t < 8; ++t) ss = __fadd_rn(ss, __fmul_rn(q[t], q[t]));
         }
         for (; d < D; ++d) ss = __fadd_rn(ss, __fmul_rn(row[d], row[d]));
         const float reward = -__fadd_rn(__fdiv_rn(ss, static_cast<float>(D)),
@@ -192,21 +232,12 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
     // ---- phase 3
     for (int j = w; j < kEnvTile && i0 + j < e.N; j += kEnvWarps) {
       const int i = i0 + j;
-      const int done_i = sdone[j];
-      const uint64_t st0 = e.rng[i];
-      float* s = e.s + static_cast<int64_t>(i) * e.ld;
+      float* s = e.s ? e.s + static_cast<int64_t>(i) * e.ld : nullptr;
       float* nxt = o.next_obs + static_cast<int64_t>(i) * o.ld_obs;
       float* bt = o.boot + static_cast<int64_t>(i) * o.ld_obs;
       float* xn = nn.out ? nn.out + static_cast<int64_t>(i) * nn.ld_out : nullptr;
-      for (int d = lane; d < D; d += 32) {
-        const float v = sv[j * ldv + d];
-        bt[d] = v;  // terminal observation on done, next observation otherwise
-        float ns = v;
-        if (done_i) {
-          uint64_t st = st0 + static_cast<uint64_t>(d);  // draw d of the reset sequence
-          ns = rng::env_uniform(st, -1.0f, 1.0f);
-        }
-        s[d] = ns;
+      auto emit = [&](int d, float ns) {
+        if (s) s[d] = ns;
         nxt[d] = ns;
         if (xn) {
           float z = ns;
@@ -217,8 +248,22 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
           }
           xn[d] = z;
         }
+      };
+      if (sdone[j]) {  // warp-uniform: terminal obs to boot, fresh reset draws
+        const uint64_t st0 = e.rng[i];
+        for (int d = lane; d < D; d += 32) {
+          bt[d] = sv[j * ldv + d];
+          uint64_t st = st0 + static_cast<uint64_t>(d);  // draw d of the reset sequence
+          emit(d, rng::env_uniform(st, -1.0f, 1.0f));
+        }
+        if (lane == 0) e.rng[i] = st0 + static_cast<uint64_t>(D);
+      } else {
+        for (int d = lane; d < D; d += 32) {
+          const float v = sv[j * ldv + d];
+          bt[d] = v;
+          emit(d, v);
+        }
       }
-      if (done_i && lane == 0) e.rng[i] = st0 + static_cast<uint64_t>(D);
     }
     // the next tile's phase 1 writes only rows owned by the same warp; saa /
     // sdone are rewritten after the next barrier
@@ -227,7 +272,8 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
 
 inline size_t env_step_smem(int D, int A) {
   const int Ap = (A + 3) & ~3;
-  return (static_cast<size_t>(D) * Ap + static_cast<size_t>(kEnvTile) * (D | 1) + 2 * kEnvTile) *
+  return (static_cast<size_t>(D) * Ap + static_cast<size_t>(kEnvTile) * (D | 1) + 2 * kEnvTile +
+          32 * kEnvWarps) *
          sizeof(float);
 }
 
@@ -282,14 +328,17 @@ struct NormState {
 };
 
 // RunningNormalizer::update (normalizer.hpp:33-50, :73-83) in one launch,
-// parallel and deterministic.  Grid (ceil(D/32), kNormGroups): warp lanes own
-// columns, warps stride the group's rows; sums are shifted by the batch's
-// first row (no cancellation for offset data).  The last block to finish
-// (atomic ticket) reduces the group partials per column in fixed order
-// (lane-strided sums + xor butterfly), forms the batch (mean, M2), merges it
-// into the running stats with Chan's formula and refreshes the fp32 apply
-// constants (normalizer.hpp:62-66).
-constexpr int kNormGroups = 64;
+// parallel and deterministic.  Grid (ceil(D/32) column strips, kNormGroups
+// row groups), 8 warps: lanes own columns, warp w sums rows r0 + w + 8t of
+// its group with all loads in flight; sums are shifted by the batch's first
+// row (no cancellation for offset data).  The last block of each column strip
+// (atomic ticket) reduces that strip's group partials in fixed order (8
+// threads per column, then the 8 parts in order), forms the batch (mean, M2),
+// merges it into the running stats with Chan's formula and refreshes the
+// fp32 apply constants (normalizer.hpp:62-66); the last strip to finish
+// advances the count.
+constexpr int kNormGroups = 128;
+constexpr int kNormRowsPerWarp = 16;  // rows per warp per group (N <= 8*16*kNormGroups in one pass)
 static __global__ void __launch_bounds__(256)
     norm_update_kernel(const float* __restrict__ x, int64_t ldx, int N, int D, double* partial,
                        unsigned int* ticket, NormState s) {
@@ -302,22 +351,21 @@ static __global__ void __launch_bounds__(256)
   double s1 = 0.0, s2 = 0.0;
   if (c < D) {
     const double shift = x[c];
-    int r = r0 + w;
-    for (; r + 24 < r1; r += 32) {
-      float v[4];
+    for (int rb = r0 + w; rb < r1; rb += 8 * kNormRowsPerWarp) {
+      float v[kNormRowsPerWarp];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = x[static_cast<int64_t>(r + 8 * u) * ldx + c];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double t = static_cast<double>(v[u]) - shift;
-        s1 += t;
-        s2 += t * t;
+      for (int u = 0; u < kNormRowsPerWarp; ++u) {
+        const int r = rb + 8 * u;
+        v[u] = r < r1 ? x[static_cast<int64_t>(r) * ldx + c] : 0.0f;
       }
-    }
-    for (; r < r1; r += 8) {
-      const double t = static_cast<double>(x[static_cast<int64_t>(r) * ldx + c]) - shift;
-      s1 += t;
-      s2 += t * t;
+#pragma unroll
+      for (int u = 0; u < kNormRowsPerWarp; ++u) {
+        if (rb + 8 * u < r1) {
+          const double t = static_cast<double>(v[u]) - shift;
+          s1 += t;
+          s2 += t * t;
+        }
+      }
     }
   }
   __shared__ double red[8][32][2];
@@ -336,47 +384,73 @@ static __global__ void __launch_bounds__(256)
   __shared__ bool last;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1;
+  if (threadIdx.x == 0) last = atomicAdd(&ticket[1 + blockIdx.x], 1u) == gridDim.y - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const int64_t n0i = *s.count;
-  const int64_t cnt = n0i + N;
-  const double nb = static_cast<double>(N);
-  const double na = static_cast<double>(n0i);
-  const double nab = na + nb;
+  // strip finish: thread (column lane, part w) sums groups w, w+8, ... in order
   const int groups = gridDim.y;
-  for (int d = w; d < D; d += blockDim.x / 32) {
-    double s1 = 0.0, s2 = 0.0;
-    for (int k = lane; k < groups; k += 32) {
-      s1 += __ldcg(partial + (static_cast<int64_t>(k) * D + d) * 2);
-      s2 += __ldcg(partial + (static_cast<int64_t>(k) * D + d) * 2 + 1);
-    }
+  {
+    double a1 = 0.0, a2 = 0.0;
+    if (c < D) {
+      constexpr int kIn = 16;
+      for (int k0 = w; k0 < groups; k0 += 8 * kIn) {
+        double v1[kIn], v2[kIn];
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        for (int q = 0; q < kIn; ++q) {
+          const int k = k0 + 8 * q;
+          const double* src = partial + (static_cast<int64_t>(k) * D + c) * 2;
+          v1[q] = k < groups ? __ldcg(src) : 0.0;
+          v2[q] = k < groups ? __ldcg(src + 1) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < kIn; ++q) {
+          a1 += v1[q];
+          a2 += v2[q];
+        }
+      }
     }
-    if (lane == 0) {
-      const double bmean = static_cast<double>(x[d]) + s1 / nb;
-      double bm2 = s2 - s1 * s1 / nb;
-      if (bm2 < 0.0) bm2 = 0.0;
-      const double delta = bmean - s.mean[d];
-      const double mean = s.mean[d] + delta * (nb / nab);
-      const double m2 = s.m2[d] + (bm2 + delta * delta * (na * nb / nab));
-      s.mean[d] = mean;
-      s.m2[d] = m2;
-      s.mean_f[d] = static_cast<float>(mean);
-      s.inv_f[d] = static_cast<float>(1.0 / sqrt(m2 / static_cast<double>(cnt) + 1e-8));
+    __syncthreads();  // red reuse
+    red[w][lane][0] = a1;
+    red[w][lane][1] = a2;
+  }
+  __syncthreads();
+  const int64_t n0i = *s.count;
+  if (w == 0 && c < D) {
+    const double nb = static_cast<double>(N);
+    const double na = static_cast<double>(n0i);
+    const double nab = na + nb;
+    const int64_t cnt = n0i + N;
+    double t1 = 0.0, t2 = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      t1 += red[k][lane][0];
+      t2 += red[k][lane][1];
     }
+    const double bmean = static_cast<double>(x[c]) + t1 / nb;
+    double bm2 = t2 - t1 * t1 / nb;
+    if (bm2 < 0.0) bm2 = 0.0;
+    const double delta = bmean - s.mean[c];
+    const double mean = s.mean[c] + delta * (nb / nab);
+    const double m2 = s.m2[c] + (bm2 + delta * delta * (na * nb / nab));
+    s.mean[c] = mean;
+    s.m2[c] = m2;
+    s.mean_f[c] = static_cast<float>(mean);
+    s.inv_f[c] = static_cast<float>(1.0 / sqrt(m2 / static_cast<double>(cnt) + 1e-8));
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    *s.count = cnt;
-    *s.identity = cnt <= 1 ? 1 : 0;
-    *ticket = 0u;
+    ticket[1 + blockIdx.x] = 0u;
+    __threadfence();
+    // every strip read the old count before its ticket: the last one advances it
+    if (atomicAdd(&ticket[0], 1u) == gridDim.x - 1) {
+      *s.count = n0i + N;
+      *s.identity = n0i + N <= 1 ? 1 : 0;
+      ticket[0] = 0u;
+    }
   }
 }
+
+inline int norm_tickets(int D) { return 1 + (D + 31) / 32; }
 
 // Standalone apply_noise (op-level hook): one thread per env row.
 static __global__ void noise_kernel(float* act, int64_t ld, int N, int A, const float* sigma,

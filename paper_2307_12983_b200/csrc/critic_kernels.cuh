@@ -2,8 +2,8 @@
 // tensor-core GEMMs: the value head 512->1 is folded into the last hidden
 // layer's epilogue as per-n-tile partial dots; these kernels finish it.
 //
-//   td_target_kernel     ddpg_critic_target  y = G + eff * min(Q1', Q2')      ddpg.hpp:24-40
-//   critic_loss_kernel   ddpg_critic_loss    e = Q - y, up = 2e/B, loss       ddpg.hpp:50-76
+//   critic_loss_kernel   ddpg_critic_target  y = G + eff * min(Q1', Q2')      ddpg.hpp:24-40
+//                        + ddpg_critic_loss  e = Q - y, up = 2e/B, loss       ddpg.hpp:50-76
 //   actor_pick_kernel    ddpg_actor_loss     pick1 = Q1 <= Q2, up = -1/B      ddpg.hpp:86-118
 //   head_backward_kernel fa::backward of the 512->1 layer + ReLU mask of the
 //                        layer below (mlp.hpp:161-184) and its bias/weight
@@ -26,34 +26,45 @@ __device__ __forceinline__ float head_value(const float* partial, int64_t ld, in
   return q;
 }
 
-struct TdArgs {
-  const float* partial;  // [2][n_tiles][ld]
-  int64_t ld;
-  int n_tiles;
-  const float* q1t;  // target nets (bias of the head at head_b_off)
-  const float* q2t;
-  int64_t head_b_off;
-  const float* ret;
-  const float* eff;
-  float* y;
-  int B;
-  uint32_t* status;  // bit1: non-finite target
-  int64_t* step;     // Adam step, incremented once per update
-};
-
-static __global__ void td_target_kernel(TdArgs a) {
-  pdl::entry();
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b == 0) *a.step += 1;
-  if (b >= a.B) return;
-  const float q1 = head_value(a.partial, a.ld, a.n_tiles, 0, a.q1t[a.head_b_off], b);
-  const float q2 = head_value(a.partial, a.ld, a.n_tiles, 1, a.q2t[a.head_b_off], b);
-  const float qmin = q2 < q1 ? q2 : q1;  // std::min(q1, q2)
-  const float y = __fadd_rn(a.ret[b], __fmul_rn(a.eff[b], qmin));
-  a.y[b] = y;
-  if (!isfinite(y)) atomicOr(a.status, 2u);
+// Block sums of l -> block_loss[blockIdx.x]; the last block (ticket) adds the
+// block sums in fixed order (lane-strided, then an xor tree) and writes
+// out = sum / B, flagging a non-finite result in status.
+__device__ __forceinline__ void block_mean_finish(double l, double* block_loss,
+                                                  unsigned int* counter, int B, float* out,
+                                                  uint32_t* status, uint32_t bit) {
+  __shared__ double red[kRowThreads / 32];
+  __shared__ bool last;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) l += __shfl_down_sync(0xffffffffu, l, d);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = l;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kRowThreads / 32; ++w) s += red[w];
+    block_loss[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x >= 32) return;
+  __threadfence();
+  const int lane = threadIdx.x;
+  double tot = 0.0;
+  for (unsigned i = lane; i < gridDim.x; i += 32) tot += __ldcg(block_loss + i);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, d);
+  if (lane == 0) {
+    *counter = 0;
+    const float v = static_cast<float>(tot / static_cast<double>(B));
+    *out = v;
+    if (!isfinite(v)) atomicOr(status, bit);
+  }
 }
 
+// ddpg_critic_target + ddpg_critic_loss in one launch (ddpg.hpp:24-40,
+// :50-76): y = G + eff * min(Q1', Q2') from the target critics' head
+// partials, e_k = Q_k - y from the online ones, up_k = 2 e_k / B, loss =
+// mean(e1^2 + e2^2).  Also advances the device Adam step (once per update).
 struct LossArgs {
   const float* partial;  // online [2][n_tiles][ld]
   int64_t ld;
@@ -61,52 +72,44 @@ struct LossArgs {
   const float* q1;
   const float* q2;
   int64_t head_b_off;
-  const float* y;
-  float* up;          // [2][B]  dLoss/dQ_k = 2 e_k / B
+  // target side (critic loss only)
+  const float* partial_t;  // target [2][n_tiles][ld]
+  const float* q1t;
+  const float* q2t;
+  const float* ret;
+  const float* eff;
+  float* y;                // [B] TD targets (kept for inspection)
+  int64_t* step;           // Adam step
+  float* up;          // [2][B]  dLoss/dQ_k
   double* block_loss; // [gridDim.x]
   unsigned int* counter;
   float* loss_out;
-  uint32_t* status;   // bit2: non-finite loss
+  uint32_t* status;   // bit1: non-finite target, bit2: non-finite loss
   int B;
 };
 
 static __global__ void __launch_bounds__(kRowThreads) critic_loss_kernel(LossArgs a) {
   pdl::entry();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b == 0) *a.step += 1;
   double l = 0.0;
   if (b < a.B) {
+    const float t1 = head_value(a.partial_t, a.ld, a.n_tiles, 0, a.q1t[a.head_b_off], b);
+    const float t2 = head_value(a.partial_t, a.ld, a.n_tiles, 1, a.q2t[a.head_b_off], b);
+    const float qmin = t2 < t1 ? t2 : t1;  // std::min(q1, q2)
+    const float y = __fadd_rn(a.ret[b], __fmul_rn(a.eff[b], qmin));
+    a.y[b] = y;
+    if (!isfinite(y)) atomicOr(a.status, 2u);
     const float q1 = head_value(a.partial, a.ld, a.n_tiles, 0, a.q1[a.head_b_off], b);
     const float q2 = head_value(a.partial, a.ld, a.n_tiles, 1, a.q2[a.head_b_off], b);
-    const float e1 = __fsub_rn(q1, a.y[b]);
-    const float e2 = __fsub_rn(q2, a.y[b]);
+    const float e1 = __fsub_rn(q1, y);
+    const float e2 = __fsub_rn(q2, y);
     l = static_cast<double>(__fadd_rn(__fmul_rn(e1, e1), __fmul_rn(e2, e2)));
     const float Bf = static_cast<float>(a.B);
     a.up[b] = __fdiv_rn(__fmul_rn(2.0f, e1), Bf);
     a.up[a.B + b] = __fdiv_rn(__fmul_rn(2.0f, e2), Bf);
   }
-  __shared__ double red[kRowThreads / 32];
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) l += __shfl_down_sync(0xffffffffu, l, d);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = l;
-  __syncthreads();
-  __shared__ bool last;
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < kRowThreads / 32; ++w) s += red[w];
-    a.block_loss[blockIdx.x] = s;
-    __threadfence();
-    last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!last || threadIdx.x != 0) return;
-  __threadfence();
-  double tot = 0.0;
-  const volatile double* bl = a.block_loss;
-  for (unsigned i = 0; i < gridDim.x; ++i) tot += bl[i];
-  *a.counter = 0;
-  const float loss = static_cast<float>(tot / static_cast<double>(a.B));
-  *a.loss_out = loss;
-  if (!isfinite(loss)) atomicOr(a.status, 4u);
+  block_mean_finish(l, a.block_loss, a.counter, a.B, a.loss_out, a.status, 4u);
 }
 
 // ddpg_actor_loss row head: pick1 = q1 <= q2; loss -= min; upstream of the
@@ -114,6 +117,7 @@ static __global__ void __launch_bounds__(kRowThreads) critic_loss_kernel(LossArg
 static __global__ void __launch_bounds__(kRowThreads) actor_pick_kernel(LossArgs a) {
   pdl::entry();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b == 0 && a.step) *a.step += 1;
   double l = 0.0;
   if (b < a.B) {
     const float q1 = head_value(a.partial, a.ld, a.n_tiles, 0, a.q1[a.head_b_off], b);
@@ -124,29 +128,7 @@ static __global__ void __launch_bounds__(kRowThreads) actor_pick_kernel(LossArgs
     a.up[b] = pick1 ? up : 0.0f;
     a.up[a.B + b] = pick1 ? 0.0f : up;
   }
-  __shared__ double red[kRowThreads / 32];
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) l += __shfl_down_sync(0xffffffffu, l, d);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = l;
-  __syncthreads();
-  __shared__ bool last;
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < kRowThreads / 32; ++w) s += red[w];
-    a.block_loss[blockIdx.x] = s;
-    __threadfence();
-    last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!last || threadIdx.x != 0) return;
-  __threadfence();
-  double tot = 0.0;
-  const volatile double* bl = a.block_loss;
-  for (unsigned i = 0; i < gridDim.x; ++i) tot += bl[i];
-  *a.counter = 0;
-  const float loss = static_cast<float>(tot / static_cast<double>(a.B));
-  *a.loss_out = loss;
-  if (!isfinite(loss)) atomicOr(a.status, 4u);
+  block_mean_finish(l, a.block_loss, a.counter, a.B, a.loss_out, a.status, 4u);
 }
 
 // Backward through the 512->1 value head for both critics.

@@ -29,6 +29,9 @@ struct Segment {
   int64_t stride;
   int64_t cols = 0;      // > 0: src rows are padded, src = (j / cols) * ld_src + j % cols
   int64_t ld_src = 0;
+  // filled by plan_finalize
+  int64_t blk0 = 0;      // first block of this segment
+  int mode = 0;          // 0: thread per element, 1: float4 per thread, 2: warp per element
 };
 
 struct FinalizeArgs {
@@ -44,36 +47,111 @@ struct FinalizeArgs {
   float max_norm;
 };
 
+// Host: give every segment its own block range (no per-element segment
+// search) and pick the float4 path where the layout allows; returns the
+// number of blocks per group.
+inline int plan_finalize(FinalizeArgs& f) {
+  int64_t blocks = 0;
+  for (int i = 0; i < f.n_seg; ++i) {
+    Segment& sg = f.seg[i];
+    const bool v = sg.cols == 0 && sg.count % 4 == 0 && sg.dst % 4 == 0 && sg.stride % 4 == 0 &&
+                   sg.group_stride % 4 == 0 && f.gstride % 4 == 0 &&
+                   (reinterpret_cast<uintptr_t>(sg.src) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(f.grads) & 15) == 0;
+    // long sums (per-row-tile bias partials: 64-128 terms) get a warp each so
+    // the kernel's critical path is not one thread's chain of dependent loads
+    sg.mode = sg.n_terms > 16 ? 2 : (v ? 1 : 0);
+    sg.blk0 = blocks;
+    const int64_t per_block = sg.mode == 2 ? kFinalizeThreads / 32
+                                           : static_cast<int64_t>(kFinalizeThreads) * (v ? 4 : 1);
+    blocks += (sg.count + per_block - 1) / per_block;
+  }
+  return static_cast<int>(blocks);
+}
+
 // __grid_constant__: the segment table is indexed dynamically; without it
 // every thread would copy the whole argument block to local memory.
 static __global__ void __launch_bounds__(kFinalizeThreads)
     finalize_kernel(const __grid_constant__ FinalizeArgs a) {
   pdl::entry();
   const int group = blockIdx.y;
+  int si = 0;
+  while (si + 1 < a.n_seg && static_cast<int64_t>(blockIdx.x) >= a.seg[si + 1].blk0) ++si;
+  const Segment& sg = a.seg[si];
+  const int64_t lb = static_cast<int64_t>(blockIdx.x) - sg.blk0;
   double sq = 0.0;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < a.total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int s = 0;
-    while (s + 1 < a.n_seg && i >= a.seg[s + 1].dst) ++s;
-    const Segment& sg = a.seg[s];
-    const int64_t j = i - sg.dst;
-    const int64_t js = sg.cols > 0 ? (j / sg.cols) * sg.ld_src + j % sg.cols : j;
-    const float* src = sg.src + group * sg.group_stride + js;
-    // terms summed in ascending order; loads issued 8 at a time so the
-    // latency of the (L2-resident) partials overlaps
-    float acc = src[0];
-    int t = 1;
-    for (; t + 8 <= sg.n_terms; t += 8) {
-      float v[8];
+  // terms summed in ascending order, 8 loads in flight
+  if (sg.mode == 2) {
+    // lane l sums terms l, l+32, ... in order; lanes combine by a fixed xor tree
+    const int lane = threadIdx.x & 31;
+    const int64_t j = lb * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (j < sg.count) {
+      const int64_t js = sg.cols > 0 ? (j / sg.cols) * sg.ld_src + j % sg.cols : j;
+      const float* src = sg.src + group * sg.group_stride + js;
+      float acc = 0.0f;
+      for (int t0 = lane; t0 < sg.n_terms; t0 += 128) {
+        float v[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = src[(t + u) * sg.stride];
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + 32 * u;
+          v[u] = t < sg.n_terms ? src[t * sg.stride] : 0.0f;
+        }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc = __fadd_rn(acc, v[u]);
+        for (int u = 0; u < 4; ++u)
+          if (t0 + 32 * u < sg.n_terms) acc = __fadd_rn(acc, v[u]);
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+      if (lane == 0) {
+        a.grads[group * a.gstride + sg.dst + j] = acc;
+        const double d = static_cast<double>(acc);
+        sq = d * d;
+      }
     }
-    for (; t < sg.n_terms; ++t) acc = __fadd_rn(acc, src[t * sg.stride]);
-    a.grads[group * a.gstride + i] = acc;
-    const double d = static_cast<double>(acc);
-    sq += d * d;
+  } else if (sg.mode == 1) {
+    const int64_t j = (lb * blockDim.x + threadIdx.x) * 4;
+    if (j < sg.count) {
+      const float* src = sg.src + group * sg.group_stride + j;
+      float4 acc = *reinterpret_cast<const float4*>(src);
+      int t = 1;
+      for (; t < sg.n_terms; t += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (t + u < sg.n_terms) v[u] = *reinterpret_cast<const float4*>(src + (t + u) * sg.stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (t + u < sg.n_terms) {
+            acc.x = __fadd_rn(acc.x, v[u].x);
+            acc.y = __fadd_rn(acc.y, v[u].y);
+            acc.z = __fadd_rn(acc.z, v[u].z);
+            acc.w = __fadd_rn(acc.w, v[u].w);
+          }
+        }
+      }
+      *reinterpret_cast<float4*>(a.grads + group * a.gstride + sg.dst + j) = acc;
+      const double d0 = acc.x, d1 = acc.y, d2 = acc.z, d3 = acc.w;
+      sq = ((d0 * d0 + d1 * d1) + d2 * d2) + d3 * d3;
+    }
+  } else {
+    const int64_t j = lb * blockDim.x + threadIdx.x;
+    if (j < sg.count) {
+      const int64_t js = sg.cols > 0 ? (j / sg.cols) * sg.ld_src + j % sg.cols : j;
+      const float* src = sg.src + group * sg.group_stride + js;
+      float acc = src[0];
+      for (int t = 1; t < sg.n_terms; t += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (t + u < sg.n_terms) v[u] = src[(t + u) * sg.stride];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (t + u < sg.n_terms) acc = __fadd_rn(acc, v[u]);
+      }
+      a.grads[group * a.gstride + sg.dst + j] = acc;
+      const double d = static_cast<double>(acc);
+      sq = d * d;
+    }
   }
   // block reduction in fixed order (fp64)
   __shared__ double red[kFinalizeThreads / 32];
@@ -148,21 +226,50 @@ static __global__ void adam_polyak_kernel(AdamArgs a) {
   const float ob1 = __fsub_rn(1.0f, a.beta1), ob2 = __fsub_rn(1.0f, a.beta2);
   const float keep = __fsub_rn(1.0f, a.tau);
   const int64_t off = group * a.gstride;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < a.n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    float gi = a.g[off + i];
+  float* __restrict__ P = a.p + off;
+  const float* __restrict__ G = a.g + off;
+  float* __restrict__ M = a.m + off;
+  float* __restrict__ V = a.v + off;
+  float* __restrict__ T = a.target ? a.target + off : nullptr;
+  auto step = [&](float p, float gi, float m, float v, float tg, float& po, float& mo, float& vo,
+                  float& to) {
     if (clipped) gi = __fmul_rn(gi, s);
-    float m = __fadd_rn(__fmul_rn(a.beta1, a.m[off + i]), __fmul_rn(ob1, gi));
-    float v = __fadd_rn(__fmul_rn(a.beta2, a.v[off + i]), __fmul_rn(ob2, __fmul_rn(gi, gi)));
-    a.m[off + i] = m;
-    a.v[off + i] = v;
-    const float mhat = __fmul_rn(m, bc.x);
-    const float vhat = __fmul_rn(v, bc.y);
+    mo = __fadd_rn(__fmul_rn(a.beta1, m), __fmul_rn(ob1, gi));
+    vo = __fadd_rn(__fmul_rn(a.beta2, v), __fmul_rn(ob2, __fmul_rn(gi, gi)));
+    const float mhat = __fmul_rn(mo, bc.x);
+    const float vhat = __fmul_rn(vo, bc.y);
     const float upd = __fmul_rn(a.lr, __fdiv_rn(mhat, __fadd_rn(__fsqrt_rn(vhat), a.eps)));
-    const float p = __fsub_rn(a.p[off + i], upd);
-    a.p[off + i] = p;
-    if (a.target)
-      a.target[off + i] = __fadd_rn(__fmul_rn(a.tau, p), __fmul_rn(keep, a.target[off + i]));
+    po = __fsub_rn(p, upd);
+    to = __fadd_rn(__fmul_rn(a.tau, po), __fmul_rn(keep, tg));
+  };
+  // float4 body (group bases are 16-byte aligned), scalar tail
+  const int64_t n4 = a.n / 4;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < n4;
+       q += stride) {
+    const float4 p4 = reinterpret_cast<const float4*>(P)[q];
+    const float4 g4 = reinterpret_cast<const float4*>(G)[q];
+    const float4 m4 = reinterpret_cast<const float4*>(M)[q];
+    const float4 v4 = reinterpret_cast<const float4*>(V)[q];
+    const float4 t4 = T ? reinterpret_cast<const float4*>(T)[q] : make_float4(0, 0, 0, 0);
+    float4 po, mo, vo, to;
+    step(p4.x, g4.x, m4.x, v4.x, t4.x, po.x, mo.x, vo.x, to.x);
+    step(p4.y, g4.y, m4.y, v4.y, t4.y, po.y, mo.y, vo.y, to.y);
+    step(p4.z, g4.z, m4.z, v4.z, t4.z, po.z, mo.z, vo.z, to.z);
+    step(p4.w, g4.w, m4.w, v4.w, t4.w, po.w, mo.w, vo.w, to.w);
+    reinterpret_cast<float4*>(P)[q] = po;
+    reinterpret_cast<float4*>(M)[q] = mo;
+    reinterpret_cast<float4*>(V)[q] = vo;
+    if (T) reinterpret_cast<float4*>(T)[q] = to;
+  }
+  for (int64_t i = 4 * n4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < a.n;
+       i += stride) {
+    float po, mo, vo, to;
+    step(P[i], G[i], M[i], V[i], T ? T[i] : 0.0f, po, mo, vo, to);
+    P[i] = po;
+    M[i] = mo;
+    V[i] = vo;
+    if (T) T[i] = to;
   }
 }
 

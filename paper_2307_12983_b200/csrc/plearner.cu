@@ -93,7 +93,6 @@ PLearner::~PLearner() {
 
 namespace {
 // Small row-wise kernels of the update (launched through closures).
-__global__ void step_increment_kernel(int64_t* step) { pdl::entry(); *step += 1; }
 }  // namespace
 
 void PLearner::build_update() {
@@ -136,7 +135,6 @@ void PLearner::build_update() {
   steps_.push_back([this, B](cudaStream_t st) {
     const uint64_t* idx = mt_mode_ ? idx_.p : nullptr;
     launch_state_sample(*states_, norm_.view(), X_.p, Kp_, sampler_.p, idx, B, st);
-    launch(step_increment_kernel, dim3(1), dim3(1), 0, st, step_.p);
   });
 
   // -------------------------------------------------------- policy forward
@@ -204,8 +202,20 @@ void PLearner::build_update() {
   }
   // ------------------------------------------------ min critic + upstream
   {
-    critic::LossArgs a{part_.p, B, nt, q[0], q[1], qnet_.b_off[nh], nullptr, up_.p,
-                       block_loss_.p, loss_counter_.p, loss_.p, status_.p, B};
+    critic::LossArgs a{};
+    a.partial = part_.p;
+    a.ld = B;
+    a.n_tiles = nt;
+    a.q1 = q[0];
+    a.q2 = q[1];
+    a.head_b_off = qnet_.b_off[nh];
+    a.up = up_.p;
+    a.block_loss = block_loss_.p;
+    a.counter = loss_counter_.p;
+    a.loss_out = loss_.p;
+    a.status = status_.p;
+    a.step = step_.p;  // Adam step of the policy, advanced once per update
+    a.B = B;
     steps_.push_back([a, loss_blocks](cudaStream_t st) {
       launch(critic::actor_pick_kernel, dim3(loss_blocks), dim3(critic::kRowThreads), 0, st, a);
     });
@@ -339,7 +349,7 @@ void PLearner::build_update() {
     f.total = pnet_.params;
     f.gstride = pnet_.params;
     f.grads = grads_.p;
-    const int fb = static_cast<int>(std::min<int64_t>(4 * mlp::kSMs, (pnet_.params + 1023) / 1024));
+    const int fb = optim::plan_finalize(f);
     block_sq_.alloc(fb);
     fin_counter_.alloc(1);
     scale_.alloc(1);

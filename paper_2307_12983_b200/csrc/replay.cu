@@ -34,7 +34,6 @@ void launch_replay_sample(const DeviceReplay& r, const replay::Norm& norm, const
                           cudaStream_t st) {
   const uint64_t blocks = (B + kWarpsPerBlock - 1) / kWarpsPerBlock;
   launch(replay::replay_sample_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kWarpsPerBlock), 0, st, r.view(), norm, g, ss, idx_dev, B);
-  launch(replay::replay_sample_finalize_kernel, dim3(1), dim3(32), 0, st, r.view(), norm, g, ss, idx_dev, B);
 }
 
 void launch_state_sample(const DeviceStates& r, const replay::Norm& norm, float* out,
@@ -42,8 +41,6 @@ void launch_state_sample(const DeviceStates& r, const replay::Norm& norm, float*
                          uint64_t B, cudaStream_t st) {
   const uint64_t blocks = (B + kWarpsPerBlock - 1) / kWarpsPerBlock;
   launch(replay::state_sample_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kWarpsPerBlock), 0, st, r.view(), norm, out, ld_out, ss, idx_dev, B);
-  launch(replay::state_sample_finalize_kernel, dim3(1), dim3(32), 0, st, r.view(), norm, out, ld_out, ss, idx_dev,
-                                                         B);
 }
 
 }  // namespace pqlg
@@ -148,7 +145,7 @@ int pqlg_replay_sample(pqlg_replay h, uint64_t batch, pqlg_rng* rng, uint64_t mi
     const uint64_t count = r.size();
     if (count < min_live || count == 0) throw Error(PQLG_NOT_READY, "replay: not enough records");
     if (norm) h->norm.set(norm->count, norm->mean, norm->m2, r.stream);
-    else h->norm.identity = 1;
+    else h->norm.set_identity(r.stream);
     const uint64_t* idx = prepare_rng(rng, batch, h->ss, h->idx, r.stream);
     replay::Gather g{o->obs, ld_or(o->ld_obs, r.D), o->act, ld_or(o->ld_act, r.A),
                      o->boot_obs, ld_or(o->ld_obs, r.D), o->ret, o->eff_disc};
@@ -250,7 +247,7 @@ int pqlg_states_sample(pqlg_states h, uint64_t batch, pqlg_rng* rng, uint64_t mi
     const uint64_t count = s.size();
     if (count < min_live || count == 0) throw Error(PQLG_NOT_READY, "states: not enough rows");
     if (norm) h->norm.set(norm->count, norm->mean, norm->m2, s.stream);
-    else h->norm.identity = 1;
+    else h->norm.set_identity(s.stream);
     const uint64_t* idx = prepare_rng(rng, batch, h->ss, h->idx, s.stream);
     launch_state_sample(s, h->norm.view(), out, ld_or(ld_out, s.D), h->ss.p, idx, batch,
                         s.stream);

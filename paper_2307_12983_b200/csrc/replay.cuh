@@ -66,7 +66,7 @@ struct Slice {
 struct Norm {
   const float* mean;
   const float* inv;
-  int identity;  // count <= 1
+  const int* identity;  // device flag: count <= 1
 };
 
 // Destination of a gathered minibatch.  obs/boot rows are normalized.
@@ -166,6 +166,15 @@ static __global__ void nstep_emit_kernel(Window w, Slice s, float reward_scale, 
   const int lane = threadIdx.x & 31;
   const int e = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   if (e >= w.N) return;
+  // every independent load first (nothing below aliases them until the
+  // window write), so their latencies overlap
+  const uint32_t h0 = w.head[e], c0 = w.count[e];
+  const bool term = s.term[e] != 0;
+  const bool done = term || (s.trunc[e] != 0);
+  const float rew_e = s.rew[e];
+  const uint32_t off_e = offs[e];
+  const uint64_t cursor0 = ring.state[0];
+  float my_rew = lane < w.n ? w.rew[static_cast<size_t>(e) * w.n + lane] : 0.0f;
   // global offset of this env's first record and the step total
   uint32_t before = 0, total = 0;
   const int my_block = e / kScanBlock;
@@ -179,34 +188,33 @@ static __global__ void nstep_emit_kernel(Window w, Slice s, float reward_scale, 
     total += __shfl_xor_sync(0xffffffffu, total, d);
     before += __shfl_xor_sync(0xffffffffu, before, d);
   }
-  const uint64_t base = static_cast<uint64_t>(before) + offs[e];
-  const uint64_t cursor0 = ring.state[0];
+  const uint64_t base = static_cast<uint64_t>(before) + off_e;
   const int n = w.n, D = ring.D, A = ring.A;
-
-  uint32_t h = w.head[e];
-  uint32_t c = w.count[e];
+  uint32_t h = h0;
+  uint32_t c = c0;
   // float4 paths when the slice rows are 16B aligned with padded strides
   const bool wide_o = aligned16(s.obs, s.ld_obs) && aligned16(s.boot, s.ld_obs) &&
                       s.ld_obs >= ((D + 3) & ~3);
   const bool wide_a = aligned16(s.act, s.ld_act) && s.ld_act >= ((A + 3) & ~3);
-  // push: window slot (head + count) % n
+  // push: window slot (head + count) % n; lane k keeps the window reward of
+  // slot k in a register (rewards are read back by shuffle, not from memory)
+  const uint32_t slot = (h + c) % n;
+  const float new_rew = __fmul_rn(rew_e, reward_scale);
+  if (lane == static_cast<int>(slot)) my_rew = new_rew;
   {
-    const uint32_t slot = (h + c) % n;
     const size_t wrow = static_cast<size_t>(e) * n + slot;
     copy_row(w.obs + wrow * w.ld_obs, s.obs + static_cast<size_t>(e) * s.ld_obs, D, wide_o, lane);
     copy_row(w.act + wrow * w.ld_act, s.act + static_cast<size_t>(e) * s.ld_act, A, wide_a, lane);
-    if (lane == 0) w.rew[wrow] = __fmul_rn(s.rew[e], reward_scale);
+    if (lane == 0) w.rew[wrow] = new_rew;
   }
   __syncwarp();
   c += 1;
-  const bool term = s.term[e] != 0;
-  const bool done = term || (s.trunc[e] != 0);
 
   uint32_t j = 0;
   auto emit = [&](uint32_t m, bool terminated) {
     float g = 0.0f, disc = 1.0f;
     for (uint32_t k = 0; k < m; ++k) {
-      const float r = w.rew[static_cast<size_t>(e) * n + (h + k) % n];
+      const float r = __shfl_sync(0xffffffffu, my_rew, static_cast<int>((h + k) % n));
       g = __fadd_rn(g, __fmul_rn(disc, r));
       disc = __fmul_rn(disc, w.gamma);
     }
@@ -327,7 +335,7 @@ struct SamplerState {
   uint64_t key;
   uint64_t counter;
   uint32_t reject;
-  uint32_t pad;
+  uint32_t ticket;  // blocks finished in the current sampling launch
 };
 
 // idx for row r: host_idx (mt19937-compat mode) or Philox + Lemire.
@@ -340,28 +348,30 @@ __device__ __forceinline__ uint64_t sample_index(const SamplerState* ss, const u
 
 __device__ __forceinline__ void gather_row(const Ring& ring, const Norm& norm, const Gather& g,
                                            uint64_t i, uint64_t r, int lane) {
+  const bool ident = *norm.identity != 0;
   const float* __restrict__ so = ring.obs + i * ring.ld_obs;
   const float* __restrict__ sb = ring.boot + i * ring.ld_obs;
   float* __restrict__ dobs = g.obs + r * g.ld_obs;
   float* __restrict__ dboot = g.boot + r * g.ld_boot;
   int d0 = 0;
   if (ring.D <= 256) {  // all loads of the row in flight before any store
-    float x[8], y[8];
+    float x[8], y[8], mu[8], iv[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int d = lane + 32 * u;
       x[u] = d < ring.D ? __ldg(so + d) : 0.0f;
       y[u] = d < ring.D ? __ldg(sb + d) : 0.0f;
+      mu[u] = (d < ring.D && !ident) ? norm.mean[d] : 0.0f;
+      iv[u] = (d < ring.D && !ident) ? norm.inv[d] : 1.0f;
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int d = lane + 32 * u;
       if (d < ring.D) {
         float xx = x[u], yy = y[u];
-        if (!norm.identity) {
-          const float mu = norm.mean[d], iv = norm.inv[d];
-          xx = normalize1(xx, mu, iv);
-          yy = normalize1(yy, mu, iv);
+        if (!ident) {
+          xx = normalize1(xx, mu[u], iv[u]);
+          yy = normalize1(yy, mu[u], iv[u]);
         }
         dobs[d] = xx;
         dboot[d] = yy;
@@ -371,7 +381,7 @@ __device__ __forceinline__ void gather_row(const Ring& ring, const Norm& norm, c
   }
   for (int d = d0 + lane; d < ring.D; d += 32) {
     float x = so[d], y = sb[d];
-    if (!norm.identity) {
+    if (!ident) {
       const float mu = norm.mean[d], iv = norm.inv[d];
       x = normalize1(x, mu, iv);
       y = normalize1(y, mu, iv);
@@ -388,48 +398,77 @@ __device__ __forceinline__ void gather_row(const Ring& ring, const Norm& norm, c
   }
 }
 
-// ReplayBuffer::sample fused with apply_stats on obs and boot_obs.
+// The last block of a sampling launch (atomic ticket in SamplerState::ticket)
+// advances the Philox counter by B, or -- when any draw hit Lemire's
+// rejection zone (probability ~count/2^64 per draw) -- redoes the whole batch
+// sequentially with libstdc++'s redraw loop and advances the counter by the
+// draws consumed.  redo(i, r, lane) gathers row r from ring index i.
+template <class Redo>
+__device__ __forceinline__ void finish_sample(SamplerState* ss, const uint64_t* host_idx,
+                                              uint64_t count, uint64_t B, Redo&& redo) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&ss->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x >= 32) return;
+  __threadfence();
+  const int lane = threadIdx.x;
+  const volatile SamplerState* vs = ss;
+  if (!host_idx) {
+    if (vs->reject == 0) {
+      if (lane == 0) ss->counter += B;
+    } else {
+      uint64_t ctr = ss->counter;
+      for (uint64_t r = 0; r < B; ++r) {
+        uint64_t i = 0;
+        if (lane == 0) {
+          bool reject = true;
+          while (reject) i = rng::lemire_step(rng::philox_draw(ss->key, ctr++), count, reject);
+        }
+        i = __shfl_sync(0xffffffffu, i, 0);
+        redo(i, r, lane);
+      }
+      if (lane == 0) {
+        ss->counter = ctr;
+        ss->reject = 0;
+      }
+    }
+  }
+  if (lane == 0) ss->ticket = 0;
+}
+
+// ReplayBuffer::sample fused with apply_stats on obs and boot_obs; one warp
+// per row, then the ticketed finish above (one launch per sample).
 static __global__ void replay_sample_kernel(Ring ring, Norm norm, Gather g, SamplerState* ss,
                                      const uint64_t* host_idx, uint64_t B) {
   pdl::entry();
   const int lane = threadIdx.x & 31;
   const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (r >= B) return;
   const uint64_t count = ring.state[1];
-  bool reject = false;
-  uint64_t i = 0;
-  if (lane == 0) i = sample_index(ss, host_idx, count, r, reject);
-  i = __shfl_sync(0xffffffffu, i, 0);
-  if (lane == 0 && reject) atomicOr(&ss->reject, 1u);
-  gather_row(ring, norm, g, i, r, lane);
-}
-
-// Sequential fix-up when any draw hit Lemire's rejection zone (probability
-// ~count/2^64 per draw): redo the whole batch with libstdc++'s redraw loop,
-// then advance the counter by the draws consumed.  Always launched (1 warp).
-static __global__ void replay_sample_finalize_kernel(Ring ring, Norm norm, Gather g, SamplerState* ss,
-                                              const uint64_t* host_idx, uint64_t B) {
-  pdl::entry();
-  const int lane = threadIdx.x & 31;
-  if (host_idx) return;
-  if (ss->reject == 0) {
-    if (lane == 0) ss->counter += B;
-    return;
-  }
-  const uint64_t count = ring.state[1];
-  uint64_t ctr = ss->counter;
-  for (uint64_t r = 0; r < B; ++r) {
+  if (r < B) {
+    bool reject = false;
     uint64_t i = 0;
-    if (lane == 0) {
-      bool reject = true;
-      while (reject) i = rng::lemire_step(rng::philox_draw(ss->key, ctr++), count, reject);
-    }
+    if (lane == 0) i = sample_index(ss, host_idx, count, r, reject);
     i = __shfl_sync(0xffffffffu, i, 0);
+    if (lane == 0 && reject) atomicOr(&ss->reject, 1u);
     gather_row(ring, norm, g, i, r, lane);
   }
-  if (lane == 0) {
-    ss->counter = ctr;
-    ss->reject = 0;
+  finish_sample(ss, host_idx, count, B,
+                [&](uint64_t i, uint64_t rr, int ln) { gather_row(ring, norm, g, i, rr, ln); });
+}
+
+__device__ __forceinline__ void gather_state(const StateRing& ring, const Norm& norm, float* out,
+                                             int64_t ld_out, uint64_t i, uint64_t r, int lane) {
+  const bool ident = *norm.identity != 0;
+  const float* so = ring.obs + i * ring.ld;
+  float* d = out + r * ld_out;
+  for (int k = lane; k < ring.D; k += 32) {
+    float x = so[k];
+    if (!ident) x = normalize1(x, norm.mean[k], norm.inv[k]);
+    d[k] = x;
   }
 }
 
@@ -439,53 +478,18 @@ static __global__ void state_sample_kernel(StateRing ring, Norm norm, float* out
   pdl::entry();
   const int lane = threadIdx.x & 31;
   const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (r >= B) return;
   const uint64_t count = ring.state[1];
-  bool reject = false;
-  uint64_t i = 0;
-  if (lane == 0) i = sample_index(ss, host_idx, count, r, reject);
-  i = __shfl_sync(0xffffffffu, i, 0);
-  if (lane == 0 && reject) atomicOr(&ss->reject, 1u);
-  const float* so = ring.obs + i * ring.ld;
-  float* d = out + r * ld_out;
-  for (int k = lane; k < ring.D; k += 32) {
-    float x = so[k];
-    if (!norm.identity) x = normalize1(x, norm.mean[k], norm.inv[k]);
-    d[k] = x;
-  }
-}
-
-static __global__ void state_sample_finalize_kernel(StateRing ring, Norm norm, float* out,
-                                             int64_t ld_out, SamplerState* ss,
-                                             const uint64_t* host_idx, uint64_t B) {
-  pdl::entry();
-  const int lane = threadIdx.x & 31;
-  if (host_idx) return;
-  if (ss->reject == 0) {
-    if (lane == 0) ss->counter += B;
-    return;
-  }
-  const uint64_t count = ring.state[1];
-  uint64_t ctr = ss->counter;
-  for (uint64_t r = 0; r < B; ++r) {
+  if (r < B) {
+    bool reject = false;
     uint64_t i = 0;
-    if (lane == 0) {
-      bool reject = true;
-      while (reject) i = rng::lemire_step(rng::philox_draw(ss->key, ctr++), count, reject);
-    }
+    if (lane == 0) i = sample_index(ss, host_idx, count, r, reject);
     i = __shfl_sync(0xffffffffu, i, 0);
-    const float* so = ring.obs + i * ring.ld;
-    float* d = out + r * ld_out;
-    for (int k = lane; k < ring.D; k += 32) {
-      float x = so[k];
-      if (!norm.identity) x = normalize1(x, norm.mean[k], norm.inv[k]);
-      d[k] = x;
-    }
+    if (lane == 0 && reject) atomicOr(&ss->reject, 1u);
+    gather_state(ring, norm, out, ld_out, i, r, lane);
   }
-  if (lane == 0) {
-    ss->counter = ctr;
-    ss->reject = 0;
-  }
+  finish_sample(ss, host_idx, count, B, [&](uint64_t i, uint64_t rr, int ln) {
+    gather_state(ring, norm, out, ld_out, i, rr, ln);
+  });
 }
 
 }  // namespace pqlg::replay

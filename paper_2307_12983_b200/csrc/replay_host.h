@@ -14,18 +14,24 @@ namespace pqlg {
 // fp32 normalization constants on device (normalizer.hpp:56-70).
 struct DeviceNorm {
   DevBuf<float> mean, inv;
-  int identity = 1;
+  DevBuf<int> ident;  // device flag: kernels (and captured graphs) read it at run time
   int D = 0;
   void init(int dim) {
     D = dim;
     mean.alloc(dim);
     inv.alloc(dim);
-    identity = 1;
+    ident.alloc(1);
+    set_identity(nullptr);
+  }
+  void set_identity(cudaStream_t st) {
+    static const int one = 1;
+    PQLG_CUDA(cudaMemcpyAsync(ident.p, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+    PQLG_CUDA(cudaStreamSynchronize(st));
   }
   // NormStats -> (mean_f, inv_f) exactly as normalizer.hpp:62-66 (host double).
   void set(int64_t count, const double* m, const double* m2, cudaStream_t st) {
     if (count <= 1) {
-      identity = 1;
+      set_identity(st);
       return;
     }
     std::vector<float> mf(D), inv_f(D);
@@ -34,12 +40,13 @@ struct DeviceNorm {
       const double var = m2[j] / static_cast<double>(count);
       inv_f[j] = static_cast<float>(1.0 / std::sqrt(var + 1e-8));
     }
+    static const int zero = 0;
     PQLG_CUDA(cudaMemcpyAsync(mean.p, mf.data(), D * sizeof(float), cudaMemcpyHostToDevice, st));
     PQLG_CUDA(cudaMemcpyAsync(inv.p, inv_f.data(), D * sizeof(float), cudaMemcpyHostToDevice, st));
+    PQLG_CUDA(cudaMemcpyAsync(ident.p, &zero, sizeof(int), cudaMemcpyHostToDevice, st));
     PQLG_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
-    identity = 0;
   }
-  replay::Norm view() const { return replay::Norm{mean.p, inv.p, identity}; }
+  replay::Norm view() const { return replay::Norm{mean.p, inv.p, ident.p}; }
 };
 
 struct DeviceReplay {
@@ -114,7 +121,7 @@ struct DeviceNStep {
 
   DeviceNStep(int n_envs, int obs_dim, int act_dim, float g, int horizon)
       : N(n_envs), D(obs_dim), A(act_dim), n(horizon), gamma(g) {
-    require(horizon >= 1, "nstep: horizon must be >= 1");
+    require(horizon >= 1 && horizon <= 32, "nstep: horizon must be in [1, 32]");
     require(n_envs >= 1, "nstep: n_envs must be >= 1");
     ld_obs = round_up(D, 4);
     ld_act = round_up(A, 4);

@@ -214,19 +214,29 @@ void VLearner::build_update() {
   };
 
   critic_fwd(true);
-  // ------------------------------------------------------------- TD target
-  {
-    critic::TdArgs a{part_t_.p, B, nt, q1t, q2t, qnet_.b_off[nh], ret_.p, eff_.p, y_.p, B,
-                     status_.p, step_.p};
-    steps_.push_back([a, B](cudaStream_t st) {
-      launch(critic::td_target_kernel, dim3((B + 255) / 256), dim3(256), 0, st, a);
-    });
-  }
   critic_fwd(false);
-  // ------------------------------------------------------------------ loss
+  // ------------------------------------------- TD target + loss + upstream
   {
-    critic::LossArgs a{part_o_.p, B, nt, q1, q2, qnet_.b_off[nh], y_.p, up_.p,
-                       block_loss_.p, loss_counter_.p, loss_.p, status_.p, B};
+    critic::LossArgs a{};
+    a.partial = part_o_.p;
+    a.ld = B;
+    a.n_tiles = nt;
+    a.q1 = q1;
+    a.q2 = q2;
+    a.head_b_off = qnet_.b_off[nh];
+    a.partial_t = part_t_.p;
+    a.q1t = q1t;
+    a.q2t = q2t;
+    a.ret = ret_.p;
+    a.eff = eff_.p;
+    a.y = y_.p;
+    a.step = step_.p;
+    a.up = up_.p;
+    a.block_loss = block_loss_.p;
+    a.counter = loss_counter_.p;
+    a.loss_out = loss_.p;
+    a.status = status_.p;
+    a.B = B;
     steps_.push_back([a, loss_blocks](cudaStream_t st) {
       launch(critic::critic_loss_kernel, dim3(loss_blocks), dim3(critic::kRowThreads), 0, st, a);
     });
@@ -316,7 +326,7 @@ void VLearner::build_update() {
     f.total = P;
     f.gstride = Ps_;
     f.grads = grads_.p;
-    fin_blocks_ = static_cast<int>(std::min<int64_t>(4 * mlp::kSMs, (P + 1023) / 1024));
+    fin_blocks_ = optim::plan_finalize(f);
     block_sq_.alloc(2ull * fin_blocks_);
     fin_counter_.alloc(2);
     scale_.alloc(2);
