@@ -187,11 +187,20 @@ def run_ours(args, rank, world, local):
     D, A, H, nh, B, N, cap = CONFIGS[args.config]
     stream = torch.cuda.Stream(device=local)
     cfg = _lib.default_config(batch_size=B, buffer_capacity=cap, hidden=H, hidden_layers=nh,
-                              n_envs=N, seed=rank)
+                              n_envs=N, seed=0)
     dims = _lib.TaskDims(D, A, -1.0, 1.0)
     h = C.c_void_p()
-    _lib.call("pqlg_vlearner_create", C.byref(cfg), C.byref(dims), 12345 + rank,
-              C.c_void_p(stream.cuda_stream), C.byref(h))
+    comm = None
+    if world > 1:
+        # data-parallel critic (SURVEY 8(e) option i): one NCCL all-reduce of
+        # the twin-critic gradients + loss per update; every rank samples its
+        # own replay shard with its own Philox stream; same init everywhere
+        comm = _lib.comm_from_torch_dist(rank, world)
+        _lib.call("pqlg_vlearner_create_dp", C.byref(cfg), C.byref(dims), 12345, comm,
+                  C.c_void_p(stream.cuda_stream), C.byref(h))
+    else:
+        _lib.call("pqlg_vlearner_create", C.byref(cfg), C.byref(dims), 12345,
+                  C.c_void_p(stream.cuda_stream), C.byref(h))
     rp = C.c_void_p()
     _lib.call("pqlg_vlearner_replay", h, C.byref(rp))
     _lib.call("pqlg_replay_fill_synthetic", rp, cap, 1000 + rank, np.float32(0.970299), 200)
@@ -280,6 +289,8 @@ def run_ours(args, rank, world, local):
         roof["update_tflops"] = round(flops / (ms_step * 1e-3) / 1e12, 2)
         roof["update_frac_of_tf32_peak"] = round(flops / (ms_step * 1e-3) / 1e12 / peak, 4)
     _lib.call("pqlg_vlearner_destroy", h)
+    if comm is not None:
+        _lib.call("pqlg_comm_destroy", comm)
     return dict(value=value, ms_step=ms_step, loss=loss.value, e2e=e2e, roof=roof,
                 clocks=clk.summary(), launches=int(launches), kpu=kpu.value)
 
@@ -295,7 +306,7 @@ def run_actor(args, rank, world, local, steps, warmup):
     stream = torch.cuda.Stream(device=local)
     sp = C.c_void_p(stream.cuda_stream)
     cfg = _lib.default_config(batch_size=B, buffer_capacity=cap, hidden=H, hidden_layers=nh,
-                              n_envs=N, seed=rank, env_offset=rank * N, envs_total=world * N,
+                              n_envs=N, seed=0, env_offset=rank * N, envs_total=world * N,
                               max_episode_len=1000)
     dims = _lib.TaskDims(D, A, -1.0, 1.0)
     act, vl, pl = C.c_void_p(), C.c_void_p(), C.c_void_p()
@@ -360,11 +371,17 @@ def run_policy(args, rank, world, local, steps, warmup):
     D, A, H, nh, B, N, cap = CONFIGS[args.config]
     stream = torch.cuda.Stream(device=local)
     cfg = _lib.default_config(batch_size=B, buffer_capacity=1_000_000, hidden=H,
-                              hidden_layers=nh, n_envs=N, seed=rank)
+                              hidden_layers=nh, n_envs=N, seed=0)
     dims = _lib.TaskDims(D, A, -1.0, 1.0)
     pl = C.c_void_p()
-    _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 1,
-              C.c_void_p(stream.cuda_stream), C.byref(pl))
+    comm = None
+    if world > 1:  # data-parallel policy update (one all-reduce per update)
+        comm = _lib.comm_from_torch_dist(rank, world)
+        _lib.call("pqlg_plearner_create_dp", C.byref(cfg), C.byref(dims), 1, comm,
+                  C.c_void_p(stream.cuda_stream), C.byref(pl))
+    else:
+        _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 1,
+                  C.c_void_p(stream.cuda_stream), C.byref(pl))
     states = torch.randn(1_000_000, D, device="cuda")
     _lib.call("pqlg_plearner_ingest", pl, states.data_ptr(), D, 1_000_000)
     _lib.call("pqlg_plearner_update_n", pl, warmup)
@@ -376,7 +393,10 @@ def run_policy(args, rank, world, local, steps, warmup):
     ev1.synchronize()
     ms = max_over_ranks(ev0.elapsed_time(ev1), world)
     _lib.call("pqlg_plearner_destroy", pl)
-    return {"value": world * steps / (ms * 1e-3), "unit": "updates/s", "ms_per_step": ms / steps}
+    if comm is not None:
+        _lib.call("pqlg_comm_destroy", comm)
+    return {"value": world * steps / (ms * 1e-3), "unit": "updates/s", "ms_per_step": ms / steps,
+            "parallelism": f"dp{world}" if world > 1 else "single"}
 
 
 # ------------------------------------------------------ reference arm
@@ -457,7 +477,12 @@ def main():
             "data": "synthetic (device-generated replay fill, SURVEY 8d distributions)",
             "config": {"workload": f"{args.config}: CriticLearnerCore::update, obs {D} / act {A}, "
                                    f"{nh}x{H} MLPs, batch {B}, {cap} record replay",
-                       "global_batch": B * world, "parallelism": f"replicas x{world}",
+                       "global_batch": B * world,
+                       "parallelism": (f"dp{world}: data-parallel critic, NCCL all-reduce of "
+                                       f"gradients + loss per update, B={B} per GPU"
+                                       if world > 1 else "single GPU"),
+                       "value_unit_note": "updates/s counted in batch-8192 updates: a dp-N "
+                                          "update processes N x 8192 rows and counts N",
                        "l2": "inputs sampled from an 8.9 GB ring (>> 126 MB L2)"}}
     if args.impl == "reference":
         if rank != 0:

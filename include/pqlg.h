@@ -207,6 +207,21 @@ typedef struct {
 
 PQLG_API void pqlg_config_default(pqlg_config* cfg);
 
+/* ------------------------------------------------ data-parallel communicator
+ * NCCL communicator for the data-parallel critic / policy updates of config 5
+ * (SURVEY 8(e)): one process per GPU, one rank per process.  The 128-byte
+ * id is created on rank 0 and shipped to the other ranks by the caller (any
+ * host channel; the benchmark uses torch.distributed).  pqlg_comm_init must
+ * run with the rank's CUDA device current.  NCCL failures -> PQLG_ENCCL. */
+#define PQLG_COMM_ID_BYTES 128
+typedef struct pqlg_comm_s* pqlg_comm;
+PQLG_API int pqlg_comm_unique_id(uint8_t* id_out /* [PQLG_COMM_ID_BYTES] */);
+PQLG_API int pqlg_comm_init(int rank, int world, const uint8_t* id, pqlg_comm* out);
+PQLG_API int pqlg_comm_destroy(pqlg_comm c);
+PQLG_API int pqlg_comm_rank(pqlg_comm c, int* rank, int* world);
+/* In-place sum all-reduce of n floats on `stream` (device pointer). */
+PQLG_API int pqlg_comm_allreduce_f32(pqlg_comm c, float* buf_dev, uint64_t n, void* stream);
+
 /* ------------------------------------------------ V-learner (critic core) */
 typedef struct pqlg_vlearner_s* pqlg_vlearner;
 
@@ -218,6 +233,16 @@ typedef struct pqlg_vlearner_s* pqlg_vlearner;
  * reference's mt19937_64 stream. */
 PQLG_API int pqlg_vlearner_create(const pqlg_config* cfg, const pqlg_task_dims* dims,
                                   uint64_t init_rng_seed, void* stream, pqlg_vlearner* out);
+/* Data-parallel CriticLearnerCore (SURVEY 8(e) option i): every rank samples
+ * cfg->batch_size rows from its own replay shard (Philox key
+ * derive_seed(seed, sample, 1 + 2*rank)), scales dLoss/dQ by
+ * 1/(batch_size*world), and one NCCL all-reduce per update sums the twin
+ * critics' gradients and the loss before clip + Adam + Polyak, so every rank
+ * applies the full-batch update.  world == 1 is bit-identical to
+ * pqlg_vlearner_create.  `comm` must outlive the learner. */
+PQLG_API int pqlg_vlearner_create_dp(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                                     uint64_t init_rng_seed, pqlg_comm comm, void* stream,
+                                     pqlg_vlearner* out);
 PQLG_API int pqlg_vlearner_destroy(pqlg_vlearner h);
 /* adopt_policy: equal-or-newer version replaces (learners.cpp:37-42) */
 PQLG_API int pqlg_vlearner_adopt_policy(pqlg_vlearner h, const float* flat_host, int64_t version);
@@ -265,6 +290,12 @@ typedef struct pqlg_plearner_s* pqlg_plearner;
  * derive_seed(seed, sample, 2). */
 PQLG_API int pqlg_plearner_create(const pqlg_config* cfg, const pqlg_task_dims* dims,
                                   uint64_t init_rng_seed, void* stream, pqlg_plearner* out);
+/* Data-parallel PolicyLearnerCore: as pqlg_vlearner_create_dp (sample key
+ * derive_seed(seed, sample, 2 + 2*rank); one all-reduce of the policy
+ * gradient and the loss per update). */
+PQLG_API int pqlg_plearner_create_dp(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                                     uint64_t init_rng_seed, pqlg_comm comm, void* stream,
+                                     pqlg_plearner* out);
 PQLG_API int pqlg_plearner_destroy(pqlg_plearner h);
 /* adopt_critics(snapshot): equal-or-newer version replaces (learners.cpp:222-227) */
 PQLG_API int pqlg_plearner_adopt_critics(pqlg_plearner h, const float* q1_host,

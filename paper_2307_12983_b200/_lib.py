@@ -82,7 +82,13 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_states_insert": (i32, [vp, vp, i64, u64]),
     "pqlg_states_sample": (i32, [vp, u64, P(Rng), u64, P(NormStats), vp, i64]),
     "pqlg_config_default": (None, [P(Config)]),
+    "pqlg_comm_unique_id": (i32, [vp]),
+    "pqlg_comm_init": (i32, [i32, i32, vp, P(vp)]),
+    "pqlg_comm_destroy": (i32, [vp]),
+    "pqlg_comm_rank": (i32, [vp, P(i32), P(i32)]),
+    "pqlg_comm_allreduce_f32": (i32, [vp, vp, u64, vp]),
     "pqlg_vlearner_create": (i32, [P(Config), P(TaskDims), u64, vp, P(vp)]),
+    "pqlg_vlearner_create_dp": (i32, [P(Config), P(TaskDims), u64, vp, vp, P(vp)]),
     "pqlg_vlearner_destroy": (i32, [vp]),
     "pqlg_vlearner_adopt_policy": (i32, [vp, vp, i64]),
     "pqlg_vlearner_adopt_norm": (i32, [vp, P(NormStats)]),
@@ -105,6 +111,7 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_k_gemm_tf32_repeat": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32,
                                       vp]),
     "pqlg_plearner_create": (i32, [P(Config), P(TaskDims), u64, vp, P(vp)]),
+    "pqlg_plearner_create_dp": (i32, [P(Config), P(TaskDims), u64, vp, vp, P(vp)]),
     "pqlg_plearner_destroy": (i32, [vp]),
     "pqlg_plearner_adopt_critics": (i32, [vp, vp, vp, i64]),
     "pqlg_plearner_adopt_norm": (i32, [vp, P(NormStats)]),
@@ -200,3 +207,31 @@ def check(status: int) -> int:
 
 def call(name: str, *args) -> int:
     return check(getattr(lib(), name)(*args))
+
+
+COMM_ID_BYTES = 128
+
+
+def exchange_comm_id(rank: int, world: int) -> bytes:
+    """Rank 0 makes the NCCL unique id (pqlg_comm_unique_id); torch.distributed
+    (any backend, gloo included) broadcasts the 128 bytes to every rank."""
+    import torch
+    import torch.distributed as dist
+    buf = (C.c_uint8 * COMM_ID_BYTES)()
+    if rank == 0:
+        call("pqlg_comm_unique_id", buf)
+    t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+    if world > 1:
+        if dist.get_backend() == "nccl":
+            t = t.cuda()
+        dist.broadcast(t, 0)
+    return bytes(t.cpu().tolist())
+
+
+def comm_from_torch_dist(rank: int, world: int) -> C.c_void_p:
+    """NCCL communicator for this process (one rank per GPU, its CUDA device
+    current): the id exchange above, then pqlg_comm_init."""
+    ident = (C.c_uint8 * COMM_ID_BYTES)(*exchange_comm_id(rank, world))
+    comm = C.c_void_p()
+    call("pqlg_comm_init", rank, world, ident, C.byref(comm))
+    return comm

@@ -1,0 +1,38 @@
+// NCCL communicator behind pqlg_comm (data-parallel learners).
+#pragma once
+
+#include <nccl.h>
+
+#include <string>
+
+#include "common.h"
+
+struct pqlg_comm_s {
+  ncclComm_t nccl = nullptr;
+  int rank = 0;
+  int world = 1;
+};
+
+namespace pqlg {
+
+[[noreturn]] inline void throw_nccl(ncclResult_t r, const char* what) {
+  throw Error(PQLG_ENCCL, std::string("NCCL error ") + ncclGetErrorString(r) + ": " + what);
+}
+
+#define PQLG_NCCL(expr)                                        \
+  do {                                                         \
+    ncclResult_t _r = (expr);                                  \
+    if (_r != ncclSuccess) ::pqlg::throw_nccl(_r, #expr);      \
+  } while (0)
+
+// One grouped in-place sum all-reduce of up to two float buffers (gradients
+// and the loss scalar travel in the same NCCL launch).
+inline void allreduce_sum(pqlg_comm_s* c, float* a, size_t na, float* b, size_t nb,
+                          cudaStream_t st) {
+  PQLG_NCCL(ncclGroupStart());
+  PQLG_NCCL(ncclAllReduce(a, a, na, ncclFloat32, ncclSum, c->nccl, st));
+  if (b && nb) PQLG_NCCL(ncclAllReduce(b, b, nb, ncclFloat32, ncclSum, c->nccl, st));
+  PQLG_NCCL(ncclGroupEnd());
+}
+
+}  // namespace pqlg

@@ -86,6 +86,7 @@ struct LossArgs {
   float* loss_out;
   uint32_t* status;   // bit1: non-finite target, bit2: non-finite loss
   int B;
+  int Bg;             // mean divisor: B, or the global batch of a data-parallel update
 };
 
 static __global__ void __launch_bounds__(kRowThreads) critic_loss_kernel(LossArgs a) {
@@ -105,11 +106,11 @@ static __global__ void __launch_bounds__(kRowThreads) critic_loss_kernel(LossArg
     const float e1 = __fsub_rn(q1, y);
     const float e2 = __fsub_rn(q2, y);
     l = static_cast<double>(__fadd_rn(__fmul_rn(e1, e1), __fmul_rn(e2, e2)));
-    const float Bf = static_cast<float>(a.B);
+    const float Bf = static_cast<float>(a.Bg);
     a.up[b] = __fdiv_rn(__fmul_rn(2.0f, e1), Bf);
     a.up[a.B + b] = __fdiv_rn(__fmul_rn(2.0f, e2), Bf);
   }
-  block_mean_finish(l, a.block_loss, a.counter, a.B, a.loss_out, a.status, 4u);
+  block_mean_finish(l, a.block_loss, a.counter, a.Bg, a.loss_out, a.status, 4u);
 }
 
 // ddpg_actor_loss row head: pick1 = q1 <= q2; loss -= min; upstream of the
@@ -124,11 +125,11 @@ static __global__ void __launch_bounds__(kRowThreads) actor_pick_kernel(LossArgs
     const float q2 = head_value(a.partial, a.ld, a.n_tiles, 1, a.q2[a.head_b_off], b);
     const bool pick1 = q1 <= q2;
     l = -static_cast<double>(pick1 ? q1 : q2);
-    const float up = __fdiv_rn(-1.0f, static_cast<float>(a.B));
+    const float up = __fdiv_rn(-1.0f, static_cast<float>(a.Bg));
     a.up[b] = pick1 ? up : 0.0f;
     a.up[a.B + b] = pick1 ? 0.0f : up;
   }
-  block_mean_finish(l, a.block_loss, a.counter, a.B, a.loss_out, a.status, 4u);
+  block_mean_finish(l, a.block_loss, a.counter, a.Bg, a.loss_out, a.status, 4u);
 }
 
 // Backward through the 512->1 value head for both critics.

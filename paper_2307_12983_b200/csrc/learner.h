@@ -10,13 +10,16 @@
 #include "net.h"
 #include "replay_host.h"
 
+struct pqlg_comm_s;
+
 namespace pqlg {
 
 // CriticLearnerCore (learners.hpp:77-106).
 class VLearner {
  public:
+  // comm (nullable): data-parallel mode, one NCCL all-reduce per update
   VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t init_seed,
-           cudaStream_t st);
+           cudaStream_t st, pqlg_comm_s* comm = nullptr);
   ~VLearner();
 
   void adopt_policy(const float* flat_host, int64_t version);
@@ -49,6 +52,8 @@ class VLearner {
   pqlg_task_dims dims_;
   cudaStream_t stream_;
   cudaStream_t owned_stream_ = nullptr;
+  pqlg_comm_s* comm_ = nullptr;  // data-parallel communicator (nullable)
+  int rank_ = 0, world_ = 1;
   int D_, A_, H_, nh_, B_, Kp_;
   float reward_scale_, gamma_;
   NetShape qnet_, pnet_;
@@ -88,6 +93,7 @@ class VLearner {
   DevBuf<double> block_sq_;
   DevBuf<unsigned int> fin_counter_;
   DevBuf<float> scale_;
+  DevBuf<double> block_sq2_;  // data-parallel: norm pass after the all-reduce
 
   std::vector<mlp::Step> steps_;
   cudaGraphExec_t graph_exec_ = nullptr;
@@ -101,7 +107,7 @@ class VLearner {
 class PLearner {
  public:
   PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t init_seed,
-           cudaStream_t st);
+           cudaStream_t st, pqlg_comm_s* comm = nullptr);
   ~PLearner();
 
   void adopt_critics(const float* q1_host, const float* q2_host, int64_t version);
@@ -133,6 +139,8 @@ class PLearner {
   pqlg_task_dims dims_;
   cudaStream_t stream_;
   cudaStream_t owned_stream_ = nullptr;
+  pqlg_comm_s* comm_ = nullptr;  // data-parallel communicator (nullable)
+  int rank_ = 0, world_ = 1;
   int D_, A_, Ap_, H_, nh_, B_, Kp_;
   NetShape qnet_, pnet_;
   int64_t Ps_ = 0;
@@ -167,6 +175,7 @@ class PLearner {
   DevBuf<double> block_sq_;
   DevBuf<unsigned int> fin_counter_;
   DevBuf<float> scale_;
+  DevBuf<double> block_sq2_;
 
   std::vector<mlp::Step> steps_;
   cudaGraphExec_t graph_exec_ = nullptr;

@@ -45,6 +45,9 @@ struct FinalizeArgs {
   float* scale;             // [groups] clip scale (1 if not clipped)
   uint32_t* status;         // bit0: non-finite gradient norm
   float max_norm;
+  int skip_norm;            // 1: reduction only (a data-parallel all-reduce follows)
+  const float* check;       // nullable: a scalar (the all-reduced loss) whose
+                            // non-finiteness sets status bit 2
 };
 
 // Host: give every segment its own block range (no per-element segment
@@ -60,7 +63,9 @@ inline int plan_finalize(FinalizeArgs& f) {
                    (reinterpret_cast<uintptr_t>(f.grads) & 15) == 0;
     // long sums (per-row-tile bias partials: 64-128 terms) get a warp each so
     // the kernel's critical path is not one thread's chain of dependent loads
-    sg.mode = sg.n_terms > 16 ? 2 : (v ? 1 : 0);
+    // (a warp per element only pays for short segments: on a weight segment
+    // its strided reads waste 28 of every 32 bytes fetched)
+    sg.mode = (sg.n_terms > 16 && sg.count <= 4096) ? 2 : (v ? 1 : 0);
     sg.blk0 = blocks;
     const int64_t per_block = sg.mode == 2 ? kFinalizeThreads / 32
                                            : static_cast<int64_t>(kFinalizeThreads) * (v ? 4 : 1);
@@ -153,6 +158,7 @@ static __global__ void __launch_bounds__(kFinalizeThreads)
       sq = d * d;
     }
   }
+  if (a.skip_norm) return;
   // block reduction in fixed order (fp64)
   __shared__ double red[kFinalizeThreads / 32];
 #pragma unroll
@@ -185,6 +191,7 @@ static __global__ void __launch_bounds__(kFinalizeThreads)
   double tot = 0.0;
   for (int w = 0; w < kFinalizeThreads / 32; ++w) tot += red[w];
   a.counter[group] = 0;
+  if (a.check && !isfinite(*a.check)) atomicOr(a.status, 4u);
   const double norm = sqrt(tot);
   float s = 1.0f;
   if (!isfinite(norm)) {

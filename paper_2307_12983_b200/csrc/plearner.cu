@@ -12,6 +12,7 @@
 #include <random>
 #include <vector>
 
+#include "comm.h"
 #include "critic_kernels.cuh"
 #include "learner.h"
 #include "optim.cuh"
@@ -19,8 +20,12 @@
 namespace pqlg {
 
 PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t init_seed,
-                   cudaStream_t st)
-    : cfg_(cfg), dims_(dims), stream_(st) {
+                   cudaStream_t st, pqlg_comm_s* comm)
+    : cfg_(cfg), dims_(dims), stream_(st), comm_(comm) {
+  if (comm_) {
+    rank_ = comm_->rank;
+    world_ = comm_->world;
+  }
   if (!stream_) {
     PQLG_CUDA(cudaStreamCreateWithFlags(&owned_stream_, cudaStreamNonBlocking));
     stream_ = owned_stream_;
@@ -68,9 +73,11 @@ PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   states_ = std::make_unique<DeviceStates>(cfg.buffer_capacity, D_, stream_);
   norm_.init(D_);
   sampler_.alloc(1);
-  replay::SamplerState s0{rng::derive_seed(cfg.seed, rng::kSample, 2), 0, 0, 0};
+  // make_rng(seed, sample, 2) (learners.cpp:212); data-parallel rank r: 2 + 2r
+  const uint64_t skey = rng::derive_seed(cfg.seed, rng::kSample, 2 + 2 * static_cast<uint64_t>(rank_));
+  replay::SamplerState s0{skey, 0, 0, 0};
   PQLG_CUDA(cudaMemcpy(sampler_.p, &s0, sizeof(s0), cudaMemcpyHostToDevice));
-  mt_.seed(rng::derive_seed(cfg.seed, rng::kSample, 2));
+  mt_.seed(skey);
   idx_.alloc(B_);
   idx_host_.resize(B_);
   step_.alloc(1);
@@ -216,6 +223,7 @@ void PLearner::build_update() {
     a.status = status_.p;
     a.step = step_.p;  // Adam step of the policy, advanced once per update
     a.B = B;
+    a.Bg = B * world_;
     steps_.push_back([a, loss_blocks](cudaStream_t st) {
       launch(critic::actor_pick_kernel, dim3(loss_blocks), dim3(critic::kRowThreads), 0, st, a);
     });
@@ -358,9 +366,28 @@ void PLearner::build_update() {
     f.scale = scale_.p;
     f.status = status_.p;
     f.max_norm = 0.5f;
+    f.skip_norm = comm_ ? 1 : 0;
     steps_.push_back([f, fb](cudaStream_t st) {
       launch(optim::finalize_kernel, dim3(dim3(fb, 1)), dim3(optim::kFinalizeThreads), 0, st, f);
     });
+    if (comm_) {  // data parallel: see VLearner::build_update
+      pqlg_comm_s* c = comm_;
+      float* g = grads_.p;
+      float* l = loss_.p;
+      const size_t n = static_cast<size_t>(pnet_.params);
+      steps_.push_back([c, g, n, l](cudaStream_t st) { allreduce_sum(c, g, n, l, 1, st); });
+      optim::FinalizeArgs f2 = f;
+      f2.seg[0] = optim::Segment{0, pnet_.params, grads_.p, 0, 1, 0};
+      f2.n_seg = 1;
+      f2.skip_norm = 0;
+      f2.check = loss_.p;
+      const int fb2 = optim::plan_finalize(f2);
+      block_sq2_.alloc(fb2);
+      f2.block_sq = block_sq2_.p;
+      steps_.push_back([f2, fb2](cudaStream_t st) {
+        launch(optim::finalize_kernel, dim3(dim3(fb2, 1)), dim3(optim::kFinalizeThreads), 0, st, f2);
+      });
+    }
     optim::AdamArgs a{};
     a.p = pol_.p;
     a.g = grads_.p;
@@ -539,6 +566,18 @@ int pqlg_plearner_create(const pqlg_config* cfg, const pqlg_task_dims* dims,
     auto h = std::make_unique<pqlg_plearner_s>();
     h->p = std::make_unique<PLearner>(*cfg, *dims, init_rng_seed,
                                       static_cast<cudaStream_t>(stream));
+    *out = h.release();
+  });
+}
+
+int pqlg_plearner_create_dp(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                            uint64_t init_rng_seed, pqlg_comm comm, void* stream,
+                            pqlg_plearner* out) {
+  return guarded([&] {
+    require(cfg && dims && out && comm, "plearner_create_dp: null argument");
+    auto h = std::make_unique<pqlg_plearner_s>();
+    h->p = std::make_unique<PLearner>(*cfg, *dims, init_rng_seed,
+                                      static_cast<cudaStream_t>(stream), comm);
     *out = h.release();
   });
 }

@@ -9,6 +9,7 @@
 #include <random>
 #include <vector>
 
+#include "comm.h"
 #include "critic_kernels.cuh"
 #include "learner.h"
 #include "optim.cuh"
@@ -18,8 +19,12 @@ namespace pqlg {
 using mlp::Step;
 
 VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t init_seed,
-                   cudaStream_t st)
-    : cfg_(cfg), dims_(dims), stream_(st) {
+                   cudaStream_t st, pqlg_comm_s* comm)
+    : cfg_(cfg), dims_(dims), stream_(st), comm_(comm) {
+  if (comm_) {
+    rank_ = comm_->rank;
+    world_ = comm_->world;
+  }
   if (!stream_) {  // the legacy default stream cannot be graph-captured
     PQLG_CUDA(cudaStreamCreateWithFlags(&owned_stream_, cudaStreamNonBlocking));
     stream_ = owned_stream_;
@@ -75,9 +80,12 @@ VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   nstep_ = std::make_unique<DeviceNStep>(cfg.n_envs, D_, A_, gamma_, cfg.n_step);
   norm_.init(D_);
   sampler_.alloc(1);
-  replay::SamplerState s0{rng::derive_seed(cfg.seed, rng::kSample, 1), 0, 0, 0};
+  // sample stream make_rng(seed, sample, 1) (learners.cpp:136); data-parallel
+  // rank r draws from its own stream 1 + 2r (rank 0 = the reference's)
+  const uint64_t skey = rng::derive_seed(cfg.seed, rng::kSample, 1 + 2 * static_cast<uint64_t>(rank_));
+  replay::SamplerState s0{skey, 0, 0, 0};
   PQLG_CUDA(cudaMemcpy(sampler_.p, &s0, sizeof(s0), cudaMemcpyHostToDevice));
-  mt_.seed(rng::derive_seed(cfg.seed, rng::kSample, 1));
+  mt_.seed(skey);
   idx_.alloc(B_);
   idx_host_.resize(B_);
 
@@ -237,6 +245,7 @@ void VLearner::build_update() {
     a.loss_out = loss_.p;
     a.status = status_.p;
     a.B = B;
+    a.Bg = B * world_;
     steps_.push_back([a, loss_blocks](cudaStream_t st) {
       launch(critic::critic_loss_kernel, dim3(loss_blocks), dim3(critic::kRowThreads), 0, st, a);
     });
@@ -335,10 +344,33 @@ void VLearner::build_update() {
     f.scale = scale_.p;
     f.status = status_.p;
     f.max_norm = 0.5f;
+    f.skip_norm = comm_ ? 1 : 0;
     const int fb = fin_blocks_;
     steps_.push_back([f, fb](cudaStream_t st) {
       launch(optim::finalize_kernel, dim3(dim3(fb, 2)), dim3(optim::kFinalizeThreads), 0, st, f);
     });
+    if (comm_) {
+      // data parallel: sum the twin gradients (each rank's upstream already
+      // carries 1/(B*world)) and the loss over ranks, then the norm + clip
+      // scale of the full-batch gradient (clip_global_norm per critic,
+      // learners.cpp:182-183) as an in-place single-term pass.
+      pqlg_comm_s* c = comm_;
+      float* g = grads_.p;
+      float* l = loss_.p;
+      const size_t n = 2 * static_cast<size_t>(Ps_);
+      steps_.push_back([c, g, n, l](cudaStream_t st) { allreduce_sum(c, g, n, l, 1, st); });
+      optim::FinalizeArgs f2 = f;
+      f2.seg[0] = optim::Segment{0, P, grads_.p, Ps_, 1, 0};
+      f2.n_seg = 1;
+      f2.skip_norm = 0;
+      f2.check = loss_.p;
+      const int fb2 = optim::plan_finalize(f2);
+      block_sq2_.alloc(2ull * fb2);
+      f2.block_sq = block_sq2_.p;
+      steps_.push_back([f2, fb2](cudaStream_t st) {
+        launch(optim::finalize_kernel, dim3(dim3(fb2, 2)), dim3(optim::kFinalizeThreads), 0, st, f2);
+      });
+    }
   }
   // ------------------------------------------------ clip + Adam + Polyak
   {
@@ -600,6 +632,20 @@ int pqlg_vlearner_create(const pqlg_config* cfg, const pqlg_task_dims* dims,
     auto h = std::make_unique<pqlg_vlearner_s>();
     h->v = std::make_unique<VLearner>(*cfg, *dims, init_rng_seed,
                                       static_cast<cudaStream_t>(stream));
+    h->replay_view.r = h->v->replay();
+    h->replay_view.norm.init(dims->obs_dim);
+    *out = h.release();
+  });
+}
+
+int pqlg_vlearner_create_dp(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                            uint64_t init_rng_seed, pqlg_comm comm, void* stream,
+                            pqlg_vlearner* out) {
+  return guarded([&] {
+    require(cfg && dims && out && comm, "vlearner_create_dp: null argument");
+    auto h = std::make_unique<pqlg_vlearner_s>();
+    h->v = std::make_unique<VLearner>(*cfg, *dims, init_rng_seed,
+                                      static_cast<cudaStream_t>(stream), comm);
     h->replay_view.r = h->v->replay();
     h->replay_view.norm.init(dims->obs_dim);
     *out = h.release();

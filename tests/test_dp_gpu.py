@@ -1,0 +1,117 @@
+"""Data-parallel learners (config 5) on one B200.
+
+The round-end box has one GPU, so the multi-rank exchange itself is covered
+by the gloo tests in test_dp_cpu.py; here a world-1 NCCL communicator runs
+the data-parallel update path (reduction-only finalize -> NCCL all-reduce of
+gradients + loss -> norm/clip pass -> Adam) and must equal the plain learner
+bit for bit, and a rank-1 learner must sample with its own Philox stream.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle_lib import param_count, ptr
+from paper_2307_12983_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def comm_world1():
+    ident = (C.c_uint8 * _lib.COMM_ID_BYTES)()
+    _lib.call("pqlg_comm_unique_id", ident)
+    comm = C.c_void_p()
+    _lib.call("pqlg_comm_init", 0, 1, ident, C.byref(comm))
+    return comm
+
+
+def fill(rp, n, seed):
+    _lib.call("pqlg_replay_fill_synthetic", rp, n, seed, np.float32(0.970299), 200)
+
+
+@pytest.mark.parametrize("D,A,H,nh,B", [(17, 6, 64, 2, 256), (211, 20, 512, 3, 1024)])
+def test_vlearner_dp_world1_bit_identical(D, A, H, nh, B):
+    import torch
+    torch.cuda.set_device(0)
+    comm = comm_world1()
+    r, w = C.c_int(), C.c_int()
+    _lib.call("pqlg_comm_rank", comm, C.byref(r), C.byref(w))
+    assert (r.value, w.value) == (0, 1)
+    cfg = _lib.default_config(batch_size=B, buffer_capacity=20000, hidden=H, hidden_layers=nh,
+                              n_envs=8)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    plain, dp = C.c_void_p(), C.c_void_p()
+    _lib.call("pqlg_vlearner_create", C.byref(cfg), C.byref(dims), 7, None, C.byref(plain))
+    _lib.call("pqlg_vlearner_create_dp", C.byref(cfg), C.byref(dims), 7, comm, None, C.byref(dp))
+    mean = np.zeros(D)
+    m2 = np.full(D, 1e6)
+    for h in (plain, dp):
+        rp = C.c_void_p()
+        _lib.call("pqlg_vlearner_replay", h, C.byref(rp))
+        fill(rp, 20000, 3)
+        ns = _lib.NormStats(10 ** 6, ptr(mean), ptr(m2))
+        _lib.call("pqlg_vlearner_adopt_norm", h, C.byref(ns))
+    l_plain, l_dp = C.c_float(), C.c_float()
+    for _ in range(3):
+        _lib.call("pqlg_vlearner_update", plain, C.byref(l_plain))
+        _lib.call("pqlg_vlearner_update", dp, C.byref(l_dp))
+        assert l_plain.value == l_dp.value
+    # graph replay path too
+    _lib.call("pqlg_vlearner_update_n", plain, 4)
+    _lib.call("pqlg_vlearner_update_n", dp, 4)
+    P = param_count([D + A] + [H] * nh + [1])
+    for which in range(4):
+        a = np.zeros(P, np.float32)
+        b = np.zeros(P, np.float32)
+        _lib.call("pqlg_vlearner_get_params", plain, which, ptr(a))
+        _lib.call("pqlg_vlearner_get_params", dp, which, ptr(b))
+        assert np.array_equal(a, b), which
+    kp, kd = C.c_int(), C.c_int()
+    _lib.call("pqlg_vlearner_kernels_per_update", plain, C.byref(kp))
+    _lib.call("pqlg_vlearner_kernels_per_update", dp, C.byref(kd))
+    assert kd.value == kp.value + 1  # the post-all-reduce norm pass
+    for h in (plain, dp):
+        _lib.call("pqlg_vlearner_destroy", h)
+    _lib.call("pqlg_comm_destroy", comm)
+
+
+def test_plearner_dp_world1_bit_identical():
+    import torch
+    torch.cuda.set_device(0)
+    D, A, H, nh, B = 31, 7, 64, 2, 512
+    comm = comm_world1()
+    cfg = _lib.default_config(batch_size=B, buffer_capacity=10000, hidden=H, hidden_layers=nh,
+                              n_envs=8)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    plain, dp = C.c_void_p(), C.c_void_p()
+    _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 5, None, C.byref(plain))
+    _lib.call("pqlg_plearner_create_dp", C.byref(cfg), C.byref(dims), 5, comm, None, C.byref(dp))
+    states = torch.randn(5000, D, device="cuda")
+    for h in (plain, dp):
+        _lib.call("pqlg_plearner_ingest", h, states.data_ptr(), D, 5000)
+    la, lb = C.c_float(), C.c_float()
+    for _ in range(3):
+        _lib.call("pqlg_plearner_update", plain, C.byref(la))
+        _lib.call("pqlg_plearner_update", dp, C.byref(lb))
+        assert la.value == lb.value
+    P = param_count([D] + [H] * nh + [A])
+    a = np.zeros(P, np.float32)
+    b = np.zeros(P, np.float32)
+    _lib.call("pqlg_plearner_get_params", plain, 0, ptr(a))
+    _lib.call("pqlg_plearner_get_params", dp, 0, ptr(b))
+    assert np.array_equal(a, b)
+    for h in (plain, dp):
+        _lib.call("pqlg_plearner_destroy", h)
+    _lib.call("pqlg_comm_destroy", comm)
+
+
+def test_comm_allreduce_world1_identity():
+    import torch
+    torch.cuda.set_device(0)
+    comm = comm_world1()
+    x = torch.randn(1000, device="cuda")
+    y = x.clone()
+    _lib.call("pqlg_comm_allreduce_f32", comm, y.data_ptr(), 1000, None)
+    torch.cuda.synchronize()
+    assert torch.equal(x, y)
+    _lib.call("pqlg_comm_destroy", comm)

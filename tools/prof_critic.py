@@ -34,4 +34,18 @@ if which in ("critic", "both"):
     for _ in range(3):
         _lib.call("pqlg_vlearner_update", h, C.byref(loss))
     st.synchronize()
+if which == "policy":
+    D, A, H, nh, B = 211, 20, 512, 3, 8192
+    cfg = _lib.default_config(batch_size=B, buffer_capacity=200_000, hidden=H, hidden_layers=nh,
+                              n_envs=16384)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    pl = C.c_void_p()
+    _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 1, C.c_void_p(st.cuda_stream),
+              C.byref(pl))
+    states = torch.randn(200_000, D, device="cuda")
+    _lib.call("pqlg_plearner_ingest", pl, states.data_ptr(), D, 200_000)
+    loss = C.c_float()
+    for _ in range(3):
+        _lib.call("pqlg_plearner_update", pl, C.byref(loss))
+    st.synchronize()
 print("done")
