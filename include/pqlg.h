@@ -275,7 +275,8 @@ PQLG_API int pqlg_vlearner_replay(pqlg_vlearner h, pqlg_replay* out);
  * for 0/1, critic.hpp:33-36); resets nothing else. */
 PQLG_API int pqlg_vlearner_set_params(pqlg_vlearner h, int which, const float* flat_host);
 /* Intermediates of the last update for parity checks: 0 TD target y [B],
- * 1 dLoss/dQ [2 x B], 2 flat gradients before clipping [2 x P],
+ * 1 dLoss/dQ [2 x B] (C51: dLoss/dlogits [2 x B x n_atoms]),
+ * 2 flat gradients before clipping [2 x P],
  * 3 clip scales [2], 4 sampled critic input [B x (obs_dim+act_dim)]. */
 PQLG_API int pqlg_vlearner_debug_read(pqlg_vlearner h, int what, float* host_out);
 /* Number of kernels one update launches (graph nodes). */

@@ -264,6 +264,54 @@ def gen_vupdate(R, out):
     out.update(pu_losses=pl, pu_params=pp)
 
 
+def gen_c51update(R, out):
+    """k=3 successive PQL-D (C51) V-learner updates and 3 P-learner updates
+    (c51_critic_loss / c51_actor_loss compositions, learners.cpp:157-188,
+    :239-270) with 51 atoms on [-10, 10]."""
+    rng = np.random.default_rng(8)
+    D, A, H, nh, B, cap, L = 9, 4, 32, 2, 48, 500, 51
+    ps = [D] + [H] * nh + [A]
+    qs = [D + A] + [H] * nh + [L]
+    pol = f32(rng.standard_normal(param_count(ps)) * 0.2)
+    q1 = f32(rng.standard_normal(param_count(qs)) * 0.2)
+    q2 = f32(rng.standard_normal(param_count(qs)) * 0.2)
+    n_rows = 300
+    obs = f32(rng.standard_normal((n_rows, D))); act = f32(rng.uniform(-1, 1, (n_rows, A)))
+    boot = f32(rng.standard_normal((n_rows, D))); ret = f32(rng.standard_normal(n_rows) * 2.0)
+    eff = f32(np.where(rng.uniform(size=n_rows) < 0.05, 0.0, 0.970299))
+    cnt = 1000; mean = rng.standard_normal(D) * 0.1; m2 = np.abs(rng.standard_normal(D)) * cnt
+    h = R.ref_vupdate_create(D, A, H, nh, B, cap, 0, ptr(q1), ptr(q2), ptr(pol), 1, L,
+                             np.float32(-10), np.float32(10))
+    R.ref_vupdate_insert(h, ptr(obs), ptr(act), ptr(boot), ptr(ret), ptr(eff), n_rows)
+    R.ref_vupdate_adopt_norm(h, cnt, ptr(mean), ptr(m2))
+    losses = np.zeros(3, np.float32)
+    for k in range(3):
+        l = np.zeros(1, np.float32)
+        assert R.ref_vupdate_step(h, ptr(l)) == 0
+        losses[k] = l[0]
+    P = param_count(qs)
+    res = np.zeros((4, P), np.float32)
+    for w in range(4):
+        R.ref_vupdate_params(h, w, ptr(res[w]))
+    R.ref_vupdate_destroy(h)
+    out.update(cu_dims=np.array([D, A, H, nh, B, cap, L]), cu_pol=pol, cu_q1=q1, cu_q2=q2,
+               cu_obs=obs, cu_act=act, cu_boot=boot, cu_ret=ret, cu_eff=eff,
+               cu_norm=np.array([cnt]), cu_mean=mean, cu_m2=m2, cu_losses=losses, cu_params=res)
+    h = R.ref_pupdate_create(D, A, H, nh, B, cap, 0, ptr(pol), ptr(q1), ptr(q2), 1, L,
+                             np.float32(-10), np.float32(10))
+    R.ref_pupdate_insert(h, ptr(obs), n_rows)
+    R.ref_pupdate_adopt_norm(h, cnt, ptr(mean), ptr(m2))
+    pl = np.zeros(3, np.float32)
+    for k in range(3):
+        l = np.zeros(1, np.float32)
+        assert R.ref_pupdate_step(h, ptr(l)) == 0
+        pl[k] = l[0]
+    pp = np.zeros(param_count(ps), np.float32)
+    R.ref_pupdate_params(h, ptr(pp))
+    R.ref_pupdate_destroy(h)
+    out.update(cpu_losses=pl, cpu_params=pp)
+
+
 def main():
     R = ref()
     if R is None:
@@ -271,7 +319,10 @@ def main():
     GOLDEN.mkdir(parents=True, exist_ok=True)
     for name, fn in [("indices", gen_indices), ("nstep", gen_nstep),
                      ("elementwise", gen_elementwise), ("norm", gen_norm), ("noise", gen_noise),
-                     ("mlp", gen_mlp), ("agents", gen_agents), ("vupdate", gen_vupdate)]:
+                     ("mlp", gen_mlp), ("agents", gen_agents), ("vupdate", gen_vupdate),
+                     ("c51update", gen_c51update)]:
+        if len(sys.argv) > 1 and name not in sys.argv[1:]:
+            continue
         out: dict = {}
         fn(R, out)
         np.savez_compressed(GOLDEN / f"{name}.npz", **out)

@@ -29,10 +29,11 @@ __device__ __forceinline__ float head_value(const float* partial, int64_t ld, in
 // Block sums of l -> block_loss[blockIdx.x]; the last block (ticket) adds the
 // block sums in fixed order (lane-strided, then an xor tree) and writes
 // out = sum / B, flagging a non-finite result in status.
+template <int kThreads = kRowThreads>
 __device__ __forceinline__ void block_mean_finish(double l, double* block_loss,
                                                   unsigned int* counter, int B, float* out,
                                                   uint32_t* status, uint32_t bit) {
-  __shared__ double red[kRowThreads / 32];
+  __shared__ double red[kThreads / 32];
   __shared__ bool last;
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) l += __shfl_down_sync(0xffffffffu, l, d);
@@ -40,7 +41,7 @@ __device__ __forceinline__ void block_mean_finish(double l, double* block_loss,
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int w = 0; w < kRowThreads / 32; ++w) s += red[w];
+    for (int w = 0; w < kThreads / 32; ++w) s += red[w];
     block_loss[blockIdx.x] = s;
     __threadfence();
     last = atomicAdd(counter, 1u) == gridDim.x - 1;

@@ -281,3 +281,68 @@ struct Store {
 };
 
 }  // namespace pqlg::epi
+
+namespace pqlg::epi {
+
+// Categorical (C51) critic head, c51.hpp:43-53 and :117-126: logits = acc +
+// b over the L <= 64 atoms of a row (one 64-column tile, so each epilogue
+// thread owns a whole row), then softmax_row (max, exp, running sum, divide)
+// and the expected value E = sum_j p_j z_j (float, j ascending, no FMA).
+// Writes probs[m*ld + j] and, if ev is set, ev[m].
+struct C51Head {
+  static constexpr int kStoreRank = 0;
+  static constexpr int kMaxAtoms = 64;
+  const float* bias[2];
+  float* probs[2];
+  int64_t ld;
+  float* ev[2];  // nullable
+  const float* atoms;
+  int M, L;
+  struct Row {
+    float x[kMaxAtoms];
+  };
+  __device__ void prepare(Row&, int group, int, int, int, float* scratch) const {
+    const int t = threadIdx.x - 64;
+    for (int i = t; i < kMaxAtoms; i += 128) {
+      scratch[i] = i < L ? bias[group][i] : 0.0f;
+      scratch[kMaxAtoms + i] = i < L ? atoms[i] : 0.0f;
+    }
+    ptx::named_bar_sync(1, 128);
+  }
+  __device__ bool chunk(Row& r, int, int, int, int n0, float (&v)[32], const float* scratch) const {
+    if (n0 == 0) {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) r.x[t] = __fadd_rn(v[t], scratch[t]);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) r.x[32 + t] = __fadd_rn(v[t], scratch[32 + t]);
+    }
+    return false;
+  }
+  __device__ void end(Row& r, int group, int, int m, int) const {
+    if (m >= M) return;
+    float mx = r.x[0];
+#pragma unroll
+    for (int j = 1; j < kMaxAtoms; ++j)
+      if (j < L) mx = mx < r.x[j] ? r.x[j] : mx;  // std::max(mx, l)
+    float sum = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kMaxAtoms; ++j)
+      if (j < L) {
+        r.x[j] = expf(__fsub_rn(r.x[j], mx));
+        sum = __fadd_rn(sum, r.x[j]);
+      }
+    float e = 0.0f;
+    float* out = probs[group] + static_cast<int64_t>(m) * ld;
+#pragma unroll
+    for (int j = 0; j < kMaxAtoms; ++j)
+      if (j < L) {
+        const float p = __fdiv_rn(r.x[j], sum);
+        out[j] = p;
+        e = __fadd_rn(e, __fmul_rn(p, __ldg(atoms + j)));
+      }
+    if (ev[group]) ev[group][m] = e;
+  }
+};
+
+}  // namespace pqlg::epi

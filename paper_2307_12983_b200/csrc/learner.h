@@ -55,6 +55,8 @@ class VLearner {
   pqlg_comm_s* comm_ = nullptr;  // data-parallel communicator (nullable)
   int rank_ = 0, world_ = 1;
   int D_, A_, H_, nh_, B_, Kp_;
+  bool dist_ = false;  // PQL-D: categorical (C51) critics with L_ atoms
+  int L_ = 1, Lp_ = 1;
   float reward_scale_, gamma_;
   NetShape qnet_, pnet_;
   int64_t Ps_ = 0;  // group stride of the twin-critic parameter blocks
@@ -94,6 +96,12 @@ class VLearner {
   DevBuf<unsigned int> fin_counter_;
   DevBuf<float> scale_;
   DevBuf<double> block_sq2_;  // data-parallel: norm pass after the all-reduce
+  // C51 (PQL-D) head state: atoms, target/online probabilities, expected
+  // values, upstream [2][B x Lp], head-bias partials, head weight partials,
+  // padded head mirrors (q1, q2, q1_target, q2_target)
+  DevBuf<float> atoms_, probs_t_, probs_o_, ev_t_, up51_, db51_, head_wpart_;
+  std::array<WeightMirror, 4> heads_;
+  int head_splits_ = 0, c51_blocks_ = 0;
 
   std::vector<mlp::Step> steps_;
   cudaGraphExec_t graph_exec_ = nullptr;
@@ -142,6 +150,8 @@ class PLearner {
   pqlg_comm_s* comm_ = nullptr;  // data-parallel communicator (nullable)
   int rank_ = 0, world_ = 1;
   int D_, A_, Ap_, H_, nh_, B_, Kp_;
+  bool dist_ = false;  // PQL-D actor objective (c51_actor_loss)
+  int L_ = 1, Lp_ = 1;
   NetShape qnet_, pnet_;
   int64_t Ps_ = 0;
   int64_t critic_version_ = 0;
@@ -176,6 +186,8 @@ class PLearner {
   DevBuf<unsigned int> fin_counter_;
   DevBuf<float> scale_;
   DevBuf<double> block_sq2_;
+  DevBuf<float> atoms_, probs_, ev_, up51_;  // C51 actor objective
+  std::array<WeightMirror, 2> heads_;
 
   std::vector<mlp::Step> steps_;
   cudaGraphExec_t graph_exec_ = nullptr;

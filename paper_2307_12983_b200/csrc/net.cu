@@ -22,6 +22,41 @@ void launch_pad_rows(const float* src, float* dst, int rows, int cols, int ld, c
 }
 
 namespace {
+struct PadMulti {
+  const float* src[4];
+  float* dst[4];
+  int rows, cols, ld;
+};
+__global__ void pad_rows_multi_kernel(const __grid_constant__ PadMulti a) {
+  pdl::entry();
+  const int k = blockIdx.y;
+  const int64_t n = static_cast<int64_t>(a.rows) * a.cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / a.cols, c = i % a.cols;
+    a.dst[k][r * a.ld + c] = a.src[k][i];
+  }
+}
+}  // namespace
+
+void refresh_mirrors(const WeightMirror* m, int n, cudaStream_t st) {
+  if (n <= 0 || !m[0].needed()) return;
+  require(n <= 4, "refresh_mirrors: at most 4");
+  PadMulti a{};
+  for (int k = 0; k < n; ++k) {
+    require(m[k].in == m[0].in && m[k].out == m[0].out, "refresh_mirrors: shapes differ");
+    a.src[k] = m[k].src;
+    a.dst[k] = m[k].buf.p;
+  }
+  a.rows = m[0].in;
+  a.cols = m[0].out;
+  a.ld = m[0].ld;
+  const int64_t total = static_cast<int64_t>(a.rows) * a.cols;
+  const int blocks = static_cast<int>(std::min<int64_t>(148, (total + 255) / 256));
+  launch(pad_rows_multi_kernel, dim3(blocks, n), dim3(256), 0, st, a);
+}
+
+namespace {
 // detail::orthogonalize (mlp.hpp:209-225), T = float.
 void orthogonalize(std::vector<float>& a, size_t rows, size_t cols) {
   for (size_t c = 0; c < cols; ++c) {

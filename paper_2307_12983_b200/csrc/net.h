@@ -60,6 +60,20 @@ struct WeightMirror {
   }
 };
 
+// Refreshes up to 4 mirrors of the same shape in one launch.
+void refresh_mirrors(const WeightMirror* m, int n, cudaStream_t st);
+
+// CategoricalHead::create (c51.hpp:21-34): z_j = float(vmin + dz*j) in fp64,
+// the end points exact.
+inline std::vector<float> c51_atoms(int L, float vmin, float vmax) {
+  std::vector<float> z(L);
+  const double dz = (static_cast<double>(vmax) - vmin) / static_cast<double>(L - 1);
+  for (int j = 0; j < L; ++j) z[j] = static_cast<float>(static_cast<double>(vmin) + dz * j);
+  z.front() = vmin;
+  z.back() = vmax;
+  return z;
+}
+
 // Orthogonal init (mlp.hpp:230-249): modified Gram-Schmidt on a
 // normal_distribution<double> draw, in T = float, with -ffp-contract=off
 // semantics (this TU is compiled without contraction for host code).

@@ -12,6 +12,7 @@
 #include <random>
 #include <vector>
 
+#include "c51_kernels.cuh"
 #include "comm.h"
 #include "critic_kernels.cuh"
 #include "learner.h"
@@ -30,7 +31,15 @@ PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
     PQLG_CUDA(cudaStreamCreateWithFlags(&owned_stream_, cudaStreamNonBlocking));
     stream_ = owned_stream_;
   }
-  require(cfg.algo == PQLG_ALGO_DDPG, "plearner: the C51 actor objective is not built yet");
+  require(cfg.algo == PQLG_ALGO_DDPG || cfg.algo == PQLG_ALGO_C51, "plearner: unknown algo");
+  dist_ = cfg.algo == PQLG_ALGO_C51;
+  if (dist_) {
+    require(cfg.n_atoms >= 2 && cfg.n_atoms <= c51::kMaxAtoms,
+            "plearner: n_atoms must be in [2, 64]");
+    require(cfg.vmin < cfg.vmax, "categorical head: bad support");
+    L_ = cfg.n_atoms;
+    Lp_ = static_cast<int>(round_up(L_, 4));
+  }
   require(cfg.hidden_layers >= 1 && cfg.hidden >= 32 && cfg.hidden % 32 == 0,
           "plearner: hidden width must be a multiple of 32");
   D_ = dims.obs_dim;
@@ -47,7 +56,7 @@ PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
     qs.push_back(H_);
     ps.push_back(H_);
   }
-  qs.push_back(1);
+  qs.push_back(L_);  // learners.cpp:206-209
   ps.push_back(A_);
   qnet_ = NetShape::make(qs);
   pnet_ = NetShape::make(ps);
@@ -128,14 +137,26 @@ void PLearner::build_update() {
     cmask_[k].resize(nh);
     Gc_[k].resize(nh);
     for (int l = 0; l < nh; ++l) {
-      cact_[k][l].alloc(l + 1 < nh ? static_cast<size_t>(B) * H : 0);
+      cact_[k][l].alloc((l + 1 < nh || dist_) ? static_cast<size_t>(B) * H : 0);
       cmask_[k][l].alloc(static_cast<size_t>(B) * wpr);
       Gc_[k][l].alloc(static_cast<size_t>(B) * H);
     }
     dact_[k].alloc(static_cast<size_t>(B) * Ap_);
   }
   const int loss_blocks = (B + critic::kRowThreads - 1) / critic::kRowThreads;
-  block_loss_.alloc(loss_blocks);
+  block_loss_.alloc((B + c51::kThreads - 1) / c51::kThreads);  // >= either pick kernel's grid
+  if (dist_) {
+    const auto z = c51_atoms(L_, static_cast<float>(cfg_.vmin), static_cast<float>(cfg_.vmax));
+    atoms_.alloc(L_);
+    PQLG_CUDA(cudaMemcpy(atoms_.p, z.data(), L_ * 4, cudaMemcpyHostToDevice));
+    probs_.alloc(2ull * B * Lp_);
+    ev_.alloc(2ull * B);
+    up51_.alloc(2ull * B * Lp_);
+    for (int k = 0; k < 2; ++k) heads_[k].init(q[k] + qnet_.w_off[nh], H, L_);
+    // critic snapshots are adopted between updates: refresh the padded heads first
+    const WeightMirror* hm = heads_.data();
+    steps_.push_back([hm](cudaStream_t st) { refresh_mirrors(hm, 2, st); });
+  }
   loss_counter_.alloc(1);
 
   // ------------------------------------------------- sample + normalize
@@ -192,8 +213,8 @@ void PLearner::build_update() {
     e.M = B;
     e.N = H;
     const bool last = l + 1 == nh;
-    e.store = last ? 0 : 1;
-    if (last) {
+    e.store = (last && !dist_) ? 0 : 1;
+    if (last && !dist_) {
       for (int k = 0; k < 2; ++k) e.w_head[k] = q[k] + qnet_.w_off[nh];
       e.partial = part_.p;
       e.ld_part = B;
@@ -203,12 +224,49 @@ void PLearner::build_update() {
     const float* a1 = l == 0 ? X_.p : cact_[1][l - 1].p;
     const int64_t lda = l == 0 ? Kp_ : H;
     const int K = l == 0 ? K0 : H;
+    const bool st = !last || dist_;
     steps_.push_back(mlp::fwd(a0, a1, lda, q[0] + qnet_.w_off[l], q[1] + qnet_.w_off[l], B, H, K,
-                              2, e, 0, last ? nullptr : cact_[0][l].p,
-                              last ? nullptr : cact_[1][l].p, H));
+                              2, e, 0, st ? cact_[0][l].p : nullptr,
+                              st ? cact_[1][l].p : nullptr, H));
+  }
+  if (dist_) {
+    // categorical heads at (s, pi(s)): softmax + expected value (c51.hpp:175-187)
+    epi::C51Head ch{};
+    for (int k = 0; k < 2; ++k) {
+      ch.bias[k] = q[k] + qnet_.b_off[nh];
+      ch.probs[k] = probs_.p + static_cast<size_t>(k) * B * Lp_;
+      ch.ev[k] = ev_.p + static_cast<size_t>(k) * B;
+    }
+    ch.ld = Lp_;
+    ch.atoms = atoms_.p;
+    ch.M = B;
+    ch.L = L_;
+    steps_.push_back(mlp::fwd(cact_[0][nh - 1].p, cact_[1][nh - 1].p, H, heads_[0].ptr(),
+                              heads_[1].ptr(), B, L_, H, 2, ch, heads_[0].stride()));
   }
   // ------------------------------------------------ min critic + upstream
-  {
+  if (dist_) {
+    c51::ActorPickArgs a{};
+    for (int k = 0; k < 2; ++k) {
+      a.po[k] = probs_.p + static_cast<size_t>(k) * B * Lp_;
+      a.ev[k] = ev_.p + static_cast<size_t>(k) * B;
+    }
+    a.ld = Lp_;
+    a.atoms = atoms_.p;
+    a.L = L_;
+    a.up = up51_.p;
+    a.step = step_.p;
+    a.block_loss = block_loss_.p;
+    a.counter = loss_counter_.p;
+    a.loss_out = loss_.p;
+    a.status = status_.p;
+    a.B = B;
+    a.Bg = B * world_;
+    const int blocks = (B + c51::kThreads - 1) / c51::kThreads;
+    steps_.push_back([a, blocks](cudaStream_t st) {
+      launch(c51::c51_actor_pick_kernel, dim3(blocks), dim3(c51::kThreads), 0, st, a);
+    });
+  } else {
     critic::LossArgs a{};
     a.partial = part_.p;
     a.ld = B;
@@ -229,7 +287,18 @@ void PLearner::build_update() {
     });
   }
   // --------------------------------- input gradient through the critics
-  {
+  if (dist_) {
+    // backward_input_only through the categorical heads: G = (up W^T) * mask
+    epi::DgradMask dm{};
+    for (int k = 0; k < 2; ++k) dm.mask[k] = cmask_[k][nh - 1].p;
+    dm.ld_mask = wpr;
+    dm.bn = bnH;
+    dm.M = B;
+    dm.N = H;
+    steps_.push_back(mlp::dgrad(up51_.p, up51_.p + static_cast<size_t>(B) * Lp_, Lp_,
+                                heads_[0].ptr(), heads_[1].ptr(), heads_[0].stride(), B, H, L_, 2,
+                                dm, Gc_[0][nh - 1].p, Gc_[1][nh - 1].p, H));
+  } else {
     critic::HeadInputGradArgs a{};
     a.up = up_.p;
     for (int k = 0; k < 2; ++k) {

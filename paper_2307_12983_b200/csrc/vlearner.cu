@@ -9,6 +9,7 @@
 #include <random>
 #include <vector>
 
+#include "c51_kernels.cuh"
 #include "comm.h"
 #include "critic_kernels.cuh"
 #include "learner.h"
@@ -31,7 +32,15 @@ VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   }
   st = stream_;
   require(cfg.algo == PQLG_ALGO_DDPG || cfg.algo == PQLG_ALGO_C51, "vlearner: unknown algo");
-  require(cfg.algo == PQLG_ALGO_DDPG, "vlearner: the C51 critic is not built in this version");
+  dist_ = cfg.algo == PQLG_ALGO_C51;
+  if (dist_) {
+    // CategoricalHead::create (c51.hpp:21-27) validation
+    require(cfg.n_atoms >= 2 && cfg.n_atoms <= c51::kMaxAtoms,
+            "vlearner: n_atoms must be in [2, 64]");
+    require(cfg.vmin < cfg.vmax, "categorical head: bad support");
+    L_ = cfg.n_atoms;
+    Lp_ = static_cast<int>(round_up(L_, 4));
+  }
   require(cfg.hidden_layers >= 1 && cfg.hidden >= 32 && cfg.hidden % 32 == 0,
           "vlearner: hidden width must be a multiple of 32");
   require(cfg.batch_size >= 1, "vlearner: batch_size must be >= 1");
@@ -49,7 +58,7 @@ VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
     qs.push_back(H_);
     ps.push_back(H_);
   }
-  qs.push_back(1);
+  qs.push_back(L_);  // learners.cpp:127-130: n_atoms outputs for pql_d, else 1
   ps.push_back(A_);
   qnet_ = NetShape::make(qs);
   pnet_ = NetShape::make(ps);
@@ -134,7 +143,7 @@ void VLearner::build_update() {
     omask_[k].resize(nh);
     G_[k].resize(nh);
     for (int l = 0; l < nh; ++l) {
-      tact_[k][l].alloc(l + 1 < nh ? static_cast<size_t>(B) * H : 0);
+      tact_[k][l].alloc((l + 1 < nh || dist_) ? static_cast<size_t>(B) * H : 0);
       oact_[k][l].alloc(static_cast<size_t>(B) * H);
       omask_[k][l].alloc(static_cast<size_t>(B) * wpr);
       G_[k][l].alloc(static_cast<size_t>(B) * H);
@@ -144,8 +153,30 @@ void VLearner::build_update() {
   part_o_.alloc(2ull * nt * B);
   up_.alloc(2ull * B);
   const int loss_blocks = (B + critic::kRowThreads - 1) / critic::kRowThreads;
-  block_loss_.alloc(loss_blocks);
+  block_loss_.alloc((B + c51::kThreads - 1) / c51::kThreads);  // >= either loss kernel's grid
   loss_counter_.alloc(1);
+
+  if (dist_) {
+    const auto z = c51_atoms(L_, static_cast<float>(cfg_.vmin), static_cast<float>(cfg_.vmax));
+    atoms_.alloc(L_);
+    PQLG_CUDA(cudaMemcpy(atoms_.p, z.data(), L_ * 4, cudaMemcpyHostToDevice));
+    probs_t_.alloc(2ull * B * Lp_);
+    probs_o_.alloc(2ull * B * Lp_);
+    ev_t_.alloc(2ull * B);
+    up51_.alloc(2ull * B * Lp_);
+    c51_blocks_ = (B + c51::kThreads - 1) / c51::kThreads;
+    db51_.alloc(2ull * c51_blocks_ * L_);
+    // the GEMMs read the 51-wide heads from padded mirrors (16-byte rows),
+    // refreshed at the start of every update (the previous update's Adam /
+    // Polyak, or set_params, changed them)
+    const float* src[4] = {q1, q2, q1t, q2t};
+    for (int k = 0; k < 4; ++k) heads_[k].init(src[k] + qnet_.w_off[nh], H, L_);
+    const WeightMirror* hm = heads_.data();
+    steps_.push_back([hm](cudaStream_t st) { refresh_mirrors(hm, 4, st); });
+    PQLG_CUDA(cudaFuncSetAttribute(c51::c51_critic_loss_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(c51::kLossSmem)));
+  }
 
   // ---------------------------------------------------------------- sample
   steps_.push_back([this, B](cudaStream_t st) {
@@ -202,8 +233,8 @@ void VLearner::build_update() {
       e.M = B;
       e.N = H;
       const bool last = l + 1 == nh;
-      e.store = (!target || !last) ? 1 : 0;
-      if (last) {
+      e.store = (!target || !last || dist_) ? 1 : 0;
+      if (last && !dist_) {
         for (int k = 0; k < 2; ++k) e.w_head[k] = nets[k] + qnet_.w_off[nh];
         e.partial = part;
         e.ld_part = B;
@@ -219,12 +250,61 @@ void VLearner::build_update() {
       steps_.push_back(mlp::fwd(a0, a1, lda, nets[0] + qnet_.w_off[l], nets[1] + qnet_.w_off[l],
                                 B, H, K, 2, e, 0, d0, d1, H));
     }
+    if (dist_) {
+      // categorical head H -> L: logits + softmax (+ expected values of the
+      // target heads) in the epilogue (c51.hpp:114-126, :135-138)
+      epi::C51Head ch{};
+      float* pr = target ? probs_t_.p : probs_o_.p;
+      for (int k = 0; k < 2; ++k) {
+        ch.bias[k] = nets[k] + qnet_.b_off[nh];
+        ch.probs[k] = pr + static_cast<size_t>(k) * B * Lp_;
+        ch.ev[k] = target ? ev_t_.p + static_cast<size_t>(k) * B : nullptr;
+      }
+      ch.ld = Lp_;
+      ch.atoms = atoms_.p;
+      ch.M = B;
+      ch.L = L_;
+      const int mi = target ? 2 : 0;
+      const auto& hl = target ? tact_ : oact_;
+      steps_.push_back(mlp::fwd(hl[0][nh - 1].p, hl[1][nh - 1].p, H, heads_[mi].ptr(),
+                                heads_[mi + 1].ptr(), B, L_, H, 2, ch, heads_[mi].stride()));
+    }
   };
 
   critic_fwd(true);
   critic_fwd(false);
   // ------------------------------------------- TD target + loss + upstream
-  {
+  if (dist_) {
+    c51::CriticLossArgs a{};
+    for (int k = 0; k < 2; ++k) {
+      a.pt[k] = probs_t_.p + static_cast<size_t>(k) * B * Lp_;
+      a.evt[k] = ev_t_.p + static_cast<size_t>(k) * B;
+      a.po[k] = probs_o_.p + static_cast<size_t>(k) * B * Lp_;
+    }
+    a.ld = Lp_;
+    a.ret = ret_.p;
+    a.eff = eff_.p;
+    a.atoms = atoms_.p;
+    const float vmin = static_cast<float>(cfg_.vmin), vmax = static_cast<float>(cfg_.vmax);
+    a.vmin = vmin;  // head.vmin / vmax are floats widened to double (c51.hpp:72)
+    a.vmax = vmax;
+    a.dz = (static_cast<double>(vmax) - vmin) / static_cast<double>(L_ - 1);
+    a.L = L_;
+    a.up = up51_.p;
+    a.db_part = db51_.p;
+    a.step = step_.p;
+    a.block_loss = block_loss_.p;
+    a.counter = loss_counter_.p;
+    a.loss_out = loss_.p;
+    a.status = status_.p;
+    a.B = B;
+    a.Bg = B * world_;
+    const int blocks = c51_blocks_;
+    steps_.push_back([a, blocks](cudaStream_t st) {
+      launch(c51::c51_critic_loss_kernel, dim3(blocks), dim3(c51::kThreads), c51::kLossSmem, st,
+             a);
+    });
+  } else {
     critic::LossArgs a{};
     a.partial = part_o_.p;
     a.ld = B;
@@ -265,7 +345,28 @@ void VLearner::build_update() {
   head_dw_.alloc(2ull * ht * H);
   head_db_.alloc(2ull * ht);
   head_cs_.alloc(2ull * ht * H);
-  {
+  if (dist_) {
+    // categorical head layer H -> L (fa::backward, mlp.hpp:161-184):
+    //   dW_head = h^T up   (split-K over the batch, fixed-order reduction)
+    //   G_{nh-1} = (up W_head^T) * [h > 0]  + bias column sums of layer nh-1
+    head_splits_ = mlp::wgrad_splits(H, L_, B, 2);
+    head_wpart_.alloc(2ull * head_splits_ * H * Lp_);
+    const float* u0 = up51_.p;
+    const float* u1 = up51_.p + static_cast<size_t>(B) * Lp_;
+    steps_.push_back(mlp::wgrad(oact_[0][nh - 1].p, oact_[1][nh - 1].p, H, u0, u1, Lp_, H, L_,
+                                B, 2, head_splits_, epi::Partial{}, head_wpart_.p, Lp_));
+    epi::DgradMask dm{};
+    for (int k = 0; k < 2; ++k) dm.mask[k] = omask_[k][nh - 1].p;
+    dm.ld_mask = wpr;
+    dm.colsum = colsum_[nh - 1].p;
+    dm.ld_cs = H;
+    dm.m_tiles = mt;
+    dm.bn = bnH;
+    dm.M = B;
+    dm.N = H;
+    steps_.push_back(mlp::dgrad(u0, u1, Lp_, heads_[0].ptr(), heads_[1].ptr(), heads_[0].stride(),
+                                B, H, L_, 2, dm, G_[0][nh - 1].p, G_[1][nh - 1].p, H));
+  } else {
     critic::HeadBwdArgs a{};
     a.up = up_.p;
     for (int k = 0; k < 2; ++k) {
@@ -320,16 +421,27 @@ void VLearner::build_update() {
       f.seg[s++] = optim::Segment{qnet_.w_off[l], static_cast<int64_t>(in) * H, wpart_[l].p,
                                   static_cast<int64_t>(wsplits_[l]) * in * H, wsplits_[l],
                                   static_cast<int64_t>(in) * H};
-      if (l + 1 < nh)
+      if (l + 1 < nh || dist_)
         f.seg[s++] = optim::Segment{qnet_.b_off[l], H, colsum_[l].p,
                                     static_cast<int64_t>(mt) * H, mt, H};
       else
         f.seg[s++] = optim::Segment{qnet_.b_off[l], H, head_cs_.p, static_cast<int64_t>(ht) * H,
                                     ht, H};
     }
-    f.seg[s++] = optim::Segment{qnet_.w_off[nh], H, head_dw_.p, static_cast<int64_t>(ht) * H,
-                                ht, H};
-    f.seg[s++] = optim::Segment{qnet_.b_off[nh], 1, head_db_.p, ht, ht, 1};
+    if (dist_) {
+      optim::Segment wh{qnet_.w_off[nh], static_cast<int64_t>(H) * L_, head_wpart_.p,
+                        static_cast<int64_t>(head_splits_) * H * Lp_, head_splits_,
+                        static_cast<int64_t>(H) * Lp_};
+      wh.cols = L_;
+      wh.ld_src = Lp_;
+      f.seg[s++] = wh;
+      f.seg[s++] = optim::Segment{qnet_.b_off[nh], L_, db51_.p,
+                                  static_cast<int64_t>(c51_blocks_) * L_, c51_blocks_, L_};
+    } else {
+      f.seg[s++] = optim::Segment{qnet_.w_off[nh], H, head_dw_.p, static_cast<int64_t>(ht) * H,
+                                  ht, H};
+      f.seg[s++] = optim::Segment{qnet_.b_off[nh], 1, head_db_.p, ht, ht, 1};
+    }
     require(s <= optim::kMaxSegments, "vlearner: too many layers");
     f.n_seg = s;
     f.total = P;
@@ -568,7 +680,11 @@ void VLearner::debug_read(int what, float* out) {
       PQLG_CUDA(cudaMemcpyAsync(out, y_.p, B_ * 4, cudaMemcpyDeviceToHost, stream_));
       break;
     case 1:
-      PQLG_CUDA(cudaMemcpyAsync(out, up_.p, 2ull * B_ * 4, cudaMemcpyDeviceToHost, stream_));
+      if (dist_)  // C51: dLoss/dlogits [2 x B x L]
+        PQLG_CUDA(cudaMemcpy2DAsync(out, L_ * 4, up51_.p, Lp_ * 4, L_ * 4, 2ull * B_,
+                                    cudaMemcpyDeviceToHost, stream_));
+      else
+        PQLG_CUDA(cudaMemcpyAsync(out, up_.p, 2ull * B_ * 4, cudaMemcpyDeviceToHost, stream_));
       break;
     case 2:
       PQLG_CUDA(cudaMemcpy2DAsync(out, P * 4, grads_.p, Ps_ * 4, P * 4, 2,

@@ -370,6 +370,29 @@ def test_vupdate_k_steps_match_reference_golden():
     assert np.linalg.norm(p.pol - G["pu_params"]) / np.linalg.norm(G["pu_params"]) < 1e-4
 
 
+def test_c51_update_k_steps_match_reference_golden():
+    """PQL-D: 3 c51 critic updates + 3 c51 policy updates (51 atoms) of the
+    restatement vs the compiled reference (tests/golden/c51update.npz)."""
+    G = golden("c51update")
+    D, A, H, nh, B, cap, L = (int(v) for v in G["cu_dims"])
+    o = OracleVUpdate(D, A, H, nh, B, G["cu_q1"], G["cu_q2"], G["cu_pol"], distributional=True,
+                      n_atoms=L)
+    o.set_rows(G["cu_obs"], G["cu_act"], G["cu_boot"], G["cu_ret"], G["cu_eff"])
+    o.norm = (int(G["cu_norm"][0]), G["cu_mean"], G["cu_m2"])
+    losses = [o.step()[0] for _ in range(3)]
+    np.testing.assert_allclose(losses, G["cu_losses"], rtol=1e-5)
+    for w, arr in enumerate([o.q[0], o.q[1], o.qt[0], o.qt[1]]):
+        want = G["cu_params"][w]
+        assert np.linalg.norm(arr - want) / np.linalg.norm(want) < 1e-4
+    p = OraclePUpdate(D, A, H, nh, B, G["cu_pol"], G["cu_q1"], G["cu_q2"], distributional=True,
+                      n_atoms=L)
+    p.states = G["cu_obs"]
+    p.norm = o.norm
+    pl = [p.step()[0] for _ in range(3)]
+    np.testing.assert_allclose(pl, G["cpu_losses"], rtol=1e-5)
+    assert np.linalg.norm(p.pol - G["cpu_params"]) / np.linalg.norm(G["cpu_params"]) < 1e-4
+
+
 def test_init_orthogonal_golden_present():
     G = golden("mlp")
     assert G["init_policy"].size == param_count([6, 16, 16, 3])
