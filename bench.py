@@ -295,6 +295,55 @@ def run_ours(args, rank, world, local):
                 clocks=clk.summary(), launches=int(launches), kpu=kpu.value)
 
 
+def run_c51(args, rank, world, local, steps, warmup):
+    """Config 4 (PQL-D): C51 critic updates/s and policy updates/s at batch
+    8192 with 51 atoms on [-10, 10], c3 dims, graph-replayed."""
+    import torch
+    from paper_2307_12983_b200 import _lib
+    D, A, H, nh, B, N, cap = CONFIGS["c3"]
+    stream = torch.cuda.Stream(device=local)
+    sp = C.c_void_p(stream.cuda_stream)
+    cfg = _lib.default_config(algo=_lib.ALGO_C51, n_atoms=51, vmin=-10.0, vmax=10.0,
+                              reward_scale=0.01, batch_size=B, buffer_capacity=1_000_000,
+                              hidden=H, hidden_layers=nh, n_envs=N, seed=0)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    vl, pl = C.c_void_p(), C.c_void_p()
+    comm = _lib.comm_from_torch_dist(rank, world) if world > 1 else None
+    if comm is not None:
+        _lib.call("pqlg_vlearner_create_dp", C.byref(cfg), C.byref(dims), 1, comm, sp, C.byref(vl))
+        _lib.call("pqlg_plearner_create_dp", C.byref(cfg), C.byref(dims), 1, comm, sp, C.byref(pl))
+    else:
+        _lib.call("pqlg_vlearner_create", C.byref(cfg), C.byref(dims), 1, sp, C.byref(vl))
+        _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 1, sp, C.byref(pl))
+    rp = C.c_void_p()
+    _lib.call("pqlg_vlearner_replay", vl, C.byref(rp))
+    _lib.call("pqlg_replay_fill_synthetic", rp, 1_000_000, 2000 + rank, np.float32(0.970299), 200)
+    states = torch.randn(1_000_000, D, device=f"cuda:{local}")
+    _lib.call("pqlg_plearner_ingest", pl, states.data_ptr(), D, 1_000_000)
+    out = {"workload": "c4: PQL-D critic (51 atoms on [-10, 10]) + policy, c3 dims, batch 8192"}
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for key, h, fn in (("critic_updates", vl, "pqlg_vlearner_update_n"),
+                       ("policy_updates", pl, "pqlg_plearner_update_n")):
+        _lib.call(fn, h, warmup)
+        stream.synchronize()
+        barrier(world)
+        ev0.record(stream)
+        _lib.call(fn, h, steps)
+        ev1.record(stream)
+        ev1.synchronize()
+        ms = max_over_ranks(ev0.elapsed_time(ev1), world)
+        out[key] = {"value": world * steps / (ms * 1e-3), "unit": "updates/s",
+                    "ms_per_step": ms / steps}
+    loss = C.c_float()
+    _lib.call("pqlg_vlearner_last_loss", vl, C.byref(loss))
+    out["last_critic_loss"] = loss.value
+    _lib.call("pqlg_vlearner_destroy", vl)
+    _lib.call("pqlg_plearner_destroy", pl)
+    if comm is not None:
+        _lib.call("pqlg_comm_destroy", comm)
+    return out
+
+
 def run_actor(args, rank, world, local, steps, warmup):
     """Actor transitions/s: one ActorCore::rollout_step over N envs (normalize
     -> policy -> mixed noise -> synthetic env -> StepSlice -> normalizer
@@ -512,11 +561,13 @@ def main():
     r = run_ours(args, rank, world, local)
     actor = run_actor(args, rank, world, local, max(10, args.steps // 4), max(3, args.warmup // 4))
     policy = run_policy(args, rank, world, local, args.steps, args.warmup)
+    c51 = run_c51(args, rank, world, local, max(10, args.steps // 2), max(3, args.warmup // 2))
     if rank != 0:
         return
     out = dict(base)
     out["actor"] = actor
     out["policy_updates"] = policy
+    out["c51"] = c51
     out.update(value=r["value"], ms_per_step=r["ms_step"], e2e=r["e2e"], roofline=r["roof"],
                clocks=r["clocks"], gpu_launches=r["launches"],
                kernels_per_update=r["kpu"], last_loss=r["loss"])

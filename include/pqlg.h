@@ -49,6 +49,11 @@ PQLG_API const char* pqlg_last_error(void);
 PQLG_API int pqlg_abi_version(void);
 /* Number of kernels this library launched since load (evidence counter). */
 PQLG_API uint64_t pqlg_launch_count(void);
+/* Per-launch device timing for profiling: between begin and end every kernel
+ * this library launches outside CUDA-graph capture is bracketed by events;
+ * end synchronizes and writes "name\tms\n" lines into out (cap bytes). */
+PQLG_API int pqlg_profile_begin(void);
+PQLG_API int pqlg_profile_end(char* out, int cap);
 
 /* ------------------------------------------------- operator-level test hooks
  * Device-pointer restatements of pql::kernels (kernels.hpp:25-60); there is

@@ -64,6 +64,8 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_last_error": (C.c_char_p, []),
     "pqlg_abi_version": (i32, []),
     "pqlg_launch_count": (u64, []),
+    "pqlg_profile_begin": (i32, []),
+    "pqlg_profile_end": (i32, [C.c_char_p, i32]),
     "pqlg_k_gemm_tf32": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32,
                                i32, vp]),
     "pqlg_replay_create": (i32, [u64, i32, i32, vp, P(vp)]),

@@ -13,9 +13,6 @@
 //   c51_actor_pick_kernel   c51_actor_loss (c51.hpp:159-205): loss -= min E,
 //                           upstream -s_k (z_k - E)/B of the picked head only.
 //
-// One thread per row (the projection's float accumulation order is the
-// reference's); the projected distribution / upstream rows live in shared
-// memory as [atom][thread] so a warp's accesses hit distinct banks.
 #pragma once
 
 #include <cstdint>
@@ -25,10 +22,10 @@
 
 namespace pqlg::c51 {
 
-constexpr int kThreads = 128;
+constexpr int kThreads = 128;    // actor-pick kernel: one thread per row
 constexpr int kMaxAtoms = 64;
-constexpr int kSmemStride = kThreads + 1;
-constexpr size_t kLossSmem = 2ull * kMaxAtoms * kSmemStride * sizeof(float);
+constexpr int kLossWarps = 8;    // critic-loss kernel: one warp per row
+constexpr int kLossBlocks = 296; // 2 x 148 SMs; warps stride over the rows
 
 struct CriticLossArgs {
   const float* pt[2];   // target probs [B x ld]
@@ -41,7 +38,7 @@ struct CriticLossArgs {
   double vmin, vmax, dz;
   int L;
   float* up;       // [2][B x ld] dLoss/dlogits
-  float* db_part;  // [2][gridDim.x][L] per-block column sums of up
+  float* db_part;  // [2][kLossBlocks * kLossWarps][L] per-warp column sums of up
   int64_t* step;   // Adam step, advanced once per update
   double* block_loss;
   unsigned int* counter;
@@ -51,81 +48,118 @@ struct CriticLossArgs {
   int Bg;  // mean divisor (global batch when data-parallel)
 };
 
-static __global__ void __launch_bounds__(kThreads)
+// One warp per row, lane j owning atoms j and j + 32.  The projection's
+// float accumulation into each atom keeps the reference's order, source
+// atoms j ascending (c51.hpp:79-95): every lane first computes its sources'
+// (lo, mass-to-lo, mass-to-lo+1); since Tz_j = G + eff*z_j is nondecreasing
+// in j (eff >= 0), lo_j is sorted, so the sources of target atom i are one
+// contiguous run -- those with lo_j == i-1 (split mass) followed by those
+// with lo_j == i -- found by binary search and folded left to right.
+static __global__ void __launch_bounds__(kLossWarps * 32)
     c51_critic_loss_kernel(const __grid_constant__ CriticLossArgs a) {
-  extern __shared__ float sm[];
-  float* q1 = sm;                             // [atom][thread]: proj, then up of q1
-  float* q2 = sm + kMaxAtoms * kSmemStride;   // up of q2
+  __shared__ int s_lo[kLossWarps][kMaxAtoms];
+  __shared__ float s_cl[kLossWarps][kMaxAtoms];
+  __shared__ float s_ch[kLossWarps][kMaxAtoms];
   pdl::entry();
-  const int tid = threadIdx.x;
-  const int b = blockIdx.x * kThreads + tid;
-  if (b == 0) *a.step += 1;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int warp = blockIdx.x * kLossWarps + wib;
+  const int n_warps = gridDim.x * kLossWarps;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.step += 1;
   const int L = a.L;
-  for (int j = 0; j < kMaxAtoms; ++j) {
-    q1[j * kSmemStride + tid] = 0.0f;
-    q2[j * kSmemStride + tid] = 0.0f;
-  }
+  const float Bf = static_cast<float>(a.Bg);
+  int* lo_s = s_lo[wib];
+  float* cl_s = s_cl[wib];
+  float* ch_s = s_ch[wib];
+  float db[2][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}};  // [critic][atom lane / lane+32]
   double l = 0.0;
-  if (b < a.B) {
-    // target distribution: the head with the lower expected value (c51.hpp:123-124)
-    const int pick = a.evt[0][b] <= a.evt[1][b] ? 0 : 1;
+  for (int b = warp; b < a.B; b += n_warps) {
+    const int pick = a.evt[0][b] <= a.evt[1][b] ? 0 : 1;  // c51.hpp:123-124
     const float* p = a.pt[pick] + static_cast<int64_t>(b) * a.ld;
-    double mass = 0.0;
-    for (int j = 0; j < L; ++j) mass = __dadd_rn(mass, static_cast<double>(p[j]));
-    if (fabs(mass - 1.0) > 1e-5) atomicOr(a.status, 8u);
     const double g = a.ret[b], e = a.eff[b];
-    for (int j = 0; j < L; ++j) {
-      double tz = __dadd_rn(g, __dmul_rn(e, static_cast<double>(a.atoms[j])));
-      if (tz < a.vmin) tz = a.vmin;
-      if (tz > a.vmax) tz = a.vmax;
-      double pos = __ddiv_rn(__dsub_rn(tz, a.vmin), a.dz);
-      const double snapped = rint(pos);  // std::nearbyint, round-to-nearest-even
-      if (fabs(__dsub_rn(pos, snapped)) < 1e-5) pos = snapped;
-      const int lo = static_cast<int>(pos);
-      const double frac = __dsub_rn(pos, static_cast<double>(lo));
-      const float pj = p[j];
-      float* ql = q1 + lo * kSmemStride + tid;
-      if (frac == 0.0) {
-        *ql = __fadd_rn(*ql, pj);
-      } else {
-        *ql = __fadd_rn(*ql, static_cast<float>(__dmul_rn(pj, __dsub_rn(1.0, frac))));
-        ql[kSmemStride] = __fadd_rn(ql[kSmemStride], static_cast<float>(__dmul_rn(pj, frac)));
+    double mass = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = lane + 32 * h;
+      float cl = 0.0f, ch = 0.0f;
+      int lo = 1 << 20;  // beyond every target (j >= L)
+      if (j < L) {
+        const float pj = p[j];
+        mass += static_cast<double>(pj);
+        double tz = __dadd_rn(g, __dmul_rn(e, static_cast<double>(a.atoms[j])));
+        if (tz < a.vmin) tz = a.vmin;
+        if (tz > a.vmax) tz = a.vmax;
+        double pos = __ddiv_rn(__dsub_rn(tz, a.vmin), a.dz);
+        const double snapped = rint(pos);  // std::nearbyint (round-half-even)
+        if (fabs(__dsub_rn(pos, snapped)) < 1e-5) pos = snapped;
+        lo = static_cast<int>(pos);
+        const double frac = __dsub_rn(pos, static_cast<double>(lo));
+        if (frac == 0.0) {
+          cl = pj;  // whole mass to lo, nothing to lo + 1
+        } else {
+          cl = static_cast<float>(__dmul_rn(pj, __dsub_rn(1.0, frac)));
+          ch = static_cast<float>(__dmul_rn(pj, frac));
+        }
       }
+      lo_s[j] = lo;
+      cl_s[j] = cl;
+      ch_s[j] = ch;
     }
-    // cross-entropy of both online heads against the projection (c51.hpp:138-150)
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mass += __shfl_xor_sync(0xffffffffu, mass, o);
+    if (lane == 0 && fabs(mass - 1.0) > 1e-5) atomicOr(a.status, 8u);
+    __syncwarp();
     const float* s1 = a.po[0] + static_cast<int64_t>(b) * a.ld;
     const float* s2 = a.po[1] + static_cast<int64_t>(b) * a.ld;
     float* u1 = a.up + static_cast<int64_t>(b) * a.ld;
     float* u2 = u1 + static_cast<int64_t>(a.B) * a.ld;
-    const float Bf = static_cast<float>(a.Bg);
     float lr = 0.0f;
-    for (int j = 0; j < L; ++j) {
-      const float pj = q1[j * kSmemStride + tid];
-      const float x1 = s1[j], x2 = s2[j];
-      if (pj > 0.0f) {
-        lr = __fsub_rn(lr, __fmul_rn(pj, logf(x1 > 1e-30f ? x1 : 1e-30f)));
-        lr = __fsub_rn(lr, __fmul_rn(pj, logf(x2 > 1e-30f ? x2 : 1e-30f)));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = lane + 32 * h;
+      if (i < L) {
+        // first source with lo >= i - 1, then fold while lo <= i
+        int lo_idx = 0, hi_idx = L;
+        while (lo_idx < hi_idx) {
+          const int mid = (lo_idx + hi_idx) >> 1;
+          if (lo_s[mid] < i - 1) lo_idx = mid + 1;
+          else hi_idx = mid;
+        }
+        float q = 0.0f;
+        for (int j = lo_idx; j < L; ++j) {
+          const int lj = lo_s[j];
+          if (lj > i) break;
+          q = __fadd_rn(q, lj == i ? cl_s[j] : ch_s[j]);  // lj == i-1: the split remainder
+        }
+        // cross-entropy of both online heads (c51.hpp:138-150)
+        const float x1 = s1[i], x2 = s2[i];
+        if (q > 0.0f) {
+          lr = __fsub_rn(lr, __fmul_rn(q, logf(x1 > 1e-30f ? x1 : 1e-30f)));
+          lr = __fsub_rn(lr, __fmul_rn(q, logf(x2 > 1e-30f ? x2 : 1e-30f)));
+        }
+        const float g1 = __fdiv_rn(__fsub_rn(x1, q), Bf);
+        const float g2 = __fdiv_rn(__fsub_rn(x2, q), Bf);
+        u1[i] = g1;
+        u2[i] = g2;
+        db[0][h] = __fadd_rn(db[0][h], g1);
+        db[1][h] = __fadd_rn(db[1][h], g2);
       }
-      const float g1 = __fdiv_rn(__fsub_rn(x1, pj), Bf);
-      const float g2 = __fdiv_rn(__fsub_rn(x2, pj), Bf);
-      u1[j] = g1;
-      u2[j] = g2;
-      q1[j * kSmemStride + tid] = g1;
-      q2[j * kSmemStride + tid] = g2;
     }
-    l = static_cast<double>(lr);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) lr += __shfl_xor_sync(0xffffffffu, lr, o);
+    if (lane == 0) l += static_cast<double>(lr);
+    __syncwarp();
   }
-  __syncthreads();
-  // head bias gradient partials: column sums of the block's upstream rows
-  for (int c = tid; c < 2 * L; c += kThreads) {
-    const int k = c / L, j = c % L;
-    const float* col = (k ? q2 : q1) + j * kSmemStride;
-    float s = 0.0f;
-    for (int r = 0; r < kThreads; ++r) s = __fadd_rn(s, col[r]);
-    a.db_part[(static_cast<int64_t>(k) * gridDim.x + blockIdx.x) * L + j] = s;
-  }
-  critic::block_mean_finish<kThreads>(l, a.block_loss, a.counter, a.Bg, a.loss_out, a.status,
-                                      4u);
+  // head bias gradient partials: this warp's column sums (rows in its order)
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = lane + 32 * h;
+      if (i < L) a.db_part[(static_cast<int64_t>(k) * n_warps + warp) * L + i] = db[k][h];
+    }
+  critic::block_mean_finish<kLossWarps * 32>(l, a.block_loss, a.counter, a.Bg, a.loss_out,
+                                             a.status, 4u);
 }
 
 struct ActorPickArgs {

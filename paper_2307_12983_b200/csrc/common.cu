@@ -5,7 +5,10 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
+#include <string>
+#include <vector>
 
 namespace pqlg {
 
@@ -104,3 +107,93 @@ const char* pqlg_last_error(void) { return pqlg::g_last_error.c_str(); }
 int pqlg_abi_version(void) { return 1; }
 uint64_t pqlg_launch_count(void) { return pqlg::g_launches.load(); }
 }
+
+// ------------------------------------------------------------ launch profiler
+namespace pqlg {
+
+namespace {
+struct ProfRec {
+  cudaEvent_t a, b;
+  const void* fn;
+};
+std::atomic<bool> g_prof{false};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof_recs;
+thread_local bool g_prof_skip = false;
+
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  return cs != cudaStreamCaptureStatusNone;
+}
+}  // namespace
+
+bool profiling_active() { return g_prof.load(std::memory_order_relaxed); }
+
+void profile_before(cudaStream_t st, const void* fn) {
+  g_prof_skip = capturing(st);
+  if (g_prof_skip) return;
+  ProfRec r{};
+  r.fn = fn;
+  PQLG_CUDA(cudaEventCreate(&r.a));
+  PQLG_CUDA(cudaEventCreate(&r.b));
+  PQLG_CUDA(cudaEventRecord(r.a, st));
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_recs.push_back(r);
+}
+
+void profile_after(cudaStream_t st) {
+  if (g_prof_skip) return;
+  cudaEvent_t b;
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    b = g_prof_recs.back().b;
+  }
+  PQLG_CUDA(cudaEventRecord(b, st));
+}
+}  // namespace pqlg
+
+extern "C" {
+
+PQLG_API int pqlg_profile_begin(void) {
+  return pqlg::guarded([] {
+    std::lock_guard<std::mutex> lk(pqlg::g_prof_mu);
+    for (auto& r : pqlg::g_prof_recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    pqlg::g_prof_recs.clear();
+    pqlg::g_prof = true;
+  });
+}
+
+// Writes "kernel-name\tmilliseconds\n" per profiled launch into out (NUL-
+// terminated, truncated to cap bytes) and stops profiling.  Synchronizes.
+PQLG_API int pqlg_profile_end(char* out, int cap) {
+  return pqlg::guarded([&] {
+    pqlg::g_prof = false;
+    PQLG_CUDA(cudaDeviceSynchronize());
+    std::string s;
+    std::lock_guard<std::mutex> lk(pqlg::g_prof_mu);
+    for (auto& r : pqlg::g_prof_recs) {
+      float ms = 0.0f;
+      PQLG_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      const char* name = nullptr;
+      if (cudaFuncGetName(&name, r.fn) != cudaSuccess || !name) name = "?";
+      s += name;
+      s += '\t';
+      s += std::to_string(ms);
+      s += '\n';
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    pqlg::g_prof_recs.clear();
+    if (out && cap > 0) {
+      const size_t n = std::min(static_cast<size_t>(cap - 1), s.size());
+      std::memcpy(out, s.data(), n);
+      out[n] = 0;
+    }
+  });
+}
+
+}  // extern "C"

@@ -46,9 +46,17 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
 // stream-serialisation attribute (PDL, see pdl.cuh) unless PQLG_PDL=0.
 bool pdl_enabled();
 
+// Per-launch device timing (pqlg_profile_begin/end): when active, launch()
+// brackets every kernel issued outside stream capture with a pair of events.
+bool profiling_active();
+void profile_before(cudaStream_t st, const void* fn);
+void profile_after(cudaStream_t st);
+
 template <class... KArgs, class... Args>
 void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
             Args&&... args) {
+  const bool prof = profiling_active();
+  if (prof) profile_before(st, reinterpret_cast<const void*>(kernel));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -61,6 +69,7 @@ void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaSt
   cfg.numAttrs = 1;
   PQLG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
   count_launch();
+  if (prof) profile_after(st);
 }
 
 // Wraps an ABI entry point: converts exceptions to status codes.

@@ -21,57 +21,75 @@
 
 namespace pqlg::epi {
 
+// Where an epilogue thread is: its tile, its row, and how the tile's columns
+// are shared between the epilogue warps (halves == 2: two warps per row,
+// warp `half` takes columns [half*BN/2, (half+1)*BN/2)).
+struct Ctx {
+  int group, split, m_tile, n_tile;
+  int m;     // this thread's row
+  int row0;  // first row of the warp's 32-row slab
+  int et;    // epilogue thread index in [0, ne)
+  int ne;    // epilogue threads
+  int half, halves;
+};
+
 // relu(acc + b) -> TMA store (store = 1) and/or a ReLU bitmask (bit t of
 // word n/32 = post[m, n] > 0) used by the backward; optional head dot
 // sum_n relu(.)*w_head[n] per n-tile -> partial[(group*n_tiles + n_tile)*ld_part + m].
 struct Hidden {
   static constexpr int kStoreRank = 2;
+  static constexpr bool kSplitCols = true;
   const float* bias[2];
   const float* w_head[2];  // null: no head dot
   uint32_t* mask[2];       // null: no bitmask
   int ld_mask;             // words per row (= N/32)
-  float* partial;
+  float* partial;          // [group][slot][ld_part], slot = n_tile * halves + half
   int64_t ld_part;
-  int n_tiles;
+  int n_slots;             // n_tiles * halves (mlp::hidden_slots)
   int bn;
   int M, N;
   int store;  // 0: skip storing the activation (target critics' last layer)
   struct Row {
     float dot;
   };
-  __device__ void prepare(Row& r, int group, int, int, int n_tile, float* scratch) const {
+  __device__ void prepare(Row& r, const Ctx& c, float* scratch) const {
     r.dot = 0.0f;
-    const int t = threadIdx.x - 64;  // epilogue threads 0..127
-    const float* b = bias[group];
-    const float* wh = w_head[group];
-    for (int i = t; i < bn; i += 128) {
-      const int n = n_tile * bn + i;
+    const float* b = bias[c.group];
+    const float* wh = w_head[c.group];
+    for (int i = c.et; i < bn; i += c.ne) {
+      const int n = c.n_tile * bn + i;
       scratch[i] = n < N ? b[n] : 0.0f;
       if (wh) scratch[bn + i] = n < N ? wh[n] : 0.0f;
     }
-    ptx::named_bar_sync(1, 128);
   }
-  __device__ bool chunk(Row& r, int group, int, int m, int n0, float (&v)[32],
-                        const float* scratch) const {
+  __device__ bool chunk(Row& r, const Ctx& c, int n0, float (&v)[32], float* scratch) const {
     const int c0 = n0 % bn;
     uint32_t bits = 0;
 #pragma unroll
-    for (int t = 0; t < 32; ++t) {
-      const float y = __fadd_rn(v[t], scratch[c0 + t]);
-      const float x = y > 0.0f ? y : 0.0f;
-      v[t] = x;
-      bits |= (x > 0.0f ? 1u : 0u) << t;
+    for (int t = 0; t < 32; t += 4) {
+      const float4 b4 = *reinterpret_cast<const float4*>(scratch + c0 + t);
+      const float bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float y = __fadd_rn(v[t + u], bb[u]);
+        const float x = y > 0.0f ? y : 0.0f;
+        v[t + u] = x;
+        bits |= (x > 0.0f ? 1u : 0u) << (t + u);
+      }
     }
-    if (w_head[group]) {
+    if (w_head[c.group]) {
 #pragma unroll
       for (int t = 0; t < 32; ++t) r.dot = __fadd_rn(r.dot, __fmul_rn(v[t], scratch[bn + c0 + t]));
     }
-    if (mask[group] && m < M) mask[group][static_cast<int64_t>(m) * ld_mask + (n0 >> 5)] = bits;
+    if (mask[c.group] && c.m < M)
+      mask[c.group][static_cast<int64_t>(c.m) * ld_mask + (n0 >> 5)] = bits;
     return store != 0;
   }
-  __device__ void end(Row& r, int group, int, int m, int n_tile) const {
-    if (m < M && w_head[group])
-      partial[(static_cast<int64_t>(group) * n_tiles + n_tile) * ld_part + m] = r.dot;
+  __device__ void end(Row& r, const Ctx& c) const {
+    if (c.m < M && w_head[c.group]) {
+      const int slot = c.n_tile * c.halves + c.half;
+      partial[(static_cast<int64_t>(c.group) * n_slots + slot) * ld_part + c.m] = r.dot;
+    }
   }
 };
 
@@ -83,6 +101,7 @@ struct Hidden {
 // (stream position, cached polar value) persists across 32-column chunks.
 struct PolicyHead {
   static constexpr int kStoreRank = 0;
+  static constexpr bool kSplitCols = false;
   const float* bias;
   float* act;
   int64_t ld_act;
@@ -101,9 +120,9 @@ struct PolicyHead {
     float z[32];
     float sig;
   };
-  __device__ void prepare(Row& r, int, int, int m, int, float* scratch) const {
-    const int t = threadIdx.x - 64;
-    for (int i = t; i < A; i += 128) scratch[i] = bias[i];
+  __device__ void prepare(Row& r, const Ctx& c, float* scratch) const {
+    const int m = c.m;
+    for (int i = c.et; i < A; i += c.ne) scratch[i] = bias[i];
     r.sig = 0.0f;
     if (noise_state && m < M) {
       r.sig = sigma[m];
@@ -120,10 +139,9 @@ struct PolicyHead {
         noise_state[m] = st;
       }
     }
-    ptx::named_bar_sync(1, 128);
   }
-  __device__ bool chunk(Row& r, int, int, int m, int n0, float (&v)[32],
-                        const float* scratch) const {
+  __device__ bool chunk(Row& r, const Ctx& c, int n0, float (&v)[32], float* scratch) const {
+    const int m = c.m;
     if (m >= M) return false;
     float* out = act + static_cast<int64_t>(m) * ld_act;
 #pragma unroll
@@ -144,7 +162,7 @@ struct PolicyHead {
     }
     return false;
   }
-  __device__ void end(Row&, int, int, int, int) const {}
+  __device__ void end(Row&, const Ctx&) const {}
 };
 
 // dgrad output with the ReLU mask of the layer below (from its bitmask),
@@ -152,6 +170,7 @@ struct PolicyHead {
 // gradient of that layer) written to colsum[(group*m_tiles + m_tile)*ld_cs + n].
 struct DgradMask {
   static constexpr int kStoreRank = 2;
+  static constexpr bool kSplitCols = true;
   const uint32_t* mask[2];  // nullable: no mask
   int ld_mask;
   float* colsum;  // nullable
@@ -162,24 +181,23 @@ struct DgradMask {
   struct Row {
     uint32_t bits[8];  // mask words of this row for the n-tile (bn <= 256)
   };
-  __device__ void prepare(Row& r, int group, int, int m, int n_tile, float*) const {
+  __device__ void prepare(Row& r, const Ctx& c, float*) const {
 #pragma unroll
     for (int i = 0; i < 8; ++i) r.bits[i] = 0xffffffffu;
-    if (mask[group] && m < M) {
-      const uint32_t* p = mask[group] + static_cast<int64_t>(m) * ld_mask + n_tile * (bn >> 5);
+    if (mask[c.group] && c.m < M) {
+      const uint32_t* p = mask[c.group] + static_cast<int64_t>(c.m) * ld_mask + c.n_tile * (bn >> 5);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         if (i < (bn >> 5)) r.bits[i] = p[i];
     }
   }
-  __device__ bool chunk(Row& r, int group, int, int m, int n0, float (&v)[32],
-                        float* scratch) const {
-    const int c = (n0 % bn) >> 5;
+  __device__ bool chunk(Row& r, const Ctx& c, int n0, float (&v)[32], float* scratch) const {
+    const int ci = (n0 % bn) >> 5;
     uint32_t bits = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-      if (i == c) bits = r.bits[i];
-    const bool row_ok = m < M;
+      if (i == ci) bits = r.bits[i];
+    const bool row_ok = c.m < M;
 #pragma unroll
     for (int t = 0; t < 32; ++t) {
       const bool keep = row_ok && (n0 + t < N) && ((bits >> t) & 1u);
@@ -187,7 +205,8 @@ struct DgradMask {
     }
     if (colsum) {
       // Column sums over the 32 rows of this warp: recursive halving leaves
-      // lane l with the sum of column l (fixed order -> deterministic).
+      // lane l with the sum of column l (fixed order -> deterministic); then
+      // the 4 warps of this column half add their slabs in quadrant order.
       float g[32];
 #pragma unroll
       for (int t = 0; t < 32; ++t) g[t] = v[t];
@@ -204,50 +223,48 @@ struct DgradMask {
         }
       }
       const int q = (threadIdx.x >> 5) & 3;
-      scratch[q * 32 + lane] = g[0];
-      ptx::named_bar_sync(2, 128);
+      float* sc = scratch + c.half * 128;  // (DgradMask keeps no constants in scratch)
+      sc[q * 32 + lane] = g[0];
+      ptx::named_bar_sync(2 + c.half, 128);
       if (q == 0 && n0 + lane < N) {
-        const float s = __fadd_rn(__fadd_rn(scratch[lane], scratch[32 + lane]),
-                                  __fadd_rn(scratch[64 + lane], scratch[96 + lane]));
-        const int m_tile = (m - lane) / 128;
-        colsum[(static_cast<int64_t>(group) * m_tiles + m_tile) * ld_cs + n0 + lane] = s;
+        const float s = __fadd_rn(__fadd_rn(sc[lane], sc[32 + lane]),
+                                  __fadd_rn(sc[64 + lane], sc[96 + lane]));
+        colsum[(static_cast<int64_t>(c.group) * m_tiles + c.m_tile) * ld_cs + n0 + lane] = s;
       }
-      ptx::named_bar_sync(2, 128);
+      ptx::named_bar_sync(2 + c.half, 128);
     }
     return true;
   }
-  __device__ void end(Row&, int, int, int, int) const {}
+  __device__ void end(Row&, const Ctx&) const {}
 };
 
 // Split-K partial tiles, TMA-stored through a 3-D map
 // {N, M, groups*splits}: W[((group*splits + split)*M + m)*N + n].
 struct Partial {
   static constexpr int kStoreRank = 3;
+  static constexpr bool kSplitCols = true;
   struct Row {};
-  __device__ void prepare(Row&, int, int, int, int, float*) const {}
-  __device__ bool chunk(Row&, int, int, int, int, float (&)[32], const float*) const {
-    return true;
-  }
-  __device__ void end(Row&, int, int, int, int) const {}
+  __device__ void prepare(Row&, const Ctx&, float*) const {}
+  __device__ bool chunk(Row&, const Ctx&, int, float (&)[32], float*) const { return true; }
+  __device__ void end(Row&, const Ctx&) const {}
 };
 
 // out = acc (+ bias) (ReLU optional), TMA-stored: the plain affine layer.
 struct Linear {
   static constexpr int kStoreRank = 2;
+  static constexpr bool kSplitCols = true;
   const float* bias;  // nullable
   int relu;
   int bn;
   int N;
   struct Row {};
-  __device__ void prepare(Row&, int, int, int, int n_tile, float* scratch) const {
-    const int t = threadIdx.x - 64;
-    for (int i = t; i < bn; i += 128) {
-      const int n = n_tile * bn + i;
+  __device__ void prepare(Row&, const Ctx& c, float* scratch) const {
+    for (int i = c.et; i < bn; i += c.ne) {
+      const int n = c.n_tile * bn + i;
       scratch[i] = (bias && n < N) ? bias[n] : 0.0f;
     }
-    ptx::named_bar_sync(1, 128);
   }
-  __device__ bool chunk(Row&, int, int, int, int n0, float (&v)[32], const float* scratch) const {
+  __device__ bool chunk(Row&, const Ctx&, int n0, float (&v)[32], float* scratch) const {
     const int c0 = n0 % bn;
 #pragma unroll
     for (int t = 0; t < 32; ++t) {
@@ -257,27 +274,28 @@ struct Linear {
     }
     return true;
   }
-  __device__ void end(Row&, int, int, int, int) const {}
+  __device__ void end(Row&, const Ctx&) const {}
 };
 
 // Raw store of the accumulator (narrow outputs, e.g. the action columns of
 // the critic input gradient).
 struct Store {
   static constexpr int kStoreRank = 0;
+  static constexpr bool kSplitCols = false;
   float* out[2];
   int64_t ld_out;
   int M, N;
   struct Row {};
-  __device__ void prepare(Row&, int, int, int, int, float*) const {}
-  __device__ bool chunk(Row&, int group, int, int m, int n0, float (&v)[32], const float*) const {
-    if (m >= M) return false;
-    float* o = out[group] + static_cast<int64_t>(m) * ld_out;
+  __device__ void prepare(Row&, const Ctx&, float*) const {}
+  __device__ bool chunk(Row&, const Ctx& c, int n0, float (&v)[32], float*) const {
+    if (c.m >= M) return false;
+    float* o = out[c.group] + static_cast<int64_t>(c.m) * ld_out;
 #pragma unroll
     for (int t = 0; t < 32; ++t)
       if (n0 + t < N) o[n0 + t] = v[t];
     return false;
   }
-  __device__ void end(Row&, int, int, int, int) const {}
+  __device__ void end(Row&, const Ctx&) const {}
 };
 
 }  // namespace pqlg::epi
@@ -291,6 +309,7 @@ namespace pqlg::epi {
 // Writes probs[m*ld + j] and, if ev is set, ev[m].
 struct C51Head {
   static constexpr int kStoreRank = 0;
+  static constexpr bool kSplitCols = false;
   static constexpr int kMaxAtoms = 64;
   const float* bias[2];
   float* probs[2];
@@ -301,15 +320,13 @@ struct C51Head {
   struct Row {
     float x[kMaxAtoms];
   };
-  __device__ void prepare(Row&, int group, int, int, int, float* scratch) const {
-    const int t = threadIdx.x - 64;
-    for (int i = t; i < kMaxAtoms; i += 128) {
-      scratch[i] = i < L ? bias[group][i] : 0.0f;
+  __device__ void prepare(Row&, const Ctx& c, float* scratch) const {
+    for (int i = c.et; i < kMaxAtoms; i += c.ne) {
+      scratch[i] = i < L ? bias[c.group][i] : 0.0f;
       scratch[kMaxAtoms + i] = i < L ? atoms[i] : 0.0f;
     }
-    ptx::named_bar_sync(1, 128);
   }
-  __device__ bool chunk(Row& r, int, int, int, int n0, float (&v)[32], const float* scratch) const {
+  __device__ bool chunk(Row& r, const Ctx&, int n0, float (&v)[32], float* scratch) const {
     if (n0 == 0) {
 #pragma unroll
       for (int t = 0; t < 32; ++t) r.x[t] = __fadd_rn(v[t], scratch[t]);
@@ -319,7 +336,8 @@ struct C51Head {
     }
     return false;
   }
-  __device__ void end(Row& r, int group, int, int m, int) const {
+  __device__ void end(Row& r, const Ctx& c) const {
+    const int m = c.m, group = c.group;
     if (m >= M) return;
     float mx = r.x[0];
 #pragma unroll

@@ -22,6 +22,7 @@ inline CUtensorMap map_b(const float* B, int N, int K, int ldb, bool mn, int BN,
 }
 
 inline Problem make_problem(int M, int N, int K, int splits) {
+  require(M > 0 && N > 0 && K > 0, "gemm: empty problem");
   Problem p{};
   p.M = M;
   p.N = N;
@@ -30,27 +31,36 @@ inline Problem make_problem(int M, int N, int K, int splits) {
   if (splits < 1) splits = 1;
   if (splits > p.k_tiles) splits = p.k_tiles;
   p.k_tiles_per_split = (p.k_tiles + splits - 1) / splits;
-  p.splits = (p.k_tiles + p.k_tiles_per_split - 1) / p.k_tiles_per_split;
+  p.splits = (p.k_tiles + p.k_tiles_per_split - 1) / p.k_tiles_per_split;  // none empty
+  p.groups = 1;
   return p;
 }
 
-template <int BN>
-constexpr int default_stages() {
-  return BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
+inline int sm_count() {
+  static int n = [] {
+    int dev = 0, c = 0;
+    PQLG_CUDA(cudaGetDevice(&dev));
+    PQLG_CUDA(cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev));
+    return c;
+  }();
+  return n;
 }
 
-template <int BN, bool kAMN, bool kBMN, class Epi, int kStages = default_stages<BN>()>
-void launch(const Operands& ops, const Problem& p, int groups, const Epi& epi, cudaStream_t st) {
-  using L = SmemLayout<BN, kStages>;
-  auto kern = gemm_tf32_kernel<BN, kStages, kAMN, kBMN, Epi>;
+// Persistent launch: min(tiles, SMs) CTAs, one per SM, walking the tiles.
+template <int BN, bool kAMN, bool kBMN, class Epi>
+void launch(const Operands& ops, Problem p, int groups, const Epi& epi, cudaStream_t st) {
+  using L = SmemLayout<BN, Epi>;
+  auto kern = gemm_tf32_kernel<BN, kAMN, kBMN, Epi>;
   static bool configured = false;
   if (!configured) {
     PQLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    L::kDynamic));
     configured = true;
   }
-  dim3 grid((p.M + kBM - 1) / kBM, (p.N + BN - 1) / BN, p.splits * groups);
-  ::pqlg::launch(kern, grid, dim3(kThreads), L::kDynamic, st, ops, p, epi);
+  p.groups = groups;
+  const int tiles = ((p.M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN) * p.splits * groups;
+  const int grid = tiles < sm_count() ? tiles : sm_count();
+  ::pqlg::launch(kern, dim3(grid), dim3(L::kThreads), L::kDynamic, st, ops, p, epi);
 }
 
 }  // namespace pqlg::gemm

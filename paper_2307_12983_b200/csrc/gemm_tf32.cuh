@@ -14,29 +14,58 @@
 // Operand tensor maps are typed TFLOAT32 so TMA rounds fp32 -> tf32 to
 // nearest on the way into shared memory (the MMA alone would truncate).
 //
-// Structure (one 128 x BN output tile per CTA, 192 threads):
-//   warp 0      TMA producer   (one elected lane, kStages-deep smem ring)
-//   warp 1      TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..5  epilogue: Epi::prepare() preloads per-tile constants while the
-//               mainloop runs; then tcgen05.ld 32 columns at a time ->
-//               Epi::chunk() -> 128B-swizzled staging in the (now idle)
-//               pipeline smem -> TMA bulk tensor store (coalesced, async).
-// Split-K over blockIdx.z lets the K=8192 weight-gradient GEMMs fill 148 SMs;
-// their epilogue stores partial tiles that a fixed-order reduction sums.
+// Structure: a persistent kernel (grid = min(tiles, SMs), one CTA per SM)
+// walking 128 x BN output tiles round-robin:
+//   warp 0      TMA producer   (one elected lane, kStages-deep smem ring that
+//               runs on across tile boundaries)
+//   warp 1      TMEM allocator + MMA issuer (one elected lane); the
+//               accumulator is double-buffered in TMEM (2 x BN columns), so
+//               tile i+1's mainloop runs while the epilogue drains tile i
+//   warps 2..   epilogue (4 warps, or 8 when the tile is >= 128 columns wide:
+//               two warps per TMEM lane quadrant, one per column half):
+//               Epi::prepare() loads per-tile constants, then tcgen05.ld 32
+//               columns at a time -> Epi::chunk() -> 128B-swizzled staging
+//               (two 4 KB buffers per warp) -> TMA bulk tensor store.
+// Split-K over the z tile coordinate lets the K=8192 weight-gradient GEMMs
+// fill 148 SMs; their epilogue stores partial tiles that a fixed-order
+// reduction sums.
 #pragma once
 
 #include <cstdint>
 
+#include "epilogues.cuh"
 #include "pdl.cuh"
 #include "ptx.cuh"
 
 namespace pqlg::gemm {
 
+// Phase timestamps per CTA (tools/gemm_trace.cu builds a traced copy of the
+// kernel with -DPQLG_GEMM_TRACE; the library itself never defines it).
+#ifdef PQLG_GEMM_TRACE
+__device__ unsigned long long* g_trace;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PQLG_TRACE(slot, value)                                                       \
+  do {                                                                                \
+    if (g_trace) {                                                                    \
+      const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
+      g_trace[bid * 8 + (slot)] = (value);                                            \
+    }                                                                                 \
+  } while (0)
+#else
+#define PQLG_TRACE(slot, value) \
+  do {                          \
+  } while (0)
+#endif
+
 constexpr int kBM = 128;       // UMMA M (cta_group::1)
 constexpr int kBK = 32;        // fp32 elements per 128-byte swizzle row
 constexpr int kUmmaK = 8;      // K per tcgen05.mma.kind::tf32
-constexpr int kThreads = 192;  // 6 warps
-constexpr int kScratchBytes = 4096;  // per-tile epilogue constants
+constexpr int kScratchBytes = 2048;  // per-tile epilogue constants
+constexpr int kMaxDynSmem = 232448;  // 227 KB per CTA on sm_100
 
 struct Operands {
   CUtensorMap a[2];  // one per group (twin critics share a launch)
@@ -49,22 +78,40 @@ struct Problem {
   int k_tiles;          // ceil(K / kBK)
   int k_tiles_per_split;
   int splits;
+  int groups;
 };
 
-template <int BN, int kStages>
+// Epilogue warp count: two warps per TMEM lane quadrant (column halves) for
+// tiles >= 128 columns whose epilogue supports it.
+template <int BN, class Epi>
+constexpr int epi_warps() {
+  return (BN >= 128 && Epi::kSplitCols) ? 8 : 4;
+}
+
+template <int BN, class Epi>
 struct SmemLayout {
-  static constexpr int kABytes = kBM * kBK * 4;        // 16 KB
+  static constexpr int kEpiWarps = epi_warps<BN, Epi>();
+  static constexpr int kThreads = 64 + 32 * kEpiWarps;
+  static constexpr int kABytes = kBM * kBK * 4;  // 16 KB
   static constexpr int kBBytes = BN * kBK * 4;
   static constexpr int kStageBytes = kABytes + kBBytes;
+  // one 4 KB (32 x 32 fp32, 128B-swizzled) TMA-store staging buffer per warp
+  static constexpr int kStagingBytes = Epi::kStoreRank > 0 ? kEpiWarps * 4096 : 0;
+  static constexpr int kFixed = kStagingBytes + kScratchBytes + 256;
+  static constexpr int kFit = (kMaxDynSmem - kFixed) / kStageBytes;
+  static constexpr int kStages = kFit > 8 ? 8 : kFit;
+  static_assert(kStages >= 4, "pipeline too shallow");
   static constexpr int kPipeBytes = kStages * kStageBytes;
-  // epilogue staging reuses the pipeline ring: 4 warps x (BN/32) x 4 KB
-  static constexpr int kStageOutBytes = 4 * (BN / 32) * 4096;
-  static_assert(kStageOutBytes <= kPipeBytes, "staging must fit in the pipeline smem");
-  static constexpr int kScratchOffset = kPipeBytes;
+  static constexpr int kStagingOffset = kPipeBytes;
+  static constexpr int kScratchOffset = kStagingOffset + kStagingBytes;
   static constexpr int kBarOffset = kScratchOffset + kScratchBytes;
-  // full[kStages], empty[kStages], tmem_full, tmem pointer
-  static constexpr int kTotal = kBarOffset + (2 * kStages + 1) * 8 + 16;
-  static constexpr int kDynamic = kTotal + 1024;  // slack for 1024B alignment
+  // full[kStages], empty[kStages], tmem_full[2], tmem_empty[2], tmem pointer
+  static constexpr int kTotal = kBarOffset + (2 * kStages + 4) * 8 + 16;
+  // the dynamic window starts 1024B-aligned (no static smem in this kernel;
+  // checked at entry), so no alignment slack is reserved
+  static constexpr int kDynamic = kTotal;
+  static_assert(kDynamic <= kMaxDynSmem, "shared memory budget");
+  static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
 };
 
 // UMMA shared-memory descriptor (sm_100 "version 1" format).
@@ -131,171 +178,263 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
       : "memory");
 }
 
-// Epi concept:
+// Epi concept (see epilogues.cuh, epi::Ctx):
 //   static constexpr int kStoreRank;   // 0: Epi stores itself; 2/3: TMA store of v
+//   static constexpr bool kSplitCols;  // two warps may share a row (column halves)
 //   struct Row;                        // per-thread row state
-//   __device__ void prepare(Row&, int group, int split, int m, int n_tile, float* scratch) const;
-//       called by all 128 epilogue threads before the accumulator is ready;
-//       must end with ptx::named_bar_sync(1, 128) if it writes `scratch`.
-//   __device__ bool chunk(Row&, int group, int split, int m, int n0, float (&v)[32],
-//                         const float* scratch) const;  // transforms v; true = store v
-//   __device__ void end(Row&, int group, int split, int m, int n_tile) const;
+//   __device__ void prepare(Row&, const epi::Ctx&, float* scratch) const;
+//       per tile, all epilogue threads, before the accumulator is ready; the
+//       kernel synchronises the epilogue threads before and after it
+//   __device__ bool chunk(Row&, const epi::Ctx&, int n0, float (&v)[32], float* scratch) const;
+//       transforms v (columns n0..n0+31 of the row); true = TMA-store v
+//   __device__ void end(Row&, const epi::Ctx&) const;
 // `m` may be >= M (rows beyond the problem are zero-filled by TMA; TMA stores
 // clip them); the epilogue masks its own direct stores.
-template <int BN, int kStages, bool kAMN, bool kBMN, class Epi>
-__global__ void __launch_bounds__(kThreads, 1)
+struct TileCoord {
+  int m_tile, n_tile, split, group;
+};
+
+__device__ __forceinline__ TileCoord tile_coord(int t, const Problem& p, int tiles_m,
+                                                int tiles_n) {
+  TileCoord c;
+  c.m_tile = t % tiles_m;
+  const int r = t / tiles_m;
+  c.n_tile = r % tiles_n;
+  const int z = r / tiles_n;
+  c.split = z % p.splits;
+  c.group = z / p.splits;
+  return c;
+}
+
+template <int BN, bool kAMN, bool kBMN, class Epi>
+__global__ void __launch_bounds__(SmemLayout<BN, Epi>::kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ Operands ops, const Problem prob, const Epi epi) {
-  using L = SmemLayout<BN, kStages>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  using L = SmemLayout<BN, Epi>;
+  constexpr int kStages = L::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((ptx::smem_u32(smem) & 1023) != 0) __trap();  // SW128 tiles need 1024B alignment
   float* scratch = reinterpret_cast<float*>(smem + L::kScratchOffset);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
   uint64_t* empty = full + kStages;
-  uint64_t* tmem_full = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + kStages;   // [2]
+  uint64_t* tmem_empty = tmem_full + 2;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5;
-  const int m_tile = blockIdx.x;
-  const int n_tile = blockIdx.y;
-  const int split = blockIdx.z % prob.splits;
-  const int group = blockIdx.z / prob.splits;
-  const int kt_begin = split * prob.k_tiles_per_split;
-  int kt_end = kt_begin + prob.k_tiles_per_split;
-  if (kt_end > prob.k_tiles) kt_end = prob.k_tiles;
-  const int n_kt = kt_end > kt_begin ? kt_end - kt_begin : 0;
-
-  constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+  const int tiles_m = (prob.M + kBM - 1) / kBM;
+  const int tiles_n = (prob.N + BN - 1) / BN;
+  const int n_tiles_total = tiles_m * tiles_n * prob.splits * prob.groups;
 
   if (warp == 0 && ptx::elect_one()) {
-    ptx::tma_prefetch(&ops.a[group]);
-    ptx::tma_prefetch(&ops.b[group]);
+    for (int g = 0; g < prob.groups; ++g) {
+      ptx::tma_prefetch(&ops.a[g]);
+      ptx::tma_prefetch(&ops.b[g]);
+    }
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
-    ptx::mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tmem_full[a], 1);
+      ptx::mbar_init(&tmem_empty[a], L::kEpiWarps);
+    }
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 1) ptx::tmem_alloc<L::kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   // everything above overlapped the previous kernel's tail (PDL)
   pdl::entry();
   const uint32_t tmem_base = *tmem_slot;
+#ifdef PQLG_GEMM_TRACE
+  if (threadIdx.x == 0) {
+    PQLG_TRACE(0, gtimer());
+    PQLG_TRACE(1, clock64());
+    unsigned sm;
+    asm("mov.u32 %0, %%smid;" : "=r"(sm));
+    PQLG_TRACE(7, sm);
+  }
+#endif
+
+  auto k_range = [&](int split, int& kt0, int& nkt) {
+    kt0 = split * prob.k_tiles_per_split;
+    int kt1 = kt0 + prob.k_tiles_per_split;
+    if (kt1 > prob.k_tiles) kt1 = prob.k_tiles;
+    nkt = kt1 - kt0;  // >= 1: make_problem never creates an empty split
+  };
 
   if (warp == 0) {
     if (ptx::elect_one()) {
-      const int m0 = m_tile * kBM;
-      const int n0 = n_tile * BN;
-      for (int i = 0; i < n_kt; ++i) {
-        const int s = i % kStages;
-        const uint32_t ph = (i / kStages) & 1;
-        ptx::mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* sa = smem + s * L::kStageBytes;
-        uint8_t* sb = sa + L::kABytes;
-        ptx::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
-        const int k0 = (kt_begin + i) * kBK;
-        if constexpr (kAMN) {
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+        const TileCoord tc = tile_coord(t, prob, tiles_m, tiles_n);
+        int kt0, nkt;
+        k_range(tc.split, kt0, nkt);
+        const int m0 = tc.m_tile * kBM;
+        const int n0 = tc.n_tile * BN;
+        for (int i = 0; i < nkt; ++i, ++it) {
+          const int s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sa = smem + s * L::kStageBytes;
+          uint8_t* sb = sa + L::kABytes;
+          ptx::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
+          const int k0 = (kt0 + i) * kBK;
+          if constexpr (kAMN) {
 #pragma unroll
-          for (int j = 0; j < kBM / 32; ++j)
-            ptx::tma_load_2d(&ops.a[group], &full[s], sa + j * (32 * kBK * 4), m0 + 32 * j, k0);
-        } else {
-          ptx::tma_load_2d(&ops.a[group], &full[s], sa, k0, m0);
-        }
-        if constexpr (kBMN) {
+            for (int j = 0; j < kBM / 32; ++j)
+              ptx::tma_load_2d(&ops.a[tc.group], &full[s], sa + j * (32 * kBK * 4), m0 + 32 * j,
+                               k0);
+          } else {
+            ptx::tma_load_2d(&ops.a[tc.group], &full[s], sa, k0, m0);
+          }
+          if constexpr (kBMN) {
 #pragma unroll
-          for (int j = 0; j < BN / 32; ++j)
-            ptx::tma_load_2d(&ops.b[group], &full[s], sb + j * (32 * kBK * 4), n0 + 32 * j, k0);
-        } else {
-          ptx::tma_load_2d(&ops.b[group], &full[s], sb, k0, n0);
+            for (int j = 0; j < BN / 32; ++j)
+              ptx::tma_load_2d(&ops.b[tc.group], &full[s], sb + j * (32 * kBK * 4), n0 + 32 * j,
+                               k0);
+          } else {
+            ptx::tma_load_2d(&ops.b[tc.group], &full[s], sb, k0, n0);
+          }
         }
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = make_idesc<BN, kAMN, kBMN>();
     if (ptx::elect_one()) {
-      for (int i = 0; i < n_kt; ++i) {
-        const int s = i % kStages;
-        const uint32_t ph = (i / kStages) & 1;
-        ptx::mbar_wait(&full[s], ph);
+      uint32_t it = 0, lt = 0;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++lt) {
+        const TileCoord tc = tile_coord(t, prob, tiles_m, tiles_n);
+        int kt0, nkt;
+        k_range(tc.split, kt0, nkt);
+        const uint32_t a = lt & 1;
+        ptx::mbar_wait(&tmem_empty[a], ((lt >> 1) & 1) ^ 1);  // epilogue drained this buffer
         ptx::tc_fence_after();
-        const uint32_t sa = ptx::smem_u32(smem + s * L::kStageBytes);
-        const uint32_t sb = sa + L::kABytes;
+        const uint32_t d_tmem = tmem_base + a * BN;
+        for (int i = 0; i < nkt; ++i, ++it) {
+          const int s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          ptx::mbar_wait(&full[s], ph);
+          ptx::tc_fence_after();
+#ifdef PQLG_GEMM_TRACE
+          if (it == 0) PQLG_TRACE(2, clock64());
+#endif
+          const uint32_t sa = ptx::smem_u32(smem + s * L::kStageBytes);
+          const uint32_t sb = sa + L::kABytes;
 #pragma unroll
-        for (int j = 0; j < kBK / kUmmaK; ++j) {
-          const uint64_t ad = operand_desc<kAMN>(sa + j * k_step_bytes<kAMN>());
-          const uint64_t bd = operand_desc<kBMN>(sb + j * k_step_bytes<kBMN>());
-          ptx::mma_tf32(tmem_base, ad, bd, idesc, (i > 0 || j > 0) ? 1u : 0u);
+          for (int j = 0; j < kBK / kUmmaK; ++j) {
+            const uint64_t ad = operand_desc<kAMN>(sa + j * k_step_bytes<kAMN>());
+            const uint64_t bd = operand_desc<kBMN>(sb + j * k_step_bytes<kBMN>());
+            ptx::mma_tf32(d_tmem, ad, bd, idesc, (i > 0 || j > 0) ? 1u : 0u);
+          }
+          ptx::mma_commit(&empty[s]);
         }
-        ptx::mma_commit(&empty[s]);
+        ptx::mma_commit(&tmem_full[a]);
       }
-      ptx::mma_commit(tmem_full);
+#ifdef PQLG_GEMM_TRACE
+      PQLG_TRACE(3, clock64());
+#endif
     }
     __syncwarp();
   } else {
-    // Epilogue warps 2..5: TMEM lane quadrant = warp % 4.
+    // Epilogue: warp w reads TMEM lane quadrant w % 4 (hardware rule) and
+    // column half (w - 2) / 4 of the tile.
+    constexpr int kHalves = L::kEpiWarps / 4;
+    constexpr int kChunks = BN / 32;
+    constexpr int kChunksPerWarp = kChunks / kHalves;
+    const int ew = warp - 2;
     const int q = warp & 3;
     const int lane = threadIdx.x & 31;
-    const int row0 = m_tile * kBM + q * 32;
-    const int m = row0 + lane;
-    typename Epi::Row row;
-    epi.prepare(row, group, split, m, n_tile, scratch);
-    if (n_kt > 0) {
-      ptx::mbar_wait(tmem_full, 0);
+    epi::Ctx ctx{};
+    ctx.et = threadIdx.x - 64;
+    ctx.ne = 32 * L::kEpiWarps;
+    ctx.half = ew >> 2;
+    ctx.halves = kHalves;
+    uint8_t* stage = smem + L::kStagingOffset + ew * 4096;
+    uint32_t nstore = 0;
+    uint32_t lt = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++lt) {
+      const TileCoord tc = tile_coord(t, prob, tiles_m, tiles_n);
+      ctx.group = tc.group;
+      ctx.split = tc.split;
+      ctx.n_tile = tc.n_tile;
+      ctx.m_tile = tc.m_tile;
+      ctx.row0 = tc.m_tile * kBM + q * 32;
+      ctx.m = ctx.row0 + lane;
+      const uint32_t a = lt & 1;
+      if (lt > 0) ptx::named_bar_sync(1, 32 * L::kEpiWarps);  // previous tile done with scratch
+      typename Epi::Row row;
+      epi.prepare(row, ctx, scratch);
+      ptx::named_bar_sync(1, 32 * L::kEpiWarps);
+      ptx::mbar_wait(&tmem_full[a], (lt >> 1) & 1);
       ptx::tc_fence_after();
-    }
-    // staging for this warp: (BN/32) buffers of 32 rows x 128 B (SW128)
-    uint8_t* stage = smem + q * (BN / 32) * 4096;
+#ifdef PQLG_GEMM_TRACE
+      if (threadIdx.x == 64 && lt == 0) PQLG_TRACE(4, clock64());
+#endif
+      const uint32_t t_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + a * BN;
+      uint32_t r[32];
+      const int c_begin = ctx.half * kChunksPerWarp;
+      ptx::tmem_ld32(t_addr + c_begin * 32, r);
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      float v[32];
-      if (n_kt > 0) {
-        uint32_t r[32];
-        ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c * 32, r);
+      for (int c = c_begin; c < c_begin + kChunksPerWarp; ++c) {
         ptx::tmem_ld_wait();
+        float v[32];
 #pragma unroll
-        for (int t = 0; t < 32; ++t) v[t] = __uint_as_float(r[t]);
-      } else {
+        for (int u = 0; u < 32; ++u) v[u] = __uint_as_float(r[u]);
+        // next chunk's TMEM load overlaps this chunk's math and stores
+        if (c + 1 < c_begin + kChunksPerWarp) ptx::tmem_ld32(t_addr + (c + 1) * 32, r);
+        const int n0 = tc.n_tile * BN + c * 32;
+        const bool st = epi.chunk(row, ctx, n0, v, scratch);
+        if constexpr (Epi::kStoreRank > 0) {
+          if (st) {
+            uint8_t* buf = stage;
+            // the previous store from this buffer has finished reading it
+            if (lane == 0 && nstore > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
 #pragma unroll
-        for (int t = 0; t < 32; ++t) v[t] = 0.0f;
-      }
-      const int n0 = n_tile * BN + c * 32;
-      const bool st = epi.chunk(row, group, split, m, n0, v, scratch);
-      if constexpr (Epi::kStoreRank > 0) {
-        if (st) {
-          uint8_t* buf = stage + c * 4096;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float4* dst = reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4));
-            *dst = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) {
-            if constexpr (Epi::kStoreRank == 2) {
-              tma_store_2d(&ops.d[group], buf, n0, row0);
-            } else {
-              tma_store_3d(&ops.d[0], buf, n0, row0, group * prob.splits + split);
+            for (int j = 0; j < 8; ++j) {
+              float4* dst = reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4));
+              *dst = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             }
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (Epi::kStoreRank == 2) {
+                tma_store_2d(&ops.d[tc.group], buf, n0, ctx.row0);
+              } else {
+                tma_store_3d(&ops.d[0], buf, n0, ctx.row0, tc.group * prob.splits + tc.split);
+              }
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            ++nstore;
           }
         }
       }
+      // every tcgen05.ld of this warp has completed: release the accumulator
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tmem_empty[a]);
+      epi.end(row, ctx);
     }
-    epi.end(row, group, split, m, n_tile);
     if constexpr (Epi::kStoreRank > 0) {
-      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       __syncwarp();
     }
+#ifdef PQLG_GEMM_TRACE
+    if (threadIdx.x == 64) {
+      PQLG_TRACE(5, clock64());
+      PQLG_TRACE(6, gtimer());
+    }
+#endif
   }
 
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<kTmemCols>(tmem_base);
+    ptx::tmem_dealloc<L::kTmemCols>(tmem_base);
   }
 }
 

@@ -113,7 +113,7 @@ namespace {
 
 void PLearner::build_update() {
   const int B = B_, D = D_, A = A_, H = H_, nh = nh_, K0 = D + A;
-  const int nt = mlp::n_tiles(H);
+  const int nt = mlp::hidden_slots(H);  // head-dot partial slots
   const int bnH = mlp::bn_for(H);
   const int mt = (B + 127) / 128;
   const int wpr = H / 32;
@@ -218,7 +218,7 @@ void PLearner::build_update() {
       for (int k = 0; k < 2; ++k) e.w_head[k] = q[k] + qnet_.w_off[nh];
       e.partial = part_.p;
       e.ld_part = B;
-      e.n_tiles = nt;
+      e.n_slots = nt;
     }
     const float* a0 = l == 0 ? X_.p : cact_[0][l - 1].p;
     const float* a1 = l == 0 ? X_.p : cact_[1][l - 1].p;

@@ -32,14 +32,14 @@ void DeviceStates::insert(const float* rows, int64_t ld_rows, uint64_t n, cudaSt
 void launch_replay_sample(const DeviceReplay& r, const replay::Norm& norm, const replay::Gather& g,
                           replay::SamplerState* ss, const uint64_t* idx_dev, uint64_t B,
                           cudaStream_t st) {
-  const uint64_t blocks = (B + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const uint64_t blocks = (B + replay::kSampleRows - 1) / replay::kSampleRows;
   launch(replay::replay_sample_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kWarpsPerBlock), 0, st, r.view(), norm, g, ss, idx_dev, B);
 }
 
 void launch_state_sample(const DeviceStates& r, const replay::Norm& norm, float* out,
                          int64_t ld_out, replay::SamplerState* ss, const uint64_t* idx_dev,
                          uint64_t B, cudaStream_t st) {
-  const uint64_t blocks = (B + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const uint64_t blocks = (B + replay::kSampleRows - 1) / replay::kSampleRows;
   launch(replay::state_sample_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kWarpsPerBlock), 0, st, r.view(), norm, out, ld_out, ss, idx_dev, B);
 }
 

@@ -440,21 +440,107 @@ __device__ __forceinline__ void finish_sample(SamplerState* ss, const uint64_t* 
   if (lane == 0) ss->ticket = 0;
 }
 
-// ReplayBuffer::sample fused with apply_stats on obs and boot_obs; one warp
-// per row, then the ticketed finish above (one launch per sample).
-static __global__ void replay_sample_kernel(Ring ring, Norm norm, Gather g, SamplerState* ss,
-                                     const uint64_t* host_idx, uint64_t B) {
+// ReplayBuffer::sample fused with apply_stats on obs and boot_obs.  A block
+// owns kSampleRows rows: its first warp draws their indices (one Philox draw
+// per lane, in parallel), then each warp gathers kRowsPerWarp rows with all
+// of their loads in flight before any store (the gather is latency-bound:
+// random ~850 B rows).  The ticketed finish above ends the launch.
+constexpr int kSampleRows = 32;
+constexpr int kRowsPerWarp = kSampleRows / kWarpsPerBlock;  // 4
+
+__device__ __forceinline__ void draw_block_indices(const SamplerState* ss,
+                                                   const uint64_t* host_idx, uint64_t count,
+                                                   uint64_t B, uint64_t* s_idx) {
+  if (threadIdx.x < kSampleRows) {
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kSampleRows + threadIdx.x;
+    uint64_t i = 0;
+    if (r < B) {
+      bool reject = false;
+      i = sample_index(ss, host_idx, count, r, reject);
+      if (reject) atomicOr(const_cast<uint32_t*>(&ss->reject), 1u);
+    }
+    s_idx[threadIdx.x] = i;
+  }
+  __syncthreads();
+}
+
+static __global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    replay_sample_kernel(Ring ring, Norm norm, Gather g, SamplerState* ss,
+                         const uint64_t* host_idx, uint64_t B) {
+  __shared__ uint64_t s_idx[kSampleRows];
   pdl::entry();
   const int lane = threadIdx.x & 31;
-  const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int w = threadIdx.x >> 5;
   const uint64_t count = ring.state[1];
-  if (r < B) {
-    bool reject = false;
-    uint64_t i = 0;
-    if (lane == 0) i = sample_index(ss, host_idx, count, r, reject);
-    i = __shfl_sync(0xffffffffu, i, 0);
-    if (lane == 0 && reject) atomicOr(&ss->reject, 1u);
-    gather_row(ring, norm, g, i, r, lane);
+  draw_block_indices(ss, host_idx, count, B, s_idx);
+  const uint64_t rb = static_cast<uint64_t>(blockIdx.x) * kSampleRows + w * kRowsPerWarp;
+  if (ring.D <= 256) {
+    const bool ident = *norm.identity != 0;
+    float x[kRowsPerWarp][8], y[kRowsPerWarp][8];
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      const uint64_t i = s_idx[w * kRowsPerWarp + k];
+      const float* so = ring.obs + i * ring.ld_obs;
+      const float* sb = ring.boot + i * ring.ld_obs;
+      const bool ok = rb + k < B;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int d = lane + 32 * u;
+        x[k][u] = (ok && d < ring.D) ? __ldg(so + d) : 0.0f;
+        y[k][u] = (ok && d < ring.D) ? __ldg(sb + d) : 0.0f;
+      }
+    }
+    float av[kRowsPerWarp], rv[kRowsPerWarp], ev[kRowsPerWarp];
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      const uint64_t i = s_idx[w * kRowsPerWarp + k];
+      const bool ok = rb + k < B;
+      av[k] = (ok && lane < ring.A) ? __ldg(ring.act + i * ring.ld_act + lane) : 0.0f;
+      rv[k] = (ok && lane == 0) ? __ldg(ring.ret + i) : 0.0f;
+      ev[k] = (ok && lane == 0) ? __ldg(ring.eff + i) : 0.0f;
+    }
+    float mu[8], iv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int d = lane + 32 * u;
+      mu[u] = (d < ring.D && !ident) ? norm.mean[d] : 0.0f;
+      iv[u] = (d < ring.D && !ident) ? norm.inv[d] : 1.0f;
+    }
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      const uint64_t r = rb + k;
+      if (r >= B) break;
+      float* dobs = g.obs + r * g.ld_obs;
+      float* dboot = g.boot + r * g.ld_boot;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int d = lane + 32 * u;
+        if (d < ring.D) {
+          float xx = x[k][u], yy = y[k][u];
+          if (!ident) {
+            xx = normalize1(xx, mu[u], iv[u]);
+            yy = normalize1(yy, mu[u], iv[u]);
+          }
+          dobs[d] = xx;
+          dboot[d] = yy;
+        }
+      }
+      if (lane < ring.A) g.act[r * g.ld_act + lane] = av[k];
+      if (lane == 0) {
+        g.ret[r] = rv[k];
+        g.eff[r] = ev[k];
+      }
+    }
+    if (ring.A > 32) {  // wide actions: the generic path for the columns >= 32
+      for (int k = 0; k < kRowsPerWarp && rb + k < B; ++k) {
+        const uint64_t i = s_idx[w * kRowsPerWarp + k];
+        for (int d = 32 + lane; d < ring.A; d += 32)
+          g.act[(rb + k) * g.ld_act + d] = ring.act[i * ring.ld_act + d];
+      }
+    }
+  } else {
+    for (int k = 0; k < kRowsPerWarp && rb + k < B; ++k)
+      gather_row(ring, norm, g, s_idx[w * kRowsPerWarp + k], rb + k, lane);
   }
   finish_sample(ss, host_idx, count, B,
                 [&](uint64_t i, uint64_t rr, int ln) { gather_row(ring, norm, g, i, rr, ln); });
@@ -472,20 +558,44 @@ __device__ __forceinline__ void gather_state(const StateRing& ring, const Norm& 
   }
 }
 
-// StateBuffer::sample fused with apply_stats.
-static __global__ void state_sample_kernel(StateRing ring, Norm norm, float* out, int64_t ld_out,
-                                    SamplerState* ss, const uint64_t* host_idx, uint64_t B) {
+// StateBuffer::sample fused with apply_stats (block layout as above).
+static __global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    state_sample_kernel(StateRing ring, Norm norm, float* out, int64_t ld_out, SamplerState* ss,
+                        const uint64_t* host_idx, uint64_t B) {
+  __shared__ uint64_t s_idx[kSampleRows];
   pdl::entry();
   const int lane = threadIdx.x & 31;
-  const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int w = threadIdx.x >> 5;
   const uint64_t count = ring.state[1];
-  if (r < B) {
-    bool reject = false;
-    uint64_t i = 0;
-    if (lane == 0) i = sample_index(ss, host_idx, count, r, reject);
-    i = __shfl_sync(0xffffffffu, i, 0);
-    if (lane == 0 && reject) atomicOr(&ss->reject, 1u);
-    gather_state(ring, norm, out, ld_out, i, r, lane);
+  draw_block_indices(ss, host_idx, count, B, s_idx);
+  const uint64_t rb = static_cast<uint64_t>(blockIdx.x) * kSampleRows + w * kRowsPerWarp;
+  if (ring.D <= 256) {
+    const bool ident = *norm.identity != 0;
+    float x[kRowsPerWarp][8];
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      const float* so = ring.obs + s_idx[w * kRowsPerWarp + k] * ring.ld;
+      const bool ok = rb + k < B;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int d = lane + 32 * u;
+        x[k][u] = (ok && d < ring.D) ? __ldg(so + d) : 0.0f;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      const uint64_t r = rb + k;
+      if (r >= B) break;
+      float* d_out = out + r * ld_out;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int d = lane + 32 * u;
+        if (d < ring.D) d_out[d] = ident ? x[k][u] : normalize1(x[k][u], norm.mean[d], norm.inv[d]);
+      }
+    }
+  } else {
+    for (int k = 0; k < kRowsPerWarp && rb + k < B; ++k)
+      gather_state(ring, norm, out, ld_out, s_idx[w * kRowsPerWarp + k], rb + k, lane);
   }
   finish_sample(ss, host_idx, count, B, [&](uint64_t i, uint64_t rr, int ln) {
     gather_state(ring, norm, out, ld_out, i, rr, ln);

@@ -5,6 +5,7 @@
 // twin online critics -> loss -> backward (head, then wgrad/dgrad per layer)
 // -> fixed-order gradient reduction + fp64 norm -> fused clip/Adam/Polyak.
 // Every step is a pre-built launch; update_n() replays them from a CUDA graph.
+#include <algorithm>
 #include <memory>
 #include <random>
 #include <vector>
@@ -121,7 +122,7 @@ VLearner::~VLearner() {
 void VLearner::build_update() {
   const int B = B_, D = D_, A = A_, H = H_, nh = nh_, K0 = D + A;
   const int64_t P = qnet_.params;
-  const int nt = mlp::n_tiles(H);
+  const int nt = mlp::hidden_slots(H);  // head-dot partial slots
   const int bnH = mlp::bn_for(H);
   const int mt = (B + 127) / 128;
   const int wpr = H / 32;  // mask words per row
@@ -153,7 +154,7 @@ void VLearner::build_update() {
   part_o_.alloc(2ull * nt * B);
   up_.alloc(2ull * B);
   const int loss_blocks = (B + critic::kRowThreads - 1) / critic::kRowThreads;
-  block_loss_.alloc((B + c51::kThreads - 1) / c51::kThreads);  // >= either loss kernel's grid
+  block_loss_.alloc(std::max((B + c51::kThreads - 1) / c51::kThreads, c51::kLossBlocks));
   loss_counter_.alloc(1);
 
   if (dist_) {
@@ -164,7 +165,7 @@ void VLearner::build_update() {
     probs_o_.alloc(2ull * B * Lp_);
     ev_t_.alloc(2ull * B);
     up51_.alloc(2ull * B * Lp_);
-    c51_blocks_ = (B + c51::kThreads - 1) / c51::kThreads;
+    c51_blocks_ = c51::kLossBlocks * c51::kLossWarps;  // head-bias partial terms (warps)
     db51_.alloc(2ull * c51_blocks_ * L_);
     // the GEMMs read the 51-wide heads from padded mirrors (16-byte rows),
     // refreshed at the start of every update (the previous update's Adam /
@@ -173,9 +174,6 @@ void VLearner::build_update() {
     for (int k = 0; k < 4; ++k) heads_[k].init(src[k] + qnet_.w_off[nh], H, L_);
     const WeightMirror* hm = heads_.data();
     steps_.push_back([hm](cudaStream_t st) { refresh_mirrors(hm, 4, st); });
-    PQLG_CUDA(cudaFuncSetAttribute(c51::c51_critic_loss_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(c51::kLossSmem)));
   }
 
   // ---------------------------------------------------------------- sample
@@ -238,7 +236,7 @@ void VLearner::build_update() {
         for (int k = 0; k < 2; ++k) e.w_head[k] = nets[k] + qnet_.w_off[nh];
         e.partial = part;
         e.ld_part = B;
-        e.n_tiles = nt;
+        e.n_slots = nt;
       }
       const float* a0 = l == 0 ? X : (target ? tact_[0][l - 1].p : oact_[0][l - 1].p);
       const float* a1 = l == 0 ? X : (target ? tact_[1][l - 1].p : oact_[1][l - 1].p);
@@ -299,10 +297,9 @@ void VLearner::build_update() {
     a.status = status_.p;
     a.B = B;
     a.Bg = B * world_;
-    const int blocks = c51_blocks_;
-    steps_.push_back([a, blocks](cudaStream_t st) {
-      launch(c51::c51_critic_loss_kernel, dim3(blocks), dim3(c51::kThreads), c51::kLossSmem, st,
-             a);
+    steps_.push_back([a](cudaStream_t st) {
+      launch(c51::c51_critic_loss_kernel, dim3(c51::kLossBlocks), dim3(c51::kLossWarps * 32), 0,
+             st, a);
     });
   } else {
     critic::LossArgs a{};

@@ -1,0 +1,45 @@
+// Traced copy of the forward-layer GEMM (tools only): per-CTA phase
+// timestamps to split a launch into prologue / pipeline fill / mainloop /
+// epilogue.  Build: see tools/gemm_trace.py.
+#define PQLG_GEMM_TRACE 1
+#include "../paper_2307_12983_b200/csrc/epilogues.cuh"
+#include "../paper_2307_12983_b200/csrc/gemm_host.cuh"
+
+using namespace pqlg;
+
+// kind 0: hidden layer (BN 256, Hidden epilogue); 1: policy head (BN 32,
+// PolicyHead: bias + tanh squash, no noise) with N <= 32.
+extern "C" __attribute__((visibility("default"))) int trace_gemm(
+    const float* A, const float* B, float* D, const float* bias, int M, int N, int K, int groups,
+    unsigned long long* trace, int iters, int store, int kind, void* stream) {
+  return guarded([&] {
+    auto st = static_cast<cudaStream_t>(stream);
+    PQLG_CUDA(cudaMemcpyToSymbol(gemm::g_trace, &trace, sizeof(trace)));
+    gemm::Operands ops;
+    const gemm::Problem p = gemm::make_problem(M, N, K, 1);
+    if (kind == 0) {
+      ops.a[0] = ops.a[1] = gemm::map_a(A, M, K, K, false, true);
+      ops.b[0] = ops.b[1] = gemm::map_b(B, N, K, N, true, 256, true);
+      ops.d[0] = ops.d[1] = make_store_map(D, M, N, N);
+      epi::Hidden e{};
+      e.bias[0] = e.bias[1] = bias;
+      e.bn = 256;
+      e.M = M;
+      e.N = N;
+      e.store = store;
+      for (int i = 0; i < iters; ++i) gemm::launch<256, false, true>(ops, p, groups, e, st);
+    } else {
+      ops.a[0] = ops.a[1] = gemm::map_a(A, M, K, K, false, true);
+      ops.b[0] = ops.b[1] = gemm::map_b(B, N, K, N, true, 32, true);
+      epi::PolicyHead e{};
+      e.bias = bias;
+      e.act = D;
+      e.ld_act = N;
+      e.M = M;
+      e.A = N;
+      e.mid = 0.0f;
+      e.half = 1.0f;
+      for (int i = 0; i < iters; ++i) gemm::launch<32, false, true>(ops, p, groups, e, st);
+    }
+  });
+}

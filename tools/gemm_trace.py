@@ -1,0 +1,55 @@
+"""Per-CTA phase timing of the forward-layer tcgen05 GEMM (GPU box).
+
+Builds tools/_build/libgemmtrace.so (the library's GEMM with
+-DPQLG_GEMM_TRACE), runs M x 512 x K with 1 or 2 groups, and prints the
+median prologue->first-stage, mainloop and epilogue cycles plus the launch
+span from %globaltimer."""
+import ctypes as C
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from paper_2307_12983_b200 import build as b  # noqa: E402
+
+out = ROOT / "tools" / "_build" / "libgemmtrace.so"
+out.parent.mkdir(exist_ok=True)
+src = ROOT / "tools" / "gemm_trace.cu"
+subprocess.run([b.nvcc(), *b.ARCH, *b.NVCC_FLAGS, "-shared", str(src),
+                str(ROOT / "paper_2307_12983_b200" / "csrc" / "common.cu"), "-o", str(out),
+                "-lcuda"], check=True)
+lib = C.CDLL(str(out))
+st = torch.cuda.Stream()
+import os
+STORE = int(os.environ.get("TRACE_STORE", "1"))
+KIND = int(os.environ.get("TRACE_KIND", "0"))
+shapes = ([(8192, 512, 512, 1), (8192, 512, 512, 2), (8192, 512, 232, 2), (16384, 512, 512, 1),
+           (8192, 512, 4096, 1)] if KIND == 0 else [(8192, 20, 512, 1), (16384, 20, 512, 1)])
+for (M, N, K, groups) in shapes:
+    a = torch.randn(M, K, device="cuda"); w = torch.randn(K, (N + 3) // 4 * 4, device="cuda")
+    d = torch.empty(M, N, device="cuda"); bias = torch.zeros(N, device="cuda")
+    bn = 256 if KIND == 0 else 32
+    ctas = min((M // 128) * ((N + bn - 1) // bn) * groups, 148)
+    tr = torch.zeros(ctas * 8, dtype=torch.int64, device="cuda")
+    for it in range(3):
+        rc = lib.trace_gemm(C.c_void_p(a.data_ptr()), C.c_void_p(w.data_ptr()),
+                            C.c_void_p(d.data_ptr()), C.c_void_p(bias.data_ptr()), M, N, K, groups,
+                            C.c_void_p(tr.data_ptr()), 1, STORE, KIND, C.c_void_p(st.cuda_stream))
+        assert rc == 0
+        st.synchronize()
+    t = tr.view(ctas, 8).cpu().numpy().astype(np.int64)
+    g0 = t[:, 0] - t[:, 0].min()
+    fill = t[:, 2] - t[:, 1]
+    main = t[:, 3] - t[:, 2]
+    wait_epi = t[:, 4] - t[:, 1]
+    tail = t[:, 5] - t[:, 3]
+    span = (t[:, 6].max() - t[:, 0].min()) / 1e3
+    print(f"store={STORE} M={M} N={N} K={K} groups={groups} ctas={ctas}: span {span:.1f} us; "
+          f"start offsets us (p50/max) {np.median(g0)/1e3:.2f}/{g0.max()/1e3:.2f}; "
+          f"cycles p50: fill {np.median(fill):.0f} all-tile mainloop {np.median(main):.0f} "
+          f"entry->first acc {np.median(wait_epi):.0f} last-MMA->epilogue end "
+          f"{np.median(tail):.0f}; SMs used {len(set(t[:, 7]))}", flush=True)

@@ -19,10 +19,11 @@ if which in ("gemm", "both"):
     _lib.call("pqlg_k_gemm_tf32_repeat", a.data_ptr(), b.data_ptr(), d.data_ptr(),
               bias.data_ptr(), M, N, K, K, N, N, 1, 3, C.c_void_p(st.cuda_stream))
     st.synchronize()
-if which in ("critic", "both"):
+if which in ("critic", "both", "c51"):
     D, A, H, nh, B, cap = 211, 20, 512, 3, 8192, 200_000
+    extra = dict(algo=_lib.ALGO_C51, n_atoms=51) if which == "c51" else {}
     cfg = _lib.default_config(batch_size=B, buffer_capacity=cap, hidden=H, hidden_layers=nh,
-                              n_envs=16384)
+                              n_envs=16384, **extra)
     dims = _lib.TaskDims(D, A, -1.0, 1.0)
     h = C.c_void_p()
     _lib.call("pqlg_vlearner_create", C.byref(cfg), C.byref(dims), 1, C.c_void_p(st.cuda_stream),
