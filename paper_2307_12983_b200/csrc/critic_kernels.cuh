@@ -211,17 +211,31 @@ struct HeadInputGradArgs {
   int B, H;
 };
 
-static __global__ void head_input_grad_kernel(const __grid_constant__ HeadInputGradArgs a) {
+// Row-blocked: each warp takes whole rows, lane l covering columns
+// [4l, 4l+4) + 128j -- one mask word per 8 lanes, float4 stores.
+static __global__ void __launch_bounds__(256)
+    head_input_grad_kernel(const __grid_constant__ HeadInputGradArgs a) {
   pdl::entry();
   const int k = blockIdx.y;
-  const int64_t n = static_cast<int64_t>(a.B) * a.H;
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
   const int words = a.H >> 5;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t b = e / a.H;
-    const int i = static_cast<int>(e % a.H);
-    const uint32_t bits = a.mask[k][b * words + (i >> 5)];
-    a.G[k][e] = ((bits >> (i & 31)) & 1u) ? __fmul_rn(a.up[k * a.B + b], a.w[k][i]) : 0.0f;
+  const float* __restrict__ w = a.w[k];
+  const float* __restrict__ up = a.up + static_cast<int64_t>(k) * a.B;
+  for (int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < a.B; b += warps) {
+    const float u = up[b];
+    const uint32_t* mrow = a.mask[k] + static_cast<int64_t>(b) * words;
+    float* g = a.G[k] + static_cast<int64_t>(b) * a.H;
+    for (int c = 4 * lane; c < a.H; c += 128) {
+      const uint32_t bits = mrow[c >> 5] >> (c & 31);
+      const float4 w4 = *reinterpret_cast<const float4*>(w + c);
+      float4 o;
+      o.x = (bits & 1u) ? __fmul_rn(u, w4.x) : 0.0f;
+      o.y = (bits & 2u) ? __fmul_rn(u, w4.y) : 0.0f;
+      o.z = (bits & 4u) ? __fmul_rn(u, w4.z) : 0.0f;
+      o.w = (bits & 8u) ? __fmul_rn(u, w4.w) : 0.0f;
+      *reinterpret_cast<float4*>(g + c) = o;
+    }
   }
 }
 
@@ -242,23 +256,35 @@ struct PolicyHeadBwdArgs {
   int B, A, rows_per_tile;
 };
 
-static __global__ void policy_head_backward_kernel(const __grid_constant__ PolicyHeadBwdArgs a) {
+// One warp per tile of rows_per_tile (<= 8) rows, lane = action column:
+// every load of the tile is in flight before the math.
+static __global__ void __launch_bounds__(32)
+    policy_head_backward_kernel(const __grid_constant__ PolicyHeadBwdArgs a) {
   pdl::entry();
   const int tile = blockIdx.x;
   const int b0 = tile * a.rows_per_tile;
-  const int b1 = min(b0 + a.rows_per_tile, a.B);
-  for (int c = threadIdx.x; c < a.A; c += blockDim.x) {
-    float db = 0.0f;
-    for (int b = b0; b < b1; ++b) {
-      const float da = __fadd_rn(a.dact1[static_cast<int64_t>(b) * a.ld_dact + c],
-                                 a.dact2[static_cast<int64_t>(b) * a.ld_dact + c]);
-      const float t = a.t[static_cast<int64_t>(b) * a.ld_t + c];
-      const float g = __fmul_rn(__fmul_rn(da, a.half), __fsub_rn(1.0f, __fmul_rn(t, t)));
-      a.dy[static_cast<int64_t>(b) * a.ld_dy + c] = g;
-      db = __fadd_rn(db, g);
-    }
-    a.db_part[static_cast<int64_t>(tile) * a.A + c] = db;
+  const int c = threadIdx.x;
+  if (c >= a.A) return;
+  float d1[8], d2[8], tv[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int b = b0 + u;
+    const bool ok = u < a.rows_per_tile && b < a.B;
+    d1[u] = ok ? a.dact1[static_cast<int64_t>(b) * a.ld_dact + c] : 0.0f;
+    d2[u] = ok ? a.dact2[static_cast<int64_t>(b) * a.ld_dact + c] : 0.0f;
+    tv[u] = ok ? a.t[static_cast<int64_t>(b) * a.ld_t + c] : 0.0f;
   }
+  float db = 0.0f;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int b = b0 + u;
+    if (u >= a.rows_per_tile || b >= a.B) break;
+    const float da = __fadd_rn(d1[u], d2[u]);
+    const float g = __fmul_rn(__fmul_rn(da, a.half), __fsub_rn(1.0f, __fmul_rn(tv[u], tv[u])));
+    a.dy[static_cast<int64_t>(b) * a.ld_dy + c] = g;
+    db = __fadd_rn(db, g);
+  }
+  a.db_part[static_cast<int64_t>(tile) * a.A + c] = db;
 }
 
 }  // namespace pqlg::critic

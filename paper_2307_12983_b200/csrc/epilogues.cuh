@@ -39,16 +39,16 @@ struct Ctx {
 struct Hidden {
   static constexpr int kStoreRank = 2;
   static constexpr bool kSplitCols = true;
-  const float* bias[2];
-  const float* w_head[2];  // null: no head dot
-  uint32_t* mask[2];       // null: no bitmask
+  const float* bias[4];
+  const float* w_head[4];  // null: no head dot
+  uint32_t* mask[4];       // null: no bitmask
   int ld_mask;             // words per row (= N/32)
-  float* partial;          // [group][slot][ld_part], slot = n_tile * halves + half
+  float* partial[4];       // per group [slot][ld_part], slot = n_tile * halves + half
   int64_t ld_part;
   int n_slots;             // n_tiles * halves (mlp::hidden_slots)
   int bn;
   int M, N;
-  int store;  // 0: skip storing the activation (target critics' last layer)
+  int store;  // bit g: store group g's activation (0 for the target critics' last layer)
   struct Row {
     float dot;
   };
@@ -83,12 +83,12 @@ struct Hidden {
     }
     if (mask[c.group] && c.m < M)
       mask[c.group][static_cast<int64_t>(c.m) * ld_mask + (n0 >> 5)] = bits;
-    return store != 0;
+    return ((store >> c.group) & 1) != 0;
   }
   __device__ void end(Row& r, const Ctx& c) const {
     if (c.m < M && w_head[c.group]) {
       const int slot = c.n_tile * c.halves + c.half;
-      partial[(static_cast<int64_t>(c.group) * n_slots + slot) * ld_part + c.m] = r.dot;
+      partial[c.group][static_cast<int64_t>(slot) * ld_part + c.m] = r.dot;
     }
   }
 };
@@ -311,10 +311,10 @@ struct C51Head {
   static constexpr int kStoreRank = 0;
   static constexpr bool kSplitCols = false;
   static constexpr int kMaxAtoms = 64;
-  const float* bias[2];
-  float* probs[2];
+  const float* bias[4];
+  float* probs[4];
   int64_t ld;
-  float* ev[2];  // nullable
+  float* ev[4];  // nullable
   const float* atoms;
   int M, L;
   struct Row {

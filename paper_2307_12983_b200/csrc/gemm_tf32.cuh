@@ -67,10 +67,12 @@ constexpr int kUmmaK = 8;      // K per tcgen05.mma.kind::tf32
 constexpr int kScratchBytes = 2048;  // per-tile epilogue constants
 constexpr int kMaxDynSmem = 232448;  // 227 KB per CTA on sm_100
 
+constexpr int kMaxGroups = 4;  // online + target twin critics share one launch
+
 struct Operands {
-  CUtensorMap a[2];  // one per group (twin critics share a launch)
-  CUtensorMap b[2];
-  CUtensorMap d[2];  // output maps (Epi::kStoreRank > 0)
+  CUtensorMap a[kMaxGroups];  // one per group
+  CUtensorMap b[kMaxGroups];
+  CUtensorMap d[kMaxGroups];  // output maps (Epi::kStoreRank > 0)
 };
 
 struct Problem {

@@ -83,6 +83,33 @@ Step fwd(const float* A0, const float* A1, int64_t lda, const float* W0, const f
   return step;
 }
 
+// Forward layer over `groups` (<= gemm::kMaxGroups) independent nets sharing
+// one launch: A[g] [M x K] (stride lda), W[g] [K x N] (stride ldw), outputs
+// D[g] [M x N] (stride ldd; null: the epilogue stores nothing / itself).
+template <class Epi>
+Step fwd_groups(const float* const* A, int64_t lda, const float* const* W, int M, int N, int K,
+                int groups, Epi epi, int64_t ldw, const float* const* D, int64_t ldd) {
+  require(groups >= 1 && groups <= gemm::kMaxGroups, "fwd_groups: 1..4 groups");
+  Step step;
+  if (ldw == 0) ldw = N;
+  if (ldd == 0) ldd = N;
+  with_bn(N, [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    gemm::Operands ops;
+    std::memset(&ops, 0, sizeof(ops));
+    for (int g = 0; g < groups; ++g) {
+      ops.a[g] = gemm::map_a(A[g], M, K, lda, false, true);
+      ops.b[g] = gemm::map_b(W[g], N, K, ldw, true, BN, true);
+      if (D && D[g]) ops.d[g] = make_store_map(D[g], M, N, ldd);
+    }
+    const gemm::Problem p = gemm::make_problem(M, N, K, 1);
+    step = [ops, p, groups, epi](cudaStream_t st) {
+      gemm::launch<BN, false, true>(ops, p, groups, epi, st);
+    };
+  });
+  return step;
+}
+
 // din[M x N_in] = G[M x N_out] * W^T, W = [N_in x N_out] row-major (ld = ldw).
 template <class Epi>
 Step dgrad(const float* G0, const float* G1, int64_t ldg, const float* W0, const float* W1,

@@ -213,10 +213,12 @@ void PLearner::build_update() {
     e.M = B;
     e.N = H;
     const bool last = l + 1 == nh;
-    e.store = (last && !dist_) ? 0 : 1;
+    e.store = (last && !dist_) ? 0 : 3;
     if (last && !dist_) {
-      for (int k = 0; k < 2; ++k) e.w_head[k] = q[k] + qnet_.w_off[nh];
-      e.partial = part_.p;
+      for (int k = 0; k < 2; ++k) {
+        e.w_head[k] = q[k] + qnet_.w_off[nh];
+        e.partial[k] = part_.p + static_cast<size_t>(k) * nt * B;
+      }
       e.ld_part = B;
       e.n_slots = nt;
     }
@@ -336,7 +338,7 @@ void PLearner::build_update() {
                                 q[1] + qnet_.w_off[0] + D * H, H, B, A, H, 2, s));
   }
   // ------------------------------------------------- policy head backward
-  const int ptiles = (B + 63) / 64;
+  const int ptiles = (B + 7) / 8;  // policy-head backward tiles (8 rows, one warp each)
   head_db_.alloc(static_cast<size_t>(ptiles) * A);
   {
     critic::PolicyHeadBwdArgs a{};
@@ -351,7 +353,7 @@ void PLearner::build_update() {
     a.half = (dims_.high - dims_.low) / 2.0f;
     a.B = B;
     a.A = A;
-    a.rows_per_tile = 64;
+    a.rows_per_tile = 8;
     steps_.push_back([a, ptiles](cudaStream_t st) {
       launch(critic::policy_head_backward_kernel, dim3(ptiles), dim3(32), 0, st, a);
     });

@@ -215,62 +215,66 @@ void VLearner::build_update() {
     steps_.push_back(mlp::fwd(in, in, ld, W, W, B, A, H, 1, ph, lagged_head_.stride()));
   }
 
-  // --------------------------------------------- twin critics, shared helper
-  auto critic_fwd = [&](bool target) {
-    float* nets[2] = {target ? q1t : q1, target ? q2t : q2};
-    const float* X = target ? Xtg_.p : Xon_.p;
-    float* part = target ? part_t_.p : part_o_.p;
+  // ---------- twin target + twin online critics: one 4-group launch per layer
+  // Groups (q1', q2', q1, q2): the target and online chains are independent
+  // given their inputs [norm(boot) | pi(boot)] and [norm(obs) | act], so each
+  // layer is one persistent launch of 4 x (M/128) x (H/BN) tiles.
+  {
+    float* nets[4] = {q1t, q2t, q1, q2};
     for (int l = 0; l < nh; ++l) {
       epi::Hidden e{};
-      for (int k = 0; k < 2; ++k) {
-        e.bias[k] = nets[k] + qnet_.b_off[l];
-        e.mask[k] = target ? nullptr : omask_[k][l].p;
+      const float* A[4];
+      const float* W[4];
+      const float* Dst[4];
+      const bool last = l + 1 == nh;
+      for (int g = 0; g < 4; ++g) {
+        const bool tgt = g < 2;
+        const int k = g & 1;
+        e.bias[g] = nets[g] + qnet_.b_off[l];
+        e.mask[g] = tgt ? nullptr : omask_[k][l].p;
+        W[g] = nets[g] + qnet_.w_off[l];
+        A[g] = l == 0 ? (tgt ? Xtg_.p : Xon_.p) : (tgt ? tact_[k][l - 1].p : oact_[k][l - 1].p);
+        const bool store = !tgt || !last || dist_;
+        if (store) e.store |= 1 << g;
+        Dst[g] = store ? (tgt ? tact_[k][l].p : oact_[k][l].p) : nullptr;
+        if (last && !dist_) {  // DDPG value head 512->1 folded in as partial dots
+          e.w_head[g] = nets[g] + qnet_.w_off[nh];
+          e.partial[g] = (tgt ? part_t_.p : part_o_.p) + static_cast<size_t>(k) * nt * B;
+        }
       }
       e.ld_mask = wpr;
       e.bn = bnH;
       e.M = B;
       e.N = H;
-      const bool last = l + 1 == nh;
-      e.store = (!target || !last || dist_) ? 1 : 0;
-      if (last && !dist_) {
-        for (int k = 0; k < 2; ++k) e.w_head[k] = nets[k] + qnet_.w_off[nh];
-        e.partial = part;
-        e.ld_part = B;
-        e.n_slots = nt;
-      }
-      const float* a0 = l == 0 ? X : (target ? tact_[0][l - 1].p : oact_[0][l - 1].p);
-      const float* a1 = l == 0 ? X : (target ? tact_[1][l - 1].p : oact_[1][l - 1].p);
-      const float* d0 = target ? tact_[0][l].p : oact_[0][l].p;
-      const float* d1 = target ? tact_[1][l].p : oact_[1][l].p;
-      if (!e.store) d0 = d1 = nullptr;
+      e.ld_part = B;
+      e.n_slots = nt;
       const int64_t lda = l == 0 ? Kp_ : H;
       const int K = l == 0 ? K0 : H;
-      steps_.push_back(mlp::fwd(a0, a1, lda, nets[0] + qnet_.w_off[l], nets[1] + qnet_.w_off[l],
-                                B, H, K, 2, e, 0, d0, d1, H));
+      steps_.push_back(mlp::fwd_groups(A, lda, W, B, H, K, 4, e, 0, Dst, H));
     }
     if (dist_) {
-      // categorical head H -> L: logits + softmax (+ expected values of the
+      // categorical heads H -> L: logits + softmax (+ expected values of the
       // target heads) in the epilogue (c51.hpp:114-126, :135-138)
       epi::C51Head ch{};
-      float* pr = target ? probs_t_.p : probs_o_.p;
-      for (int k = 0; k < 2; ++k) {
-        ch.bias[k] = nets[k] + qnet_.b_off[nh];
-        ch.probs[k] = pr + static_cast<size_t>(k) * B * Lp_;
-        ch.ev[k] = target ? ev_t_.p + static_cast<size_t>(k) * B : nullptr;
+      const float* A[4];
+      const float* W[4];
+      for (int g = 0; g < 4; ++g) {
+        const bool tgt = g < 2;
+        const int k = g & 1;
+        ch.bias[g] = nets[g] + qnet_.b_off[nh];
+        ch.probs[g] = (tgt ? probs_t_.p : probs_o_.p) + static_cast<size_t>(k) * B * Lp_;
+        ch.ev[g] = tgt ? ev_t_.p + static_cast<size_t>(k) * B : nullptr;
+        A[g] = tgt ? tact_[k][nh - 1].p : oact_[k][nh - 1].p;
+        W[g] = heads_[tgt ? 2 + k : k].ptr();
       }
       ch.ld = Lp_;
       ch.atoms = atoms_.p;
       ch.M = B;
       ch.L = L_;
-      const int mi = target ? 2 : 0;
-      const auto& hl = target ? tact_ : oact_;
-      steps_.push_back(mlp::fwd(hl[0][nh - 1].p, hl[1][nh - 1].p, H, heads_[mi].ptr(),
-                                heads_[mi + 1].ptr(), B, L_, H, 2, ch, heads_[mi].stride()));
+      steps_.push_back(mlp::fwd_groups(A, H, W, B, L_, H, 4, ch, heads_[0].stride(), nullptr, 0));
     }
-  };
+  }
 
-  critic_fwd(true);
-  critic_fwd(false);
   // ------------------------------------------- TD target + loss + upstream
   if (dist_) {
     c51::CriticLossArgs a{};
