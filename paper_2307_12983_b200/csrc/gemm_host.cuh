@@ -2,6 +2,8 @@
 // launcher that sizes the grid (m tiles x n tiles x splits*groups).
 #pragma once
 
+#include <cstdlib>
+
 #include "common.h"
 #include "gemm_tf32.cuh"
 
@@ -46,21 +48,74 @@ inline int sm_count() {
   return n;
 }
 
-// Persistent launch: min(tiles, SMs) CTAs, one per SM, walking the tiles.
-template <int BN, bool kAMN, bool kBMN, class Epi>
-void launch(const Operands& ops, Problem p, int groups, const Epi& epi, cudaStream_t st) {
-  using L = SmemLayout<BN, Epi>;
-  auto kern = gemm_tf32_kernel<BN, kAMN, kBMN, Epi>;
+// CTA pairs (cta_group::2) for wide tiles when the m-tiles pair up evenly;
+// PQLG_PAIR=0 keeps one CTA per tile (A/B switch).
+inline bool pair_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PQLG_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <int BN>
+inline bool use_pair(int M) {
+  return BN >= 128 && ((M + kBM - 1) / kBM) % 2 == 0 && pair_enabled();
+}
+// Box of a K-major B operand: a pair's CTA stages half of the BN columns.
+template <int BN>
+inline int b_box(int M) {
+  return use_pair<BN>(M) ? BN / 2 : BN;
+}
+
+template <int BN, bool kAMN, bool kBMN, class Epi, bool kPair>
+void launch_impl(const Operands& ops, Problem p, int groups, const Epi& epi, cudaStream_t st) {
+  using L = SmemLayout<BN, Epi, kPair>;
+  auto kern = gemm_tf32_kernel<BN, kAMN, kBMN, Epi, kPair>;
   static bool configured = false;
   if (!configured) {
     PQLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    L::kDynamic));
+    if (kPair)
+      PQLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
     configured = true;
   }
   p.groups = groups;
   const int tiles = ((p.M + kBM - 1) / kBM) * ((p.N + BN - 1) / BN) * p.splits * groups;
-  const int grid = tiles < sm_count() ? tiles : sm_count();
-  ::pqlg::launch(kern, dim3(grid), dim3(L::kThreads), L::kDynamic, st, ops, p, epi);
+  int grid = tiles < sm_count() ? tiles : sm_count();
+  if (kPair) grid &= ~1;  // whole clusters of 2 (tiles are even here)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(L::kThreads);
+  cfg.dynamicSmemBytes = L::kDynamic;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  int na = 1;
+  if (kPair) {
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    na = 2;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  const bool prof = profiling_active();
+  if (prof) profile_before(st, reinterpret_cast<const void*>(kern));
+  PQLG_CUDA(cudaLaunchKernelEx(&cfg, kern, ops, p, epi));
+  count_launch();
+  if (prof) profile_after(st);
+}
+
+// Persistent launch: min(tiles, SMs) CTAs, one per SM, walking the tiles
+// (or, for CTA pairs, clusters of 2 walking m-tile pairs).
+template <int BN, bool kAMN, bool kBMN, class Epi>
+void launch(const Operands& ops, Problem p, int groups, const Epi& epi, cudaStream_t st) {
+  if constexpr (BN >= 128) {
+    if (use_pair<BN>(p.M)) return launch_impl<BN, kAMN, kBMN, Epi, true>(ops, p, groups, epi, st);
+  }
+  launch_impl<BN, kAMN, kBMN, Epi, false>(ops, p, groups, epi, st);
 }
 
 }  // namespace pqlg::gemm

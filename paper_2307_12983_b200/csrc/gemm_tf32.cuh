@@ -90,12 +90,17 @@ constexpr int epi_warps() {
   return (BN >= 128 && Epi::kSplitCols) ? 8 : 4;
 }
 
-template <int BN, class Epi>
+// kPair: the tile is computed by a CTA pair (cluster of 2, tcgen05
+// cta_group::2, UMMA M = 256): each CTA stages its own 128 A rows and half of
+// the BN B columns, so per-CTA operand traffic drops from (128 + BN) to
+// (128 + BN/2) rows per k-step -- the hidden-layer GEMMs are L2-bandwidth
+// bound at 1 CTA per tile.
+template <int BN, class Epi, bool kPair = false>
 struct SmemLayout {
   static constexpr int kEpiWarps = epi_warps<BN, Epi>();
   static constexpr int kThreads = 64 + 32 * kEpiWarps;
   static constexpr int kABytes = kBM * kBK * 4;  // 16 KB
-  static constexpr int kBBytes = BN * kBK * 4;
+  static constexpr int kBBytes = (kPair ? BN / 2 : BN) * kBK * 4;
   static constexpr int kStageBytes = kABytes + kBBytes;
   // one 4 KB (32 x 32 fp32, 128B-swizzled) TMA-store staging buffer per warp
   static constexpr int kStagingBytes = Epi::kStoreRank > 0 ? kEpiWarps * 4096 : 0;
@@ -148,9 +153,9 @@ constexpr uint32_t k_step_bytes() {
   return kMN ? kUmmaK * 128 : kUmmaK * 4;
 }
 
-template <int BN, bool kAMN, bool kBMN>
+template <int BN, bool kAMN, bool kBMN, bool kPair = false>
 constexpr uint32_t make_idesc() {
-  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N");
   uint32_t d = 0;
   d |= 1u << 4;                      // D format f32
   d |= 2u << 7;                      // A format tf32
@@ -158,7 +163,7 @@ constexpr uint32_t make_idesc() {
   d |= (kAMN ? 1u : 0u) << 15;       // A major
   d |= (kBMN ? 1u : 0u) << 16;       // B major
   d |= static_cast<uint32_t>(BN >> 3) << 17;
-  d |= static_cast<uint32_t>(kBM >> 4) << 24;
+  d |= static_cast<uint32_t>((kPair ? 2 * kBM : kBM) >> 4) << 24;
   return d;
 }
 
@@ -208,10 +213,10 @@ __device__ __forceinline__ TileCoord tile_coord(int t, const Problem& p, int til
   return c;
 }
 
-template <int BN, bool kAMN, bool kBMN, class Epi>
-__global__ void __launch_bounds__(SmemLayout<BN, Epi>::kThreads, 1)
+template <int BN, bool kAMN, bool kBMN, class Epi, bool kPair = false>
+__global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair>::kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ Operands ops, const Problem prob, const Epi epi) {
-  using L = SmemLayout<BN, Epi>;
+  using L = SmemLayout<BN, Epi, kPair>;
   constexpr int kStages = L::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -226,7 +231,18 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi>::kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int tiles_m = (prob.M + kBM - 1) / kBM;
   const int tiles_n = (prob.N + BN - 1) / BN;
-  const int n_tiles_total = tiles_m * tiles_n * prob.splits * prob.groups;
+  // Work units: tiles (1 CTA each) or, paired, m-tile pairs (cluster of 2).
+  const uint32_t rank = kPair ? ptx::cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int unit_m = kPair ? tiles_m / 2 : tiles_m;
+  const int n_units = unit_m * tiles_n * prob.splits * prob.groups;
+  const int unit0 = kPair ? static_cast<int>(ptx::cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int unit_step = kPair ? static_cast<int>(ptx::nclusters_x()) : static_cast<int>(gridDim.x);
+  auto coord = [&](int u) {
+    TileCoord c = tile_coord(u, prob, unit_m, tiles_n);
+    if constexpr (kPair) c.m_tile = 2 * c.m_tile + static_cast<int>(rank);
+    return c;
+  };
 
   if (warp == 0 && ptx::elect_one()) {
     for (int g = 0; g < prob.groups; ++g) {
@@ -239,13 +255,18 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi>::kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tmem_full[a], 1);
-      ptx::mbar_init(&tmem_empty[a], L::kEpiWarps);
+      // the leader's MMA waits for both CTAs' epilogues to drain a buffer
+      ptx::mbar_init(&tmem_empty[a], L::kEpiWarps * (kPair ? 2 : 1));
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc<L::kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (kPair) ptx::tmem_alloc_pair<L::kTmemCols>(tmem_slot);
+    else ptx::tmem_alloc<L::kTmemCols>(tmem_slot);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) ptx::cluster_sync();  // barrier inits + TMEM visible to the peer
+  else __syncthreads();
   ptx::tc_fence_after();
   // everything above overlapped the previous kernel's tail (PDL)
   pdl::entry();
@@ -269,50 +290,71 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi>::kThreads, 1)
 
   if (warp == 0) {
     if (ptx::elect_one()) {
+      constexpr int kBCols = kPair ? BN / 2 : BN;  // B columns staged by this CTA
       uint32_t it = 0;
-      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
-        const TileCoord tc = tile_coord(t, prob, tiles_m, tiles_n);
+      for (int u = unit0; u < n_units; u += unit_step) {
+        const TileCoord tc = coord(u);
         int kt0, nkt;
         k_range(tc.split, kt0, nkt);
         const int m0 = tc.m_tile * kBM;
-        const int n0 = tc.n_tile * BN;
+        const int n0 = tc.n_tile * BN + static_cast<int>(rank) * kBCols;
         for (int i = 0; i < nkt; ++i, ++it) {
           const int s = it % kStages;
           const uint32_t ph = (it / kStages) & 1;
           ptx::mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
-          ptx::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
           const int k0 = (kt0 + i) * kBK;
-          if constexpr (kAMN) {
+          if constexpr (kPair) {
+            // both CTAs' bytes complete on the leader's full barrier
+            if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * L::kStageBytes);
+            const uint32_t fb = ptx::mapa(&full[s], 0);
+            if constexpr (kAMN) {
 #pragma unroll
-            for (int j = 0; j < kBM / 32; ++j)
-              ptx::tma_load_2d(&ops.a[tc.group], &full[s], sa + j * (32 * kBK * 4), m0 + 32 * j,
-                               k0);
-          } else {
-            ptx::tma_load_2d(&ops.a[tc.group], &full[s], sa, k0, m0);
-          }
-          if constexpr (kBMN) {
+              for (int j = 0; j < kBM / 32; ++j)
+                ptx::tma_load_2d_pair(&ops.a[tc.group], fb, sa + j * (32 * kBK * 4), m0 + 32 * j, k0);
+            } else {
+              ptx::tma_load_2d_pair(&ops.a[tc.group], fb, sa, k0, m0);
+            }
+            if constexpr (kBMN) {
 #pragma unroll
-            for (int j = 0; j < BN / 32; ++j)
-              ptx::tma_load_2d(&ops.b[tc.group], &full[s], sb + j * (32 * kBK * 4), n0 + 32 * j,
-                               k0);
+              for (int j = 0; j < kBCols / 32; ++j)
+                ptx::tma_load_2d_pair(&ops.b[tc.group], fb, sb + j * (32 * kBK * 4), n0 + 32 * j, k0);
+            } else {
+              ptx::tma_load_2d_pair(&ops.b[tc.group], fb, sb, k0, n0);
+            }
           } else {
-            ptx::tma_load_2d(&ops.b[tc.group], &full[s], sb, k0, n0);
+            ptx::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
+            if constexpr (kAMN) {
+#pragma unroll
+              for (int j = 0; j < kBM / 32; ++j)
+                ptx::tma_load_2d(&ops.a[tc.group], &full[s], sa + j * (32 * kBK * 4), m0 + 32 * j,
+                                 k0);
+            } else {
+              ptx::tma_load_2d(&ops.a[tc.group], &full[s], sa, k0, m0);
+            }
+            if constexpr (kBMN) {
+#pragma unroll
+              for (int j = 0; j < BN / 32; ++j)
+                ptx::tma_load_2d(&ops.b[tc.group], &full[s], sb + j * (32 * kBK * 4), n0 + 32 * j,
+                                 k0);
+            } else {
+              ptx::tma_load_2d(&ops.b[tc.group], &full[s], sb, k0, n0);
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = make_idesc<BN, kAMN, kBMN>();
-    if (ptx::elect_one()) {
+    constexpr uint32_t idesc = make_idesc<BN, kAMN, kBMN, kPair>();
+    if (leader && ptx::elect_one()) {
       uint32_t it = 0, lt = 0;
-      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++lt) {
-        const TileCoord tc = tile_coord(t, prob, tiles_m, tiles_n);
+      for (int u = unit0; u < n_units; u += unit_step, ++lt) {
+        const TileCoord tc = coord(u);
         int kt0, nkt;
         k_range(tc.split, kt0, nkt);
         const uint32_t a = lt & 1;
-        ptx::mbar_wait(&tmem_empty[a], ((lt >> 1) & 1) ^ 1);  // epilogue drained this buffer
+        ptx::mbar_wait(&tmem_empty[a], ((lt >> 1) & 1) ^ 1);  // epilogue(s) drained this buffer
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + a * BN;
         for (int i = 0; i < nkt; ++i, ++it) {
@@ -329,11 +371,14 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi>::kThreads, 1)
           for (int j = 0; j < kBK / kUmmaK; ++j) {
             const uint64_t ad = operand_desc<kAMN>(sa + j * k_step_bytes<kAMN>());
             const uint64_t bd = operand_desc<kBMN>(sb + j * k_step_bytes<kBMN>());
-            ptx::mma_tf32(d_tmem, ad, bd, idesc, (i > 0 || j > 0) ? 1u : 0u);
+            if constexpr (kPair) ptx::mma_tf32_pair(d_tmem, ad, bd, idesc, (i > 0 || j > 0) ? 1u : 0u);
+            else ptx::mma_tf32(d_tmem, ad, bd, idesc, (i > 0 || j > 0) ? 1u : 0u);
           }
-          ptx::mma_commit(&empty[s]);
+          if constexpr (kPair) ptx::mma_commit_pair(&empty[s]);
+          else ptx::mma_commit(&empty[s]);
         }
-        ptx::mma_commit(&tmem_full[a]);
+        if constexpr (kPair) ptx::mma_commit_pair(&tmem_full[a]);
+        else ptx::mma_commit(&tmem_full[a]);
       }
 #ifdef PQLG_GEMM_TRACE
       PQLG_TRACE(3, clock64());
@@ -357,8 +402,8 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi>::kThreads, 1)
     uint8_t* stage = smem + L::kStagingOffset + ew * 4096;
     uint32_t nstore = 0;
     uint32_t lt = 0;
-    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++lt) {
-      const TileCoord tc = tile_coord(t, prob, tiles_m, tiles_n);
+    for (int u = unit0; u < n_units; u += unit_step, ++lt) {
+      const TileCoord tc = coord(u);
       ctx.group = tc.group;
       ctx.split = tc.split;
       ctx.n_tile = tc.n_tile;
@@ -384,7 +429,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi>::kThreads, 1)
         ptx::tmem_ld_wait();
         float v[32];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) v[u] = __uint_as_float(r[u]);
+        for (int uu = 0; uu < 32; ++uu) v[uu] = __uint_as_float(r[uu]);
         // next chunk's TMEM load overlaps this chunk's math and stores
         if (c + 1 < c_begin + kChunksPerWarp) ptx::tmem_ld32(t_addr + (c + 1) * 32, r);
         const int n0 = tc.n_tile * BN + c * 32;
@@ -417,7 +462,10 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi>::kThreads, 1)
       // every tcgen05.ld of this warp has completed: release the accumulator
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tmem_empty[a]);
+      if (lane == 0) {
+        if constexpr (kPair) ptx::mbar_arrive_cluster(ptx::mapa(&tmem_empty[a], 0));
+        else ptx::mbar_arrive(&tmem_empty[a]);
+      }
       epi.end(row, ctx);
     }
     if constexpr (Epi::kStoreRank > 0) {
@@ -433,10 +481,12 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi>::kThreads, 1)
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) ptx::cluster_sync();  // no remote arrive may target an exited CTA
+  else __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<L::kTmemCols>(tmem_base);
+    if constexpr (kPair) ptx::tmem_dealloc_pair<L::kTmemCols>(tmem_base);
+    else ptx::tmem_dealloc<L::kTmemCols>(tmem_base);
   }
 }
 

@@ -30,7 +30,7 @@ void run(const float* A, const float* B, float* D, const float* bias, int M, int
          int lda, int ldb, int ldd, int relu, int splits, bool tf32, cudaStream_t st) {
   gemm::Operands ops;
   ops.a[0] = ops.a[1] = gemm::map_a(A, M, K, lda, AMN, tf32);
-  ops.b[0] = ops.b[1] = gemm::map_b(B, N, K, ldb, BMN, BN, tf32);
+  ops.b[0] = ops.b[1] = gemm::map_b(B, N, K, ldb, BMN, BMN ? BN : gemm::b_box<BN>(M), tf32);
   gemm::Problem p = gemm::make_problem(M, N, K, splits);
   if (p.splits == 1) {
     ops.d[0] = ops.d[1] = make_store_map(D, M, N, ldd);

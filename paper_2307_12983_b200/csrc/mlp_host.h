@@ -122,8 +122,9 @@ Step dgrad(const float* G0, const float* G1, int64_t ldg, const float* W0, const
     gemm::Operands ops;
     ops.a[0] = gemm::map_a(G0, M, N_out, ldg, false, true);
     ops.a[1] = groups > 1 ? gemm::map_a(G1, M, N_out, ldg, false, true) : ops.a[0];
-    ops.b[0] = gemm::map_b(W0, N_in, N_out, ldw, false, BN, true);
-    ops.b[1] = groups > 1 ? gemm::map_b(W1, N_in, N_out, ldw, false, BN, true) : ops.b[0];
+    const int box = gemm::b_box<BN>(M);  // K-major B: a CTA pair splits the columns
+    ops.b[0] = gemm::map_b(W0, N_in, N_out, ldw, false, box, true);
+    ops.b[1] = groups > 1 ? gemm::map_b(W1, N_in, N_out, ldw, false, box, true) : ops.b[0];
     set_out(ops, D0, D1, M, N_in, ldd, groups);
     const gemm::Problem p = gemm::make_problem(M, N_in, N_out, 1);
     step = [ops, p, groups, epi](cudaStream_t st) {

@@ -18,18 +18,18 @@ extern "C" __attribute__((visibility("default"))) int trace_gemm(
     gemm::Operands ops;
     const gemm::Problem p = gemm::make_problem(M, N, K, 1);
     if (kind == 0) {
-      ops.a[0] = ops.a[1] = gemm::map_a(A, M, K, K, false, true);
-      ops.b[0] = ops.b[1] = gemm::map_b(B, N, K, N, true, 256, true);
-      ops.d[0] = ops.d[1] = make_store_map(D, M, N, N);
+      ops.a[0] = ops.a[1] = ops.a[2] = ops.a[3] = gemm::map_a(A, M, K, K, false, true);
+      ops.b[0] = ops.b[1] = ops.b[2] = ops.b[3] = gemm::map_b(B, N, K, N, true, 256, true);
+      ops.d[0] = ops.d[1] = ops.d[2] = ops.d[3] = make_store_map(D, M, N, N);
       epi::Hidden e{};
-      e.bias[0] = e.bias[1] = bias;
+      e.bias[0] = e.bias[1] = e.bias[2] = e.bias[3] = bias;
       e.bn = 256;
       e.M = M;
       e.N = N;
-      e.store = store;
+      e.store = store ? 0xF : 0;
       for (int i = 0; i < iters; ++i) gemm::launch<256, false, true>(ops, p, groups, e, st);
     } else {
-      ops.a[0] = ops.a[1] = gemm::map_a(A, M, K, K, false, true);
+      ops.a[0] = ops.a[1] = ops.a[2] = ops.a[3] = gemm::map_a(A, M, K, K, false, true);
       ops.b[0] = ops.b[1] = gemm::map_b(B, N, K, N, true, 32, true);
       epi::PolicyHead e{};
       e.bias = bias;

@@ -27,8 +27,9 @@ st = torch.cuda.Stream()
 import os
 STORE = int(os.environ.get("TRACE_STORE", "1"))
 KIND = int(os.environ.get("TRACE_KIND", "0"))
-shapes = ([(8192, 512, 512, 1), (8192, 512, 512, 2), (8192, 512, 232, 2), (16384, 512, 512, 1),
-           (8192, 512, 4096, 1)] if KIND == 0 else [(8192, 20, 512, 1), (16384, 20, 512, 1)])
+shapes = ([(8192, 512, 512, 1), (8192, 512, 512, 2), (8192, 512, 512, 4), (8192, 512, 232, 4),
+           (16384, 512, 512, 1), (8192, 512, 4096, 1)] if KIND == 0
+          else [(8192, 20, 512, 1), (16384, 20, 512, 1)])
 for (M, N, K, groups) in shapes:
     a = torch.randn(M, K, device="cuda"); w = torch.randn(K, (N + 3) // 4 * 4, device="cuda")
     d = torch.empty(M, N, device="cuda"); bias = torch.zeros(N, device="cuda")
