@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", choices=sorted(CONFIGS), default="c3")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--force-dp", action="store_true",
+                   help="use the data-parallel (NCCL) learners even at N=1 (path check)")
     return p.parse_args()
 
 
@@ -191,7 +193,7 @@ def run_ours(args, rank, world, local):
     dims = _lib.TaskDims(D, A, -1.0, 1.0)
     h = C.c_void_p()
     comm = None
-    if world > 1:
+    if world > 1 or args.force_dp:
         # data-parallel critic (SURVEY 8(e) option i): one NCCL all-reduce of
         # the twin-critic gradients + loss per update; every rank samples its
         # own replay shard with its own Philox stream; same init everywhere
@@ -308,7 +310,7 @@ def run_c51(args, rank, world, local, steps, warmup):
                               hidden=H, hidden_layers=nh, n_envs=N, seed=0)
     dims = _lib.TaskDims(D, A, -1.0, 1.0)
     vl, pl = C.c_void_p(), C.c_void_p()
-    comm = _lib.comm_from_torch_dist(rank, world) if world > 1 else None
+    comm = _lib.comm_from_torch_dist(rank, world) if (world > 1 or args.force_dp) else None
     if comm is not None:
         _lib.call("pqlg_vlearner_create_dp", C.byref(cfg), C.byref(dims), 1, comm, sp, C.byref(vl))
         _lib.call("pqlg_plearner_create_dp", C.byref(cfg), C.byref(dims), 1, comm, sp, C.byref(pl))
@@ -424,7 +426,7 @@ def run_policy(args, rank, world, local, steps, warmup):
     dims = _lib.TaskDims(D, A, -1.0, 1.0)
     pl = C.c_void_p()
     comm = None
-    if world > 1:  # data-parallel policy update (one all-reduce per update)
+    if world > 1 or args.force_dp:  # data-parallel policy update (one all-reduce per update)
         comm = _lib.comm_from_torch_dist(rank, world)
         _lib.call("pqlg_plearner_create_dp", C.byref(cfg), C.byref(dims), 1, comm,
                   C.c_void_p(stream.cuda_stream), C.byref(pl))

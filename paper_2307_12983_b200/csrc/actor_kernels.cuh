@@ -126,20 +126,32 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
   const int A4 = (A + 3) >> 2;
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int i0 = tile * kEnvTile;
-    // ---- phase 1
-    for (int j = w; j < kEnvTile && i0 + j < e.N; j += kEnvWarps) {
-      const int i = i0 + j;
+    // ---- phase 1 (all of this warp's env rows are loaded before any math)
+    constexpr int kPer = kEnvTile / kEnvWarps;
+    float sdp[kPer][kNch], up[kPer];
+#pragma unroll
+    for (int p = 0; p < kPer; ++p) {
+      const int i = i0 + w + p * kEnvWarps;
+      const bool ok = i < e.N;
       const float* s = e.s_in + static_cast<int64_t>(i) * e.ld_in;
-      float sd[kNch];
 #pragma unroll
       for (int c = 0; c < kNch; ++c) {
         const int d = lane + 32 * c;
-        sd[c] = d < D ? s[d] : 0.0f;
+        sdp[p][c] = (ok && d < D) ? s[d] : 0.0f;
       }
+      up[p] = (ok && lane < A) ? act[static_cast<int64_t>(i) * ld_act + lane] : 0.0f;
+    }
+#pragma unroll
+    for (int p = 0; p < kPer; ++p) {
+      const int j = w + p * kEnvWarps;
+      if (i0 + j >= e.N) break;
+      float sd[kNch];
+#pragma unroll
+      for (int c = 0; c < kNch; ++c) sd[c] = sdp[p][c];
       float u = 0.0f;
       bool bad = false;
       if (lane < A) {
-        u = act[static_cast<int64_t>(i) * ld_act + lane];
+        u = up[p];
         bad = !isfinite(u);
         u = u < e.low ? e.low : (u > e.high ? e.high : u);
       }
@@ -230,19 +242,26 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
     }
     __syncthreads();
     // ---- phase 3
+    float nm[kNch], ni[kNch];  // this lane's normalisation constants (d = lane + 32c)
+#pragma unroll
+    for (int c = 0; c < kNch; ++c) {
+      const int d = lane + 32 * c;
+      nm[c] = (nn.out && !id && d < D) ? nn.mean[d] : 0.0f;
+      ni[c] = (nn.out && !id && d < D) ? nn.inv[d] : 1.0f;
+    }
     for (int j = w; j < kEnvTile && i0 + j < e.N; j += kEnvWarps) {
       const int i = i0 + j;
       float* s = e.s ? e.s + static_cast<int64_t>(i) * e.ld : nullptr;
       float* nxt = o.next_obs + static_cast<int64_t>(i) * o.ld_obs;
       float* bt = o.boot + static_cast<int64_t>(i) * o.ld_obs;
       float* xn = nn.out ? nn.out + static_cast<int64_t>(i) * nn.ld_out : nullptr;
-      auto emit = [&](int d, float ns) {
+      auto emit = [&](int d, int c, float ns) {
         if (s) s[d] = ns;
         nxt[d] = ns;
         if (xn) {
           float z = ns;
           if (!id) {
-            z = __fmul_rn(__fsub_rn(ns, nn.mean[d]), nn.inv[d]);
+            z = __fmul_rn(__fsub_rn(ns, nm[c]), ni[c]);
             if (z > 5.0f) z = 5.0f;
             if (z < -5.0f) z = -5.0f;
           }
@@ -251,17 +270,25 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
       };
       if (sdone[j]) {  // warp-uniform: terminal obs to boot, fresh reset draws
         const uint64_t st0 = e.rng[i];
-        for (int d = lane; d < D; d += 32) {
-          bt[d] = sv[j * ldv + d];
-          uint64_t st = st0 + static_cast<uint64_t>(d);  // draw d of the reset sequence
-          emit(d, rng::env_uniform(st, -1.0f, 1.0f));
+#pragma unroll
+        for (int c = 0; c < kNch; ++c) {
+          const int d = lane + 32 * c;
+          if (d < D) {
+            bt[d] = sv[j * ldv + d];
+            uint64_t st = st0 + static_cast<uint64_t>(d);  // draw d of the reset sequence
+            emit(d, c, rng::env_uniform(st, -1.0f, 1.0f));
+          }
         }
         if (lane == 0) e.rng[i] = st0 + static_cast<uint64_t>(D);
       } else {
-        for (int d = lane; d < D; d += 32) {
-          const float v = sv[j * ldv + d];
-          bt[d] = v;
-          emit(d, v);
+#pragma unroll
+        for (int c = 0; c < kNch; ++c) {
+          const int d = lane + 32 * c;
+          if (d < D) {
+            const float v = sv[j * ldv + d];
+            bt[d] = v;
+            emit(d, c, v);
+          }
         }
       }
     }
@@ -382,7 +409,7 @@ static __global__ void __launch_bounds__(256)
     partial[(static_cast<int64_t>(g) * D + c) * 2 + 1] = b;
   }
   __shared__ bool last;
-  __threadfence();
+  if (w == 0) __threadfence();  // only warp 0 wrote partials
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(&ticket[1 + blockIdx.x], 1u) == gridDim.y - 1;
   __syncthreads();

@@ -99,6 +99,26 @@ __device__ __forceinline__ void copy_row(float* __restrict__ dst, const float* _
   }
 }
 
+// A padded row of up to 256 floats held by one warp: 2 float4 per lane.
+struct WarpRow {
+  float4 v[2];
+};
+__device__ __forceinline__ WarpRow load_row(const float* __restrict__ src, int n, int lane) {
+  const int n4 = (n + 3) >> 2;
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  WarpRow r;
+  r.v[0] = lane < n4 ? s4[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+  r.v[1] = lane + 32 < n4 ? s4[lane + 32] : make_float4(0.f, 0.f, 0.f, 0.f);
+  return r;
+}
+__device__ __forceinline__ void store_row(float* __restrict__ dst, const WarpRow& r, int n,
+                                          int lane) {
+  const int n4 = (n + 3) >> 2;
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  if (lane < n4) d4[lane] = r.v[0];
+  if (lane + 32 < n4) d4[lane + 32] = r.v[1];
+}
+
 __device__ __forceinline__ bool aligned16(const void* p, int64_t ld) {
   return ((reinterpret_cast<uintptr_t>(p) & 15) == 0) && ((ld & 3) == 0);
 }
@@ -201,10 +221,37 @@ static __global__ void nstep_emit_kernel(Window w, Slice s, float reward_scale, 
   const uint32_t slot = (h + c) % n;
   const float new_rew = __fmul_rn(rew_e, reward_scale);
   if (lane == static_cast<int>(slot)) my_rew = new_rew;
+  // Common case (padded rows, D <= 256, A <= 128): every row this env moves
+  // -- the new obs/act, the window front (the first emitted record's
+  // obs/act) and the boot obs -- is loaded before anything is stored, so
+  // the warp pays one memory round trip instead of one per row.
+  const bool fast = wide_o && wide_a && D <= 256 && A <= 128;
+  const bool will_emit = (c + 1 == static_cast<uint32_t>(n)) || done;
+  bool first_preloaded = false;
+  WarpRow fo{}, fa{}, bo{};
   {
     const size_t wrow = static_cast<size_t>(e) * n + slot;
-    copy_row(w.obs + wrow * w.ld_obs, s.obs + static_cast<size_t>(e) * s.ld_obs, D, wide_o, lane);
-    copy_row(w.act + wrow * w.ld_act, s.act + static_cast<size_t>(e) * s.ld_act, A, wide_a, lane);
+    if (fast) {
+      const WarpRow no = load_row(s.obs + static_cast<size_t>(e) * s.ld_obs, D, lane);
+      const WarpRow na = load_row(s.act + static_cast<size_t>(e) * s.ld_act, A, lane);
+      if (will_emit) {
+        const size_t front = static_cast<size_t>(e) * n + h;
+        bo = load_row(s.boot + static_cast<size_t>(e) * s.ld_obs, D, lane);
+        if (front == wrow) {  // empty window: the front is the record pushed now
+          fo = no;
+          fa = na;
+        } else {
+          fo = load_row(w.obs + front * w.ld_obs, D, lane);
+          fa = load_row(w.act + front * w.ld_act, A, lane);
+        }
+        first_preloaded = true;
+      }
+      store_row(w.obs + wrow * w.ld_obs, no, D, lane);
+      store_row(w.act + wrow * w.ld_act, na, A, lane);
+    } else {
+      copy_row(w.obs + wrow * w.ld_obs, s.obs + static_cast<size_t>(e) * s.ld_obs, D, wide_o, lane);
+      copy_row(w.act + wrow * w.ld_act, s.act + static_cast<size_t>(e) * s.ld_act, A, wide_a, lane);
+    }
     if (lane == 0) w.rew[wrow] = new_rew;
   }
   __syncwarp();
@@ -212,6 +259,8 @@ static __global__ void nstep_emit_kernel(Window w, Slice s, float reward_scale, 
 
   uint32_t j = 0;
   auto emit = [&](uint32_t m, bool terminated) {
+    const bool use_pre = first_preloaded;  // only the step's first record was preloaded
+    first_preloaded = false;
     float g = 0.0f, disc = 1.0f;
     for (uint32_t k = 0; k < m; ++k) {
       const float r = __shfl_sync(0xffffffffu, my_rew, static_cast<int>((h + k) % n));
@@ -223,11 +272,17 @@ static __global__ void nstep_emit_kernel(Window w, Slice s, float reward_scale, 
     if (rec + ring.capacity < total) return;
     const uint64_t p = (cursor0 + rec) % ring.capacity;
     const size_t front = static_cast<size_t>(e) * n + h;
-    // window and ring rows are padded to 16 bytes by construction
-    copy_row(ring.obs + p * ring.ld_obs, w.obs + front * w.ld_obs, D, true, lane);
-    copy_row(ring.act + p * ring.ld_act, w.act + front * w.ld_act, A, true, lane);
-    copy_row(ring.boot + p * ring.ld_obs, s.boot + static_cast<size_t>(e) * s.ld_obs, D, wide_o,
-             lane);
+    if (use_pre) {  // rows loaded up front (first record of the step)
+      store_row(ring.obs + p * ring.ld_obs, fo, D, lane);
+      store_row(ring.act + p * ring.ld_act, fa, A, lane);
+      store_row(ring.boot + p * ring.ld_obs, bo, D, lane);
+    } else {
+      // window and ring rows are padded to 16 bytes by construction
+      copy_row(ring.obs + p * ring.ld_obs, w.obs + front * w.ld_obs, D, true, lane);
+      copy_row(ring.act + p * ring.ld_act, w.act + front * w.ld_act, A, true, lane);
+      copy_row(ring.boot + p * ring.ld_obs, s.boot + static_cast<size_t>(e) * s.ld_obs, D, wide_o,
+               lane);
+    }
     if (lane == 0) {
       ring.ret[p] = g;
       ring.eff[p] = terminated ? 0.0f : disc;
