@@ -77,6 +77,13 @@ PQLG_API int pqlg_k_gemm_tf32_repeat(const float* A_dev, const float* B_dev, flo
                                      const float* bias_dev, int M, int N, int K, int lda, int ldb,
                                      int ldd, int relu, int iters, void* stream);
 
+/* `iters` launches of the update's dominant GEMM: `groups` (<= 4) hidden
+ * layers [M x K] x [K x N] in one persistent launch (Hidden epilogue: bias +
+ * ReLU + TMA store), as the twin target + twin online critics run. */
+PQLG_API int pqlg_k_gemm_tf32_repeat_groups(const float* A_dev, const float* B_dev, float* D_dev,
+                                            const float* bias_dev, int M, int N, int K, int lda,
+                                            int ldb, int ldd, int groups, int iters, void* stream);
+
 /* ------------------------------------------------------------ data views */
 
 /* StepSlice (proj/include/pql/runtime/messages.hpp:31-35) as device views.

@@ -112,6 +112,8 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_replay_fill_synthetic": (i32, [vp, u64, u64, f32, C.c_uint32]),
     "pqlg_k_gemm_tf32_repeat": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32,
                                       vp]),
+    "pqlg_k_gemm_tf32_repeat_groups": (i32, [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32,
+                                             i32, vp]),
     "pqlg_plearner_create": (i32, [P(Config), P(TaskDims), u64, vp, P(vp)]),
     "pqlg_plearner_create_dp": (i32, [P(Config), P(TaskDims), u64, vp, vp, P(vp)]),
     "pqlg_plearner_destroy": (i32, [vp]),

@@ -61,6 +61,29 @@ void run_repeat(const float* A, const float* B, float* D, const float* bias, int
   for (int i = 0; i < iters; ++i) gemm::launch<BN, false, true>(ops, p, 1, e, st);
 }
 
+// The update's dominant launch: `groups` independent hidden layers in one
+// persistent launch (the twin target + twin online critics, 4 groups), all
+// reading the same A / W and writing the same D (timing only).
+void run_repeat_groups(const float* A, const float* B, float* D, const float* bias, int M, int N,
+                       int K, int lda, int ldb, int ldd, int groups, int iters, cudaStream_t st) {
+  require(groups >= 1 && groups <= gemm::kMaxGroups, "repeat_groups: 1..4 groups");
+  require(N > 128, "repeat_groups: hidden-layer widths (N > 128)");
+  gemm::Operands ops;
+  for (int g = 0; g < gemm::kMaxGroups; ++g) {
+    ops.a[g] = gemm::map_a(A, M, K, lda, false, true);
+    ops.b[g] = gemm::map_b(B, N, K, ldb, true, 256, true);
+    ops.d[g] = make_store_map(D, M, N, ldd);
+  }
+  const gemm::Problem p = gemm::make_problem(M, N, K, 1);
+  epi::Hidden e{};
+  for (int g = 0; g < gemm::kMaxGroups; ++g) e.bias[g] = bias;
+  e.bn = 256;
+  e.M = M;
+  e.N = N;
+  e.store = 0xF;
+  for (int i = 0; i < iters; ++i) gemm::launch<256, false, true>(ops, p, groups, e, st);
+}
+
 template <int BN>
 void dispatch_major(int a_mn, int b_mn, const float* A, const float* B, float* D,
                     const float* bias, int M, int N, int K, int lda, int ldb, int ldd, int relu,
@@ -83,6 +106,16 @@ extern "C" int pqlg_k_gemm_tf32_repeat(const float* A, const float* B, float* D,
     else if (N > 64) pqlg::run_repeat<128>(A, B, D, bias, M, N, K, lda, ldb, ldd, relu, iters, st);
     else if (N > 32) pqlg::run_repeat<64>(A, B, D, bias, M, N, K, lda, ldb, ldd, relu, iters, st);
     else pqlg::run_repeat<32>(A, B, D, bias, M, N, K, lda, ldb, ldd, relu, iters, st);
+  });
+}
+
+extern "C" int pqlg_k_gemm_tf32_repeat_groups(const float* A, const float* B, float* D,
+                                              const float* bias, int M, int N, int K, int lda,
+                                              int ldb, int ldd, int groups, int iters,
+                                              void* stream) {
+  return pqlg::guarded([&] {
+    pqlg::run_repeat_groups(A, B, D, bias, M, N, K, lda, ldb, ldd, groups, iters,
+                            static_cast<cudaStream_t>(stream));
   });
 }
 

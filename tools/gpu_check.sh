@@ -35,6 +35,9 @@ if has full; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tf32_kernel -c 1 \
     -o gpurun_out/gemm_hidden_full -f python tools/prof_critic.py gemm > gpurun_out/ncu_full.log 2>&1
   ncu -i gpurun_out/gemm_hidden_full.ncu-rep --page raw --csv > gpurun_out/gemm_hidden_full_raw.csv 2>/dev/null
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tf32_kernel -c 1 \
+    -o gpurun_out/gemm4_full -f python tools/prof_critic.py gemm4 > gpurun_out/ncu_full4.log 2>&1
+  ncu -i gpurun_out/gemm4_full.ncu-rep --page raw --csv > gpurun_out/gemm4_full_raw.csv 2>/dev/null
   # and the critic update's finalize / adam kernels (HBM-bound)
   timeout 900 ncu --set full --clock-control none -k regex:"finalize_kernel|adam_polyak|replay_sample_kernel" -c 3 \
     -o gpurun_out/critic_hbm_full -f python tools/prof_critic.py critic > gpurun_out/ncu_full2.log 2>&1

@@ -12,6 +12,13 @@ from paper_2307_12983_b200 import _lib  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "both"
 st = torch.cuda.Stream()
+if which == "gemm4":  # the update's dominant launch: 4-group hidden layer
+    M, N, K = 8192, 512, 512
+    a = torch.randn(M, K, device="cuda"); b = torch.randn(K, N, device="cuda")
+    d = torch.empty(M, N, device="cuda"); bias = torch.zeros(N, device="cuda")
+    _lib.call("pqlg_k_gemm_tf32_repeat_groups", a.data_ptr(), b.data_ptr(), d.data_ptr(),
+              bias.data_ptr(), M, N, K, K, N, N, 4, 3, C.c_void_p(st.cuda_stream))
+    st.synchronize()
 if which in ("gemm", "both"):
     M, N, K = 8192, 512, 512
     a = torch.randn(M, K, device="cuda"); b = torch.randn(K, N, device="cuda")
