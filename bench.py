@@ -359,6 +359,32 @@ def run_c51(args, rank, world, local, steps, warmup):
     return out
 
 
+def run_pipeline(args, rank, world, local, actor_steps):
+    """run_parallel on this GPU: Actor, V-learner and
+    P-learner as three threads on three streams, RatioGate pacing at the
+    paper's beta_av = 1/8, beta_pv = 1/2 (Table B.1), c3 dims and nets.
+    Reports env steps/s and the learners' update rates over the run."""
+    from paper_2307_12983_b200 import _lib
+    D, A, H, nh, B, N, cap = CONFIGS[args.config]
+    cfg = _lib.default_config(batch_size=B, buffer_capacity=1_000_000, hidden=H, hidden_layers=nh,
+                              n_envs=N, seed=rank, env_offset=rank * N, envs_total=world * N)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    rc = _lib.ratio_config()
+    h = C.c_void_p()
+    _lib.call("pqlg_pipeline_create", C.byref(cfg), C.byref(dims), C.byref(rc), 1, C.byref(h))
+    rep = _lib.RunReport()
+    _lib.call("pqlg_pipeline_run", h, actor_steps, 120.0, C.byref(rep))
+    _lib.call("pqlg_pipeline_destroy", h)
+    return {"workload": f"run_parallel, {args.config} dims, {N} envs, H=4, K_pub=8, "
+                        f"beta_av=1/8, beta_pv=1/2, {actor_steps} actor steps incl. warm-up",
+            "env_steps_per_s": world * rep.env_steps / rep.wall_s,
+            "critic_updates_per_s": world * rep.c_v / rep.wall_s,
+            "policy_updates_per_s": world * rep.c_p / rep.wall_s,
+            "ratio_av": rep.ratio_av, "ratio_pv": rep.ratio_pv, "wall_s": rep.wall_s,
+            "batches_sent": rep.batches_sent, "seq_gaps": rep.seq_gaps,
+            "timing": "host wall clock over pqlg_pipeline_run (three concurrent streams)"}
+
+
 def run_actor(args, rank, world, local, steps, warmup):
     """Actor transitions/s: one ActorCore::rollout_step over N envs (normalize
     -> policy -> mixed noise -> synthetic env -> StepSlice -> normalizer
@@ -577,12 +603,14 @@ def main():
     actor = run_actor(args, rank, world, local, max(10, args.steps // 4), max(3, args.warmup // 4))
     policy = run_policy(args, rank, world, local, args.steps, args.warmup)
     c51 = run_c51(args, rank, world, local, max(10, args.steps // 2), max(3, args.warmup // 2))
+    pipe = run_pipeline(args, rank, world, local, 400)
     if rank != 0:
         return
     out = dict(base)
     out["actor"] = actor
     out["policy_updates"] = policy
     out["c51"] = c51
+    out["run_parallel"] = pipe
     out.update(value=r["value"], ms_per_step=r["ms_step"], e2e=r["e2e"], roofline=r["roof"],
                clocks=r["clocks"], gpu_launches=r["launches"],
                kernels_per_update=r["kpu"], last_loss=r["loss"])

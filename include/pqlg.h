@@ -359,6 +359,54 @@ PQLG_API int pqlg_actor_policy_version(pqlg_actor h, int64_t* out);
 PQLG_API int pqlg_actor_read(pqlg_actor h, int what, void* host_out);
 PQLG_API int pqlg_actor_kernels_per_step(pqlg_actor h, int* out);
 
+/* ------------------------------------------------ run_parallel (pipeline)
+ * The three PQL processes (Actor, V-learner, P-learner; SPEC.md:438-501,
+ * run.hpp:38) as three host threads on one GPU, each core on its own CUDA
+ * stream, paced by RatioGate's counter rule (ratio_gate.hpp:17-112) and
+ * exchanging device-resident data / snapshots through bounded channels and
+ * latest-wins slots (mailbox.hpp) with the actor as the hub. */
+typedef struct pqlg_pipeline_s* pqlg_pipeline;
+
+enum { PQLG_PROC_ACTOR = 0, PQLG_PROC_VLEARNER = 1, PQLG_PROC_PLEARNER = 2 };
+
+/* RatioConfig (ratio_gate.hpp:17-25) + the run_parallel design constants
+ * (SPEC.md:486-492): rollout horizon H, channel capacity, K_pub. */
+typedef struct {
+  double beta_av;       /* c_a / c_v target (1/8) */
+  double beta_pv;       /* c_p / c_v target (1/2) */
+  double slack_a, slack_p, slack_v;
+  int64_t warm_up;      /* rollout steps before any gating (32) */
+  int free_running;
+  int horizon;          /* rollout steps per actor iteration (4) */
+  int channel_capacity; /* batches in flight per channel (8) */
+  int publish_every;    /* learner updates per snapshot (8) */
+} pqlg_ratio_config;
+
+/* RunReport (run.hpp:11-31), the fields this pipeline produces. */
+typedef struct {
+  int ok;
+  int64_t c_a, c_v, c_p, env_steps;
+  double wall_s, ratio_av, ratio_pv;
+  int64_t batches_sent, batches_consumed_v, batches_consumed_p;
+  int64_t seq_duplicates, seq_gaps;
+  int64_t max_policy_staleness; /* publish intervals */
+  int64_t policy_version, critic_version;
+  float last_critic_loss, last_actor_loss;
+} pqlg_run_report;
+
+PQLG_API void pqlg_ratio_config_default(pqlg_ratio_config* cfg);
+/* RatioGate::may_proceed (ratio_gate.hpp:44-60): 1 proceed, 0 wait, -1 bad args. */
+PQLG_API int pqlg_ratio_may_proceed(int proc, int64_t c_a, int64_t c_v, int64_t c_p,
+                                    const pqlg_ratio_config* cfg);
+PQLG_API int pqlg_pipeline_create(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                                  const pqlg_ratio_config* ratio, uint64_t init_rng_seed,
+                                  pqlg_pipeline* out);
+/* Runs until c_a >= actor_steps or max_seconds elapsed; joins all threads.
+ * A non-finite update aborts the run with PQLG_ENONFINITE. Once per pipeline. */
+PQLG_API int pqlg_pipeline_run(pqlg_pipeline h, int64_t actor_steps, double max_seconds,
+                               pqlg_run_report* out);
+PQLG_API int pqlg_pipeline_destroy(pqlg_pipeline h);
+
 /* The synthetic EnvBatch on its own (vecenv.hpp:44-81 contract). */
 PQLG_API int pqlg_env_create(int n_envs, int obs_dim, int act_dim, uint64_t seed,
                              int max_episode_len, int env_offset, float low, float high,

@@ -59,6 +59,26 @@ class TaskDims(C.Structure):
     """pqlg_task_dims (learners.hpp:23-26)."""
     _fields_ = [("obs_dim", i32), ("act_dim", i32), ("low", f32), ("high", f32)]
 
+class RatioConfig(C.Structure):
+    """pqlg_ratio_config (RatioConfig, ratio_gate.hpp:17-25 + SPEC.md:486-492)."""
+    _fields_ = [("beta_av", C.c_double), ("beta_pv", C.c_double), ("slack_a", C.c_double),
+                ("slack_p", C.c_double), ("slack_v", C.c_double), ("warm_up", i64),
+                ("free_running", i32), ("horizon", i32), ("channel_capacity", i32),
+                ("publish_every", i32)]
+
+
+class RunReport(C.Structure):
+    """pqlg_run_report (RunReport, run.hpp:11-31)."""
+    _fields_ = [("ok", i32), ("c_a", i64), ("c_v", i64), ("c_p", i64), ("env_steps", i64),
+                ("wall_s", C.c_double), ("ratio_av", C.c_double), ("ratio_pv", C.c_double),
+                ("batches_sent", i64), ("batches_consumed_v", i64), ("batches_consumed_p", i64),
+                ("seq_duplicates", i64), ("seq_gaps", i64), ("max_policy_staleness", i64),
+                ("policy_version", i64), ("critic_version", i64),
+                ("last_critic_loss", f32), ("last_actor_loss", f32)]
+
+
+PROC_ACTOR, PROC_VLEARNER, PROC_PLEARNER = 0, 1, 2
+
 # name -> (restype, argtypes)
 SIGNATURES: dict[str, tuple] = {
     "pqlg_last_error": (C.c_char_p, []),
@@ -141,6 +161,11 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_actor_policy_version": (i32, [vp, P(i64)]),
     "pqlg_actor_read": (i32, [vp, i32, vp]),
     "pqlg_actor_kernels_per_step": (i32, [vp, P(i32)]),
+    "pqlg_ratio_config_default": (None, [P(RatioConfig)]),
+    "pqlg_ratio_may_proceed": (i32, [i32, i64, i64, i64, P(RatioConfig)]),
+    "pqlg_pipeline_create": (i32, [P(Config), P(TaskDims), P(RatioConfig), u64, P(vp)]),
+    "pqlg_pipeline_run": (i32, [vp, i64, C.c_double, P(RunReport)]),
+    "pqlg_pipeline_destroy": (i32, [vp]),
     "pqlg_env_create": (i32, [i32, i32, i32, u64, i32, i32, f32, f32, vp, P(vp)]),
     "pqlg_env_destroy": (i32, [vp]),
     "pqlg_env_reset_all": (i32, [vp, vp, i64]),
@@ -239,3 +264,11 @@ def comm_from_torch_dist(rank: int, world: int) -> C.c_void_p:
     comm = C.c_void_p()
     call("pqlg_comm_init", rank, world, ident, C.byref(comm))
     return comm
+
+
+def ratio_config(**overrides) -> RatioConfig:
+    rc = RatioConfig()
+    lib().pqlg_ratio_config_default(C.byref(rc))
+    for k, v in overrides.items():
+        setattr(rc, k, v)
+    return rc

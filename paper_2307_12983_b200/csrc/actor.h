@@ -1,0 +1,71 @@
+// ActorCore (learners.hpp:52-73, learners.cpp:62-116) on one B200: policy
+// inference with the mixed-noise head, the running normalizer and the
+// synthetic EnvBatch (actor.cu).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "mlp_host.h"
+#include "net.h"
+
+namespace pqlg {
+
+struct DeviceEnv;
+
+class Actor {
+ public:
+  Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st);
+  ~Actor();
+  void adopt_policy(const float* flat, int64_t version, bool device);
+  void rollout_step(pqlg_step_slice* out);
+  void rollout_n(int n);
+  void norm(int64_t* count, double* mean, double* m2);
+  void read_state(int what, void* out);
+  int64_t policy_version() const { return version_; }
+  cudaStream_t stream() const { return stream_; }
+  int kernels_per_step();
+  int n_envs() const { return N_; }
+  int obs_dim() const { return D_; }
+  int64_t param_count() const { return pnet_.params; }
+  // device views for the pipeline (run_parallel): the running normalizer
+  // (owned by the actor, SPEC "Normalizer statistics are owned by the Actor")
+  const float* policy_dev() const { return pol_.p; }
+  const int64_t* count_dev() const { return count_.p; }
+  const double* mean_dev() const { return mean_.p; }
+  const double* m2_dev() const { return m2_.p; }
+
+ private:
+  void build();
+  void enqueue(int cur);
+
+  pqlg_config cfg_;
+  pqlg_task_dims dims_;
+  cudaStream_t stream_;
+  cudaStream_t owned_stream_ = nullptr;
+  int N_, D_, A_, Ap_, H_, nh_;
+  int64_t Dp_;
+  NetShape pnet_;
+  int64_t version_ = 0;
+  int cur_ = 0;
+
+  std::unique_ptr<DeviceEnv> env_;
+  DevBuf<float> obs_[2], boot_, rew_, act_, Xn_;
+  DevBuf<uint8_t> term_, trunc_;
+  DevBuf<float> pol_;
+  WeightMirror head_;
+  std::vector<DevBuf<float>> pact_;
+  DevBuf<uint64_t> noise_rng_;
+  DevBuf<float> sigma_;
+  DevBuf<int64_t> count_;
+  DevBuf<double> mean_, m2_, npart_;
+  DevBuf<unsigned int> nticket_;
+  DevBuf<float> mean_f_, inv_f_;
+  DevBuf<int> identity_;
+  DevBuf<uint32_t> status_;
+  std::vector<mlp::Step> policy_steps_;
+  cudaGraphExec_t graph_[2] = {nullptr, nullptr};
+  int kps_ = 0;
+};
+
+}  // namespace pqlg

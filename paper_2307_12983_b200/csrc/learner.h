@@ -24,6 +24,15 @@ class VLearner {
 
   void adopt_policy(const float* flat_host, int64_t version);
   void adopt_norm(int64_t count, const double* mean, const double* m2);
+  // asynchronous device-pointer variants (the run_parallel pipeline)
+  void adopt_policy_device(const float* flat_dev, int64_t version);
+  void adopt_norm_device(const int64_t* count, const double* mean, const double* m2) {
+    norm_.set_device(count, mean, m2, stream_);
+  }
+  const float* critic_dev(int k) const { return q_.p + k * Ps_; }
+  int64_t critic_params() const { return qnet_.params; }
+  int64_t policy_params() const { return pnet_.params; }
+  int64_t lagged_version() const { return lagged_version_; }
   void ingest(const replay::Slice& s);
   void ingest_host(const pqlg_step_slice& host);  // copy-in path for a host StepSlice
   bool ready(int64_t c_a);
@@ -121,6 +130,11 @@ class PLearner {
   void adopt_critics(const float* q1_host, const float* q2_host, int64_t version);
   void adopt_critics_device(const float* q1_dev, const float* q2_dev, int64_t version);
   void adopt_norm(int64_t count, const double* mean, const double* m2);
+  void adopt_norm_device(const int64_t* count, const double* mean, const double* m2) {
+    norm_.set_device(count, mean, m2, stream_);
+  }
+  int64_t policy_params() const { return pnet_.params; }
+  int64_t critic_params() const { return qnet_.params; }
   void ingest(const float* states_dev, int64_t ld, uint64_t n);
   void ingest_host(const float* states_host, int64_t ld, uint64_t n);
   bool ready(int64_t c_a);

@@ -1,0 +1,595 @@
+// run_parallel on one B200: the three
+// PQL processes -- Actor, V-learner, P-learner -- as three host threads, each
+// driving its core on its own CUDA stream, paced by counter gating and
+// talking only through bounded channels and latest-wins snapshot slots.
+//
+//   reference                                   here
+//   sched::RatioGate (ratio_gate.hpp:17-112)    Gate (same proceed rule, same counters)
+//   rt::BoundedChannel (mailbox.hpp:13-63)      Channel<Batch>: host FIFO of descriptors of
+//                                               device-resident data slots
+//   rt::LatestSlot (mailbox.hpp:67-84)          SnapshotPool: 3 device buffers + events,
+//                                               latest-wins, readers never block writers
+//   DataBatch / StateBatch (messages.hpp:37-49) one DataSlot per actor iteration: H
+//                                               StepSlices, the actor's normalizer, the
+//                                               policy it used and the newest critic
+//                                               snapshot (hub topology)
+//
+// All data stays on the device; the host threads only exchange slot indices,
+// versions and CUDA events (cudaStreamWaitEvent orders the streams).
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "actor.h"
+#include "learner.h"
+
+namespace pqlg {
+namespace {
+
+enum Proc { kActor = 0, kVLearner = 1, kPLearner = 2 };
+
+// RatioGate::may_proceed (ratio_gate.hpp:44-60).
+bool may_proceed(int p, int64_t ca, int64_t cv, int64_t cp, const pqlg_ratio_config& c) {
+  if (c.free_running) return true;
+  if (ca < c.warm_up) return true;
+  switch (p) {
+    case kActor:
+      return static_cast<double>(ca) + 1.0 <= c.beta_av * static_cast<double>(cv) + c.slack_a;
+    case kPLearner:
+      return static_cast<double>(cp) + 1.0 <= c.beta_pv * static_cast<double>(cv) + c.slack_p;
+    case kVLearner:  // must not outrun available data
+      return static_cast<double>(cv) + 1.0 <= static_cast<double>(ca) / c.beta_av + c.slack_v;
+  }
+  return true;
+}
+
+class Gate {
+ public:
+  explicit Gate(const pqlg_ratio_config& c) : cfg_(c) {}
+  int64_t count(int p) const { return c_[p].load(std::memory_order_relaxed); }
+  bool may(int p) const { return may_proceed(p, count(0), count(1), count(2), cfg_); }
+  // wait_turn_for: true = proceed; false = timed out or stopped
+  bool wait_for(int p, std::chrono::microseconds t) {
+    std::unique_lock<std::mutex> lk(mu_);
+    return cv_.wait_for(lk, t, [&] { return stop_ || may(p); }) && !stop_;
+  }
+  void record(int p, int64_t n) {
+    c_[p].fetch_add(n, std::memory_order_relaxed);
+    std::lock_guard<std::mutex> lk(mu_);
+    cv_.notify_all();
+  }
+  void shutdown() {
+    std::lock_guard<std::mutex> lk(mu_);
+    stop_ = true;
+    cv_.notify_all();
+  }
+  bool stopped() {
+    std::lock_guard<std::mutex> lk(mu_);
+    return stop_;
+  }
+
+ private:
+  pqlg_ratio_config cfg_;
+  std::atomic<int64_t> c_[3]{{0}, {0}, {0}};
+  std::mutex mu_;
+  std::condition_variable cv_;
+  bool stop_ = false;
+};
+
+struct Batch {
+  int64_t seq;
+  int slot;
+  int64_t policy_version;
+  int64_t critic_version;  // 0: no critic snapshot yet
+};
+
+// BoundedChannel (mailbox.hpp:13-63): push blocks while full; close wakes all.
+class Channel {
+ public:
+  explicit Channel(size_t cap) : cap_(cap) {}
+  bool push(const Batch& b) {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_push_.wait(lk, [&] { return closed_ || q_.size() < cap_; });
+    if (closed_) return false;
+    q_.push_back(b);
+    cv_pop_.notify_one();
+    return true;
+  }
+  std::optional<Batch> pop_wait(std::chrono::microseconds t) {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_pop_.wait_for(lk, t, [&] { return closed_ || !q_.empty(); });
+    if (q_.empty()) return std::nullopt;
+    Batch b = q_.front();
+    q_.pop_front();
+    cv_push_.notify_one();
+    return b;
+  }
+  void close() {
+    std::lock_guard<std::mutex> lk(mu_);
+    closed_ = true;
+    cv_push_.notify_all();
+    cv_pop_.notify_all();
+  }
+
+ private:
+  size_t cap_;
+  std::mutex mu_;
+  std::condition_variable cv_push_, cv_pop_;
+  std::deque<Batch> q_;
+  bool closed_ = false;
+};
+
+// LatestSlot (mailbox.hpp:67-84) for device snapshots: the publisher writes
+// buffer (latest + 1) % 3 after waiting (on its stream) for the last reader of
+// that buffer; a reader copies the latest buffer under the lock and records
+// its read event before releasing it, so no buffer is overwritten mid-read.
+struct SnapshotPool {
+  DevBuf<float> buf[3];
+  cudaEvent_t written[3] = {}, read[3] = {};
+  int64_t version = 0;
+  int latest = -1;
+  std::mutex mu;
+  void init(size_t floats) {
+    for (int k = 0; k < 3; ++k) {
+      buf[k].alloc(floats);
+      PQLG_CUDA(cudaEventCreateWithFlags(&written[k], cudaEventDisableTiming));
+      PQLG_CUDA(cudaEventCreateWithFlags(&read[k], cudaEventDisableTiming));
+    }
+  }
+  ~SnapshotPool() {
+    for (int k = 0; k < 3; ++k) {
+      if (written[k]) cudaEventDestroy(written[k]);
+      if (read[k]) cudaEventDestroy(read[k]);
+    }
+  }
+  // copy(dst_buffer, stream) enqueues the writes of the snapshot
+  template <class F>
+  int64_t publish(cudaStream_t st, F&& copy) {
+    std::lock_guard<std::mutex> lk(mu);
+    const int k = (latest + 1) % 3;
+    PQLG_CUDA(cudaStreamWaitEvent(st, read[k], 0));
+    copy(buf[k].p, st);
+    PQLG_CUDA(cudaEventRecord(written[k], st));
+    latest = k;
+    return ++version;
+  }
+  // read(src_buffer, version, stream) enqueues the reads when newer than have
+  template <class F>
+  int64_t take_if_newer(int64_t have, cudaStream_t st, F&& read_fn) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (latest < 0 || version <= have) return have;
+    PQLG_CUDA(cudaStreamWaitEvent(st, written[latest], 0));
+    read_fn(buf[latest].p, version, st);
+    PQLG_CUDA(cudaEventRecord(read[latest], st));
+    return version;
+  }
+  int64_t newest() {
+    std::lock_guard<std::mutex> lk(mu);
+    return version;
+  }
+};
+
+}  // namespace
+
+class Pipeline {
+ public:
+  Pipeline(const pqlg_config& cfg, const pqlg_task_dims& dims, const pqlg_ratio_config& rc,
+           uint64_t init_seed)
+      : cfg_(cfg), dims_(dims), rc_(rc), gate_(rc) {
+    require(rc.horizon >= 1 && rc.channel_capacity >= 1 && rc.publish_every >= 1,
+            "pipeline: horizon, channel_capacity and publish_every must be >= 1");
+    require(rc.beta_av > 0 && rc.beta_pv > 0, "pipeline: ratios must be positive");
+    PQLG_CUDA(cudaGetDevice(&device_));
+    for (auto* s : {&sa_, &sv_, &sp_}) PQLG_CUDA(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+    actor_ = std::make_unique<Actor>(cfg, dims, sa_);
+    v_ = std::make_unique<VLearner>(cfg, dims, init_seed, sv_);
+    p_ = std::make_unique<PLearner>(cfg, dims, init_seed, sp_);
+    N_ = cfg.n_envs;
+    D_ = dims.obs_dim;
+    A_ = dims.act_dim;
+    Dp_ = round_up(D_, 4);
+    Ap_ = round_up(A_, 4);
+    H_ = rc.horizon;
+    const int64_t Pp = p_->policy_params(), Pq = p_->critic_params();
+    pol_pool_.init(Pp);
+    crit_pool_.init(2 * Pq);
+    // one slot per in-flight actor iteration: both channels full + one being
+    // filled + one being consumed per learner
+    const int n_slots = 2 * rc.channel_capacity + 3;
+    slots_.resize(n_slots);
+    for (int k = 0; k < n_slots; ++k) {
+      Slot& s = slots_[k];
+      s.obs.alloc(static_cast<size_t>(H_) * N_ * Dp_);
+      s.boot.alloc(static_cast<size_t>(H_) * N_ * Dp_);
+      s.act.alloc(static_cast<size_t>(H_) * N_ * Ap_);
+      s.rew.alloc(static_cast<size_t>(H_) * N_);
+      s.flags.alloc(2ull * H_ * N_);
+      s.count.alloc(1);
+      s.mean.alloc(D_);
+      s.m2.alloc(D_);
+      s.pol.alloc(Pp);
+      s.crit.alloc(2 * Pq);
+      PQLG_CUDA(cudaEventCreateWithFlags(&s.filled, cudaEventDisableTiming));
+      PQLG_CUDA(cudaEventCreateWithFlags(&s.done_v, cudaEventDisableTiming));
+      PQLG_CUDA(cudaEventCreateWithFlags(&s.done_p, cudaEventDisableTiming));
+      free_.push_back(k);
+    }
+    PQLG_CUDA(cudaDeviceSynchronize());
+  }
+
+  ~Pipeline() {
+    for (auto& s : slots_) {
+      cudaEventDestroy(s.filled);
+      cudaEventDestroy(s.done_v);
+      cudaEventDestroy(s.done_p);
+    }
+    actor_.reset();
+    v_.reset();
+    p_.reset();
+    for (auto s : {sa_, sv_, sp_}) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+
+  pqlg_run_report run(int64_t actor_steps, double max_seconds) {
+    require(!ran_, "pipeline: run() may be called once per pipeline");
+    ran_ = true;
+    ch_v_ = std::make_unique<Channel>(rc_.channel_capacity);
+    ch_p_ = std::make_unique<Channel>(rc_.channel_capacity);
+    const auto t0 = std::chrono::steady_clock::now();
+    std::thread ta([&] { guard_thread([&] { actor_loop(); }); });
+    std::thread tv([&] { guard_thread([&] { vlearner_loop(); }); });
+    std::thread tp([&] { guard_thread([&] { plearner_loop(); }); });
+    while (true) {
+      std::this_thread::sleep_for(std::chrono::microseconds(200));
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (failed_.load() || gate_.count(kActor) >= actor_steps || el >= max_seconds) break;
+    }
+    // clean shutdown: the actor finishes its iteration (its pushes complete
+    // while the learners keep draining), then the learners drain what is
+    // queued and stop -- every batch sent is consumed exactly once
+    stop_actor_ = true;
+    ta.join();
+    stop_all();
+    tv.join();
+    tp.join();
+    for (auto s : {sa_, sv_, sp_}) PQLG_CUDA(cudaStreamSynchronize(s));
+    pqlg_run_report r{};
+    r.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    r.c_a = gate_.count(kActor);
+    r.c_v = gate_.count(kVLearner);
+    r.c_p = gate_.count(kPLearner);
+    r.env_steps = r.c_a * N_;
+    r.ratio_av = r.c_v ? static_cast<double>(r.c_a) / r.c_v : 0.0;
+    r.ratio_pv = r.c_v ? static_cast<double>(r.c_p) / r.c_v : 0.0;
+    r.batches_sent = sent_;
+    r.batches_consumed_v = stats_[0].consumed;
+    r.batches_consumed_p = stats_[1].consumed;
+    r.seq_duplicates = stats_[0].dups + stats_[1].dups;
+    r.seq_gaps = stats_[0].gaps + stats_[1].gaps;
+    r.max_policy_staleness = max_stale_;
+    r.policy_version = pol_pool_.newest();
+    r.critic_version = crit_pool_.newest();
+    r.last_critic_loss = last_closs_;
+    r.last_actor_loss = last_aloss_;
+    r.ok = failed_.load() ? 0 : 1;
+    if (failed_.load()) {
+      set_last_error(error_);
+      throw Error(err_status_, error_);
+    }
+    return r;
+  }
+
+ private:
+  struct Slot {
+    DevBuf<float> obs, boot, act, rew, pol, crit;
+    DevBuf<uint8_t> flags;  // term [H x N] | trunc [H x N]
+    DevBuf<int64_t> count;
+    DevBuf<double> mean, m2;
+    cudaEvent_t filled = nullptr, done_v = nullptr, done_p = nullptr;
+    int pending = 0;  // consumers still to release it
+  };
+  struct ConsumerStats {
+    int64_t expect = 0, consumed = 0, dups = 0, gaps = 0;
+  };
+
+  template <class F>
+  void guard_thread(F&& f) {
+    try {
+      PQLG_CUDA(cudaSetDevice(device_));  // the CUDA device is per host thread
+      f();
+    } catch (const Error& e) {
+      fail(e.status, e.what());
+    } catch (const std::exception& e) {
+      fail(PQLG_EINVAL, e.what());
+    }
+  }
+  void fail(int status, const std::string& msg) {
+    {
+      std::lock_guard<std::mutex> lk(err_mu_);
+      if (!failed_.load()) {
+        error_ = "run_parallel: " + msg;
+        err_status_ = status;
+      }
+    }
+    failed_ = true;
+    stop_all();
+  }
+  void stop_all() {
+    gate_.shutdown();
+    if (ch_v_) ch_v_->close();
+    if (ch_p_) ch_p_->close();
+    std::lock_guard<std::mutex> lk(slot_mu_);
+    stopping_ = true;
+    slot_cv_.notify_all();
+  }
+
+  int take_slot() {
+    std::unique_lock<std::mutex> lk(slot_mu_);
+    slot_cv_.wait(lk, [&] { return stopping_ || !free_.empty(); });
+    if (stopping_) return -1;
+    const int k = free_.front();
+    free_.pop_front();
+    slots_[k].pending = 2;
+    return k;
+  }
+  void release_slot(int k) {
+    std::lock_guard<std::mutex> lk(slot_mu_);
+    if (--slots_[k].pending == 0) {
+      free_.push_back(k);
+      slot_cv_.notify_all();
+    }
+  }
+
+  // ---- Actor (Alg. 1, SPEC run_actor): fetch the newest policy, roll out H
+  // steps, send (transitions, policy, normalizer) to the V-learner and
+  // (states, critic snapshot, normalizer) to the P-learner, gate.
+  void actor_loop() {
+    int64_t seq = 0, crit_have = 0;
+    const int64_t Pp = p_->policy_params(), Pq = p_->critic_params();
+    while (true) {
+      bool go = false;
+      while (!go) {
+        if (gate_.stopped() || stop_actor_.load()) return;
+        go = gate_.wait_for(kActor, std::chrono::microseconds(2000));
+      }
+      const int k = take_slot();
+      if (k < 0) return;
+      Slot& s = slots_[k];
+      PQLG_CUDA(cudaStreamWaitEvent(sa_, s.done_v, 0));
+      PQLG_CUDA(cudaStreamWaitEvent(sa_, s.done_p, 0));
+      // newest policy snapshot (P-learner -> actor)
+      pol_pool_.take_if_newer(actor_->policy_version(), sa_,
+                              [&](const float* src, int64_t ver, cudaStream_t st) {
+                                (void)st;
+                                actor_->adopt_policy(src, ver, true);
+                              });
+      max_stale_ = std::max(max_stale_, pol_pool_.newest() - actor_->policy_version());
+      for (int h = 0; h < H_; ++h) {
+        pqlg_step_slice v{};
+        actor_->rollout_step(&v);
+        const size_t ro = static_cast<size_t>(h) * N_;
+        auto cp2 = [&](float* dst, int64_t ldd, const float* src, int64_t lds, int w) {
+          PQLG_CUDA(cudaMemcpy2DAsync(dst, ldd * 4, src, lds * 4, w * 4, N_,
+                                      cudaMemcpyDeviceToDevice, sa_));
+        };
+        cp2(s.obs.p + ro * Dp_, Dp_, v.obs, v.ld_obs, D_);
+        cp2(s.boot.p + ro * Dp_, Dp_, v.boot_obs, v.ld_obs, D_);
+        cp2(s.act.p + ro * Ap_, Ap_, v.act, v.ld_act, A_);
+        PQLG_CUDA(cudaMemcpyAsync(s.rew.p + ro, v.rew, N_ * 4, cudaMemcpyDeviceToDevice, sa_));
+        PQLG_CUDA(cudaMemcpyAsync(s.flags.p + ro, v.term, N_, cudaMemcpyDeviceToDevice, sa_));
+        PQLG_CUDA(cudaMemcpyAsync(s.flags.p + static_cast<size_t>(H_) * N_ + ro, v.trunc, N_,
+                                  cudaMemcpyDeviceToDevice, sa_));
+      }
+      // normalizer (owned by the actor) and the policy the data came from
+      PQLG_CUDA(cudaMemcpyAsync(s.count.p, actor_->count_dev(), 8, cudaMemcpyDeviceToDevice, sa_));
+      PQLG_CUDA(cudaMemcpyAsync(s.mean.p, actor_->mean_dev(), D_ * 8, cudaMemcpyDeviceToDevice, sa_));
+      PQLG_CUDA(cudaMemcpyAsync(s.m2.p, actor_->m2_dev(), D_ * 8, cudaMemcpyDeviceToDevice, sa_));
+      PQLG_CUDA(cudaMemcpyAsync(s.pol.p, actor_->policy_dev(), Pp * 4, cudaMemcpyDeviceToDevice, sa_));
+      // newest critic snapshot (V-learner -> actor -> P-learner)
+      crit_have = crit_pool_.take_if_newer(crit_have, sa_,
+                                           [&](const float* src, int64_t, cudaStream_t st) {
+                                             PQLG_CUDA(cudaMemcpyAsync(s.crit.p, src, 2 * Pq * 4,
+                                                                       cudaMemcpyDeviceToDevice, st));
+                                           });
+      PQLG_CUDA(cudaEventRecord(s.filled, sa_));
+      const Batch b{seq++, k, actor_->policy_version(), crit_have};
+      if (!ch_v_->push(b) || !ch_p_->push(b)) return;
+      ++sent_;
+      gate_.record(kActor, H_);
+    }
+  }
+
+  void note_seq(ConsumerStats& st, int64_t seq) {
+    if (seq < st.expect) ++st.dups;
+    else if (seq > st.expect) st.gaps += seq - st.expect;
+    st.expect = std::max(st.expect, seq + 1);
+    ++st.consumed;
+  }
+
+  // ---- V-learner (Alg. 3, SPEC run_vlearner): drain data into the replay
+  // buffer, hard-update the lagged policy, update the critics, publish a
+  // critic snapshot every K_pub updates, gate.
+  void vlearner_loop() {
+    ConsumerStats& st = stats_[0];
+    int64_t updates = 0;
+    const int64_t Pq = v_->critic_params();
+    bool have_batch = false;  // replay size >= B (monotone: checked until true)
+    auto ready = [&] {
+      if (gate_.count(kActor) < cfg_.warm_up) return false;
+      if (!have_batch) have_batch = v_->ready(gate_.count(kActor));
+      return have_batch;
+    };
+    auto drain = [&](std::chrono::microseconds first_wait) {
+      auto b = ch_v_->pop_wait(first_wait);
+      while (b) {
+        Slot& s = slots_[b->slot];
+        note_seq(st, b->seq);
+        PQLG_CUDA(cudaStreamWaitEvent(sv_, s.filled, 0));
+        for (int h = 0; h < H_; ++h) {
+          const size_t ro = static_cast<size_t>(h) * N_;
+          replay::Slice sl{s.obs.p + ro * Dp_, s.act.p + ro * Ap_, s.boot.p + ro * Dp_,
+                           s.rew.p + ro, s.flags.p + ro,
+                           s.flags.p + static_cast<size_t>(H_) * N_ + ro, Dp_, Ap_};
+          v_->ingest(sl);
+        }
+        v_->adopt_norm_device(s.count.p, s.mean.p, s.m2.p);
+        v_->adopt_policy_device(s.pol.p, b->policy_version);
+        PQLG_CUDA(cudaEventRecord(s.done_v, sv_));
+        release_slot(b->slot);
+        b = ch_v_->pop_wait(std::chrono::microseconds(0));
+      }
+    };
+    while (!gate_.stopped()) {
+      drain(std::chrono::microseconds(ready() ? 0 : 2000));
+      if (!ready()) continue;
+      if (!gate_.wait_for(kVLearner, std::chrono::microseconds(1000))) continue;
+      v_->update_n(1);
+      PQLG_CUDA(cudaStreamSynchronize(sv_));
+      gate_.record(kVLearner, 1);
+      if (++updates % rc_.publish_every == 0) {
+        last_closs_ = v_->last_loss();  // throws on a non-finite update (SPEC: abort)
+        crit_pool_.publish(sv_, [&](float* dst, cudaStream_t stm) {
+          PQLG_CUDA(cudaMemcpyAsync(dst, v_->critic_dev(0), Pq * 4, cudaMemcpyDeviceToDevice, stm));
+          PQLG_CUDA(cudaMemcpyAsync(dst + Pq, v_->critic_dev(1), Pq * 4, cudaMemcpyDeviceToDevice,
+                                    stm));
+        });
+      }
+    }
+    drain(std::chrono::microseconds(0));  // closed channel: already-queued batches still drain
+  }
+
+  // ---- P-learner (Alg. 2, SPEC run_plearner)
+  void plearner_loop() {
+    ConsumerStats& st = stats_[1];
+    int64_t updates = 0;
+    const int64_t Pq = p_->critic_params(), Pp = p_->policy_params();
+    bool have_batch = false;
+    auto ready = [&] {
+      if (gate_.count(kActor) < cfg_.warm_up) return false;
+      if (!have_batch) have_batch = p_->ready(gate_.count(kActor));
+      return have_batch;
+    };
+    auto drain = [&](std::chrono::microseconds first_wait) {
+      auto b = ch_p_->pop_wait(first_wait);
+      while (b) {
+        Slot& s = slots_[b->slot];
+        note_seq(st, b->seq);
+        PQLG_CUDA(cudaStreamWaitEvent(sp_, s.filled, 0));
+        p_->ingest(s.obs.p, Dp_, static_cast<uint64_t>(H_) * N_);
+        p_->adopt_norm_device(s.count.p, s.mean.p, s.m2.p);
+        if (b->critic_version > 0)
+          p_->adopt_critics_device(s.crit.p, s.crit.p + Pq, b->critic_version);
+        PQLG_CUDA(cudaEventRecord(s.done_p, sp_));
+        release_slot(b->slot);
+        b = ch_p_->pop_wait(std::chrono::microseconds(0));
+      }
+    };
+    while (!gate_.stopped()) {
+      drain(std::chrono::microseconds(ready() ? 0 : 2000));
+      if (!ready()) continue;
+      if (!gate_.wait_for(kPLearner, std::chrono::microseconds(1000))) continue;
+      p_->update_n(1);
+      PQLG_CUDA(cudaStreamSynchronize(sp_));
+      gate_.record(kPLearner, 1);
+      if (++updates % rc_.publish_every == 0) {
+        last_aloss_ = p_->last_loss();
+        pol_pool_.publish(sp_, [&](float* dst, cudaStream_t stm) {
+          PQLG_CUDA(cudaMemcpyAsync(dst, p_->policy_dev(), Pp * 4, cudaMemcpyDeviceToDevice, stm));
+        });
+      }
+    }
+    drain(std::chrono::microseconds(0));
+  }
+
+  pqlg_config cfg_;
+  pqlg_task_dims dims_;
+  pqlg_ratio_config rc_;
+  Gate gate_;
+  int device_ = 0;
+  cudaStream_t sa_ = nullptr, sv_ = nullptr, sp_ = nullptr;
+  std::unique_ptr<Actor> actor_;
+  std::unique_ptr<VLearner> v_;
+  std::unique_ptr<PLearner> p_;
+  int N_, D_, A_, H_;
+  int64_t Dp_, Ap_;
+  SnapshotPool pol_pool_, crit_pool_;
+  std::vector<Slot> slots_;
+  std::deque<int> free_;
+  std::mutex slot_mu_;
+  std::condition_variable slot_cv_;
+  bool stopping_ = false;
+  std::unique_ptr<Channel> ch_v_, ch_p_;
+  ConsumerStats stats_[2];
+  int64_t sent_ = 0, max_stale_ = 0;
+  float last_closs_ = 0.0f, last_aloss_ = 0.0f;
+  bool ran_ = false;
+  std::atomic<bool> failed_{false}, stop_actor_{false};
+  std::mutex err_mu_;
+  std::string error_;
+  int err_status_ = PQLG_OK;
+};
+
+}  // namespace pqlg
+
+struct pqlg_pipeline_s {
+  std::unique_ptr<pqlg::Pipeline> p;
+};
+
+using namespace pqlg;
+
+extern "C" {
+
+void pqlg_ratio_config_default(pqlg_ratio_config* c) {
+  // RatioConfig defaults (ratio_gate.hpp:17-25) + SPEC.md:486-492
+  *c = pqlg_ratio_config{};
+  c->beta_av = 1.0 / 8.0;
+  c->beta_pv = 1.0 / 2.0;
+  c->slack_a = 4.0;
+  c->slack_p = 1.0;
+  c->slack_v = 1.0;
+  c->warm_up = 32;
+  c->free_running = 0;
+  c->horizon = 4;
+  c->channel_capacity = 8;
+  c->publish_every = 8;
+}
+
+int pqlg_ratio_may_proceed(int proc, int64_t c_a, int64_t c_v, int64_t c_p,
+                           const pqlg_ratio_config* cfg) {
+  if (!cfg || proc < 0 || proc > 2) return -1;
+  return may_proceed(proc, c_a, c_v, c_p, *cfg) ? 1 : 0;
+}
+
+int pqlg_pipeline_create(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                         const pqlg_ratio_config* rc, uint64_t init_rng_seed, pqlg_pipeline* out) {
+  return guarded([&] {
+    require(cfg && dims && rc && out, "pipeline_create: null argument");
+    auto h = std::make_unique<pqlg_pipeline_s>();
+    h->p = std::make_unique<Pipeline>(*cfg, *dims, *rc, init_rng_seed);
+    *out = h.release();
+  });
+}
+
+int pqlg_pipeline_run(pqlg_pipeline h, int64_t actor_steps, double max_seconds,
+                      pqlg_run_report* out) {
+  return guarded([&] {
+    require(h && out, "pipeline_run: null argument");
+    *out = h->p->run(actor_steps, max_seconds);
+  });
+}
+
+int pqlg_pipeline_destroy(pqlg_pipeline h) {
+  return guarded([&] { delete h; });
+}
+
+}  // extern "C"

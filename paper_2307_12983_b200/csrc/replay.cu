@@ -43,6 +43,27 @@ void launch_state_sample(const DeviceStates& r, const replay::Norm& norm, float*
   launch(replay::state_sample_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kWarpsPerBlock), 0, st, r.view(), norm, out, ld_out, ss, idx_dev, B);
 }
 
+namespace {
+__global__ void norm_consts_kernel(const int64_t* count, const double* mean, const double* m2,
+                                   int D, float* mean_f, float* inv_f, int* ident) {
+  pdl::entry();
+  const int64_t c = *count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ident = c <= 1 ? 1 : 0;
+  if (c <= 1) return;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < D; j += gridDim.x * blockDim.x) {
+    mean_f[j] = static_cast<float>(mean[j]);
+    const double var = __ddiv_rn(m2[j], static_cast<double>(c));
+    inv_f[j] = static_cast<float>(__ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var, 1e-8))));
+  }
+}
+}  // namespace
+
+void DeviceNorm::set_device(const int64_t* count, const double* m, const double* m2,
+                            cudaStream_t st) {
+  launch(norm_consts_kernel, dim3((D + 255) / 256), dim3(256), 0, st, count, m, m2, D, mean.p,
+         inv.p, ident.p);
+}
+
 }  // namespace pqlg
 
 // ------------------------------------------------------------------ C ABI

@@ -46,6 +46,10 @@ struct DeviceNorm {
     PQLG_CUDA(cudaMemcpyAsync(ident.p, &zero, sizeof(int), cudaMemcpyHostToDevice, st));
     PQLG_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
   }
+  // The same from device-resident NormStats (count, mean, m2), computed on
+  // device in fp64 (IEEE division and sqrt: identical to the host formula),
+  // asynchronous on st.
+  void set_device(const int64_t* count, const double* m, const double* m2, cudaStream_t st);
   replay::Norm view() const { return replay::Norm{mean.p, inv.p, ident.p}; }
 };
 

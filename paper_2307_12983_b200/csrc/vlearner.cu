@@ -520,6 +520,13 @@ void VLearner::adopt_policy(const float* flat, int64_t version) {
   lagged_version_ = version;
 }
 
+void VLearner::adopt_policy_device(const float* flat, int64_t version) {
+  if (version < lagged_version_) return;  // learners.cpp:37-42
+  PQLG_CUDA(cudaMemcpyAsync(lagged_.p, flat, pnet_.params * 4, cudaMemcpyDeviceToDevice, stream_));
+  lagged_head_.refresh(stream_);
+  lagged_version_ = version;
+}
+
 void VLearner::adopt_norm(int64_t count, const double* mean, const double* m2) {
   norm_.set(count, mean, m2, stream_);
 }
