@@ -389,11 +389,16 @@ def run_actor(args, rank, world, local, steps, warmup):
     """Actor transitions/s: one ActorCore::rollout_step over N envs (normalize
     -> policy -> mixed noise -> synthetic env -> StepSlice -> normalizer
     update) plus the V-learner ingest (n-step assemble + ring insert) and the
-    P-learner StateBuffer insert of that slice, all on the GPU."""
+    P-learner StateBuffer insert of that slice, all on the GPU.  As in
+    run_parallel, each core runs on its own stream: the learners ingest step
+    t on their streams while the actor computes step t+1 (a slice stays valid
+    for two more rollout steps; the actor waits for the ingest of step t
+    before step t+2)."""
     import torch
     from paper_2307_12983_b200 import _lib
     D, A, H, nh, B, N, cap = CONFIGS[args.config]
     stream = torch.cuda.Stream(device=local)
+    sv_t, spl_t = torch.cuda.Stream(device=local), torch.cuda.Stream(device=local)
     sp = C.c_void_p(stream.cuda_stream)
     cfg = _lib.default_config(batch_size=B, buffer_capacity=cap, hidden=H, hidden_layers=nh,
                               n_envs=N, seed=0, env_offset=rank * N, envs_total=world * N,
@@ -401,17 +406,39 @@ def run_actor(args, rank, world, local, steps, warmup):
     dims = _lib.TaskDims(D, A, -1.0, 1.0)
     act, vl, pl = C.c_void_p(), C.c_void_p(), C.c_void_p()
     _lib.call("pqlg_actor_create", C.byref(cfg), C.byref(dims), sp, C.byref(act))
-    _lib.call("pqlg_vlearner_create", C.byref(cfg), C.byref(dims), 1, sp, C.byref(vl))
-    _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 1, sp, C.byref(pl))
+    _lib.call("pqlg_vlearner_create", C.byref(cfg), C.byref(dims), 1,
+              C.c_void_p(sv_t.cuda_stream), C.byref(vl))
+    _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 1,
+              C.c_void_p(spl_t.cuda_stream), C.byref(pl))
     s = _lib.StepSlice()
+    ev_step = [torch.cuda.Event() for _ in range(3)]
+    ev_v = [torch.cuda.Event() for _ in range(3)]
+    ev_p = [torch.cuda.Event() for _ in range(3)]
+    t_ctr = [0]
 
     def step():
+        t = t_ctr[0]
+        k = t % 3
+        if t >= 2:  # step t writes the buffers the ingest of step t-2 reads
+            stream.wait_event(ev_v[(t - 2) % 3])
+            stream.wait_event(ev_p[(t - 2) % 3])
         _lib.call("pqlg_actor_rollout_step", act, C.byref(s))
+        ev_step[k].record(stream)
+        sv_t.wait_event(ev_step[k])
         _lib.call("pqlg_vlearner_ingest", vl, C.byref(s))
+        ev_v[k].record(sv_t)
+        spl_t.wait_event(ev_step[k])
         _lib.call("pqlg_plearner_ingest", pl, s.obs, s.ld_obs, N)
+        ev_p[k].record(spl_t)
+        t_ctr[0] = t + 1
+
+    def join():  # the actor stream waits for the learners' last ingest
+        stream.wait_event(ev_v[(t_ctr[0] - 1) % 3])
+        stream.wait_event(ev_p[(t_ctr[0] - 1) % 3])
 
     for _ in range(warmup):
         step()
+    join()
     stream.synchronize()
     barrier(world)
     l0 = _lib.lib().pqlg_launch_count()
@@ -419,12 +446,14 @@ def run_actor(args, rank, world, local, steps, warmup):
     ev0.record(stream)
     for _ in range(steps):
         step()
+    join()
     ev1.record(stream)
     ev1.synchronize()
     barrier(world)
     ms = max_over_ranks(ev0.elapsed_time(ev1), world)
     launches = _lib.lib().pqlg_launch_count() - l0
     # policy-inference-only rate (graph replay of the actor step alone)
+    stream.synchronize()
     _lib.call("pqlg_actor_rollout_n", act, warmup)
     stream.synchronize()
     ev0.record(stream)
@@ -441,6 +470,8 @@ def run_actor(args, rank, world, local, steps, warmup):
     for _ in range(e2e_steps):
         step()
         _lib.call("pqlg_actor_read", act, 6, status.ctypes.data)
+    join()
+    stream.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0, world)
     for h, fn in ((act, "pqlg_actor_destroy"), (vl, "pqlg_vlearner_destroy"),
                   (pl, "pqlg_plearner_destroy")):

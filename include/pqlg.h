@@ -347,7 +347,9 @@ PQLG_API int pqlg_actor_destroy(pqlg_actor h);
 /* adopt_policy: PolicyHandle::adopt, equal-or-newer (learners.cpp:37-42) */
 PQLG_API int pqlg_actor_adopt_policy(pqlg_actor h, const float* flat_host, int64_t version);
 /* rollout_step() (learners.cpp:80-116): enqueues one step; *out receives
- * device views of the StepSlice, valid until the next rollout_step. */
+ * device views of the StepSlice, valid for the next two rollout_steps (the
+ * actor rotates three output buffer sets), so consumers on other streams can
+ * read step t while step t+1 runs; order them before step t+2 (events). */
 PQLG_API int pqlg_actor_rollout_step(pqlg_actor h, pqlg_step_slice* out);
 /* n steps replayed from CUDA graphs (no slices returned). */
 PQLG_API int pqlg_actor_rollout_n(pqlg_actor h, int n);

@@ -168,12 +168,14 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
   // environment + initial observations (make_env -> reset_all, learners.cpp:66-68)
   env_ = std::make_unique<DeviceEnv>(N_, D_, A_, cfg.seed, cfg.max_episode_len, cfg.env_offset,
                                      dims.low, dims.high);
-  for (auto& o : obs_) o.alloc(static_cast<size_t>(N_) * Dp_);
-  boot_.alloc(static_cast<size_t>(N_) * Dp_);
-  rew_.alloc(N_);
-  term_.alloc(N_);
-  trunc_.alloc(N_);
-  act_.alloc(static_cast<size_t>(N_) * Ap_);
+  for (int k = 0; k < kSets; ++k) {
+    obs_[k].alloc(static_cast<size_t>(N_) * Dp_);
+    boot_[k].alloc(static_cast<size_t>(N_) * Dp_);
+    rew_[k].alloc(N_);
+    term_[k].alloc(N_);
+    trunc_[k].alloc(N_);
+    act_[k].alloc(static_cast<size_t>(N_) * Ap_);
+  }
   Xn_.alloc(static_cast<size_t>(N_) * Dp_);
   env_->reset(obs_[0].p, Dp_, stream_);
 
@@ -230,7 +232,6 @@ void Actor::build() {
   // DeterministicPolicy::act + apply_noise (learners.cpp:96-98), fused
   epi::PolicyHead ph{};
   ph.bias = pol_.p + pnet_.b_off[nh];
-  ph.act = act_.p;
   ph.ld_act = Ap_;
   ph.M = N;
   ph.A = A;
@@ -243,7 +244,10 @@ void Actor::build() {
   head_.init(pol_.p + pnet_.w_off[nh], H, A);
   head_.refresh(stream_);
   const float* W = head_.ptr();
-  policy_steps_.push_back(mlp::fwd(in, in, ld, W, W, N, A, H, 1, ph, head_.stride()));
+  for (int k = 0; k < kSets; ++k) {
+    ph.act = act_[k].p;
+    head_steps_[k] = mlp::fwd(in, in, ld, W, W, N, A, H, 1, ph, head_.stride());
+  }
 }
 
 void Actor::enqueue(int cur) {
@@ -252,15 +256,18 @@ void Actor::enqueue(int cur) {
   const float* obs = obs_[cur].p;
   // actions = pi(obs_norm) + mixed noise; Xn_ holds apply(stats_{t-1}, obs_t)
   for (auto& s : policy_steps_) s(st);
+  head_steps_[cur](st);
   // normalizer_.update(obs_) (learners.cpp:113): it only reads this step's
   // observations, so it runs before the env step and the env kernel can emit
   // the next policy input apply(stats_t, obs_{t+1}) directly.
   actor::NormState ns{count_.p, mean_.p, m2_.p, mean_f_.p, inv_f_.p, identity_.p};
   launch(actor::norm_update_kernel, dim3(dim3((D + 31) / 32, actor::kNormGroups)), dim3(256), 0, st, obs, Dp_, N, D, npart_.p, nticket_.p, ns);
   // env_->step(actions) + next-obs normalisation
-  actor::StepOut o{obs_[1 - cur].p, boot_.p, rew_.p, term_.p, trunc_.p, nullptr, Dp_, status_.p};
+  const int nxt = (cur + 1) % kSets;
+  actor::StepOut o{obs_[nxt].p, boot_[cur].p, rew_[cur].p, term_[cur].p, trunc_[cur].p, nullptr,
+                   Dp_, status_.p};
   actor::NextNorm nn{Xn_.p, Dp_, mean_f_.p, inv_f_.p, identity_.p};
-  env_->step(act_.p, Ap_, o, st, nn, obs, Dp_);
+  env_->step(act_[cur].p, Ap_, o, st, nn, obs, Dp_);
 }
 
 int Actor::kernels_per_step() {
@@ -282,19 +289,19 @@ void Actor::rollout_step(pqlg_step_slice* out) {
   enqueue(cur);
   if (out) {
     out->obs = obs_[cur].p;
-    out->act = act_.p;
-    out->boot_obs = boot_.p;
-    out->rew = rew_.p;
-    out->term = term_.p;
-    out->trunc = trunc_.p;
+    out->act = act_[cur].p;
+    out->boot_obs = boot_[cur].p;
+    out->rew = rew_[cur].p;
+    out->term = term_[cur].p;
+    out->trunc = trunc_[cur].p;
     out->ld_obs = Dp_;
     out->ld_act = Ap_;
   }
-  cur_ = 1 - cur;
+  cur_ = (cur + 1) % kSets;
 }
 
 void Actor::rollout_n(int n) {
-  for (int c = 0; c < 2; ++c) {
+  for (int c = 0; c < kSets; ++c) {
     if (graph_[c]) continue;
     kernels_per_step();
     cudaGraph_t g;
@@ -307,7 +314,7 @@ void Actor::rollout_n(int n) {
   }
   for (int i = 0; i < n; ++i) {
     PQLG_CUDA(cudaGraphLaunch(graph_[cur_], stream_));
-    cur_ = 1 - cur_;
+    cur_ = (cur_ + 1) % kSets;
   }
   count_launch(static_cast<uint64_t>(n) * kps_);
 }
@@ -339,8 +346,8 @@ void Actor::read_state(int what, void* out) {
                                   cudaMemcpyDeviceToHost, st));
       break;
     case 1:
-      PQLG_CUDA(cudaMemcpy2DAsync(out, A_ * 4, act_.p, Ap_ * 4, A_ * 4, N_,
-                                  cudaMemcpyDeviceToHost, st));
+      PQLG_CUDA(cudaMemcpy2DAsync(out, A_ * 4, act_[(cur_ + kSets - 1) % kSets].p, Ap_ * 4,
+                                  A_ * 4, N_, cudaMemcpyDeviceToHost, st));
       break;
     case 2: PQLG_CUDA(cudaMemcpyAsync(out, noise_rng_.p, N_ * 8, cudaMemcpyDeviceToHost, st)); break;
     case 3: PQLG_CUDA(cudaMemcpyAsync(out, env_->ep.p, N_ * 8, cudaMemcpyDeviceToHost, st)); break;

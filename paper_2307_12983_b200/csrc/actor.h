@@ -50,8 +50,12 @@ class Actor {
   int cur_ = 0;
 
   std::unique_ptr<DeviceEnv> env_;
-  DevBuf<float> obs_[2], boot_, rew_, act_, Xn_;
-  DevBuf<uint8_t> term_, trunc_;
+  // Step outputs rotate over kSets buffer sets, so a slice handed out by
+  // rollout_step stays valid for two more steps (its consumers -- the
+  // learners' ingest -- can overlap the next step on their own streams).
+  static constexpr int kSets = 3;
+  DevBuf<float> obs_[kSets], boot_[kSets], rew_[kSets], act_[kSets], Xn_;
+  DevBuf<uint8_t> term_[kSets], trunc_[kSets];
   DevBuf<float> pol_;
   WeightMirror head_;
   std::vector<DevBuf<float>> pact_;
@@ -63,8 +67,9 @@ class Actor {
   DevBuf<float> mean_f_, inv_f_;
   DevBuf<int> identity_;
   DevBuf<uint32_t> status_;
-  std::vector<mlp::Step> policy_steps_;
-  cudaGraphExec_t graph_[2] = {nullptr, nullptr};
+  std::vector<mlp::Step> policy_steps_;   // hidden layers
+  mlp::Step head_steps_[kSets];           // policy head + noise into act_[set]
+  cudaGraphExec_t graph_[kSets] = {nullptr, nullptr, nullptr};
   int kps_ = 0;
 };
 
