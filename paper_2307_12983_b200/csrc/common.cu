@@ -35,6 +35,11 @@ EncodeTiledFn encode_fn() {
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
+int skip_step() {
+  const char* e = std::getenv("PQLG_SKIP_STEP");
+  return e ? std::atoi(e) : -1;
+}
+
 [[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
   char buf[512];
   std::snprintf(buf, sizeof(buf), "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),

@@ -72,6 +72,11 @@ void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaSt
   if (prof) profile_after(st);
 }
 
+// Profiling aid: PQLG_SKIP_STEP=i drops step i of an update's launch list
+// when it is (re)built, so graph replays measure each step's marginal cost
+// in situ (results are then meaningless; tools/skip_probe.py).
+int skip_step();
+
 // Wraps an ABI entry point: converts exceptions to status codes.
 template <class F>
 int guarded(F&& f) {

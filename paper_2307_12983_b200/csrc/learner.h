@@ -73,6 +73,7 @@ class VLearner {
 
   DevBuf<float> q_, qt_, m_, v_, grads_, lagged_;
   WeightMirror lagged_head_;
+  mlp::HeadSplit head_split_;  // split-K lagged-policy head
   std::unique_ptr<DeviceReplay> replay_;
   std::unique_ptr<DeviceNStep> nstep_;
   DevBuf<float> in_f_;     // host-ingest staging: obs | act | boot | rew
@@ -172,6 +173,7 @@ class PLearner {
 
   DevBuf<float> pol_, m_, v_, grads_, q_;
   WeightMirror head_;
+  mlp::HeadSplit head_split_;
   std::unique_ptr<DeviceStates> states_;
   DevBuf<float> in_f_;  // host-ingest staging
   DeviceNorm norm_;

@@ -16,6 +16,7 @@
 
 #include "epilogues.cuh"
 #include "gemm_host.cuh"
+#include "head_kernels.cuh"
 
 namespace pqlg::mlp {
 
@@ -159,6 +160,55 @@ Step wgrad(const float* H0, const float* H1, int64_t ldh, const float* G0, const
     };
   });
   return step;
+}
+
+// Narrow policy head H -> A (A <= 32) as split-K partial tiles + the
+// finishing kernel (head_kernels.cuh).  `fin` carries everything but the
+// partial buffer, which is allocated here; returns the two steps.
+struct HeadSplit {
+  DevBuf<float> part;
+  int splits = 1;
+  int64_t ld_part = 0;
+  void plan(int M, int A, int K) {
+    const int tiles = (M + gemm::kBM - 1) / gemm::kBM;
+    const int k_tiles = (K + gemm::kBK - 1) / gemm::kBK;
+    int s = (2 * kSMs + tiles - 1) / tiles;
+    const int max_s = k_tiles / 4 > 1 ? k_tiles / 4 : 1;  // >= 4 k-tiles per split
+    if (s > max_s) s = max_s;
+    splits = gemm::make_problem(M, A, K, s).splits;
+    ld_part = (A + 3) / 4 * 4;
+    part.alloc(static_cast<size_t>(splits) * M * ld_part);
+  }
+};
+
+// The head GEMM: split-K partial tiles into hs.part (plans hs).
+inline Step head_gemm_step(HeadSplit& hs, const float* A0, int64_t lda, const float* W,
+                           int64_t ldw, int M, int N, int K) {
+  require(N <= 32, "policy head: act_dim <= 32");
+  hs.plan(M, N, K);
+  gemm::Operands ops;
+  std::memset(&ops, 0, sizeof(ops));
+  ops.a[0] = gemm::map_a(A0, M, K, lda, false, true);
+  ops.b[0] = gemm::map_b(W, N, K, ldw, true, 32, true);
+  ops.d[0] = make_tmap_3d(hs.part.p, N, M, hs.splits, hs.ld_part,
+                          static_cast<uint64_t>(M) * hs.ld_part, 32, 32, Swz::k128);
+  const gemm::Problem p = gemm::make_problem(M, N, K, hs.splits);
+  return [ops, p](cudaStream_t st) { gemm::launch<32, false, true>(ops, p, 1, epi::Partial{}, st); };
+}
+
+// The finish (bias, squash, noise, stores) of a planned head.
+inline Step head_finish_step(const HeadSplit& hs, head::FinishArgs fin, int M, int N) {
+  fin.part = hs.part.p;
+  fin.S = hs.splits;
+  fin.ld_part = hs.ld_part;
+  fin.M = M;
+  fin.A = N;
+  const int rows_blocks = (M + head::kFinishWarps - 1) / head::kFinishWarps;
+  const int blocks = rows_blocks < 4 * kSMs ? rows_blocks : 4 * kSMs;
+  return [fin, blocks](cudaStream_t st) {
+    launch(head::policy_head_finish_kernel, dim3(blocks), dim3(32 * head::kFinishWarps), 0, st,
+           fin);
+  };
 }
 
 // Bias-correction table bc[t] = (float(1/(1-0.9^t)), float(1/(1-0.999^t)))

@@ -185,20 +185,18 @@ void PLearner::build_update() {
       ld = H;
       K = H;
     }
-    epi::PolicyHead ph{};
+    head::FinishArgs ph{};
     ph.bias = pol_.p + pnet_.b_off[nh];
     ph.act = X_.p + D;  // critic input [norm(s) | pi(s)]
     ph.ld_act = Kp_;
     ph.tanh_out = T_.p;
     ph.ld_tanh = Ap_;
-    ph.M = B;
-    ph.A = A;
     ph.mid = (dims_.low + dims_.high) / 2.0f;
     ph.half = (dims_.high - dims_.low) / 2.0f;
     head_.init(pol_.p + pnet_.w_off[nh], H, A);
     head_.refresh(stream_);
-    const float* W = head_.ptr();
-    steps_.push_back(mlp::fwd(in, in, ld, W, W, B, A, H, 1, ph, head_.stride()));
+    steps_.push_back(mlp::head_gemm_step(head_split_, in, ld, head_.ptr(), head_.stride(), B, A, H));
+    steps_.push_back(mlp::head_finish_step(head_split_, ph, B, A));
   }
 
   // ------------------------------------------ twin critic replicas forward
@@ -528,7 +526,9 @@ bool PLearner::ready(int64_t c_a) {
 }
 
 void PLearner::enqueue() {
-  for (auto& s : steps_) s(stream_);
+  const int skip = skip_step();
+  for (size_t i = 0; i < steps_.size(); ++i)
+    if (static_cast<int>(i) != skip) steps_[i](stream_);
 }
 
 int PLearner::check_status() {

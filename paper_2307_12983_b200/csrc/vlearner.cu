@@ -201,18 +201,17 @@ void VLearner::build_update() {
       ld = H;
       K = H;
     }
-    epi::PolicyHead ph{};
+    head::FinishArgs ph{};
     ph.bias = lagged_.p + pnet_.b_off[nh];
     ph.act = Xtg_.p + D;  // critic target input [norm(boot) | pi(boot)]
     ph.ld_act = Kp_;
-    ph.M = B;
-    ph.A = A;
     ph.mid = (dims_.low + dims_.high) / 2.0f;
     ph.half = (dims_.high - dims_.low) / 2.0f;
     lagged_head_.init(lagged_.p + pnet_.w_off[nh], H, A);
     lagged_head_.refresh(stream_);
-    const float* W = lagged_head_.ptr();
-    steps_.push_back(mlp::fwd(in, in, ld, W, W, B, A, H, 1, ph, lagged_head_.stride()));
+    steps_.push_back(mlp::head_gemm_step(head_split_, in, ld, lagged_head_.ptr(),
+                                         lagged_head_.stride(), B, A, H));
+    steps_.push_back(mlp::head_finish_step(head_split_, ph, B, A));
   }
 
   // ---------- twin target + twin online critics: one 4-group launch per layer
@@ -576,7 +575,9 @@ void VLearner::prepare_indices() {
 }
 
 void VLearner::enqueue() {
-  for (auto& s : steps_) s(stream_);
+  const int skip = skip_step();
+  for (size_t i = 0; i < steps_.size(); ++i)
+    if (static_cast<int>(i) != skip) steps_[i](stream_);
 }
 
 int VLearner::check_status() {

@@ -29,6 +29,27 @@ extern "C" __attribute__((visibility("default"))) int trace_gemm(
       e.store = store ? 0xF : 0;
       for (int i = 0; i < iters; ++i) gemm::launch<256, false, true>(ops, p, groups, e, st);
     } else {
+      if (kind == 2) {
+        // in situ: the preceding hidden layer writes the head's input (A)
+        // right before the head, as in the update / actor step
+        PQLG_CUDA(cudaMemcpyToSymbol(gemm::g_trace, &trace, sizeof(trace)));
+        unsigned long long* none = nullptr;
+        PQLG_CUDA(cudaMemcpyToSymbol(gemm::g_trace, &none, sizeof(none)));
+        gemm::Operands h;
+        for (int g = 0; g < 4; ++g) {
+          h.a[g] = gemm::map_a(D, M, K, K, false, true);  // D doubles as the hidden input
+          h.b[g] = gemm::map_b(B, K, K, K, true, 256, true);
+          h.d[g] = make_store_map(const_cast<float*>(A), M, K, K);
+        }
+        epi::Hidden e{};
+        for (int g = 0; g < 4; ++g) e.bias[g] = bias;
+        e.bn = 256;
+        e.M = M;
+        e.N = K;
+        e.store = 1;
+        gemm::launch<256, false, true>(h, gemm::make_problem(M, K, K, 1), 1, e, st);
+        PQLG_CUDA(cudaMemcpyToSymbol(gemm::g_trace, &trace, sizeof(trace)));
+      }
       ops.a[0] = ops.a[1] = ops.a[2] = ops.a[3] = gemm::map_a(A, M, K, K, false, true);
       ops.b[0] = ops.b[1] = gemm::map_b(B, N, K, N, true, 32, true);
       epi::PolicyHead e{};

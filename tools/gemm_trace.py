@@ -30,9 +30,12 @@ KIND = int(os.environ.get("TRACE_KIND", "0"))
 shapes = ([(8192, 512, 512, 1), (8192, 512, 512, 2), (8192, 512, 512, 4), (8192, 512, 232, 4),
            (16384, 512, 512, 1), (8192, 512, 4096, 1)] if KIND == 0
           else [(8192, 20, 512, 1), (16384, 20, 512, 1)])
+if KIND == 2:
+    shapes = [(8192, 20, 512, 1), (16384, 20, 512, 1)]
 for (M, N, K, groups) in shapes:
-    a = torch.randn(M, K, device="cuda"); w = torch.randn(K, (N + 3) // 4 * 4, device="cuda")
-    d = torch.empty(M, N, device="cuda"); bias = torch.zeros(N, device="cuda")
+    a = torch.randn(M, K, device="cuda")
+    w = torch.randn(K, max(K, (N + 3) // 4 * 4), device="cuda")  # kind 2: hidden W [K x K]
+    d = torch.randn(M, max(N, K), device="cuda"); bias = torch.zeros(max(N, K), device="cuda")
     bn = 256 if KIND == 0 else 32
     ctas = min((M // 128) * ((N + bn - 1) // bn) * groups, 148)
     tr = torch.zeros(ctas * 8, dtype=torch.int64, device="cuda")
