@@ -433,6 +433,32 @@ PQLG_API int pqlg_k_normalizer_update(int64_t* count_dev, double* mean_dev, doub
                                       const float* batch_dev, int64_t ld, int rows, int dim,
                                       float* mean_f_dev, float* inv_f_dev, void* stream);
 
+/* ------------------------------------------------------------ checkpoints
+ * The reference's on-disk format, byte for byte (fa::save_checkpoint /
+ * load_checkpoint, src/funcapprox/checkpoint.cpp:35-91): "PQLCKPT\x01",
+ * named nets (layer sizes, u8 activations: ReLU hidden, identity output,
+ * flat f32 params in Mlp layout), then the normalizer (dim, count, mean, m2).
+ * IO / format errors -> PQLG_EINVAL. */
+PQLG_API int pqlg_checkpoint_write(const char* path, int n_nets, const char* const* names,
+                                   const int32_t* n_layers, const int32_t* const* sizes,
+                                   const float* const* flats, int64_t count, const double* mean,
+                                   const double* m2, int dim);
+/* Reads every net's parameters concatenated in file order into flat_out
+ * (nullable: sizes only) and the normalizer (mean / m2 nullable). */
+PQLG_API int pqlg_checkpoint_read(const char* path, int* n_nets, int64_t* n_params,
+                                  float* flat_out, int64_t* count, double* mean, double* m2,
+                                  int* dim);
+/* Cores: V-learner nets "q1" "q2" "q1_target" "q2_target" "policy" (lagged),
+ * P-learner "policy" "q1" "q2", actor "policy"; the normalizer is the one the
+ * core last adopted (the actor's own running stats).  load restores the nets
+ * by name (shape-checked) and adopts the normalizer. */
+PQLG_API int pqlg_vlearner_save(pqlg_vlearner h, const char* path);
+PQLG_API int pqlg_vlearner_load(pqlg_vlearner h, const char* path);
+PQLG_API int pqlg_plearner_save(pqlg_plearner h, const char* path);
+PQLG_API int pqlg_plearner_load(pqlg_plearner h, const char* path);
+PQLG_API int pqlg_actor_save(pqlg_actor h, const char* path);
+PQLG_API int pqlg_actor_load(pqlg_actor h, const char* path);
+
 #ifdef __cplusplus
 }
 #endif

@@ -312,6 +312,32 @@ def gen_c51update(R, out):
     out.update(cpu_losses=pl, cpu_params=pp)
 
 
+def ckpt_content(seed=9):
+    """A small checkpoint payload: three nets of the learners' shapes + stats."""
+    rng = np.random.default_rng(seed)
+    nets = [("q1", [9, 32, 32, 1]), ("q2", [9, 32, 32, 1]), ("policy", [5, 32, 32, 4])]
+    flats = [f32(rng.standard_normal(param_count(sz))) for _, sz in nets]
+    mean = rng.standard_normal(5)
+    m2 = np.abs(rng.standard_normal(5)) * 100
+    return nets, flats, 1234, mean, m2
+
+
+def gen_checkpoint(R, out):
+    """fa::save_checkpoint output for ckpt_content(), kept as raw bytes
+    (tests/golden/ckpt_ref.bin) to pin the writer byte for byte."""
+    import ctypes as C
+    nets, flats, count, mean, m2 = ckpt_content()
+    names = (C.c_char_p * len(nets))(*[n.encode() for n, _ in nets])
+    nl = np.array([len(sz) - 1 for _, sz in nets], np.uint64)
+    szs = [np.array(sz, np.uint64) for _, sz in nets]
+    szp = (C.c_void_p * len(nets))(*[a.ctypes.data for a in szs])
+    fp = (C.c_void_p * len(nets))(*[a.ctypes.data for a in flats])
+    path = str(GOLDEN / "ckpt_ref.bin")
+    assert R.ref_checkpoint_save(path.encode(), len(nets), names, nl.ctypes.data, szp, fp, count,
+                                 ptr(mean), ptr(m2), 5) == 0
+    out.update(ck_dummy=np.zeros(1))
+
+
 def main():
     R = ref()
     if R is None:
@@ -320,11 +346,13 @@ def main():
     for name, fn in [("indices", gen_indices), ("nstep", gen_nstep),
                      ("elementwise", gen_elementwise), ("norm", gen_norm), ("noise", gen_noise),
                      ("mlp", gen_mlp), ("agents", gen_agents), ("vupdate", gen_vupdate),
-                     ("c51update", gen_c51update)]:
+                     ("c51update", gen_c51update), ("checkpoint", gen_checkpoint)]:
         if len(sys.argv) > 1 and name not in sys.argv[1:]:
             continue
         out: dict = {}
         fn(R, out)
+        if name == "checkpoint":  # raw bytes only (ckpt_ref.bin)
+            continue
         np.savez_compressed(GOLDEN / f"{name}.npz", **out)
         print(name, sum(v.nbytes for v in out.values()), "bytes")
 

@@ -15,6 +15,7 @@
 #include "pql/agents/c51.hpp"
 #include "pql/agents/ddpg.hpp"
 #include "pql/explore/noise.hpp"
+#include "pql/funcapprox/checkpoint.hpp"
 #include "pql/funcapprox/normalizer.hpp"
 #include "pql/funcapprox/optim.hpp"
 #include "pql/kernels/kernels.hpp"
@@ -704,4 +705,46 @@ REF_API void ref_policy_init(size_t D, size_t A, size_t hidden, uint64_t seed, f
   auto rng = make_rng(seed, RngStream::init, 0);
   auto p = rt::PolicyHandle::create(cfg, dims, rng);
   std::memcpy(out, p.net().flat.data(), p.net().flat.size() * sizeof(float));
+}
+
+// ------------------------------------------------------------ checkpoints
+// fa::save_checkpoint / load_checkpoint (src/funcapprox/checkpoint.cpp):
+// nets given as (name, n_layers, sizes[n_layers + 1], flat) with ReLU hidden
+// layers and an identity output layer (the Mlp shapes of learners.cpp).
+REF_API int ref_checkpoint_save(const char* path, int n_nets, const char* const* names,
+                                const size_t* n_layers, const size_t* const* sizes,
+                                const float* const* flats, int64_t count, const double* mean,
+                                const double* m2, size_t dim) {
+  try {
+    fa::Checkpoint c;
+    for (int k = 0; k < n_nets; ++k)
+      c.nets.emplace_back(names[k], make_mlp(sizes[k], n_layers[k], flats[k]));
+    c.norm = make_stats(count, mean, m2, dim);
+    fa::save_checkpoint(path, c);
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+
+// Parameters of every net concatenated in file order; returns the net count
+// (or -1); *n_params / *dim report sizes when the output pointers are null.
+REF_API int ref_checkpoint_load(const char* path, float* flat_out, size_t* n_params,
+                                int64_t* count, double* mean, double* m2, size_t* dim) {
+  try {
+    const fa::Checkpoint c = fa::load_checkpoint(path);
+    size_t total = 0;
+    for (const auto& [name, net] : c.nets) {
+      if (flat_out) std::memcpy(flat_out + total, net.flat.data(), net.flat.size() * 4);
+      total += net.flat.size();
+    }
+    *n_params = total;
+    *dim = c.norm.dim();
+    *count = c.norm.count;
+    if (mean) std::memcpy(mean, c.norm.mean.data(), c.norm.dim() * 8);
+    if (m2) std::memcpy(m2, c.norm.m2.data(), c.norm.dim() * 8);
+    return static_cast<int>(c.nets.size());
+  } catch (...) {
+    return -1;
+  }
 }

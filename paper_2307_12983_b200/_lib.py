@@ -161,6 +161,14 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_actor_policy_version": (i32, [vp, P(i64)]),
     "pqlg_actor_read": (i32, [vp, i32, vp]),
     "pqlg_actor_kernels_per_step": (i32, [vp, P(i32)]),
+    "pqlg_checkpoint_write": (i32, [C.c_char_p, i32, vp, vp, vp, vp, i64, vp, vp, i32]),
+    "pqlg_checkpoint_read": (i32, [C.c_char_p, P(i32), P(i64), vp, P(i64), vp, vp, P(i32)]),
+    "pqlg_vlearner_save": (i32, [vp, C.c_char_p]),
+    "pqlg_vlearner_load": (i32, [vp, C.c_char_p]),
+    "pqlg_plearner_save": (i32, [vp, C.c_char_p]),
+    "pqlg_plearner_load": (i32, [vp, C.c_char_p]),
+    "pqlg_actor_save": (i32, [vp, C.c_char_p]),
+    "pqlg_actor_load": (i32, [vp, C.c_char_p]),
     "pqlg_ratio_config_default": (None, [P(RatioConfig)]),
     "pqlg_ratio_may_proceed": (i32, [i32, i64, i64, i64, P(RatioConfig)]),
     "pqlg_pipeline_create": (i32, [P(Config), P(TaskDims), P(RatioConfig), u64, P(vp)]),

@@ -328,6 +328,16 @@ void Actor::adopt_policy(const float* flat, int64_t version, bool device) {
   version_ = version;
 }
 
+void Actor::set_norm(int64_t count, const double* mean, const double* m2) {
+  PQLG_CUDA(cudaMemcpyAsync(count_.p, &count, 8, cudaMemcpyHostToDevice, stream_));
+  PQLG_CUDA(cudaMemcpyAsync(mean_.p, mean, D_ * 8, cudaMemcpyHostToDevice, stream_));
+  PQLG_CUDA(cudaMemcpyAsync(m2_.p, m2, D_ * 8, cudaMemcpyHostToDevice, stream_));
+  launch_norm_consts(count_.p, mean_.p, m2_.p, D_, mean_f_.p, inv_f_.p, identity_.p, stream_);
+  launch(actor::normalize_kernel, dim3(4 * mlp::kSMs), dim3(256), 0, stream_, obs_[cur_].p, Dp_,
+         Xn_.p, Dp_, mean_f_.p, inv_f_.p, identity_.p, N_, D_);
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+}
+
 void Actor::norm(int64_t* count, double* mean, double* m2) {
   PQLG_CUDA(cudaMemcpyAsync(count, count_.p, 8, cudaMemcpyDeviceToHost, stream_));
   if (mean) PQLG_CUDA(cudaMemcpyAsync(mean, mean_.p, D_ * 8, cudaMemcpyDeviceToHost, stream_));
@@ -367,6 +377,13 @@ void Actor::read_state(int what, void* out) {
 struct pqlg_actor_s {
   std::unique_ptr<pqlg::Actor> a;
 };
+
+namespace pqlg {
+Actor* actor_of(pqlg_actor h) {
+  require(h != nullptr, "null actor handle");
+  return h->a.get();
+}
+}  // namespace pqlg
 struct pqlg_env_s {
   std::unique_ptr<pqlg::DeviceEnv> e;
   pqlg::DevBuf<uint32_t> status;

@@ -31,6 +31,10 @@ class Actor {
   // device views for the pipeline (run_parallel): the running normalizer
   // (owned by the actor, SPEC "Normalizer statistics are owned by the Actor")
   const float* policy_dev() const { return pol_.p; }
+  const NetShape& policy_shape() const { return pnet_; }
+  // restore the running normalizer (checkpoint load) and re-normalize the
+  // current observations for the next policy input
+  void set_norm(int64_t count, const double* mean, const double* m2);
   const int64_t* count_dev() const { return count_.p; }
   const double* mean_dev() const { return mean_.p; }
   const double* m2_dev() const { return m2_.p; }

@@ -30,9 +30,14 @@ class VLearner {
     norm_.set_device(count, mean, m2, stream_);
   }
   const float* critic_dev(int k) const { return q_.p + k * Ps_; }
+  const NetShape& policy_shape() const { return pnet_; }
+  const NetShape& critic_shape() const { return qnet_; }
   int64_t critic_params() const { return qnet_.params; }
   int64_t policy_params() const { return pnet_.params; }
   int64_t lagged_version() const { return lagged_version_; }
+  // NormStats last adopted from the host (checkpointing)
+  int64_t norm_count_ = 0;
+  std::vector<double> norm_mean_, norm_m2_;
   void ingest(const replay::Slice& s);
   void ingest_host(const pqlg_step_slice& host);  // copy-in path for a host StepSlice
   bool ready(int64_t c_a);
@@ -136,6 +141,10 @@ class PLearner {
   }
   int64_t policy_params() const { return pnet_.params; }
   int64_t critic_params() const { return qnet_.params; }
+  const NetShape& policy_shape() const { return pnet_; }
+  const NetShape& critic_shape() const { return qnet_; }
+  int64_t norm_count_ = 0;  // NormStats last adopted from the host (checkpointing)
+  std::vector<double> norm_mean_, norm_m2_;
   void ingest(const float* states_dev, int64_t ld, uint64_t n);
   void ingest_host(const float* states_host, int64_t ld, uint64_t n);
   bool ready(int64_t c_a);

@@ -502,6 +502,9 @@ void PLearner::adopt_critics_device(const float* q1, const float* q2, int64_t ve
 }
 
 void PLearner::adopt_norm(int64_t count, const double* mean, const double* m2) {
+  norm_count_ = count;
+  norm_mean_.assign(mean, mean + D_);
+  norm_m2_.assign(m2, m2 + D_);
   norm_.set(count, mean, m2, stream_);
 }
 
@@ -625,6 +628,13 @@ int64_t PLearner::param_count(int which) const {
 struct pqlg_plearner_s {
   std::unique_ptr<pqlg::PLearner> p;
 };
+
+namespace pqlg {
+PLearner* plearner_of(pqlg_plearner h) {
+  require(h != nullptr, "null plearner handle");
+  return h->p.get();
+}
+}  // namespace pqlg
 
 using namespace pqlg;
 

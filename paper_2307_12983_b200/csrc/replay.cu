@@ -58,10 +58,15 @@ __global__ void norm_consts_kernel(const int64_t* count, const double* mean, con
 }
 }  // namespace
 
+void launch_norm_consts(const int64_t* count, const double* mean, const double* m2, int D,
+                        float* mean_f, float* inv_f, int* ident, cudaStream_t st) {
+  launch(norm_consts_kernel, dim3((D + 255) / 256), dim3(256), 0, st, count, mean, m2, D, mean_f,
+         inv_f, ident);
+}
+
 void DeviceNorm::set_device(const int64_t* count, const double* m, const double* m2,
                             cudaStream_t st) {
-  launch(norm_consts_kernel, dim3((D + 255) / 256), dim3(256), 0, st, count, m, m2, D, mean.p,
-         inv.p, ident.p);
+  launch_norm_consts(count, m, m2, D, mean.p, inv.p, ident.p, st);
 }
 
 }  // namespace pqlg

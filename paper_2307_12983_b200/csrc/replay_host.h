@@ -12,6 +12,10 @@
 namespace pqlg {
 
 // fp32 normalization constants on device (normalizer.hpp:56-70).
+// (mean_f, inv_f, identity) from device NormStats, normalizer.hpp:62-66.
+void launch_norm_consts(const int64_t* count, const double* mean, const double* m2, int D,
+                        float* mean_f, float* inv_f, int* ident, cudaStream_t st);
+
 struct DeviceNorm {
   DevBuf<float> mean, inv;
   DevBuf<int> ident;  // device flag: kernels (and captured graphs) read it at run time

@@ -527,6 +527,9 @@ void VLearner::adopt_policy_device(const float* flat, int64_t version) {
 }
 
 void VLearner::adopt_norm(int64_t count, const double* mean, const double* m2) {
+  norm_count_ = count;
+  norm_mean_.assign(mean, mean + D_);
+  norm_m2_.assign(m2, m2 + D_);
   norm_.set(count, mean, m2, stream_);
 }
 
@@ -718,6 +721,13 @@ struct pqlg_vlearner_s {
   std::unique_ptr<pqlg::VLearner> v;
   pqlg_replay_s replay_view;
 };
+
+namespace pqlg {
+VLearner* vlearner_of(pqlg_vlearner h) {
+  require(h != nullptr, "null vlearner handle");
+  return h->v.get();
+}
+}  // namespace pqlg
 
 using namespace pqlg;
 
