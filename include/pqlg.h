@@ -409,6 +409,17 @@ PQLG_API int pqlg_pipeline_run(pqlg_pipeline h, int64_t actor_steps, double max_
                                pqlg_run_report* out);
 PQLG_API int pqlg_pipeline_destroy(pqlg_pipeline h);
 
+/* evaluate_policy (learners.cpp:280-325) on the synthetic task: a fresh env
+ * of `episodes` rows seeded with eval_seed, each row one full episode of the
+ * deterministic policy (flat host params, cfg->hidden / hidden_layers /
+ * max_episode_len) on apply_stats(norm, obs); mean and standard error of the
+ * undiscounted returns (returns_host nullable [episodes]).  episodes < 1 ->
+ * PQLG_EINVAL. */
+PQLG_API int pqlg_evaluate(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                           const float* policy_host, const pqlg_norm_stats* norm, int episodes,
+                           uint64_t eval_seed, double* returns_host, double* mean,
+                           double* stderr_out);
+
 /* The synthetic EnvBatch on its own (vecenv.hpp:44-81 contract). */
 PQLG_API int pqlg_env_create(int n_envs, int obs_dim, int act_dim, uint64_t seed,
                              int max_episode_len, int env_offset, float low, float high,

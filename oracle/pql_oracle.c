@@ -1120,3 +1120,52 @@ int orc_env_step(orc_env* e, const float* actions, float* next_obs, float* termi
   }
   return 0;
 }
+
+/* evaluate_policy (learners.cpp:280-325): see pql_oracle.h. */
+int orc_evaluate(const float* pol, const size_t* psizes, size_t n_layers, int64_t count,
+                 const double* mean, const double* m2, size_t episodes, uint64_t eval_seed,
+                 size_t obs_dim, size_t act_dim, float low, float high, size_t max_len,
+                 double* returns, double* mean_out, double* stderr_out) {
+  if (episodes < 1) return -1;
+  const size_t N = episodes, D = obs_dim, A = act_dim;
+  orc_env* e = orc_env_create(N, D, A, eval_seed, max_len);
+  for (size_t i = 0; i < N; ++i) e->episode_step[i] = 0;  /* make_env: fresh episodes */
+  float* obs = (float*)malloc(N * D * sizeof(float));
+  float* obs_n = (float*)malloc(N * D * sizeof(float));
+  float* act = (float*)malloc(N * A * sizeof(float));
+  float* nxt = (float*)malloc(N * D * sizeof(float));
+  float* term_obs = (float*)malloc(N * D * sizeof(float));
+  float* rew = (float*)malloc(N * sizeof(float));
+  uint8_t* done = (uint8_t*)malloc(N);
+  uint8_t* trunc = (uint8_t*)malloc(N);
+  uint8_t* finished = (uint8_t*)calloc(N, 1);
+  orc_env_observe(e, obs);
+  for (size_t i = 0; i < N; ++i) returns[i] = 0.0;
+  size_t remaining = N;
+  for (size_t step = 0; step < max_len && remaining > 0; ++step) {
+    orc_normalize_apply(count, mean, m2, obs, obs_n, N, D);
+    orc_policy_act(pol, psizes, n_layers, obs_n, N, low, high, act);
+    orc_env_step(e, act, nxt, term_obs, rew, done, trunc);
+    for (size_t i = 0; i < N; ++i) {
+      if (finished[i]) continue;
+      returns[i] += rew[i];
+      if (done[i]) {
+        finished[i] = 1;
+        --remaining;
+      }
+    }
+    memcpy(obs, nxt, N * D * sizeof(float));
+  }
+  double mu = 0.0;
+  for (size_t i = 0; i < N; ++i) mu += returns[i];
+  mu /= (double)N;
+  double var = 0.0;
+  for (size_t i = 0; i < N; ++i) var += (returns[i] - mu) * (returns[i] - mu);
+  var = N > 1 ? var / (double)(N - 1) : 0.0;
+  *mean_out = mu;
+  *stderr_out = sqrt(var / (double)N);
+  free(obs); free(obs_n); free(act); free(nxt); free(term_obs); free(rew); free(done);
+  free(trunc); free(finished);
+  orc_env_destroy(e);
+  return 0;
+}

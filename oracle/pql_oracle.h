@@ -191,6 +191,14 @@ typedef struct {
 orc_env* orc_env_create(size_t n_envs, size_t obs_dim, size_t act_dim, uint64_t seed,
                         size_t max_len);
 void orc_env_destroy(orc_env* e);
+/* evaluate_policy (learners.cpp:280-325) on the synthetic task: a fresh env
+ * of `episodes` rows (seed eval_seed, episode steps from 0), deterministic
+ * policy on apply_stats(norm, obs), one episode per row; returns[episodes]
+ * (double), mean and standard error as the reference computes them. */
+int orc_evaluate(const float* pol, const size_t* psizes, size_t n_layers, int64_t count,
+                 const double* mean, const double* m2, size_t episodes, uint64_t eval_seed,
+                 size_t obs_dim, size_t act_dim, float low, float high, size_t max_len,
+                 double* returns, double* mean_out, double* stderr_out);
 void orc_env_observe(const orc_env* e, float* obs);
 /* EnvBatch::step contract (vecenv.cpp:84-106); returns -2 on non-finite
  * action (runtime_error in the reference). */

@@ -169,6 +169,8 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_plearner_load": (i32, [vp, C.c_char_p]),
     "pqlg_actor_save": (i32, [vp, C.c_char_p]),
     "pqlg_actor_load": (i32, [vp, C.c_char_p]),
+    "pqlg_evaluate": (i32, [P(Config), P(TaskDims), vp, P(NormStats), i32, u64, vp, P(f64),
+                            P(f64)]),
     "pqlg_ratio_config_default": (None, [P(RatioConfig)]),
     "pqlg_ratio_may_proceed": (i32, [i32, i64, i64, i64, P(RatioConfig)]),
     "pqlg_pipeline_create": (i32, [P(Config), P(TaskDims), P(RatioConfig), u64, P(vp)]),

@@ -371,6 +371,131 @@ void Actor::read_state(int what, void* out) {
   PQLG_CUDA(cudaStreamSynchronize(st));
 }
 
+// ------------------------------------------------------------ evaluation
+// evaluate_policy (learners.cpp:280-325) on the synthetic task: a fresh env
+// of `episodes` rows (seed eval_seed, every row starting a full episode),
+// the deterministic policy on apply_stats(snapshot norm, obs), one episode
+// per row, returns accumulated in double until each row's first done.
+namespace {
+__global__ void eval_accumulate_kernel(const float* rew, const uint8_t* term,
+                                       const uint8_t* trunc, int N, double* ret,
+                                       uint8_t* finished, unsigned int* n_finished) {
+  pdl::entry();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    if (finished[i]) continue;
+    ret[i] += static_cast<double>(rew[i]);
+    if (term[i] || trunc[i]) {
+      finished[i] = 1;
+      atomicAdd(n_finished, 1u);
+    }
+  }
+}
+}  // namespace
+
+void evaluate_policy(const pqlg_config& cfg, const pqlg_task_dims& dims, const float* policy,
+                     int64_t count, const double* mean, const double* m2, int episodes,
+                     uint64_t eval_seed, double* returns, double* mean_out, double* stderr_out) {
+  require(episodes >= 1, "evaluate: episodes must be >= 1");  // learners.cpp:282
+  const int N = episodes, D = dims.obs_dim, A = dims.act_dim, H = cfg.hidden;
+  const int nh = cfg.hidden_layers;
+  require(A <= 32, "evaluate: act_dim > 32 not supported");
+  cudaStream_t st;
+  PQLG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+  } guard{st};
+  std::vector<int> ps{D};
+  for (int l = 0; l < nh; ++l) ps.push_back(H);
+  ps.push_back(A);
+  const NetShape pnet = NetShape::make(ps);
+  DevBuf<float> pol(pnet.params);
+  PQLG_CUDA(cudaMemcpy(pol.p, policy, pnet.params * 4, cudaMemcpyHostToDevice));
+  DeviceEnv env(N, D, A, eval_seed, cfg.max_episode_len, 0, dims.low, dims.high);
+  const int64_t Dp = round_up(D, 4), Ap = round_up(A, 4);
+  DevBuf<float> obs[2], boot, rew, act, Xn;
+  for (auto& o : obs) o.alloc(static_cast<size_t>(N) * Dp);
+  boot.alloc(static_cast<size_t>(N) * Dp);
+  rew.alloc(N);
+  act.alloc(static_cast<size_t>(N) * Ap);
+  Xn.alloc(static_cast<size_t>(N) * Dp);
+  DevBuf<uint8_t> flags(3ull * N);  // term | trunc | finished
+  DevBuf<double> ret(N);
+  DevBuf<unsigned int> n_fin(1);
+  DevBuf<uint32_t> status(1);
+  DeviceNorm norm;
+  norm.init(D);
+  norm.set(count, mean, m2, st);
+  env.reset(obs[0].p, Dp, st);
+  PQLG_CUDA(cudaMemsetAsync(env.ep.p, 0, N * 8, st));  // make_env: fresh episodes
+  launch(actor::normalize_kernel, dim3(4 * mlp::kSMs), dim3(256), 0, st, obs[0].p, Dp, Xn.p, Dp,
+         norm.mean.p, norm.inv.p, norm.ident.p, N, D);
+  // policy forward (hidden layers, squashing head without noise)
+  std::vector<DevBuf<float>> pact(nh);
+  std::vector<mlp::Step> steps;
+  const float* in = Xn.p;
+  int64_t ld = Dp;
+  int K = D;
+  for (int l = 0; l < nh; ++l) {
+    pact[l].alloc(static_cast<size_t>(N) * H);
+    epi::Hidden e{};
+    e.bias[0] = pol.p + pnet.b_off[l];
+    e.bn = mlp::bn_for(H);
+    e.M = N;
+    e.N = H;
+    e.store = 1;
+    const float* W = pol.p + pnet.w_off[l];
+    steps.push_back(mlp::fwd(in, in, ld, W, W, N, H, K, 1, e, 0, pact[l].p, pact[l].p, H));
+    in = pact[l].p;
+    ld = H;
+    K = H;
+  }
+  WeightMirror head;
+  head.init(pol.p + pnet.w_off[nh], H, A);
+  head.refresh(st);
+  epi::PolicyHead ph{};
+  ph.bias = pol.p + pnet.b_off[nh];
+  ph.act = act.p;
+  ph.ld_act = Ap;
+  ph.M = N;
+  ph.A = A;
+  ph.mid = (dims.low + dims.high) / 2.0f;
+  ph.half = (dims.high - dims.low) / 2.0f;
+  steps.push_back(mlp::fwd(in, in, ld, head.ptr(), head.ptr(), N, A, H, 1, ph, head.stride()));
+  const int blocks = std::min((N + 255) / 256, 4 * mlp::kSMs);
+  int cur = 0;
+  for (int step = 0; step < cfg.max_episode_len; ++step) {
+    for (auto& s : steps) s(st);
+    actor::StepOut o{obs[1 - cur].p, boot.p, rew.p, flags.p, flags.p + N, nullptr, Dp, status.p};
+    actor::NextNorm nn{Xn.p, Dp, norm.mean.p, norm.inv.p, norm.ident.p};
+    env.step(act.p, Ap, o, st, nn, obs[cur].p, Dp);
+    launch(eval_accumulate_kernel, dim3(blocks), dim3(256), 0, st, rew.p, flags.p, flags.p + N, N,
+           ret.p, flags.p + 2 * N, n_fin.p);
+    cur = 1 - cur;
+    if ((step & 15) == 15 || step + 1 == cfg.max_episode_len) {  // every row finished?
+      unsigned int fin = 0;
+      PQLG_CUDA(cudaMemcpyAsync(&fin, n_fin.p, 4, cudaMemcpyDeviceToHost, st));
+      PQLG_CUDA(cudaStreamSynchronize(st));
+      if (fin == static_cast<unsigned int>(N)) break;
+    }
+  }
+  std::vector<double> r(N);
+  PQLG_CUDA(cudaMemcpyAsync(r.data(), ret.p, N * 8, cudaMemcpyDeviceToHost, st));
+  uint32_t stv = 0;
+  PQLG_CUDA(cudaMemcpyAsync(&stv, status.p, 4, cudaMemcpyDeviceToHost, st));
+  PQLG_CUDA(cudaStreamSynchronize(st));
+  if (stv) throw Error(PQLG_ENONFINITE, "evaluate: non-finite action");
+  double mu = 0.0;
+  for (double x : r) mu += x;
+  mu /= static_cast<double>(N);
+  double var = 0.0;
+  for (double x : r) var += (x - mu) * (x - mu);
+  var = N > 1 ? var / static_cast<double>(N - 1) : 0.0;
+  if (returns) std::copy(r.begin(), r.end(), returns);
+  *mean_out = mu;
+  *stderr_out = std::sqrt(var / static_cast<double>(N));
+}
+
 }  // namespace pqlg
 
 // ------------------------------------------------------------------ C ABI
@@ -406,6 +531,16 @@ int pqlg_actor_create(const pqlg_config* cfg, const pqlg_task_dims* dims, void* 
 
 int pqlg_actor_destroy(pqlg_actor h) {
   return guarded([&] { delete h; });
+}
+
+int pqlg_evaluate(const pqlg_config* cfg, const pqlg_task_dims* dims, const float* policy_host,
+                  const pqlg_norm_stats* norm, int episodes, uint64_t eval_seed,
+                  double* returns_host, double* mean, double* stderr_out) {
+  return guarded([&] {
+    require(cfg && dims && policy_host && norm && mean && stderr_out, "evaluate: null argument");
+    evaluate_policy(*cfg, *dims, policy_host, norm->count, norm->mean, norm->m2, episodes,
+                    eval_seed, returns_host, mean, stderr_out);
+  });
 }
 
 int pqlg_actor_adopt_policy(pqlg_actor h, const float* flat, int64_t version) {

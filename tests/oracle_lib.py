@@ -65,6 +65,7 @@ _ORC_SIGS = {
                                    sz, f32, f32, vp, vp, vp, vp]),
     "orc_ddpg_actor_loss": (i32, [vp, vp, vp, vp, vp, sz, vp, sz, sz, sz, f32, f32, vp, vp]),
     "orc_c51_atoms": (None, [sz, f32, f32, vp]),
+    "orc_evaluate": (i32, [vp, vp, sz, i64, vp, vp, sz, u64, sz, sz, f32, f32, sz, vp, vp, vp]),
     "orc_c51_project": (i32, [vp, vp, vp, sz, sz, f32, f32, vp, vp]),
     "orc_c51_critic_loss": (i32, [vp, vp, vp, vp, vp, vp, vp, sz, vp, vp, vp, vp, vp, sz, sz,
                                   sz, f32, f32, sz, f32, f32, vp, vp, vp]),

@@ -110,3 +110,20 @@ int main(int argc, char**) {
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out
     assert out.stdout.strip() in ("einval", "runtime")
+
+
+def test_evaluate_rejects_zero_episodes_without_a_gpu():
+    """evaluate_policy throws invalid_argument for episodes < 1
+    (learners.cpp:282) before any device work."""
+    import ctypes as C
+    import numpy as np
+    from paper_2307_12983_b200 import _lib
+    cfg = _lib.default_config(hidden=32, hidden_layers=2)
+    dims = _lib.TaskDims(4, 2, -1.0, 1.0)
+    pol = np.zeros(1000, np.float32)
+    m = np.zeros(4)
+    ns = _lib.NormStats(0, m.ctypes.data, m.ctypes.data)
+    mu, se = C.c_double(), C.c_double()
+    rc = _lib.lib().pqlg_evaluate(C.byref(cfg), C.byref(dims), pol.ctypes.data, C.byref(ns), 0, 1,
+                                  None, C.byref(mu), C.byref(se))
+    assert rc == -1  # PQLG_EINVAL
