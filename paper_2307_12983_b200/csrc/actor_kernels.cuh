@@ -366,7 +366,7 @@ struct NormState {
 // advances the count.
 constexpr int kNormGroups = 128;
 constexpr int kNormRowsPerWarp = 16;  // rows per warp per group (N <= 8*16*kNormGroups in one pass)
-static __global__ void __launch_bounds__(256)
+static __global__ void __launch_bounds__(256, 4)
     norm_update_kernel(const float* __restrict__ x, int64_t ldx, int N, int D, double* partial,
                        unsigned int* ticket, NormState s) {
   pdl::entry();
@@ -420,7 +420,7 @@ static __global__ void __launch_bounds__(256)
   {
     double a1 = 0.0, a2 = 0.0;
     if (c < D) {
-      constexpr int kIn = 16;
+      constexpr int kIn = 4;
       for (int k0 = w; k0 < groups; k0 += 8 * kIn) {
         double v1[kIn], v2[kIn];
 #pragma unroll
