@@ -312,6 +312,82 @@ def gen_c51update(R, out):
     out.update(cpu_losses=pl, cpu_params=pp)
 
 
+def gen_sac(R, out):
+    """pql_sac: the eps stream (normal_distribution<float> over
+    make_rng(0, sac, 1)), GaussianPolicy::sample, k=3 V-learner and 3
+    P-learner updates (sac_critic_loss / sac_actor_loss / sac_alpha_loss,
+    learners.cpp:168-176, :246-258) and one stochastic actor step
+    (learners.cpp:87-94)."""
+    rng = np.random.default_rng(11)
+    nrm = np.zeros(1001, np.float32)
+    R.ref_normals(0, 6, 1, 1001, ptr(nrm))
+    out.update(sac_normals=nrm)
+    D, A, H, nh, B, cap = 9, 4, 32, 2, 48, 500
+    ps = [D] + [H] * nh + [2 * A]
+    qs = [D + A] + [H] * nh + [1]
+    pol = f32(rng.standard_normal(param_count(ps)) * 0.2)
+    q1 = f32(rng.standard_normal(param_count(qs)) * 0.2)
+    q2 = f32(rng.standard_normal(param_count(qs)) * 0.2)
+    # sample(): act / logp for a batch with a few log_std values clamped
+    obs = f32(rng.standard_normal((64, D)))
+    eps = f32(rng.standard_normal((64, A)))
+    act = np.zeros((64, A), np.float32)
+    logp = np.zeros(64, np.float32)
+    assert R.ref_gauss_sample(ptr(pol), ptr(sizes_arr(ps)), nh + 1, ptr(obs), ptr(eps), 64, None,
+                              None, ptr(act), ptr(logp), None) == 0
+    out.update(gs_obs=obs, gs_eps=eps, gs_act=act, gs_logp=logp)
+    n_rows = 300
+    obs = f32(rng.standard_normal((n_rows, D))); act = f32(rng.uniform(-1, 1, (n_rows, A)))
+    boot = f32(rng.standard_normal((n_rows, D))); ret = f32(rng.standard_normal(n_rows) * 2.0)
+    eff = f32(np.where(rng.uniform(size=n_rows) < 0.05, 0.0, 0.970299))
+    cnt = 1000; mean = rng.standard_normal(D) * 0.1; m2 = np.abs(rng.standard_normal(D)) * cnt
+    log_alpha = np.float32(-0.7)
+    h = R.ref_vupdate_create(D, A, H, nh, B, cap, 0, ptr(q1), ptr(q2), ptr(pol), 2, 1,
+                             np.float32(-10), np.float32(10))
+    R.ref_vupdate_set_log_alpha(h, log_alpha)
+    R.ref_vupdate_insert(h, ptr(obs), ptr(act), ptr(boot), ptr(ret), ptr(eff), n_rows)
+    R.ref_vupdate_adopt_norm(h, cnt, ptr(mean), ptr(m2))
+    losses = np.zeros(3, np.float32)
+    for k in range(3):
+        l = np.zeros(1, np.float32)
+        assert R.ref_vupdate_step(h, ptr(l)) == 0
+        losses[k] = l[0]
+    P = param_count(qs)
+    res = np.zeros((4, P), np.float32)
+    for w in range(4):
+        R.ref_vupdate_params(h, w, ptr(res[w]))
+    R.ref_vupdate_destroy(h)
+    out.update(su_dims=np.array([D, A, H, nh, B, cap]), su_pol=pol, su_q1=q1, su_q2=q2,
+               su_obs=obs, su_act=act, su_boot=boot, su_ret=ret, su_eff=eff,
+               su_norm=np.array([cnt]), su_mean=mean, su_m2=m2, su_log_alpha=np.array([log_alpha]),
+               su_losses=losses, su_params=res)
+    h = R.ref_pupdate_create(D, A, H, nh, B, cap, 0, ptr(pol), ptr(q1), ptr(q2), 2, 1,
+                             np.float32(-10), np.float32(10))
+    R.ref_pupdate_insert(h, ptr(obs), n_rows)
+    R.ref_pupdate_adopt_norm(h, cnt, ptr(mean), ptr(m2))
+    pl = np.zeros(3, np.float32)
+    la = np.zeros(3, np.float32)
+    for k in range(3):
+        l = np.zeros(1, np.float32)
+        assert R.ref_pupdate_step(h, ptr(l)) == 0
+        pl[k] = l[0]
+        la[k] = R.ref_pupdate_log_alpha(h)
+    pp = np.zeros(param_count(ps), np.float32)
+    R.ref_pupdate_params(h, ptr(pp))
+    R.ref_pupdate_destroy(h)
+    out.update(sp_losses=pl, sp_log_alpha=la, sp_params=pp)
+    # one stochastic actor step on N envs (normalizer seeded by one observe)
+    N = 40
+    a = R.ref_actor_create_sac(N, D, A, H, nh, 0, ptr(pol))
+    o0 = f32(rng.standard_normal((N, D)))
+    R.ref_actor_observe(a, ptr(o0))
+    o1 = f32(rng.standard_normal((N, D)))
+    acts = np.zeros((N, A), np.float32)
+    R.ref_actor_act(a, ptr(o1), ptr(acts))
+    R.ref_actor_destroy(a)
+    out.update(sa_obs0=o0, sa_obs1=o1, sa_act=acts)
+
+
 def ckpt_content(seed=9):
     """A small checkpoint payload: three nets of the learners' shapes + stats."""
     rng = np.random.default_rng(seed)
@@ -346,7 +422,8 @@ def main():
     for name, fn in [("indices", gen_indices), ("nstep", gen_nstep),
                      ("elementwise", gen_elementwise), ("norm", gen_norm), ("noise", gen_noise),
                      ("mlp", gen_mlp), ("agents", gen_agents), ("vupdate", gen_vupdate),
-                     ("c51update", gen_c51update), ("checkpoint", gen_checkpoint)]:
+                     ("c51update", gen_c51update), ("sac", gen_sac),
+                     ("checkpoint", gen_checkpoint)]:
         if len(sys.argv) > 1 and name not in sys.argv[1:]:
             continue
         out: dict = {}

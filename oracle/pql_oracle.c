@@ -684,20 +684,14 @@ int orc_ddpg_target(const float* pol, const size_t* psizes, const float* q1t, co
   return rc;
 }
 
-/* ddpg_critic_loss (ddpg.hpp:50-76) */
-int orc_ddpg_critic_loss(const float* pol, const size_t* psizes, const float* q1p, const float* q2p,
-                         const float* q1t, const float* q2t, const size_t* qsizes,
-                         size_t n_layers, const float* obs_norm, const float* act,
-                         const float* boot_norm, const float* ret, const float* eff, size_t B,
-                         size_t obs_dim, size_t act_dim, float low, float high, float* loss_out,
-                         float* y_out, float* dq1, float* dq2) {
-  float* y = y_out ? y_out : (float*)malloc(B * sizeof(float));
-  int rc = orc_ddpg_target(pol, psizes, q1t, q2t, qsizes, n_layers, boot_norm, ret, eff, B,
-                           obs_dim, act_dim, low, high, y);
-  if (rc) {
-    if (!y_out) free(y);
-    return rc;
-  }
+/* The regression half shared by ddpg_critic_loss (ddpg.hpp:58-76) and
+ * sac_critic_loss (sac.hpp:43-62): online twin forward on [obs | act], loss
+ * = mean(e1^2 + e2^2), upstream 2e/B, backward into dq1/dq2 (zeroed here). */
+static int critic_regress(const float* q1p, const float* q2p, const size_t* qsizes,
+                          size_t n_layers, const float* obs_norm, const float* act,
+                          const float* y, size_t B, size_t obs_dim, size_t act_dim,
+                          float* loss_out, float* dq1, float* dq2) {
+  int rc = 0;
   float* xq = concat_cols(obs_norm, obs_dim, act, act_dim, B);
   uint8_t acts[16];
   for (size_t l = 0; l < n_layers; ++l) acts[l] = (uint8_t)(l + 1 < n_layers);
@@ -729,6 +723,22 @@ int orc_ddpg_critic_loss(const float* pol, const size_t* psizes, const float* q1
     orc_mlp_backward(q2p, qsizes, acts, n_layers, xq, c2, up2, B, dq2, NULL);
   }
   free(xq); free(c1); free(c2); free(q1); free(q2); free(up1); free(up2);
+  return rc;
+}
+
+/* ddpg_critic_loss (ddpg.hpp:50-76) */
+int orc_ddpg_critic_loss(const float* pol, const size_t* psizes, const float* q1p, const float* q2p,
+                         const float* q1t, const float* q2t, const size_t* qsizes,
+                         size_t n_layers, const float* obs_norm, const float* act,
+                         const float* boot_norm, const float* ret, const float* eff, size_t B,
+                         size_t obs_dim, size_t act_dim, float low, float high, float* loss_out,
+                         float* y_out, float* dq1, float* dq2) {
+  float* y = y_out ? y_out : (float*)malloc(B * sizeof(float));
+  int rc = orc_ddpg_target(pol, psizes, q1t, q2t, qsizes, n_layers, boot_norm, ret, eff, B,
+                           obs_dim, act_dim, low, high, y);
+  if (!rc)
+    rc = critic_regress(q1p, q2p, qsizes, n_layers, obs_norm, act, y, B, obs_dim, act_dim,
+                        loss_out, dq1, dq2);
   if (!y_out) free(y);
   return rc;
 }
@@ -1168,4 +1178,248 @@ int orc_evaluate(const float* pol, const size_t* psizes, size_t n_layers, int64_
   free(trunc); free(finished);
   orc_env_destroy(e);
   return 0;
+}
+
+/* ================================================================ sac.hpp */
+
+/* generate_canonical<float, 24> over any 64-bit URBG (random.tcc:3349-3381):
+ * one draw, float(x) / 2^64, clamped below 1. */
+static float canonical_from(uint64_t x) {
+  float u = (float)x / 18446744073709551616.0f;
+  if (u >= 1.0f) u = nextafterf(1.0f, 0.0f);
+  return u;
+}
+
+static uint64_t urbg_next(int kind, orc_mt64* g, uint64_t key, uint64_t* ctr) {
+  if (kind == 0) return orc_mt64_next(g);
+  return orc_philox_draw(key, (*ctr)++);
+}
+
+/* n draws of ONE normal_distribution<float>(0, 1) object (the polar method
+ * with its cached second value, random.tcc:1811-1844), as the learners draw
+ * eps (learners.cpp:171-173, :247-249).  kind 0: std::mt19937_64 `g` (the
+ * reference's make_rng(seed, sac, 1|2)); kind 1: the Philox counter URBG of
+ * the device (draw i = philox(key, ctr + i); *ctr advanced). */
+void orc_normals(int kind, orc_mt64* g, uint64_t key, uint64_t* ctr, size_t n, float* out) {
+  int saved_ok = 0;
+  float saved = 0.0f;
+  for (size_t k = 0; k < n; ++k) {
+    if (saved_ok) {
+      saved_ok = 0;
+      out[k] = saved;
+      continue;
+    }
+    float x, y, r2;
+    do {
+      x = (float)((double)(2.0f * canonical_from(urbg_next(kind, g, key, ctr))) - 1.0);
+      y = (float)((double)(2.0f * canonical_from(urbg_next(kind, g, key, ctr))) - 1.0);
+      r2 = x * x + y * y;
+    } while (r2 > 1.0f || r2 == 0.0f);
+    const float mult = sqrtf(-2.0f * logf(r2) / r2);
+    saved = x * mult;
+    saved_ok = 1;
+    out[k] = y * mult;
+  }
+}
+
+/* The stochastic actor's eps (learners.cpp:89-93): a fresh
+ * normal_distribution<float> per env row over its SplitMix state. */
+void orc_normals_rows(uint64_t* states, size_t n_rows, size_t dim, float* out) {
+  for (size_t i = 0; i < n_rows; ++i) {
+    int saved_ok = 0;
+    float saved = 0.0f;
+    for (size_t d = 0; d < dim; ++d) {
+      if (saved_ok) {
+        saved_ok = 0;
+        out[i * dim + d] = saved;
+        continue;
+      }
+      float x, y, r2;
+      do {
+        x = (float)((double)(2.0f * canonical_f32(&states[i])) - 1.0);
+        y = (float)((double)(2.0f * canonical_f32(&states[i])) - 1.0);
+        r2 = x * x + y * y;
+      } while (r2 > 1.0f || r2 == 0.0f);
+      const float mult = sqrtf(-2.0f * logf(r2) / r2);
+      saved = x * mult;
+      saved_ok = 1;
+      out[i * dim + d] = y * mult;
+    }
+  }
+}
+
+#define SAC_LOG_STD_MIN (-5.0f)                 /* policy.hpp:61 */
+#define SAC_LOG_STD_MAX 2.0f                    /* policy.hpp:62 */
+#define SAC_SQUASH_FLOOR ((float)1e-6)          /* policy.hpp:63 */
+#define SAC_HALF_LOG_2PI ((float)(0.5 * 1.8378770664093453))
+
+/* GaussianPolicy::sample (policy.hpp:77-107) given the net output y
+ * [B x 2A] = [mean | log_std]: act, logp and pre. */
+static int gauss_squash(const float* y, const float* eps, size_t B, size_t A, float low,
+                        float high, float* act, float* logp, float* pre) {
+  const float m = (low + high) / 2.0f, h = (high - low) / 2.0f;
+  int rc = 0;
+  for (size_t b = 0; b < B; ++b) {
+    float lp = 0.0f;
+    for (size_t d = 0; d < A; ++d) {
+      const float mean = y[b * 2 * A + d];
+      float ls = y[b * 2 * A + A + d];
+      if (ls < SAC_LOG_STD_MIN) ls = SAC_LOG_STD_MIN;
+      if (ls > SAC_LOG_STD_MAX) ls = SAC_LOG_STD_MAX;
+      const float sd = expf(ls);
+      const float e = eps[b * A + d];
+      const float p = mean + sd * e;
+      const float t = tanhf(p);
+      if (pre) pre[b * A + d] = p;
+      act[b * A + d] = m + h * t;
+      const float jac = h * (1.0f - t * t) + SAC_SQUASH_FLOOR;
+      lp += -0.5f * e * e - ls - SAC_HALF_LOG_2PI - logf(jac);
+    }
+    logp[b] = lp;
+  }
+  return rc;
+}
+
+int orc_gauss_sample(const float* pol, const size_t* psizes, size_t n_layers, const float* obs,
+                     const float* eps, size_t B, float low, float high, float* act, float* logp) {
+  const size_t A = psizes[n_layers] / 2;
+  float* y = (float*)malloc(B * 2 * A * sizeof(float));
+  policy_forward_cached(pol, psizes, n_layers, obs, B, y, NULL);
+  gauss_squash(y, eps, B, A, low, high, act, logp, NULL);
+  free(y);
+  return 0;
+}
+
+/* GaussianPolicy::backward (policy.hpp:121-152): dpolicy (zeroed here) for
+ * upstream dact [B x A] and dlogp [B]; pcache from policy_forward_cached. */
+static void gauss_backward(const float* pol, const size_t* psizes, size_t n_layers,
+                           const float* states, const float* pcache, const float* eps,
+                           const float* pre, const float* dact, const float* dlogp, size_t B,
+                           float low, float high, float* dpolicy) {
+  const size_t A = psizes[n_layers] / 2;
+  const size_t yoff = cache_size(psizes, n_layers, B) - B * 2 * A;
+  const float* y = pcache + yoff;
+  const float h = (high - low) / 2.0f;
+  float* dy = (float*)malloc(B * 2 * A * sizeof(float));
+  for (size_t b = 0; b < B; ++b) {
+    for (size_t d = 0; d < A; ++d) {
+      float ls = y[b * 2 * A + A + d];
+      const int clamped = ls < SAC_LOG_STD_MIN || ls > SAC_LOG_STD_MAX;
+      if (ls < SAC_LOG_STD_MIN) ls = SAC_LOG_STD_MIN;
+      if (ls > SAC_LOG_STD_MAX) ls = SAC_LOG_STD_MAX;
+      const float sd = expf(ls);
+      const float e = eps[b * A + d];
+      const float t = tanhf(pre[b * A + d]);
+      const float sech2 = 1.0f - t * t;
+      const float jac = h * sech2 + SAC_SQUASH_FLOOR;
+      const float da_dpre = h * sech2;
+      const float dlp_dpre = 2.0f * t * h * sech2 / jac;
+      const float da = dact[b * A + d];
+      const float dlp = dlogp[b];
+      dy[b * 2 * A + d] = da * da_dpre + dlp * dlp_dpre;
+      float dls = da * da_dpre * sd * e + dlp * (dlp_dpre * sd * e - 1.0f);
+      if (clamped) dls = 0.0f;
+      dy[b * 2 * A + A + d] = dls;
+    }
+  }
+  uint8_t acts[16];
+  for (size_t l = 0; l < n_layers; ++l) acts[l] = (uint8_t)(l + 1 < n_layers);
+  memset(dpolicy, 0, orc_mlp_param_count(psizes, n_layers) * sizeof(float));
+  orc_mlp_backward(pol, psizes, acts, n_layers, states, pcache, dy, B, dpolicy, NULL);
+  free(dy);
+}
+
+/* sac_critic_loss (sac.hpp:26-63): y = G + eff * (min Q'(s+, a') -
+ * alpha * log pi(a'|s+)), a' reparameterised from eps [B x A]. */
+int orc_sac_critic_loss(const float* pol, const size_t* psizes, const float* q1p,
+                        const float* q2p, const float* q1t, const float* q2t,
+                        const size_t* qsizes, size_t n_layers, const float* obs_norm,
+                        const float* act, const float* boot_norm, const float* ret,
+                        const float* eff, size_t B, size_t obs_dim, size_t act_dim, float low,
+                        float high, float alpha, const float* eps, float* loss_out,
+                        float* y_out, float* dq1, float* dq2) {
+  float* next_act = (float*)malloc(B * act_dim * sizeof(float));
+  float* logp = (float*)malloc(B * sizeof(float));
+  orc_gauss_sample(pol, psizes, n_layers, boot_norm, eps, B, low, high, next_act, logp);
+  float* xq = concat_cols(boot_norm, obs_dim, next_act, act_dim, B);
+  float* q1 = (float*)malloc(B * sizeof(float));
+  float* q2 = (float*)malloc(B * sizeof(float));
+  uint8_t acts[16];
+  for (size_t l = 0; l < n_layers; ++l) acts[l] = (uint8_t)(l + 1 < n_layers);
+  orc_mlp_forward(q1t, qsizes, acts, n_layers, xq, B, q1, NULL);
+  orc_mlp_forward(q2t, qsizes, acts, n_layers, xq, B, q2, NULL);
+  float* y = y_out ? y_out : (float*)malloc(B * sizeof(float));
+  int rc = 0;
+  for (size_t b = 0; b < B; ++b) {
+    const float qmin = q2[b] < q1[b] ? q2[b] : q1[b];
+    y[b] = ret[b] + eff[b] * (qmin - alpha * logp[b]);
+    if (!finite_f(y[b])) rc = -2;
+  }
+  if (!rc)
+    rc = critic_regress(q1p, q2p, qsizes, n_layers, obs_norm, act, y, B, obs_dim, act_dim,
+                        loss_out, dq1, dq2);
+  free(next_act); free(logp); free(xq); free(q1); free(q2);
+  if (!y_out) free(y);
+  return rc;
+}
+
+/* sac_actor_loss (sac.hpp:72-108): loss = mean(alpha log pi - min Q),
+ * mean_logp (detached, for the alpha update) and dpolicy (zeroed here). */
+int orc_sac_actor_loss(const float* pol, const size_t* psizes, const float* q1p,
+                       const float* q2p, const size_t* qsizes, size_t n_layers,
+                       const float* states, size_t B, size_t obs_dim, size_t act_dim, float low,
+                       float high, float alpha, const float* eps, float* loss_out,
+                       float* mean_logp, float* dpolicy) {
+  const size_t A = act_dim;
+  const size_t pcs = cache_size(psizes, n_layers, B);
+  float* pc = (float*)malloc(pcs * sizeof(float));
+  float* y = (float*)malloc(B * 2 * A * sizeof(float));
+  float* act = (float*)malloc(B * A * sizeof(float));
+  float* pre = (float*)malloc(B * A * sizeof(float));
+  float* logp = (float*)malloc(B * sizeof(float));
+  policy_forward_cached(pol, psizes, n_layers, states, B, y, pc);
+  gauss_squash(y, eps, B, A, low, high, act, logp, pre);
+  float* xq = concat_cols(states, obs_dim, act, A, B);
+  uint8_t acts[16];
+  for (size_t l = 0; l < n_layers; ++l) acts[l] = (uint8_t)(l + 1 < n_layers);
+  const size_t cs = cache_size(qsizes, n_layers, B);
+  float* c1 = (float*)malloc(cs * sizeof(float));
+  float* c2 = (float*)malloc(cs * sizeof(float));
+  float* q1 = (float*)malloc(B * sizeof(float));
+  float* q2 = (float*)malloc(B * sizeof(float));
+  orc_mlp_forward(q1p, qsizes, acts, n_layers, xq, B, q1, c1);
+  orc_mlp_forward(q2p, qsizes, acts, n_layers, xq, B, q2, c2);
+  float* up1 = (float*)malloc(B * sizeof(float));
+  float* up2 = (float*)malloc(B * sizeof(float));
+  float* dlogp = (float*)malloc(B * sizeof(float));
+  float loss = 0.0f, sum_logp = 0.0f;
+  for (size_t b = 0; b < B; ++b) {
+    const int pick1 = q1[b] <= q2[b];
+    loss += alpha * logp[b] - (pick1 ? q1[b] : q2[b]);
+    sum_logp += logp[b];
+    up1[b] = pick1 ? -1.0f / (float)B : 0.0f;
+    up2[b] = pick1 ? 0.0f : -1.0f / (float)B;
+    dlogp[b] = alpha / (float)B;
+  }
+  loss = loss / (float)B;
+  *loss_out = loss;
+  *mean_logp = sum_logp / (float)B;
+  int rc = finite_f(loss) ? 0 : -2;
+  if (!rc) {
+    const size_t D = obs_dim + A;
+    float* din1 = (float*)malloc(B * D * sizeof(float));
+    float* din2 = (float*)malloc(B * D * sizeof(float));
+    mlp_backward_input_only(q1p, qsizes, acts, n_layers, c1, up1, B, din1);
+    mlp_backward_input_only(q2p, qsizes, acts, n_layers, c2, up2, B, din2);
+    float* dact = (float*)malloc(B * A * sizeof(float));
+    for (size_t b = 0; b < B; ++b)
+      for (size_t d = 0; d < A; ++d)
+        dact[b * A + d] = din1[b * D + obs_dim + d] + din2[b * D + obs_dim + d];
+    gauss_backward(pol, psizes, n_layers, states, pc, eps, pre, dact, dlogp, B, low, high,
+                   dpolicy);
+    free(din1); free(din2); free(dact);
+  }
+  free(pc); free(y); free(act); free(pre); free(logp); free(xq); free(c1); free(c2); free(q1);
+  free(q2); free(up1); free(up2); free(dlogp);
+  return rc;
 }

@@ -178,6 +178,28 @@ int orc_c51_actor_loss(const float* pol, const size_t* psizes, const float* q1, 
                        size_t obs_dim, size_t act_dim, float low, float high, size_t n_atoms,
                        float vmin, float vmax, float* loss, float* dpolicy);
 
+/* SAC (sac.hpp, policy.hpp:54-153) */
+/* n draws of one normal_distribution<float> over mt19937_64 (kind 0, `g`)
+ * or the Philox counter URBG (kind 1, key, *ctr advanced). */
+void orc_normals(int kind, orc_mt64* g, uint64_t key, uint64_t* ctr, size_t n, float* out);
+/* fresh normal_distribution<float> per row over SplitMix states. */
+void orc_normals_rows(uint64_t* states, size_t n_rows, size_t dim, float* out);
+/* GaussianPolicy::sample: psizes[n_layers] = 2 * act_dim. */
+int orc_gauss_sample(const float* pol, const size_t* psizes, size_t n_layers, const float* obs,
+                     const float* eps, size_t B, float low, float high, float* act, float* logp);
+int orc_sac_critic_loss(const float* pol, const size_t* psizes, const float* q1p,
+                        const float* q2p, const float* q1t, const float* q2t,
+                        const size_t* qsizes, size_t n_layers, const float* obs_norm,
+                        const float* act, const float* boot_norm, const float* ret,
+                        const float* eff, size_t B, size_t obs_dim, size_t act_dim, float low,
+                        float high, float alpha, const float* eps, float* loss_out,
+                        float* y_out, float* dq1, float* dq2);
+int orc_sac_actor_loss(const float* pol, const size_t* psizes, const float* q1p,
+                       const float* q2p, const size_t* qsizes, size_t n_layers,
+                       const float* states, size_t B, size_t obs_dim, size_t act_dim, float low,
+                       float high, float alpha, const float* eps, float* loss_out,
+                       float* mean_logp, float* dpolicy);
+
 /* ---------------------------------------------- synthetic env */
 typedef struct {
   size_t n_envs, obs_dim, act_dim, max_len;

@@ -14,6 +14,7 @@
 
 #include "pql/agents/c51.hpp"
 #include "pql/agents/ddpg.hpp"
+#include "pql/agents/sac.hpp"
 #include "pql/explore/noise.hpp"
 #include "pql/funcapprox/checkpoint.hpp"
 #include "pql/funcapprox/normalizer.hpp"
@@ -399,6 +400,10 @@ struct RefCritic {
   agents::CriticPair<float> critics;
   fa::AdamState<float> adam_q1, adam_q2;
   agents::DeterministicPolicy<float> lagged;
+  int sac = 0;  // algo 2: pql_sac (GaussianPolicy lagged, eps stream, alpha)
+  agents::GaussianPolicy<float> lagged_g;
+  float log_alpha = 0.0f;
+  std::mt19937_64 eps_rng;
   fa::NormStats norm;
   std::unique_ptr<replay::ReplayBuffer> buffer;
   std::mt19937_64 sample_rng;
@@ -410,6 +415,8 @@ REF_API void* ref_vupdate_create(size_t D, size_t A, size_t hidden, size_t n_hid
                                  float vmin, float vmax) {
   auto* r = new RefCritic();
   r->D = D; r->A = A; r->B = B; r->n_layers = n_hidden + 1;
+  r->sac = distributional == 2;  // `distributional` doubles as algo: 0 ddpg, 1 c51, 2 sac
+  if (r->sac) distributional = 0;
   r->distributional = distributional; r->n_atoms = n_atoms; r->vmin = vmin; r->vmax = vmax;
   r->qsizes.push_back(D + A);
   r->psizes.push_back(D);
@@ -418,11 +425,16 @@ REF_API void* ref_vupdate_create(size_t D, size_t A, size_t hidden, size_t n_hid
     r->psizes.push_back(hidden);
   }
   r->qsizes.push_back(distributional ? n_atoms : 1);
-  r->psizes.push_back(A);
+  r->psizes.push_back(r->sac ? 2 * A : A);
   r->critics = make_pair(q1, q2, nullptr, nullptr, r->qsizes.data(), r->n_layers);
   r->adam_q1 = fa::AdamState<float>(r->critics.q1.param_count());
   r->adam_q2 = fa::AdamState<float>(r->critics.q2.param_count());
-  r->lagged = make_policy(policy, r->psizes.data(), r->n_layers, -1.0f, 1.0f);
+  if (r->sac) {
+    r->lagged_g.net = make_mlp(r->psizes.data(), r->n_layers, policy);
+    r->eps_rng = make_rng(seed, RngStream::sac, 1);  // learners.cpp:137
+  } else {
+    r->lagged = make_policy(policy, r->psizes.data(), r->n_layers, -1.0f, 1.0f);
+  }
   r->buffer = std::make_unique<replay::ReplayBuffer>(capacity, D, A);
   r->sample_rng = make_rng(seed, RngStream::sample, 1);
   return r;
@@ -450,7 +462,12 @@ REF_API int ref_vupdate_step(void* h, float* loss_out) {
     batch.obs = fa::RunningNormalizer::apply_stats(r->norm, batch.obs);
     batch.boot_obs = fa::RunningNormalizer::apply_stats(r->norm, batch.boot_obs);
     agents::CriticLossResult<float> res;
-    if (r->distributional) {
+    if (r->sac) {  // learners.cpp:168-176
+      MatF eps(batch.size(), r->A);
+      std::normal_distribution<float> gauss(0.0f, 1.0f);
+      for (std::size_t k = 0; k < eps.size(); ++k) eps.data()[k] = gauss(r->eps_rng);
+      res = agents::sac_critic_loss(batch, r->lagged_g, r->critics, std::exp(r->log_alpha), eps);
+    } else if (r->distributional) {
       auto head = agents::CategoricalHead<float>::create(r->n_atoms, r->vmin, r->vmax);
       res = agents::c51_critic_loss(batch, r->lagged, r->critics, head);
     } else {
@@ -466,6 +483,10 @@ REF_API int ref_vupdate_step(void* h, float* loss_out) {
     return -2;
   }
   return 0;
+}
+
+REF_API void ref_vupdate_set_log_alpha(void* h, float log_alpha) {
+  static_cast<RefCritic*>(h)->log_alpha = log_alpha;
 }
 
 // which: 0 q1, 1 q2, 2 q1_target, 3 q2_target
@@ -485,6 +506,12 @@ struct RefPolicy {
   size_t n_atoms = 51;
   float vmin = -10.0f, vmax = 10.0f;
   agents::DeterministicPolicy<float> policy;
+  int sac = 0;
+  agents::GaussianPolicy<float> policy_g;
+  agents::EntropyCoef<float> alpha;
+  std::vector<float> alpha_param;
+  fa::AdamState<float> adam_alpha;
+  std::mt19937_64 eps_rng;
   fa::AdamState<float> adam;
   agents::CriticPair<float> critics;
   fa::NormStats norm;
@@ -498,6 +525,8 @@ REF_API void* ref_pupdate_create(size_t D, size_t A, size_t hidden, size_t n_hid
                                  size_t n_atoms, float vmin, float vmax) {
   auto* r = new RefPolicy();
   r->D = D; r->A = A; r->B = B; r->n_layers = n_hidden + 1;
+  r->sac = distributional == 2;  // algo: 0 ddpg, 1 c51, 2 sac
+  if (r->sac) distributional = 0;
   r->distributional = distributional; r->n_atoms = n_atoms; r->vmin = vmin; r->vmax = vmax;
   r->qsizes.push_back(D + A);
   r->psizes.push_back(D);
@@ -506,9 +535,18 @@ REF_API void* ref_pupdate_create(size_t D, size_t A, size_t hidden, size_t n_hid
     r->psizes.push_back(hidden);
   }
   r->qsizes.push_back(distributional ? n_atoms : 1);
-  r->psizes.push_back(A);
-  r->policy = make_policy(policy, r->psizes.data(), r->n_layers, -1.0f, 1.0f);
-  r->adam = fa::AdamState<float>(r->policy.net.param_count());
+  r->psizes.push_back(r->sac ? 2 * A : A);
+  if (r->sac) {  // learners.cpp:213-219
+    r->policy_g.net = make_mlp(r->psizes.data(), r->n_layers, policy);
+    r->adam = fa::AdamState<float>(r->policy_g.net.param_count());
+    r->alpha.target_entropy = -float(A);
+    r->alpha_param.assign(1, 0.0f);
+    r->adam_alpha = fa::AdamState<float>(1);
+    r->eps_rng = make_rng(seed, RngStream::sac, 2);
+  } else {
+    r->policy = make_policy(policy, r->psizes.data(), r->n_layers, -1.0f, 1.0f);
+    r->adam = fa::AdamState<float>(r->policy.net.param_count());
+  }
   r->critics = make_pair(q1, q2, nullptr, nullptr, r->qsizes.data(), r->n_layers);
   r->states = std::make_unique<replay::StateBuffer>(capacity, D);
   r->sample_rng = make_rng(seed, RngStream::sample, 2);
@@ -535,6 +573,22 @@ REF_API int ref_pupdate_step(void* h, float* loss_out) {
     MatF states = fa::RunningNormalizer::apply_stats(r->norm, *sampled);
     float loss;
     std::vector<float> dpolicy;
+    if (r->sac) {  // learners.cpp:246-258
+      MatF eps(states.rows(), r->A);
+      std::normal_distribution<float> gauss(0.0f, 1.0f);
+      for (std::size_t k = 0; k < eps.size(); ++k) eps.data()[k] = gauss(r->eps_rng);
+      r->alpha.log_alpha = r->alpha_param[0];
+      auto res = agents::sac_actor_loss(states, r->policy_g, r->critics, r->alpha.alpha(), eps);
+      loss = res.loss;
+      dpolicy = std::move(res.dpolicy);
+      auto ares = agents::sac_alpha_loss(res.mean_logp, r->alpha);
+      std::vector<float> dalpha{ares.dlog_alpha};
+      fa::adam_step(r->alpha_param, dalpha, r->adam_alpha, r->lr);
+      fa::clip_global_norm(dpolicy, 0.5f);
+      fa::adam_step(r->policy_g.net.flat, dpolicy, r->adam, r->lr);
+      *loss_out = loss;
+      return 0;
+    }
     if (r->distributional) {
       auto head = agents::CategoricalHead<float>::create(r->n_atoms, r->vmin, r->vmax);
       auto res = agents::c51_actor_loss(states, r->policy, r->critics, head);
@@ -556,7 +610,13 @@ REF_API int ref_pupdate_step(void* h, float* loss_out) {
 
 REF_API void ref_pupdate_params(void* h, float* out) {
   auto* r = static_cast<RefPolicy*>(h);
-  std::memcpy(out, r->policy.net.flat.data(), r->policy.net.flat.size() * sizeof(float));
+  const auto& net = r->sac ? r->policy_g.net : r->policy.net;
+  std::memcpy(out, net.flat.data(), net.flat.size() * sizeof(float));
+}
+
+REF_API float ref_pupdate_log_alpha(void* h) {
+  auto* r = static_cast<RefPolicy*>(h);
+  return r->sac ? r->alpha_param[0] : 0.0f;
 }
 
 // --------------------------------------------------- actor step (agents)
@@ -572,6 +632,8 @@ struct RefActor {
   fa::RunningNormalizer normalizer;
   explore::NoiseSchedule schedule;
   std::vector<env::SplitMixEngine> noise_rng;
+  int sac = 0;
+  agents::GaussianPolicy<float> policy_g;
 };
 
 REF_API void* ref_actor_create(size_t N, size_t D, size_t A, size_t hidden, size_t n_hidden,
@@ -589,12 +651,64 @@ REF_API void* ref_actor_create(size_t N, size_t D, size_t A, size_t hidden, size
   return r;
 }
 
+// The stochastic (pql_sac) actor: GaussianPolicy with [mean | log_std] head.
+REF_API void* ref_actor_create_sac(size_t N, size_t D, size_t A, size_t hidden, size_t n_hidden,
+                                   uint64_t seed, const float* policy) {
+  auto* r = static_cast<RefActor*>(ref_actor_create(N, D, A, hidden, n_hidden, seed, nullptr,
+                                                    0.05f, 0.8f));
+  r->sac = 1;
+  std::vector<size_t> ps(r->psizes);
+  ps.back() = 2 * A;
+  r->policy_g.net = make_mlp(ps.data(), r->n_layers, policy);
+  return r;
+}
+
+// n draws of one normal_distribution<float>(0, 1) over make_rng(seed, stream, index)
+REF_API void ref_normals(uint64_t seed, uint64_t stream, uint64_t index, size_t n, float* out) {
+  auto rng = make_rng(seed, static_cast<RngStream>(stream), index);
+  std::normal_distribution<float> gauss(0.0f, 1.0f);
+  for (size_t k = 0; k < n; ++k) out[k] = gauss(rng);
+}
+
+// GaussianPolicy::sample (policy.hpp:77-107) and its backward (:121-152)
+// for one batch: act [B x A], logp [B], and dpolicy for (dact, dlogp).
+REF_API int ref_gauss_sample(const float* pol, const size_t* psizes, size_t n_layers,
+                             const float* obs, const float* eps, size_t B, const float* dact,
+                             const float* dlogp, float* act, float* logp, float* dpolicy) {
+  agents::GaussianPolicy<float> p;
+  p.net = make_mlp(psizes, n_layers, pol);
+  const size_t A = psizes[n_layers] / 2;
+  try {
+    auto s = p.sample(make_mat(obs, B, psizes[0]), make_mat(eps, B, A));
+    std::memcpy(act, s.act.data(), B * A * sizeof(float));
+    std::memcpy(logp, s.logp.data(), B * sizeof(float));
+    if (dpolicy) {
+      std::vector<float> g;
+      p.backward(s, make_mat(dact, B, A), std::vector<float>(dlogp, dlogp + B), g);
+      std::memcpy(dpolicy, g.data(), g.size() * sizeof(float));
+    }
+  } catch (const std::exception&) {
+    return -2;
+  }
+  return 0;
+}
+
 REF_API void ref_actor_destroy(void* h) { delete static_cast<RefActor*>(h); }
 
 REF_API void ref_actor_act(void* h, const float* obs, float* actions) {
   auto* r = static_cast<RefActor*>(h);
   MatF o = make_mat(obs, r->N, r->D);
   MatF obs_norm = r->normalizer.apply(o);
+  if (r->sac) {  // learners.cpp:87-94: a fresh normal_distribution per env
+    MatF eps(r->N, r->A);
+    for (std::size_t i = 0; i < r->N; ++i) {
+      std::normal_distribution<float> gauss(0.0f, 1.0f);
+      for (std::size_t d = 0; d < r->A; ++d) eps(i, d) = gauss(r->noise_rng[i]);
+    }
+    MatF a = r->policy_g.sample(obs_norm, eps).act;
+    std::memcpy(actions, a.data(), r->N * r->A * sizeof(float));
+    return;
+  }
   MatF a = r->policy.act(obs_norm);
   explore::apply_noise(a, r->schedule, r->policy.low, r->policy.high, r->noise_rng);
   std::memcpy(actions, a.data(), r->N * r->A * sizeof(float));

@@ -71,6 +71,13 @@ _ORC_SIGS = {
                                   sz, f32, f32, sz, f32, f32, vp, vp, vp]),
     "orc_c51_actor_loss": (i32, [vp, vp, vp, vp, vp, sz, vp, sz, sz, sz, f32, f32, sz, f32, f32,
                                  vp, vp]),
+    "orc_normals": (None, [i32, vp, u64, vp, sz, vp]),
+    "orc_normals_rows": (None, [vp, sz, sz, vp]),
+    "orc_gauss_sample": (i32, [vp, vp, sz, vp, vp, sz, f32, f32, vp, vp]),
+    "orc_sac_critic_loss": (i32, [vp, vp, vp, vp, vp, vp, vp, sz, vp, vp, vp, vp, vp, sz, sz,
+                                  sz, f32, f32, f32, vp, vp, vp, vp, vp]),
+    "orc_sac_actor_loss": (i32, [vp, vp, vp, vp, vp, sz, vp, sz, sz, sz, f32, f32, f32, vp, vp,
+                                 vp, vp]),
     "orc_env_create": (vp, [sz, sz, sz, u64, sz]),
     "orc_env_destroy": (None, [vp]),
     "orc_env_observe": (None, [vp, vp]),
@@ -111,6 +118,11 @@ _REF_SIGS = {
     "ref_vupdate_adopt_norm": (None, [vp, i64, vp, vp]),
     "ref_vupdate_step": (i32, [vp, vp]),
     "ref_vupdate_params": (None, [vp, i32, vp]),
+    "ref_vupdate_set_log_alpha": (None, [vp, f32]),
+    "ref_pupdate_log_alpha": (f32, [vp]),
+    "ref_actor_create_sac": (vp, [sz, sz, sz, sz, sz, u64, vp]),
+    "ref_normals": (None, [u64, u64, u64, sz, vp]),
+    "ref_gauss_sample": (i32, [vp, vp, sz, vp, vp, sz, vp, vp, vp, vp, vp]),
     "ref_pupdate_create": (vp, [sz, sz, sz, sz, sz, sz, u64, vp, vp, vp, i32, sz, f32, f32]),
     "ref_pupdate_destroy": (None, [vp]),
     "ref_pupdate_insert": (None, [vp, vp, sz]),
@@ -204,3 +216,4 @@ def derive_seed(master: int, stream: int, index: int) -> int:
 
 
 STREAM_ENV, STREAM_NOISE, STREAM_INIT, STREAM_SAMPLE = 1, 2, 3, 4
+STREAM_SAC = 6

@@ -5,8 +5,8 @@ from __future__ import annotations
 
 import numpy as np
 
-from oracle_lib import (MT64, STREAM_SAMPLE, acts_arr, derive_seed, orc, param_count, ptr,
-                        sizes_arr)
+from oracle_lib import (MT64, STREAM_SAC, STREAM_SAMPLE, acts_arr, derive_seed, orc, param_count,
+                        ptr, sizes_arr)
 
 
 def f32(a):
@@ -37,6 +37,24 @@ def policy_act(flat, sizes, x, low=-1.0, high=1.0):
     return y
 
 
+class EpsStream:
+    """The learners' eps draws (one normal_distribution<float> per update,
+    learners.cpp:171-173, :247-249) over make_rng(seed, sac, learner)
+    (mt19937_64) or the device's Philox URBG with the same key."""
+
+    def __init__(self, seed, learner, philox=False):
+        self.key = derive_seed(seed, STREAM_SAC, learner)
+        self.philox = philox
+        self.mt = MT64(self.key)
+        self.ctr = np.zeros(1, np.uint64)
+
+    def draw(self, B, A):
+        out = np.zeros((B, A), np.float32)
+        orc().orc_normals(1 if self.philox else 0, None if self.philox else self.mt.handle,
+                          self.key, ptr(self.ctr), B * A, ptr(out))
+        return out
+
+
 def adam(p, g, m, v, t, lr):
     bc1 = np.zeros(1, np.float32)
     bc2 = np.zeros(1, np.float32)
@@ -50,11 +68,14 @@ class OracleVUpdate:
     sampling with mt19937_64 (make_rng(seed, sample, 1)) or Philox."""
 
     def __init__(self, D, A, hidden, n_hidden, B, q1, q2, policy, seed=0, lr=5e-4, tau=0.05,
-                 philox=False, distributional=False, n_atoms=51, vmin=-10.0, vmax=10.0):
+                 philox=False, distributional=False, n_atoms=51, vmin=-10.0, vmax=10.0,
+                 sac=False, log_alpha=0.0):
         self.D, self.A, self.B = D, A, B
-        self.ps = [D] + [hidden] * n_hidden + [A]
+        self.ps = [D] + [hidden] * n_hidden + [2 * A if sac else A]
         self.qs = [D + A] + [hidden] * n_hidden + [n_atoms if distributional else 1]
         self.L = n_hidden + 1
+        self.sac, self.log_alpha = sac, np.float32(log_alpha)
+        self.eps = EpsStream(seed, 1, philox) if sac else None
         self.q = [f32(q1).copy(), f32(q2).copy()]
         self.qt = [self.q[0].copy(), self.q[1].copy()]
         self.pol = f32(policy).copy()
@@ -98,7 +119,12 @@ class OracleVUpdate:
                 ptr(self.qt[0]), ptr(self.qt[1]), ptr(sizes_arr(self.qs)), self.L, ptr(obs_n),
                 ptr(f32(act)), ptr(boot_n), ptr(f32(ret)), ptr(f32(eff)), self.B, self.D, self.A,
                 np.float32(-1), np.float32(1))
-        if self.distributional:
+        if self.sac:
+            eps = self.eps.draw(self.B, self.A)
+            alpha = np.float32(np.exp(self.log_alpha))
+            rc = orc().orc_sac_critic_loss(*args, alpha, ptr(eps), ptr(loss), ptr(y), ptr(dq[0]),
+                                           ptr(dq[1]))
+        elif self.distributional:
             rc = orc().orc_c51_critic_loss(*args, self.n_atoms, np.float32(self.vmin),
                                            np.float32(self.vmax), ptr(loss), ptr(dq[0]),
                                            ptr(dq[1]))
@@ -121,9 +147,15 @@ class OraclePUpdate:
     """PolicyLearnerCore::update (learners.cpp:239-270) on explicit state."""
 
     def __init__(self, D, A, hidden, n_hidden, B, policy, q1, q2, seed=0, lr=5e-4, philox=False,
-                 distributional=False, n_atoms=51, vmin=-10.0, vmax=10.0):
+                 distributional=False, n_atoms=51, vmin=-10.0, vmax=10.0, sac=False):
         self.D, self.A, self.B = D, A, B
-        self.ps = [D] + [hidden] * n_hidden + [A]
+        self.ps = [D] + [hidden] * n_hidden + [2 * A if sac else A]
+        self.sac = sac
+        self.eps = EpsStream(seed, 2, philox) if sac else None
+        # log alpha and its Adam state (learners.cpp:217-219)
+        self.alpha_p = np.zeros(1, np.float32)
+        self.alpha_m = np.zeros(1, np.float32)
+        self.alpha_v = np.zeros(1, np.float32)
         self.qs = [D + A] + [hidden] * n_hidden + [n_atoms if distributional else 1]
         self.L = n_hidden + 1
         self.pol = f32(policy).copy()
@@ -157,6 +189,21 @@ class OraclePUpdate:
         args = (ptr(self.pol), ptr(sizes_arr(self.ps)), ptr(self.q[0]), ptr(self.q[1]),
                 ptr(sizes_arr(self.qs)), self.L, ptr(s), self.B, self.D, self.A, np.float32(-1),
                 np.float32(1))
+        if self.sac:
+            eps = self.eps.draw(self.B, self.A)
+            alpha = np.float32(np.exp(self.alpha_p[0]))
+            mean_logp = np.zeros(1, np.float32)
+            rc = orc().orc_sac_actor_loss(*args, alpha, ptr(eps), ptr(loss), ptr(mean_logp),
+                                          ptr(dp))
+            if rc != 0:
+                raise FloatingPointError("non-finite actor loss")
+            # sac_alpha_loss (sac.hpp:117-125) + adam_step on log alpha
+            drift = np.float32(mean_logp[0] + np.float32(-self.A))
+            self.t += 1
+            adam(self.alpha_p, f32([-drift]), self.alpha_m, self.alpha_v, self.t, self.lr)
+            orc().orc_clip_global_norm(ptr(dp), P, np.float32(0.5))
+            adam(self.pol, dp, self.m, self.v, self.t, self.lr)
+            return float(loss[0]), dict(idx=idx, dp=dp, qscale=1.0, mean_logp=float(mean_logp[0]))
         if self.distributional:
             rc = orc().orc_c51_actor_loss(*args, self.n_atoms, np.float32(self.vmin),
                                           np.float32(self.vmax), ptr(loss), ptr(dp))
