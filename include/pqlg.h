@@ -182,9 +182,16 @@ PQLG_API int pqlg_states_sample(pqlg_states h, uint64_t batch, pqlg_rng* rng, ui
  * plus `hidden_layers` (the reference hard-codes 2: learners.cpp:22-23,
  * :127-130, :206-209; configs 2-5 need 3) and the synthetic env's time
  * limit.  pqlg_config_default() fills the Table B.1 defaults. */
-enum { PQLG_ALGO_DDPG = 0, PQLG_ALGO_C51 = 1 };
+/* pql_sac (algo.hpp:8, sac.hpp): the policy is a GaussianPolicy whose net
+ * emits [mean | log_std] (2 x act_dim outputs, learners.cpp:20-22);
+ * param_count / get_params / set_params of the policy are the net's.  The
+ * snapshot's log_alpha (PolicySnapshot::log_alpha, messages.hpp:18-19)
+ * travels beside it: pqlg_plearner_log_alpha reads the P-learner's,
+ * pqlg_vlearner_adopt_policy_sac installs both in the V-learner, and the
+ * run_parallel pipeline moves them together on the device. */
+enum { PQLG_ALGO_DDPG = 0, PQLG_ALGO_C51 = 1, PQLG_ALGO_SAC = 2 };
 typedef struct {
-  int algo;               /* PQLG_ALGO_DDPG (pql_ddpg) or PQLG_ALGO_C51 (pql_d) */
+  int algo;               /* PQLG_ALGO_DDPG (pql_ddpg), PQLG_ALGO_C51 (pql_d), PQLG_ALGO_SAC (pql_sac) */
   int n_envs;
   int batch_size;
   uint64_t buffer_capacity;
@@ -258,6 +265,11 @@ PQLG_API int pqlg_vlearner_create_dp(const pqlg_config* cfg, const pqlg_task_dim
 PQLG_API int pqlg_vlearner_destroy(pqlg_vlearner h);
 /* adopt_policy: equal-or-newer version replaces (learners.cpp:37-42) */
 PQLG_API int pqlg_vlearner_adopt_policy(pqlg_vlearner h, const float* flat_host, int64_t version);
+/* pql_sac: adopt a PolicySnapshot's net and log_alpha (learners.cpp:37-42) */
+PQLG_API int pqlg_vlearner_adopt_policy_sac(pqlg_vlearner h, const float* flat_host,
+                                            float log_alpha, int64_t version);
+/* pql_sac: the lagged policy's log_alpha (0 for other algos) */
+PQLG_API int pqlg_vlearner_log_alpha(pqlg_vlearner h, float* out);
 PQLG_API int pqlg_vlearner_adopt_norm(pqlg_vlearner h, const pqlg_norm_stats* norm);
 /* ingest(StepSlice): reward scale + n-step + insert (learners.cpp:144-151) */
 PQLG_API int pqlg_vlearner_ingest(pqlg_vlearner h, const pqlg_step_slice* dev);
@@ -289,7 +301,9 @@ PQLG_API int pqlg_vlearner_set_params(pqlg_vlearner h, int which, const float* f
 /* Intermediates of the last update for parity checks: 0 TD target y [B],
  * 1 dLoss/dQ [2 x B] (C51: dLoss/dlogits [2 x B x n_atoms]),
  * 2 flat gradients before clipping [2 x P],
- * 3 clip scales [2], 4 sampled critic input [B x (obs_dim+act_dim)]. */
+ * 3 clip scales [2], 4 sampled critic input [B x (obs_dim+act_dim)],
+ * 5 (pql_sac) eps [B x act_dim], 6 (pql_sac) log pi(a'|s+) [B],
+ * 7 target critic input [B x (obs_dim+act_dim)] = [norm(boot) | a']. */
 PQLG_API int pqlg_vlearner_debug_read(pqlg_vlearner h, int what, float* host_out);
 /* Number of kernels one update launches (graph nodes). */
 PQLG_API int pqlg_vlearner_kernels_per_update(pqlg_vlearner h, int* out);
@@ -330,6 +344,8 @@ PQLG_API int pqlg_plearner_snapshot(pqlg_plearner h, float* flat_host);
 PQLG_API int pqlg_plearner_get_params(pqlg_plearner h, int which, float* flat_host);
 PQLG_API int pqlg_plearner_set_params(pqlg_plearner h, int which, const float* flat_host);
 PQLG_API int pqlg_plearner_param_count(pqlg_plearner h, int which, int64_t* out);
+/* pql_sac: the learned log alpha (alpha_param_[0], learners.cpp:218, :254-257) */
+PQLG_API int pqlg_plearner_log_alpha(pqlg_plearner h, float* out);
 PQLG_API int pqlg_plearner_buffer_size(pqlg_plearner h, uint64_t* out);
 PQLG_API int pqlg_plearner_set_sampler(pqlg_plearner h, int mode);
 PQLG_API int pqlg_plearner_kernels_per_update(pqlg_plearner h, int* out);

@@ -41,7 +41,7 @@ class Rng(C.Structure):
 
 
 RNG_PHILOX, RNG_INDICES = 0, 1
-ALGO_DDPG, ALGO_C51 = 0, 1
+ALGO_DDPG, ALGO_C51, ALGO_SAC = 0, 1, 2
 P = C.POINTER
 
 
@@ -113,6 +113,8 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_vlearner_create_dp": (i32, [P(Config), P(TaskDims), u64, vp, vp, P(vp)]),
     "pqlg_vlearner_destroy": (i32, [vp]),
     "pqlg_vlearner_adopt_policy": (i32, [vp, vp, i64]),
+    "pqlg_vlearner_adopt_policy_sac": (i32, [vp, vp, f32, i64]),
+    "pqlg_vlearner_log_alpha": (i32, [vp, P(f32)]),
     "pqlg_vlearner_adopt_norm": (i32, [vp, P(NormStats)]),
     "pqlg_vlearner_ingest": (i32, [vp, P(StepSlice)]),
     "pqlg_vlearner_ingest_host": (i32, [vp, P(StepSlice)]),
@@ -149,6 +151,7 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_plearner_get_params": (i32, [vp, i32, vp]),
     "pqlg_plearner_set_params": (i32, [vp, i32, vp]),
     "pqlg_plearner_param_count": (i32, [vp, i32, P(i64)]),
+    "pqlg_plearner_log_alpha": (i32, [vp, P(f32)]),
     "pqlg_plearner_buffer_size": (i32, [vp, P(u64)]),
     "pqlg_plearner_set_sampler": (i32, [vp, i32]),
     "pqlg_plearner_kernels_per_update": (i32, [vp, P(i32)]),

@@ -117,7 +117,10 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
     PQLG_CUDA(cudaStreamCreateWithFlags(&owned_stream_, cudaStreamNonBlocking));
     stream_ = owned_stream_;
   }
-  require(cfg.algo == PQLG_ALGO_DDPG || cfg.algo == PQLG_ALGO_C51, "actor: unknown algo");
+  require(cfg.algo == PQLG_ALGO_DDPG || cfg.algo == PQLG_ALGO_C51 || cfg.algo == PQLG_ALGO_SAC,
+          "actor: unknown algo");
+  sac_ = cfg.algo == PQLG_ALGO_SAC;
+  require(!sac_ || dims.act_dim <= 32, "actor: pql_sac needs act_dim <= 32");
   require(cfg.hidden_layers >= 1 && cfg.hidden >= 32 && cfg.hidden % 32 == 0,
           "actor: hidden width must be a multiple of 32");
   N_ = cfg.n_envs;
@@ -129,14 +132,14 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
   Dp_ = round_up(D_, 4);
   std::vector<int> ps{D_};
   for (int i = 0; i < nh_; ++i) ps.push_back(H_);
-  ps.push_back(A_);
+  ps.push_back(sac_ ? 2 * A_ : A_);  // GaussianPolicy: [mean | log_std] (learners.cpp:20-22)
   pnet_ = NetShape::make(ps);
 
   // policy: PolicyHandle::create with make_rng(seed, init, 0) (learners.cpp:69)
   std::mt19937_64 prng(rng::derive_seed(cfg.seed, rng::kInit, 0));
   std::vector<float> pol;
   init_orthogonal(pnet_, pol, prng, static_cast<float>(std::sqrt(2.0)), 1e-2f);
-  pol_.alloc(pnet_.params);
+  pol_.alloc(snapshot_len());  // [net | log_alpha] for pql_sac (log_alpha unused here)
   PQLG_CUDA(cudaMemcpy(pol_.p, pol.data(), pol.size() * 4, cudaMemcpyHostToDevice));
 
   // exploration: build_schedule over the global env count (noise.hpp:23-42;
@@ -228,6 +231,28 @@ void Actor::build() {
     in = pact_[l].p;
     ld = H;
     K = H;
+  }
+  if (sac_) {
+    // GaussianPolicy::sample with a fresh normal_distribution per env over
+    // its noise stream (learners.cpp:87-94): split-K head + sampling finish
+    head_.init(pol_.p + pnet_.w_off[nh], H, 2 * A);
+    head_.refresh(stream_);
+    auto gemm = mlp::head_gemm_step(head_split_, in, ld, head_.ptr(), head_.stride(), N, 2 * A, H);
+    sac::GaussArgs g{};
+    g.bias = pol_.p + pnet_.b_off[nh];
+    g.rng = noise_rng_.p;
+    g.ld_act = Ap_;
+    g.mid = (dims_.low + dims_.high) / 2.0f;
+    g.half = (dims_.high - dims_.low) / 2.0f;
+    for (int k = 0; k < kSets; ++k) {
+      g.act = act_[k].p;
+      auto fin = gauss_finish_step(head_split_, g, N, A);
+      head_steps_[k] = [gemm, fin](cudaStream_t st) {
+        gemm(st);
+        fin(st);
+      };
+    }
+    return;
   }
   // DeterministicPolicy::act + apply_noise (learners.cpp:96-98), fused
   epi::PolicyHead ph{};
@@ -321,7 +346,8 @@ void Actor::rollout_n(int n) {
 
 void Actor::adopt_policy(const float* flat, int64_t version, bool device) {
   if (version < version_) return;  // PolicyHandle::adopt (learners.cpp:37-42)
-  PQLG_CUDA(cudaMemcpyAsync(pol_.p, flat, pnet_.params * 4,
+  // device snapshots carry [net | log_alpha]; the host ABI passes the net
+  PQLG_CUDA(cudaMemcpyAsync(pol_.p, flat, (device ? snapshot_len() : pnet_.params) * 4,
                             device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream_));
   head_.refresh(stream_);
   if (!device) PQLG_CUDA(cudaStreamSynchronize(stream_));
@@ -405,9 +431,13 @@ void evaluate_policy(const pqlg_config& cfg, const pqlg_task_dims& dims, const f
     cudaStream_t s;
     ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
   } guard{st};
+  // pql_sac evaluates the squashed mean (GaussianPolicy::mean_act,
+  // policy.hpp:110-118): the first A of the 2A head outputs
+  const bool sac = cfg.algo == PQLG_ALGO_SAC;
+  const int hout = sac ? 2 * A : A;
   std::vector<int> ps{D};
   for (int l = 0; l < nh; ++l) ps.push_back(H);
-  ps.push_back(A);
+  ps.push_back(hout);
   const NetShape pnet = NetShape::make(ps);
   DevBuf<float> pol(pnet.params);
   PQLG_CUDA(cudaMemcpy(pol.p, policy, pnet.params * 4, cudaMemcpyHostToDevice));
@@ -451,7 +481,7 @@ void evaluate_policy(const pqlg_config& cfg, const pqlg_task_dims& dims, const f
     K = H;
   }
   WeightMirror head;
-  head.init(pol.p + pnet.w_off[nh], H, A);
+  head.init(pol.p + pnet.w_off[nh], H, hout);
   head.refresh(st);
   epi::PolicyHead ph{};
   ph.bias = pol.p + pnet.b_off[nh];

@@ -28,6 +28,7 @@ class Actor {
   int n_envs() const { return N_; }
   int obs_dim() const { return D_; }
   int64_t param_count() const { return pnet_.params; }
+  int64_t snapshot_len() const { return pnet_.params + (sac_ ? 1 : 0); }
   // device views for the pipeline (run_parallel): the running normalizer
   // (owned by the actor, SPEC "Normalizer statistics are owned by the Actor")
   const float* policy_dev() const { return pol_.p; }
@@ -48,6 +49,8 @@ class Actor {
   cudaStream_t stream_;
   cudaStream_t owned_stream_ = nullptr;
   int N_, D_, A_, Ap_, H_, nh_;
+  bool sac_ = false;            // pql_sac: Gaussian policy, no schedule noise
+  mlp::HeadSplit head_split_;   // pql_sac: split-K [mean | log_std] head
   int64_t Dp_;
   NetShape pnet_;
   int64_t version_ = 0;

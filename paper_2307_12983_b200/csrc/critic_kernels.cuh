@@ -80,6 +80,8 @@ struct LossArgs {
   const float* ret;
   const float* eff;
   float* y;                // [B] TD targets (kept for inspection)
+  const float* logp;       // pql_sac: log pi(a'|s+) [B] (null: DDPG target)
+  const float* log_alpha;  // pql_sac: the lagged policy's log alpha
   int64_t* step;           // Adam step
   float* up;          // [2][B]  dLoss/dQ_k
   double* block_loss; // [gridDim.x]
@@ -98,7 +100,9 @@ static __global__ void __launch_bounds__(kRowThreads) critic_loss_kernel(LossArg
   if (b < a.B) {
     const float t1 = head_value(a.partial_t, a.ld, a.n_tiles, 0, a.q1t[a.head_b_off], b);
     const float t2 = head_value(a.partial_t, a.ld, a.n_tiles, 1, a.q2t[a.head_b_off], b);
-    const float qmin = t2 < t1 ? t2 : t1;  // std::min(q1, q2)
+    float qmin = t2 < t1 ? t2 : t1;  // std::min(q1, q2)
+    if (a.logp)  // sac_critic_loss: qmin - alpha * log pi (sac.hpp:38-39)
+      qmin = __fsub_rn(qmin, __fmul_rn(expf(*a.log_alpha), a.logp[b]));
     const float y = __fadd_rn(a.ret[b], __fmul_rn(a.eff[b], qmin));
     a.y[b] = y;
     if (!isfinite(y)) atomicOr(a.status, 2u);

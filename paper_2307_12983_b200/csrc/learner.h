@@ -9,6 +9,7 @@
 #include "mlp_host.h"
 #include "net.h"
 #include "replay_host.h"
+#include "sac_host.h"
 
 struct pqlg_comm_s;
 
@@ -23,9 +24,14 @@ class VLearner {
   ~VLearner();
 
   void adopt_policy(const float* flat_host, int64_t version);
+  // pql_sac: the snapshot's log_alpha travels with the net (messages.hpp:18-19)
+  void adopt_policy_sac(const float* flat_host, float log_alpha, int64_t version);
+  float log_alpha();
   void adopt_norm(int64_t count, const double* mean, const double* m2);
-  // asynchronous device-pointer variants (the run_parallel pipeline)
+  // asynchronous device-pointer variants (the run_parallel pipeline); the
+  // device snapshot is [net | log_alpha] (snapshot_len floats)
   void adopt_policy_device(const float* flat_dev, int64_t version);
+  int64_t snapshot_len() const { return pnet_.params + (sac_ ? 1 : 0); }
   void adopt_norm_device(const int64_t* count, const double* mean, const double* m2) {
     norm_.set_device(count, mean, m2, stream_);
   }
@@ -70,8 +76,11 @@ class VLearner {
   int rank_ = 0, world_ = 1;
   int D_, A_, H_, nh_, B_, Kp_;
   bool dist_ = false;  // PQL-D: categorical (C51) critics with L_ atoms
+  bool sac_ = false;   // pql_sac: Gaussian lagged policy, entropy term in the target
   int L_ = 1, Lp_ = 1;
   float reward_scale_, gamma_;
+  EpsStream eps_;      // pql_sac eps draws
+  DevBuf<float> logp_; // log pi(a'|s+) [B]
   NetShape qnet_, pnet_;
   int64_t Ps_ = 0;  // group stride of the twin-critic parameter blocks
   int64_t lagged_version_ = 0;
@@ -141,6 +150,9 @@ class PLearner {
   }
   int64_t policy_params() const { return pnet_.params; }
   int64_t critic_params() const { return qnet_.params; }
+  // device policy snapshot [net | log_alpha] (pql_sac) as the pipeline moves it
+  int64_t snapshot_len() const { return pnet_.params + (sac_ ? 1 : 0); }
+  float log_alpha();
   const NetShape& policy_shape() const { return pnet_; }
   const NetShape& critic_shape() const { return qnet_; }
   int64_t norm_count_ = 0;  // NormStats last adopted from the host (checkpointing)
@@ -174,7 +186,11 @@ class PLearner {
   pqlg_comm_s* comm_ = nullptr;  // data-parallel communicator (nullable)
   int rank_ = 0, world_ = 1;
   int D_, A_, Ap_, H_, nh_, B_, Kp_;
+  int Ah_ = 0, Ahp_ = 0;  // policy head outputs (A, or 2A for pql_sac) and padded stride
   bool dist_ = false;  // PQL-D actor objective (c51_actor_loss)
+  bool sac_ = false;   // pql_sac actor objective + alpha update
+  EpsStream eps_;
+  DevBuf<float> sd_, logp_;  // pql_sac: +-std [B x Ap], log pi [B]
   int L_ = 1, Lp_ = 1;
   NetShape qnet_, pnet_;
   int64_t Ps_ = 0;

@@ -181,19 +181,23 @@ struct HeadSplit {
   }
 };
 
-// The head GEMM: split-K partial tiles into hs.part (plans hs).
+// The head GEMM: split-K partial tiles into hs.part (plans hs).  N <= 32
+// (act_dim) or <= 64 (the SAC head's [mean | log_std]).
 inline Step head_gemm_step(HeadSplit& hs, const float* A0, int64_t lda, const float* W,
                            int64_t ldw, int M, int N, int K) {
-  require(N <= 32, "policy head: act_dim <= 32");
+  require(N <= 64, "policy head: at most 64 head outputs");
   hs.plan(M, N, K);
   gemm::Operands ops;
   std::memset(&ops, 0, sizeof(ops));
   ops.a[0] = gemm::map_a(A0, M, K, lda, false, true);
-  ops.b[0] = gemm::map_b(W, N, K, ldw, true, 32, true);
+  const int bn = N <= 32 ? 32 : 64;
+  ops.b[0] = gemm::map_b(W, N, K, ldw, true, bn, true);
   ops.d[0] = make_tmap_3d(hs.part.p, N, M, hs.splits, hs.ld_part,
                           static_cast<uint64_t>(M) * hs.ld_part, 32, 32, Swz::k128);
   const gemm::Problem p = gemm::make_problem(M, N, K, hs.splits);
-  return [ops, p](cudaStream_t st) { gemm::launch<32, false, true>(ops, p, 1, epi::Partial{}, st); };
+  if (bn == 32)
+    return [ops, p](cudaStream_t st) { gemm::launch<32, false, true>(ops, p, 1, epi::Partial{}, st); };
+  return [ops, p](cudaStream_t st) { gemm::launch<64, false, true>(ops, p, 1, epi::Partial{}, st); };
 }
 
 // The finish (bias, squash, noise, stores) of a planned head.

@@ -203,6 +203,17 @@ static __global__ void __launch_bounds__(kFinalizeThreads)
   a.scale[group] = s;
 }
 
+// pql_sac: sac_alpha_loss + adam_step on log alpha (sac.hpp:117-125,
+// learners.cpp:254-256), done by one thread of the policy's Adam launch.
+struct AlphaStep {
+  float* log_alpha;        // null: no alpha update
+  float* m;
+  float* v;
+  const float* mean_logp;  // this update's mean log-prob (detached)
+  float target_entropy;    // -act_dim (learners.cpp:217)
+  float lr;                // lr_actor
+};
+
 struct AdamArgs {
   float* p;        // [groups x n]
   const float* g;  // [groups x n]
@@ -217,6 +228,7 @@ struct AdamArgs {
   const float2* bc;     // bias-correction table, index t (clamped)
   int64_t bc_len;
   float lr, beta1, beta2, eps, tau;
+  AlphaStep alpha;
 };
 
 static __global__ void adam_polyak_kernel(AdamArgs a) {
@@ -232,6 +244,17 @@ static __global__ void adam_polyak_kernel(AdamArgs a) {
   const bool clipped = s != 1.0f;
   const float ob1 = __fsub_rn(1.0f, a.beta1), ob2 = __fsub_rn(1.0f, a.beta2);
   const float keep = __fsub_rn(1.0f, a.tau);
+  if (a.alpha.log_alpha && blockIdx.x == 0 && group == 0 && threadIdx.x == 0) {
+    const float drift = __fadd_rn(*a.alpha.mean_logp, a.alpha.target_entropy);
+    const float gi = -drift;  // dloss/dlog_alpha
+    const float mo = __fadd_rn(__fmul_rn(a.beta1, *a.alpha.m), __fmul_rn(ob1, gi));
+    const float vo = __fadd_rn(__fmul_rn(a.beta2, *a.alpha.v), __fmul_rn(ob2, __fmul_rn(gi, gi)));
+    const float upd = __fmul_rn(
+        a.alpha.lr, __fdiv_rn(__fmul_rn(mo, bc.x), __fadd_rn(__fsqrt_rn(__fmul_rn(vo, bc.y)), a.eps)));
+    *a.alpha.m = mo;
+    *a.alpha.v = vo;
+    *a.alpha.log_alpha = __fsub_rn(*a.alpha.log_alpha, upd);
+  }
   const int64_t off = group * a.gstride;
   float* __restrict__ P = a.p + off;
   const float* __restrict__ G = a.g + off;

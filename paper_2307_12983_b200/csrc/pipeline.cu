@@ -198,7 +198,7 @@ class Pipeline {
     Dp_ = round_up(D_, 4);
     Ap_ = round_up(A_, 4);
     H_ = rc.horizon;
-    const int64_t Pp = p_->policy_params(), Pq = p_->critic_params();
+    const int64_t Pp = p_->snapshot_len(), Pq = p_->critic_params();  // [net | log_alpha]
     pol_pool_.init(Pp);
     crit_pool_.init(2 * Pq);
     // one slot per in-flight actor iteration: both channels full + one being
@@ -355,7 +355,7 @@ class Pipeline {
   // (states, critic snapshot, normalizer) to the P-learner, gate.
   void actor_loop() {
     int64_t seq = 0, crit_have = 0;
-    const int64_t Pp = p_->policy_params(), Pq = p_->critic_params();
+    const int64_t Pp = p_->snapshot_len(), Pq = p_->critic_params();  // [net | log_alpha]
     while (true) {
       bool go = false;
       while (!go) {
@@ -472,7 +472,7 @@ class Pipeline {
   void plearner_loop() {
     ConsumerStats& st = stats_[1];
     int64_t updates = 0;
-    const int64_t Pq = p_->critic_params(), Pp = p_->policy_params();
+    const int64_t Pq = p_->critic_params(), Pp = p_->snapshot_len();
     bool have_batch = false;
     auto ready = [&] {
       if (gate_.count(kActor) < cfg_.warm_up) return false;

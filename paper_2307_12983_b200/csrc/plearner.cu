@@ -17,6 +17,7 @@
 #include "critic_kernels.cuh"
 #include "learner.h"
 #include "optim.cuh"
+#include "sac_host.h"
 
 namespace pqlg {
 
@@ -31,8 +32,10 @@ PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
     PQLG_CUDA(cudaStreamCreateWithFlags(&owned_stream_, cudaStreamNonBlocking));
     stream_ = owned_stream_;
   }
-  require(cfg.algo == PQLG_ALGO_DDPG || cfg.algo == PQLG_ALGO_C51, "plearner: unknown algo");
+  require(cfg.algo == PQLG_ALGO_DDPG || cfg.algo == PQLG_ALGO_C51 || cfg.algo == PQLG_ALGO_SAC,
+          "plearner: unknown algo");
   dist_ = cfg.algo == PQLG_ALGO_C51;
+  sac_ = cfg.algo == PQLG_ALGO_SAC;
   if (dist_) {
     require(cfg.n_atoms >= 2 && cfg.n_atoms <= c51::kMaxAtoms,
             "plearner: n_atoms must be in [2, 64]");
@@ -57,7 +60,9 @@ PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
     ps.push_back(H_);
   }
   qs.push_back(L_);  // learners.cpp:206-209
-  ps.push_back(A_);
+  Ah_ = sac_ ? 2 * A_ : A_;  // GaussianPolicy head: [mean | log_std] (learners.cpp:20-22)
+  Ahp_ = static_cast<int>(round_up(Ah_, 4));
+  ps.push_back(Ah_);
   qnet_ = NetShape::make(qs);
   pnet_ = NetShape::make(ps);
   Ps_ = round_up(qnet_.params, 64);
@@ -71,9 +76,11 @@ PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   std::mt19937_64 prng(rng::derive_seed(cfg.seed, rng::kInit, 0));
   init_orthogonal(pnet_, pol, prng, static_cast<float>(std::sqrt(2.0)), 1e-2f);
   q_.alloc(2 * Ps_);
-  pol_.alloc(pnet_.params);
-  m_.alloc(pnet_.params);
-  v_.alloc(pnet_.params);
+  // [net | log_alpha] (log alpha starts at 0, learners.cpp:218); its Adam
+  // moments sit at the same index of m_ / v_
+  pol_.alloc(snapshot_len());
+  m_.alloc(snapshot_len());
+  v_.alloc(snapshot_len());
   grads_.alloc(pnet_.params);
   PQLG_CUDA(cudaMemcpy(q_.p, q1.data(), q1.size() * 4, cudaMemcpyHostToDevice));
   PQLG_CUDA(cudaMemcpy(q_.p + Ps_, q2.data(), q2.size() * 4, cudaMemcpyHostToDevice));
@@ -89,12 +96,16 @@ PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   mt_.seed(skey);
   idx_.alloc(B_);
   idx_host_.resize(B_);
+  // eps stream make_rng(seed, sac, 2) (learners.cpp:213); rank r: 2 + 2r
+  if (sac_)
+    eps_.init(rng::derive_seed(cfg.seed, rng::kSac, 2 + 2 * static_cast<uint64_t>(rank_)),
+              static_cast<int64_t>(B_) * A_);
   step_.alloc(1);
   auto tab = mlp::adam_bias_table(0.9, 0.999);
   bc_.alloc(tab.size());
   PQLG_CUDA(cudaMemcpy(bc_.p, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
   status_.alloc(1);
-  loss_.alloc(1);
+  loss_.alloc(2);  // actor loss (+ pql_sac: mean log-prob for the alpha update)
   build_update();
   PQLG_CUDA(cudaDeviceSynchronize());
 }
@@ -121,7 +132,11 @@ void PLearner::build_update() {
 
   X_.alloc(static_cast<size_t>(B) * Kp_);
   T_.alloc(static_cast<size_t>(B) * Ap_);
-  dy_.alloc(static_cast<size_t>(B) * Ap_);
+  dy_.alloc(static_cast<size_t>(B) * Ahp_);
+  if (sac_) {
+    sd_.alloc(static_cast<size_t>(B) * Ap_);
+    logp_.alloc(B);
+  }
   up_.alloc(2ull * B);
   part_.alloc(2ull * nt * B);
   pact_.resize(nh);
@@ -144,7 +159,8 @@ void PLearner::build_update() {
     dact_[k].alloc(static_cast<size_t>(B) * Ap_);
   }
   const int loss_blocks = (B + critic::kRowThreads - 1) / critic::kRowThreads;
-  block_loss_.alloc((B + c51::kThreads - 1) / c51::kThreads);  // >= either pick kernel's grid
+  block_loss_.alloc(std::max((B + c51::kThreads - 1) / c51::kThreads,
+                             2 * ((B + sac::kRowThreads - 1) / sac::kRowThreads)));
   if (dist_) {
     const auto z = c51_atoms(L_, static_cast<float>(cfg_.vmin), static_cast<float>(cfg_.vmax));
     atoms_.alloc(L_);
@@ -164,6 +180,12 @@ void PLearner::build_update() {
     const uint64_t* idx = mt_mode_ ? idx_.p : nullptr;
     launch_state_sample(*states_, norm_.view(), X_.p, Kp_, sampler_.p, idx, B, st);
   });
+  if (sac_) {  // eps of the reparameterised actions (learners.cpp:247-249)
+    steps_.push_back([this](cudaStream_t st) {
+      if (mt_mode_) eps_.fill_mt(st);
+      else eps_.enqueue(st);
+    });
+  }
 
   // -------------------------------------------------------- policy forward
   {
@@ -185,18 +207,36 @@ void PLearner::build_update() {
       ld = H;
       K = H;
     }
-    head::FinishArgs ph{};
-    ph.bias = pol_.p + pnet_.b_off[nh];
-    ph.act = X_.p + D;  // critic input [norm(s) | pi(s)]
-    ph.ld_act = Kp_;
-    ph.tanh_out = T_.p;
-    ph.ld_tanh = Ap_;
-    ph.mid = (dims_.low + dims_.high) / 2.0f;
-    ph.half = (dims_.high - dims_.low) / 2.0f;
-    head_.init(pol_.p + pnet_.w_off[nh], H, A);
+    head_.init(pol_.p + pnet_.w_off[nh], H, Ah_);
     head_.refresh(stream_);
-    steps_.push_back(mlp::head_gemm_step(head_split_, in, ld, head_.ptr(), head_.stride(), B, A, H));
-    steps_.push_back(mlp::head_finish_step(head_split_, ph, B, A));
+    steps_.push_back(
+        mlp::head_gemm_step(head_split_, in, ld, head_.ptr(), head_.stride(), B, Ah_, H));
+    if (sac_) {
+      // s = policy.sample(states, eps) (sac.hpp:77): actions, log-probs, and
+      // tanh(pre) / std kept for the backward
+      sac::GaussArgs g{};
+      g.bias = pol_.p + pnet_.b_off[nh];
+      g.eps = eps_.out.p;
+      g.act = X_.p + D;
+      g.ld_act = Kp_;
+      g.logp = logp_.p;
+      g.tanh_out = T_.p;
+      g.sd_out = sd_.p;
+      g.ld_aux = Ap_;
+      g.mid = (dims_.low + dims_.high) / 2.0f;
+      g.half = (dims_.high - dims_.low) / 2.0f;
+      steps_.push_back(gauss_finish_step(head_split_, g, B, A));
+    } else {
+      head::FinishArgs ph{};
+      ph.bias = pol_.p + pnet_.b_off[nh];
+      ph.act = X_.p + D;  // critic input [norm(s) | pi(s)]
+      ph.ld_act = Kp_;
+      ph.tanh_out = T_.p;
+      ph.ld_tanh = Ap_;
+      ph.mid = (dims_.low + dims_.high) / 2.0f;
+      ph.half = (dims_.high - dims_.low) / 2.0f;
+      steps_.push_back(mlp::head_finish_step(head_split_, ph, B, A));
+    }
   }
 
   // ------------------------------------------ twin critic replicas forward
@@ -265,6 +305,29 @@ void PLearner::build_update() {
     const int blocks = (B + c51::kThreads - 1) / c51::kThreads;
     steps_.push_back([a, blocks](cudaStream_t st) {
       launch(c51::c51_actor_pick_kernel, dim3(blocks), dim3(c51::kThreads), 0, st, a);
+    });
+  } else if (sac_) {
+    // sac_actor_loss rows (sac.hpp:86-96): loss, mean log-prob, upstream
+    sac::PickArgs a{};
+    a.partial = part_.p;
+    a.ld = B;
+    a.n_tiles = nt;
+    a.q1 = q[0];
+    a.q2 = q[1];
+    a.head_b_off = qnet_.b_off[nh];
+    a.logp = logp_.p;
+    a.log_alpha = pol_.p + pnet_.params;
+    a.up = up_.p;
+    a.step = step_.p;
+    a.block_part = block_loss_.p;
+    a.counter = loss_counter_.p;
+    a.out = loss_.p;
+    a.status = status_.p;
+    a.B = B;
+    a.Bg = B * world_;
+    const int blocks = (B + sac::kRowThreads - 1) / sac::kRowThreads;
+    steps_.push_back([a, blocks](cudaStream_t st) {
+      launch(sac::sac_pick_kernel, dim3(blocks), dim3(sac::kRowThreads), 0, st, a);
     });
   } else {
     critic::LossArgs a{};
@@ -337,8 +400,30 @@ void PLearner::build_update() {
   }
   // ------------------------------------------------- policy head backward
   const int ptiles = (B + 7) / 8;  // policy-head backward tiles (8 rows, one warp each)
-  head_db_.alloc(static_cast<size_t>(ptiles) * A);
-  {
+  head_db_.alloc(static_cast<size_t>(ptiles) * Ah_);
+  if (sac_) {
+    // GaussianPolicy::backward's dy (policy.hpp:127-150), dlogp = alpha / B
+    sac::HeadBwdArgs a{};
+    a.dact1 = dact_[0].p;
+    a.dact2 = dact_[1].p;
+    a.ld_dact = Ap_;
+    a.tanh_in = T_.p;
+    a.sd_in = sd_.p;
+    a.ld_aux = Ap_;
+    a.eps = eps_.out.p;
+    a.log_alpha = pol_.p + pnet_.params;
+    a.dy = dy_.p;
+    a.ld_dy = Ahp_;
+    a.db_part = head_db_.p;
+    a.half = (dims_.high - dims_.low) / 2.0f;
+    a.B = B;
+    a.A = A;
+    a.Bg = B * world_;
+    a.rows_per_tile = 8;
+    steps_.push_back([a, ptiles](cudaStream_t st) {
+      launch(sac::sac_head_backward_kernel, dim3(ptiles), dim3(32), 0, st, a);
+    });
+  } else {
     critic::PolicyHeadBwdArgs a{};
     a.dact1 = dact_[0].p;
     a.dact2 = dact_[1].p;
@@ -362,15 +447,15 @@ void PLearner::build_update() {
   wsplits_.resize(nh + 1);
   for (int l = 0; l <= nh; ++l) {
     const int in = l == 0 ? D : H;
-    const int out = l == nh ? A : H;
-    const int ldo = l == nh ? Ap_ : H;
+    const int out = l == nh ? Ah_ : H;
+    const int ldo = l == nh ? Ahp_ : H;
     wsplits_[l] = mlp::wgrad_splits(in, out, B, 1);
     wpart_[l].alloc(static_cast<size_t>(wsplits_[l]) * in * ldo);
     if (l < nh) colsum_[l].alloc(static_cast<size_t>(mt) * H);
   }
   // head layer: dW_nh = act_{nh-1}^T dy ; G_{nh-1} = (dy W_nh^T) * mask
-  steps_.push_back(mlp::wgrad(pact_[nh - 1].p, pact_[nh - 1].p, H, dy_.p, dy_.p, Ap_, H, A, B, 1,
-                              wsplits_[nh], epi::Partial{}, wpart_[nh].p, Ap_));
+  steps_.push_back(mlp::wgrad(pact_[nh - 1].p, pact_[nh - 1].p, H, dy_.p, dy_.p, Ahp_, H, Ah_, B,
+                              1, wsplits_[nh], epi::Partial{}, wpart_[nh].p, Ahp_));
   {
     epi::DgradMask dm{};
     dm.mask[0] = dm.mask[1] = pmask_[nh - 1].p;
@@ -381,8 +466,8 @@ void PLearner::build_update() {
     dm.bn = bnH;
     dm.M = B;
     dm.N = H;
-    steps_.push_back(mlp::dgrad(dy_.p, dy_.p, Ap_, head_.ptr(), head_.ptr(), head_.stride(), B,
-                                H, A, 1, dm, Gp_[nh - 1].p, Gp_[nh - 1].p, H));
+    steps_.push_back(mlp::dgrad(dy_.p, dy_.p, Ahp_, head_.ptr(), head_.ptr(), head_.stride(), B,
+                                H, Ah_, 1, dm, Gp_[nh - 1].p, Gp_[nh - 1].p, H));
   }
   for (int l = nh - 1; l >= 0; --l) {
     const int in = l == 0 ? D : H;
@@ -415,12 +500,12 @@ void PLearner::build_update() {
                                   wsplits_[l], static_cast<int64_t>(in) * H};
       f.seg[s++] = optim::Segment{pnet_.b_off[l], H, colsum_[l].p, 0, mt, H};
     }
-    optim::Segment wh{pnet_.w_off[nh], static_cast<int64_t>(H) * A, wpart_[nh].p, 0,
-                      wsplits_[nh], static_cast<int64_t>(H) * Ap_};
-    wh.cols = A;
-    wh.ld_src = Ap_;
+    optim::Segment wh{pnet_.w_off[nh], static_cast<int64_t>(H) * Ah_, wpart_[nh].p, 0,
+                      wsplits_[nh], static_cast<int64_t>(H) * Ahp_};
+    wh.cols = Ah_;
+    wh.ld_src = Ahp_;
     f.seg[s++] = wh;
-    f.seg[s++] = optim::Segment{pnet_.b_off[nh], A, head_db_.p, 0, ptiles, A};
+    f.seg[s++] = optim::Segment{pnet_.b_off[nh], Ah_, head_db_.p, 0, ptiles, Ah_};
     require(s <= optim::kMaxSegments, "plearner: too many layers");
     f.n_seg = s;
     f.total = pnet_.params;
@@ -444,7 +529,8 @@ void PLearner::build_update() {
       float* g = grads_.p;
       float* l = loss_.p;
       const size_t n = static_cast<size_t>(pnet_.params);
-      steps_.push_back([c, g, n, l](cudaStream_t st) { allreduce_sum(c, g, n, l, 1, st); });
+      const int nl = sac_ ? 2 : 1;  // + the mean log-prob of the alpha update
+      steps_.push_back([c, g, n, l, nl](cudaStream_t st) { allreduce_sum(c, g, n, l, nl, st); });
       optim::FinalizeArgs f2 = f;
       f2.seg[0] = optim::Segment{0, pnet_.params, grads_.p, 0, 1, 0};
       f2.n_seg = 1;
@@ -475,6 +561,14 @@ void PLearner::build_update() {
     a.beta2 = 0.999f;
     a.eps = 1e-8f;
     a.tau = 0.0f;
+    if (sac_) {  // alpha step (learners.cpp:254-256), Adam state at index params
+      a.alpha.log_alpha = pol_.p + pnet_.params;
+      a.alpha.m = m_.p + pnet_.params;
+      a.alpha.v = v_.p + pnet_.params;
+      a.alpha.mean_logp = loss_.p + 1;
+      a.alpha.target_entropy = -static_cast<float>(A);
+      a.alpha.lr = static_cast<float>(cfg_.lr_actor);
+    }
     const int blocks = static_cast<int>(std::min<int64_t>(4 * mlp::kSMs, (pnet_.params + 255) / 256));
     steps_.push_back([a, blocks](cudaStream_t st) {
       launch(optim::adam_polyak_kernel, dim3(dim3(blocks, 1)), dim3(256), 0, st, a);
@@ -622,6 +716,15 @@ int64_t PLearner::param_count(int which) const {
   return which == 0 ? pnet_.params : qnet_.params;
 }
 
+float PLearner::log_alpha() {
+  float v = 0.0f;
+  if (sac_) {
+    PQLG_CUDA(cudaMemcpyAsync(&v, pol_.p + pnet_.params, 4, cudaMemcpyDeviceToHost, stream_));
+    PQLG_CUDA(cudaStreamSynchronize(stream_));
+  }
+  return v;
+}
+
 }  // namespace pqlg
 
 // ------------------------------------------------------------------ C ABI
@@ -717,6 +820,10 @@ int pqlg_plearner_set_params(pqlg_plearner h, int which, const float* flat) {
 
 int pqlg_plearner_param_count(pqlg_plearner h, int which, int64_t* out) {
   return guarded([&] { *out = h->p->param_count(which); });
+}
+
+int pqlg_plearner_log_alpha(pqlg_plearner h, float* out) {
+  return guarded([&] { *out = h->p->log_alpha(); });
 }
 
 int pqlg_plearner_buffer_size(pqlg_plearner h, uint64_t* out) {

@@ -15,6 +15,7 @@
 #include "critic_kernels.cuh"
 #include "learner.h"
 #include "optim.cuh"
+#include "sac_host.h"
 
 namespace pqlg {
 
@@ -32,8 +33,11 @@ VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
     stream_ = owned_stream_;
   }
   st = stream_;
-  require(cfg.algo == PQLG_ALGO_DDPG || cfg.algo == PQLG_ALGO_C51, "vlearner: unknown algo");
+  require(cfg.algo == PQLG_ALGO_DDPG || cfg.algo == PQLG_ALGO_C51 || cfg.algo == PQLG_ALGO_SAC,
+          "vlearner: unknown algo");
   dist_ = cfg.algo == PQLG_ALGO_C51;
+  sac_ = cfg.algo == PQLG_ALGO_SAC;
+  require(!sac_ || dims.act_dim <= 32, "vlearner: pql_sac needs act_dim <= 32");
   if (dist_) {
     // CategoricalHead::create (c51.hpp:21-27) validation
     require(cfg.n_atoms >= 2 && cfg.n_atoms <= c51::kMaxAtoms,
@@ -60,7 +64,7 @@ VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
     ps.push_back(H_);
   }
   qs.push_back(L_);  // learners.cpp:127-130: n_atoms outputs for pql_d, else 1
-  ps.push_back(A_);
+  ps.push_back(sac_ ? 2 * A_ : A_);  // GaussianPolicy: [mean | log_std] (learners.cpp:20-22)
   qnet_ = NetShape::make(qs);
   pnet_ = NetShape::make(ps);
   const int64_t P = qnet_.params;
@@ -79,7 +83,7 @@ VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   m_.alloc(2 * Ps);
   v_.alloc(2 * Ps);
   grads_.alloc(2 * Ps);
-  lagged_.alloc(pnet_.params);
+  lagged_.alloc(snapshot_len());  // [net | log_alpha] for pql_sac
   PQLG_CUDA(cudaMemcpy(q_.p, q1.data(), P * 4, cudaMemcpyHostToDevice));
   PQLG_CUDA(cudaMemcpy(q_.p + Ps, q2.data(), P * 4, cudaMemcpyHostToDevice));
   PQLG_CUDA(cudaMemcpy(qt_.p, q_.p, 2 * Ps * 4, cudaMemcpyDeviceToDevice));
@@ -98,6 +102,10 @@ VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   mt_.seed(skey);
   idx_.alloc(B_);
   idx_host_.resize(B_);
+  // eps stream make_rng(seed, sac, 1) (learners.cpp:137); rank r: 1 + 2r
+  if (sac_)
+    eps_.init(rng::derive_seed(cfg.seed, rng::kSac, 1 + 2 * static_cast<uint64_t>(rank_)),
+              static_cast<int64_t>(B_) * A_);
 
   // --- optimizer state
   step_.alloc(1);
@@ -182,6 +190,13 @@ void VLearner::build_update() {
     replay::Gather g{Xon_.p, Kp_, Xon_.p + D_, Kp_, Xtg_.p, Kp_, ret_.p, eff_.p};
     launch_replay_sample(*replay_, norm_.view(), g, sampler_.p, idx, B, st);
   });
+  if (sac_) {  // eps for the reparameterised next actions (learners.cpp:171-173)
+    logp_.alloc(B);
+    steps_.push_back([this](cudaStream_t st) {
+      if (mt_mode_) eps_.fill_mt(st);
+      else eps_.enqueue(st);
+    });
+  }
 
   // ------------------------------------------- target policy (lagged, 1 group)
   {
@@ -201,17 +216,31 @@ void VLearner::build_update() {
       ld = H;
       K = H;
     }
-    head::FinishArgs ph{};
-    ph.bias = lagged_.p + pnet_.b_off[nh];
-    ph.act = Xtg_.p + D;  // critic target input [norm(boot) | pi(boot)]
-    ph.ld_act = Kp_;
-    ph.mid = (dims_.low + dims_.high) / 2.0f;
-    ph.half = (dims_.high - dims_.low) / 2.0f;
-    lagged_head_.init(lagged_.p + pnet_.w_off[nh], H, A);
+    const int hout = sac_ ? 2 * A : A;
+    lagged_head_.init(lagged_.p + pnet_.w_off[nh], H, hout);
     lagged_head_.refresh(stream_);
     steps_.push_back(mlp::head_gemm_step(head_split_, in, ld, lagged_head_.ptr(),
-                                         lagged_head_.stride(), B, A, H));
-    steps_.push_back(mlp::head_finish_step(head_split_, ph, B, A));
+                                         lagged_head_.stride(), B, hout, H));
+    if (sac_) {
+      // next = lagged.sample(boot, eps) (sac.hpp:31): actions + log-probs
+      sac::GaussArgs g{};
+      g.bias = lagged_.p + pnet_.b_off[nh];
+      g.eps = eps_.out.p;
+      g.act = Xtg_.p + D;
+      g.ld_act = Kp_;
+      g.logp = logp_.p;
+      g.mid = (dims_.low + dims_.high) / 2.0f;
+      g.half = (dims_.high - dims_.low) / 2.0f;
+      steps_.push_back(gauss_finish_step(head_split_, g, B, A));
+    } else {
+      head::FinishArgs ph{};
+      ph.bias = lagged_.p + pnet_.b_off[nh];
+      ph.act = Xtg_.p + D;  // critic target input [norm(boot) | pi(boot)]
+      ph.ld_act = Kp_;
+      ph.mid = (dims_.low + dims_.high) / 2.0f;
+      ph.half = (dims_.high - dims_.low) / 2.0f;
+      steps_.push_back(mlp::head_finish_step(head_split_, ph, B, A));
+    }
   }
 
   // ---------- twin target + twin online critics: one 4-group launch per layer
@@ -318,6 +347,10 @@ void VLearner::build_update() {
     a.ret = ret_.p;
     a.eff = eff_.p;
     a.y = y_.p;
+    if (sac_) {  // y = G + eff * (min Q' - alpha log pi) (sac.hpp:36-41)
+      a.logp = logp_.p;
+      a.log_alpha = lagged_.p + pnet_.params;
+    }
     a.step = step_.p;
     a.up = up_.p;
     a.block_loss = block_loss_.p;
@@ -519,9 +552,21 @@ void VLearner::adopt_policy(const float* flat, int64_t version) {
   lagged_version_ = version;
 }
 
+void VLearner::adopt_policy_sac(const float* flat, float log_alpha, int64_t version) {
+  require(sac_, "adopt_policy_sac: learner is not pql_sac");
+  if (version < lagged_version_) return;
+  PQLG_CUDA(cudaMemcpyAsync(lagged_.p, flat, pnet_.params * 4, cudaMemcpyHostToDevice, stream_));
+  PQLG_CUDA(cudaMemcpyAsync(lagged_.p + pnet_.params, &log_alpha, 4, cudaMemcpyHostToDevice,
+                            stream_));
+  lagged_head_.refresh(stream_);
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+  lagged_version_ = version;
+}
+
 void VLearner::adopt_policy_device(const float* flat, int64_t version) {
   if (version < lagged_version_) return;  // learners.cpp:37-42
-  PQLG_CUDA(cudaMemcpyAsync(lagged_.p, flat, pnet_.params * 4, cudaMemcpyDeviceToDevice, stream_));
+  PQLG_CUDA(cudaMemcpyAsync(lagged_.p, flat, snapshot_len() * 4, cudaMemcpyDeviceToDevice,
+                            stream_));
   lagged_head_.refresh(stream_);
   lagged_version_ = version;
 }
@@ -685,6 +730,15 @@ void VLearner::set_params(int which, const float* flat) {
   PQLG_CUDA(cudaStreamSynchronize(stream_));
 }
 
+float VLearner::log_alpha() {
+  float v = 0.0f;
+  if (sac_) {
+    PQLG_CUDA(cudaMemcpyAsync(&v, lagged_.p + pnet_.params, 4, cudaMemcpyDeviceToHost, stream_));
+    PQLG_CUDA(cudaStreamSynchronize(stream_));
+  }
+  return v;
+}
+
 void VLearner::debug_read(int what, float* out) {
   const int64_t P = qnet_.params;
   switch (what) {
@@ -709,7 +763,20 @@ void VLearner::debug_read(int what, float* out) {
       PQLG_CUDA(cudaMemcpy2DAsync(out, (D_ + A_) * 4, Xon_.p, Kp_ * 4, (D_ + A_) * 4, B_,
                                   cudaMemcpyDeviceToHost, stream_));
       break;
-    default: throw Error(PQLG_EINVAL, "debug_read: what must be 0..4");
+    case 5:  // pql_sac: this update's eps [B x A]
+      require(sac_, "debug_read(5): pql_sac only");
+      PQLG_CUDA(cudaMemcpyAsync(out, eps_.out.p, static_cast<size_t>(B_) * A_ * 4,
+                                cudaMemcpyDeviceToHost, stream_));
+      break;
+    case 6:  // pql_sac: log pi(a'|s+) of the target actions [B]
+      require(sac_, "debug_read(6): pql_sac only");
+      PQLG_CUDA(cudaMemcpyAsync(out, logp_.p, B_ * 4, cudaMemcpyDeviceToHost, stream_));
+      break;
+    case 7:  // the target critics' input [B x (D + A)]: [norm(boot) | a']
+      PQLG_CUDA(cudaMemcpy2DAsync(out, (D_ + A_) * 4, Xtg_.p, Kp_ * 4, (D_ + A_) * 4, B_,
+                                  cudaMemcpyDeviceToHost, stream_));
+      break;
+    default: throw Error(PQLG_EINVAL, "debug_read: what must be 0..7");
   }
   PQLG_CUDA(cudaStreamSynchronize(stream_));
 }
@@ -793,6 +860,15 @@ int pqlg_vlearner_destroy(pqlg_vlearner h) {
 
 int pqlg_vlearner_adopt_policy(pqlg_vlearner h, const float* flat, int64_t version) {
   return guarded([&] { h->v->adopt_policy(flat, version); });
+}
+
+int pqlg_vlearner_adopt_policy_sac(pqlg_vlearner h, const float* flat, float log_alpha,
+                                   int64_t version) {
+  return guarded([&] { h->v->adopt_policy_sac(flat, log_alpha, version); });
+}
+
+int pqlg_vlearner_log_alpha(pqlg_vlearner h, float* out) {
+  return guarded([&] { *out = h->v->log_alpha(); });
 }
 
 int pqlg_vlearner_adopt_norm(pqlg_vlearner h, const pqlg_norm_stats* n) {
