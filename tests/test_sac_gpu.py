@@ -67,7 +67,7 @@ def test_eps_stream_bit_exact_and_counter_advance(B, A):
     normal_distribution over the same Philox URBG (orc_normals, kind 1), for
     3 consecutive updates: the counter advance is exact too.  B*A odd for
     (64, 3) -> the last pair's cached value is discarded."""
-    D, H, nh, n = 6, 32, 2, 400
+    D, H, nh, n = 6, 32, 2, B + 400
     rng = np.random.default_rng(5)
     h = make_vl(D, A, H, nh, B, n)
     insert_rows(h, *random_rows(rng, n, D, A))
@@ -179,7 +179,8 @@ def test_sac_target_sample_vs_oracle():
     rng = np.random.default_rng(22)
     h = make_vl(D, A, H, nh, B, n)
     Pp = param_count([D] + [H] * nh + [2 * A])
-    pol = f32(rng.standard_normal(Pp) * 0.3)  # log_std spread over the clamp range
+    pol = params(h, 4, Pp)  # orthogonal init; log_std biases spread over both clamps
+    pol[Pp - A:] = np.linspace(-6.0, 3.0, A, dtype=np.float32)
     v_adopt(h, pol, 0.2)
     insert_rows(h, *random_rows(rng, n, D, A))
     v_update(h)
