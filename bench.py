@@ -310,17 +310,23 @@ def run_ours(args, rank, world, local):
                 clocks=clk.summary(), launches=int(launches), kpu=kpu.value)
 
 
-def run_c51(args, rank, world, local, steps, warmup):
+def run_c51(args, rank, world, local, steps, warmup, sac=False):
     """Config 4 (PQL-D): C51 critic updates/s and policy updates/s at batch
-    8192 with 51 atoms on [-10, 10], c3 dims, graph-replayed."""
+    8192 with 51 atoms on [-10, 10], c3 dims, graph-replayed.  sac=True: the
+    same legs for pql_sac (Gaussian policy, entropy-regularised target, alpha
+    step) at config 3."""
     import torch
     from paper_2307_12983_b200 import _lib
     D, A, H, nh, B, N, cap = CONFIGS["c3"]
     stream = torch.cuda.Stream(device=local)
     sp = C.c_void_p(stream.cuda_stream)
-    cfg = _lib.default_config(algo=_lib.ALGO_C51, n_atoms=51, vmin=-10.0, vmax=10.0,
-                              reward_scale=0.01, batch_size=B, buffer_capacity=1_000_000,
-                              hidden=H, hidden_layers=nh, n_envs=N, seed=0)
+    if sac:
+        cfg = _lib.default_config(algo=_lib.ALGO_SAC, batch_size=B, buffer_capacity=1_000_000,
+                                  hidden=H, hidden_layers=nh, n_envs=N, seed=0)
+    else:
+        cfg = _lib.default_config(algo=_lib.ALGO_C51, n_atoms=51, vmin=-10.0, vmax=10.0,
+                                  reward_scale=0.01, batch_size=B, buffer_capacity=1_000_000,
+                                  hidden=H, hidden_layers=nh, n_envs=N, seed=0)
     dims = _lib.TaskDims(D, A, -1.0, 1.0)
     vl, pl = C.c_void_p(), C.c_void_p()
     comm = _lib.comm_from_torch_dist(rank, world) if (world > 1 or args.force_dp) else None
@@ -335,7 +341,8 @@ def run_c51(args, rank, world, local, steps, warmup):
     _lib.call("pqlg_replay_fill_synthetic", rp, 1_000_000, 2000 + rank, np.float32(0.970299), 200)
     states = torch.randn(1_000_000, D, device=f"cuda:{local}")
     _lib.call("pqlg_plearner_ingest", pl, states.data_ptr(), D, 1_000_000)
-    out = {"workload": "c4: PQL-D critic (51 atoms on [-10, 10]) + policy, c3 dims, batch 8192"}
+    out = {"workload": ("c3: pql_sac critic + policy/alpha, batch 8192" if sac else
+                        "c4: PQL-D critic (51 atoms on [-10, 10]) + policy, c3 dims, batch 8192")}
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for key, h, fn in (("critic_updates", vl, "pqlg_vlearner_update_n"),
                        ("policy_updates", pl, "pqlg_plearner_update_n")):
@@ -634,6 +641,8 @@ def main():
     actor = run_actor(args, rank, world, local, max(10, args.steps // 4), max(3, args.warmup // 4))
     policy = run_policy(args, rank, world, local, args.steps, args.warmup)
     c51 = run_c51(args, rank, world, local, max(10, args.steps // 2), max(3, args.warmup // 2))
+    sac = run_c51(args, rank, world, local, max(10, args.steps // 2), max(3, args.warmup // 2),
+                  sac=True)
     pipe = run_pipeline(args, rank, world, local, 400)
     if rank != 0:
         return
@@ -641,6 +650,7 @@ def main():
     out["actor"] = actor
     out["policy_updates"] = policy
     out["c51"] = c51
+    out["sac"] = sac
     out["run_parallel"] = pipe
     out.update(value=r["value"], ms_per_step=r["ms_step"], e2e=r["e2e"], roofline=r["roof"],
                clocks=r["clocks"], gpu_launches=r["launches"],

@@ -29,16 +29,18 @@ def fill(rp, n, seed):
     _lib.call("pqlg_replay_fill_synthetic", rp, n, seed, np.float32(0.970299), 200)
 
 
-@pytest.mark.parametrize("D,A,H,nh,B", [(17, 6, 64, 2, 256), (211, 20, 512, 3, 1024)])
-def test_vlearner_dp_world1_bit_identical(D, A, H, nh, B):
+@pytest.mark.parametrize("D,A,H,nh,B,algo", [(17, 6, 64, 2, 256, _lib.ALGO_DDPG),
+                                             (211, 20, 512, 3, 1024, _lib.ALGO_DDPG),
+                                             (17, 6, 64, 2, 256, _lib.ALGO_SAC)])
+def test_vlearner_dp_world1_bit_identical(D, A, H, nh, B, algo):
     import torch
     torch.cuda.set_device(0)
     comm = comm_world1()
     r, w = C.c_int(), C.c_int()
     _lib.call("pqlg_comm_rank", comm, C.byref(r), C.byref(w))
     assert (r.value, w.value) == (0, 1)
-    cfg = _lib.default_config(batch_size=B, buffer_capacity=20000, hidden=H, hidden_layers=nh,
-                              n_envs=8)
+    cfg = _lib.default_config(algo=algo, batch_size=B, buffer_capacity=20000, hidden=H,
+                              hidden_layers=nh, n_envs=8)
     dims = _lib.TaskDims(D, A, -1.0, 1.0)
     plain, dp = C.c_void_p(), C.c_void_p()
     _lib.call("pqlg_vlearner_create", C.byref(cfg), C.byref(dims), 7, None, C.byref(plain))
@@ -75,13 +77,14 @@ def test_vlearner_dp_world1_bit_identical(D, A, H, nh, B):
     _lib.call("pqlg_comm_destroy", comm)
 
 
-def test_plearner_dp_world1_bit_identical():
+@pytest.mark.parametrize("algo", [_lib.ALGO_DDPG, _lib.ALGO_SAC])
+def test_plearner_dp_world1_bit_identical(algo):
     import torch
     torch.cuda.set_device(0)
     D, A, H, nh, B = 31, 7, 64, 2, 512
     comm = comm_world1()
-    cfg = _lib.default_config(batch_size=B, buffer_capacity=10000, hidden=H, hidden_layers=nh,
-                              n_envs=8)
+    cfg = _lib.default_config(algo=algo, batch_size=B, buffer_capacity=10000, hidden=H,
+                              hidden_layers=nh, n_envs=8)
     dims = _lib.TaskDims(D, A, -1.0, 1.0)
     plain, dp = C.c_void_p(), C.c_void_p()
     _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 5, None, C.byref(plain))
@@ -94,12 +97,17 @@ def test_plearner_dp_world1_bit_identical():
         _lib.call("pqlg_plearner_update", plain, C.byref(la))
         _lib.call("pqlg_plearner_update", dp, C.byref(lb))
         assert la.value == lb.value
-    P = param_count([D] + [H] * nh + [A])
+    P = param_count([D] + [H] * nh + [2 * A if algo == _lib.ALGO_SAC else A])
     a = np.zeros(P, np.float32)
     b = np.zeros(P, np.float32)
     _lib.call("pqlg_plearner_get_params", plain, 0, ptr(a))
     _lib.call("pqlg_plearner_get_params", dp, 0, ptr(b))
     assert np.array_equal(a, b)
+    if algo == _lib.ALGO_SAC:  # the alpha step sees the all-reduced mean log-prob
+        xa, xb = C.c_float(), C.c_float()
+        _lib.call("pqlg_plearner_log_alpha", plain, C.byref(xa))
+        _lib.call("pqlg_plearner_log_alpha", dp, C.byref(xb))
+        assert xa.value == xb.value != 0.0
     for h in (plain, dp):
         _lib.call("pqlg_plearner_destroy", h)
     _lib.call("pqlg_comm_destroy", comm)

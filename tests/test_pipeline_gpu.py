@@ -24,7 +24,7 @@ def run_pipeline(cfg, dims, rc, steps, seconds=60.0, seed=3):
     return rep
 
 
-@pytest.mark.parametrize("algo", [_lib.ALGO_DDPG, _lib.ALGO_C51])
+@pytest.mark.parametrize("algo", [_lib.ALGO_DDPG, _lib.ALGO_C51, _lib.ALGO_SAC])
 def test_pipeline_invariants(algo):
     cfg = _lib.default_config(algo=algo, n_envs=256, batch_size=512, buffer_capacity=100_000,
                               hidden=64, hidden_layers=2, seed=1)
