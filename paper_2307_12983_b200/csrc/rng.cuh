@@ -71,18 +71,20 @@ __host__ __device__ __forceinline__ uint64_t lemire_step(uint64_t x, uint64_t ra
 }
 
 // ------------------------------------------------------ glibc 2.39 logf
+// Table of glibc e_logf_data.c (LOGF_TABLE_BITS = 4): {invc, logc}.  In
+// global memory (read through the L1): a constexpr array indexed by a
+// per-lane value would be rebuilt on every call's stack.
+__device__ static const double2 kLogfTab[16] = {
+    {0x1.661ec79f8f3bep+0, -0x1.57bf7808caadep-2}, {0x1.571ed4aaf883dp+0, -0x1.2bef0a7c06ddbp-2},
+    {0x1.49539f0f010bp+0, -0x1.01eae7f513a67p-2},  {0x1.3c995b0b80385p+0, -0x1.b31d8a68224e9p-3},
+    {0x1.30d190c8864a5p+0, -0x1.6574f0ac07758p-3}, {0x1.25e227b0b8eap+0, -0x1.1aa2bc79c81p-3},
+    {0x1.1bb4a4a1a343fp+0, -0x1.a4e76ce8c0e5ep-4}, {0x1.12358f08ae5bap+0, -0x1.1973c5a611cccp-4},
+    {0x1.0953f419900a7p+0, -0x1.252f438e10c1ep-5}, {0x1p+0, 0x0p+0},
+    {0x1.e608cfd9a47acp-1, 0x1.aa5aa5df25984p-5},  {0x1.ca4b31f026aap-1, 0x1.c5e53aa362eb4p-4},
+    {0x1.b2036576afce6p-1, 0x1.526e57720db08p-3},  {0x1.9c2d163a1aa2dp-1, 0x1.bc2860d22477p-3},
+    {0x1.886e6037841edp-1, 0x1.1058bc8a07ee1p-2},  {0x1.767dcf5534862p-1, 0x1.4043057b6ee09p-2}};
+
 __device__ __forceinline__ float glibc_logf(float x) {
-  // Table and polynomial of glibc e_logf_data.c (LOGF_TABLE_BITS = 4).
-  constexpr double invc[16] = {
-      0x1.661ec79f8f3bep+0, 0x1.571ed4aaf883dp+0, 0x1.49539f0f010bp+0,  0x1.3c995b0b80385p+0,
-      0x1.30d190c8864a5p+0, 0x1.25e227b0b8eap+0,  0x1.1bb4a4a1a343fp+0, 0x1.12358f08ae5bap+0,
-      0x1.0953f419900a7p+0, 0x1p+0,               0x1.e608cfd9a47acp-1, 0x1.ca4b31f026aap-1,
-      0x1.b2036576afce6p-1, 0x1.9c2d163a1aa2dp-1, 0x1.886e6037841edp-1, 0x1.767dcf5534862p-1};
-  constexpr double logc[16] = {
-      -0x1.57bf7808caadep-2, -0x1.2bef0a7c06ddbp-2, -0x1.01eae7f513a67p-2, -0x1.b31d8a68224e9p-3,
-      -0x1.6574f0ac07758p-3, -0x1.1aa2bc79c81p-3,   -0x1.a4e76ce8c0e5ep-4, -0x1.1973c5a611cccp-4,
-      -0x1.252f438e10c1ep-5, 0x0p+0,                0x1.aa5aa5df25984p-5,  0x1.c5e53aa362eb4p-4,
-      0x1.526e57720db08p-3,  0x1.bc2860d22477p-3,   0x1.1058bc8a07ee1p-2,  0x1.4043057b6ee09p-2};
   constexpr double kLn2 = 0x1.62e42fefa39efp-1;
   constexpr double A0 = -0x1.00ea348b88334p-2, A1 = 0x1.5575b0be00b6ap-2,
                    A2 = -0x1.ffffef20a4123p-2;
@@ -99,8 +101,9 @@ __device__ __forceinline__ float glibc_logf(float x) {
   const int k = static_cast<int32_t>(tmp) >> 23;
   const uint32_t iz = ix - (tmp & (0x1ffu << 23));
   const double z = static_cast<double>(__uint_as_float(iz));
-  const double r = __dadd_rn(__dmul_rn(z, invc[i]), -1.0);
-  const double y0 = __dadd_rn(logc[i], __dmul_rn(static_cast<double>(k), kLn2));
+  const double2 t = __ldg(&kLogfTab[i]);
+  const double r = __dadd_rn(__dmul_rn(z, t.x), -1.0);
+  const double y0 = __dadd_rn(t.y, __dmul_rn(static_cast<double>(k), kLn2));
   const double r2 = __dmul_rn(r, r);
   double y = __dadd_rn(__dmul_rn(A1, r), A2);
   y = __dadd_rn(__dmul_rn(A0, r2), y);

@@ -41,6 +41,8 @@ struct EpsStream {
     counts.alloc(blocks);
     ticket.alloc(1);
     last_j.alloc(1);
+    const int64_t none = -1;
+    PQLG_CUDA(cudaMemcpy(last_j.p, &none, 8, cudaMemcpyHostToDevice));
     mt.seed(key);
     host.resize(static_cast<size_t>(n));
   }

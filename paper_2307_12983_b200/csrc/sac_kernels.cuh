@@ -37,7 +37,7 @@ struct EpsState {
 };
 
 constexpr int kEpsThreads = 256;
-constexpr int kEpsPer = 4;  // candidates per thread
+constexpr int kEpsPer = 1;  // candidates per thread (many blocks: the draws are latency-bound)
 constexpr int kEpsChunk = kEpsThreads * kEpsPer;
 
 struct EpsArgs {
@@ -47,7 +47,7 @@ struct EpsArgs {
   int64_t need;          // accepted pairs needed = ceil(n / 2)
   unsigned int* counts;  // [gridDim.x] accepted candidates per block
   unsigned int* ticket;
-  int64_t* last_j;       // candidate index of pair need-1 (written by its block)
+  int64_t* last_j;       // candidate index of pair need-1 (written by its block; -1 between calls)
 };
 
 // Candidate pair j of the stream at counter c: (x, y, r2) from draws c+2j, c+2j+1.
@@ -141,8 +141,10 @@ static __global__ void __launch_bounds__(kEpsThreads) eps_emit_kernel(EpsArgs a)
     if (!ok[u]) continue;
     if (p < a.need) {
       eps_write(a, p, x[u], y[u], r2[u]);
-      if (p == a.need - 1)
+      if (p == a.need - 1) {
         *a.last_j = static_cast<int64_t>(blockIdx.x) * kEpsChunk + threadIdx.x * kEpsPer + u;
+        __threadfence();  // visible to the last block (ticket below)
+      }
     }
     ++p;
   }
@@ -157,14 +159,11 @@ static __global__ void __launch_bounds__(kEpsThreads) eps_emit_kernel(EpsArgs a)
   if (!last || threadIdx.x != 0) return;
   __threadfence();
   *a.ticket = 0;
-  int64_t total = 0;
-  for (unsigned i = 0; i < gridDim.x; ++i) total += __ldcg(a.counts + i);
-  int64_t lj;
-  if (total >= a.need) {
-    lj = __ldcg(a.last_j);
-  } else {
+  int64_t lj = __ldcg(a.last_j);
+  if (lj < 0) {  // shortfall: every candidate was taken; continue sequentially
+    int64_t q = 0;
+    for (unsigned i = 0; i < gridDim.x; ++i) q += __ldcg(a.counts + i);
     int64_t j = static_cast<int64_t>(gridDim.x) * kEpsChunk;
-    int64_t q = total;
     for (;; ++j) {
       float xx, yy, rr;
       if (!eps_candidate(key, c, j, xx, yy, rr)) continue;
@@ -173,6 +172,7 @@ static __global__ void __launch_bounds__(kEpsThreads) eps_emit_kernel(EpsArgs a)
     }
     lj = j;
   }
+  *a.last_j = -1;
   a.st->ctr = c + 2 * static_cast<uint64_t>(lj + 1);
 }
 

@@ -58,8 +58,9 @@ def graph_time(fn, h, n=50):
 
 what = sys.argv[1:] or ["critic", "policy", "actor", "c51"]
 for w in what:
-    if w in ("critic", "c51"):
-        extra = dict(algo=_lib.ALGO_C51, n_atoms=51) if w == "c51" else {}
+    if w in ("critic", "c51", "sac"):
+        extra = {"c51": dict(algo=_lib.ALGO_C51, n_atoms=51),
+                 "sac": dict(algo=_lib.ALGO_SAC)}.get(w, {})
         cfg = _lib.default_config(batch_size=B, buffer_capacity=1_000_000, hidden=H,
                                   hidden_layers=nh, n_envs=N, **extra)
         dims = _lib.TaskDims(D, A, -1.0, 1.0)
@@ -74,9 +75,10 @@ for w in what:
         print(f"{w}: graph-replayed update {graph_time('pqlg_vlearner_update_n', h):.1f} us")
         prof(lambda: _lib.call("pqlg_vlearner_update", h, None))
         _lib.call("pqlg_vlearner_destroy", h)
-    elif w == "policy":
+    elif w in ("policy", "sac_policy"):
+        extra = dict(algo=_lib.ALGO_SAC) if w == "sac_policy" else {}
         cfg = _lib.default_config(batch_size=B, buffer_capacity=1_000_000, hidden=H,
-                                  hidden_layers=nh, n_envs=N)
+                                  hidden_layers=nh, n_envs=N, **extra)
         dims = _lib.TaskDims(D, A, -1.0, 1.0)
         h = C.c_void_p()
         _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 1, sp, C.byref(h))
@@ -85,9 +87,10 @@ for w in what:
         print(f"policy: graph-replayed update {graph_time('pqlg_plearner_update_n', h):.1f} us")
         prof(lambda: _lib.call("pqlg_plearner_update", h, None))
         _lib.call("pqlg_plearner_destroy", h)
-    elif w == "actor":
+    elif w in ("actor", "sac_actor"):
+        extra = dict(algo=_lib.ALGO_SAC) if w == "sac_actor" else {}
         cfg = _lib.default_config(batch_size=B, buffer_capacity=1_000_000, hidden=H,
-                                  hidden_layers=nh, n_envs=N)
+                                  hidden_layers=nh, n_envs=N, **extra)
         dims = _lib.TaskDims(D, A, -1.0, 1.0)
         act, vl, pl = C.c_void_p(), C.c_void_p(), C.c_void_p()
         _lib.call("pqlg_actor_create", C.byref(cfg), C.byref(dims), sp, C.byref(act))
