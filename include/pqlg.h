@@ -425,6 +425,57 @@ PQLG_API int pqlg_pipeline_run(pqlg_pipeline h, int64_t actor_steps, double max_
                                pqlg_run_report* out);
 PQLG_API int pqlg_pipeline_destroy(pqlg_pipeline h);
 
+/* ------------------------------------------------------------ metrics CSV
+ * MetricsRow / MetricsWriter (metrics.hpp:9-32, metrics.cpp:8-29):
+ * header "wall_clock_s,env_steps,c_a,c_v,c_p,eval_return_mean,
+ * eval_return_stderr,critic_loss_ema,actor_loss_ema", then one flushed line
+ * per row formatted "%.3f,%lld,%lld,%lld,%lld,%.6g,%.6g,%.6g,%.6g" --
+ * byte-identical to the reference writer.  Host only (no GPU work). */
+typedef struct {
+  double wall_clock_s;
+  int64_t env_steps, c_a, c_v, c_p;
+  double eval_return_mean, eval_return_stderr;
+  double critic_loss_ema, actor_loss_ema;
+} pqlg_metrics_row;
+typedef struct pqlg_metrics_s* pqlg_metrics;
+PQLG_API const char* pqlg_metrics_header(void);
+/* Truncates `path` and writes the header; PQLG_EINVAL if it cannot be opened. */
+PQLG_API int pqlg_metrics_open(const char* path, pqlg_metrics* out);
+PQLG_API int pqlg_metrics_append(pqlg_metrics h, const pqlg_metrics_row* row);
+PQLG_API int pqlg_metrics_close(pqlg_metrics h);
+
+/* The evaluator + metrics writer of run_parallel / run_synchronous
+ * (SPEC.md:461, :494): every interval_s of wall clock (parallel) or every
+ * every_actor_steps rollout steps (synchronous) the actor's current policy
+ * and normalizer are evaluated (evaluate_policy, eval_episodes episodes,
+ * eval_seed) and a row is appended; a last row is written at the end of the
+ * run.  Loss EMAs: the first sample seeds them, then ema = f*ema + (1-f)*x
+ * with f = `ema`, sampled at every snapshot publication (K_pub updates). */
+typedef struct {
+  const char* path;
+  double interval_s;
+  int64_t every_actor_steps;
+  int eval_episodes;
+  uint64_t eval_seed;
+  double ema;
+} pqlg_metrics_config;
+PQLG_API void pqlg_metrics_config_default(pqlg_metrics_config* m);
+/* Before pqlg_pipeline_run; path == NULL disables. */
+PQLG_API int pqlg_pipeline_set_metrics(pqlg_pipeline h, const pqlg_metrics_config* m);
+
+/* run_synchronous (algos sync_ddpg_n / sync_sac_n): the
+ * same three cores on one stream in one host thread, in Algorithm order:
+ * roll out H steps (ingest into both learners), then H / beta_av critic
+ * updates, a policy update after every critic update that keeps
+ * c_p <= beta_pv * c_v, critic snapshot -> P-learner and policy snapshot ->
+ * actor + V-learner every publish_every updates.  Bit-deterministic for a
+ * fixed seed (the metrics CSV differs only in its wall_clock_s column).
+ * metrics nullable. */
+PQLG_API int pqlg_run_synchronous(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                                  const pqlg_ratio_config* ratio, uint64_t init_rng_seed,
+                                  int64_t actor_steps, const pqlg_metrics_config* metrics,
+                                  pqlg_run_report* out);
+
 /* evaluate_policy (learners.cpp:280-325) on the synthetic task: a fresh env
  * of `episodes` rows seeded with eval_seed, each row one full episode of the
  * deterministic policy (flat host params, cfg->hidden / hidden_layers /

@@ -388,6 +388,23 @@ def gen_sac(R, out):
     out.update(sa_obs0=o0, sa_obs1=o1, sa_act=acts)
 
 
+METRICS_ROWS = [
+    [0.0, 0, 0, 0, 0, 0.0, 0.0, 0.0, 0.0],
+    [1.23456, 262144, 64, 256, 128, -1234.5678912, 12.3456789, 0.000123456789, -7.25],
+    [59.9995, 1 << 40, 1 << 26, (1 << 29) + 3, 1 << 28, 1e-300, 3.5e12, 123456789.0, -0.0],
+    [3600.0004, 16384 * 1000, 1000, 8000, 4000, -200.0, 0.5, 1.0 / 3.0, 2.0 / 3.0],
+    [0.0005, 7, 7, 1, 0, float("inf"), float("nan"), -float("inf"), 1e-7],
+]
+
+
+def gen_metrics(R, out):
+    """rt::MetricsWriter output for METRICS_ROWS (tests/golden/metrics_ref.csv)."""
+    rows = np.ascontiguousarray(np.array(METRICS_ROWS, np.float64))
+    path = str(GOLDEN / "metrics_ref.csv")
+    assert R.ref_metrics_write(path.encode(), ptr(rows), rows.shape[0]) == 0
+    out.update(mt_dummy=np.zeros(1))
+
+
 def ckpt_content(seed=9):
     """A small checkpoint payload: three nets of the learners' shapes + stats."""
     rng = np.random.default_rng(seed)
@@ -423,12 +440,12 @@ def main():
                      ("elementwise", gen_elementwise), ("norm", gen_norm), ("noise", gen_noise),
                      ("mlp", gen_mlp), ("agents", gen_agents), ("vupdate", gen_vupdate),
                      ("c51update", gen_c51update), ("sac", gen_sac),
-                     ("checkpoint", gen_checkpoint)]:
+                     ("checkpoint", gen_checkpoint), ("metrics", gen_metrics)]:
         if len(sys.argv) > 1 and name not in sys.argv[1:]:
             continue
         out: dict = {}
         fn(R, out)
-        if name == "checkpoint":  # raw bytes only (ckpt_ref.bin)
+        if name in ("checkpoint", "metrics"):  # raw bytes only (ckpt_ref.bin, metrics_ref.csv)
             continue
         np.savez_compressed(GOLDEN / f"{name}.npz", **out)
         print(name, sum(v.nbytes for v in out.values()), "bytes")

@@ -24,6 +24,7 @@
 #include "pql/replay/replay_buffer.hpp"
 #include "pql/rng.hpp"
 #include "pql/runtime/learners.hpp"
+#include "pql/runtime/metrics.hpp"
 #include "pql/vecenv/vecenv.hpp"
 
 using namespace pql;
@@ -861,4 +862,30 @@ REF_API int ref_checkpoint_load(const char* path, float* flat_out, size_t* n_par
   } catch (...) {
     return -1;
   }
+}
+
+// ------------------------------------------------------------ metrics CSV
+// rt::MetricsWriter (metrics.cpp:8-29): rows given as 9 doubles each in the
+// MetricsRow field order (the integer fields rounded).
+REF_API int ref_metrics_write(const char* path, const double* rows, size_t n) {
+  try {
+    rt::MetricsWriter w(path);
+    for (size_t i = 0; i < n; ++i) {
+      const double* r = rows + 9 * i;
+      rt::MetricsRow m;
+      m.wall_clock_s = r[0];
+      m.env_steps = static_cast<std::int64_t>(r[1]);
+      m.c_a = static_cast<std::int64_t>(r[2]);
+      m.c_v = static_cast<std::int64_t>(r[3]);
+      m.c_p = static_cast<std::int64_t>(r[4]);
+      m.eval_return_mean = r[5];
+      m.eval_return_stderr = r[6];
+      m.critic_loss_ema = r[7];
+      m.actor_loss_ema = r[8];
+      w.append(m);
+    }
+  } catch (...) {
+    return -1;
+  }
+  return 0;
 }

@@ -77,6 +77,20 @@ class RunReport(C.Structure):
                 ("last_critic_loss", f32), ("last_actor_loss", f32)]
 
 
+class MetricsRow(C.Structure):
+    """pqlg_metrics_row (MetricsRow, metrics.hpp:9-15)."""
+    _fields_ = [("wall_clock_s", C.c_double), ("env_steps", i64), ("c_a", i64), ("c_v", i64),
+                ("c_p", i64), ("eval_return_mean", C.c_double),
+                ("eval_return_stderr", C.c_double), ("critic_loss_ema", C.c_double),
+                ("actor_loss_ema", C.c_double)]
+
+
+class MetricsConfig(C.Structure):
+    """pqlg_metrics_config: the evaluator + metrics writer of a run."""
+    _fields_ = [("path", C.c_char_p), ("interval_s", C.c_double), ("every_actor_steps", i64),
+                ("eval_episodes", i32), ("eval_seed", u64), ("ema", C.c_double)]
+
+
 PROC_ACTOR, PROC_VLEARNER, PROC_PLEARNER = 0, 1, 2
 
 # name -> (restype, argtypes)
@@ -179,6 +193,14 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_pipeline_create": (i32, [P(Config), P(TaskDims), P(RatioConfig), u64, P(vp)]),
     "pqlg_pipeline_run": (i32, [vp, i64, C.c_double, P(RunReport)]),
     "pqlg_pipeline_destroy": (i32, [vp]),
+    "pqlg_pipeline_set_metrics": (i32, [vp, P(MetricsConfig)]),
+    "pqlg_run_synchronous": (i32, [P(Config), P(TaskDims), P(RatioConfig), u64, i64,
+                                   P(MetricsConfig), P(RunReport)]),
+    "pqlg_metrics_header": (C.c_char_p, []),
+    "pqlg_metrics_open": (i32, [C.c_char_p, P(vp)]),
+    "pqlg_metrics_append": (i32, [vp, P(MetricsRow)]),
+    "pqlg_metrics_close": (i32, [vp]),
+    "pqlg_metrics_config_default": (None, [P(MetricsConfig)]),
     "pqlg_env_create": (i32, [i32, i32, i32, u64, i32, i32, f32, f32, vp, P(vp)]),
     "pqlg_env_destroy": (i32, [vp]),
     "pqlg_env_reset_all": (i32, [vp, vp, i64]),
@@ -277,6 +299,15 @@ def comm_from_torch_dist(rank: int, world: int) -> C.c_void_p:
     comm = C.c_void_p()
     call("pqlg_comm_init", rank, world, ident, C.byref(comm))
     return comm
+
+
+def metrics_config(path: str, **overrides) -> MetricsConfig:
+    m = MetricsConfig()
+    lib().pqlg_metrics_config_default(C.byref(m))
+    m.path = path.encode()
+    for k, v in overrides.items():
+        setattr(m, k, v)
+    return m
 
 
 def ratio_config(**overrides) -> RatioConfig:

@@ -80,4 +80,9 @@ class Actor {
   int kps_ = 0;
 };
 
+// evaluate_policy (learners.cpp:280-325) on the synthetic task (actor.cu).
+void evaluate_policy(const pqlg_config& cfg, const pqlg_task_dims& dims, const float* policy,
+                     int64_t count, const double* mean, const double* m2, int episodes,
+                     uint64_t eval_seed, double* returns, double* mean_out, double* stderr_out);
+
 }  // namespace pqlg

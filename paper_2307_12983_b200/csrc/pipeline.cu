@@ -30,6 +30,7 @@
 
 #include "actor.h"
 #include "learner.h"
+#include "metrics.h"
 
 namespace pqlg {
 namespace {
@@ -240,6 +241,20 @@ class Pipeline {
     }
   }
 
+  // the evaluator + metrics writer
+  void set_metrics(const pqlg_metrics_config& m) {
+    require(!ran_, "pipeline: set_metrics before run()");
+    if (!m.path) {
+      writer_.reset();
+      return;
+    }
+    require(m.interval_s > 0.0 && m.eval_episodes >= 1 && m.ema >= 0.0 && m.ema < 1.0,
+            "pipeline: metrics needs interval_s > 0, eval_episodes >= 1, 0 <= ema < 1");
+    mcfg_ = m;
+    closs_ema_.f = aloss_ema_.f = m.ema;
+    writer_ = std::make_unique<MetricsWriter>(m.path);
+  }
+
   pqlg_run_report run(int64_t actor_steps, double max_seconds) {
     require(!ran_, "pipeline: run() may be called once per pipeline");
     ran_ = true;
@@ -249,6 +264,9 @@ class Pipeline {
     std::thread ta([&] { guard_thread([&] { actor_loop(); }); });
     std::thread tv([&] { guard_thread([&] { vlearner_loop(); }); });
     std::thread tp([&] { guard_thread([&] { plearner_loop(); }); });
+    t0_ = t0;
+    std::thread te;
+    if (writer_) te = std::thread([&] { guard_thread([&] { evaluator_loop(); }); });
     while (true) {
       std::this_thread::sleep_for(std::chrono::microseconds(200));
       const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -258,11 +276,21 @@ class Pipeline {
     // while the learners keep draining), then the learners drain what is
     // queued and stop -- every batch sent is consumed exactly once
     stop_actor_ = true;
+    {
+      std::lock_guard<std::mutex> lk(ev_mu_);
+      ev_stop_ = true;
+      ev_cv_.notify_all();
+    }
     ta.join();
+    if (te.joinable()) te.join();
     stop_all();
     tv.join();
     tp.join();
     for (auto s : {sa_, sv_, sp_}) PQLG_CUDA(cudaStreamSynchronize(s));
+    if (writer_ && !failed_.load()) {  // final metrics row (run_parallel returns final metrics)
+      snapshot_for_eval();
+      append_row();
+    }
     pqlg_run_report r{};
     r.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     r.c_a = gate_.count(kActor);
@@ -360,6 +388,7 @@ class Pipeline {
       bool go = false;
       while (!go) {
         if (gate_.stopped() || stop_actor_.load()) return;
+        serve_eval();
         go = gate_.wait_for(kActor, std::chrono::microseconds(2000));
       }
       const int k = take_slot();
@@ -458,6 +487,10 @@ class Pipeline {
       gate_.record(kVLearner, 1);
       if (++updates % rc_.publish_every == 0) {
         last_closs_ = v_->last_loss();  // throws on a non-finite update (SPEC: abort)
+        {
+          std::lock_guard<std::mutex> lk(ema_mu_);
+          closs_ema_.add(last_closs_);
+        }
         crit_pool_.publish(sv_, [&](float* dst, cudaStream_t stm) {
           PQLG_CUDA(cudaMemcpyAsync(dst, v_->critic_dev(0), Pq * 4, cudaMemcpyDeviceToDevice, stm));
           PQLG_CUDA(cudaMemcpyAsync(dst + Pq, v_->critic_dev(1), Pq * 4, cudaMemcpyDeviceToDevice,
@@ -503,12 +536,76 @@ class Pipeline {
       gate_.record(kPLearner, 1);
       if (++updates % rc_.publish_every == 0) {
         last_aloss_ = p_->last_loss();
+        {
+          std::lock_guard<std::mutex> lk(ema_mu_);
+          aloss_ema_.add(last_aloss_);
+        }
         pol_pool_.publish(sp_, [&](float* dst, cudaStream_t stm) {
           PQLG_CUDA(cudaMemcpyAsync(dst, p_->policy_dev(), Pp * 4, cudaMemcpyDeviceToDevice, stm));
         });
       }
     }
     drain(std::chrono::microseconds(0));
+  }
+
+  // The actor thread copies its policy + normalizer to the host on request,
+  // between rollouts (stream order makes the snapshot consistent).
+  void serve_eval() {
+    if (!ev_req_.load()) return;
+    snapshot_for_eval();
+    std::lock_guard<std::mutex> lk(ev_mu_);
+    ev_req_ = false;
+    ev_ready_ = true;
+    ev_cv_.notify_all();
+  }
+  void snapshot_for_eval() {
+    ev_pol_.resize(static_cast<size_t>(actor_->param_count()));
+    ev_mean_.resize(D_);
+    ev_m2_.resize(D_);
+    PQLG_CUDA(cudaMemcpyAsync(ev_pol_.data(), actor_->policy_dev(), ev_pol_.size() * 4,
+                              cudaMemcpyDeviceToHost, sa_));
+    PQLG_CUDA(cudaMemcpyAsync(&ev_count_, actor_->count_dev(), 8, cudaMemcpyDeviceToHost, sa_));
+    PQLG_CUDA(cudaMemcpyAsync(ev_mean_.data(), actor_->mean_dev(), D_ * 8, cudaMemcpyDeviceToHost, sa_));
+    PQLG_CUDA(cudaMemcpyAsync(ev_m2_.data(), actor_->m2_dev(), D_ * 8, cudaMemcpyDeviceToHost, sa_));
+    PQLG_CUDA(cudaStreamSynchronize(sa_));
+  }
+  void append_row() {
+    double mu = 0.0, se = 0.0;
+    evaluate_policy(cfg_, dims_, ev_pol_.data(), ev_count_, ev_mean_.data(), ev_m2_.data(),
+                    mcfg_.eval_episodes, mcfg_.eval_seed, nullptr, &mu, &se);
+    pqlg_metrics_row r{};
+    r.wall_clock_s =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count();
+    r.c_a = gate_.count(kActor);
+    r.c_v = gate_.count(kVLearner);
+    r.c_p = gate_.count(kPLearner);
+    r.env_steps = r.c_a * N_;
+    r.eval_return_mean = mu;
+    r.eval_return_stderr = se;
+    {
+      std::lock_guard<std::mutex> lk(ema_mu_);
+      r.critic_loss_ema = closs_ema_.v;
+      r.actor_loss_ema = aloss_ema_.v;
+    }
+    writer_->append(r);
+    ++rows_;
+  }
+  // every interval_s: ask the actor for a snapshot, evaluate it, append a row
+  void evaluator_loop() {
+    auto next = t0_ + std::chrono::duration_cast<std::chrono::steady_clock::duration>(
+                          std::chrono::duration<double>(mcfg_.interval_s));
+    while (true) {
+      std::unique_lock<std::mutex> lk(ev_mu_);
+      if (ev_cv_.wait_until(lk, next, [&] { return ev_stop_; })) return;
+      ev_req_ = true;
+      ev_ready_ = false;
+      ev_cv_.wait(lk, [&] { return ev_ready_ || ev_stop_; });
+      if (!ev_ready_) return;
+      lk.unlock();
+      append_row();
+      next += std::chrono::duration_cast<std::chrono::steady_clock::duration>(
+          std::chrono::duration<double>(mcfg_.interval_s));
+    }
   }
 
   pqlg_config cfg_;
@@ -534,10 +631,144 @@ class Pipeline {
   float last_closs_ = 0.0f, last_aloss_ = 0.0f;
   bool ran_ = false;
   std::atomic<bool> failed_{false}, stop_actor_{false};
+  // metrics / evaluator
+  pqlg_metrics_config mcfg_{};
+  std::unique_ptr<MetricsWriter> writer_;
+  std::mutex ema_mu_;
+  Ema closs_ema_, aloss_ema_;
+  std::chrono::steady_clock::time_point t0_;
+  std::mutex ev_mu_;
+  std::condition_variable ev_cv_;
+  std::atomic<bool> ev_req_{false};
+  bool ev_ready_ = false, ev_stop_ = false;
+  std::vector<float> ev_pol_;
+  int64_t ev_count_ = 0;
+  std::vector<double> ev_mean_, ev_m2_;
+  int64_t rows_ = 0;
   std::mutex err_mu_;
   std::string error_;
   int err_status_ = PQLG_OK;
 };
+
+// run_synchronous: the same cores, one stream, one host
+// thread, Algorithm order.  Deterministic: every update replays the same
+// graphs on the same stream with Philox streams, so two runs with one seed
+// produce identical parameters, losses and metrics (wall clock aside).
+pqlg_run_report run_synchronous(const pqlg_config& cfg, const pqlg_task_dims& dims,
+                                const pqlg_ratio_config& rc, uint64_t init_seed,
+                                int64_t actor_steps, const pqlg_metrics_config* mc) {
+  require(rc.horizon >= 1 && rc.publish_every >= 1, "run_synchronous: horizon, publish_every >= 1");
+  require(rc.beta_av > 0 && rc.beta_pv > 0, "run_synchronous: ratios must be positive");
+  std::unique_ptr<MetricsWriter> writer;
+  Ema closs, aloss;
+  if (mc && mc->path) {
+    require(mc->every_actor_steps >= 1 && mc->eval_episodes >= 1 && mc->ema >= 0.0 && mc->ema < 1.0,
+            "run_synchronous: metrics needs every_actor_steps >= 1, eval_episodes >= 1, 0 <= ema < 1");
+    closs.f = aloss.f = mc->ema;
+    writer = std::make_unique<MetricsWriter>(mc->path);
+  }
+  cudaStream_t st;
+  PQLG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+  } guard{st};
+  Actor actor(cfg, dims, st);
+  VLearner v(cfg, dims, init_seed, st);
+  PLearner p(cfg, dims, init_seed, st);
+  const int N = cfg.n_envs, D = dims.obs_dim, H = rc.horizon;
+  const int64_t Pq = v.critic_params(), Pp = p.snapshot_len();
+  (void)Pq;
+  const auto t0 = std::chrono::steady_clock::now();
+  int64_t ca = 0, cv = 0, cp = 0, pol_ver = 0, crit_ver = 0, next_eval = 0;
+  float last_c = 0.0f, last_a = 0.0f;
+  std::vector<float> pol(static_cast<size_t>(actor.param_count()));
+  std::vector<double> mean(D), m2(D);
+  auto row = [&] {
+    int64_t count = 0;
+    PQLG_CUDA(cudaMemcpyAsync(pol.data(), actor.policy_dev(), pol.size() * 4,
+                              cudaMemcpyDeviceToHost, st));
+    PQLG_CUDA(cudaMemcpyAsync(&count, actor.count_dev(), 8, cudaMemcpyDeviceToHost, st));
+    PQLG_CUDA(cudaMemcpyAsync(mean.data(), actor.mean_dev(), D * 8, cudaMemcpyDeviceToHost, st));
+    PQLG_CUDA(cudaMemcpyAsync(m2.data(), actor.m2_dev(), D * 8, cudaMemcpyDeviceToHost, st));
+    PQLG_CUDA(cudaStreamSynchronize(st));
+    double mu = 0.0, se = 0.0;
+    evaluate_policy(cfg, dims, pol.data(), count, mean.data(), m2.data(), mc->eval_episodes,
+                    mc->eval_seed, nullptr, &mu, &se);
+    pqlg_metrics_row r{};
+    r.wall_clock_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    r.env_steps = ca * N;
+    r.c_a = ca;
+    r.c_v = cv;
+    r.c_p = cp;
+    r.eval_return_mean = mu;
+    r.eval_return_stderr = se;
+    r.critic_loss_ema = closs.v;
+    r.actor_loss_ema = aloss.v;
+    writer->append(r);
+  };
+  if (writer) next_eval = mc->every_actor_steps;
+  const int64_t n_v = static_cast<int64_t>(std::llround(H / rc.beta_av));
+  while (ca < actor_steps) {
+    // Alg. 1: roll out H steps, send the transitions / states to the learners
+    for (int h = 0; h < H; ++h) {
+      pqlg_step_slice sl{};
+      actor.rollout_step(&sl);
+      v.ingest(replay::Slice{sl.obs, sl.act, sl.boot_obs, sl.rew, sl.term, sl.trunc, sl.ld_obs,
+                             sl.ld_act});
+      p.ingest(sl.obs, sl.ld_obs, static_cast<uint64_t>(N));
+    }
+    ca += H;
+    // the actor's normalizer travels with the data
+    v.adopt_norm_device(actor.count_dev(), actor.mean_dev(), actor.m2_dev());
+    p.adopt_norm_device(actor.count_dev(), actor.mean_dev(), actor.m2_dev());
+    if (ca >= rc.warm_up && v.ready(ca) && p.ready(ca)) {
+      // Alg. 3 / 2: H / beta_av critic updates, policy updates interleaved so
+      // that c_p stays at beta_pv * c_v
+      for (int64_t k = 0; k < n_v; ++k) {
+        v.update_n(1);
+        ++cv;
+        if (cv % rc.publish_every == 0) {  // critic snapshot -> P-learner
+          last_c = v.last_loss();
+          closs.add(last_c);
+          p.adopt_critics_device(v.critic_dev(0), v.critic_dev(1), ++crit_ver);
+        }
+        while (static_cast<double>(cp) + 1.0 <= rc.beta_pv * static_cast<double>(cv)) {
+          p.update_n(1);
+          ++cp;
+          if (cp % rc.publish_every == 0) {  // policy snapshot -> actor -> V-learner
+            last_a = p.last_loss();
+            aloss.add(last_a);
+            ++pol_ver;
+            actor.adopt_policy(p.policy_dev(), pol_ver, true);
+            v.adopt_policy_device(p.policy_dev(), pol_ver);
+          }
+        }
+      }
+    }
+    if (writer && ca >= next_eval) {
+      row();
+      next_eval += mc->every_actor_steps;
+    }
+  }
+  PQLG_CUDA(cudaStreamSynchronize(st));
+  if (writer) row();
+  pqlg_run_report r{};
+  r.ok = 1;
+  r.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  r.c_a = ca;
+  r.c_v = cv;
+  r.c_p = cp;
+  r.env_steps = ca * N;
+  r.ratio_av = cv ? static_cast<double>(ca) / cv : 0.0;
+  r.ratio_pv = cv ? static_cast<double>(cp) / cv : 0.0;
+  r.policy_version = pol_ver;
+  r.critic_version = crit_ver;
+  r.last_critic_loss = cv ? v.last_loss() : 0.0f;
+  r.last_actor_loss = cp ? p.last_loss() : 0.0f;
+  (void)Pp;
+  return r;
+}
 
 }  // namespace pqlg
 
@@ -590,6 +821,22 @@ int pqlg_pipeline_run(pqlg_pipeline h, int64_t actor_steps, double max_seconds,
 
 int pqlg_pipeline_destroy(pqlg_pipeline h) {
   return guarded([&] { delete h; });
+}
+
+int pqlg_pipeline_set_metrics(pqlg_pipeline h, const pqlg_metrics_config* m) {
+  return guarded([&] {
+    require(h && m, "pipeline_set_metrics: null argument");
+    h->p->set_metrics(*m);
+  });
+}
+
+int pqlg_run_synchronous(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                         const pqlg_ratio_config* rc, uint64_t init_rng_seed, int64_t actor_steps,
+                         const pqlg_metrics_config* metrics, pqlg_run_report* out) {
+  return guarded([&] {
+    require(cfg && dims && rc && out, "run_synchronous: null argument");
+    *out = run_synchronous(*cfg, *dims, *rc, init_rng_seed, actor_steps, metrics);
+  });
 }
 
 }  // extern "C"

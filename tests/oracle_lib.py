@@ -143,6 +143,7 @@ _REF_SIGS = {
     "ref_vcore_adopt_policy": (None, [vp, vp, i64]),
     "ref_vcore_update": (i32, [vp, vp]),
     "ref_vcore_params": (None, [vp, i32, vp]),
+    "ref_metrics_write": (i32, [C.c_char_p, vp, sz]),
     "ref_checkpoint_save": (i32, [C.c_char_p, i32, vp, vp, vp, vp, i64, vp, vp, sz]),
     "ref_checkpoint_load": (i32, [C.c_char_p, vp, C.POINTER(sz), C.POINTER(i64), vp, vp, C.POINTER(sz)]),
 }

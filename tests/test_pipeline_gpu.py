@@ -59,3 +59,80 @@ def test_pipeline_free_running_actor_only_pacing_off():
     r = run_pipeline(cfg, dims, rc, 200)
     assert r.ok == 1 and r.c_a >= 200
     assert r.batches_consumed_v == r.batches_sent and r.seq_gaps == 0
+
+
+def read_csv(path):
+    lines = path.read_text().splitlines()
+    assert lines[0] == _lib.lib().pqlg_metrics_header().decode()
+    rows = [ln.split(",") for ln in lines[1:]]
+    return [[float(x) for x in r] for r in rows]
+
+
+def test_pipeline_metrics_csv(tmp_path):
+    """a well-formed metrics CSV with a strictly increasing
+    wall clock; env_steps = c_a * N; counters monotone; the last row is the
+    run's final state."""
+    N = 256
+    cfg = _lib.default_config(n_envs=N, batch_size=512, buffer_capacity=100_000, hidden=64,
+                              hidden_layers=2, seed=1, max_episode_len=50)
+    dims = _lib.TaskDims(17, 6, -1.0, 1.0)
+    rc = _lib.ratio_config()
+    path = tmp_path / "metrics.csv"
+    m = _lib.metrics_config(str(path), interval_s=0.25, eval_episodes=16)
+    h = C.c_void_p()
+    _lib.call("pqlg_pipeline_create", C.byref(cfg), C.byref(dims), C.byref(rc), 3, C.byref(h))
+    _lib.call("pqlg_pipeline_set_metrics", h, C.byref(m))
+    rep = _lib.RunReport()
+    try:
+        _lib.call("pqlg_pipeline_run", h, 100_000, 2.0, C.byref(rep))
+    finally:
+        _lib.call("pqlg_pipeline_destroy", h)
+    rows = read_csv(path)
+    print(f"\n{len(rows)} rows; last {rows[-1]}")
+    assert len(rows) >= 3
+    for a, b in zip(rows, rows[1:]):
+        assert b[0] > a[0]                                   # wall clock strictly increasing
+        assert all(b[k] >= a[k] for k in (1, 2, 3, 4))       # counters monotone
+    for r in rows:
+        assert r[1] == r[2] * N                               # env_steps = c_a * N
+        assert r[5] == r[5] and r[6] >= 0.0                   # finite eval, stderr >= 0
+    last = rows[-1]
+    assert (last[2], last[3], last[4]) == (rep.c_a, rep.c_v, rep.c_p)
+    assert last[7] != 0.0 and last[8] != 0.0                  # both loss EMAs sampled
+
+
+@pytest.mark.parametrize("algo", [_lib.ALGO_DDPG, _lib.ALGO_SAC])
+def test_run_synchronous_deterministic_and_paced(tmp_path, algo):
+    """one sequential loop in Algorithm order; fixed seed ->
+    identical metrics (all columns but the wall clock) and identical final
+    losses; update counts follow the ratios exactly."""
+    N = 128
+    cfg = _lib.default_config(algo=algo, n_envs=N, batch_size=256, buffer_capacity=50_000,
+                              hidden=64, hidden_layers=2, seed=5, max_episode_len=40)
+    dims = _lib.TaskDims(11, 4, -1.0, 1.0)
+    rc = _lib.ratio_config()
+    outs = []
+    for k in range(2):
+        path = tmp_path / f"sync{k}.csv"
+        m = _lib.metrics_config(str(path), every_actor_steps=40, eval_episodes=8)
+        rep = _lib.RunReport()
+        _lib.call("pqlg_run_synchronous", C.byref(cfg), C.byref(dims), C.byref(rc), 9, 200,
+                  C.byref(m), C.byref(rep))
+        outs.append((rep, read_csv(path)))
+    (r0, m0), (r1, m1) = outs
+    print(f"\nc_a={r0.c_a} c_v={r0.c_v} c_p={r0.c_p} losses {r0.last_critic_loss} "
+          f"{r0.last_actor_loss} rows {len(m0)}")
+    assert (r0.c_a, r0.c_v, r0.c_p) == (r1.c_a, r1.c_v, r1.c_p)
+    assert r0.last_critic_loss == r1.last_critic_loss
+    assert r0.last_actor_loss == r1.last_actor_loss
+    assert [r[1:] for r in m0] == [r[1:] for r in m1]
+    # pacing: every post-warm-up iteration runs H / beta_av critic updates
+    # and policy updates up to beta_pv * c_v
+    H = rc.horizon
+    iters = r0.c_a // H
+    assert r0.c_a == 200
+    warm = max(-(-rc.warm_up // H), -(-cfg.batch_size // N)) - 1
+    assert r0.c_v == (iters - warm) * round(H / rc.beta_av)
+    assert r0.c_p == int(rc.beta_pv * r0.c_v)
+    assert r0.policy_version == r0.c_p // rc.publish_every
+    assert r0.critic_version == r0.c_v // rc.publish_every
