@@ -537,20 +537,26 @@ def ref_lib():
     return ref()
 
 
-def reference_critic_rate(cfg_name, n_updates, batch_override=None):
+def reference_critic_rate(cfg_name, n_updates, batch_override=None, threads=None):
     """The reference's own CPU path (oracle/_ref, compiled from
     /root/reference): the CriticLearnerCore::update composition of
     learners.cpp:157-188 over the config's 3x512 nets (agents-level, since
-    RunConfig can only express 2 hidden layers), single-threaded as the
-    reference runs it.  Returns (updates/s, sample description)."""
+    RunConfig can only express 2 hidden layers).  One update is
+    single-threaded, as the reference runs it; to use every
+    host core, `threads` independent learners (replicas with their own
+    buffers) update concurrently -- ctypes releases the GIL inside each
+    call -- and the rate is their aggregate.  Returns (updates/s, sample,
+    threads)."""
+    import threading
     R = ref_lib()
     if R is None:
-        return None, "oracle/_ref/libpqlref.so not built"
+        return None, "oracle/_ref/libpqlref.so not built", 0
     sys.path.insert(0, str(ROOT / "tests"))
     from oracle_lib import param_count, ptr
     D, A, H, nh, B, N, cap = CONFIGS[cfg_name]
     if batch_override:
         B = batch_override
+    threads = threads or os.cpu_count() or 1
     rng = np.random.default_rng(0)
     qs = [D + A] + [H] * nh + [1]
     ps = [D] + [H] * nh + [A]
@@ -558,29 +564,48 @@ def reference_critic_rate(cfg_name, n_updates, batch_override=None):
     q2 = (rng.standard_normal(param_count(qs)) * 0.05).astype(np.float32)
     pol = (rng.standard_normal(param_count(ps)) * 0.05).astype(np.float32)
     n_rows = max(4 * B, 20000)
-    h = R.ref_vupdate_create(D, A, H, nh, B, n_rows, 0, ptr(q1), ptr(q2), ptr(pol), 0, 51,
-                             np.float32(-10), np.float32(10))
     obs = rng.standard_normal((n_rows, D)).astype(np.float32)
     act = rng.uniform(-1, 1, (n_rows, A)).astype(np.float32)
     boot = rng.standard_normal((n_rows, D)).astype(np.float32)
     ret = (rng.standard_normal(n_rows) * 0.1).astype(np.float32)
     eff = np.full(n_rows, 0.970299, np.float32)
-    R.ref_vupdate_insert(h, ptr(obs), ptr(act), ptr(boot), ptr(ret), ptr(eff), n_rows)
     mean = np.zeros(D); m2 = np.full(D, 1e6)
-    R.ref_vupdate_adopt_norm(h, 10 ** 6, ptr(mean), ptr(m2))
-    loss = np.zeros(1, np.float32)
-    R.ref_vupdate_step(h, ptr(loss))  # warm
+    handles = []
+    for k in range(threads):
+        h = R.ref_vupdate_create(D, A, H, nh, B, n_rows, k, ptr(q1), ptr(q2), ptr(pol), 0, 51,
+                                 np.float32(-10), np.float32(10))
+        R.ref_vupdate_insert(h, ptr(obs), ptr(act), ptr(boot), ptr(ret), ptr(eff), n_rows)
+        R.ref_vupdate_adopt_norm(h, 10 ** 6, ptr(mean), ptr(m2))
+        handles.append(h)
+    start = threading.Barrier(threads + 1)
+    done = threading.Barrier(threads + 1)
+
+    def work(h):
+        loss = np.zeros(1, np.float32)
+        R.ref_vupdate_step(h, ptr(loss))  # warm
+        start.wait()
+        for _ in range(n_updates):
+            R.ref_vupdate_step(h, ptr(loss))
+        done.wait()
+
+    ts = [threading.Thread(target=work, args=(h,)) for h in handles]
+    for t in ts:
+        t.start()
+    start.wait()
     t0 = time.perf_counter()
-    for _ in range(n_updates):
-        R.ref_vupdate_step(h, ptr(loss))
+    done.wait()
     dt = time.perf_counter() - t0
-    R.ref_vupdate_destroy(h)
-    rate = n_updates / dt
+    for t in ts:
+        t.join()
+    for h in handles:
+        R.ref_vupdate_destroy(h)
+    rate = threads * n_updates / dt
     if batch_override:
         rate *= batch_override / CONFIGS[cfg_name][4]  # per full-batch update
-    sample = (f"{n_updates} CriticLearnerCore-equivalent updates at B={B} "
-              f"({cfg_name} dims, 3x512), reference AVX2 build, 1 thread")
-    return rate, sample
+    sample = (f"{threads} concurrent CriticLearnerCore-equivalent learners x {n_updates} "
+              f"updates at B={B} ({cfg_name} dims, 3x512), reference AVX2 build, one host "
+              f"thread each (a single update is single-threaded in the reference)")
+    return rate, sample, threads
 
 
 def cpu_info():
@@ -619,16 +644,17 @@ def main():
         per = 1 if args.steps * 2.5 < 150 else None
         t0 = time.perf_counter()
         if per:
-            rate, sample = reference_critic_rate(args.config, args.steps + 0)
+            rate, sample, cores = reference_critic_rate(args.config, args.steps + 0)
         else:
-            rate, sample = reference_critic_rate(args.config, args.steps, batch_override=512)
+            rate, sample, cores = reference_critic_rate(args.config, args.steps,
+                                                        batch_override=512)
         if rate is None:
             print(json.dumps({"impl": "reference", "unavailable": sample}))
             return
         model, ncpu = cpu_info()
         out = dict(base)
         out.update(impl="reference", value=rate, ms_per_step=1e3 / rate,
-                   cpu_baseline={"value": rate, "unit": "updates/s", "cores": 1,
+                   cpu_baseline={"value": rate, "unit": "updates/s", "cores": cores,
                                  "kind": "reference", "sample": sample, "cpu": model,
                                  "host_cores": ncpu},
                    e2e={"value": rate, "unit": "updates/s", "h2d_bytes_per_step": 0,
@@ -656,9 +682,9 @@ def main():
                clocks=r["clocks"], gpu_launches=r["launches"],
                kernels_per_update=r["kpu"], last_loss=r["loss"])
     if world == 1 and not args.no_cpu_baseline:
-        rate, sample = reference_critic_rate(args.config, 3)
+        rate, sample, cores = reference_critic_rate(args.config, 2)
         model, ncpu = cpu_info()
-        out["cpu_baseline"] = ({"value": rate, "unit": "updates/s", "cores": 1,
+        out["cpu_baseline"] = ({"value": rate, "unit": "updates/s", "cores": cores,
                                 "kind": "reference", "sample": sample, "cpu": model,
                                 "host_cores": ncpu} if rate else None)
     print(json.dumps(out))
