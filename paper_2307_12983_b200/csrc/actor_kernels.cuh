@@ -88,7 +88,7 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
   float* sv = sM + static_cast<int64_t>(D) * Ap;        // [kEnvTile x ldv]  s'
   float* saa = sv + kEnvTile * ldv;                      // [kEnvTile]        sum a^2
   int* sdone = reinterpret_cast<int*>(saa + kEnvTile);   // [kEnvTile]
-  float* sa_all = saa + 2 * kEnvTile;                    // [kEnvWarps x 32]  clamped actions
+  float* sa_all = saa + 2 * kEnvTile;                    // [kEnvWarps x kPer x 32] clamped actions
   {
     // stage M (constant since env creation) before the PDL wait, under the
     // previous kernel's tail
@@ -120,7 +120,8 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
   __syncthreads();
   pdl::entry();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float* sa = sa_all + w * 32;
+  constexpr int kPerW = kEnvTile / kEnvWarps;
+  float* sa = sa_all + w * 32 * kPerW;
   const bool id = nn.out ? (*nn.identity != 0) : true;
   const int n_tiles = (e.N + kEnvTile - 1) / kEnvTile;
   const int A4 = (A + 3) >> 2;
@@ -141,73 +142,92 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
       }
       up[p] = (ok && lane < A) ? act[static_cast<int64_t>(i) * ld_act + lane] : 0.0f;
     }
+    // clamped actions of the warp's kPer envs -> smem (one row of 32 each)
 #pragma unroll
     for (int p = 0; p < kPer; ++p) {
-      const int j = w + p * kEnvWarps;
-      if (i0 + j >= e.N) break;
-      float sd[kNch];
-#pragma unroll
-      for (int c = 0; c < kNch; ++c) sd[c] = sdp[p][c];
+      const int i = i0 + w + p * kEnvWarps;
       float u = 0.0f;
       bool bad = false;
-      if (lane < A) {
+      if (lane < A && i < e.N) {
         u = up[p];
         bad = !isfinite(u);
         u = u < e.low ? e.low : (u > e.high ? e.high : u);
       }
-      sa[lane] = u;
+      sa[p * 32 + lane] = u;
       if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(o.status, 8u);
-      __syncwarp();
-      float acc[kNch];
+    }
+    __syncwarp();
+    // M a for all kPer envs at once: each M quad read from smem feeds kPer
+    // independent k-ascending chains per d (mul then add, no FMA)
+    float acc[kPer][kNch];
 #pragma unroll
-      for (int c = 0; c < kNch; ++c) acc[c] = 0.0f;
+    for (int p = 0; p < kPer; ++p)
+#pragma unroll
+      for (int c = 0; c < kNch; ++c) acc[p][c] = 0.0f;
 #pragma unroll 1
-      for (int k4 = 0; k4 < A4; ++k4) {
-        const float4 a4 = reinterpret_cast<const float4*>(sa)[k4];
-        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-        const int nu = A - 4 * k4;
-        if (nu >= 4) {  // full quad (always when A % 4 == 0)
+    for (int k4 = 0; k4 < A4; ++k4) {
+      float av[kPer][4];
 #pragma unroll
-          for (int c = 0; c < kNch; ++c) {
-            const int d = lane + 32 * c;
-            if (c + 1 < kNch || d < D) {
-              const float4 m4 = reinterpret_cast<const float4*>(sM + d * Ap)[k4];
-              acc[c] = __fadd_rn(acc[c], __fmul_rn(m4.x, av[0]));
-              acc[c] = __fadd_rn(acc[c], __fmul_rn(m4.y, av[1]));
-              acc[c] = __fadd_rn(acc[c], __fmul_rn(m4.z, av[2]));
-              acc[c] = __fadd_rn(acc[c], __fmul_rn(m4.w, av[3]));
-            }
-          }
-        } else {
+      for (int p = 0; p < kPer; ++p) {
+        const float4 a4 = reinterpret_cast<const float4*>(sa + p * 32)[k4];
+        av[p][0] = a4.x;
+        av[p][1] = a4.y;
+        av[p][2] = a4.z;
+        av[p][3] = a4.w;
+      }
+      const int nu = A - 4 * k4;
+      if (nu >= 4) {  // full quad (always when A % 4 == 0)
 #pragma unroll
-          for (int c = 0; c < kNch; ++c) {
-            const int d = lane + 32 * c;
-            if (d < D) {
-              const float4 m4 = reinterpret_cast<const float4*>(sM + d * Ap)[k4];
-              const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+        for (int c = 0; c < kNch; ++c) {
+          const int d = lane + 32 * c;
+          if (c + 1 < kNch || d < D) {
+            const float4 m4 = reinterpret_cast<const float4*>(sM + d * Ap)[k4];
 #pragma unroll
-              for (int q = 0; q < 4; ++q)
-                if (q < nu) acc[c] = __fadd_rn(acc[c], __fmul_rn(mm[q], av[q]));
+            for (int p = 0; p < kPer; ++p) {
+              acc[p][c] = __fadd_rn(acc[p][c], __fmul_rn(m4.x, av[p][0]));
+              acc[p][c] = __fadd_rn(acc[p][c], __fmul_rn(m4.y, av[p][1]));
+              acc[p][c] = __fadd_rn(acc[p][c], __fmul_rn(m4.z, av[p][2]));
+              acc[p][c] = __fadd_rn(acc[p][c], __fmul_rn(m4.w, av[p][3]));
             }
           }
         }
+      } else {
+#pragma unroll
+        for (int c = 0; c < kNch; ++c) {
+          const int d = lane + 32 * c;
+          if (d < D) {
+            const float4 m4 = reinterpret_cast<const float4*>(sM + d * Ap)[k4];
+            const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+            for (int p = 0; p < kPer; ++p)
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (q < nu) acc[p][c] = __fadd_rn(acc[p][c], __fmul_rn(mm[q], av[p][q]));
+          }
+        }
       }
+    }
+#pragma unroll
+    for (int p = 0; p < kPer; ++p) {
+      const int j = w + p * kEnvWarps;
+      if (i0 + j >= e.N) break;
 #pragma unroll
       for (int c = 0; c < kNch; ++c) {
         const int d = lane + 32 * c;
         if (d < D) {
-          float v = __fadd_rn(__fmul_rn(0.95f, sd[c]), __fmul_rn(0.05f, acc[c]));
+          float v = __fadd_rn(__fmul_rn(0.95f, sdp[p][c]), __fmul_rn(0.05f, acc[p][c]));
           v = v < -10.0f ? -10.0f : (v > 10.0f ? 10.0f : v);
           sv[j * ldv + d] = v;
         }
       }
       if (lane == 0) {
+        const float* ap = sa + p * 32;
         float aa = 0.0f;
-        for (int k = 0; k < A; ++k) aa = __fadd_rn(aa, __fmul_rn(sa[k], sa[k]));
+        for (int k = 0; k < A; ++k) aa = __fadd_rn(aa, __fmul_rn(ap[k], ap[k]));
         saa[j] = aa;
       }
-      __syncwarp();
     }
+    __syncwarp();
     __syncthreads();
     // ---- phase 2
     if (w == 0) {
@@ -300,7 +320,7 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
 inline size_t env_step_smem(int D, int A) {
   const int Ap = (A + 3) & ~3;
   return (static_cast<size_t>(D) * Ap + static_cast<size_t>(kEnvTile) * (D | 1) + 2 * kEnvTile +
-          32 * kEnvWarps) *
+          32 * kEnvTile) *
          sizeof(float);
 }
 
