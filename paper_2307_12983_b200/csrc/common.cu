@@ -40,6 +40,14 @@ int skip_step() {
   return e ? std::atoi(e) : -1;
 }
 
+bool eager_updates() {
+  static const bool on = [] {
+    const char* e = std::getenv("PQLG_EAGER");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 [[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
   char buf[512];
   std::snprintf(buf, sizeof(buf), "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),

@@ -76,6 +76,9 @@ void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaSt
 // when it is (re)built, so graph replays measure each step's marginal cost
 // in situ (results are then meaningless; tools/skip_probe.py).
 int skip_step();
+// Profiling aid: PQLG_EAGER=1 makes update() launch its kernels one by one
+// (the launch profiler brackets each) instead of replaying the update graph.
+bool eager_updates();
 
 // Wraps an ABI entry point: converts exceptions to status codes.
 template <class F>
@@ -122,6 +125,25 @@ struct DevBuf {
   }
   size_t bytes() const { return n * sizeof(T); }
   T* get() const { return p; }
+};
+
+// Owning pinned host allocation (cudaMallocHost): truly asynchronous copies.
+template <class T>
+struct PinnedBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void alloc(size_t count) {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = count;
+    if (count) PQLG_CUDA(cudaMallocHost(&p, count * sizeof(T)));
+  }
 };
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }

@@ -103,6 +103,7 @@ class VLearner {
   DevBuf<float2> bc_;
   DevBuf<uint32_t> status_;
   DevBuf<float> loss_;
+  PinnedBuf<uint32_t> hbuf_;  // update(): loss bits + status
 
   // workspaces
   DevBuf<float> Xon_, Xtg_, ret_, eff_, y_;
@@ -211,6 +212,7 @@ class PLearner {
   DevBuf<float2> bc_;
   DevBuf<uint32_t> status_;
   DevBuf<float> loss_;
+  PinnedBuf<uint32_t> hbuf_;  // update(): loss bits + status
 
   DevBuf<float> X_, T_, dy_, up_, part_;
   std::vector<DevBuf<float>> pact_, Gp_;

@@ -8,6 +8,7 @@
 // wgrad/dgrad chain -> fixed-order gradient reduction + fp64 norm -> clip +
 // Adam (no Polyak for the policy).
 #include "pdl.cuh"
+#include <cstring>
 #include <memory>
 #include <random>
 #include <vector>
@@ -105,6 +106,7 @@ PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   bc_.alloc(tab.size());
   PQLG_CUDA(cudaMemcpy(bc_.p, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
   status_.alloc(1);
+  hbuf_.alloc(2);
   loss_.alloc(2);  // actor loss (+ pql_sac: mean log-prob for the alpha update)
   build_update();
   PQLG_CUDA(cudaDeviceSynchronize());
@@ -642,17 +644,28 @@ int PLearner::check_status() {
 float PLearner::update() {
   if (states_->size() < static_cast<uint64_t>(B_))
     throw Error(PQLG_NOT_READY, "policy update before state warm-up");
-  if (mt_mode_) {
+  if (mt_mode_ || eager_updates()) {
     const uint64_t count = states_->size();
     std::uniform_int_distribution<std::size_t> pick(0, count - 1);
-    for (int r = 0; r < B_; ++r) idx_host_[r] = pick(mt_);
-    PQLG_CUDA(cudaMemcpyAsync(idx_.p, idx_host_.data(), B_ * sizeof(uint64_t),
-                              cudaMemcpyHostToDevice, stream_));
+    if (mt_mode_) {
+      for (int r = 0; r < B_; ++r) idx_host_[r] = pick(mt_);
+      PQLG_CUDA(cudaMemcpyAsync(idx_.p, idx_host_.data(), B_ * sizeof(uint64_t),
+                                cudaMemcpyHostToDevice, stream_));
+    }
+    enqueue();
+  } else {
+    update_n(1);  // one replay of the captured update graph
   }
-  enqueue();
-  float loss = 0.0f;
-  PQLG_CUDA(cudaMemcpyAsync(&loss, loss_.p, 4, cudaMemcpyDeviceToHost, stream_));
-  if (check_status() != PQLG_OK) throw Error(PQLG_ENONFINITE, "ddpg actor update: non-finite");
+  // loss + status into pinned memory, one synchronisation
+  PQLG_CUDA(cudaMemcpyAsync(&hbuf_.p[0], loss_.p, 4, cudaMemcpyDeviceToHost, stream_));
+  PQLG_CUDA(cudaMemcpyAsync(&hbuf_.p[1], status_.p, 4, cudaMemcpyDeviceToHost, stream_));
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+  if (hbuf_.p[1] != 0u) {
+    PQLG_CUDA(cudaMemsetAsync(status_.p, 0, 4, stream_));
+    throw Error(PQLG_ENONFINITE, "ddpg actor update: non-finite");
+  }
+  float loss;
+  std::memcpy(&loss, &hbuf_.p[0], 4);
   return loss;
 }
 

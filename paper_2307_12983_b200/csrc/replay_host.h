@@ -20,17 +20,35 @@ struct DeviceNorm {
   DevBuf<float> mean, inv;
   DevBuf<int> ident;  // device flag: kernels (and captured graphs) read it at run time
   int D = 0;
+  // pinned staging [mean_f D | inv_f D | ident] so set() is asynchronous; the
+  // event guards reuse while a previous copy is in flight
+  float* stage = nullptr;
+  cudaEvent_t staged = nullptr;
+  DeviceNorm() = default;
+  DeviceNorm(const DeviceNorm&) = delete;
+  DeviceNorm& operator=(const DeviceNorm&) = delete;
+  ~DeviceNorm() {
+    if (staged) {
+      cudaEventSynchronize(staged);
+      cudaEventDestroy(staged);
+    }
+    if (stage) cudaFreeHost(stage);
+  }
   void init(int dim) {
     D = dim;
     mean.alloc(dim);
     inv.alloc(dim);
     ident.alloc(1);
+    PQLG_CUDA(cudaMallocHost(&stage, (2 * static_cast<size_t>(dim) + 1) * sizeof(float)));
+    PQLG_CUDA(cudaEventCreateWithFlags(&staged, cudaEventDisableTiming));
     set_identity(nullptr);
+    PQLG_CUDA(cudaEventSynchronize(staged));
   }
   void set_identity(cudaStream_t st) {
-    static const int one = 1;
-    PQLG_CUDA(cudaMemcpyAsync(ident.p, &one, sizeof(int), cudaMemcpyHostToDevice, st));
-    PQLG_CUDA(cudaStreamSynchronize(st));
+    PQLG_CUDA(cudaEventSynchronize(staged));
+    reinterpret_cast<int*>(stage)[2 * D] = 1;
+    PQLG_CUDA(cudaMemcpyAsync(ident.p, stage + 2 * D, sizeof(int), cudaMemcpyHostToDevice, st));
+    PQLG_CUDA(cudaEventRecord(staged, st));
   }
   // NormStats -> (mean_f, inv_f) exactly as normalizer.hpp:62-66 (host double).
   void set(int64_t count, const double* m, const double* m2, cudaStream_t st) {
@@ -38,17 +56,19 @@ struct DeviceNorm {
       set_identity(st);
       return;
     }
-    std::vector<float> mf(D), inv_f(D);
+    PQLG_CUDA(cudaEventSynchronize(staged));  // the previous staged copy has landed
+    float* mf = stage;
+    float* inv_f = stage + D;
     for (int j = 0; j < D; ++j) {
       mf[j] = static_cast<float>(m[j]);
       const double var = m2[j] / static_cast<double>(count);
       inv_f[j] = static_cast<float>(1.0 / std::sqrt(var + 1e-8));
     }
-    static const int zero = 0;
-    PQLG_CUDA(cudaMemcpyAsync(mean.p, mf.data(), D * sizeof(float), cudaMemcpyHostToDevice, st));
-    PQLG_CUDA(cudaMemcpyAsync(inv.p, inv_f.data(), D * sizeof(float), cudaMemcpyHostToDevice, st));
-    PQLG_CUDA(cudaMemcpyAsync(ident.p, &zero, sizeof(int), cudaMemcpyHostToDevice, st));
-    PQLG_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+    reinterpret_cast<int*>(stage)[2 * D] = 0;
+    PQLG_CUDA(cudaMemcpyAsync(mean.p, mf, D * sizeof(float), cudaMemcpyHostToDevice, st));
+    PQLG_CUDA(cudaMemcpyAsync(inv.p, inv_f, D * sizeof(float), cudaMemcpyHostToDevice, st));
+    PQLG_CUDA(cudaMemcpyAsync(ident.p, stage + 2 * D, sizeof(int), cudaMemcpyHostToDevice, st));
+    PQLG_CUDA(cudaEventRecord(staged, st));
   }
   // The same from device-resident NormStats (count, mean, m2), computed on
   // device in fp64 (IEEE division and sqrt: identical to the host formula),

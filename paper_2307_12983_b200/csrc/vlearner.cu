@@ -6,6 +6,7 @@
 // -> fixed-order gradient reduction + fp64 norm -> fused clip/Adam/Polyak.
 // Every step is a pre-built launch; update_n() replays them from a CUDA graph.
 #include <algorithm>
+#include <cstring>
 #include <memory>
 #include <random>
 #include <vector>
@@ -113,6 +114,7 @@ VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   bc_.alloc(tab.size());
   PQLG_CUDA(cudaMemcpy(bc_.p, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
   status_.alloc(1);
+  hbuf_.alloc(2);
   loss_.alloc(1);
 
   build_update();
@@ -642,11 +644,22 @@ int VLearner::check_status() {
 float VLearner::update() {
   if (replay_->size() < static_cast<uint64_t>(B_))
     throw Error(PQLG_NOT_READY, "critic update before buffer warm-up");
-  if (mt_mode_) prepare_indices();
-  enqueue();
-  float loss = 0.0f;
-  PQLG_CUDA(cudaMemcpyAsync(&loss, loss_.p, 4, cudaMemcpyDeviceToHost, stream_));
-  if (check_status() != PQLG_OK) throw Error(PQLG_ENONFINITE, "ddpg critic update: non-finite");
+  if (mt_mode_ || eager_updates()) {  // host-drawn indices / profiling: eager launches
+    if (mt_mode_) prepare_indices();
+    enqueue();
+  } else {
+    update_n(1);  // one replay of the captured update graph
+  }
+  // loss + status into pinned memory, one synchronisation
+  PQLG_CUDA(cudaMemcpyAsync(&hbuf_.p[0], loss_.p, 4, cudaMemcpyDeviceToHost, stream_));
+  PQLG_CUDA(cudaMemcpyAsync(&hbuf_.p[1], status_.p, 4, cudaMemcpyDeviceToHost, stream_));
+  PQLG_CUDA(cudaStreamSynchronize(stream_));
+  if (hbuf_.p[1] != 0u) {
+    PQLG_CUDA(cudaMemsetAsync(status_.p, 0, 4, stream_));
+    throw Error(PQLG_ENONFINITE, "ddpg critic update: non-finite");
+  }
+  float loss;
+  std::memcpy(&loss, &hbuf_.p[0], 4);
   return loss;
 }
 

@@ -8,6 +8,7 @@ replayed time of the same step for comparison.
   python tools/kprof.py [critic|policy|actor|c51 ...]
 """
 import ctypes as C
+import os
 import sys
 from collections import defaultdict
 from pathlib import Path
@@ -15,6 +16,7 @@ from pathlib import Path
 import numpy as np
 import torch
 
+os.environ["PQLG_EAGER"] = "1"  # update(): per-kernel launches the profiler can bracket
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2307_12983_b200 import _lib  # noqa: E402
 
