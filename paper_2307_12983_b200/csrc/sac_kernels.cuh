@@ -196,53 +196,6 @@ struct GaussArgs {
   float mid, half;
 };
 
-// k-th (0-based) set bit of m
-__device__ __forceinline__ int nth_set_bit(unsigned int m, int k) {
-  for (int i = 0; i < k; ++i) m &= m - 1;
-  return __ffs(m) - 1;
-}
-
-// A fresh normal_distribution<float> over the row's SplitMix state
-// (learners.cpp:89-92), the polar candidates drawn 32 at a time across the
-// warp: lane l of round r tries pair r*32 + l (states s + 2(r*32 + l), +1);
-// accepted pairs are taken in lane order.  Returns lane d's normal (d < A).
-__device__ __forceinline__ float row_normals(uint64_t* state, int A, int lane) {
-  const uint64_t s0 = *state;
-  const int need = (A + 1) / 2;
-  int got = 0;
-  float val = 0.0f;
-  uint64_t consumed = 0;
-  for (int round = 0;; ++round) {
-    uint64_t s = s0 + 2 * (static_cast<uint64_t>(round) * 32 + lane);
-    const float x = __double2float_rn(
-        static_cast<double>(__fmul_rn(2.0f, rng::canonical_f32(s))) - 1.0);
-    const float y = __double2float_rn(
-        static_cast<double>(__fmul_rn(2.0f, rng::canonical_f32(s))) - 1.0);
-    const float r2 = __fadd_rn(__fmul_rn(x, x), __fmul_rn(y, y));
-    const bool ok = !(r2 > 1.0f || r2 == 0.0f);
-    const unsigned int bal = __ballot_sync(0xffffffffu, ok);
-    float vx = 0.0f, vy = 0.0f;
-    if (ok) {
-      const float mult = __fsqrt_rn(__fdiv_rn(__fmul_rn(-2.0f, rng::glibc_logf(r2)), r2));
-      vx = __fmul_rn(x, mult);
-      vy = __fmul_rn(y, mult);
-    }
-    const int n = __popc(bal);
-    const int p = lane / 2 - got;  // this lane's pair within this round
-    const int owner = (lane < A && p >= 0 && p < n) ? nth_set_bit(bal, p) : 0;
-    const float oy = __shfl_sync(0xffffffffu, vy, owner);
-    const float ox = __shfl_sync(0xffffffffu, vx, owner);
-    if (lane < A && p >= 0 && p < n) val = (lane & 1) ? ox : oy;
-    if (got + n >= need) {
-      consumed = static_cast<uint64_t>(round) * 32 + nth_set_bit(bal, need - got - 1) + 1;
-      break;
-    }
-    got += n;
-  }
-  if (lane == 0) *state = s0 + 2 * consumed;
-  return val;
-}
-
 // Warp per row (grid-stride), lane d < A handles mean column d and log_std
 // column A + d; the log-prob sum runs over d ascending as the reference's.
 static __global__ void __launch_bounds__(32 * kFinishWarps)
@@ -259,7 +212,7 @@ static __global__ void __launch_bounds__(32 * kFinishWarps)
     if (a.eps) {
       if (on) e = a.eps[static_cast<int64_t>(m) * a.A + lane];
     } else {
-      e = row_normals(a.rng + m, a.A, lane);
+      e = rng::warp_row_normals(a.rng + m, a.A, lane);
     }
     float term = 0.0f;
     if (on) {
