@@ -412,7 +412,12 @@ def run_actor(args, rank, world, local, steps, warmup):
                               max_episode_len=1000)
     dims = _lib.TaskDims(D, A, -1.0, 1.0)
     act, vl, pl = C.c_void_p(), C.c_void_p(), C.c_void_p()
-    _lib.call("pqlg_actor_create", C.byref(cfg), C.byref(dims), sp, C.byref(act))
+    comm = _lib.comm_from_torch_dist(rank, world) if world > 1 else None
+    if comm is not None:  # shard of one actor: normalizer merged over all shards every step
+        _lib.call("pqlg_actor_create_sharded", C.byref(cfg), C.byref(dims), comm, sp,
+                  C.byref(act))
+    else:
+        _lib.call("pqlg_actor_create", C.byref(cfg), C.byref(dims), sp, C.byref(act))
     _lib.call("pqlg_vlearner_create", C.byref(cfg), C.byref(dims), 1,
               C.c_void_p(sv_t.cuda_stream), C.byref(vl))
     _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 1,
@@ -483,6 +488,8 @@ def run_actor(args, rank, world, local, steps, warmup):
     for h, fn in ((act, "pqlg_actor_destroy"), (vl, "pqlg_vlearner_destroy"),
                   (pl, "pqlg_plearner_destroy")):
         _lib.call(fn, h)
+    if comm is not None:
+        _lib.call("pqlg_comm_destroy", comm)
     return {"value": world * N * steps / (ms * 1e-3), "unit": "transitions/s",
             "n_envs_per_gpu": N, "ms_per_step": ms / steps,
             "actor_step_only": {"value": world * N * steps / (ms_actor_only * 1e-3),

@@ -359,6 +359,14 @@ typedef struct pqlg_env_s* pqlg_env;
  * Env/noise streams use global env indices env_offset + i. */
 PQLG_API int pqlg_actor_create(const pqlg_config* cfg, const pqlg_task_dims* dims, void* stream,
                                pqlg_actor* out);
+/* A shard of a multi-GPU actor: cfg->env_offset / envs_total
+ * place its envs in the global index space (streams, noise schedule), and
+ * the running normalizer is merged over the communicator every step (an
+ * all-gather of each shard's batch mean / M2 / n, combined in rank order),
+ * so every shard normalises with the statistics of all envs.  A world-1
+ * communicator reproduces pqlg_actor_create bit for bit. */
+PQLG_API int pqlg_actor_create_sharded(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                                       pqlg_comm comm, void* stream, pqlg_actor* out);
 PQLG_API int pqlg_actor_destroy(pqlg_actor h);
 /* adopt_policy: PolicyHandle::adopt, equal-or-newer (learners.cpp:37-42) */
 PQLG_API int pqlg_actor_adopt_policy(pqlg_actor h, const float* flat_host, int64_t version);

@@ -351,6 +351,37 @@ void orc_norm_update(int64_t* count, double* mean, double* m2, const float* batc
   free(bmean); free(bm2);
 }
 
+/* Sharded normalizer: one shard's batch statistics (the
+ * batch Welford of RunningNormalizer::update, normalizer.hpp:33-50) ... */
+void orc_norm_batch_stats(const float* batch, size_t rows, size_t d, double* bmean, double* bm2) {
+  memset(bmean, 0, d * sizeof(double));
+  memset(bm2, 0, d * sizeof(double));
+  double n = 0.0;
+  for (size_t r = 0; r < rows; ++r) {
+    n += 1.0;
+    for (size_t j = 0; j < d; ++j) {
+      const double x = batch[r * d + j];
+      const double delta = x - bmean[j];
+      bmean[j] += delta / n;
+      bm2[j] += delta * (x - bmean[j]);
+    }
+  }
+}
+
+/* ... and Chan's merge of a batch (nb, bmean, bm2) into (count, mean, m2)
+ * (normalizer.hpp:73-83).  The shards' batches are combined in rank order
+ * with this merge, then merged into the running stats. */
+void orc_norm_merge(double* count, double* mean, double* m2, size_t d, double nb,
+                    const double* bmean, const double* bm2) {
+  const double na = *count, nab = na + nb;
+  for (size_t j = 0; j < d; ++j) {
+    const double delta = bmean[j] - mean[j];
+    mean[j] += delta * (nb / nab);
+    m2[j] += bm2[j] + delta * delta * (na * nb / nab);
+  }
+  *count = nab;
+}
+
 /* =============================================================== optim.hpp */
 
 /* optim.hpp:35-39 (beta1 0.9, beta2 0.999) */

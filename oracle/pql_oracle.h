@@ -109,6 +109,12 @@ void orc_normalize_apply(int64_t count, const double* mean, const double* m2, co
 void orc_norm_update(int64_t* count, double* mean, double* m2, const float* batch, size_t rows,
                      size_t d);
 
+/* Sharded normalizer: a shard's batch (mean, M2), and Chan's merge of a
+ * batch into (count, mean, m2) (normalizer.hpp:33-50, :73-83). */
+void orc_norm_batch_stats(const float* batch, size_t rows, size_t d, double* bmean, double* bm2);
+void orc_norm_merge(double* count, double* mean, double* m2, size_t d, double nb,
+                    const double* bmean, const double* bm2);
+
 /* ---------------------------------------------------------- optim.hpp */
 void orc_adam_bias_corrections(int64_t t, float* bc1, float* bc2);
 void orc_adam_update(float* p, const float* g, float* m, float* v, size_t n, float lr, float beta1,

@@ -170,6 +170,7 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_plearner_set_sampler": (i32, [vp, i32]),
     "pqlg_plearner_kernels_per_update": (i32, [vp, P(i32)]),
     "pqlg_actor_create": (i32, [P(Config), P(TaskDims), vp, P(vp)]),
+    "pqlg_actor_create_sharded": (i32, [P(Config), P(TaskDims), vp, vp, P(vp)]),
     "pqlg_actor_destroy": (i32, [vp]),
     "pqlg_actor_adopt_policy": (i32, [vp, vp, i64]),
     "pqlg_actor_rollout_step": (i32, [vp, P(StepSlice)]),

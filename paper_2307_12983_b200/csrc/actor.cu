@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "actor.h"
+#include "comm.h"
 #include "actor_kernels.cuh"
 #include "learner.h"
 
@@ -111,8 +112,9 @@ struct DeviceEnv {
 
 
 
-Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st)
-    : cfg_(cfg), dims_(dims), stream_(st) {
+Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st,
+             pqlg_comm_s* comm)
+    : cfg_(cfg), dims_(dims), stream_(st), comm_(comm) {
   if (!stream_) {
     PQLG_CUDA(cudaStreamCreateWithFlags(&owned_stream_, cudaStreamNonBlocking));
     stream_ = owned_stream_;
@@ -192,6 +194,11 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
   const int one = 1;
   PQLG_CUDA(cudaMemcpy(identity_.p, &one, 4, cudaMemcpyHostToDevice));
   npart_.alloc(static_cast<size_t>(actor::kNormGroups) * D_ * 2);
+  if (comm_) {
+    require(D_ <= 1024, "actor: sharded normalizer needs obs_dim <= 1024");
+    nbatch_.alloc(2 * static_cast<size_t>(D_) + 1);
+    ngather_.alloc(static_cast<size_t>(comm_->world) * (2 * D_ + 1));
+  }
   nticket_.alloc(actor::norm_tickets(D_));
   status_.alloc(1);
   // first policy input: apply_stats with count 0 is the identity
@@ -285,8 +292,17 @@ void Actor::enqueue(int cur) {
   // normalizer_.update(obs_) (learners.cpp:113): it only reads this step's
   // observations, so it runs before the env step and the env kernel can emit
   // the next policy input apply(stats_t, obs_{t+1}) directly.
-  actor::NormState ns{count_.p, mean_.p, m2_.p, mean_f_.p, inv_f_.p, identity_.p};
+  actor::NormState ns{count_.p, mean_.p, m2_.p, mean_f_.p, inv_f_.p, identity_.p,
+                      comm_ ? nbatch_.p : nullptr};
   launch(actor::norm_update_kernel, dim3(dim3((D + 31) / 32, actor::kNormGroups)), dim3(256), 0, st, obs, Dp_, N, D, npart_.p, nticket_.p, ns);
+  if (comm_) {
+    // sharded: every shard's batch statistics, merged in rank
+    // order into identical running stats on all shards (5 KB at config 3)
+    allgather_f64(comm_, nbatch_.p, ngather_.p, 2 * static_cast<size_t>(D) + 1, st);
+    ns.batch = nullptr;
+    launch(actor::norm_merge_kernel, dim3(1), dim3((D + 31) / 32 * 32), 0, st, ngather_.p,
+           comm_->world, D, ns);
+  }
   // env_->step(actions) + next-obs normalisation
   const int nxt = (cur + 1) % kSets;
   actor::StepOut o{obs_[nxt].p, boot_[cur].p, rew_[cur].p, term_[cur].p, trunc_[cur].p, nullptr,
@@ -555,6 +571,16 @@ int pqlg_actor_create(const pqlg_config* cfg, const pqlg_task_dims* dims, void* 
     require(cfg && dims && out, "actor_create: null argument");
     auto h = std::make_unique<pqlg_actor_s>();
     h->a = std::make_unique<Actor>(*cfg, *dims, static_cast<cudaStream_t>(stream));
+    *out = h.release();
+  });
+}
+
+int pqlg_actor_create_sharded(const pqlg_config* cfg, const pqlg_task_dims* dims, pqlg_comm comm,
+                              void* stream, pqlg_actor* out) {
+  return guarded([&] {
+    require(cfg && dims && out && comm, "actor_create_sharded: null argument");
+    auto h = std::make_unique<pqlg_actor_s>();
+    h->a = std::make_unique<Actor>(*cfg, *dims, static_cast<cudaStream_t>(stream), comm);
     *out = h.release();
   });
 }

@@ -9,13 +9,18 @@
 #include "mlp_host.h"
 #include "net.h"
 
+struct pqlg_comm_s;
+
 namespace pqlg {
 
 struct DeviceEnv;
 
 class Actor {
  public:
-  Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st);
+  // comm (nullable): a sharded actor whose running normalizer is merged over
+  // all shards every step (all-gather of the batch statistics)
+  Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st,
+        pqlg_comm_s* comm = nullptr);
   ~Actor();
   void adopt_policy(const float* flat, int64_t version, bool device);
   void rollout_step(pqlg_step_slice* out);
@@ -50,6 +55,8 @@ class Actor {
   cudaStream_t owned_stream_ = nullptr;
   int N_, D_, A_, Ap_, H_, nh_;
   bool sac_ = false;            // pql_sac: Gaussian policy, no schedule noise
+  pqlg_comm_s* comm_ = nullptr; // sharded: normalizer merged across shards
+  DevBuf<double> nbatch_, ngather_;
   mlp::HeadSplit head_split_;   // pql_sac: split-K [mean | log_std] head
   int64_t Dp_;
   NetShape pnet_;

@@ -372,7 +372,20 @@ struct NormState {
   float* mean_f;
   float* inv_f;
   int* identity;
+  // sharded actor: non-null -> the batch's (mean [D], M2 [D], n) are written
+  // here instead of being merged (norm_merge_kernel merges every shard's)
+  double* batch;
 };
+
+// Chan's parallel merge of (na, mean_a, m2_a) with a batch (nb, mean_b, m2_b)
+// (normalizer.hpp:73-83), fp64, in the reference's operation order.
+__device__ __forceinline__ void chan_merge(double na, double& mean, double& m2, double nb,
+                                           double bmean, double bm2) {
+  const double nab = na + nb;
+  const double delta = bmean - mean;
+  mean = mean + delta * (nb / nab);
+  m2 = m2 + (bm2 + delta * delta * (na * nb / nab));
+}
 
 // RunningNormalizer::update (normalizer.hpp:33-50, :73-83) in one launch,
 // parallel and deterministic.  Grid (ceil(D/32) column strips, kNormGroups
@@ -462,11 +475,10 @@ static __global__ void __launch_bounds__(256, 4)
     red[w][lane][1] = a2;
   }
   __syncthreads();
-  const int64_t n0i = *s.count;
+  const int64_t n0i = s.batch ? 0 : *s.count;
   if (w == 0 && c < D) {
     const double nb = static_cast<double>(N);
     const double na = static_cast<double>(n0i);
-    const double nab = na + nb;
     const int64_t cnt = n0i + N;
     double t1 = 0.0, t2 = 0.0;
     for (int k = 0; k < 8; ++k) {
@@ -476,13 +488,17 @@ static __global__ void __launch_bounds__(256, 4)
     const double bmean = static_cast<double>(x[c]) + t1 / nb;
     double bm2 = t2 - t1 * t1 / nb;
     if (bm2 < 0.0) bm2 = 0.0;
-    const double delta = bmean - s.mean[c];
-    const double mean = s.mean[c] + delta * (nb / nab);
-    const double m2 = s.m2[c] + (bm2 + delta * delta * (na * nb / nab));
-    s.mean[c] = mean;
-    s.m2[c] = m2;
-    s.mean_f[c] = static_cast<float>(mean);
-    s.inv_f[c] = static_cast<float>(1.0 / sqrt(m2 / static_cast<double>(cnt) + 1e-8));
+    if (s.batch) {
+      s.batch[c] = bmean;
+      s.batch[D + c] = bm2;
+    } else {
+      double mean = s.mean[c], m2 = s.m2[c];
+      chan_merge(na, mean, m2, nb, bmean, bm2);
+      s.mean[c] = mean;
+      s.m2[c] = m2;
+      s.mean_f[c] = static_cast<float>(mean);
+      s.inv_f[c] = static_cast<float>(1.0 / sqrt(m2 / static_cast<double>(cnt) + 1e-8));
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -490,10 +506,50 @@ static __global__ void __launch_bounds__(256, 4)
     __threadfence();
     // every strip read the old count before its ticket: the last one advances it
     if (atomicAdd(&ticket[0], 1u) == gridDim.x - 1) {
-      *s.count = n0i + N;
-      *s.identity = n0i + N <= 1 ? 1 : 0;
+      if (s.batch) {
+        s.batch[2 * D] = static_cast<double>(N);
+      } else {
+        *s.count = n0i + N;
+        *s.identity = n0i + N <= 1 ? 1 : 0;
+      }
       ticket[0] = 0u;
     }
+  }
+}
+
+// Sharded actor: after an all-gather of every shard's batch
+// statistics ([world][2D + 1]: mean, M2, n), each rank combines them in rank
+// order (Chan) and merges the result into its running stats, so all shards
+// keep identical normalizers -- the statistics of the concatenated batch up
+// to fp64 rounding.  With one shard this is the unsharded update bit for bit.
+// One block, a thread per column (D <= 1024).
+static __global__ void norm_merge_kernel(const double* __restrict__ gathered, int world, int D,
+                                         NormState s) {
+  pdl::entry();
+  const int c = threadIdx.x;
+  const int64_t stride = 2 * static_cast<int64_t>(D) + 1;
+  const int64_t n0i = *s.count;
+  int64_t nsum = 0;
+  for (int k = 0; k < world; ++k) nsum += static_cast<int64_t>(gathered[k * stride + 2 * D]);
+  if (c < D) {
+    double nb = gathered[2 * D];
+    double bmean = gathered[c], bm2 = gathered[D + c];
+    for (int k = 1; k < world; ++k) {
+      const double* g = gathered + k * stride;
+      chan_merge(nb, bmean, bm2, g[2 * D], g[c], g[D + c]);
+      nb += g[2 * D];
+    }
+    double mean = s.mean[c], m2 = s.m2[c];
+    chan_merge(static_cast<double>(n0i), mean, m2, nb, bmean, bm2);
+    s.mean[c] = mean;
+    s.m2[c] = m2;
+    s.mean_f[c] = static_cast<float>(mean);
+    s.inv_f[c] = static_cast<float>(1.0 / sqrt(m2 / static_cast<double>(n0i + nsum) + 1e-8));
+  }
+  __syncthreads();  // every thread has read the old count
+  if (c == 0) {
+    *s.count = n0i + nsum;
+    *s.identity = n0i + nsum <= 1 ? 1 : 0;
   }
 }
 

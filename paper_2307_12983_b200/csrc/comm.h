@@ -35,4 +35,10 @@ inline void allreduce_sum(pqlg_comm_s* c, float* a, size_t na, float* b, size_t 
   PQLG_NCCL(ncclGroupEnd());
 }
 
+// All-gather of fp64 records (the sharded actor's batch statistics).
+inline void allgather_f64(pqlg_comm_s* c, const double* send, double* recv, size_t n,
+                          cudaStream_t st) {
+  PQLG_NCCL(ncclAllGather(send, recv, n, ncclFloat64, c->nccl, st));
+}
+
 }  // namespace pqlg

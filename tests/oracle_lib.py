@@ -72,6 +72,8 @@ _ORC_SIGS = {
     "orc_c51_actor_loss": (i32, [vp, vp, vp, vp, vp, sz, vp, sz, sz, sz, f32, f32, sz, f32, f32,
                                  vp, vp]),
     "orc_normals": (None, [i32, vp, u64, vp, sz, vp]),
+    "orc_norm_batch_stats": (None, [vp, sz, sz, vp, vp]),
+    "orc_norm_merge": (None, [vp, vp, vp, sz, f64, vp, vp]),
     "orc_normals_rows": (None, [vp, sz, sz, vp]),
     "orc_gauss_sample": (i32, [vp, vp, sz, vp, vp, sz, f32, f32, vp, vp]),
     "orc_sac_critic_loss": (i32, [vp, vp, vp, vp, vp, vp, vp, sz, vp, vp, vp, vp, vp, sz, sz,

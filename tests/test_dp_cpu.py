@@ -134,3 +134,69 @@ def test_dp_critic_update_matches_single_process_on_concatenated_batch():
     want = apply_update(pb, dq)
     for got, w in zip(res[0][4], want):
         assert np.max(np.abs(got - w)) <= 1e-6 + 1e-5 * np.max(np.abs(w))
+
+
+def _norm_worker(rank, world, port, q):
+    """A sharded actor's normalizer step (pqlg_actor_create_sharded): the
+    shard's batch (mean, M2, n), an all-gather, the rank-order combination
+    and the merge into the running stats -- on every rank."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(3)
+        D, n, steps = 17, 40, 3
+        count = np.array([500.0])
+        mean = rng.standard_normal(D) * 0.5
+        m2 = np.abs(rng.standard_normal(D)) * 500.0
+        for t in range(steps):
+            rows = f32(rng.standard_normal((world * n, D)) * 2.0 + 3.0)  # same on every rank
+            mine = np.ascontiguousarray(rows[rank * n:(rank + 1) * n])
+            bm, b2 = np.zeros(D), np.zeros(D)
+            orc().orc_norm_batch_stats(ptr(mine), n, D, ptr(bm), ptr(b2))
+            rec = torch.from_numpy(np.concatenate([bm, b2, [float(n)]]))
+            recs = [torch.zeros_like(rec) for _ in range(world)]
+            dist.all_gather(recs, rec)
+            g = [r.numpy() for r in recs]
+            # combine shards in rank order, then merge into the running stats
+            cn = np.array([g[0][2 * D]])
+            cm, c2 = g[0][:D].copy(), g[0][D:2 * D].copy()
+            for k in range(1, world):
+                orc().orc_norm_merge(ptr(cn), ptr(cm), ptr(c2), D, g[k][2 * D],
+                                     ptr(np.ascontiguousarray(g[k][:D])),
+                                     ptr(np.ascontiguousarray(g[k][D:2 * D])))
+            orc().orc_norm_merge(ptr(count), ptr(mean), ptr(m2), D, cn[0], ptr(cm), ptr(c2))
+        q.put((rank, float(count[0]), mean.copy(), m2.copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_normalizer_merge_matches_single_normalizer():
+    """the shards' merged running stats equal RunningNormalizer
+    on the concatenated batches (fp64 rounding, 1e-12 rel) and are
+    identical on every rank."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_norm_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][1] == res[1][1]
+    assert np.array_equal(res[0][2], res[1][2]) and np.array_equal(res[0][3], res[1][3])
+    rng = np.random.default_rng(3)
+    D, n, steps = 17, 40, 3
+    count = np.array([500], np.int64)
+    mean = rng.standard_normal(D) * 0.5
+    m2 = np.abs(rng.standard_normal(D)) * 500.0
+    for t in range(steps):
+        rows = f32(rng.standard_normal((world * n, D)) * 2.0 + 3.0)
+        orc().orc_norm_update(ptr(count), ptr(mean), ptr(m2), ptr(rows), world * n, D)
+    assert res[0][1] == float(count[0])
+    np.testing.assert_allclose(res[0][2], mean, rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(res[0][3], m2, rtol=1e-12)

@@ -123,3 +123,52 @@ def test_comm_allreduce_world1_identity():
     torch.cuda.synchronize()
     assert torch.equal(x, y)
     _lib.call("pqlg_comm_destroy", comm)
+
+
+def test_sharded_actor_world1_bit_identical():
+    """pqlg_actor_create_sharded over a world-1 NCCL communicator (batch
+    statistics -> all-gather -> rank-order merge) reproduces the plain actor
+    bit for bit: observations, actions, normalizer stats; eager steps and
+    graph replays (the all-gather is captured with the step)."""
+    import torch
+    torch.cuda.set_device(0)
+    comm = comm_world1()
+    N, D, A = 512, 37, 6
+    cfg = _lib.default_config(n_envs=N, hidden=64, hidden_layers=2, seed=4, max_episode_len=9)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    plain, sh = C.c_void_p(), C.c_void_p()
+    _lib.call("pqlg_actor_create", C.byref(cfg), C.byref(dims), None, C.byref(plain))
+    _lib.call("pqlg_actor_create_sharded", C.byref(cfg), C.byref(dims), comm, None, C.byref(sh))
+    sl = _lib.StepSlice()
+
+    def state(h):
+        obs = np.zeros((N, D), np.float32)
+        act = np.zeros((N, A), np.float32)
+        _lib.call("pqlg_actor_read", h, 0, ptr(obs))
+        _lib.call("pqlg_actor_read", h, 1, ptr(act))
+        cnt = C.c_int64()
+        mean = np.zeros(D)
+        m2 = np.zeros(D)
+        _lib.call("pqlg_actor_norm", h, C.byref(cnt), ptr(mean), ptr(m2))
+        return obs, act, cnt.value, mean, m2
+
+    for _ in range(5):
+        for h in (plain, sh):
+            _lib.call("pqlg_actor_rollout_step", h, C.byref(sl))
+        a, b = state(plain), state(sh)
+        assert a[2] == b[2] == a[2]
+        for x, y in zip(a[:2] + a[3:], b[:2] + b[3:]):
+            assert np.array_equal(x, y)
+    for h in (plain, sh):
+        _lib.call("pqlg_actor_rollout_n", h, 6)
+    a, b = state(plain), state(sh)
+    assert a[2] == b[2]
+    for x, y in zip(a[:2] + a[3:], b[:2] + b[3:]):
+        assert np.array_equal(x, y)
+    kp, ks = C.c_int(), C.c_int()
+    _lib.call("pqlg_actor_kernels_per_step", plain, C.byref(kp))
+    _lib.call("pqlg_actor_kernels_per_step", sh, C.byref(ks))
+    assert ks.value == kp.value + 1  # the merge kernel
+    for h in (plain, sh):
+        _lib.call("pqlg_actor_destroy", h)
+    _lib.call("pqlg_comm_destroy", comm)
