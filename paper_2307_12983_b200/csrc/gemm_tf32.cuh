@@ -215,7 +215,8 @@ __device__ __forceinline__ TileCoord tile_coord(int t, const Problem& p, int til
 
 template <int BN, bool kAMN, bool kBMN, class Epi, bool kPair = false>
 __global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair>::kThreads, 1)
-    gemm_tf32_kernel(const __grid_constant__ Operands ops, const Problem prob, const Epi epi) {
+    gemm_tf32_kernel(const __grid_constant__ Operands ops, const Problem prob,
+                     const __grid_constant__ Epi epi) {
   using L = SmemLayout<BN, Epi, kPair>;
   constexpr int kStages = L::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];

@@ -520,7 +520,8 @@ __device__ __forceinline__ void draw_block_indices(const SamplerState* ss,
 }
 
 static __global__ void __launch_bounds__(32 * kWarpsPerBlock)
-    replay_sample_kernel(Ring ring, Norm norm, Gather g, SamplerState* ss,
+    replay_sample_kernel(const __grid_constant__ Ring ring, const __grid_constant__ Norm norm,
+                         const __grid_constant__ Gather g, SamplerState* ss,
                          const uint64_t* host_idx, uint64_t B) {
   __shared__ uint64_t s_idx[kSampleRows];
   pdl::entry();
