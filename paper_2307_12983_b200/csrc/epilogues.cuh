@@ -326,17 +326,21 @@ struct C51Head {
       scratch[kMaxAtoms + i] = i < L ? atoms[i] : 0.0f;
     }
   }
-  __device__ bool chunk(Row& r, const Ctx&, int n0, float (&v)[32], float* scratch) const {
+  __device__ bool chunk(Row& r, const Ctx& c, int n0, float (&v)[32], float* scratch) const {
     if (n0 == 0) {
 #pragma unroll
       for (int t = 0; t < 32; ++t) r.x[t] = __fadd_rn(v[t], scratch[t]);
+      if (L > 32) return false;
     } else {
 #pragma unroll
       for (int t = 0; t < 32; ++t) r.x[32 + t] = __fadd_rn(v[t], scratch[32 + t]);
     }
+    // last chunk of the row (BN = 64 covers L <= 64): softmax_row + E with
+    // the atoms from shared memory (c51.hpp:44-53, :135-138)
+    finish(r, c, scratch + kMaxAtoms);
     return false;
   }
-  __device__ void end(Row& r, const Ctx& c) const {
+  __device__ void finish(Row& r, const Ctx& c, const float* z) const {
     const int m = c.m, group = c.group;
     if (m >= M) return;
     float mx = r.x[0];
@@ -357,10 +361,11 @@ struct C51Head {
       if (j < L) {
         const float p = __fdiv_rn(r.x[j], sum);
         out[j] = p;
-        e = __fadd_rn(e, __fmul_rn(p, __ldg(atoms + j)));
+        e = __fadd_rn(e, __fmul_rn(p, z[j]));
       }
     if (ev[group]) ev[group][m] = e;
   }
+  __device__ void end(Row&, const Ctx&) const {}
 };
 
 }  // namespace pqlg::epi
