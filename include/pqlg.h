@@ -273,6 +273,11 @@ PQLG_API int pqlg_vlearner_log_alpha(pqlg_vlearner h, float* out);
 PQLG_API int pqlg_vlearner_adopt_norm(pqlg_vlearner h, const pqlg_norm_stats* norm);
 /* ingest(StepSlice): reward scale + n-step + insert (learners.cpp:144-151) */
 PQLG_API int pqlg_vlearner_ingest(pqlg_vlearner h, const pqlg_step_slice* dev);
+/* The learner's stream waits for a cudaEvent_t (e.g. pqlg_actor_step_event)
+ * before its next work: orders cross-stream reads of a device StepSlice. */
+PQLG_API int pqlg_vlearner_wait_event(pqlg_vlearner h, void* event);
+/* Records (and returns) the handle's event at the current end of its stream. */
+PQLG_API int pqlg_vlearner_record_event(pqlg_vlearner h, void** event_out);
 /* ingest from HOST buffers (a CPU-produced StepSlice): copied in on the
  * learner's stream; returns once the slice may be reused. */
 PQLG_API int pqlg_vlearner_ingest_host(pqlg_vlearner h, const pqlg_step_slice* host);
@@ -331,6 +336,8 @@ PQLG_API int pqlg_plearner_adopt_norm(pqlg_plearner h, const pqlg_norm_stats* no
 /* ingest(states) = StateBuffer::insert (learners.hpp:117) */
 PQLG_API int pqlg_plearner_ingest(pqlg_plearner h, const float* states_dev, int64_t ld,
                                   uint64_t n);
+PQLG_API int pqlg_plearner_wait_event(pqlg_plearner h, void* event);
+PQLG_API int pqlg_plearner_record_event(pqlg_plearner h, void** event_out);
 PQLG_API int pqlg_plearner_ingest_host(pqlg_plearner h, const float* states_host, int64_t ld,
                                        uint64_t n);
 PQLG_API int pqlg_plearner_ready(pqlg_plearner h, int64_t c_a, int* ready);
@@ -375,6 +382,14 @@ PQLG_API int pqlg_actor_adopt_policy(pqlg_actor h, const float* flat_host, int64
  * actor rotates three output buffer sets), so consumers on other streams can
  * read step t while step t+1 runs; order them before step t+2 (events). */
 PQLG_API int pqlg_actor_rollout_step(pqlg_actor h, pqlg_step_slice* out);
+/* The cudaEvent_t (as void*) recorded on the actor's stream after the last
+ * rollout_step: a consumer on another stream orders its reads of the slice
+ * after it with pqlg_{vlearner,plearner}_wait_event (the threading contract's
+ * exported events).  NULL before the first rollout_step. */
+PQLG_API int pqlg_actor_step_event(pqlg_actor h, void** event_out);
+/* The actor's stream waits for an event (e.g. a learner's record_event after
+ * ingesting step t) before reusing step t's buffers at step t + 3. */
+PQLG_API int pqlg_actor_wait_event(pqlg_actor h, void* event);
 /* n steps replayed from CUDA graphs (no slices returned). */
 PQLG_API int pqlg_actor_rollout_n(pqlg_actor h, int n);
 /* norm(): the running NormStats (host copies); synchronizes. */

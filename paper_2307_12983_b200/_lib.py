@@ -171,6 +171,12 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_plearner_kernels_per_update": (i32, [vp, P(i32)]),
     "pqlg_actor_create": (i32, [P(Config), P(TaskDims), vp, P(vp)]),
     "pqlg_actor_create_sharded": (i32, [P(Config), P(TaskDims), vp, vp, P(vp)]),
+    "pqlg_actor_step_event": (i32, [vp, P(vp)]),
+    "pqlg_vlearner_wait_event": (i32, [vp, vp]),
+    "pqlg_actor_wait_event": (i32, [vp, vp]),
+    "pqlg_vlearner_record_event": (i32, [vp, P(vp)]),
+    "pqlg_plearner_record_event": (i32, [vp, P(vp)]),
+    "pqlg_plearner_wait_event": (i32, [vp, vp]),
     "pqlg_actor_destroy": (i32, [vp]),
     "pqlg_actor_adopt_policy": (i32, [vp, vp, i64]),
     "pqlg_actor_rollout_step": (i32, [vp, P(StepSlice)]),
@@ -243,6 +249,14 @@ def lib() -> C.CDLL:
             raise RuntimeError(
                 f"{LIB_PATH} is missing: run `python -m paper_2307_12983_b200.build` "
                 "(there is no CPU fallback)")
+        # libpqlg.so links NCCL by its SONAME (libnccl.so.2).  Load torch's
+        # bundled NCCL first when torch is present: otherwise the system
+        # libnccl.so.2 (older) would claim that SONAME and a later
+        # `import torch` could not resolve its newer NCCL symbols.
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
         handle = C.CDLL(str(LIB_PATH), mode=C.RTLD_GLOBAL)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(handle, name)

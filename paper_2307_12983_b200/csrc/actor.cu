@@ -210,6 +210,7 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
 }
 
 Actor::~Actor() {
+  if (step_done_) cudaEventDestroy(step_done_);
   for (auto& g : graph_)
     if (g) cudaGraphExecDestroy(g);
   if (owned_stream_) {
@@ -328,6 +329,8 @@ int Actor::kernels_per_step() {
 void Actor::rollout_step(pqlg_step_slice* out) {
   const int cur = cur_;
   enqueue(cur);
+  if (!step_done_) PQLG_CUDA(cudaEventCreateWithFlags(&step_done_, cudaEventDisableTiming));
+  PQLG_CUDA(cudaEventRecord(step_done_, stream_));  // consumers on other streams wait on it
   if (out) {
     out->obs = obs_[cur].p;
     out->act = act_[cur].p;
@@ -582,6 +585,20 @@ int pqlg_actor_create_sharded(const pqlg_config* cfg, const pqlg_task_dims* dims
     auto h = std::make_unique<pqlg_actor_s>();
     h->a = std::make_unique<Actor>(*cfg, *dims, static_cast<cudaStream_t>(stream), comm);
     *out = h.release();
+  });
+}
+
+int pqlg_actor_step_event(pqlg_actor h, void** event_out) {
+  return guarded([&] {
+    require(h && event_out, "actor_step_event: null argument");
+    *event_out = h->a->step_event();
+  });
+}
+
+int pqlg_actor_wait_event(pqlg_actor h, void* event) {
+  return guarded([&] {
+    require(h && event, "actor_wait_event: null argument");
+    PQLG_CUDA(cudaStreamWaitEvent(h->a->stream(), static_cast<cudaEvent_t>(event), 0));
   });
 }
 

@@ -29,6 +29,8 @@ class Actor {
   void read_state(int what, void* out);
   int64_t policy_version() const { return version_; }
   cudaStream_t stream() const { return stream_; }
+  // recorded on the actor's stream after every rollout_step (null before the first)
+  cudaEvent_t step_event() const { return step_done_; }
   int kernels_per_step();
   int n_envs() const { return N_; }
   int obs_dim() const { return D_; }
@@ -56,6 +58,7 @@ class Actor {
   int N_, D_, A_, Ap_, H_, nh_;
   bool sac_ = false;            // pql_sac: Gaussian policy, no schedule noise
   pqlg_comm_s* comm_ = nullptr; // sharded: normalizer merged across shards
+  cudaEvent_t step_done_ = nullptr;
   DevBuf<double> nbatch_, ngather_;
   mlp::HeadSplit head_split_;   // pql_sac: split-K [mean | log_std] head
   int64_t Dp_;

@@ -743,6 +743,10 @@ float PLearner::log_alpha() {
 // ------------------------------------------------------------------ C ABI
 struct pqlg_plearner_s {
   std::unique_ptr<pqlg::PLearner> p;
+  cudaEvent_t ev = nullptr;  // record_event
+  ~pqlg_plearner_s() {
+    if (ev) cudaEventDestroy(ev);
+  }
 };
 
 namespace pqlg {
@@ -776,6 +780,22 @@ int pqlg_plearner_create_dp(const pqlg_config* cfg, const pqlg_task_dims* dims,
     h->p = std::make_unique<PLearner>(*cfg, *dims, init_rng_seed,
                                       static_cast<cudaStream_t>(stream), comm);
     *out = h.release();
+  });
+}
+
+int pqlg_plearner_wait_event(pqlg_plearner h, void* event) {
+  return guarded([&] {
+    require(h && event, "plearner_wait_event: null argument");
+    PQLG_CUDA(cudaStreamWaitEvent(h->p->stream(), static_cast<cudaEvent_t>(event), 0));
+  });
+}
+
+int pqlg_plearner_record_event(pqlg_plearner h, void** event_out) {
+  return guarded([&] {
+    require(h && event_out, "plearner_record_event: null argument");
+    if (!h->ev) PQLG_CUDA(cudaEventCreateWithFlags(&h->ev, cudaEventDisableTiming));
+    PQLG_CUDA(cudaEventRecord(h->ev, h->p->stream()));
+    *event_out = h->ev;
   });
 }
 

@@ -800,6 +800,10 @@ void VLearner::debug_read(int what, float* out) {
 struct pqlg_vlearner_s {
   std::unique_ptr<pqlg::VLearner> v;
   pqlg_replay_s replay_view;
+  cudaEvent_t ev = nullptr;  // record_event
+  ~pqlg_vlearner_s() {
+    if (ev) cudaEventDestroy(ev);
+  }
 };
 
 namespace pqlg {
@@ -864,6 +868,22 @@ int pqlg_vlearner_create_dp(const pqlg_config* cfg, const pqlg_task_dims* dims,
     h->replay_view.r = h->v->replay();
     h->replay_view.norm.init(dims->obs_dim);
     *out = h.release();
+  });
+}
+
+int pqlg_vlearner_wait_event(pqlg_vlearner h, void* event) {
+  return guarded([&] {
+    require(h && event, "vlearner_wait_event: null argument");
+    PQLG_CUDA(cudaStreamWaitEvent(h->v->stream(), static_cast<cudaEvent_t>(event), 0));
+  });
+}
+
+int pqlg_vlearner_record_event(pqlg_vlearner h, void** event_out) {
+  return guarded([&] {
+    require(h && event_out, "vlearner_record_event: null argument");
+    if (!h->ev) PQLG_CUDA(cudaEventCreateWithFlags(&h->ev, cudaEventDisableTiming));
+    PQLG_CUDA(cudaEventRecord(h->ev, h->v->stream()));
+    *event_out = h->ev;
   });
 }
 

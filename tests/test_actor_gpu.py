@@ -182,3 +182,52 @@ def test_rollout_steps_vs_oracle(cfg):
     assert np.all(np.abs(mean - o.mean) <= 1e-3 * std)
     np.testing.assert_allclose(m2, o.m2, rtol=2e-3)
     _lib.call("pqlg_actor_destroy", h)
+
+
+def test_cross_stream_ingest_ordered_by_exported_events():
+    """Actor and V-learner on different streams, ordered only by the ABI's
+    events (pqlg_actor_step_event -> pqlg_vlearner_wait_event, and
+    pqlg_vlearner_record_event -> pqlg_actor_wait_event): the replay ring
+    equals the one built with everything on one stream."""
+    import torch
+    N, D, A, steps = 1024, 23, 6, 9
+    cfg = _lib.default_config(n_envs=N, hidden=64, hidden_layers=2, batch_size=256,
+                              buffer_capacity=20000, seed=2, max_episode_len=5)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+
+    def run(shared):
+        s0 = torch.cuda.Stream()
+        s1 = s0 if shared else torch.cuda.Stream()
+        act, vl = C.c_void_p(), C.c_void_p()
+        _lib.call("pqlg_actor_create", C.byref(cfg), C.byref(dims), C.c_void_p(s0.cuda_stream),
+                  C.byref(act))
+        _lib.call("pqlg_vlearner_create", C.byref(cfg), C.byref(dims), 1,
+                  C.c_void_p(s1.cuda_stream), C.byref(vl))
+        sl = _lib.StepSlice()
+        for _ in range(steps):
+            _lib.call("pqlg_actor_rollout_step", act, C.byref(sl))
+            if not shared:
+                ev = C.c_void_p()
+                _lib.call("pqlg_actor_step_event", act, C.byref(ev))
+                _lib.call("pqlg_vlearner_wait_event", vl, ev)
+            _lib.call("pqlg_vlearner_ingest", vl, C.byref(sl))
+            if not shared:
+                ev2 = C.c_void_p()
+                _lib.call("pqlg_vlearner_record_event", vl, C.byref(ev2))
+                _lib.call("pqlg_actor_wait_event", act, ev2)
+        rp = C.c_void_p()
+        _lib.call("pqlg_vlearner_replay", vl, C.byref(rp))
+        n = C.c_uint64()
+        _lib.call("pqlg_replay_size", rp, C.byref(n))
+        out = [np.zeros((n.value, D), np.float32), np.zeros((n.value, A), np.float32),
+               np.zeros((n.value, D), np.float32), np.zeros(n.value, np.float32),
+               np.zeros(n.value, np.float32)]
+        _lib.call("pqlg_replay_read_rows", rp, 0, n.value, *(ptr(x) for x in out))
+        for h, fn in ((act, "pqlg_actor_destroy"), (vl, "pqlg_vlearner_destroy")):
+            _lib.call(fn, h)
+        return out
+
+    a, b = run(True), run(False)
+    assert a[3].size > 0
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)

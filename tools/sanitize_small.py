@@ -23,6 +23,10 @@ for algo in (_lib.ALGO_DDPG, _lib.ALGO_C51, _lib.ALGO_SAC):
     s = _lib.StepSlice()
     for _ in range(8):
         _lib.call("pqlg_actor_rollout_step", act, C.byref(s))
+        ev = C.c_void_p()
+        _lib.call("pqlg_actor_step_event", act, C.byref(ev))
+        _lib.call("pqlg_vlearner_wait_event", vl, ev)
+        _lib.call("pqlg_plearner_wait_event", pl, ev)
         _lib.call("pqlg_vlearner_ingest", vl, C.byref(s))
         _lib.call("pqlg_plearner_ingest", pl, s.obs, s.ld_obs, N)
     loss = C.c_float()
