@@ -295,7 +295,7 @@ void Actor::enqueue(int cur) {
   // the next policy input apply(stats_t, obs_{t+1}) directly.
   actor::NormState ns{count_.p, mean_.p, m2_.p, mean_f_.p, inv_f_.p, identity_.p,
                       comm_ ? nbatch_.p : nullptr};
-  launch(actor::norm_update_kernel, dim3(dim3((D + 31) / 32, actor::kNormGroups)), dim3(256), 0, st, obs, Dp_, N, D, npart_.p, nticket_.p, ns);
+  launch(actor::norm_update_kernel, dim3(dim3((D + 31) / 32, actor::norm_groups(D))), dim3(256), 0, st, obs, Dp_, N, D, npart_.p, nticket_.p, ns);
   if (comm_) {
     // sharded: every shard's batch statistics, merged in rank
     // order into identical running stats on all shards (5 KB at config 3)
@@ -702,7 +702,7 @@ int pqlg_k_normalizer_update(int64_t* count_dev, double* mean_dev, double* m2_de
     DevBuf<unsigned int> ticket(actor::norm_tickets(dim));
     const int64_t ldx = ld > 0 ? ld : dim;
     actor::NormState ns{count_dev, mean_dev, m2_dev, mean_f_dev, inv_f_dev, ident.p};
-    launch(actor::norm_update_kernel, dim3(dim3((dim + 31) / 32, actor::kNormGroups)), dim3(256), 0, st, batch_dev, ldx, rows, dim, part.p, ticket.p, ns);
+    launch(actor::norm_update_kernel, dim3(dim3((dim + 31) / 32, actor::norm_groups(dim))), dim3(256), 0, st, batch_dev, ldx, rows, dim, part.p, ticket.p, ns);
     PQLG_CUDA(cudaStreamSynchronize(st));
   });
 }

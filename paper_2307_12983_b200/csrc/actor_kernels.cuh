@@ -397,7 +397,15 @@ __device__ __forceinline__ void chan_merge(double na, double& mean, double& m2, 
 // merges it into the running stats with Chan's formula and refreshes the
 // fp32 apply constants (normalizer.hpp:62-66); the last strip to finish
 // advances the count.
-constexpr int kNormGroups = 128;
+constexpr int kNormGroups = 128;  // upper bound (partials buffer)
+// row groups so the (strips x groups) grid is one wave at 4 blocks per SM
+inline int norm_groups(int D) {
+  const int strips = (D + 31) / 32;
+  int g = 4 * 148 / strips;
+  if (g > kNormGroups) g = kNormGroups;
+  if (g < 1) g = 1;
+  return g;
+}
 constexpr int kNormRowsPerWarp = 16;  // rows per warp per group (N <= 8*16*kNormGroups in one pass)
 static __global__ void __launch_bounds__(256, 4)
     norm_update_kernel(const float* __restrict__ x, int64_t ldx, int N, int D, double* partial,
