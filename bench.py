@@ -259,7 +259,7 @@ def run_ours(args, rank, world, local):
 
     # ---- roofline of the dominant kernel: the 4-group hidden-layer GEMM (twin
     # target + twin online critics, one persistent launch per layer; 3 of the
-    # update's 17 launches and its largest single kernel), CUDA events on the
+    # update's 18 launches and its largest single kernel), CUDA events on the
     # stream the kernel is launched on.  The lone 1-group layer (the target
     # policy's) is reported beside it.
     roof = None
