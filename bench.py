@@ -366,6 +366,53 @@ def run_c51(args, rank, world, local, steps, warmup, sac=False):
     return out
 
 
+def run_other_config(args, rank, world, local, name, steps, warmup):
+    """Critic updates/s and actor steps/s (rollout only, graph replay) at
+    another BASELINE config (c2: Ant-like dims, 4096 envs; c1: the
+    reference's CPU case), same kernels, synthetic replay fill."""
+    import torch
+    from paper_2307_12983_b200 import _lib
+    D, A, H, nh, B, N, cap = CONFIGS[name]
+    stream = torch.cuda.Stream(device=local)
+    sp = C.c_void_p(stream.cuda_stream)
+    cap = min(cap, 1_000_000)
+    cfg = _lib.default_config(batch_size=B, buffer_capacity=cap, hidden=H, hidden_layers=nh,
+                              n_envs=N, seed=0, env_offset=rank * N, envs_total=world * N)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    vl, act = C.c_void_p(), C.c_void_p()
+    comm = _lib.comm_from_torch_dist(rank, world) if world > 1 else None
+    if comm is not None:
+        _lib.call("pqlg_vlearner_create_dp", C.byref(cfg), C.byref(dims), 1, comm, sp, C.byref(vl))
+        _lib.call("pqlg_actor_create_sharded", C.byref(cfg), C.byref(dims), comm, sp, C.byref(act))
+    else:
+        _lib.call("pqlg_vlearner_create", C.byref(cfg), C.byref(dims), 1, sp, C.byref(vl))
+        _lib.call("pqlg_actor_create", C.byref(cfg), C.byref(dims), sp, C.byref(act))
+    rp = C.c_void_p()
+    _lib.call("pqlg_vlearner_replay", vl, C.byref(rp))
+    _lib.call("pqlg_replay_fill_synthetic", rp, cap, 3000 + rank, np.float32(0.970299), 200)
+    out = {"workload": f"{name}: obs {D} / act {A}, {nh}x{H} MLPs, batch {B}, {N} envs per GPU"}
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for key, h, fn, unit, per in (("critic_updates", vl, "pqlg_vlearner_update_n", "updates/s", 1),
+                                  ("actor_transitions", act, "pqlg_actor_rollout_n",
+                                   "transitions/s", N)):
+        _lib.call(fn, h, warmup)
+        stream.synchronize()
+        barrier(world)
+        ev0.record(stream)
+        _lib.call(fn, h, steps)
+        ev1.record(stream)
+        ev1.synchronize()
+        ms = max_over_ranks(ev0.elapsed_time(ev1), world)
+        out[key] = {"value": world * per * steps / (ms * 1e-3), "unit": unit,
+                    "ms_per_step": ms / steps}
+    out["actor_transitions"]["note"] = "rollout_step only (no ingest)"
+    _lib.call("pqlg_vlearner_destroy", vl)
+    _lib.call("pqlg_actor_destroy", act)
+    if comm is not None:
+        _lib.call("pqlg_comm_destroy", comm)
+    return out
+
+
 def run_pipeline(args, rank, world, local, actor_steps):
     """run_parallel on this GPU: Actor, V-learner and
     P-learner as three threads on three streams, RatioGate pacing at the
@@ -677,6 +724,9 @@ def main():
     sac = run_c51(args, rank, world, local, max(10, args.steps // 2), max(3, args.warmup // 2),
                   sac=True)
     pipe = run_pipeline(args, rank, world, local, 400)
+    others = {c: run_other_config(args, rank, world, local, c, max(20, args.steps // 2),
+                                  max(3, args.warmup // 2))
+              for c in ("c2", "c1") if c != args.config}
     if rank != 0:
         return
     out = dict(base)
@@ -685,6 +735,7 @@ def main():
     out["c51"] = c51
     out["sac"] = sac
     out["run_parallel"] = pipe
+    out["other_configs"] = others
     out.update(value=r["value"], ms_per_step=r["ms_step"], e2e=r["e2e"], roofline=r["roof"],
                clocks=r["clocks"], gpu_launches=r["launches"],
                kernels_per_update=r["kpu"], last_loss=r["loss"])
