@@ -53,6 +53,34 @@ struct EpsStream {
     launch(sac::eps_emit_kernel, dim3(blocks), dim3(sac::kEpsThreads), 0, s, a);
   }
 
+  // The draws depend on nothing but the stream's own counter: fork them onto
+  // a side stream (a parallel branch of the captured update graph) so they
+  // run beside the sample and the policy GEMMs; join() before the consumer.
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  void fork(cudaStream_t main) {
+    if (!side) {
+      PQLG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      PQLG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      PQLG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    PQLG_CUDA(cudaEventRecord(ev_fork, main));
+    PQLG_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    enqueue(side);
+    PQLG_CUDA(cudaEventRecord(ev_join, side));
+  }
+  void join(cudaStream_t main) const {
+    if (ev_join) PQLG_CUDA(cudaStreamWaitEvent(main, ev_join, 0));
+  }
+  ~EpsStream() {
+    if (side) {
+      cudaStreamSynchronize(side);
+      cudaStreamDestroy(side);
+      cudaEventDestroy(ev_fork);
+      cudaEventDestroy(ev_join);
+    }
+  }
+
   // the reference's sequential stream (learners.cpp:171-173)
   void fill_mt(cudaStream_t s) {
     std::normal_distribution<float> gauss(0.0f, 1.0f);

@@ -196,7 +196,7 @@ void VLearner::build_update() {
     logp_.alloc(B);
     steps_.push_back([this](cudaStream_t st) {
       if (mt_mode_) eps_.fill_mt(st);
-      else eps_.enqueue(st);
+      else eps_.fork(st);  // parallel branch, joined before the sampling finish
     });
   }
 
@@ -233,6 +233,7 @@ void VLearner::build_update() {
       g.logp = logp_.p;
       g.mid = (dims_.low + dims_.high) / 2.0f;
       g.half = (dims_.high - dims_.low) / 2.0f;
+      steps_.push_back([this](cudaStream_t st) { eps_.join(st); });
       steps_.push_back(gauss_finish_step(head_split_, g, B, A));
     } else {
       head::FinishArgs ph{};
