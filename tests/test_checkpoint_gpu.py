@@ -105,3 +105,41 @@ def test_plearner_save_load_round_trip(tmp_path):
         _lib.call("pqlg_plearner_load", c, path)
     for h in (a, b, c):
         _lib.call("pqlg_plearner_destroy", h)
+
+
+def test_sac_learners_and_actor_round_trip(tmp_path):
+    """pql_sac cores checkpoint their GaussianPolicy nets (2 x act_dim
+    outputs) in the same format; log alpha is not part of the reference's
+    checkpoint (checkpoint.hpp:11-21) and is left untouched."""
+    cfg = _lib.default_config(algo=_lib.ALGO_SAC, batch_size=64, buffer_capacity=2000, hidden=H,
+                              hidden_layers=nh, n_envs=16)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    Pp = param_count([D] + [H] * nh + [2 * A])
+    pa, pb = C.c_void_p(), C.c_void_p()
+    _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 3, None, C.byref(pa))
+    _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 4, None, C.byref(pb))
+    import torch
+    s = torch.randn(500, D, device="cuda")
+    _lib.call("pqlg_plearner_ingest", pa, s.data_ptr(), D, 500)
+    _lib.call("pqlg_plearner_update_n", pa, 2)
+    path = str(tmp_path / "p.ckpt").encode()
+    _lib.call("pqlg_plearner_save", pa, path)
+    _lib.call("pqlg_plearner_load", pb, path)
+    x, y = np.zeros(Pp, np.float32), np.zeros(Pp, np.float32)
+    _lib.call("pqlg_plearner_get_params", pa, 0, ptr(x))
+    _lib.call("pqlg_plearner_get_params", pb, 0, ptr(y))
+    assert np.array_equal(x, y)
+    la, lb = C.c_float(), C.c_float()
+    _lib.call("pqlg_plearner_log_alpha", pa, C.byref(la))
+    _lib.call("pqlg_plearner_log_alpha", pb, C.byref(lb))
+    assert la.value != 0.0 and lb.value == 0.0
+    # the actor loads the policy net of the P-learner's file
+    act = C.c_void_p()
+    _lib.call("pqlg_actor_create", C.byref(cfg), C.byref(dims), None, C.byref(act))
+    _lib.call("pqlg_actor_load", act, path)
+    z = np.zeros(Pp, np.float32)
+    _lib.call("pqlg_actor_read", act, 5, ptr(z))
+    assert np.array_equal(z, x)
+    for h, fn in ((pa, "pqlg_plearner_destroy"), (pb, "pqlg_plearner_destroy"),
+                  (act, "pqlg_actor_destroy")):
+        _lib.call(fn, h)
