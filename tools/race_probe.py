@@ -1,3 +1,6 @@
+"""Checksums of the actor, V-learner and P-learner state after a few eager
+steps (GPU box): run once plainly and once under `compute-sanitizer --tool
+racecheck` and diff the outputs (the tools must not change the results)."""
 import ctypes as C, os, sys, numpy as np
 os.environ["PQLG_EAGER"] = "1"
 sys.path.insert(0, os.getcwd())
