@@ -200,3 +200,36 @@ def test_c51_rejects_bad_support():
     h = C.c_void_p()
     with pytest.raises(ValueError):
         _lib.call("pqlg_vlearner_create", C.byref(cfg), C.byref(dims), 1, None, C.byref(h))
+
+
+@pytest.mark.parametrize("L", [2, 33, 64])
+def test_c51_atom_count_edges_vs_oracle(L):
+    """The categorical head at the smallest support (2 atoms), a ragged one
+    (33: two 32-column chunks, the second nearly empty) and the largest the
+    kernels take (64): one critic update vs the oracle."""
+    D, A, H, nh, B, n = 12, 3, 64, 2, 256, 3000
+    rng = np.random.default_rng(40 + L)
+    h = make_vl(D, A, H, nh, B, n, L)
+    P = param_count([D + A] + [H] * nh + [L])
+    q1, q2 = params(h, 0, P), params(h, 1, P)
+    pol = params(h, 4, param_count([D] + [H] * nh + [A]))
+    obs, act, boot, ret, eff = random_rows(rng, n, D, A)
+    ret = f32(ret * 20.0)
+    insert_rows(h, obs, act, boot, ret, eff)
+    _lib.call("pqlg_vlearner_set_sampler", h, _lib.RNG_INDICES)
+    o = OracleVUpdate(D, A, H, nh, B, q1, q2, pol, seed=0, distributional=True, n_atoms=L)
+    o.set_rows(obs, act, boot, ret, eff)
+    loss_o, info = o.step()
+    l = C.c_float()
+    _lib.call("pqlg_vlearner_update", h, C.byref(l))
+    g = np.zeros(2 * P, np.float32)
+    _lib.call("pqlg_vlearner_debug_read", h, 2, ptr(g))
+    sc = np.zeros(2, np.float32)
+    _lib.call("pqlg_vlearner_debug_read", h, 3, ptr(sc))
+    r = [rel(g[k * P:(k + 1) * P] * sc[k], info["dq"][k]) for k in range(2)]
+    print(f"\nL={L}: loss gpu={l.value:.6f} oracle={loss_o:.6f} g_rel={r}")
+    assert abs(l.value - loss_o) <= 2e-3 * abs(loss_o)
+    assert max(r) <= 1e-2
+    for w, want in enumerate([o.q[0], o.q[1], o.qt[0], o.qt[1]]):
+        check_weights(params(h, w, P), want, 5e-4, 1)
+    _lib.call("pqlg_vlearner_destroy", h)
