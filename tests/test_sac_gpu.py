@@ -61,7 +61,7 @@ def v_adopt(h, pol, log_alpha, version=1):
     _lib.call("pqlg_vlearner_adopt_policy_sac", h, ptr(f32(pol)), np.float32(log_alpha), version)
 
 
-@pytest.mark.parametrize("B,A", [(64, 3), (1024, 8), (8192, 20)])
+@pytest.mark.parametrize("B,A", [(64, 3), (1024, 8), (8192, 20), (1, 1), (37, 32)])
 def test_eps_stream_bit_exact_and_counter_advance(B, A):
     """The device's parallel polar draws equal the sequential
     normal_distribution over the same Philox URBG (orc_normals, kind 1), for
@@ -269,7 +269,8 @@ def test_sac_graph_replay_philox_vs_oracle():
     _lib.call("pqlg_plearner_destroy", hp)
 
 
-@pytest.mark.parametrize("N,D,A", [(40, 9, 4), (4096, 211, 20), (300, 17, 7)])
+@pytest.mark.parametrize("N,D,A", [(40, 9, 4), (4096, 211, 20), (300, 17, 7), (64, 7, 1),
+                                   (96, 40, 32)])
 def test_sac_actor_step_vs_oracle(N, D, A):
     """ActorCore::rollout_step for pql_sac: the per-env eps draws (fresh
     normal_distribution over the noise streams) bit-exact -- checked through
