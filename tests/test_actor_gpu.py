@@ -231,3 +231,33 @@ def test_cross_stream_ingest_ordered_by_exported_events():
     assert a[3].size > 0
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_zero_sigma_rows_draw_no_noise():
+    """build_fixed_schedule(0) (noise.hpp:44-50): sigma = 0 on every env, so
+    apply_noise draws nothing -- the noise streams do not advance and the
+    actions are the squashed policy output (clamped)."""
+    N, D, A, H, nh = 256, 11, 4, 64, 2
+    conf = _lib.default_config(n_envs=N, hidden=H, hidden_layers=nh, seed=6, sigma_fixed=0.0)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    h = C.c_void_p()
+    _lib.call("pqlg_actor_create", C.byref(conf), C.byref(dims), None, C.byref(h))
+    ps = [D] + [H] * nh + [A]
+    pol = np.zeros(param_count(ps), np.float32)
+    _lib.call("pqlg_actor_read", h, 5, ptr(pol))
+    obs0 = np.zeros((N, D), np.float32)
+    _lib.call("pqlg_actor_read", h, 0, ptr(obs0))
+    ns0 = np.zeros(N, np.uint64)
+    _lib.call("pqlg_actor_read", h, 2, ptr(ns0))
+    sl = _lib.StepSlice()
+    _lib.call("pqlg_actor_rollout_step", h, C.byref(sl))
+    act = np.zeros((N, A), np.float32)
+    _lib.call("pqlg_actor_read", h, 1, ptr(act))
+    ns1 = np.zeros(N, np.uint64)
+    _lib.call("pqlg_actor_read", h, 2, ptr(ns1))
+    np.testing.assert_array_equal(ns0, ns1)
+    want = np.zeros((N, A), np.float32)
+    orc().orc_policy_act(ptr(pol), ptr(np.asarray(ps, np.uintp)), nh + 1, ptr(obs0), N,
+                         np.float32(-1), np.float32(1), ptr(want))
+    assert np.max(np.abs(act - want)) <= 2e-3
+    _lib.call("pqlg_actor_destroy", h)
