@@ -136,3 +136,14 @@ def test_run_synchronous_deterministic_and_paced(tmp_path, algo):
     assert r0.c_p == int(rc.beta_pv * r0.c_v)
     assert r0.policy_version == r0.c_p // rc.publish_every
     assert r0.critic_version == r0.c_v // rc.publish_every
+
+
+def test_pipeline_nonfinite_update_aborts_the_run():
+    """SPEC.md:461 (child fault -> propagate): a critic update that turns
+    non-finite stops every thread and run() reports PQLG_ENONFINITE."""
+    cfg = _lib.default_config(n_envs=128, batch_size=256, buffer_capacity=50_000, hidden=32,
+                              hidden_layers=2, seed=2, lr_critic=1e30, lr_actor=1e30)
+    dims = _lib.TaskDims(9, 3, -1.0, 1.0)
+    rc = _lib.ratio_config()
+    with pytest.raises(_lib.NonFinite):
+        run_pipeline(cfg, dims, rc, 2000, seconds=30.0)
