@@ -147,3 +147,30 @@ def test_pipeline_nonfinite_update_aborts_the_run():
     rc = _lib.ratio_config()
     with pytest.raises(_lib.NonFinite):
         run_pipeline(cfg, dims, rc, 2000, seconds=30.0)
+
+
+def test_run_synchronous_nonfinite_update_raises():
+    cfg = _lib.default_config(n_envs=128, batch_size=256, buffer_capacity=50_000, hidden=32,
+                              hidden_layers=2, seed=2, lr_critic=1e30, lr_actor=1e30)
+    dims = _lib.TaskDims(9, 3, -1.0, 1.0)
+    rc = _lib.ratio_config()
+    rep = _lib.RunReport()
+    with pytest.raises(_lib.NonFinite):
+        _lib.call("pqlg_run_synchronous", C.byref(cfg), C.byref(dims), C.byref(rc), 1, 400, None,
+                  C.byref(rep))
+
+
+def test_pipeline_time_budget_shutdown_joins_promptly():
+    """SPEC.md:464 (deterministic shutdown): a run stopped by its wall-clock
+    budget joins all threads within 5 s and still consumed every batch."""
+    import time
+    cfg = _lib.default_config(n_envs=512, batch_size=512, buffer_capacity=200_000, hidden=64,
+                              hidden_layers=2, seed=3)
+    dims = _lib.TaskDims(17, 6, -1.0, 1.0)
+    rc = _lib.ratio_config()
+    t0 = time.perf_counter()
+    r = run_pipeline(cfg, dims, rc, 10**9, seconds=1.0)
+    dt = time.perf_counter() - t0
+    print(f"\nstopped after {r.wall_s:.2f}s (call {dt:.2f}s), c_a={r.c_a}")
+    assert r.ok == 1 and r.wall_s < 5.0
+    assert r.batches_consumed_v == r.batches_sent == r.batches_consumed_p
