@@ -190,6 +190,13 @@ PQLG_API int pqlg_states_sample(pqlg_states h, uint64_t batch, pqlg_rng* rng, ui
  * pqlg_vlearner_adopt_policy_sac installs both in the V-learner, and the
  * run_parallel pipeline moves them together on the device. */
 enum { PQLG_ALGO_DDPG = 0, PQLG_ALGO_C51 = 1, PQLG_ALGO_SAC = 2 };
+/* GEMM precision of the MLP layers (the reference computes them in fp32,
+ * scalar.hpp:12-55).  TF32: operands rounded to tf32 (10-bit mantissa), one
+ * tcgen05 MMA per K step -- the speed mode.  3XTF32: each operand split into
+ * tf32 hi + lo parts in shared memory and a_lo*b_hi + a_hi*b_lo + a_hi*b_hi
+ * accumulated in fp32 -- products within a few fp32 ulps, 3x the MMA work;
+ * the parity mode. */
+enum { PQLG_PREC_TF32 = 0, PQLG_PREC_3XTF32 = 1 };
 typedef struct {
   int algo;               /* PQLG_ALGO_DDPG (pql_ddpg), PQLG_ALGO_C51 (pql_d), PQLG_ALGO_SAC (pql_sac) */
   int n_envs;
@@ -214,6 +221,7 @@ typedef struct {
   int max_episode_len;    /* synthetic env time limit */
   int env_offset;         /* global index of this shard's first env (sharded actors) */
   int envs_total;         /* global env count of a sharded actor (0: n_envs)          */
+  int precision;          /* PQLG_PREC_TF32 (speed) or PQLG_PREC_3XTF32 (fp32-faithful) */
 } pqlg_config;
 
 /* TaskDims (learners.hpp:23-26) */
@@ -447,6 +455,13 @@ PQLG_API int pqlg_pipeline_create(const pqlg_config* cfg, const pqlg_task_dims* 
 PQLG_API int pqlg_pipeline_run(pqlg_pipeline h, int64_t actor_steps, double max_seconds,
                                pqlg_run_report* out);
 PQLG_API int pqlg_pipeline_destroy(pqlg_pipeline h);
+/* Test hooks for the snapshot exchange: before run, record a host copy of
+ * every critic snapshot the V-learner publishes; after run, the P-learner's
+ * critic replicas vs the snapshot published under the version it holds
+ * (*max_abs_diff = 0 when they are that snapshot; -1 when it holds none). */
+PQLG_API int pqlg_pipeline_record_snapshots(pqlg_pipeline h, int on);
+PQLG_API int pqlg_pipeline_check_critics(pqlg_pipeline h, int64_t* p_version,
+                                         double* max_abs_diff);
 
 /* ------------------------------------------------------------ metrics CSV
  * MetricsRow / MetricsWriter (metrics.hpp:9-32, metrics.cpp:8-29):

@@ -42,6 +42,7 @@ class Rng(C.Structure):
 
 RNG_PHILOX, RNG_INDICES = 0, 1
 ALGO_DDPG, ALGO_C51, ALGO_SAC = 0, 1, 2
+PREC_TF32, PREC_3XTF32 = 0, 1
 P = C.POINTER
 
 
@@ -52,7 +53,8 @@ class Config(C.Structure):
                 ("lr_critic", f64), ("warm_up", i64), ("sigma_min", f64), ("sigma_max", f64),
                 ("sigma_fixed", f64), ("reward_scale", f64), ("seed", u64), ("hidden", i32),
                 ("hidden_layers", i32), ("n_atoms", i32), ("vmin", f64), ("vmax", f64),
-                ("max_episode_len", i32), ("env_offset", i32), ("envs_total", i32)]
+                ("max_episode_len", i32), ("env_offset", i32), ("envs_total", i32),
+                ("precision", i32)]
 
 
 class TaskDims(C.Structure):
@@ -200,6 +202,8 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_pipeline_create": (i32, [P(Config), P(TaskDims), P(RatioConfig), u64, P(vp)]),
     "pqlg_pipeline_run": (i32, [vp, i64, C.c_double, P(RunReport)]),
     "pqlg_pipeline_destroy": (i32, [vp]),
+    "pqlg_pipeline_record_snapshots": (i32, [vp, i32]),
+    "pqlg_pipeline_check_critics": (i32, [vp, P(i64), P(C.c_double)]),
     "pqlg_pipeline_set_metrics": (i32, [vp, P(MetricsConfig)]),
     "pqlg_run_synchronous": (i32, [P(Config), P(TaskDims), P(RatioConfig), u64, i64,
                                    P(MetricsConfig), P(RunReport)]),

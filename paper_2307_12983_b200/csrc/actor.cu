@@ -119,6 +119,8 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
     PQLG_CUDA(cudaStreamCreateWithFlags(&owned_stream_, cudaStreamNonBlocking));
     stream_ = owned_stream_;
   }
+  require(cfg.precision == PQLG_PREC_TF32 || cfg.precision == PQLG_PREC_3XTF32,
+          "actor: unknown precision");
   require(cfg.algo == PQLG_ALGO_DDPG || cfg.algo == PQLG_ALGO_C51 || cfg.algo == PQLG_ALGO_SAC,
           "actor: unknown algo");
   sac_ = cfg.algo == PQLG_ALGO_SAC;
@@ -205,7 +207,10 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
   launch(actor::normalize_kernel, dim3(4 * mlp::kSMs), dim3(256), 0, stream_, obs_[0].p, Dp_, Xn_.p, Dp_,
                                                                mean_f_.p, inv_f_.p, identity_.p,
                                                                N_, D_);
-  build();
+  {
+    gemm::PrecisionScope prec(cfg.precision == PQLG_PREC_3XTF32);
+    build();
+  }
   PQLG_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -444,6 +449,9 @@ void evaluate_policy(const pqlg_config& cfg, const pqlg_task_dims& dims, const f
   const int N = episodes, D = dims.obs_dim, A = dims.act_dim, H = cfg.hidden;
   const int nh = cfg.hidden_layers;
   require(A <= 32, "evaluate: act_dim > 32 not supported");
+  require(cfg.precision == PQLG_PREC_TF32 || cfg.precision == PQLG_PREC_3XTF32,
+          "evaluate: unknown precision");
+  gemm::PrecisionScope prec(cfg.precision == PQLG_PREC_3XTF32);
   cudaStream_t st;
   PQLG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   struct StreamGuard {

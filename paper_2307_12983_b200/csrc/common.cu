@@ -117,7 +117,7 @@ bool pdl_enabled() {
 
 extern "C" {
 const char* pqlg_last_error(void) { return pqlg::g_last_error.c_str(); }
-int pqlg_abi_version(void) { return 1; }
+int pqlg_abi_version(void) { return 2; }  // 2: pqlg_config::precision
 uint64_t pqlg_launch_count(void) { return pqlg::g_launches.load(); }
 }
 

@@ -9,6 +9,23 @@
 
 namespace pqlg::gemm {
 
+// GEMM precision of the closures built on this thread: the cores' constructors
+// set it from pqlg_config::precision for the duration of their plan building.
+//   TF32   operand maps typed TFLOAT32 (TMA rounds to nearest), one MMA per K step
+//   3xTF32 operand maps FLOAT32, hi/lo split in shared memory, three MMAs per K
+//          step (fp32-faithful parity mode; gemm_tf32.cuh)
+inline thread_local bool t_build_x3 = false;
+struct PrecisionScope {
+  bool prev;
+  explicit PrecisionScope(bool x3) : prev(t_build_x3) { t_build_x3 = x3; }
+  ~PrecisionScope() { t_build_x3 = prev; }
+  PrecisionScope(const PrecisionScope&) = delete;
+  PrecisionScope& operator=(const PrecisionScope&) = delete;
+};
+inline bool build_x3() { return t_build_x3; }
+// Operand maps of the current build precision (TFLOAT32 unless 3xTF32).
+inline bool tf32_maps() { return !t_build_x3; }
+
 // A operand. mn = false: A is [M x K] row-major (stride lda >= K).
 //            mn = true:  A is stored [K x M] row-major (stride lda >= M).
 inline CUtensorMap map_a(const float* A, int M, int K, int lda, bool mn, bool tf32 = false) {
@@ -67,10 +84,10 @@ inline int b_box(int M) {
   return use_pair<BN>(M) ? BN / 2 : BN;
 }
 
-template <int BN, bool kAMN, bool kBMN, class Epi, bool kPair>
+template <int BN, bool kAMN, bool kBMN, class Epi, bool kPair, bool k3x>
 void launch_impl(const Operands& ops, Problem p, int groups, const Epi& epi, cudaStream_t st) {
-  using L = SmemLayout<BN, Epi, kPair>;
-  auto kern = gemm_tf32_kernel<BN, kAMN, kBMN, Epi, kPair>;
+  using L = SmemLayout<BN, Epi, kPair, k3x>;
+  auto kern = gemm_tf32_kernel<BN, kAMN, kBMN, Epi, kPair, k3x>;
   static bool configured = false;
   if (!configured) {
     PQLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -109,13 +126,23 @@ void launch_impl(const Operands& ops, Problem p, int groups, const Epi& epi, cud
 }
 
 // Persistent launch: min(tiles, SMs) CTAs, one per SM, walking the tiles
-// (or, for CTA pairs, clusters of 2 walking m-tile pairs).
+// (or, for CTA pairs, clusters of 2 walking m-tile pairs).  x3: the 3xTF32
+// variant (the operand maps must then be FLOAT32-typed).
 template <int BN, bool kAMN, bool kBMN, class Epi>
-void launch(const Operands& ops, Problem p, int groups, const Epi& epi, cudaStream_t st) {
-  if constexpr (BN >= 128) {
-    if (use_pair<BN>(p.M)) return launch_impl<BN, kAMN, kBMN, Epi, true>(ops, p, groups, epi, st);
+void launch(const Operands& ops, Problem p, int groups, const Epi& epi, cudaStream_t st,
+            bool x3 = false) {
+  if (x3) {
+    if constexpr (BN >= 128) {
+      if (use_pair<BN>(p.M))
+        return launch_impl<BN, kAMN, kBMN, Epi, true, true>(ops, p, groups, epi, st);
+    }
+    return launch_impl<BN, kAMN, kBMN, Epi, false, true>(ops, p, groups, epi, st);
   }
-  launch_impl<BN, kAMN, kBMN, Epi, false>(ops, p, groups, epi, st);
+  if constexpr (BN >= 128) {
+    if (use_pair<BN>(p.M))
+      return launch_impl<BN, kAMN, kBMN, Epi, true, false>(ops, p, groups, epi, st);
+  }
+  launch_impl<BN, kAMN, kBMN, Epi, false, false>(ops, p, groups, epi, st);
 }
 
 }  // namespace pqlg::gemm

@@ -29,6 +29,15 @@
 // Split-K over the z tile coordinate lets the K=8192 weight-gradient GEMMs
 // fill 148 SMs; their epilogue stores partial tiles that a fixed-order
 // reduction sums.
+//
+// k3x (the fp32-faithful "3xTF32" mode, pqlg_config::precision): operands
+// arrive as raw fp32 (FLOAT32 tensor maps), four converter warps split every
+// stage in shared memory into x_hi = rna_tf32(x) (in place) and
+// x_lo = rna_tf32(x - x_hi) (a mirror region of the stage), and the MMA warp
+// issues lo_A*hi_B + hi_A*lo_B + hi_A*hi_B per UMMA K step into the same TMEM
+// accumulator.  The representation error is ~2^-24 |x|, so products match
+// fp32 to a few ulps (the dropped lo*lo term is ~2^-22 relative) at 3x the
+// MMA work.
 #pragma once
 
 #include <cstdint>
@@ -90,30 +99,36 @@ constexpr int epi_warps() {
   return (BN >= 128 && Epi::kSplitCols) ? 8 : 4;
 }
 
+constexpr int kConvWarps = 4;  // 3xTF32 hi/lo converter warps
+
 // kPair: the tile is computed by a CTA pair (cluster of 2, tcgen05
 // cta_group::2, UMMA M = 256): each CTA stages its own 128 A rows and half of
 // the BN B columns, so per-CTA operand traffic drops from (128 + BN) to
 // (128 + BN/2) rows per k-step -- the hidden-layer GEMMs are L2-bandwidth
 // bound at 1 CTA per tile.
-template <int BN, class Epi, bool kPair = false>
+template <int BN, class Epi, bool kPair = false, bool k3x = false>
 struct SmemLayout {
   static constexpr int kEpiWarps = epi_warps<BN, Epi>();
-  static constexpr int kThreads = 64 + 32 * kEpiWarps;
+  static constexpr int kConvWarps3 = k3x ? kConvWarps : 0;
+  static constexpr int kThreads = 64 + 32 * kEpiWarps + 32 * kConvWarps3;
   static constexpr int kABytes = kBM * kBK * 4;  // 16 KB
   static constexpr int kBBytes = (kPair ? BN / 2 : BN) * kBK * 4;
-  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kLoadBytes = kABytes + kBBytes;  // TMA bytes per stage and CTA
+  // 3xTF32: [A_hi | B_hi | A_lo | B_lo] per stage
+  static constexpr int kStageBytes = k3x ? 2 * kLoadBytes : kLoadBytes;
   // one 4 KB (32 x 32 fp32, 128B-swizzled) TMA-store staging buffer per warp
   static constexpr int kStagingBytes = Epi::kStoreRank > 0 ? kEpiWarps * 4096 : 0;
   static constexpr int kFixed = kStagingBytes + kScratchBytes + 256;
   static constexpr int kFit = (kMaxDynSmem - kFixed) / kStageBytes;
   static constexpr int kStages = kFit > 8 ? 8 : kFit;
-  static_assert(kStages >= 4, "pipeline too shallow");
+  static_assert(kStages >= (k3x ? 2 : 4), "pipeline too shallow");
   static constexpr int kPipeBytes = kStages * kStageBytes;
   static constexpr int kStagingOffset = kPipeBytes;
   static constexpr int kScratchOffset = kStagingOffset + kStagingBytes;
   static constexpr int kBarOffset = kScratchOffset + kScratchBytes;
-  // full[kStages], empty[kStages], tmem_full[2], tmem_empty[2], tmem pointer
-  static constexpr int kTotal = kBarOffset + (2 * kStages + 4) * 8 + 16;
+  // full[kStages], empty[kStages], tmem_full[2], tmem_empty[2],
+  // (3xTF32) conv[kStages], tmem pointer
+  static constexpr int kTotal = kBarOffset + ((k3x ? 3 : 2) * kStages + 4) * 8 + 16;
   // the dynamic window starts 1024B-aligned (no static smem in this kernel;
   // checked at entry), so no alignment slack is reserved
   static constexpr int kDynamic = kTotal;
@@ -213,11 +228,36 @@ __device__ __forceinline__ TileCoord tile_coord(int t, const Problem& p, int til
   return c;
 }
 
-template <int BN, bool kAMN, bool kBMN, class Epi, bool kPair = false>
-__global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair>::kThreads, 1)
+// One converter pass over stage `st` (3xTF32): x -> (hi in place, lo mirror).
+template <int kLoadBytes>
+__device__ __forceinline__ void split_stage(uint8_t* st, int ct) {
+  float4* hi = reinterpret_cast<float4*>(st);
+  float4* lo = reinterpret_cast<float4*>(st + kLoadBytes);
+  constexpr int kVec = kLoadBytes / 16;
+  constexpr int kT = 32 * kConvWarps;
+  static_assert(kVec % kT == 0, "stage size");
+#pragma unroll 4
+  for (int e = ct; e < kVec; e += kT) {
+    const float4 x = hi[e];
+    float4 h, l;
+    h.x = ptx::to_tf32(x.x);
+    h.y = ptx::to_tf32(x.y);
+    h.z = ptx::to_tf32(x.z);
+    h.w = ptx::to_tf32(x.w);
+    l.x = ptx::to_tf32(__fsub_rn(x.x, h.x));
+    l.y = ptx::to_tf32(__fsub_rn(x.y, h.y));
+    l.z = ptx::to_tf32(__fsub_rn(x.z, h.z));
+    l.w = ptx::to_tf32(__fsub_rn(x.w, h.w));
+    hi[e] = h;
+    lo[e] = l;
+  }
+}
+
+template <int BN, bool kAMN, bool kBMN, class Epi, bool kPair = false, bool k3x = false>
+__global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair, k3x>::kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ Operands ops, const Problem prob,
                      const __grid_constant__ Epi epi) {
-  using L = SmemLayout<BN, Epi, kPair>;
+  using L = SmemLayout<BN, Epi, kPair, k3x>;
   constexpr int kStages = L::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -227,7 +267,8 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair>::kThreads, 1)
   uint64_t* empty = full + kStages;
   uint64_t* tmem_full = empty + kStages;   // [2]
   uint64_t* tmem_empty = tmem_full + 2;    // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* conv = tmem_empty + 2;         // [kStages] (3xTF32 only)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(conv + (k3x ? kStages : 0));
 
   const int warp = threadIdx.x >> 5;
   const int tiles_m = (prob.M + kBM - 1) / kBM;
@@ -253,6 +294,8 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair>::kThreads, 1)
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
+      // the leader's MMA waits for every converter warp of the pair
+      if constexpr (k3x) ptx::mbar_init(&conv[s], kConvWarps * (kPair ? 2 : 1));
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tmem_full[a], 1);
@@ -306,9 +349,9 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair>::kThreads, 1)
           uint8_t* sa = smem + s * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
           const int k0 = (kt0 + i) * kBK;
-          if constexpr (kPair) {
+          if constexpr (kPair && !k3x) {
             // both CTAs' bytes complete on the leader's full barrier
-            if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * L::kStageBytes);
+            if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * L::kLoadBytes);
             const uint32_t fb = ptx::mapa(&full[s], 0);
             if constexpr (kAMN) {
 #pragma unroll
@@ -325,7 +368,9 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair>::kThreads, 1)
               ptx::tma_load_2d_pair(&ops.b[tc.group], fb, sb, k0, n0);
             }
           } else {
-            ptx::mbar_arrive_expect_tx(&full[s], L::kStageBytes);
+            // (3xTF32 pairs: each CTA's bytes complete on its own barrier,
+            // where its converter warps wait)
+            ptx::mbar_arrive_expect_tx(&full[s], L::kLoadBytes);
             if constexpr (kAMN) {
 #pragma unroll
               for (int j = 0; j < kBM / 32; ++j)
@@ -336,7 +381,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair>::kThreads, 1)
             }
             if constexpr (kBMN) {
 #pragma unroll
-              for (int j = 0; j < BN / 32; ++j)
+              for (int j = 0; j < kBCols / 32; ++j)
                 ptx::tma_load_2d(&ops.b[tc.group], &full[s], sb + j * (32 * kBK * 4), n0 + 32 * j,
                                  k0);
             } else {
@@ -361,19 +406,33 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair>::kThreads, 1)
         for (int i = 0; i < nkt; ++i, ++it) {
           const int s = it % kStages;
           const uint32_t ph = (it / kStages) & 1;
-          ptx::mbar_wait(&full[s], ph);
+          if constexpr (k3x && kPair) ptx::mbar_wait_cluster(&conv[s], ph);
+          else if constexpr (k3x) ptx::mbar_wait(&conv[s], ph);
+          else ptx::mbar_wait(&full[s], ph);
           ptx::tc_fence_after();
 #ifdef PQLG_GEMM_TRACE
           if (it == 0) PQLG_TRACE(2, clock64());
 #endif
           const uint32_t sa = ptx::smem_u32(smem + s * L::kStageBytes);
           const uint32_t sb = sa + L::kABytes;
+          auto mma = [&](uint64_t ad, uint64_t bd, uint32_t acc) {
+            if constexpr (kPair) ptx::mma_tf32_pair(d_tmem, ad, bd, idesc, acc);
+            else ptx::mma_tf32(d_tmem, ad, bd, idesc, acc);
+          };
 #pragma unroll
           for (int j = 0; j < kBK / kUmmaK; ++j) {
             const uint64_t ad = operand_desc<kAMN>(sa + j * k_step_bytes<kAMN>());
             const uint64_t bd = operand_desc<kBMN>(sb + j * k_step_bytes<kBMN>());
-            if constexpr (kPair) ptx::mma_tf32_pair(d_tmem, ad, bd, idesc, (i > 0 || j > 0) ? 1u : 0u);
-            else ptx::mma_tf32(d_tmem, ad, bd, idesc, (i > 0 || j > 0) ? 1u : 0u);
+            const uint32_t acc = (i > 0 || j > 0) ? 1u : 0u;
+            if constexpr (k3x) {
+              const uint64_t al = operand_desc<kAMN>(sa + L::kLoadBytes + j * k_step_bytes<kAMN>());
+              const uint64_t bl = operand_desc<kBMN>(sb + L::kLoadBytes + j * k_step_bytes<kBMN>());
+              mma(al, bd, acc);  // small terms first
+              mma(ad, bl, 1u);
+              mma(ad, bd, 1u);
+            } else {
+              mma(ad, bd, acc);
+            }
           }
           if constexpr (kPair) ptx::mma_commit_pair(&empty[s]);
           else ptx::mma_commit(&empty[s]);
@@ -386,6 +445,29 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair>::kThreads, 1)
 #endif
     }
     __syncwarp();
+  } else if (k3x && warp >= 2 + L::kEpiWarps) {
+    // 3xTF32 converter warps: split each landed stage into hi / lo, make the
+    // generic-proxy stores visible to the tensor core (async proxy), then
+    // arrive on the MMA leader's conv barrier.
+    const int ct = threadIdx.x - 32 * (2 + L::kEpiWarps);
+    const int lane = threadIdx.x & 31;
+    uint32_t it = 0;
+    for (int u = unit0; u < n_units; u += unit_step) {
+      const TileCoord tc = coord(u);
+      int kt0, nkt;
+      k_range(tc.split, kt0, nkt);
+      for (int i = 0; i < nkt; ++i, ++it) {
+        const int s = it % kStages;
+        ptx::mbar_wait(&full[s], (it / kStages) & 1);
+        split_stage<L::kLoadBytes>(smem + s * L::kStageBytes, ct);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (kPair) ptx::mbar_arrive_cluster_release(ptx::mapa(&conv[s], 0));
+          else ptx::mbar_arrive(&conv[s]);
+        }
+      }
+    }
   } else {
     // Epilogue: warp w reads TMEM lane quadrant w % 4 (hardware rule) and
     // column half (w - 2) / 4 of the tile.

@@ -3,6 +3,8 @@
 // learners' epilogue path (bias + ReLU, TMA store, split-K partials + a
 // fixed-order reduction).  Used by the per-op parity tests and the bench's
 // roofline measurement.
+#include <cstring>
+
 #include "pdl.cuh"
 #include "epilogues.cuh"
 #include "gemm_host.cuh"
@@ -27,14 +29,16 @@ __global__ void reduce_splits(const float* W, int splits, int M, int N, float* D
 
 template <int BN, bool AMN, bool BMN>
 void run(const float* A, const float* B, float* D, const float* bias, int M, int N, int K,
-         int lda, int ldb, int ldd, int relu, int splits, bool tf32, cudaStream_t st) {
+         int lda, int ldb, int ldd, int relu, int splits, int round_mode, cudaStream_t st) {
+  const bool tf32 = round_mode == 1;
+  const bool x3 = round_mode == 2;
   gemm::Operands ops;
   ops.a[0] = ops.a[1] = gemm::map_a(A, M, K, lda, AMN, tf32);
   ops.b[0] = ops.b[1] = gemm::map_b(B, N, K, ldb, BMN, BMN ? BN : gemm::b_box<BN>(M), tf32);
   gemm::Problem p = gemm::make_problem(M, N, K, splits);
   if (p.splits == 1) {
     ops.d[0] = ops.d[1] = make_store_map(D, M, N, ldd);
-    gemm::launch<BN, AMN, BMN>(ops, p, 1, epi::Linear{bias, relu, BN, N}, st);
+    gemm::launch<BN, AMN, BMN>(ops, p, 1, epi::Linear{bias, relu, BN, N}, st, x3);
     return;
   }
   require(N % 4 == 0, "split-K partials need N % 4 == 0");
@@ -42,7 +46,7 @@ void run(const float* A, const float* B, float* D, const float* bias, int M, int
   PQLG_CUDA(cudaMallocAsync(&W, sizeof(float) * p.splits * M * N, st));
   ops.d[0] = ops.d[1] = make_tmap_3d(W, N, M, p.splits, N, static_cast<uint64_t>(M) * N, 32, 32,
                                      Swz::k128);
-  gemm::launch<BN, AMN, BMN>(ops, p, 1, epi::Partial{}, st);
+  gemm::launch<BN, AMN, BMN>(ops, p, 1, epi::Partial{}, st, x3);
   launch(reduce_splits, dim3(296), dim3(256), 0, st, W, p.splits, M, N, D, ldd, bias, relu);
   PQLG_CUDA(cudaFreeAsync(W, st));
 }
@@ -62,21 +66,24 @@ void run_repeat(const float* A, const float* B, float* D, const float* bias, int
 }
 
 // The update's dominant launch: `groups` independent hidden layers in one
-// persistent launch (the twin target + twin online critics, 4 groups), all
-// reading the same A / W and writing the same D (timing only).
+// persistent launch (the twin target + twin online critics, 4 groups).  Group
+// g reads its own A + g*M*lda, W = B + g*K*ldb, bias + g*N and writes its own
+// D + g*M*ldd, as the four critics of an update do (distinct operands, so
+// the timing sees the in-update DRAM/L2 traffic, not one L2-resident set).
 void run_repeat_groups(const float* A, const float* B, float* D, const float* bias, int M, int N,
                        int K, int lda, int ldb, int ldd, int groups, int iters, cudaStream_t st) {
   require(groups >= 1 && groups <= gemm::kMaxGroups, "repeat_groups: 1..4 groups");
   require(N > 128, "repeat_groups: hidden-layer widths (N > 128)");
   gemm::Operands ops;
-  for (int g = 0; g < gemm::kMaxGroups; ++g) {
-    ops.a[g] = gemm::map_a(A, M, K, lda, false, true);
-    ops.b[g] = gemm::map_b(B, N, K, ldb, true, 256, true);
-    ops.d[g] = make_store_map(D, M, N, ldd);
+  std::memset(&ops, 0, sizeof(ops));
+  epi::Hidden e{};
+  for (int g = 0; g < groups; ++g) {
+    ops.a[g] = gemm::map_a(A + static_cast<size_t>(g) * M * lda, M, K, lda, false, true);
+    ops.b[g] = gemm::map_b(B + static_cast<size_t>(g) * K * ldb, N, K, ldb, true, 256, true);
+    ops.d[g] = make_store_map(D + static_cast<size_t>(g) * M * ldd, M, N, ldd);
+    e.bias[g] = bias + static_cast<size_t>(g) * N;
   }
   const gemm::Problem p = gemm::make_problem(M, N, K, 1);
-  epi::Hidden e{};
-  for (int g = 0; g < gemm::kMaxGroups; ++g) e.bias[g] = bias;
   e.bn = 256;
   e.M = M;
   e.N = N;
@@ -87,7 +94,7 @@ void run_repeat_groups(const float* A, const float* B, float* D, const float* bi
 template <int BN>
 void dispatch_major(int a_mn, int b_mn, const float* A, const float* B, float* D,
                     const float* bias, int M, int N, int K, int lda, int ldb, int ldd, int relu,
-                    int splits, bool tf32, cudaStream_t st) {
+                    int splits, int tf32, cudaStream_t st) {
   if (!a_mn && !b_mn) run<BN, false, false>(A, B, D, bias, M, N, K, lda, ldb, ldd, relu, splits, tf32, st);
   else if (!a_mn && b_mn) run<BN, false, true>(A, B, D, bias, M, N, K, lda, ldb, ldd, relu, splits, tf32, st);
   else if (a_mn && !b_mn) run<BN, true, false>(A, B, D, bias, M, N, K, lda, ldb, ldd, relu, splits, tf32, st);
@@ -125,7 +132,8 @@ extern "C" int pqlg_k_gemm_tf32(const float* A, const float* B, float* D, const 
   return pqlg::guarded([&] {
     pqlg::require(M > 0 && N > 0 && K > 0, "gemm: empty shape");
     auto st = static_cast<cudaStream_t>(stream);
-    const bool tf32 = round_mode == 1;
+    pqlg::require(round_mode >= 0 && round_mode <= 2, "gemm: round_mode 0, 1 or 2");
+    const int tf32 = round_mode;
     if (N > 128)
       pqlg::dispatch_major<256>(a_mn, b_mn, A, B, D, bias, M, N, K, lda, ldb, ldd, relu, splits, tf32, st);
     else if (N > 64)

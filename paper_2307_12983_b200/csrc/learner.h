@@ -61,12 +61,14 @@ class VLearner {
   int obs_dim() const { return D_; }
   int act_dim() const { return A_; }
   cudaStream_t stream() const { return stream_; }
+  // Synchronizes; PQLG_ENONFINITE (and clears the sticky status word) if an
+  // update since the last check was non-finite.
+  int check_status();
 
  private:
   void build_update();
   void enqueue();
   void prepare_indices();
-  int check_status();
 
   pqlg_config cfg_;
   pqlg_task_dims dims_;
@@ -174,11 +176,11 @@ class PLearner {
   int obs_dim() const { return D_; }
   cudaStream_t stream() const { return stream_; }
   int64_t critic_version() const { return critic_version_; }
+  int check_status();  // as VLearner::check_status
 
  private:
   void build_update();
   void enqueue();
-  int check_status();
 
   pqlg_config cfg_;
   pqlg_task_dims dims_;

@@ -71,14 +71,15 @@ Step fwd(const float* A0, const float* A1, int64_t lda, const float* W0, const f
   with_bn(N, [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
     gemm::Operands ops;
-    ops.a[0] = gemm::map_a(A0, M, K, lda, false, true);
-    ops.a[1] = groups > 1 ? gemm::map_a(A1, M, K, lda, false, true) : ops.a[0];
-    ops.b[0] = gemm::map_b(W0, N, K, ldw, true, BN, true);
-    ops.b[1] = groups > 1 ? gemm::map_b(W1, N, K, ldw, true, BN, true) : ops.b[0];
+    ops.a[0] = gemm::map_a(A0, M, K, lda, false, gemm::tf32_maps());
+    ops.a[1] = groups > 1 ? gemm::map_a(A1, M, K, lda, false, gemm::tf32_maps()) : ops.a[0];
+    ops.b[0] = gemm::map_b(W0, N, K, ldw, true, BN, gemm::tf32_maps());
+    ops.b[1] = groups > 1 ? gemm::map_b(W1, N, K, ldw, true, BN, gemm::tf32_maps()) : ops.b[0];
     set_out(ops, D0, D1, M, N, ldd, groups);
     const gemm::Problem p = gemm::make_problem(M, N, K, 1);
-    step = [ops, p, groups, epi](cudaStream_t st) {
-      gemm::launch<BN, false, true>(ops, p, groups, epi, st);
+    const bool x3 = gemm::build_x3();
+    step = [ops, p, groups, epi, x3](cudaStream_t st) {
+      gemm::launch<BN, false, true>(ops, p, groups, epi, st, x3);
     };
   });
   return step;
@@ -99,13 +100,14 @@ Step fwd_groups(const float* const* A, int64_t lda, const float* const* W, int M
     gemm::Operands ops;
     std::memset(&ops, 0, sizeof(ops));
     for (int g = 0; g < groups; ++g) {
-      ops.a[g] = gemm::map_a(A[g], M, K, lda, false, true);
-      ops.b[g] = gemm::map_b(W[g], N, K, ldw, true, BN, true);
+      ops.a[g] = gemm::map_a(A[g], M, K, lda, false, gemm::tf32_maps());
+      ops.b[g] = gemm::map_b(W[g], N, K, ldw, true, BN, gemm::tf32_maps());
       if (D && D[g]) ops.d[g] = make_store_map(D[g], M, N, ldd);
     }
     const gemm::Problem p = gemm::make_problem(M, N, K, 1);
-    step = [ops, p, groups, epi](cudaStream_t st) {
-      gemm::launch<BN, false, true>(ops, p, groups, epi, st);
+    const bool x3 = gemm::build_x3();
+    step = [ops, p, groups, epi, x3](cudaStream_t st) {
+      gemm::launch<BN, false, true>(ops, p, groups, epi, st, x3);
     };
   });
   return step;
@@ -121,15 +123,16 @@ Step dgrad(const float* G0, const float* G1, int64_t ldg, const float* W0, const
   with_bn(N_in, [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
     gemm::Operands ops;
-    ops.a[0] = gemm::map_a(G0, M, N_out, ldg, false, true);
-    ops.a[1] = groups > 1 ? gemm::map_a(G1, M, N_out, ldg, false, true) : ops.a[0];
+    ops.a[0] = gemm::map_a(G0, M, N_out, ldg, false, gemm::tf32_maps());
+    ops.a[1] = groups > 1 ? gemm::map_a(G1, M, N_out, ldg, false, gemm::tf32_maps()) : ops.a[0];
     const int box = gemm::b_box<BN>(M);  // K-major B: a CTA pair splits the columns
-    ops.b[0] = gemm::map_b(W0, N_in, N_out, ldw, false, box, true);
-    ops.b[1] = groups > 1 ? gemm::map_b(W1, N_in, N_out, ldw, false, box, true) : ops.b[0];
+    ops.b[0] = gemm::map_b(W0, N_in, N_out, ldw, false, box, gemm::tf32_maps());
+    ops.b[1] = groups > 1 ? gemm::map_b(W1, N_in, N_out, ldw, false, box, gemm::tf32_maps()) : ops.b[0];
     set_out(ops, D0, D1, M, N_in, ldd, groups);
     const gemm::Problem p = gemm::make_problem(M, N_in, N_out, 1);
-    step = [ops, p, groups, epi](cudaStream_t st) {
-      gemm::launch<BN, false, false>(ops, p, groups, epi, st);
+    const bool x3 = gemm::build_x3();
+    step = [ops, p, groups, epi, x3](cudaStream_t st) {
+      gemm::launch<BN, false, false>(ops, p, groups, epi, st, x3);
     };
   });
   return step;
@@ -146,17 +149,18 @@ Step wgrad(const float* H0, const float* H1, int64_t ldh, const float* G0, const
   with_bn(N, [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
     gemm::Operands ops;
-    ops.a[0] = gemm::map_a(H0, M, K, ldh, true, true);
-    ops.a[1] = groups > 1 ? gemm::map_a(H1, M, K, ldh, true, true) : ops.a[0];
-    ops.b[0] = gemm::map_b(G0, N, K, ldg, true, BN, true);
-    ops.b[1] = groups > 1 ? gemm::map_b(G1, N, K, ldg, true, BN, true) : ops.b[0];
+    ops.a[0] = gemm::map_a(H0, M, K, ldh, true, gemm::tf32_maps());
+    ops.a[1] = groups > 1 ? gemm::map_a(H1, M, K, ldh, true, gemm::tf32_maps()) : ops.a[0];
+    ops.b[0] = gemm::map_b(G0, N, K, ldg, true, BN, gemm::tf32_maps());
+    ops.b[1] = groups > 1 ? gemm::map_b(G1, N, K, ldg, true, BN, gemm::tf32_maps()) : ops.b[0];
     const gemm::Problem p = gemm::make_problem(M, N, K, splits);
     require(p.splits == splits, "wgrad: split count must divide the k tiles evenly");
     ops.d[0] = ops.d[1] = make_tmap_3d(W, N, M, static_cast<uint64_t>(groups) * splits,
                                        ldw_part, static_cast<uint64_t>(M) * ldw_part, 32, 32,
                                        Swz::k128);
-    step = [ops, p, groups, epi](cudaStream_t st) {
-      gemm::launch<BN, true, true>(ops, p, groups, epi, st);
+    const bool x3 = gemm::build_x3();
+    step = [ops, p, groups, epi, x3](cudaStream_t st) {
+      gemm::launch<BN, true, true>(ops, p, groups, epi, st, x3);
     };
   });
   return step;
@@ -189,15 +193,20 @@ inline Step head_gemm_step(HeadSplit& hs, const float* A0, int64_t lda, const fl
   hs.plan(M, N, K);
   gemm::Operands ops;
   std::memset(&ops, 0, sizeof(ops));
-  ops.a[0] = gemm::map_a(A0, M, K, lda, false, true);
+  ops.a[0] = gemm::map_a(A0, M, K, lda, false, gemm::tf32_maps());
   const int bn = N <= 32 ? 32 : 64;
-  ops.b[0] = gemm::map_b(W, N, K, ldw, true, bn, true);
+  ops.b[0] = gemm::map_b(W, N, K, ldw, true, bn, gemm::tf32_maps());
   ops.d[0] = make_tmap_3d(hs.part.p, N, M, hs.splits, hs.ld_part,
                           static_cast<uint64_t>(M) * hs.ld_part, 32, 32, Swz::k128);
   const gemm::Problem p = gemm::make_problem(M, N, K, hs.splits);
+  const bool x3 = gemm::build_x3();
   if (bn == 32)
-    return [ops, p](cudaStream_t st) { gemm::launch<32, false, true>(ops, p, 1, epi::Partial{}, st); };
-  return [ops, p](cudaStream_t st) { gemm::launch<64, false, true>(ops, p, 1, epi::Partial{}, st); };
+    return [ops, p, x3](cudaStream_t st) {
+      gemm::launch<32, false, true>(ops, p, 1, epi::Partial{}, st, x3);
+    };
+  return [ops, p, x3](cudaStream_t st) {
+    gemm::launch<64, false, true>(ops, p, 1, epi::Partial{}, st, x3);
+  };
 }
 
 // The finish (bias, squash, noise, stores) of a planned head.

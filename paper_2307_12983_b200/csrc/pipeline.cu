@@ -21,6 +21,8 @@
 #include <chrono>
 #include <condition_variable>
 #include <deque>
+#include <cmath>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <optional>
@@ -255,6 +257,29 @@ class Pipeline {
     writer_ = std::make_unique<MetricsWriter>(m.path);
   }
 
+  void record_snapshots(bool on) { record_snapshots_ = on; }
+
+  // After run(): the P-learner's critic replicas against the snapshot the
+  // V-learner published under the version the P-learner holds (version 0:
+  // the replicas it was created with, compared with nothing: diff -1).
+  void check_critics(int64_t* p_version, double* max_abs_diff) {
+    require(ran_, "pipeline: check_critics after run()");
+    require(record_snapshots_, "pipeline: check_critics needs record_snapshots before run()");
+    const int64_t Pq = p_->critic_params();
+    *p_version = p_->critic_version();
+    *max_abs_diff = -1.0;
+    std::lock_guard<std::mutex> lk(hist_mu_);
+    auto it = crit_hist_.find(*p_version);
+    if (it == crit_hist_.end()) return;
+    std::vector<float> got(2 * Pq);
+    p_->get_params(1, got.data());
+    p_->get_params(2, got.data() + Pq);
+    double mx = 0.0;
+    for (int64_t i = 0; i < 2 * Pq; ++i)
+      mx = std::max(mx, std::fabs(static_cast<double>(got[i]) - it->second[i]));
+    *max_abs_diff = mx;
+  }
+
   pqlg_run_report run(int64_t actor_steps, double max_seconds) {
     require(!ran_, "pipeline: run() may be called once per pipeline");
     ran_ = true;
@@ -286,8 +311,15 @@ class Pipeline {
     stop_all();
     tv.join();
     tp.join();
+    if (failed_.load()) {
+      // a sticky device error would make a checked sync throw first and
+      // replace the worker's error: drain the streams, ignoring errors
+      for (auto s : {sa_, sv_, sp_}) (void)cudaStreamSynchronize(s);
+      set_last_error(error_);
+      throw Error(err_status_, error_);
+    }
     for (auto s : {sa_, sv_, sp_}) PQLG_CUDA(cudaStreamSynchronize(s));
-    if (writer_ && !failed_.load()) {  // final metrics row (run_parallel returns final metrics)
+    if (writer_) {  // final metrics row (run_parallel returns final metrics)
       snapshot_for_eval();
       append_row();
     }
@@ -309,11 +341,7 @@ class Pipeline {
     r.critic_version = crit_pool_.newest();
     r.last_critic_loss = last_closs_;
     r.last_actor_loss = last_aloss_;
-    r.ok = failed_.load() ? 0 : 1;
-    if (failed_.load()) {
-      set_last_error(error_);
-      throw Error(err_status_, error_);
-    }
+    r.ok = 1;
     return r;
   }
 
@@ -326,6 +354,9 @@ class Pipeline {
     cudaEvent_t filled = nullptr, done_v = nullptr, done_p = nullptr;
     int pending = 0;  // consumers still to release it
   };
+  bool record_snapshots_ = false;
+  std::mutex hist_mu_;
+  std::map<int64_t, std::vector<float>> crit_hist_;
   struct ConsumerStats {
     int64_t expect = 0, consumed = 0, dups = 0, gaps = 0;
   };
@@ -424,14 +455,19 @@ class Pipeline {
       PQLG_CUDA(cudaMemcpyAsync(s.mean.p, actor_->mean_dev(), D_ * 8, cudaMemcpyDeviceToDevice, sa_));
       PQLG_CUDA(cudaMemcpyAsync(s.m2.p, actor_->m2_dev(), D_ * 8, cudaMemcpyDeviceToDevice, sa_));
       PQLG_CUDA(cudaMemcpyAsync(s.pol.p, actor_->policy_dev(), Pp * 4, cudaMemcpyDeviceToDevice, sa_));
-      // newest critic snapshot (V-learner -> actor -> P-learner)
+      // newest critic snapshot (V-learner -> actor -> P-learner).  Only a slot
+      // that received a copy in this iteration carries a critic version: a
+      // reused slot's s.crit holds an older snapshot (or nothing), which the
+      // P-learner's equal-or-newer rule would otherwise adopt.
+      bool fresh = false;
       crit_have = crit_pool_.take_if_newer(crit_have, sa_,
                                            [&](const float* src, int64_t, cudaStream_t st) {
                                              PQLG_CUDA(cudaMemcpyAsync(s.crit.p, src, 2 * Pq * 4,
                                                                        cudaMemcpyDeviceToDevice, st));
+                                             fresh = true;
                                            });
       PQLG_CUDA(cudaEventRecord(s.filled, sa_));
-      const Batch b{seq++, k, actor_->policy_version(), crit_have};
+      const Batch b{seq++, k, actor_->policy_version(), fresh ? crit_have : 0};
       if (!ch_v_->push(b) || !ch_p_->push(b)) return;
       ++sent_;
       gate_.record(kActor, H_);
@@ -483,7 +519,10 @@ class Pipeline {
       if (!ready()) continue;
       if (!gate_.wait_for(kVLearner, std::chrono::microseconds(1000))) continue;
       v_->update_n(1);
-      PQLG_CUDA(cudaStreamSynchronize(sv_));
+      // the status word after every update: a non-finite update aborts the
+      // run before it is counted or drives the gate (SPEC: abort)
+      if (v_->check_status() != PQLG_OK)
+        throw Error(PQLG_ENONFINITE, "critic update: non-finite target / loss / gradient");
       gate_.record(kVLearner, 1);
       if (++updates % rc_.publish_every == 0) {
         last_closs_ = v_->last_loss();  // throws on a non-finite update (SPEC: abort)
@@ -491,11 +530,20 @@ class Pipeline {
           std::lock_guard<std::mutex> lk(ema_mu_);
           closs_ema_.add(last_closs_);
         }
-        crit_pool_.publish(sv_, [&](float* dst, cudaStream_t stm) {
+        const int64_t ver = crit_pool_.publish(sv_, [&](float* dst, cudaStream_t stm) {
           PQLG_CUDA(cudaMemcpyAsync(dst, v_->critic_dev(0), Pq * 4, cudaMemcpyDeviceToDevice, stm));
           PQLG_CUDA(cudaMemcpyAsync(dst + Pq, v_->critic_dev(1), Pq * 4, cudaMemcpyDeviceToDevice,
                                     stm));
         });
+        if (record_snapshots_) {  // test hook: host copy of every published snapshot
+          std::vector<float> h(2 * Pq);
+          PQLG_CUDA(cudaMemcpyAsync(h.data(), v_->critic_dev(0), Pq * 4, cudaMemcpyDeviceToHost, sv_));
+          PQLG_CUDA(cudaMemcpyAsync(h.data() + Pq, v_->critic_dev(1), Pq * 4,
+                                    cudaMemcpyDeviceToHost, sv_));
+          PQLG_CUDA(cudaStreamSynchronize(sv_));
+          std::lock_guard<std::mutex> lk(hist_mu_);
+          crit_hist_[ver] = std::move(h);
+        }
       }
     }
     drain(std::chrono::microseconds(0));  // closed channel: already-queued batches still drain
@@ -532,7 +580,8 @@ class Pipeline {
       if (!ready()) continue;
       if (!gate_.wait_for(kPLearner, std::chrono::microseconds(1000))) continue;
       p_->update_n(1);
-      PQLG_CUDA(cudaStreamSynchronize(sp_));
+      if (p_->check_status() != PQLG_OK)
+        throw Error(PQLG_ENONFINITE, "actor update: non-finite loss / gradient");
       gate_.record(kPLearner, 1);
       if (++updates % rc_.publish_every == 0) {
         last_aloss_ = p_->last_loss();
@@ -709,6 +758,8 @@ pqlg_run_report run_synchronous(const pqlg_config& cfg, const pqlg_task_dims& di
   };
   if (writer) next_eval = mc->every_actor_steps;
   const int64_t n_v = static_cast<int64_t>(std::llround(H / rc.beta_av));
+  require(n_v >= 1, "run_synchronous: horizon / beta_av rounds to zero critic updates per "
+                    "iteration (beta_av must be <= 2 * horizon)");
   while (ca < actor_steps) {
     // Alg. 1: roll out H steps, send the transitions / states to the learners
     for (int h = 0; h < H; ++h) {
@@ -816,6 +867,20 @@ int pqlg_pipeline_run(pqlg_pipeline h, int64_t actor_steps, double max_seconds,
   return guarded([&] {
     require(h && out, "pipeline_run: null argument");
     *out = h->p->run(actor_steps, max_seconds);
+  });
+}
+
+int pqlg_pipeline_record_snapshots(pqlg_pipeline h, int on) {
+  return guarded([&] {
+    require(h, "pipeline_record_snapshots: null handle");
+    h->p->record_snapshots(on != 0);
+  });
+}
+
+int pqlg_pipeline_check_critics(pqlg_pipeline h, int64_t* p_version, double* max_abs_diff) {
+  return guarded([&] {
+    require(h && p_version && max_abs_diff, "pipeline_check_critics: null argument");
+    h->p->check_critics(p_version, max_abs_diff);
   });
 }
 

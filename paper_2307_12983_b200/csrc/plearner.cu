@@ -33,6 +33,8 @@ PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
     PQLG_CUDA(cudaStreamCreateWithFlags(&owned_stream_, cudaStreamNonBlocking));
     stream_ = owned_stream_;
   }
+  require(cfg.precision == PQLG_PREC_TF32 || cfg.precision == PQLG_PREC_3XTF32,
+          "plearner: unknown precision");
   require(cfg.algo == PQLG_ALGO_DDPG || cfg.algo == PQLG_ALGO_C51 || cfg.algo == PQLG_ALGO_SAC,
           "plearner: unknown algo");
   dist_ = cfg.algo == PQLG_ALGO_C51;
@@ -108,7 +110,10 @@ PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   status_.alloc(1);
   hbuf_.alloc(2);
   loss_.alloc(2);  // actor loss (+ pql_sac: mean log-prob for the alpha update)
-  build_update();
+  {
+    gemm::PrecisionScope prec(cfg.precision == PQLG_PREC_3XTF32);
+    build_update();
+  }
   PQLG_CUDA(cudaDeviceSynchronize());
 }
 

@@ -64,6 +64,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Wait with cluster-scope acquire: pairs with mbar_arrive_cluster_release
+// from a peer CTA whose shared-memory writes the waiter then consumes.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680)
+      : "memory");
+}
+
 // -------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -178,6 +192,13 @@ __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
 // global stores (measured: ~20% of the epilogue's stall samples).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+}
+// Remote arrive with cluster-scope release: orders this thread's (fenced)
+// shared-memory writes before the peer's acquire (the 3xTF32 converter's
+// hand-off of split operands to the pair leader's MMA).
+__device__ __forceinline__ void mbar_arrive_cluster_release(uint32_t bar_cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr)
+               : "memory");
 }
 // 2-SM TMA load: data lands in this CTA's smem, the transaction bytes are
 // reported on the pair leader's mbarrier (shared::cluster address).

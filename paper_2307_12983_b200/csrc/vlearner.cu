@@ -34,6 +34,8 @@ VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
     stream_ = owned_stream_;
   }
   st = stream_;
+  require(cfg.precision == PQLG_PREC_TF32 || cfg.precision == PQLG_PREC_3XTF32,
+          "vlearner: unknown precision");
   require(cfg.algo == PQLG_ALGO_DDPG || cfg.algo == PQLG_ALGO_C51 || cfg.algo == PQLG_ALGO_SAC,
           "vlearner: unknown algo");
   dist_ = cfg.algo == PQLG_ALGO_C51;
@@ -117,7 +119,10 @@ VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   hbuf_.alloc(2);
   loss_.alloc(1);
 
-  build_update();
+  {
+    gemm::PrecisionScope prec(cfg.precision == PQLG_PREC_3XTF32);
+    build_update();
+  }
   PQLG_CUDA(cudaDeviceSynchronize());
 }
 
@@ -843,6 +848,7 @@ void pqlg_config_default(pqlg_config* c) {
   c->vmax = 10.0;
   c->max_episode_len = 1000;
   c->env_offset = 0;
+  c->precision = PQLG_PREC_TF32;
 }
 
 int pqlg_vlearner_create(const pqlg_config* cfg, const pqlg_task_dims* dims,

@@ -174,3 +174,31 @@ def test_pipeline_time_budget_shutdown_joins_promptly():
     print(f"\nstopped after {r.wall_s:.2f}s (call {dt:.2f}s), c_a={r.c_a}")
     assert r.ok == 1 and r.wall_s < 5.0
     assert r.batches_consumed_v == r.batches_sent == r.batches_consumed_p
+
+
+@pytest.mark.parametrize("free_running,publish_every", [(1, 8), (0, 3), (0, 1)])
+def test_pipeline_p_learner_critics_are_a_published_snapshot(free_running, publish_every):
+    """The P-learner's critic replicas at the end of a run are exactly the
+    snapshot the V-learner published under the version the P-learner holds
+    (learners.cpp:222-227), also when actor iterations carry no new critic
+    snapshot (free running, other publish intervals): a slot reused from an
+    earlier iteration must not hand its stale buffer on as current."""
+    cfg = _lib.default_config(n_envs=256, batch_size=256, buffer_capacity=100_000, hidden=32,
+                              hidden_layers=2, seed=5)
+    dims = _lib.TaskDims(9, 3, -1.0, 1.0)
+    rc = _lib.ratio_config(free_running=free_running, publish_every=publish_every)
+    h = C.c_void_p()
+    _lib.call("pqlg_pipeline_create", C.byref(cfg), C.byref(dims), C.byref(rc), 7, C.byref(h))
+    try:
+        _lib.call("pqlg_pipeline_record_snapshots", h, 1)
+        rep = _lib.RunReport()
+        _lib.call("pqlg_pipeline_run", h, 600, 60.0, C.byref(rep))
+        ver, diff = C.c_int64(), C.c_double()
+        _lib.call("pqlg_pipeline_check_critics", h, C.byref(ver), C.byref(diff))
+    finally:
+        _lib.call("pqlg_pipeline_destroy", h)
+    print(f"\nfree={free_running} K_pub={publish_every}: critic versions published "
+          f"{rep.critic_version}, P-learner holds {ver.value}, max|diff| {diff.value}")
+    assert rep.ok == 1 and rep.critic_version >= 2
+    assert ver.value >= 1
+    assert diff.value == 0.0
