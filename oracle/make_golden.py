@@ -15,7 +15,7 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT / "tests"))
-from oracle_lib import acts_arr, param_count, ptr, ref, sizes_arr  # noqa: E402
+from oracle_lib import acts_arr, param_count, ptr, ref, sizes_arr, traj_hash  # noqa: E402
 
 GOLDEN = ROOT / "tests" / "golden"
 
@@ -431,6 +431,160 @@ def gen_checkpoint(R, out):
     out.update(ck_dummy=np.zeros(1))
 
 
+def synth_coupling(seed, D, A):
+    """The synthetic task's M (SyntheticEnv in ref_harness.cpp) -- used only to
+    build actions that drive |s_0| past the terminal threshold."""
+    R = ref()
+    mseed = R.ref_derive_seed(seed, 1, 1 << 40)
+    from oracle_lib import orc
+    M = np.zeros((D, A))
+    for d in range(D):
+        for k in range(A):
+            u = orc().orc_splitmix64((mseed + d * A + k) & ((1 << 64) - 1))
+            M[d, k] = float(np.float32((u >> 11) * 2.0**-53 * 2.0 - 1.0))
+    return M
+
+
+ENV_CASES = [  # N, D, A, max_len, T, seed, full trajectories stored
+    (64, 5, 2, 7, 60, 3, True),
+    (40, 60, 8, 13, 30, 3, True),
+    (32, 211, 20, 200, 80, 15, False),
+]
+
+
+def gen_env(R, out):
+    """The reference's own EnvBatch::reset_all / step (vecenv.cpp:73-106) on the
+    synthetic task (SyntheticEnv, ref_harness.cpp), staggered time limits:
+    random (partly out-of-range) actions, and for the c3-dims case half the
+    envs pushed along sign(M[0]) so |s_0| crosses 9 (terminal resets)."""
+    for k, (N, D, A, max_len, T, seed, full) in enumerate(ENV_CASES):
+        rng = np.random.default_rng(100 + k)
+        obs0 = np.zeros((N, D), np.float32)
+        h = R.ref_synth_env_create(N, D, A, seed, max_len, np.float32(-1), np.float32(1), 1,
+                                   ptr(obs0))
+        drive = np.sign(synth_coupling(seed, D, A)[0]).astype(np.float32)
+        acts = np.zeros((T, N, A), np.float32)
+        nxt = np.zeros((T, N, D), np.float32)
+        term_obs = np.zeros((T, N, D), np.float32)
+        rew = np.zeros((T, N), np.float32)
+        done = np.zeros((T, N), np.uint8)
+        trunc = np.zeros((T, N), np.uint8)
+        hashes = np.zeros((T, 2), np.uint64)
+        for t in range(T):
+            a = f32(rng.uniform(-1.5, 1.5, (N, A)))
+            a[: N // 2] = np.where(rng.uniform(size=(N // 2, 1)) < 0.9, drive, a[: N // 2])
+            acts[t] = a
+            assert R.ref_synth_env_step(h, ptr(acts[t]), ptr(nxt[t]), ptr(term_obs[t]),
+                                        ptr(rew[t]), ptr(done[t]), ptr(trunc[t])) == 0
+            term_obs[t][done[t] == 0] = 0.0
+            hashes[t] = (traj_hash(nxt[t]), traj_hash(term_obs[t]))
+        ep = np.zeros(N, np.int64)
+        R.ref_synth_env_episode_steps(h, ptr(ep))
+        last = nxt[T - 1].copy()
+        bad = f32(np.full((N, A), np.nan))
+        nan_rc = R.ref_synth_env_step(h, ptr(bad), ptr(nxt[0]), ptr(term_obs[0]), ptr(rew[0]),
+                                      ptr(done[0]), ptr(trunc[0]))
+        R.ref_synth_env_destroy(h)
+        out[f"env{k}_args"] = np.array([N, D, A, max_len, T, seed], np.int64)
+        out[f"env{k}_obs0"] = obs0
+        out[f"env{k}_act"] = acts
+        out[f"env{k}_rew"] = rew
+        out[f"env{k}_done"] = done
+        out[f"env{k}_trunc"] = trunc
+        out[f"env{k}_hash"] = hashes
+        out[f"env{k}_last"] = last
+        out[f"env{k}_nan_rc"] = np.array([nan_rc], np.int64)
+        out[f"env{k}_episode_step"] = ep
+        if full:
+            out[f"env{k}_next"] = nxt
+            out[f"env{k}_term_obs"] = term_obs
+        n_term = int(np.sum(done & (trunc == 0)))
+        print(f"  env{k}: terminals {n_term}, truncations {int(trunc.sum())}, nan rc {nan_rc}")
+
+
+ACTOR_CASES = [  # N, D, A, hidden, seed, max_len, T, sac
+    (256, 32, 8, 256, 5, 50, 5, 0),
+    (256, 211, 20, 512, 7, 1000, 3, 0),
+    (128, 17, 6, 64, 9, 20, 6, 1),
+]
+
+
+def gen_actor_core(R, out):
+    """The reference's own rt::ActorCore (learners.cpp:62-116: constructor,
+    PolicyHandle::create, noise schedule / streams, rollout_step) on the
+    synthetic task: the StepSlices of T steps and the final normalizer.
+    Generated with the scalar kernel backend (kernels::set_backend), the
+    op-order ground truth the restatement follows bit for bit (the AVX2
+    backend's FMA-reassociated policy layers differ in the last ulp)."""
+    R.ref_set_backend(0)
+    for k, (N, D, A, H, seed, max_len, T, sac) in enumerate(ACTOR_CASES):
+        h = R.ref_actor_core_create(N, D, A, H, seed, 0.05, 0.8, -1.0, max_len, sac)
+        P = R.ref_actor_core_policy(h, None)
+        pol = np.zeros(P, np.float32)
+        R.ref_actor_core_policy(h, ptr(pol))
+        obs = np.zeros((T, N, D), np.float32)
+        act = np.zeros((T, N, A), np.float32)
+        boot = np.zeros((T, N, D), np.float32)
+        rew = np.zeros((T, N), np.float32)
+        term = np.zeros((T, N), np.uint8)
+        trunc = np.zeros((T, N), np.uint8)
+        for t in range(T):
+            assert R.ref_actor_core_step(h, ptr(obs[t]), ptr(act[t]), ptr(boot[t]), ptr(rew[t]),
+                                         ptr(term[t]), ptr(trunc[t])) == 0
+        cnt = np.zeros(1, np.int64)
+        mean, m2 = np.zeros(D), np.zeros(D)
+        R.ref_actor_core_norm(h, ptr(cnt), ptr(mean), ptr(m2))
+        ep = np.zeros(N, np.int64)
+        R.ref_actor_core_episode_steps(h, ptr(ep))
+        R.ref_actor_core_destroy(h)
+        out[f"ac{k}_args"] = np.array([N, D, A, H, seed, max_len, T, sac], np.int64)
+        if pol.size > 100_000:  # re-derivable (PolicyHandle::create): keep only its digest
+            out[f"ac{k}_policy_hash"] = np.array([traj_hash(pol)], np.uint64)
+        else:
+            out[f"ac{k}_policy"] = pol
+        out[f"ac{k}_obs"] = obs
+        out[f"ac{k}_act"] = act
+        out[f"ac{k}_boot"] = boot
+        out[f"ac{k}_rew"] = rew
+        out[f"ac{k}_term"] = term
+        out[f"ac{k}_trunc"] = trunc
+        out[f"ac{k}_norm"] = np.concatenate([cnt.astype(np.float64), mean, m2])
+        out[f"ac{k}_episode_step"] = ep
+    R.ref_set_backend(1)
+
+
+EVAL_CASES = [  # D, A, H, n_hidden, episodes, eval_seed, max_len, sac
+    (19, 6, 64, 2, 96, 77, 40, 0),
+    (19, 6, 64, 2, 96, 77, 200, 0),
+    (31, 5, 64, 3, 64, 78, 60, 0),
+    (23, 4, 64, 2, 48, 79, 50, 1),
+]
+
+
+def gen_evaluate(R, out):
+    """The reference's own rt::evaluate_policy (learners.cpp:280-325) on the
+    synthetic task: mean return and standard error (scalar kernel backend,
+    as gen_actor_core)."""
+    R.ref_set_backend(0)
+    for k, (D, A, H, nh, M, seed, max_len, sac) in enumerate(EVAL_CASES):
+        rng = np.random.default_rng(200 + k)
+        ps = [D] + [H] * nh + [2 * A if sac else A]
+        pol = f32(rng.standard_normal(param_count(ps)) * 0.1)
+        mean = rng.standard_normal(D) * 0.1
+        m2 = np.abs(rng.standard_normal(D)) * 50 + 10
+        count = 100
+        mu, se = np.zeros(1), np.zeros(1)
+        assert R.ref_evaluate_synth(ptr(pol), ptr(sizes_arr(ps)), nh + 1, sac, count, ptr(mean),
+                                    ptr(m2), M, seed, max_len, np.float32(-1), np.float32(1),
+                                    ptr(mu), ptr(se)) == 0
+        out[f"ev{k}_args"] = np.array([D, A, H, nh, M, seed, max_len, sac, count], np.int64)
+        out[f"ev{k}_policy"] = pol
+        out[f"ev{k}_mean"] = mean
+        out[f"ev{k}_m2"] = m2
+        out[f"ev{k}_result"] = np.array([mu[0], se[0]])
+    R.ref_set_backend(1)
+
+
 def main():
     R = ref()
     if R is None:
@@ -440,7 +594,9 @@ def main():
                      ("elementwise", gen_elementwise), ("norm", gen_norm), ("noise", gen_noise),
                      ("mlp", gen_mlp), ("agents", gen_agents), ("vupdate", gen_vupdate),
                      ("c51update", gen_c51update), ("sac", gen_sac),
-                     ("checkpoint", gen_checkpoint), ("metrics", gen_metrics)]:
+                     ("checkpoint", gen_checkpoint), ("metrics", gen_metrics),
+                     ("env", gen_env), ("actor_core", gen_actor_core),
+                     ("evaluate", gen_evaluate)]:
         if len(sys.argv) > 1 and name not in sys.argv[1:]:
             continue
         out: dict = {}

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <memory>
 #include <random>
+#include <stdexcept>
 #include <vector>
 
 #include "pql/agents/c51.hpp"
@@ -69,6 +70,16 @@ fa::NormStats make_stats(int64_t count, const double* mean, const double* m2, si
 }
 
 }  // namespace
+
+// ------------------------------------------------------------ backend
+// kernels::set_backend (kernels.hpp:17-20): 0 scalar (op-order ground truth),
+// 1 avx2 (the default on this CPU; FMA-reassociated affine kernels).
+REF_API void ref_set_backend(int b) {
+  kernels::set_backend(b == 0 ? kernels::Backend::scalar : kernels::Backend::avx2);
+}
+REF_API int ref_active_backend() {
+  return kernels::active_backend() == kernels::Backend::scalar ? 0 : 1;
+}
 
 // ---------------------------------------------------------------- rng
 REF_API uint64_t ref_derive_seed(uint64_t master, uint64_t stream, uint64_t index) {
@@ -886,6 +897,257 @@ REF_API int ref_metrics_write(const char* path, const double* rows, size_t n) {
     }
   } catch (...) {
     return -1;
+  }
+  return 0;
+}
+
+// ================================================ the synthetic task
+// SyntheticEnv is an EnvBatch subclass built through the reference's
+// protected constructor and its three virtuals (vecenv.hpp:62-69), so the
+// reference's own EnvBatch::reset_all / step (vecenv.cpp:73-106: non-finite
+// check, episode counter, time limit, terminal observation, auto-reset,
+// truncation flags) and its per-env SplitMix streams (derive_seed(seed, env,
+// i), vecenv.cpp:66) run on the synthetic dynamics:
+//   s' = clamp(0.95 s + 0.05 (M clamp(a, lo, hi)), +-10)     d-ascending sums
+//   reward = -(sum s'^2 / D + 0.01 sum a^2 / A)              float mul/add only
+//   terminal when |s'_0| > 9; reset draws s ~ U(-1, 1) on the 53-bit path
+//   M[d][k] = 2 u - 1, u = (splitmix64(derive_seed(seed, env, 2^40) + d A + k) >> 11) 2^-53
+// `make_env` is the link seam: vecenv.cpp is compiled with
+// -Dmake_env=pql_ref_make_env_builtin (oracle/Makefile), and the definition
+// below returns a SyntheticEnv while g_synth.on is set (so the reference's
+// ActorCore constructor and evaluate_policy build it), else the builtin task.
+namespace pql::env {
+std::unique_ptr<EnvBatch> pql_ref_make_env_builtin(TaskId task, std::size_t n_envs,
+                                                   std::uint64_t seed);
+}
+
+namespace {
+
+struct SynthSpec {
+  bool on = false;
+  size_t D = 0, A = 0, max_len = 1000;
+  float low = -1.0f, high = 1.0f;
+};
+SynthSpec g_synth;
+
+// vecenv.cpp:19-23 (file-local there): the reset draw on the 53-bit path
+float synth_uniform(env::SplitMixEngine& rng, float lo, float hi) {
+  const double u = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+  return static_cast<float>(lo + (hi - lo) * u);
+}
+
+class SyntheticEnv final : public env::EnvBatch {
+ public:
+  SyntheticEnv(size_t n, uint64_t seed, const SynthSpec& sp)
+      : EnvBatch(env::TaskId::pendulum /* tag only */, n, seed, sp.D, sp.A, sp.low, sp.high,
+                 sp.max_len, 1.0f),
+        s_(n * sp.D, 0.0f),
+        M_(sp.D * sp.A) {
+    const uint64_t mseed = derive_seed(seed, RngStream::env, 1ull << 40);
+    for (size_t d = 0; d < sp.D; ++d)
+      for (size_t k = 0; k < sp.A; ++k) {
+        const uint64_t u = splitmix64(mseed + d * sp.A + k);
+        M_[d * sp.A + k] = static_cast<float>(static_cast<double>(u >> 11) * 0x1.0p-53 * 2.0 - 1.0);
+      }
+  }
+  // staggered time limits, episode_step = i mod max_len
+  void stagger() {
+    for (size_t i = 0; i < n_envs_; ++i)
+      episode_step_[i] = static_cast<int64_t>(i % max_episode_len_);
+  }
+
+ private:
+  void reset_row(size_t i) override {
+    for (size_t d = 0; d < obs_dim_; ++d) s_[i * obs_dim_ + d] = synth_uniform(rng(i), -1.0f, 1.0f);
+  }
+  bool step_row(size_t i, const float* action, float& reward) override {
+    const size_t D = obs_dim_, A = act_dim_;
+    float a[256];
+    float aa = 0.0f;
+    for (size_t k = 0; k < A; ++k) {
+      float u = action[k];
+      u = u < action_low_ ? action_low_ : (u > action_high_ ? action_high_ : u);
+      a[k] = u;
+      aa = aa + u * u;
+    }
+    float* s = s_.data() + i * D;
+    float ss = 0.0f;
+    for (size_t d = 0; d < D; ++d) {
+      float ma = 0.0f;
+      for (size_t k = 0; k < A; ++k) ma = ma + M_[d * A + k] * a[k];
+      float v = 0.95f * s[d] + 0.05f * ma;
+      v = v < -10.0f ? -10.0f : (v > 10.0f ? 10.0f : v);
+      s[d] = v;
+      ss = ss + v * v;
+    }
+    reward = -(ss / static_cast<float>(D) + 0.01f * (aa / static_cast<float>(A)));
+    return std::fabs(s[0]) > 9.0f;
+  }
+  void observe_row(size_t i, float* obs) const override {
+    std::memcpy(obs, s_.data() + i * obs_dim_, obs_dim_ * sizeof(float));
+  }
+
+  std::vector<float> s_, M_;
+};
+
+}  // namespace
+
+namespace pql::env {
+std::unique_ptr<EnvBatch> make_env(TaskId task, std::size_t n_envs, std::uint64_t seed) {
+  if (g_synth.on) {
+    if (n_envs == 0) throw std::invalid_argument("make_env: n_envs must be >= 1");
+    return std::make_unique<SyntheticEnv>(n_envs, seed, g_synth);
+  }
+  return pql_ref_make_env_builtin(task, n_envs, seed);
+}
+}  // namespace pql::env
+
+namespace {
+std::unique_ptr<env::EnvBatch> make_synth(size_t n, size_t D, size_t A, uint64_t seed,
+                                          size_t max_len, float low, float high) {
+  g_synth = SynthSpec{true, D, A, max_len, low, high};
+  auto e = env::make_env(env::TaskId::pendulum, n, seed);
+  g_synth.on = false;
+  return e;
+}
+}  // namespace
+
+// The synthetic EnvBatch on its own: make_env + reset_all (+ stagger);
+// writes the initial observations.
+REF_API void* ref_synth_env_create(size_t n, size_t D, size_t A, uint64_t seed, size_t max_len,
+                                   float low, float high, int stagger, float* obs0) {
+  auto e = make_synth(n, D, A, seed, max_len, low, high);
+  MatF o = e->reset_all();
+  if (stagger) static_cast<SyntheticEnv&>(*e).stagger();
+  if (obs0) std::memcpy(obs0, o.data(), n * D * sizeof(float));
+  return e.release();
+}
+
+REF_API void ref_synth_env_destroy(void* h) { delete static_cast<env::EnvBatch*>(h); }
+
+// EnvBatch::step (vecenv.cpp:84-106); -2 on the non-finite-action throw
+REF_API int ref_synth_env_step(void* h, const float* act, float* next_obs, float* terminal_obs,
+                               float* rew, uint8_t* dones, uint8_t* trunc) {
+  auto* e = static_cast<env::EnvBatch*>(h);
+  const size_t N = e->n_envs(), D = e->obs_dim();
+  try {
+    const auto& r = e->step(make_mat(act, N, e->act_dim()));
+    std::memcpy(next_obs, r.next_observations.data(), N * D * sizeof(float));
+    // rows without a done keep whatever the buffer held (valid iff dones[i])
+    for (size_t i = 0; i < N; ++i)
+      if (r.dones[i]) std::memcpy(terminal_obs + i * D, r.terminal_observations.row(i), D * 4);
+    std::memcpy(rew, r.rewards.data(), N * sizeof(float));
+    std::memcpy(dones, r.dones.data(), N);
+    std::memcpy(trunc, r.truncated.data(), N);
+  } catch (const std::runtime_error&) {
+    return -2;
+  }
+  return 0;
+}
+
+REF_API void ref_synth_env_episode_steps(void* h, int64_t* out) {
+  auto* e = static_cast<env::EnvBatch*>(h);
+  std::memcpy(out, e->episode_step().data(), e->n_envs() * sizeof(int64_t));
+}
+
+// ---------------------------------------- rt::ActorCore on the synthetic task
+// The reference's own ActorCore (learners.cpp:62-116) -- constructor (env,
+// reset_all, PolicyHandle::create with make_rng(seed, init, 0), noise
+// schedule, per-env noise streams) and rollout_step -- with make_env
+// returning the synthetic task.  Its policy is PolicyHandle::create's: two
+// hidden layers of `hidden` (learners.cpp:22-23).
+struct RefActorCore {
+  RunConfig cfg;
+  std::unique_ptr<rt::ActorCore> core;
+  size_t N = 0, D = 0, A = 0;
+};
+
+REF_API void* ref_actor_core_create(size_t n_envs, size_t D, size_t A, size_t hidden,
+                                    uint64_t seed, double sigma_min, double sigma_max,
+                                    double sigma_fixed, size_t max_len, int sac) {
+  auto* r = new RefActorCore();
+  r->cfg.n_envs = n_envs;
+  r->cfg.hidden = hidden;
+  r->cfg.seed = seed;
+  r->cfg.sigma_min = sigma_min;
+  r->cfg.sigma_max = sigma_max;
+  r->cfg.sigma_fixed = sigma_fixed;
+  r->cfg.algo = sac ? agents::Algo::pql_sac : agents::Algo::pql_ddpg;
+  r->N = n_envs;
+  r->D = D;
+  r->A = A;
+  g_synth = SynthSpec{true, D, A, max_len, -1.0f, 1.0f};
+  r->core = std::make_unique<rt::ActorCore>(r->cfg, rt::TaskDims{D, A, -1.0f, 1.0f});
+  g_synth.on = false;
+  static_cast<SyntheticEnv&>(r->core->envs()).stagger();
+  return r;
+}
+
+REF_API void ref_actor_core_destroy(void* h) { delete static_cast<RefActorCore*>(h); }
+
+// One rollout_step: the StepSlice (obs, act, boot_obs, rew, term, trunc).
+REF_API int ref_actor_core_step(void* h, float* obs, float* act, float* boot, float* rew,
+                                uint8_t* term, uint8_t* trunc) {
+  auto* r = static_cast<RefActorCore*>(h);
+  try {
+    const rt::StepSlice s = r->core->rollout_step();
+    if (obs) std::memcpy(obs, s.obs.data(), r->N * r->D * sizeof(float));
+    if (act) std::memcpy(act, s.act.data(), r->N * r->A * sizeof(float));
+    if (boot) std::memcpy(boot, s.boot_obs.data(), r->N * r->D * sizeof(float));
+    if (rew) std::memcpy(rew, s.rew.data(), r->N * sizeof(float));
+    if (term) std::memcpy(term, s.term.data(), r->N);
+    if (trunc) std::memcpy(trunc, s.trunc.data(), r->N);
+  } catch (const std::runtime_error&) {
+    return -2;
+  }
+  return 0;
+}
+
+REF_API void ref_actor_core_norm(void* h, int64_t* count, double* mean, double* m2) {
+  auto* r = static_cast<RefActorCore*>(h);
+  const auto& s = r->core->norm();
+  *count = s.count;
+  std::memcpy(mean, s.mean.data(), r->D * sizeof(double));
+  std::memcpy(m2, s.m2.data(), r->D * sizeof(double));
+}
+
+REF_API size_t ref_actor_core_policy(void* h, float* out) {
+  auto* r = static_cast<RefActorCore*>(h);
+  const auto& flat = r->core->policy().net().flat;
+  if (out) std::memcpy(out, flat.data(), flat.size() * sizeof(float));
+  return flat.size();
+}
+
+REF_API void ref_actor_core_episode_steps(void* h, int64_t* out) {
+  auto* r = static_cast<RefActorCore*>(h);
+  std::memcpy(out, r->core->envs().episode_step().data(), r->N * sizeof(int64_t));
+}
+
+// --------------------------------------- rt::evaluate_policy on the synthetic task
+// learners.cpp:280-325 as written, with make_env returning the synthetic
+// task (fresh episodes, no stagger).  The snapshot's net may have any depth.
+REF_API int ref_evaluate_synth(const float* pol, const size_t* psizes, size_t n_layers, int sac,
+                               int64_t count, const double* mean, const double* m2,
+                               size_t episodes, uint64_t eval_seed, size_t max_len, float low,
+                               float high, double* mean_out, double* stderr_out) {
+  rt::PolicySnapshot snap;
+  snap.net = make_mlp(psizes, n_layers, pol);
+  snap.stochastic = sac != 0;
+  const size_t D = psizes[0];
+  const size_t A = sac ? psizes[n_layers] / 2 : psizes[n_layers];
+  snap.norm = make_stats(count, mean, m2, D);
+  g_synth = SynthSpec{true, D, A, max_len, low, high};
+  try {
+    const rt::EvalResult r = rt::evaluate_policy(snap, env::TaskId::pendulum, episodes, eval_seed);
+    g_synth.on = false;
+    *mean_out = r.mean;
+    *stderr_out = r.stderr_mean;
+  } catch (const std::invalid_argument&) {
+    g_synth.on = false;
+    return -1;
+  } catch (const std::runtime_error&) {
+    g_synth.on = false;
+    return -2;
   }
   return 0;
 }

@@ -114,6 +114,19 @@ _REF_SIGS = {
                                   sz, f32, f32, sz, f32, f32, vp, vp, vp]),
     "ref_c51_actor_loss": (i32, [vp, vp, vp, vp, vp, sz, vp, sz, sz, f32, f32, sz, f32, f32, vp,
                                  vp]),
+    "ref_set_backend": (None, [i32]),
+    "ref_active_backend": (i32, []),
+    "ref_synth_env_create": (vp, [sz, sz, sz, u64, sz, f32, f32, i32, vp]),
+    "ref_synth_env_destroy": (None, [vp]),
+    "ref_synth_env_step": (i32, [vp, vp, vp, vp, vp, vp, vp]),
+    "ref_synth_env_episode_steps": (None, [vp, vp]),
+    "ref_actor_core_create": (vp, [sz, sz, sz, sz, u64, f64, f64, f64, sz, i32]),
+    "ref_actor_core_destroy": (None, [vp]),
+    "ref_actor_core_step": (i32, [vp, vp, vp, vp, vp, vp, vp]),
+    "ref_actor_core_norm": (None, [vp, vp, vp, vp]),
+    "ref_actor_core_policy": (sz, [vp, vp]),
+    "ref_actor_core_episode_steps": (None, [vp, vp]),
+    "ref_evaluate_synth": (i32, [vp, vp, sz, i32, i64, vp, vp, sz, u64, sz, f32, f32, vp, vp]),
     "ref_vupdate_create": (vp, [sz, sz, sz, sz, sz, sz, u64, vp, vp, vp, i32, sz, f32, f32]),
     "ref_vupdate_destroy": (None, [vp]),
     "ref_vupdate_insert": (None, [vp, vp, vp, vp, vp, vp, sz]),
@@ -212,6 +225,14 @@ class MT64:
 
     def __call__(self) -> int:
         return orc().orc_mt64_next(self._state)
+
+
+def traj_hash(x) -> np.uint64:
+    """Order-sensitive 64-bit digest of a float32 array's bit patterns (the
+    golden fixtures store it where a full trajectory would be megabytes)."""
+    b = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64).ravel()
+    w = np.arange(1, b.size + 1, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+    return np.bitwise_xor.reduce(b * w) if b.size else np.uint64(0)
 
 
 def derive_seed(master: int, stream: int, index: int) -> int:

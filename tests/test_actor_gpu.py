@@ -1,7 +1,11 @@
-"""Actor path on the GPU: the synthetic EnvBatch and the exploration noise
-bit-exact against the oracle (and the reference's noise fixtures), the
-normalizer update to 1e-10, and ActorCore::rollout_step end to end
-(actions within the TF32 tolerance, noise/env stream states exact)."""
+"""Actor path on the GPU: the synthetic EnvBatch bit-exact against the
+reference's own EnvBatch::step on SyntheticEnv (tests/golden/env.npz) and
+the oracle, the exploration noise bit-exact against the reference's noise
+fixtures, the normalizer update to 1e-10, and rollout_step end to end
+against the reference's own rt::ActorCore (tests/golden/actor_core.npz):
+initial observations and policy, termination / truncation flags and episode
+counters exact; actions, observations and rewards within the precision
+mode's bar (TF32 2e-3, 3xTF32 2e-5 norm-wise)."""
 import ctypes as C
 from pathlib import Path
 
@@ -27,6 +31,120 @@ def host(t):
 
 def u32(a):
     return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def d2h(ptr_dev, ld, rows, cols, dtype=np.float32):
+    """Rows of a device view (a StepSlice field) to host."""
+    from cuda.bindings import runtime as rt
+    out = np.zeros((rows, cols), dtype)
+    w = cols * out.itemsize
+    err, = rt.cudaMemcpy2D(out.ctypes.data, w, ptr_dev, (ld or cols) * out.itemsize, w, rows,
+                           rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+    assert err == rt.cudaError_t.cudaSuccess, err
+    return out
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / (np.linalg.norm(b) + 1e-30))
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_env_bit_exact_vs_reference_golden(k):
+    """The device env replays the actions of tests/golden/env.npz and matches
+    the reference's EnvBatch::step on SyntheticEnv bit for bit: rewards,
+    dones, truncations, next and terminal observations (full arrays or
+    per-step digests), episode counters, and the non-finite-action error."""
+    import torch
+    from oracle_lib import traj_hash
+    G = np.load(GOLDEN / "env.npz")
+    N, D, A, max_len, T, seed = (int(x) for x in G[f"env{k}_args"])
+    h = C.c_void_p()
+    _lib.call("pqlg_env_create", N, D, A, seed, max_len, 0, np.float32(-1), np.float32(1), None,
+              C.byref(h))
+    obs = torch.zeros(N, D, device="cuda")
+    _lib.call("pqlg_env_reset_all", h, obs.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert np.array_equal(u32(host(obs)), u32(G[f"env{k}_obs0"]))
+    nxt = torch.zeros(N, D, device="cuda")
+    term_obs = torch.zeros(N, D, device="cuda")
+    rew = torch.zeros(N, device="cuda")
+    done = torch.zeros(N, dtype=torch.uint8, device="cuda")
+    trunc = torch.zeros(N, dtype=torch.uint8, device="cuda")
+    for t in range(T):
+        ad = dev(G[f"env{k}_act"][t])
+        _lib.call("pqlg_env_step", h, ad.data_ptr(), 0, nxt.data_ptr(), term_obs.data_ptr(),
+                  rew.data_ptr(), done.data_ptr(), trunc.data_ptr(), 0)
+        torch.cuda.synchronize()
+        dn = host(done)
+        assert np.array_equal(dn, G[f"env{k}_done"][t]), t
+        assert np.array_equal(host(trunc), G[f"env{k}_trunc"][t]), t
+        assert np.array_equal(u32(host(rew)), u32(G[f"env{k}_rew"][t])), t
+        to = host(term_obs).copy()
+        to[dn == 0] = 0.0
+        assert traj_hash(host(nxt)) == G[f"env{k}_hash"][t, 0], t
+        assert traj_hash(to) == G[f"env{k}_hash"][t, 1], t
+    assert np.array_equal(u32(host(nxt)), u32(G[f"env{k}_last"]))
+    bad = dev(f32(np.full((N, A), np.nan)))
+    with pytest.raises(_lib.NonFinite):
+        _lib.call("pqlg_env_step", h, bad.data_ptr(), 0, nxt.data_ptr(), term_obs.data_ptr(),
+                  rew.data_ptr(), done.data_ptr(), trunc.data_ptr(), 0)
+    _lib.call("pqlg_env_destroy", h)
+
+
+@pytest.mark.parametrize("k,prec", [(0, _lib.PREC_TF32), (0, _lib.PREC_3XTF32),
+                                    (1, _lib.PREC_TF32), (1, _lib.PREC_3XTF32),
+                                    (2, _lib.PREC_TF32), (2, _lib.PREC_3XTF32)])
+def test_rollout_vs_reference_actor_core(k, prec):
+    """pqlg_actor_rollout_step vs the reference's rt::ActorCore::rollout_step
+    on the synthetic task (tests/golden/actor_core.npz; DDPG with mixed
+    noise at c1 and c3-width dims, and pql_sac).  Both start from the same
+    state by construction: the device's initial policy must equal
+    PolicyHandle::create's bit for bit."""
+    from oracle_lib import traj_hash
+    G = np.load(GOLDEN / "actor_core.npz")
+    N, D, A, H, seed, max_len, T, sac = (int(x) for x in G[f"ac{k}_args"])
+    conf = _lib.default_config(n_envs=N, hidden=H, hidden_layers=2, seed=seed,
+                               max_episode_len=max_len, precision=prec,
+                               algo=_lib.ALGO_SAC if sac else _lib.ALGO_DDPG)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    h = C.c_void_p()
+    _lib.call("pqlg_actor_create", C.byref(conf), C.byref(dims), None, C.byref(h))
+    pol = np.zeros(param_count([D, H, H, 2 * A if sac else A]), np.float32)
+    _lib.call("pqlg_actor_read", h, 5, ptr(pol))
+    if f"ac{k}_policy" in G:
+        assert np.array_equal(u32(pol), u32(G[f"ac{k}_policy"]))
+    else:
+        assert traj_hash(pol) == G[f"ac{k}_policy_hash"][0]
+    bar = 2e-3 if prec == _lib.PREC_TF32 else 2e-5
+    worst = {}
+    for t in range(T):
+        sl = _lib.StepSlice()
+        _lib.call("pqlg_actor_rollout_step", h, C.byref(sl))
+        got = dict(obs=d2h(sl.obs, sl.ld_obs, N, D), act=d2h(sl.act, sl.ld_act, N, A),
+                   boot=d2h(sl.boot_obs, sl.ld_obs, N, D), rew=d2h(sl.rew, 0, N, 1)[:, 0],
+                   term=d2h(sl.term, 0, N, 1, np.uint8)[:, 0],
+                   trunc=d2h(sl.trunc, 0, N, 1, np.uint8)[:, 0])
+        if t == 0:  # reset_all observations: exact
+            assert np.array_equal(u32(got["obs"]), u32(G[f"ac{k}_obs"][0]))
+        for key in ("obs", "act", "boot", "rew"):
+            r = rel(got[key], G[f"ac{k}_{key}"][t])
+            worst[key] = max(worst.get(key, 0.0), r)
+            assert r <= bar, (t, key, r)
+        assert np.array_equal(got["term"], G[f"ac{k}_term"][t]), t
+        assert np.array_equal(got["trunc"], G[f"ac{k}_trunc"][t]), t
+    ep = np.zeros(N, np.int64)
+    _lib.call("pqlg_actor_read", h, 3, ptr(ep))
+    assert np.array_equal(ep, G[f"ac{k}_episode_step"])
+    cnt = C.c_int64()
+    mean, m2 = np.zeros(D), np.zeros(D)
+    _lib.call("pqlg_actor_norm", h, C.byref(cnt), ptr(mean), ptr(m2))
+    norm = G[f"ac{k}_norm"]
+    assert cnt.value == int(norm[0]) == N * T
+    std = np.sqrt(norm[1 + D:] / norm[0])
+    assert np.all(np.abs(mean - norm[1:1 + D]) <= bar * std)
+    np.testing.assert_allclose(m2, norm[1 + D:], rtol=bar)
+    print(f"\nactor_core case {k} precision {prec}: worst rel {worst}")
+    _lib.call("pqlg_actor_destroy", h)
 
 
 @pytest.mark.parametrize("N,D,A,max_len", [(64, 5, 2, 7), (96, 211, 20, 1000), (40, 60, 8, 13)])

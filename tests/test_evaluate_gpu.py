@@ -1,7 +1,10 @@
-"""evaluate_policy (learners.cpp:280-325) on the GPU vs the oracle
-restatement (orc_evaluate) on the synthetic task: per-episode returns,
-mean and standard error.  Actions come from the TF32 policy, so returns are
-compared with a tolerance; the env and the accumulation are exact."""
+"""evaluate_policy (learners.cpp:280-325) on the GPU vs the reference's own
+rt::evaluate_policy on the synthetic task (tests/golden/evaluate.npz: the
+unmodified function, with make_env returning SyntheticEnv -- see
+oracle/ref_harness.cpp) and vs the oracle restatement (orc_evaluate):
+per-episode returns, mean and standard error.  Actions come from the
+TF32 / 3xTF32 policy, so returns are compared with the precision mode's
+tolerance; the env and the accumulation are exact."""
 import ctypes as C
 
 import numpy as np
@@ -42,3 +45,26 @@ def test_evaluate_matches_oracle(max_len):
     # the reported statistics are the reference's formulas over the returns
     assert mu.value == pytest.approx(np.mean(ret), rel=1e-12)
     assert se.value == pytest.approx(np.std(ret, ddof=1) / np.sqrt(M), rel=1e-9)
+
+
+@pytest.mark.parametrize("prec", [_lib.PREC_TF32, _lib.PREC_3XTF32])
+@pytest.mark.parametrize("k", [0, 1, 2, 3])
+def test_evaluate_vs_reference_golden(k, prec):
+    from pathlib import Path
+    G = np.load(Path(__file__).resolve().parent / "golden" / "evaluate.npz")
+    D, A, H, nh, M, seed, max_len, sac, count = (int(x) for x in G[f"ev{k}_args"])
+    cfg = _lib.default_config(hidden=H, hidden_layers=nh, max_episode_len=max_len,
+                              algo=_lib.ALGO_SAC if sac else _lib.ALGO_DDPG, precision=prec)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    mean = np.ascontiguousarray(G[f"ev{k}_mean"])
+    m2 = np.ascontiguousarray(G[f"ev{k}_m2"])
+    ns = _lib.NormStats(count, ptr(mean), ptr(m2))
+    mu, se = C.c_double(), C.c_double()
+    _lib.call("pqlg_evaluate", C.byref(cfg), C.byref(dims), ptr(G[f"ev{k}_policy"]), C.byref(ns),
+              M, seed, None, C.byref(mu), C.byref(se))
+    want_mu, want_se = G[f"ev{k}_result"]
+    bar = 2e-3 if prec == _lib.PREC_TF32 else 2e-5
+    print(f"\nevaluate case {k} prec {prec}: mean gpu={mu.value:.8f} ref={want_mu:.8f} "
+          f"stderr {se.value:.8f}/{want_se:.8f}")
+    assert abs(mu.value - want_mu) <= bar * abs(want_mu) + 1e-6
+    assert abs(se.value - want_se) <= 10 * bar * abs(want_se) + 1e-6
