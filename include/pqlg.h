@@ -320,6 +320,12 @@ PQLG_API int pqlg_vlearner_set_params(pqlg_vlearner h, int which, const float* f
 PQLG_API int pqlg_vlearner_debug_read(pqlg_vlearner h, int what, float* host_out);
 /* Number of kernels one update launches (graph nodes). */
 PQLG_API int pqlg_vlearner_kernels_per_update(pqlg_vlearner h, int* out);
+/* Measurement hook: the update graph captured with an event-record node
+ * around every kernel, replayed `reps` times (after two warm-up replays, each
+ * a real update); writes "kernel\tavg_ms\tshape\n" per launch in order and
+ * a final "__graph__\tavg_ms\t\n" line (NUL-terminated, cap bytes).  The
+ * event nodes remove programmatic-dependent-launch overlap between kernels. */
+PQLG_API int pqlg_vlearner_time_update(pqlg_vlearner h, int reps, char* out, int cap);
 
 /* ------------------------------------------------ P-learner (policy core) */
 typedef struct pqlg_plearner_s* pqlg_plearner;
@@ -364,6 +370,8 @@ PQLG_API int pqlg_plearner_log_alpha(pqlg_plearner h, float* out);
 PQLG_API int pqlg_plearner_buffer_size(pqlg_plearner h, uint64_t* out);
 PQLG_API int pqlg_plearner_set_sampler(pqlg_plearner h, int mode);
 PQLG_API int pqlg_plearner_kernels_per_update(pqlg_plearner h, int* out);
+/* As pqlg_vlearner_time_update, for the policy update graph. */
+PQLG_API int pqlg_plearner_time_update(pqlg_plearner h, int reps, char* out, int cap);
 
 /* ------------------------------------------------------------ actor */
 typedef struct pqlg_actor_s* pqlg_actor;
@@ -406,7 +414,16 @@ PQLG_API int pqlg_actor_policy_version(pqlg_actor h, int64_t* out);
 /* what: 0 obs [N x D] f32, 1 actions [N x A] f32, 2 noise streams [N] u64,
  * 3 episode steps [N] i64, 4 env streams [N] u64, 5 policy params, 6 status */
 PQLG_API int pqlg_actor_read(pqlg_actor h, int what, void* host_out);
+/* The last rollout_step's StepSlice (messages.hpp:31-35) as dense host rows:
+ * obs / boot_obs [N x obs_dim], act [N x act_dim], rew [N], term / trunc [N]
+ * (any pointer may be NULL); synchronizes.  The copy-out path of a host
+ * consumer (the reference's StepSlice-by-value ActorCore::rollout_step). */
+PQLG_API int pqlg_actor_read_slice(pqlg_actor h, float* obs, float* act, float* boot_obs,
+                                   float* rew, uint8_t* term, uint8_t* trunc);
 PQLG_API int pqlg_actor_kernels_per_step(pqlg_actor h, int* out);
+/* As pqlg_vlearner_time_update for the rollout-step graphs; one replay runs
+ * three consecutive steps (every output buffer set once). */
+PQLG_API int pqlg_actor_time_steps(pqlg_actor h, int reps, char* out, int cap);
 
 /* ------------------------------------------------ run_parallel (pipeline)
  * The three PQL processes (Actor, V-learner, P-learner; SPEC.md:438-501,

@@ -87,6 +87,26 @@ class VLearner {
     check(pqlg_vlearner_buffer_size(h_, &n));
     return n;
   }
+  // which: 0 q1, 1 q2, 2 q1_target, 3 q2_target, 4 lagged policy
+  std::int64_t param_count(int which) const {
+    std::int64_t n = 0;
+    check(pqlg_vlearner_param_count(h_, which, &n));
+    return n;
+  }
+  void set_params(int which, const std::vector<float>& flat) {
+    if (static_cast<std::int64_t>(flat.size()) != param_count(which))
+      throw std::invalid_argument("set_params: parameter count mismatch");
+    check(pqlg_vlearner_set_params(h_, which, flat.data()));
+  }
+  void get_params(int which, std::vector<float>& flat) const {
+    flat.resize(static_cast<std::size_t>(param_count(which)));
+    check(pqlg_vlearner_get_params(h_, which, flat.data()));
+  }
+  // pql_sac: adopt a PolicySnapshot's net and log_alpha (equal-or-newer)
+  void adopt_policy_sac(const std::vector<float>& flat, float log_alpha, std::int64_t version) {
+    check(pqlg_vlearner_adopt_policy_sac(h_, flat.data(), log_alpha, version));
+  }
+  void set_sampler(int mode) { check(pqlg_vlearner_set_sampler(h_, mode)); }
   pqlg_vlearner handle() const { return h_; }
 
  private:
@@ -138,6 +158,32 @@ class PLearner {
     check(pqlg_plearner_snapshot(h_, flat.data()));
     return flat;
   }
+  // which: 0 policy, 1 critic replica q1, 2 critic replica q2
+  std::int64_t param_count(int which) const {
+    std::int64_t n = 0;
+    check(pqlg_plearner_param_count(h_, which, &n));
+    return n;
+  }
+  void set_params(int which, const std::vector<float>& flat) {
+    if (static_cast<std::int64_t>(flat.size()) != param_count(which))
+      throw std::invalid_argument("set_params: parameter count mismatch");
+    check(pqlg_plearner_set_params(h_, which, flat.data()));
+  }
+  void get_params(int which, std::vector<float>& flat) const {
+    flat.resize(static_cast<std::size_t>(param_count(which)));
+    check(pqlg_plearner_get_params(h_, which, flat.data()));
+  }
+  float log_alpha() const {
+    float a = 0.0f;
+    check(pqlg_plearner_log_alpha(h_, &a));
+    return a;
+  }
+  std::uint64_t buffer_size() const {
+    std::uint64_t n = 0;
+    check(pqlg_plearner_buffer_size(h_, &n));
+    return n;
+  }
+  void set_sampler(int mode) { check(pqlg_plearner_set_sampler(h_, mode)); }
   pqlg_plearner handle() const { return h_; }
 
  private:
@@ -169,6 +215,17 @@ class Actor {
     std::int64_t v = 0;
     check(pqlg_actor_policy_version(h_, &v));
     return v;
+  }
+  // the last rollout_step's StepSlice into host rows (any pointer may be null)
+  void read_slice(float* obs, float* act, float* boot_obs, float* rew, std::uint8_t* term,
+                  std::uint8_t* trunc) const {
+    check(pqlg_actor_read_slice(h_, obs, act, boot_obs, rew, term, trunc));
+  }
+  // running NormStats (mean / m2 sized obs_dim)
+  std::int64_t norm(double* mean, double* m2) const {
+    std::int64_t count = 0;
+    check(pqlg_actor_norm(h_, &count, mean, m2));
+    return count;
   }
   pqlg_actor handle() const { return h_; }
 

@@ -202,6 +202,10 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_pipeline_create": (i32, [P(Config), P(TaskDims), P(RatioConfig), u64, P(vp)]),
     "pqlg_pipeline_run": (i32, [vp, i64, C.c_double, P(RunReport)]),
     "pqlg_pipeline_destroy": (i32, [vp]),
+    "pqlg_vlearner_time_update": (i32, [vp, i32, C.c_char_p, i32]),
+    "pqlg_plearner_time_update": (i32, [vp, i32, C.c_char_p, i32]),
+    "pqlg_actor_time_steps": (i32, [vp, i32, C.c_char_p, i32]),
+    "pqlg_actor_read_slice": (i32, [vp, vp, vp, vp, vp, vp, vp]),
     "pqlg_pipeline_record_snapshots": (i32, [vp, i32]),
     "pqlg_pipeline_check_critics": (i32, [vp, P(i64), P(C.c_double)]),
     "pqlg_pipeline_set_metrics": (i32, [vp, P(MetricsConfig)]),
@@ -335,3 +339,18 @@ def ratio_config(**overrides) -> RatioConfig:
     for k, v in overrides.items():
         setattr(rc, k, v)
     return rc
+
+
+def time_graph(fn: str, h, reps: int = 20):
+    """In-graph per-kernel device times (pqlg_*_time_update / _time_steps):
+    returns ([(kernel, ms, shape), ...] in launch order, graph_ms)."""
+    buf = C.create_string_buffer(1 << 20)
+    call(fn, h, reps, buf, len(buf))
+    rows, graph_ms = [], None
+    for line in buf.value.decode().splitlines():
+        name, ms, shape = (line.split("\t") + ["", ""])[:3]
+        if name == "__graph__":
+            graph_ms = float(ms)
+        else:
+            rows.append((name, float(ms), shape))
+    return rows, graph_ms

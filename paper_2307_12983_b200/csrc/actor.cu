@@ -334,6 +334,7 @@ int Actor::kernels_per_step() {
 void Actor::rollout_step(pqlg_step_slice* out) {
   const int cur = cur_;
   enqueue(cur);
+  stepped_ = true;
   if (!step_done_) PQLG_CUDA(cudaEventCreateWithFlags(&step_done_, cudaEventDisableTiming));
   PQLG_CUDA(cudaEventRecord(step_done_, stream_));  // consumers on other streams wait on it
   if (out) {
@@ -347,6 +348,14 @@ void Actor::rollout_step(pqlg_step_slice* out) {
     out->ld_act = Ap_;
   }
   cur_ = (cur + 1) % kSets;
+}
+
+std::string Actor::time_steps(int reps) {
+  return time_in_graph(
+      [&] {
+        for (int k = 0; k < kSets; ++k) enqueue((cur_ + k) % kSets);
+      },
+      stream_, reps);
 }
 
 void Actor::rollout_n(int n) {
@@ -418,6 +427,26 @@ void Actor::read_state(int what, void* out) {
     case 6: PQLG_CUDA(cudaMemcpyAsync(out, status_.p, 4, cudaMemcpyDeviceToHost, st)); break;
     default: throw Error(PQLG_EINVAL, "actor_read: what must be 0..6");
   }
+  PQLG_CUDA(cudaStreamSynchronize(st));
+}
+
+void Actor::read_last_slice(float* obs, float* act, float* boot, float* rew, uint8_t* term,
+                            uint8_t* trunc) {
+  require(stepped_, "actor_read_slice: no rollout_step yet");
+  const int k = (cur_ + kSets - 1) % kSets;
+  auto st = stream_;
+  if (obs)
+    PQLG_CUDA(cudaMemcpy2DAsync(obs, D_ * 4, obs_[k].p, Dp_ * 4, D_ * 4, N_,
+                                cudaMemcpyDeviceToHost, st));
+  if (act)
+    PQLG_CUDA(cudaMemcpy2DAsync(act, A_ * 4, act_[k].p, Ap_ * 4, A_ * 4, N_,
+                                cudaMemcpyDeviceToHost, st));
+  if (boot)
+    PQLG_CUDA(cudaMemcpy2DAsync(boot, D_ * 4, boot_[k].p, Dp_ * 4, D_ * 4, N_,
+                                cudaMemcpyDeviceToHost, st));
+  if (rew) PQLG_CUDA(cudaMemcpyAsync(rew, rew_[k].p, N_ * 4, cudaMemcpyDeviceToHost, st));
+  if (term) PQLG_CUDA(cudaMemcpyAsync(term, term_[k].p, N_, cudaMemcpyDeviceToHost, st));
+  if (trunc) PQLG_CUDA(cudaMemcpyAsync(trunc, trunc_[k].p, N_, cudaMemcpyDeviceToHost, st));
   PQLG_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -648,8 +677,23 @@ int pqlg_actor_read(pqlg_actor h, int what, void* out) {
   return guarded([&] { h->a->read_state(what, out); });
 }
 
+int pqlg_actor_read_slice(pqlg_actor h, float* obs, float* act, float* boot_obs, float* rew,
+                          uint8_t* term, uint8_t* trunc) {
+  return guarded([&] {
+    require(h, "actor_read_slice: null handle");
+    h->a->read_last_slice(obs, act, boot_obs, rew, term, trunc);
+  });
+}
+
 int pqlg_actor_kernels_per_step(pqlg_actor h, int* out) {
   return guarded([&] { *out = h->a->kernels_per_step(); });
+}
+
+int pqlg_actor_time_steps(pqlg_actor h, int reps, char* out, int cap) {
+  return guarded([&] {
+    require(h && out && cap > 0, "actor_time_steps: null argument");
+    copy_cstr(h->a->time_steps(reps), out, cap);
+  });
 }
 
 int pqlg_env_create(int n_envs, int obs_dim, int act_dim, uint64_t seed, int max_episode_len,

@@ -27,11 +27,19 @@ class Actor {
   void rollout_n(int n);
   void norm(int64_t* count, double* mean, double* m2);
   void read_state(int what, void* out);
+  // The last rollout_step's StepSlice, dense rows into host buffers (any may
+  // be null); synchronizes.
+  void read_last_slice(float* obs, float* act, float* boot, float* rew, uint8_t* term,
+                       uint8_t* trunc);
   int64_t policy_version() const { return version_; }
   cudaStream_t stream() const { return stream_; }
   // recorded on the actor's stream after every rollout_step (null before the first)
   cudaEvent_t step_event() const { return step_done_; }
   int kernels_per_step();
+  // Per-kernel device times of the step graph: one replay runs kSets
+  // consecutive steps (every output buffer set once), so the actor's state
+  // advances as after kSets rollout steps.
+  std::string time_steps(int reps);
   int n_envs() const { return N_; }
   int obs_dim() const { return D_; }
   int64_t param_count() const { return pnet_.params; }
@@ -65,6 +73,7 @@ class Actor {
   NetShape pnet_;
   int64_t version_ = 0;
   int cur_ = 0;
+  bool stepped_ = false;
 
   std::unique_ptr<DeviceEnv> env_;
   // Step outputs rotate over kSets buffer sets, so a slice handed out by

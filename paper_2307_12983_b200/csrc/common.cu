@@ -128,11 +128,14 @@ namespace {
 struct ProfRec {
   cudaEvent_t a, b;
   const void* fn;
+  std::string shape;
 };
 std::atomic<bool> g_prof{false};
 std::mutex g_prof_mu;
 std::vector<ProfRec> g_prof_recs;
 thread_local bool g_prof_skip = false;
+// the instrumented capture of time_in_graph (this thread only)
+thread_local std::vector<ProfRec>* t_graph_recs = nullptr;
 
 bool capturing(cudaStream_t st) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -141,9 +144,22 @@ bool capturing(cudaStream_t st) {
 }
 }  // namespace
 
-bool profiling_active() { return g_prof.load(std::memory_order_relaxed); }
+bool profiling_active() {
+  return t_graph_recs != nullptr || g_prof.load(std::memory_order_relaxed);
+}
 
-void profile_before(cudaStream_t st, const void* fn) {
+void profile_before(cudaStream_t st, const void* fn, const char* shape) {
+  if (t_graph_recs) {  // instrumented capture: an event-record node in the graph
+    ProfRec r{};
+    r.fn = fn;
+    if (shape) r.shape = shape;
+    PQLG_CUDA(cudaEventCreate(&r.a));
+    PQLG_CUDA(cudaEventCreate(&r.b));
+    PQLG_CUDA(cudaEventRecordWithFlags(r.a, st, cudaEventRecordExternal));
+    t_graph_recs->push_back(r);
+    g_prof_skip = false;
+    return;
+  }
   g_prof_skip = capturing(st);
   if (g_prof_skip) return;
   ProfRec r{};
@@ -156,6 +172,10 @@ void profile_before(cudaStream_t st, const void* fn) {
 }
 
 void profile_after(cudaStream_t st) {
+  if (t_graph_recs) {
+    PQLG_CUDA(cudaEventRecordWithFlags(t_graph_recs->back().b, st, cudaEventRecordExternal));
+    return;
+  }
   if (g_prof_skip) return;
   cudaEvent_t b;
   {
@@ -163,6 +183,70 @@ void profile_after(cudaStream_t st) {
     b = g_prof_recs.back().b;
   }
   PQLG_CUDA(cudaEventRecord(b, st));
+}
+
+std::string time_in_graph(const std::function<void()>& enqueue, cudaStream_t st, int reps) {
+  require(reps >= 1, "time_in_graph: reps must be >= 1");
+  std::vector<ProfRec> recs;
+  cudaEvent_t g0, g1;
+  PQLG_CUDA(cudaEventCreate(&g0));
+  PQLG_CUDA(cudaEventCreate(&g1));
+  cudaGraph_t g = nullptr;
+  const uint64_t before = g_launches.load();
+  t_graph_recs = &recs;
+  try {
+    PQLG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    enqueue();
+    PQLG_CUDA(cudaStreamEndCapture(st, &g));
+  } catch (...) {
+    t_graph_recs = nullptr;
+    cudaGraph_t junk = nullptr;
+    cudaStreamEndCapture(st, &junk);
+    if (junk) cudaGraphDestroy(junk);
+    throw;
+  }
+  t_graph_recs = nullptr;
+  const uint64_t per = g_launches.load() - before;
+  g_launches.fetch_sub(per);  // captured, not launched
+  cudaGraphExec_t ge;
+  PQLG_CUDA(cudaGraphInstantiate(&ge, g, 0));
+  cudaGraphDestroy(g);
+  std::vector<double> acc(recs.size(), 0.0);
+  double gacc = 0.0;
+  for (int i = 0; i < reps + 2; ++i) {
+    PQLG_CUDA(cudaEventRecord(g0, st));
+    PQLG_CUDA(cudaGraphLaunch(ge, st));
+    PQLG_CUDA(cudaEventRecord(g1, st));
+    PQLG_CUDA(cudaStreamSynchronize(st));
+    if (i < 2) continue;  // warm-up replays
+    float ms = 0.0f;
+    PQLG_CUDA(cudaEventElapsedTime(&ms, g0, g1));
+    gacc += ms;
+    for (size_t k = 0; k < recs.size(); ++k) {
+      PQLG_CUDA(cudaEventElapsedTime(&ms, recs[k].a, recs[k].b));
+      acc[k] += ms;
+    }
+  }
+  count_launch(static_cast<uint64_t>(reps + 2) * per);
+  std::string out;
+  char buf[64];
+  for (size_t k = 0; k < recs.size(); ++k) {
+    const char* name = nullptr;
+    if (cudaFuncGetName(&name, recs[k].fn) != cudaSuccess || !name) name = "?";
+    std::snprintf(buf, sizeof(buf), "\t%.6f\t", acc[k] / reps);
+    out += name;
+    out += buf;
+    out += recs[k].shape;
+    out += '\n';
+    cudaEventDestroy(recs[k].a);
+    cudaEventDestroy(recs[k].b);
+  }
+  std::snprintf(buf, sizeof(buf), "__graph__\t%.6f\t\n", gacc / reps);
+  out += buf;
+  cudaGraphExecDestroy(ge);
+  cudaEventDestroy(g0);
+  cudaEventDestroy(g1);
+  return out;
 }
 }  // namespace pqlg
 

@@ -9,6 +9,9 @@
 #include <atomic>
 #include <cstdint>
 #include <stdexcept>
+#include <algorithm>
+#include <cstring>
+#include <functional>
 #include <string>
 #include <utility>
 
@@ -48,9 +51,27 @@ bool pdl_enabled();
 
 // Per-launch device timing (pqlg_profile_begin/end): when active, launch()
 // brackets every kernel issued outside stream capture with a pair of events.
+// During an instrumented capture (time_in_graph) the same hooks record
+// event-record nodes into the graph instead, so kernels are timed as they run
+// inside the replayed graph.  `shape` describes GEMM launches (groups, M, N, K).
 bool profiling_active();
-void profile_before(cudaStream_t st, const void* fn);
+void profile_before(cudaStream_t st, const void* fn, const char* shape = nullptr);
 void profile_after(cudaStream_t st);
+
+// Captures enqueue() on `st` into a graph with an event-record node before
+// and after every library kernel, replays it `reps` times (after 2 warm-up
+// replays) and returns "kernel\tavg_ms\tshape\n" per launch in launch order,
+// followed by "__graph__\tavg_ms\t\n" (the whole instrumented replay).
+// The event nodes break programmatic-dependent-launch overlap between
+// neighbours, so these are per-kernel durations without PDL prologue overlap.
+// NUL-terminated copy into a caller buffer of `cap` bytes (truncating).
+inline void copy_cstr(const std::string& s, char* out, int cap) {
+  const size_t n = std::min(static_cast<size_t>(cap - 1), s.size());
+  std::memcpy(out, s.data(), n);
+  out[n] = 0;
+}
+
+std::string time_in_graph(const std::function<void()>& enqueue, cudaStream_t st, int reps);
 
 template <class... KArgs, class... Args>
 void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

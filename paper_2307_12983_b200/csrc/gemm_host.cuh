@@ -2,6 +2,7 @@
 // launcher that sizes the grid (m tiles x n tiles x splits*groups).
 #pragma once
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.h"
@@ -119,7 +120,12 @@ void launch_impl(const Operands& ops, Problem p, int groups, const Epi& epi, cud
   cfg.attrs = attr;
   cfg.numAttrs = na;
   const bool prof = profiling_active();
-  if (prof) profile_before(st, reinterpret_cast<const void*>(kern));
+  if (prof) {
+    char shape[96];
+    std::snprintf(shape, sizeof(shape), "groups=%d M=%d N=%d K=%d splits=%d%s%s", groups, p.M,
+                  p.N, p.K, p.splits, kPair ? " pair" : "", k3x ? " 3xtf32" : "");
+    profile_before(st, reinterpret_cast<const void*>(kern), shape);
+  }
   PQLG_CUDA(cudaLaunchKernelEx(&cfg, kern, ops, p, epi));
   count_launch();
   if (prof) profile_after(st);

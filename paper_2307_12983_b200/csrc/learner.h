@@ -56,6 +56,8 @@ class VLearner {
   void debug_read(int what, float* out);
   void set_mt_mode(bool on) { mt_mode_ = on; }
   int kernels_per_update();
+  // Per-kernel device times of the update graph (time_in_graph, common.h).
+  std::string time_update(int reps);
 
   DeviceReplay* replay() { return replay_.get(); }
   int obs_dim() const { return D_; }
@@ -171,6 +173,8 @@ class PLearner {
   int64_t param_count(int which) const;
   void set_mt_mode(bool on) { mt_mode_ = on; }
   int kernels_per_update();
+  // Per-kernel device times of the update graph (time_in_graph, common.h).
+  std::string time_update(int reps);
   uint64_t buffer_size() { return states_->size(); }
   const float* policy_dev() const { return pol_.p; }
   int obs_dim() const { return D_; }

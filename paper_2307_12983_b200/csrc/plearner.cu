@@ -636,6 +636,13 @@ void PLearner::enqueue() {
     if (static_cast<int>(i) != skip) steps_[i](stream_);
 }
 
+std::string PLearner::time_update(int reps) {
+  require(!mt_mode_, "time_update: graph replay needs the Philox sampler");
+  if (states_->size() < static_cast<uint64_t>(B_))
+    throw Error(PQLG_NOT_READY, "policy update before state warm-up");
+  return time_in_graph([&] { enqueue(); }, stream_, reps);
+}
+
 int PLearner::check_status() {
   uint32_t st = 0;
   PQLG_CUDA(cudaMemcpyAsync(&st, status_.p, 4, cudaMemcpyDeviceToHost, stream_));
@@ -878,6 +885,13 @@ int pqlg_plearner_set_sampler(pqlg_plearner h, int mode) {
 
 int pqlg_plearner_kernels_per_update(pqlg_plearner h, int* out) {
   return guarded([&] { *out = h->p->kernels_per_update(); });
+}
+
+int pqlg_plearner_time_update(pqlg_plearner h, int reps, char* out, int cap) {
+  return guarded([&] {
+    require(h && out && cap > 0, "plearner_time_update: null argument");
+    copy_cstr(h->p->time_update(reps), out, cap);
+  });
 }
 
 }  // extern "C"

@@ -636,6 +636,13 @@ void VLearner::enqueue() {
     if (static_cast<int>(i) != skip) steps_[i](stream_);
 }
 
+std::string VLearner::time_update(int reps) {
+  require(!mt_mode_, "time_update: graph replay needs the Philox sampler");
+  if (replay_->size() < static_cast<uint64_t>(B_))
+    throw Error(PQLG_NOT_READY, "critic update before buffer warm-up");
+  return time_in_graph([&] { enqueue(); }, stream_, reps);
+}
+
 int VLearner::check_status() {
   uint32_t st = 0;
   PQLG_CUDA(cudaMemcpyAsync(&st, status_.p, 4, cudaMemcpyDeviceToHost, stream_));
@@ -990,6 +997,13 @@ int pqlg_vlearner_debug_read(pqlg_vlearner h, int what, float* out) {
 
 int pqlg_vlearner_kernels_per_update(pqlg_vlearner h, int* out) {
   return guarded([&] { *out = h->v->kernels_per_update(); });
+}
+
+int pqlg_vlearner_time_update(pqlg_vlearner h, int reps, char* out, int cap) {
+  return guarded([&] {
+    require(h && out && cap > 0, "vlearner_time_update: null argument");
+    copy_cstr(h->v->time_update(reps), out, cap);
+  });
 }
 
 }  // extern "C"

@@ -35,7 +35,7 @@ the compiled reference's own fa::clip_global_norm / fa::adam_step /
 fa::soft_update (optim.hpp:28-79) fed the learner's own pre-clip gradients.
 
 Observed magnitudes are appended to $PQLG_ERRLOG (JSON lines) when set;
-profiles/r2_precision_errors.json is that log from the B200.
+profiles/r2_precision_errors.jsonl is that log from the B200.
 """
 import ctypes as C
 import json
