@@ -560,6 +560,14 @@ PQLG_API int pqlg_env_step(pqlg_env h, const float* act_dev, int64_t ld_act, flo
 PQLG_API int pqlg_k_apply_noise(float* act_dev, int64_t ld, int n, int act_dim,
                                 const float* sigma_dev, float low, float high,
                                 uint64_t* states_dev, void* stream);
+/* The replay sampler's index draw alone (test hook): B indices of
+ * uniform_int_distribution<size_t>(0, count-1) over the Philox URBG
+ * (key, *counter), drawn by the device sampler (parallel draws, and the
+ * sequential Lemire redo when a draw is rejected) for any virtual live count;
+ * *counter advances by the draws consumed; *rejected (nullable) = 1 when the
+ * redo path ran.  Synchronizes. */
+PQLG_API int pqlg_k_sample_indices(uint64_t key, uint64_t* counter, uint64_t count,
+                                   uint64_t batch, uint64_t* out_host, uint32_t* rejected);
 /* RunningNormalizer::update (normalizer.hpp:33-50, :73-83) on device; also
  * writes the fp32 apply constants.  Synchronizes. */
 PQLG_API int pqlg_k_normalizer_update(int64_t* count_dev, double* mean_dev, double* m2_dev,

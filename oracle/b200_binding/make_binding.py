@@ -33,7 +33,8 @@ def edit(text: str, old: str, new: str, count: int = 1) -> str:
 def patch_header(h: str) -> str:
     h = edit(h, '#include "pql/vecenv/vecenv.hpp"\n',
              '#include "pql/vecenv/vecenv.hpp"\n'
-             '\n#ifdef PQL_B200\n#include "pqlg.hpp"  // B200 path: libpqlg.so (include/pqlg.h)\n'
+             '\n#ifdef PQL_B200\n#include <cstdlib>\n#include <cstring>\n'
+             '#include "pqlg.hpp"  // B200 path: libpqlg.so (include/pqlg.h)\n'
              '#define PQL_B200_MUTABLE mutable\n#else\n#define PQL_B200_MUTABLE\n#endif\n')
     b200_member = '#ifdef PQL_B200\n  struct B200;  // the device core (b200_cores.inc)\n' \
                   '  std::shared_ptr<B200> b200_;\n#endif\n};'

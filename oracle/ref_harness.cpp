@@ -26,6 +26,7 @@
 #include "pql/rng.hpp"
 #include "pql/runtime/learners.hpp"
 #include "pql/runtime/metrics.hpp"
+#include "pql/sched/ratio_gate.hpp"
 #include "pql/vecenv/vecenv.hpp"
 
 using namespace pql;
@@ -70,6 +71,67 @@ fa::NormStats make_stats(int64_t count, const double* mean, const double* m2, si
 }
 
 }  // namespace
+
+// ------------------------------------------------- Philox URBG
+// Random123 Philox4x32-10 (the published algorithm; the device uses the same
+// rounds and constants, rng.cuh) as a UniformRandomBitGenerator: draw k is
+// the 64-bit (out0 | out1 << 32) of philox(key, ctr + k).  Driving libstdc++'s
+// own uniform_int_distribution<size_t> -- the call of ReplayBuffer::sample
+// (replay_buffer.hpp:58-60) -- with it defines the device sampler's indices.
+namespace {
+struct PhiloxURBG {
+  using result_type = uint64_t;
+  uint64_t key, ctr;
+  static constexpr result_type min() { return 0; }
+  static constexpr result_type max() { return ~result_type(0); }
+  result_type operator()() {
+    uint32_t c[4] = {static_cast<uint32_t>(ctr), static_cast<uint32_t>(ctr >> 32), 0u, 0u};
+    uint32_t k[2] = {static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32)};
+    for (int round = 0; round < 10; ++round) {
+      const uint64_t p0 = static_cast<uint64_t>(0xD2511F53u) * c[0];
+      const uint64_t p1 = static_cast<uint64_t>(0xCD9E8D57u) * c[2];
+      const uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ c[1] ^ k[0];
+      const uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ c[3] ^ k[1];
+      c[0] = n0;
+      c[1] = static_cast<uint32_t>(p1);
+      c[2] = n2;
+      c[3] = static_cast<uint32_t>(p0);
+      k[0] += 0x9E3779B9u;
+      k[1] += 0xBB67AE85u;
+    }
+    ++ctr;
+    return static_cast<uint64_t>(c[0]) | (static_cast<uint64_t>(c[1]) << 32);
+  }
+};
+}  // namespace
+
+// B draws of std::uniform_int_distribution<size_t>(0, count-1) over PhiloxURBG;
+// returns the advanced counter.
+REF_API uint64_t ref_sample_indices_philox(uint64_t key, uint64_t counter, uint64_t count,
+                                           size_t B, uint64_t* out) {
+  PhiloxURBG g{key, counter};
+  std::uniform_int_distribution<std::size_t> pick(0, count - 1);
+  for (size_t r = 0; r < B; ++r) out[r] = pick(g);
+  return g.ctr;
+}
+
+// RatioGate::may_proceed (ratio_gate.hpp:44-60), compiled from the reference
+REF_API int ref_ratio_may_proceed(int proc, int64_t ca, int64_t cv, int64_t cp, double beta_av,
+                                  double beta_pv, double slack_a, double slack_p,
+                                  double slack_v, int64_t warm_up, int free_running) {
+  sched::RatioConfig c;
+  c.beta_av = beta_av;
+  c.beta_pv = beta_pv;
+  c.slack_a = slack_a;
+  c.slack_p = slack_p;
+  c.slack_v = slack_v;
+  c.warm_up = warm_up;
+  c.free_running = free_running != 0;
+  const sched::Proc p = proc == 0 ? sched::Proc::actor
+                        : proc == 1 ? sched::Proc::vlearner
+                                    : sched::Proc::plearner;
+  return sched::RatioGate::may_proceed(p, ca, cv, cp, c) ? 1 : 0;
+}
 
 // ------------------------------------------------------------ backend
 // kernels::set_backend (kernels.hpp:17-20): 0 scalar (op-order ground truth),
@@ -821,6 +883,90 @@ REF_API void ref_vcore_params(void* h, int which, float* out) {
   const auto& c = r->core->critics();
   const fa::Mlp<float>* nets[4] = {&c.q1, &c.q2, &c.q1_target, &c.q2_target};
   std::memcpy(out, nets[which]->flat.data(), nets[which]->flat.size() * sizeof(float));
+}
+
+// make_snapshot(version) (learners.cpp:190-196): the online nets
+REF_API void ref_vcore_snapshot(void* h, int64_t version, float* q1, float* q2) {
+  auto* r = static_cast<RefVCore*>(h);
+  const rt::CriticSnapshot s = r->core->make_snapshot(version);
+  std::memcpy(q1, s.q1.flat.data(), s.q1.flat.size() * sizeof(float));
+  std::memcpy(q2, s.q2.flat.data(), s.q2.flat.size() * sizeof(float));
+}
+
+// --------------------------------------------------- PolicyLearnerCore
+// The reference's own runtime core (learners.cpp:202-274): ingest (the
+// StateBuffer insert), adopt_critics / adopt_norm, ready, update, snapshot.
+struct RefPCore {
+  RunConfig cfg;
+  size_t D = 0, A = 0;
+  std::unique_ptr<rt::PolicyLearnerCore> core;
+};
+
+REF_API void* ref_pcore_create(size_t batch, size_t capacity, size_t hidden, size_t D, size_t A,
+                               uint64_t seed, uint64_t init_seed, int algo) {
+  auto* r = new RefPCore();
+  r->cfg.batch_size = batch;
+  r->cfg.buffer_capacity = capacity;
+  r->cfg.hidden = hidden;
+  r->cfg.seed = seed;
+  r->cfg.algo = algo == 1 ? agents::Algo::pql_d
+                : algo == 2 ? agents::Algo::pql_sac
+                            : agents::Algo::pql_ddpg;
+  r->D = D;
+  r->A = A;
+  rt::TaskDims dims{D, A, -1.0f, 1.0f};
+  r->core = std::make_unique<rt::PolicyLearnerCore>(r->cfg, dims, std::mt19937_64(init_seed));
+  return r;
+}
+
+REF_API void ref_pcore_destroy(void* h) { delete static_cast<RefPCore*>(h); }
+
+REF_API void ref_pcore_ingest(void* h, const float* states, size_t n) {
+  auto* r = static_cast<RefPCore*>(h);
+  r->core->ingest(make_mat(states, n, r->D));
+}
+
+REF_API int ref_pcore_ready(void* h, int64_t c_a) {
+  return static_cast<RefPCore*>(h)->core->ready(c_a) ? 1 : 0;
+}
+
+REF_API size_t ref_pcore_buffer_size(void* h) {
+  return static_cast<RefPCore*>(h)->core->buffer_size();
+}
+
+REF_API void ref_pcore_adopt_norm(void* h, int64_t count, const double* mean, const double* m2) {
+  auto* r = static_cast<RefPCore*>(h);
+  r->core->adopt_norm(make_stats(count, mean, m2, r->D));
+}
+
+REF_API void ref_pcore_adopt_critics(void* h, const float* q1, const float* q2, int64_t version) {
+  auto* r = static_cast<RefPCore*>(h);
+  const size_t L = agents::is_distributional(r->cfg.algo) ? r->cfg.n_atoms : 1;
+  const size_t sizes[4] = {r->D + r->A, r->cfg.hidden, r->cfg.hidden, L};
+  rt::CriticSnapshot snap;
+  snap.version = version;
+  snap.q1 = make_mlp(sizes, 3, q1);
+  snap.q2 = make_mlp(sizes, 3, q2);
+  r->core->adopt_critics(snap);
+}
+
+REF_API int ref_pcore_update(void* h, float* loss) {
+  auto* r = static_cast<RefPCore*>(h);
+  try {
+    *loss = r->core->update();
+  } catch (const std::exception&) {
+    return -2;
+  }
+  return 0;
+}
+
+// make_snapshot(version) (learners.cpp:272-274): the policy net + log_alpha
+REF_API size_t ref_pcore_snapshot(void* h, int64_t version, float* flat, float* log_alpha) {
+  auto* r = static_cast<RefPCore*>(h);
+  const rt::PolicySnapshot s = r->core->make_snapshot(version);
+  if (flat) std::memcpy(flat, s.net.flat.data(), s.net.flat.size() * sizeof(float));
+  if (log_alpha) *log_alpha = s.log_alpha;
+  return s.net.flat.size();
 }
 
 REF_API void ref_policy_init(size_t D, size_t A, size_t hidden, uint64_t seed, float* out) {

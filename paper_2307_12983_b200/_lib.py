@@ -206,6 +206,7 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_plearner_time_update": (i32, [vp, i32, C.c_char_p, i32]),
     "pqlg_actor_time_steps": (i32, [vp, i32, C.c_char_p, i32]),
     "pqlg_actor_read_slice": (i32, [vp, vp, vp, vp, vp, vp, vp]),
+    "pqlg_k_sample_indices": (i32, [u64, P(u64), u64, u64, vp, P(C.c_uint32)]),
     "pqlg_pipeline_record_snapshots": (i32, [vp, i32]),
     "pqlg_pipeline_check_critics": (i32, [vp, P(i64), P(C.c_double)]),
     "pqlg_pipeline_set_metrics": (i32, [vp, P(MetricsConfig)]),

@@ -604,10 +604,18 @@ void PLearner::adopt_critics_device(const float* q1, const float* q2, int64_t ve
 }
 
 void PLearner::adopt_norm(int64_t count, const double* mean, const double* m2) {
+  // an empty NormStats (count <= 1: identity, normalizer.hpp:18-19) may come
+  // without vectors, as a default-constructed fa::NormStats does
+  require(count <= 1 || (mean && m2), "adopt_norm: mean / m2 required when count > 1");
   norm_count_ = count;
-  norm_mean_.assign(mean, mean + D_);
-  norm_m2_.assign(m2, m2 + D_);
-  norm_.set(count, mean, m2, stream_);
+  if (mean && m2) {
+    norm_mean_.assign(mean, mean + D_);
+    norm_m2_.assign(m2, m2 + D_);
+  } else {
+    norm_mean_.assign(D_, 0.0);
+    norm_m2_.assign(D_, 0.0);
+  }
+  norm_.set(count, norm_mean_.data(), norm_m2_.data(), stream_);
 }
 
 void PLearner::ingest(const float* states, int64_t ld, uint64_t n) {

@@ -181,6 +181,31 @@ int pqlg_replay_sample(pqlg_replay h, uint64_t batch, pqlg_rng* rng, uint64_t mi
   return rc;
 }
 
+int pqlg_k_sample_indices(uint64_t key, uint64_t* counter, uint64_t count, uint64_t batch,
+                          uint64_t* out_host, uint32_t* rejected) {
+  return guarded([&] {
+    require(counter && out_host && count >= 1 && batch >= 1, "sample_indices: bad arguments");
+    cudaStream_t st;
+    PQLG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    DevBuf<replay::SamplerState> ss(1);
+    DevBuf<uint64_t> out(batch);
+    const replay::SamplerState s0{key, *counter, 0, 0};
+    PQLG_CUDA(cudaMemcpyAsync(ss.p, &s0, sizeof(s0), cudaMemcpyHostToDevice, st));
+    const uint64_t blocks = (batch + replay::kSampleRows - 1) / replay::kSampleRows;
+    // the reject flag is cleared by the finish: read it through a probe copy
+    // taken before (flag state after the draws is what the finish saw)
+    launch(replay::sample_indices_kernel, dim3(static_cast<unsigned>(blocks)),
+           dim3(32 * kWarpsPerBlock), 0, st, ss.p, count, batch, out.p);
+    replay::SamplerState s1{};
+    PQLG_CUDA(cudaMemcpyAsync(&s1, ss.p, sizeof(s1), cudaMemcpyDeviceToHost, st));
+    PQLG_CUDA(cudaMemcpyAsync(out_host, out.p, batch * 8, cudaMemcpyDeviceToHost, st));
+    PQLG_CUDA(cudaStreamSynchronize(st));
+    PQLG_CUDA(cudaStreamDestroy(st));
+    if (rejected) *rejected = (s1.counter - *counter) > batch ? 1u : 0u;
+    *counter = s1.counter;
+  });
+}
+
 int pqlg_replay_fill_synthetic(pqlg_replay h, uint64_t n, uint64_t seed, float disc,
                                uint32_t terminal_every) {
   return guarded([&] {

@@ -519,6 +519,25 @@ __device__ __forceinline__ void draw_block_indices(const SamplerState* ss,
   __syncthreads();
 }
 
+// Index-only sampling (test hook pqlg_k_sample_indices): the sampler's own
+// parallel draw and ticketed finish (including the sequential Lemire redo)
+// over a virtual live count, the indices written to `out` instead of rows
+// being gathered.  With count just above 2^63 about half the draws land in
+// the rejection zone, so the redo path runs.
+static __global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    sample_indices_kernel(SamplerState* ss, uint64_t count, uint64_t B, uint64_t* out) {
+  __shared__ uint64_t s_idx[kSampleRows];
+  pdl::entry();
+  draw_block_indices(ss, nullptr, count, B, s_idx);
+  if (threadIdx.x < kSampleRows) {
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kSampleRows + threadIdx.x;
+    if (r < B) out[r] = s_idx[threadIdx.x];
+  }
+  finish_sample(ss, nullptr, count, B, [&](uint64_t i, uint64_t r, int ln) {
+    if (ln == 0) out[r] = i;
+  });
+}
+
 static __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     replay_sample_kernel(const __grid_constant__ Ring ring, const __grid_constant__ Norm norm,
                          const __grid_constant__ Gather g, SamplerState* ss,

@@ -114,6 +114,18 @@ _REF_SIGS = {
                                   sz, f32, f32, sz, f32, f32, vp, vp, vp]),
     "ref_c51_actor_loss": (i32, [vp, vp, vp, vp, vp, sz, vp, sz, sz, f32, f32, sz, f32, f32, vp,
                                  vp]),
+    "ref_vcore_snapshot": (None, [vp, i64, vp, vp]),
+    "ref_pcore_create": (vp, [sz, sz, sz, sz, sz, u64, u64, i32]),
+    "ref_pcore_destroy": (None, [vp]),
+    "ref_pcore_ingest": (None, [vp, vp, sz]),
+    "ref_pcore_ready": (i32, [vp, i64]),
+    "ref_pcore_buffer_size": (sz, [vp]),
+    "ref_pcore_adopt_norm": (None, [vp, i64, vp, vp]),
+    "ref_pcore_adopt_critics": (None, [vp, vp, vp, i64]),
+    "ref_pcore_update": (i32, [vp, vp]),
+    "ref_pcore_snapshot": (sz, [vp, i64, vp, vp]),
+    "ref_sample_indices_philox": (u64, [u64, u64, u64, sz, vp]),
+    "ref_ratio_may_proceed": (i32, [i32, i64, i64, i64, f64, f64, f64, f64, f64, i64, i32]),
     "ref_set_backend": (None, [i32]),
     "ref_active_backend": (i32, []),
     "ref_synth_env_create": (vp, [sz, sz, sz, u64, sz, f32, f32, i32, vp]),
@@ -165,6 +177,8 @@ _REF_SIGS = {
 
 _orc = None
 _ref = None
+_ref_b200 = None
+REF_B200_SO = ORACLE / "_ref" / "libpqlref_b200.so"
 
 
 def _bind(path: Path, sigs: dict) -> C.CDLL:
@@ -191,6 +205,16 @@ def ref():
     if _ref is None and REF_SO.exists():
         _ref = _bind(REF_SO, _REF_SIGS)
     return _ref
+
+
+def ref_b200():
+    """The reference with its runtime cores bound to libpqlg.so (oracle/Makefile
+    b200: learners.hpp/.cpp patched at build time under PQL_B200), driven by
+    the same ref_* entry points; None if it was not built."""
+    global _ref_b200
+    if _ref_b200 is None and REF_B200_SO.exists():
+        _ref_b200 = _bind(REF_B200_SO, _REF_SIGS)
+    return _ref_b200
 
 
 def ptr(a: np.ndarray):

@@ -1,8 +1,14 @@
 """run_parallel pacing rule on CPU: pqlg_ratio_may_proceed (the library's
-RatioGate::may_proceed) against a direct transcription of
-proj/include/pql/sched/ratio_gate.hpp:44-60 over a grid of counters, plus
-the SPEC.md pacing examples.  Pure host logic: no GPU needed."""
+RatioGate::may_proceed) against the compiled reference's own
+sched::RatioGate::may_proceed (ratio_gate.hpp:44-60, ref_ratio_may_proceed
+in oracle/ref_harness.cpp) and a transcription of it, over a grid of
+counters and ratio settings, plus the SPEC.md pacing examples.  Pure host
+logic: no GPU needed."""
 import itertools
+
+import pytest
+
+from oracle_lib import ref
 
 from paper_2307_12983_b200 import _lib
 
@@ -34,6 +40,25 @@ def test_may_proceed_matches_reference_rule_on_a_grid():
                                                range(0, 600, 23), range(0, 300, 17)):
             got = _lib.lib().pqlg_ratio_may_proceed(p, ca, cv, cp, rc)
             assert got == int(ref_may_proceed(p, ca, cv, cp, rc)), (free, p, ca, cv, cp)
+
+
+def test_may_proceed_matches_compiled_ratio_gate():
+    R = ref()
+    if R is None:
+        pytest.skip("oracle/_ref not built")
+    n = 0
+    for free, beta_av, beta_pv, slack_a, warm in itertools.product(
+            (0, 1), (1 / 8, 1 / 4, 1.0, 3.0), (1 / 2, 1.0, 0.25), (4.0, 0.0, 2.5), (32, 0, 7)):
+        rc = _lib.ratio_config(free_running=free, beta_av=beta_av, beta_pv=beta_pv,
+                               slack_a=slack_a, warm_up=warm)
+        for p, ca, cv, cp in itertools.product(range(3), (0, 6, 7, 31, 32, 33, 64, 101),
+                                               range(0, 420, 37), range(0, 220, 29)):
+            want = R.ref_ratio_may_proceed(p, ca, cv, cp, rc.beta_av, rc.beta_pv, rc.slack_a,
+                                           rc.slack_p, rc.slack_v, rc.warm_up, rc.free_running)
+            assert _lib.lib().pqlg_ratio_may_proceed(p, ca, cv, cp, rc) == want, \
+                (free, beta_av, beta_pv, slack_a, warm, p, ca, cv, cp)
+            n += 1
+    assert n > 100_000
 
 
 def test_pacing_examples():
