@@ -199,6 +199,9 @@ def test_pipeline_p_learner_critics_are_a_published_snapshot(free_running, publi
         _lib.call("pqlg_pipeline_destroy", h)
     print(f"\nfree={free_running} K_pub={publish_every}: critic versions published "
           f"{rep.critic_version}, P-learner holds {ver.value}, max|diff| {diff.value}")
-    assert rep.ok == 1 and rep.critic_version >= 2
+    assert rep.ok == 1 and rep.critic_version >= 1
+    # every actor iteration after the first publish forwards a batch; most
+    # of them carry no new snapshot (the stale-slot case) when free running
+    assert rep.batches_sent > rep.critic_version
     assert ver.value >= 1
     assert diff.value == 0.0

@@ -210,3 +210,37 @@ def test_state_buffer_insert_sample(mode):
     _lib.call("pqlg_states_sample", s, B, C.byref(r), B, None, out.data_ptr(), 0)
     assert np.array_equal(host(out), ring[idx.astype(np.int64)])
     _lib.call("pqlg_states_destroy", s)
+
+
+@pytest.mark.parametrize("count,B", [(1, 8), (100, 64), (5_000_000, 8192), (30_000, 300),
+                                     ((1 << 63) + 1, 512), ((3 << 62) + 12345, 300),
+                                     ((1 << 64) - 1, 256)])
+def test_device_sampler_indices_match_libstdcxx_over_philox(count, B):
+    """The device sampler's index draw (parallel Philox draws + Lemire, and
+    the last block's sequential redo when any draw is rejected) equals
+    libstdc++'s own uniform_int_distribution<size_t>(0, count-1) driven by
+    the same Philox URBG (compiled into the reference harness), including
+    counts above 2^63 where about half the draws are rejected, so the redo
+    path runs."""
+    from oracle_lib import orc, ref
+    key = 0x0F1E_2D3C_4B5A_6978 ^ count
+    for ctr0 in (0, 11, (1 << 41) + 5):
+        got = np.zeros(B, np.uint64)
+        ctr = C.c_uint64(ctr0)
+        rej = C.c_uint32()
+        _lib.call("pqlg_k_sample_indices", key, C.byref(ctr), count, B, got.ctypes.data,
+                  C.byref(rej))
+        want = np.zeros(B, np.uint64)
+        R = ref()
+        if R is not None:
+            ctr_ref = R.ref_sample_indices_philox(key, ctr0, count, B, want.ctypes.data)
+        else:  # the restatement, itself pinned to the reference (test_sampler_cpu.py)
+            c = np.array([ctr0], np.uint64)
+            orc().orc_sample_indices_philox(key, c.ctypes.data, count, B, want.ctypes.data)
+            ctr_ref = int(c[0])
+        assert np.array_equal(got, want)
+        assert ctr.value == ctr_ref
+        if count == (1 << 63) + 1:
+            assert rej.value == 1 and ctr.value - ctr0 > B
+        if count <= 5_000_000:
+            assert rej.value == 0 and ctr.value - ctr0 == B
