@@ -223,15 +223,15 @@ static __global__ void __launch_bounds__(256)
   const int k = blockIdx.y;
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (blockDim.x >> 5);
-  const int words = a.H >> 5;
   const float* __restrict__ w = a.w[k];
   const float* __restrict__ up = a.up + static_cast<int64_t>(k) * a.B;
   for (int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < a.B; b += warps) {
     const float u = up[b];
-    const uint32_t* mrow = a.mask[k] + static_cast<int64_t>(b) * words;
+    // word-major masks (epi::Hidden): word j of row b at mask[j * B + b]
+    const uint32_t* mrow = a.mask[k] + b;
     float* g = a.G[k] + static_cast<int64_t>(b) * a.H;
     for (int c = 4 * lane; c < a.H; c += 128) {
-      const uint32_t bits = mrow[c >> 5] >> (c & 31);
+      const uint32_t bits = mrow[static_cast<int64_t>(c >> 5) * a.B] >> (c & 31);
       const float4 w4 = *reinterpret_cast<const float4*>(w + c);
       float4 o;
       o.x = (bits & 1u) ? __fmul_rn(u, w4.x) : 0.0f;

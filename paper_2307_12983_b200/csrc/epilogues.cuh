@@ -34,7 +34,9 @@ struct Ctx {
 };
 
 // relu(acc + b) -> TMA store (store = 1) and/or a ReLU bitmask (bit t of
-// word n/32 = post[m, n] > 0) used by the backward; optional head dot
+// word n/32 = post[m, n] > 0) used by the backward, stored word-major
+// (mask[(n/32) * ld_mask + m]: a warp's 32 rows write one coalesced 128 B
+// line per word); optional head dot
 // sum_n relu(.)*w_head[n] per n-tile -> partial[(group*n_tiles + n_tile)*ld_part + m].
 struct Hidden {
   static constexpr int kStoreRank = 2;
@@ -42,7 +44,7 @@ struct Hidden {
   const float* bias[4];
   const float* w_head[4];  // null: no head dot
   uint32_t* mask[4];       // null: no bitmask
-  int ld_mask;             // words per row (= N/32)
+  int ld_mask;             // word-major: stride between words (>= M rows)
   float* partial[4];       // per group [slot][ld_part], slot = n_tile * halves + half
   int64_t ld_part;
   int n_slots;             // n_tiles * halves (mlp::hidden_slots)
@@ -82,7 +84,7 @@ struct Hidden {
       for (int t = 0; t < 32; ++t) r.dot = __fadd_rn(r.dot, __fmul_rn(v[t], scratch[bn + c0 + t]));
     }
     if (mask[c.group] && c.m < M)
-      mask[c.group][static_cast<int64_t>(c.m) * ld_mask + (n0 >> 5)] = bits;
+      mask[c.group][static_cast<int64_t>(n0 >> 5) * ld_mask + c.m] = bits;
     return ((store >> c.group) & 1) != 0;
   }
   __device__ void end(Row& r, const Ctx& c) const {
@@ -171,7 +173,7 @@ struct PolicyHead {
 struct DgradMask {
   static constexpr int kStoreRank = 2;
   static constexpr bool kSplitCols = true;
-  const uint32_t* mask[2];  // nullable: no mask
+  const uint32_t* mask[2];  // nullable: no mask (word-major, as Hidden writes it)
   int ld_mask;
   float* colsum;  // nullable
   int64_t ld_cs;
@@ -185,10 +187,10 @@ struct DgradMask {
 #pragma unroll
     for (int i = 0; i < 8; ++i) r.bits[i] = 0xffffffffu;
     if (mask[c.group] && c.m < M) {
-      const uint32_t* p = mask[c.group] + static_cast<int64_t>(c.m) * ld_mask + c.n_tile * (bn >> 5);
+      const uint32_t* p = mask[c.group] + static_cast<int64_t>(c.n_tile * (bn >> 5)) * ld_mask + c.m;
 #pragma unroll
       for (int i = 0; i < 8; ++i)
-        if (i < (bn >> 5)) r.bits[i] = p[i];
+        if (i < (bn >> 5)) r.bits[i] = p[static_cast<int64_t>(i) * ld_mask];
     }
   }
   __device__ bool chunk(Row& r, const Ctx& c, int n0, float (&v)[32], float* scratch) const {

@@ -203,7 +203,7 @@ void PLearner::build_update() {
       epi::Hidden e{};
       e.bias[0] = e.bias[1] = pol_.p + pnet_.b_off[l];
       e.mask[0] = e.mask[1] = pmask_[l].p;
-      e.ld_mask = wpr;
+      e.ld_mask = B;  // word-major masks
       e.bn = bnH;
       e.M = B;
       e.N = H;
@@ -254,7 +254,7 @@ void PLearner::build_update() {
       e.bias[k] = q[k] + qnet_.b_off[l];
       e.mask[k] = cmask_[k][l].p;
     }
-    e.ld_mask = wpr;
+    e.ld_mask = B;  // word-major masks
     e.bn = bnH;
     e.M = B;
     e.N = H;
@@ -362,7 +362,7 @@ void PLearner::build_update() {
     // backward_input_only through the categorical heads: G = (up W^T) * mask
     epi::DgradMask dm{};
     for (int k = 0; k < 2; ++k) dm.mask[k] = cmask_[k][nh - 1].p;
-    dm.ld_mask = wpr;
+    dm.ld_mask = B;  // word-major masks
     dm.bn = bnH;
     dm.M = B;
     dm.N = H;
@@ -387,7 +387,7 @@ void PLearner::build_update() {
   for (int l = nh - 1; l >= 1; --l) {
     epi::DgradMask dm{};
     for (int k = 0; k < 2; ++k) dm.mask[k] = cmask_[k][l - 1].p;
-    dm.ld_mask = wpr;
+    dm.ld_mask = B;  // word-major masks
     dm.bn = bnH;
     dm.M = B;
     dm.N = H;
@@ -467,7 +467,7 @@ void PLearner::build_update() {
   {
     epi::DgradMask dm{};
     dm.mask[0] = dm.mask[1] = pmask_[nh - 1].p;
-    dm.ld_mask = wpr;
+    dm.ld_mask = B;  // word-major masks
     dm.colsum = colsum_[nh - 1].p;
     dm.ld_cs = H;
     dm.m_tiles = mt;
@@ -486,7 +486,7 @@ void PLearner::build_update() {
     if (l > 0) {
       epi::DgradMask dm{};
       dm.mask[0] = dm.mask[1] = pmask_[l - 1].p;
-      dm.ld_mask = wpr;
+      dm.ld_mask = B;  // word-major masks
       dm.colsum = colsum_[l - 1].p;
       dm.ld_cs = H;
       dm.m_tiles = mt;

@@ -202,6 +202,7 @@ def test_pipeline_p_learner_critics_are_a_published_snapshot(free_running, publi
     assert rep.ok == 1 and rep.critic_version >= 1
     # every actor iteration after the first publish forwards a batch; most
     # of them carry no new snapshot (the stale-slot case) when free running
-    assert rep.batches_sent > rep.critic_version
+    if free_running:
+        assert rep.batches_sent > rep.critic_version
     assert ver.value >= 1
     assert diff.value == 0.0
