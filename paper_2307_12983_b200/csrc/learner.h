@@ -15,6 +15,8 @@ struct pqlg_comm_s;
 
 namespace pqlg {
 
+class DpBuckets;  // dp_buckets.h
+
 // CriticLearnerCore (learners.hpp:77-106).
 class VLearner {
  public:
@@ -84,6 +86,7 @@ class VLearner {
   int L_ = 1, Lp_ = 1;
   float reward_scale_, gamma_;
   EpsStream eps_;      // pql_sac eps draws
+  std::unique_ptr<DpBuckets> dp_;  // data-parallel gradient buckets (comm_ only)
   DevBuf<float> logp_; // log pi(a'|s+) [B]
   NetShape qnet_, pnet_;
   int64_t Ps_ = 0;  // group stride of the twin-critic parameter blocks
@@ -124,7 +127,6 @@ class VLearner {
   DevBuf<double> block_sq_;
   DevBuf<unsigned int> fin_counter_;
   DevBuf<float> scale_;
-  DevBuf<double> block_sq2_;  // data-parallel: norm pass after the all-reduce
   // C51 (PQL-D) head state: atoms, target/online probabilities, expected
   // values, upstream [2][B x Lp], head-bias partials, head weight partials,
   // padded head mirrors (q1, q2, q1_target, q2_target)
@@ -234,7 +236,7 @@ class PLearner {
   DevBuf<double> block_sq_;
   DevBuf<unsigned int> fin_counter_;
   DevBuf<float> scale_;
-  DevBuf<double> block_sq2_;
+  std::unique_ptr<DpBuckets> dp_;  // data-parallel gradient buckets (comm_ only)
   DevBuf<float> atoms_, probs_, ev_, up51_;  // C51 actor objective
   std::array<WeightMirror, 2> heads_;
 

@@ -16,6 +16,7 @@
 #include "c51_kernels.cuh"
 #include "comm.h"
 #include "critic_kernels.cuh"
+#include "dp_buckets.h"
 #include "learner.h"
 #include "optim.cuh"
 #include "sac_host.h"
@@ -461,9 +462,37 @@ void PLearner::build_update() {
     wpart_[l].alloc(static_cast<size_t>(wsplits_[l]) * in * ldo);
     if (l < nh) colsum_[l].alloc(static_cast<size_t>(mt) * H);
   }
+  // gradient segments of policy layer l (l == nh: the head), see VLearner
+  auto layer_segs = [&](int l) {
+    std::vector<optim::Segment> v;
+    if (l == nh) {
+      optim::Segment wh{pnet_.w_off[nh], static_cast<int64_t>(H) * Ah_, wpart_[nh].p, 0,
+                        wsplits_[nh], static_cast<int64_t>(H) * Ahp_};
+      wh.cols = Ah_;
+      wh.ld_src = Ahp_;
+      v.push_back(wh);
+      v.push_back(optim::Segment{pnet_.b_off[nh], Ah_, head_db_.p, 0, ptiles, Ah_});
+    } else {
+      const int in = l == 0 ? D : H;
+      v.push_back(optim::Segment{pnet_.w_off[l], static_cast<int64_t>(in) * H, wpart_[l].p, 0,
+                                 wsplits_[l], static_cast<int64_t>(in) * H});
+      v.push_back(optim::Segment{pnet_.b_off[l], H, colsum_[l].p, 0, mt, H});
+    }
+    return v;
+  };
+  // data parallel: bucketed reduce + all-reduce per layer (dp_buckets.h); the
+  // head bucket carries the loss (and pql_sac's mean log-prob, loss_[1])
+  if (comm_) dp_ = std::make_unique<DpBuckets>(comm_, grads_.p, 1, pnet_.params);
+  auto dp_bucket = [&](int l) {
+    const int64_t lo = pnet_.w_off[l], hi = pnet_.b_off[l] + pnet_.sizes[l + 1];
+    const bool head = l == nh;
+    steps_.push_back(dp_->bucket(layer_segs(l), lo, hi, head ? loss_.p : nullptr,
+                                 head ? (sac_ ? 2 : 1) : 0));
+  };
   // head layer: dW_nh = act_{nh-1}^T dy ; G_{nh-1} = (dy W_nh^T) * mask
   steps_.push_back(mlp::wgrad(pact_[nh - 1].p, pact_[nh - 1].p, H, dy_.p, dy_.p, Ahp_, H, Ah_, B,
                               1, wsplits_[nh], epi::Partial{}, wpart_[nh].p, Ahp_));
+  if (dp_) dp_bucket(nh);
   {
     epi::DgradMask dm{};
     dm.mask[0] = dm.mask[1] = pmask_[nh - 1].p;
@@ -483,6 +512,7 @@ void PLearner::build_update() {
     const int64_t ldh = l == 0 ? Kp_ : H;
     steps_.push_back(mlp::wgrad(h, h, ldh, Gp_[l].p, Gp_[l].p, H, in, H, B, 1, wsplits_[l],
                                 epi::Partial{}, wpart_[l].p));
+    if (dp_) dp_bucket(l);
     if (l > 0) {
       epi::DgradMask dm{};
       dm.mask[0] = dm.mask[1] = pmask_[l - 1].p;
@@ -502,18 +532,14 @@ void PLearner::build_update() {
   {
     optim::FinalizeArgs f{};
     int s = 0;
-    for (int l = 0; l < nh; ++l) {
-      const int in = l == 0 ? D : H;
-      f.seg[s++] = optim::Segment{pnet_.w_off[l], static_cast<int64_t>(in) * H, wpart_[l].p, 0,
-                                  wsplits_[l], static_cast<int64_t>(in) * H};
-      f.seg[s++] = optim::Segment{pnet_.b_off[l], H, colsum_[l].p, 0, mt, H};
+    if (comm_) {  // the buckets hold the all-reduced gradient: norm + clip pass
+      steps_.push_back(dp_->join());
+      f.seg[s++] = optim::Segment{0, pnet_.params, grads_.p, 0, 1, 0};
+      f.check = loss_.p;
+    } else {
+      for (int l = 0; l <= nh; ++l)
+        for (const auto& sg : layer_segs(l)) f.seg[s++] = sg;
     }
-    optim::Segment wh{pnet_.w_off[nh], static_cast<int64_t>(H) * Ah_, wpart_[nh].p, 0,
-                      wsplits_[nh], static_cast<int64_t>(H) * Ahp_};
-    wh.cols = Ah_;
-    wh.ld_src = Ahp_;
-    f.seg[s++] = wh;
-    f.seg[s++] = optim::Segment{pnet_.b_off[nh], Ah_, head_db_.p, 0, ptiles, Ah_};
     require(s <= optim::kMaxSegments, "plearner: too many layers");
     f.n_seg = s;
     f.total = pnet_.params;
@@ -528,29 +554,9 @@ void PLearner::build_update() {
     f.scale = scale_.p;
     f.status = status_.p;
     f.max_norm = 0.5f;
-    f.skip_norm = comm_ ? 1 : 0;
     steps_.push_back([f, fb](cudaStream_t st) {
       launch(optim::finalize_kernel, dim3(dim3(fb, 1)), dim3(optim::kFinalizeThreads), 0, st, f);
     });
-    if (comm_) {  // data parallel: see VLearner::build_update
-      pqlg_comm_s* c = comm_;
-      float* g = grads_.p;
-      float* l = loss_.p;
-      const size_t n = static_cast<size_t>(pnet_.params);
-      const int nl = sac_ ? 2 : 1;  // + the mean log-prob of the alpha update
-      steps_.push_back([c, g, n, l, nl](cudaStream_t st) { allreduce_sum(c, g, n, l, nl, st); });
-      optim::FinalizeArgs f2 = f;
-      f2.seg[0] = optim::Segment{0, pnet_.params, grads_.p, 0, 1, 0};
-      f2.n_seg = 1;
-      f2.skip_norm = 0;
-      f2.check = loss_.p;
-      const int fb2 = optim::plan_finalize(f2);
-      block_sq2_.alloc(fb2);
-      f2.block_sq = block_sq2_.p;
-      steps_.push_back([f2, fb2](cudaStream_t st) {
-        launch(optim::finalize_kernel, dim3(dim3(fb2, 1)), dim3(optim::kFinalizeThreads), 0, st, f2);
-      });
-    }
     optim::AdamArgs a{};
     a.p = pol_.p;
     a.g = grads_.p;

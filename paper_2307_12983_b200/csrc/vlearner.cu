@@ -14,6 +14,7 @@
 #include "c51_kernels.cuh"
 #include "comm.h"
 #include "critic_kernels.cuh"
+#include "dp_buckets.h"
 #include "learner.h"
 #include "optim.cuh"
 #include "sac_host.h"
@@ -388,6 +389,48 @@ void VLearner::build_update() {
   head_dw_.alloc(2ull * ht * H);
   head_db_.alloc(2ull * ht);
   head_cs_.alloc(2ull * ht * H);
+  // gradient segments (split-K / row-tile partials -> flat gradient) of
+  // hidden layer l and of the head layer, for the finalize pass(es)
+  auto layer_segs = [&](int l) {
+    const int in = l == 0 ? K0 : H;
+    std::vector<optim::Segment> v;
+    v.push_back(optim::Segment{qnet_.w_off[l], static_cast<int64_t>(in) * H, wpart_[l].p,
+                               static_cast<int64_t>(wsplits_[l]) * in * H, wsplits_[l],
+                               static_cast<int64_t>(in) * H});
+    if (l + 1 < nh || dist_)
+      v.push_back(optim::Segment{qnet_.b_off[l], H, colsum_[l].p, static_cast<int64_t>(mt) * H,
+                                 mt, H});
+    else  // the last hidden layer's bias gradient comes from the head backward
+      v.push_back(optim::Segment{qnet_.b_off[l], H, head_cs_.p, static_cast<int64_t>(ht) * H,
+                                 ht, H});
+    return v;
+  };
+  auto head_segs = [&]() {
+    std::vector<optim::Segment> v;
+    if (dist_) {
+      optim::Segment wh{qnet_.w_off[nh], static_cast<int64_t>(H) * L_, head_wpart_.p,
+                        static_cast<int64_t>(head_splits_) * H * Lp_, head_splits_,
+                        static_cast<int64_t>(H) * Lp_};
+      wh.cols = L_;
+      wh.ld_src = Lp_;
+      v.push_back(wh);
+      v.push_back(optim::Segment{qnet_.b_off[nh], L_, db51_.p,
+                                 static_cast<int64_t>(c51_blocks_) * L_, c51_blocks_, L_});
+    } else {
+      v.push_back(optim::Segment{qnet_.w_off[nh], H, head_dw_.p, static_cast<int64_t>(ht) * H,
+                                 ht, H});
+      v.push_back(optim::Segment{qnet_.b_off[nh], 1, head_db_.p, ht, ht, 1});
+    }
+    return v;
+  };
+  // data parallel: bucketed reduce + all-reduce per layer on
+  // a communication branch, issued as each layer's gradient completes
+  if (comm_) dp_ = std::make_unique<DpBuckets>(comm_, grads_.p, 2, Ps_);
+  auto dp_bucket = [&](std::vector<optim::Segment> segs, int layer, bool with_loss) {
+    const int64_t lo = qnet_.w_off[layer], hi = qnet_.b_off[layer] + qnet_.sizes[layer + 1];
+    steps_.push_back(dp_->bucket(std::move(segs), lo, hi, with_loss ? loss_.p : nullptr,
+                                 with_loss ? 1 : 0));
+  };
   if (dist_) {
     // categorical head layer H -> L (fa::backward, mlp.hpp:161-184):
     //   dW_head = h^T up   (split-K over the batch, fixed-order reduction)
@@ -409,6 +452,7 @@ void VLearner::build_update() {
     dm.N = H;
     steps_.push_back(mlp::dgrad(u0, u1, Lp_, heads_[0].ptr(), heads_[1].ptr(), heads_[0].stride(),
                                 B, H, L_, 2, dm, G_[0][nh - 1].p, G_[1][nh - 1].p, H));
+    if (dp_) dp_bucket(head_segs(), nh, true);
   } else {
     critic::HeadBwdArgs a{};
     a.up = up_.p;
@@ -429,6 +473,7 @@ void VLearner::build_update() {
     steps_.push_back([a, ht](cudaStream_t st) {
       launch(critic::head_backward_kernel, dim3(dim3(ht, 2)), dim3(critic::kHeadThreads), 0, st, a);
     });
+    if (dp_) dp_bucket(head_segs(), nh, true);
   }
   for (int l = nh - 1; l >= 0; --l) {
     const int in = l == 0 ? K0 : H;
@@ -438,6 +483,7 @@ void VLearner::build_update() {
     const int64_t ldh = l == 0 ? Kp_ : H;
     steps_.push_back(mlp::wgrad(h0, h1, ldh, G_[0][l].p, G_[1][l].p, H, in, H, B, 2,
                                 wsplits_[l], epi::Partial{}, wpart_[l].p));
+    if (dp_) dp_bucket(layer_segs(l), l, false);
     if (l > 0) {
       // dgrad: G_{l-1} = (G_l W_l^T) * [act_{l-1} > 0], + bias colsums of layer l-1
       epi::DgradMask dm{};
@@ -459,31 +505,18 @@ void VLearner::build_update() {
   {
     optim::FinalizeArgs f{};
     int s = 0;
-    for (int l = 0; l < nh; ++l) {
-      const int in = l == 0 ? K0 : H;
-      f.seg[s++] = optim::Segment{qnet_.w_off[l], static_cast<int64_t>(in) * H, wpart_[l].p,
-                                  static_cast<int64_t>(wsplits_[l]) * in * H, wsplits_[l],
-                                  static_cast<int64_t>(in) * H};
-      if (l + 1 < nh || dist_)
-        f.seg[s++] = optim::Segment{qnet_.b_off[l], H, colsum_[l].p,
-                                    static_cast<int64_t>(mt) * H, mt, H};
-      else
-        f.seg[s++] = optim::Segment{qnet_.b_off[l], H, head_cs_.p, static_cast<int64_t>(ht) * H,
-                                    ht, H};
-    }
-    if (dist_) {
-      optim::Segment wh{qnet_.w_off[nh], static_cast<int64_t>(H) * L_, head_wpart_.p,
-                        static_cast<int64_t>(head_splits_) * H * Lp_, head_splits_,
-                        static_cast<int64_t>(H) * Lp_};
-      wh.cols = L_;
-      wh.ld_src = Lp_;
-      f.seg[s++] = wh;
-      f.seg[s++] = optim::Segment{qnet_.b_off[nh], L_, db51_.p,
-                                  static_cast<int64_t>(c51_blocks_) * L_, c51_blocks_, L_};
+    if (comm_) {
+      // the buckets hold the all-reduced full-batch gradient (each rank's
+      // upstream already carries 1/(B*world)): the norm + clip scale
+      // (clip_global_norm per critic, learners.cpp:182-183) as a
+      // single-term pass over it, flagging a non-finite all-reduced loss
+      steps_.push_back(dp_->join());
+      f.seg[s++] = optim::Segment{0, P, grads_.p, Ps_, 1, 0};
+      f.check = loss_.p;
     } else {
-      f.seg[s++] = optim::Segment{qnet_.w_off[nh], H, head_dw_.p, static_cast<int64_t>(ht) * H,
-                                  ht, H};
-      f.seg[s++] = optim::Segment{qnet_.b_off[nh], 1, head_db_.p, ht, ht, 1};
+      for (int l = 0; l < nh; ++l)
+        for (const auto& sg : layer_segs(l)) f.seg[s++] = sg;
+      for (const auto& sg : head_segs()) f.seg[s++] = sg;
     }
     require(s <= optim::kMaxSegments, "vlearner: too many layers");
     f.n_seg = s;
@@ -499,33 +532,10 @@ void VLearner::build_update() {
     f.scale = scale_.p;
     f.status = status_.p;
     f.max_norm = 0.5f;
-    f.skip_norm = comm_ ? 1 : 0;
     const int fb = fin_blocks_;
     steps_.push_back([f, fb](cudaStream_t st) {
       launch(optim::finalize_kernel, dim3(dim3(fb, 2)), dim3(optim::kFinalizeThreads), 0, st, f);
     });
-    if (comm_) {
-      // data parallel: sum the twin gradients (each rank's upstream already
-      // carries 1/(B*world)) and the loss over ranks, then the norm + clip
-      // scale of the full-batch gradient (clip_global_norm per critic,
-      // learners.cpp:182-183) as an in-place single-term pass.
-      pqlg_comm_s* c = comm_;
-      float* g = grads_.p;
-      float* l = loss_.p;
-      const size_t n = 2 * static_cast<size_t>(Ps_);
-      steps_.push_back([c, g, n, l](cudaStream_t st) { allreduce_sum(c, g, n, l, 1, st); });
-      optim::FinalizeArgs f2 = f;
-      f2.seg[0] = optim::Segment{0, P, grads_.p, Ps_, 1, 0};
-      f2.n_seg = 1;
-      f2.skip_norm = 0;
-      f2.check = loss_.p;
-      const int fb2 = optim::plan_finalize(f2);
-      block_sq2_.alloc(2ull * fb2);
-      f2.block_sq = block_sq2_.p;
-      steps_.push_back([f2, fb2](cudaStream_t st) {
-        launch(optim::finalize_kernel, dim3(dim3(fb2, 2)), dim3(optim::kFinalizeThreads), 0, st, f2);
-      });
-    }
   }
   // ------------------------------------------------ clip + Adam + Polyak
   {

@@ -2,9 +2,10 @@
 
 The round-end box has one GPU, so the multi-rank exchange itself is covered
 by the gloo tests in test_dp_cpu.py; here a world-1 NCCL communicator runs
-the data-parallel update path (reduction-only finalize -> NCCL all-reduce of
-gradients + loss -> norm/clip pass -> Adam) and must equal the plain learner
-bit for bit, and a rank-1 learner must sample with its own Philox stream.
+the data-parallel update path (per-layer buckets on a communication branch:
+reduction-only finalize + NCCL all-reduce as each layer's gradient completes
+-> norm/clip pass -> Adam, dp_buckets.h) and must equal the plain learner bit
+for bit, and a rank-1 learner must sample with its own Philox stream.
 """
 import ctypes as C
 
@@ -71,7 +72,9 @@ def test_vlearner_dp_world1_bit_identical(D, A, H, nh, B, algo):
     kp, kd = C.c_int(), C.c_int()
     _lib.call("pqlg_vlearner_kernels_per_update", plain, C.byref(kp))
     _lib.call("pqlg_vlearner_kernels_per_update", dp, C.byref(kd))
-    assert kd.value == kp.value + 1  # the post-all-reduce norm pass
+    # one reduce + all-reduce bucket per layer (head + nh hidden layers) on
+    # the communication branch; the norm pass replaces the single finalize
+    assert kd.value == kp.value + nh + 1
     for h in (plain, dp):
         _lib.call("pqlg_vlearner_destroy", h)
     _lib.call("pqlg_comm_destroy", comm)
