@@ -38,7 +38,7 @@ struct DeviceEnv {
   int N, D, A, max_len, offset;
   int64_t ld;
   float low, high;
-  DevBuf<float> s, M;
+  DevBuf<float> s, M, MT;
   DevBuf<int64_t> ep;
   DevBuf<uint64_t> rng;
 
@@ -53,6 +53,11 @@ struct DeviceEnv {
     auto m = coupling_matrix(seed, D, A);
     M.alloc(m.size());
     PQLG_CUDA(cudaMemcpy(M.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice));
+    if (A <= actor::kMaxA && D <= actor::kMaxD) {
+      const auto t = actor::env_transpose_M(m, D, A);
+      MT.alloc(t.size());
+      PQLG_CUDA(cudaMemcpy(MT.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+    }
     ep.alloc(N);
     std::vector<uint64_t> r(N);
     for (int i = 0; i < N; ++i) r[i] = rng::derive_seed(seed, rng::kEnv, offset + i);
@@ -60,23 +65,27 @@ struct DeviceEnv {
     PQLG_CUDA(cudaMemcpy(rng.p, r.data(), N * 8, cudaMemcpyHostToDevice));
   }
   actor::EnvState view() const {
-    return actor::EnvState{s.p, ld, s.p, ld, M.p, ep.p, rng.p, N, D, A, max_len, low, high};
+    return actor::EnvState{s.p, ld, s.p, ld, M.p, reinterpret_cast<const float4*>(MT.p), ep.p, rng.p,
+                           N, D, A, max_len, low, high, 1.0f};
   }
   void reset(float* obs, int64_t ld_obs, cudaStream_t st) {
     launch(actor::env_reset_kernel, dim3((N + actor::kEnvWarps - 1) / actor::kEnvWarps), dim3(32 * actor::kEnvWarps), 0, st, view(), obs, ld_obs, offset);
   }
   // persistent grid: as many blocks as fit (occupancy), at most one per tile
-  template <int kNch>
+  template <int kSlots>
   void step_as(const float* act, int64_t ld_act, const actor::StepOut& o, cudaStream_t st,
-               const actor::NextNorm& nn, size_t smem, const float* cur, int64_t ld_cur) {
-    auto kern = actor::env_step_kernel<kNch>;
+               const actor::NextNorm& nn, const float* cur, int64_t ld_cur) {
+    auto kern = actor::env_step_kernel<kSlots>;
+    const size_t smem = actor::env_step_smem(D, A, kSlots);
     static int per_sm = 0;
-    if (per_sm == 0) {
+    static size_t per_sm_smem = 0;
+    if (per_sm == 0 || per_sm_smem != smem) {
       PQLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      200 * 1024));
       PQLG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
                                                               32 * actor::kEnvWarps, smem));
       if (per_sm < 1) per_sm = 1;
+      per_sm_smem = smem;
     }
     const int tiles = (N + actor::kEnvTile - 1) / actor::kEnvTile;
     const int blocks = std::min(tiles, per_sm * mlp::kSMs);
@@ -86,6 +95,8 @@ struct DeviceEnv {
       v.s_in = cur;
       v.ld_in = ld_cur;
     }
+    require(v.ld_in % 4 == 0 && (reinterpret_cast<uintptr_t>(v.s_in) & 15) == 0,
+            "env: state rows must be 16-byte aligned");
     launch(kern, dim3(blocks), dim3(32 * actor::kEnvWarps), smem, st, v, act, ld_act, o, nn);
   }
   // cur: optional obs buffer holding the current state (the actor's double
@@ -94,23 +105,11 @@ struct DeviceEnv {
             const actor::NextNorm& nn = actor::NextNorm{}, const float* cur = nullptr,
             int64_t ld_cur = 0) {
     require(A <= actor::kMaxA, "env: act_dim > 32 not supported");
-    require(D <= 32 * actor::kMaxDChunks, "env: obs_dim > 256 not supported");
-    const size_t smem = actor::env_step_smem(D, A);
-    switch ((D + 31) / 32) {
-      case 1: step_as<1>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
-      case 2: step_as<2>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
-      case 3: step_as<3>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
-      case 4: step_as<4>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
-      case 5: step_as<5>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
-      case 6: step_as<6>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
-      case 7: step_as<7>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
-      default: step_as<8>(act, ld_act, o, st, nn, smem, cur, ld_cur); break;
-    }
+    require(D <= actor::kMaxD, "env: obs_dim > 256 not supported");
+    if ((D + 3) / 4 <= 32) step_as<1>(act, ld_act, o, st, nn, cur, ld_cur);
+    else step_as<2>(act, ld_act, o, st, nn, cur, ld_cur);
   }
 };
-
-
-
 
 Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st,
              pqlg_comm_s* comm)
@@ -195,7 +194,7 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
   identity_.alloc(1);
   const int one = 1;
   PQLG_CUDA(cudaMemcpy(identity_.p, &one, 4, cudaMemcpyHostToDevice));
-  npart_.alloc(static_cast<size_t>(actor::kNormGroups) * D_ * 2);
+  npart_.alloc(static_cast<size_t>(actor::kNormBlocks) * D_ * 2);
   if (comm_) {
     require(D_ <= 1024, "actor: sharded normalizer needs obs_dim <= 1024");
     nbatch_.alloc(2 * static_cast<size_t>(D_) + 1);
@@ -248,9 +247,7 @@ void Actor::build() {
   if (sac_) {
     // GaussianPolicy::sample with a fresh normal_distribution per env over
     // its noise stream (learners.cpp:87-94): split-K head + sampling finish
-    head_.init(pol_.p + pnet_.w_off[nh], H, 2 * A);
-    head_.refresh(stream_);
-    auto gemm = mlp::head_gemm_step(head_split_, in, ld, head_.ptr(), head_.stride(), N, 2 * A, H);
+    auto gemm = mlp::head_raw_step(head_split_, in, ld, pol_.p + pnet_.w_off[nh], N, 2 * A, H);
     sac::GaussArgs g{};
     g.bias = pol_.p + pnet_.b_off[nh];
     g.rng = noise_rng_.p;
@@ -268,23 +265,19 @@ void Actor::build() {
     return;
   }
   // DeterministicPolicy::act + apply_noise (learners.cpp:96-98), fused
-  epi::PolicyHead ph{};
+  head::RowsArgs ph{};
   ph.bias = pol_.p + pnet_.b_off[nh];
-  ph.ld_act = Ap_;
-  ph.M = N;
-  ph.A = A;
+  ph.ld_out = Ap_;
   ph.mid = (dims_.low + dims_.high) / 2.0f;
   ph.half = (dims_.high - dims_.low) / 2.0f;
   ph.noise_state = noise_rng_.p;
   ph.sigma = sigma_.p;
   ph.low = dims_.low;
   ph.high = dims_.high;
-  head_.init(pol_.p + pnet_.w_off[nh], H, A);
-  head_.refresh(stream_);
-  const float* W = head_.ptr();
+  const float* W = pol_.p + pnet_.w_off[nh];
   for (int k = 0; k < kSets; ++k) {
-    ph.act = act_[k].p;
-    head_steps_[k] = mlp::fwd(in, in, ld, W, W, N, A, H, 1, ph, head_.stride());
+    ph.out = act_[k].p;
+    head_steps_[k] = mlp::head_squash_step(ph, in, ld, W, N, A, H);
   }
 }
 
@@ -300,7 +293,7 @@ void Actor::enqueue(int cur) {
   // the next policy input apply(stats_t, obs_{t+1}) directly.
   actor::NormState ns{count_.p, mean_.p, m2_.p, mean_f_.p, inv_f_.p, identity_.p,
                       comm_ ? nbatch_.p : nullptr};
-  launch(actor::norm_update_kernel, dim3(dim3((D + 31) / 32, actor::norm_groups(D))), dim3(256), 0, st, obs, Dp_, N, D, npart_.p, nticket_.p, ns);
+  actor::norm_update(obs, Dp_, N, D, npart_.p, nticket_.p, ns, st);
   if (comm_) {
     // sharded: every shard's batch statistics, merged in rank
     // order into identical running stats on all shards (5 KB at config 3)
@@ -382,7 +375,6 @@ void Actor::adopt_policy(const float* flat, int64_t version, bool device) {
   // device snapshots carry [net | log_alpha]; the host ABI passes the net
   PQLG_CUDA(cudaMemcpyAsync(pol_.p, flat, (device ? snapshot_len() : pnet_.params) * 4,
                             device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream_));
-  head_.refresh(stream_);
   if (!device) PQLG_CUDA(cudaStreamSynchronize(stream_));
   version_ = version;
 }
@@ -536,18 +528,14 @@ void evaluate_policy(const pqlg_config& cfg, const pqlg_task_dims& dims, const f
     ld = H;
     K = H;
   }
-  WeightMirror head;
-  head.init(pol.p + pnet.w_off[nh], H, hout);
-  head.refresh(st);
-  epi::PolicyHead ph{};
+  head::RowsArgs ph{};
   ph.bias = pol.p + pnet.b_off[nh];
-  ph.act = act.p;
-  ph.ld_act = Ap;
-  ph.M = N;
-  ph.A = A;
+  ph.out = act.p;
+  ph.ld_out = Ap;
+  ph.ldw = hout;  // pql_sac: the mean columns of [mean | log_std]
   ph.mid = (dims.low + dims.high) / 2.0f;
   ph.half = (dims.high - dims.low) / 2.0f;
-  steps.push_back(mlp::fwd(in, in, ld, head.ptr(), head.ptr(), N, A, H, 1, ph, head.stride()));
+  steps.push_back(mlp::head_squash_step(ph, in, ld, pol.p + pnet.w_off[nh], N, A, H));
   const int blocks = std::min((N + 255) / 256, 4 * mlp::kSMs);
   int cur = 0;
   for (int step = 0; step < cfg.max_episode_len; ++step) {
@@ -749,12 +737,12 @@ int pqlg_k_normalizer_update(int64_t* count_dev, double* mean_dev, double* m2_de
   return guarded([&] {
     auto st = static_cast<cudaStream_t>(stream);
     if (rows == 0) return;  // normalizer.hpp:34
-    DevBuf<double> part(static_cast<size_t>(actor::kNormGroups) * dim * 2);
+    DevBuf<double> part(static_cast<size_t>(actor::kNormBlocks) * dim * 2);
     DevBuf<int> ident(1);
     DevBuf<unsigned int> ticket(actor::norm_tickets(dim));
     const int64_t ldx = ld > 0 ? ld : dim;
     actor::NormState ns{count_dev, mean_dev, m2_dev, mean_f_dev, inv_f_dev, ident.p};
-    launch(actor::norm_update_kernel, dim3(dim3((dim + 31) / 32, actor::norm_groups(dim))), dim3(256), 0, st, batch_dev, ldx, rows, dim, part.p, ticket.p, ns);
+    actor::norm_update(batch_dev, ldx, rows, dim, part.p, ticket.p, ns, st);
     PQLG_CUDA(cudaStreamSynchronize(st));
   });
 }

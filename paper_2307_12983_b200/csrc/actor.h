@@ -83,7 +83,6 @@ class Actor {
   DevBuf<float> obs_[kSets], boot_[kSets], rew_[kSets], act_[kSets], Xn_;
   DevBuf<uint8_t> term_[kSets], trunc_[kSets];
   DevBuf<float> pol_;
-  WeightMirror head_;
   std::vector<DevBuf<float>> pact_;
   DevBuf<uint64_t> noise_rng_;
   DevBuf<float> sigma_;

@@ -14,25 +14,32 @@
 
 #include "pdl.cuh"
 #include <cstdint>
+#include <vector>
 
 #include "rng.cuh"
+#include "common.h"
 
 namespace pqlg::actor {
 
 constexpr int kEnvWarps = 8;
-constexpr int kNormChunk = 128;
+constexpr int kEnvPer = 4;                         // envs per warp per tile
+constexpr int kEnvTile = kEnvWarps * kEnvPer;      // 32 envs per block iteration
+constexpr int kMaxA = 32;
+constexpr int kMaxD = 256;                         // 64 float4 quads: two per lane
 
 struct EnvState {
   float* s;                // [N x ld] state (= observation); null: the caller keeps the
   int64_t ld;              //   state in its obs buffers (s_in = this step's obs)
-  const float* s_in;       // state read by the step (= s unless aliased)
-  int64_t ld_in;
+  const float* s_in;       // state read by the step (= s unless aliased); rows 16-byte
+  int64_t ld_in;           //   aligned, ld_in % 4 == 0
   const float* M;          // [D x A] coupling
+  const float4* MT;        // [round_up(A, 4)][kMaxD / 4] M^T, zero padded (env_transpose_M)
   int64_t* episode_step;   // [N]
   uint64_t* rng;           // [N] SplitMix state per env
   int N, D, A;
   int max_len;
   float low, high;
+  float one = 1.0f;        // a runtime 1.0f (see add2 below)
 };
 
 struct StepOut {
@@ -58,269 +65,321 @@ struct NextNorm {
   const int* identity;
 };
 
-// Tiles of 32 envs per block iteration (persistent grid, M staged once per
-// block in shared memory):
-//   phase 1  warp per env: s' = clamp(0.95 s + 0.05 M a) lane-parallel over d,
-//            up to 8 independent k-ascending chains per lane; s' -> smem tile
-//   phase 2  thread per env (warp 0): the d-ascending sum of s'^2, reward,
-//            termination, time limit -- the order-sensitive serial sums run
-//            32 envs at a time instead of on one lane of a warp
-//   phase 3  warp per env: boot obs, auto-reset draws, next obs, state and
-//            the fused next-obs normalisation
-// All sums are float mul/add in d-ascending order, so states, rewards and
-// flags are bit-exact.
-constexpr int kMaxA = 32;
-constexpr int kEnvTile = 32;
-constexpr int kMaxDChunks = 8;  // obs_dim <= 256
+// ---- paired fp32 arithmetic (sm_100 FMUL2 / FFMA2), rounding like the scalar ops.
+// ptxas contracts a paired mul feeding a paired add into one FFMA2 (even
+// with explicit .rn), which would skip the product's rounding.  The sum is
+// therefore formed as fma(p, one, acc) with `one` a kernel argument equal to
+// 1.0f: p * 1 is exact, so the result is round(p + acc), the reference's
+// separately rounded add, and there is no multiply left to contract.
+__device__ __forceinline__ uint64_t pk(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t p, uint64_t acc, uint64_t one2) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(p), "l"(one2), "l"(acc));
+  return r;
+}
 
-__device__ __forceinline__ int env_tile_ld(int D) { return D | 1; }  // odd: conflict-free rows
+__device__ __forceinline__ float clamp10(float v) {
+  return v < -10.0f ? -10.0f : (v > 10.0f ? 10.0f : v);
+}
 
-// kNch = number of 32-wide obs chunks per lane (ceil(D/32) rounded up to 1, 2, 4 or 8).
-template <int kNch>
+// Synthetic EnvBatch::step (vecenv.cpp:84-106 contract, SURVEY 8(d) task).
+// A warp owns kEnvPer envs of a 32-env block tile; lane l owns observation
+// quads l and l + 32 (d = 4q..4q+3), so rows move as float4.
+//   1  s' = clamp(0.95 s + 0.05 M a): M^T (pre-transposed at env creation)
+//      copied into shared memory; for every k the lane's quad of M^T[k] (one
+//      LDS.128) feeds kEnvPer envs with paired mul / add (k ascending, no
+//      FMA: bit-exact; the k >= A padding adds +0 products, which leave the
+//      +0-started sums unchanged)
+//   2  done flags from s'_0 and the episode counter (prefetched with the
+//      state), boot / next obs (fresh reset draws on done) / next-obs
+//      normalisation stored by the owning warp straight away
+//   3  the order-sensitive d-ascending sum of s'^2 (the reward) runs one
+//      thread per env over the block's 32 rows in shared memory (double
+//      buffered: one warp per tile, while the others start the next tile)
+template <int kSlots>
 static __global__ void __launch_bounds__(32 * kEnvWarps)
     env_step_kernel(EnvState e, const float* __restrict__ act, int64_t ld_act, StepOut o,
                     NextNorm nn) {
   extern __shared__ float4 sh4[];
-  const int D = e.D, A = e.A;
+  constexpr int kQT = 32 * kSlots;                       // M^T row stride (float4)
+  const int D = e.D, A = e.A, Q = (D + 3) >> 2;
   const int Ap = (A + 3) & ~3;
-  const int ldv = env_tile_ld(D);
-  float* sM = reinterpret_cast<float*>(sh4);             // [D x Ap]
-  float* sv = sM + static_cast<int64_t>(D) * Ap;        // [kEnvTile x ldv]  s'
-  float* saa = sv + kEnvTile * ldv;                      // [kEnvTile]        sum a^2
-  int* sdone = reinterpret_cast<int*>(saa + kEnvTile);   // [kEnvTile]
-  float* sa_all = saa + 2 * kEnvTile;                    // [kEnvWarps x kPer x 32] clamped actions
-  {
-    // stage M (constant since env creation) before the PDL wait, under the
-    // previous kernel's tail
-    if ((A & 3) == 0) {  // rows are float4-aligned: straight vector copy
-      const int total4 = D * A / 4;
-      const float4* src = reinterpret_cast<const float4*>(e.M);
-      for (int idx = threadIdx.x; idx < total4; idx += blockDim.x) sh4[idx] = src[idx];
-    } else {
-      const int total = D * Ap;
-      for (int base = threadIdx.x; base < total; base += 8 * blockDim.x) {
-        float v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int idx = base + q * blockDim.x;
-          v[q] = 0.0f;
-          if (idx < total) {
-            const int d = idx / Ap, k = idx - d * Ap;
-            if (k < A) v[q] = e.M[static_cast<int64_t>(d) * A + k];
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int idx = base + q * blockDim.x;
-          if (idx < total) sM[idx] = v[q];
-        }
-      }
-    }
+  const int ldv = D | 1;                                 // odd: conflict-free chain reads
+  float4* sMT = sh4;                                     // [Ap][kQT]
+  float* sv = reinterpret_cast<float*>(sMT + Ap * kQT);  // [2][kEnvTile][ldv]   s'
+  float* sa = sv + 2 * kEnvTile * ldv;                   // [kEnvTile][32]       clamped a
+  float* saa = sa + kEnvTile * 32;                       // [2][kEnvTile]        sum a^2
+  int* sflag = reinterpret_cast<int*>(saa + 2 * kEnvTile);  // [2][kEnvTile] done | trunc<<1
+  // M^T (constant since env creation) before the PDL wait
+  for (int idx = threadIdx.x; idx < Ap * kQT; idx += blockDim.x) {
+    const int k = idx / kQT, q = idx - k * kQT;
+    sMT[idx] = __ldg(e.MT + k * (kMaxD / 4) + q);
   }
   __syncthreads();
   pdl::entry();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  constexpr int kPerW = kEnvTile / kEnvWarps;
-  float* sa = sa_all + w * 32 * kPerW;
+  const uint64_t one2 = pk(e.one, e.one);
+  const uint64_t c095 = pk(0.95f, 0.95f), c005 = pk(0.05f, 0.05f);
   const bool id = nn.out ? (*nn.identity != 0) : true;
-  const int n_tiles = (e.N + kEnvTile - 1) / kEnvTile;
-  const int A4 = (A + 3) >> 2;
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int i0 = tile * kEnvTile;
-    // ---- phase 1 (all of this warp's env rows are loaded before any math)
-    constexpr int kPer = kEnvTile / kEnvWarps;
-    float sdp[kPer][kNch], up[kPer];
+  const bool xnorm = nn.out != nullptr && !id;
+  const bool vec = ((o.ld_obs & 3) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(o.next_obs) | reinterpret_cast<uintptr_t>(o.boot)) & 15) == 0 &&
+                   (!nn.out || (((nn.ld_out & 3) == 0) && (reinterpret_cast<uintptr_t>(nn.out) & 15) == 0)) &&
+                   (!e.s || (((e.ld & 3) == 0) && (reinterpret_cast<uintptr_t>(e.s) & 15) == 0));
+  // this lane's normalisation constants
+  float nm[kSlots][4], ni[kSlots][4];
 #pragma unroll
-    for (int p = 0; p < kPer; ++p) {
-      const int i = i0 + w + p * kEnvWarps;
-      const bool ok = i < e.N;
-      const float* s = e.s_in + static_cast<int64_t>(i) * e.ld_in;
+  for (int sl = 0; sl < kSlots; ++sl)
 #pragma unroll
-      for (int c = 0; c < kNch; ++c) {
-        const int d = lane + 32 * c;
-        sdp[p][c] = (ok && d < D) ? s[d] : 0.0f;
-      }
-      up[p] = (ok && lane < A) ? act[static_cast<int64_t>(i) * ld_act + lane] : 0.0f;
+    for (int c = 0; c < 4; ++c) {
+      const int d = 4 * (lane + 32 * sl) + c;
+      nm[sl][c] = (xnorm && d < D) ? nn.mean[d] : 0.0f;
+      ni[sl][c] = (xnorm && d < D) ? nn.inv[d] : 1.0f;
     }
-    // clamped actions of the warp's kPer envs -> smem (one row of 32 each)
+  const int n_tiles = (e.N + kEnvTile - 1) / kEnvTile;
+  float* sa_w = sa + w * kEnvPer * 32;
+  int it = 0;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const int i0 = tile * kEnvTile;
+    const int base = i0 + w * kEnvPer;
+    const int nv = e.N - base;  // valid envs of this warp (may be <= 0)
+    // ---- loads: state quads, actions and episode counters of the warp's envs
+    float4 s4[kEnvPer][kSlots];
 #pragma unroll
-    for (int p = 0; p < kPer; ++p) {
-      const int i = i0 + w + p * kEnvWarps;
-      float u = 0.0f;
-      bool bad = false;
-      if (lane < A && i < e.N) {
-        u = up[p];
-        bad = !isfinite(u);
-        u = u < e.low ? e.low : (u > e.high ? e.high : u);
+    for (int p = 0; p < kEnvPer; ++p) {
+      const float* srow = e.s_in + static_cast<int64_t>(base + p) * e.ld_in;
+#pragma unroll
+      for (int sl = 0; sl < kSlots; ++sl) {
+        const int q = lane + 32 * sl;
+        s4[p][sl] = (p < nv && q < Q) ? __ldg(reinterpret_cast<const float4*>(srow) + q)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      sa[p * 32 + lane] = u;
+    }
+    float up[kEnvPer];
+#pragma unroll
+    for (int p = 0; p < kEnvPer; ++p)
+      up[p] = (lane < A && p < nv) ? __ldg(act + static_cast<int64_t>(base + p) * ld_act + lane) : 0.0f;
+    const int64_t ep_prev = (lane < kEnvPer && lane < nv) ? e.episode_step[base + lane] : 0;
+    {
+      bool bad = false;
+#pragma unroll
+      for (int p = 0; p < kEnvPer; ++p) {
+        float u = up[p];
+        if (lane < A && p < nv) {
+          bad |= !isfinite(u);
+          u = u < e.low ? e.low : (u > e.high ? e.high : u);
+        }
+        sa_w[p * 32 + lane] = u;
+      }
       if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(o.status, 8u);
     }
     __syncwarp();
-    // M a for all kPer envs at once: each M quad read from smem feeds kPer
-    // independent k-ascending chains per d (mul then add, no FMA)
-    float acc[kPer][kNch];
+    if (lane < kEnvPer) {  // sum a^2, k ascending
+      const float* ap = sa_w + lane * 32;
+      float aa = 0.0f;
+      for (int k = 0; k < A; ++k) aa = __fadd_rn(aa, __fmul_rn(ap[k], ap[k]));
+      saa[buf * kEnvTile + w * kEnvPer + lane] = aa;
+    }
+    // ---- 1: M a, k ascending (sums start at +0 like the reference's loop)
+    uint64_t acc[kEnvPer][kSlots][2];
 #pragma unroll
-    for (int p = 0; p < kPer; ++p)
+    for (int p = 0; p < kEnvPer; ++p)
 #pragma unroll
-      for (int c = 0; c < kNch; ++c) acc[p][c] = 0.0f;
+      for (int sl = 0; sl < kSlots; ++sl) acc[p][sl][0] = acc[p][sl][1] = 0ull;
 #pragma unroll 1
-    for (int k4 = 0; k4 < A4; ++k4) {
-      float av[kPer][4];
+    for (int k4 = 0; k4 < Ap; k4 += 4) {
+      float4 u4[kEnvPer];
 #pragma unroll
-      for (int p = 0; p < kPer; ++p) {
-        const float4 a4 = reinterpret_cast<const float4*>(sa + p * 32)[k4];
-        av[p][0] = a4.x;
-        av[p][1] = a4.y;
-        av[p][2] = a4.z;
-        av[p][3] = a4.w;
+      for (int p = 0; p < kEnvPer; ++p) u4[p] = *reinterpret_cast<const float4*>(sa_w + p * 32 + k4);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        uint64_t m2[kSlots][2];
+#pragma unroll
+        for (int sl = 0; sl < kSlots; ++sl) {
+          const float4 m = sMT[(k4 + kk) * kQT + lane + 32 * sl];
+          m2[sl][0] = pk(m.x, m.y);
+          m2[sl][1] = pk(m.z, m.w);
+        }
+#pragma unroll
+        for (int p = 0; p < kEnvPer; ++p) {
+          const float u = kk == 0 ? u4[p].x : (kk == 1 ? u4[p].y : (kk == 2 ? u4[p].z : u4[p].w));
+          const uint64_t uu = pk(u, u);
+#pragma unroll
+          for (int sl = 0; sl < kSlots; ++sl) {
+            acc[p][sl][0] = add2(mul2(m2[sl][0], uu), acc[p][sl][0], one2);
+            acc[p][sl][1] = add2(mul2(m2[sl][1], uu), acc[p][sl][1], one2);
+          }
+        }
       }
-      const int nu = A - 4 * k4;
-      if (nu >= 4) {  // full quad (always when A % 4 == 0)
+    }
+    // s' = clamp(0.95 s + 0.05 acc) -> registers (s4) and the chain buffer
+    float* svb = sv + buf * kEnvTile * ldv;
 #pragma unroll
-        for (int c = 0; c < kNch; ++c) {
-          const int d = lane + 32 * c;
-          if (c + 1 < kNch || d < D) {
-            const float4 m4 = reinterpret_cast<const float4*>(sM + d * Ap)[k4];
+    for (int p = 0; p < kEnvPer; ++p)
 #pragma unroll
-            for (int p = 0; p < kPer; ++p) {
-              acc[p][c] = __fadd_rn(acc[p][c], __fmul_rn(m4.x, av[p][0]));
-              acc[p][c] = __fadd_rn(acc[p][c], __fmul_rn(m4.y, av[p][1]));
-              acc[p][c] = __fadd_rn(acc[p][c], __fmul_rn(m4.z, av[p][2]));
-              acc[p][c] = __fadd_rn(acc[p][c], __fmul_rn(m4.w, av[p][3]));
+      for (int sl = 0; sl < kSlots; ++sl) {
+        float4& v = s4[p][sl];
+        const uint64_t t01 = mul2(pk(v.x, v.y), c095), t23 = mul2(pk(v.z, v.w), c095);
+        const uint64_t r01 = add2(mul2(acc[p][sl][0], c005), t01, one2);
+        const uint64_t r23 = add2(mul2(acc[p][sl][1], c005), t23, one2);
+        upk(r01, v.x, v.y);
+        upk(r23, v.z, v.w);
+        v.x = clamp10(v.x);
+        v.y = clamp10(v.y);
+        v.z = clamp10(v.z);
+        v.w = clamp10(v.w);
+        const int d0 = 4 * (lane + 32 * sl);
+        float* row = svb + (w * kEnvPer + p) * ldv;
+        if (d0 + 3 < D) {
+          row[d0] = v.x;
+          row[d0 + 1] = v.y;
+          row[d0 + 2] = v.z;
+          row[d0 + 3] = v.w;
+        } else {
+          if (d0 < D) row[d0] = v.x;
+          if (d0 + 1 < D) row[d0 + 1] = v.y;
+          if (d0 + 2 < D) row[d0 + 2] = v.z;
+        }
+      }
+    // ---- 2: flags (lane p: env base + p), then the rows
+    int flag = 0;
+    {
+      float mine = 0.0f;
+#pragma unroll
+      for (int p = 0; p < kEnvPer; ++p) {
+        const float v0 = __shfl_sync(0xffffffffu, s4[p][0].x, 0);
+        if (lane == p) mine = v0;
+      }
+      if (lane < kEnvPer && lane < nv) {
+        const int i = base + lane;
+        const bool terminal = fabsf(mine) > 9.0f;
+        const int64_t ep = ep_prev + 1;
+        const bool timeout = ep >= e.max_len;
+        const bool done = terminal || timeout;
+        const bool trunc = !terminal && timeout;
+        e.episode_step[i] = done ? 0 : ep;
+        flag = (done ? 1 : 0) | (trunc ? 2 : 0);
+        sflag[buf * kEnvTile + w * kEnvPer + lane] = flag;
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < kEnvPer; ++p) {
+      if (p >= nv) break;
+      const int i = base + p;
+      const bool done = (__shfl_sync(0xffffffffu, flag, p) & 1) != 0;
+      const uint64_t st0 = done ? e.rng[i] : 0ull;
+      const int64_t ro = static_cast<int64_t>(i) * o.ld_obs;
+      float* bt = o.boot + ro;
+      float* nx = o.next_obs + ro;
+      float* sr = e.s ? e.s + static_cast<int64_t>(i) * e.ld : nullptr;
+      float* xn = nn.out ? nn.out + static_cast<int64_t>(i) * nn.ld_out : nullptr;
+#pragma unroll
+      for (int sl = 0; sl < kSlots; ++sl) {
+        const int q = lane + 32 * sl;
+        if (q >= Q) continue;
+        const int d0 = 4 * q;
+        const float4 v = s4[p][sl];
+        float4 nv4 = v;
+        if (done) {  // auto-reset: draw d of the reset sequence (vecenv.cpp:100-103)
+          uint64_t t0 = st0 + static_cast<uint64_t>(d0);
+          nv4.x = rng::env_uniform(t0, -1.0f, 1.0f);
+          uint64_t t1 = st0 + static_cast<uint64_t>(d0 + 1);
+          nv4.y = rng::env_uniform(t1, -1.0f, 1.0f);
+          uint64_t t2 = st0 + static_cast<uint64_t>(d0 + 2);
+          nv4.z = rng::env_uniform(t2, -1.0f, 1.0f);
+          uint64_t t3 = st0 + static_cast<uint64_t>(d0 + 3);
+          nv4.w = rng::env_uniform(t3, -1.0f, 1.0f);
+        }
+        float4 z = nv4;
+        if (xnorm) {
+          float zz[4] = {nv4.x, nv4.y, nv4.z, nv4.w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float t = __fmul_rn(__fsub_rn(zz[c], nm[sl][c]), ni[sl][c]);
+            if (t > 5.0f) t = 5.0f;
+            if (t < -5.0f) t = -5.0f;
+            zz[c] = t;
+          }
+          z = make_float4(zz[0], zz[1], zz[2], zz[3]);
+        }
+        if (vec && d0 + 3 < D) {
+          *reinterpret_cast<float4*>(bt + d0) = v;
+          *reinterpret_cast<float4*>(nx + d0) = nv4;
+          if (sr) *reinterpret_cast<float4*>(sr + d0) = nv4;
+          if (xn) *reinterpret_cast<float4*>(xn + d0) = z;
+        } else {
+          const float vv[4] = {v.x, v.y, v.z, v.w}, nn4[4] = {nv4.x, nv4.y, nv4.z, nv4.w},
+                      z4[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (d0 + c < D) {
+              bt[d0 + c] = vv[c];
+              nx[d0 + c] = nn4[c];
+              if (sr) sr[d0 + c] = nn4[c];
+              if (xn) xn[d0 + c] = z4[c];
             }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < kNch; ++c) {
-          const int d = lane + 32 * c;
-          if (d < D) {
-            const float4 m4 = reinterpret_cast<const float4*>(sM + d * Ap)[k4];
-            const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
-#pragma unroll
-            for (int p = 0; p < kPer; ++p)
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                if (q < nu) acc[p][c] = __fadd_rn(acc[p][c], __fmul_rn(mm[q], av[p][q]));
-          }
         }
       }
+      if (done && lane == 0) e.rng[i] = st0 + static_cast<uint64_t>(D);
     }
-#pragma unroll
-    for (int p = 0; p < kPer; ++p) {
-      const int j = w + p * kEnvWarps;
-      if (i0 + j >= e.N) break;
-#pragma unroll
-      for (int c = 0; c < kNch; ++c) {
-        const int d = lane + 32 * c;
-        if (d < D) {
-          float v = __fadd_rn(__fmul_rn(0.95f, sdp[p][c]), __fmul_rn(0.05f, acc[p][c]));
-          v = v < -10.0f ? -10.0f : (v > 10.0f ? 10.0f : v);
-          sv[j * ldv + d] = v;
-        }
-      }
-      if (lane == 0) {
-        const float* ap = sa + p * 32;
-        float aa = 0.0f;
-        for (int k = 0; k < A; ++k) aa = __fadd_rn(aa, __fmul_rn(ap[k], ap[k]));
-        saa[j] = aa;
-      }
-    }
-    __syncwarp();
+    // ---- 3: the reward chains of this tile (one warp, lane = env)
     __syncthreads();
-    // ---- phase 2
-    if (w == 0) {
+    if (w == (it & (kEnvWarps - 1))) {
       const int i = i0 + lane;
-      int done_i = 0;
       if (i < e.N) {
-        const float* row = sv + lane * ldv;
+        const float* row = svb + lane * ldv;
         float ss = 0.0f;
         int d = 0;
         for (; d + 8 <= D; d += 8) {
-          float q[8];
+          float q8[8];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) q[t] = row[d + t];
+          for (int t = 0; t < 8; ++t) q8[t] = row[d + t];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) ss = __fadd_rn(ss, __fmul_rn(q[t], q[t]));
+          for (int t = 0; t < 8; ++t) ss = __fadd_rn(ss, __fmul_rn(q8[t], q8[t]));
         }
         for (; d < D; ++d) ss = __fadd_rn(ss, __fmul_rn(row[d], row[d]));
-        const float reward = -__fadd_rn(__fdiv_rn(ss, static_cast<float>(D)),
-                                        __fmul_rn(0.01f, __fdiv_rn(saa[lane], static_cast<float>(A))));
-        const bool terminal = fabsf(row[0]) > 9.0f;
-        const int64_t ep = e.episode_step[i] + 1;
-        const bool timeout = ep >= e.max_len;
-        done_i = terminal || timeout;
-        const int trunc_i = !terminal && timeout;
-        e.episode_step[i] = done_i ? 0 : ep;
+        const float reward =
+            -__fadd_rn(__fdiv_rn(ss, static_cast<float>(D)),
+                       __fmul_rn(0.01f, __fdiv_rn(saa[buf * kEnvTile + lane], static_cast<float>(A))));
+        const int f = sflag[buf * kEnvTile + lane];
+        const bool done = (f & 1) != 0, trunc = (f & 2) != 0;
         o.rew[i] = reward;
-        o.term[i] = static_cast<uint8_t>(done_i && !trunc_i);
-        o.trunc[i] = static_cast<uint8_t>(trunc_i);
-        if (o.done) o.done[i] = static_cast<uint8_t>(done_i);
-      }
-      sdone[lane] = done_i;
-    }
-    __syncthreads();
-    // ---- phase 3
-    float nm[kNch], ni[kNch];  // this lane's normalisation constants (d = lane + 32c)
-#pragma unroll
-    for (int c = 0; c < kNch; ++c) {
-      const int d = lane + 32 * c;
-      nm[c] = (nn.out && !id && d < D) ? nn.mean[d] : 0.0f;
-      ni[c] = (nn.out && !id && d < D) ? nn.inv[d] : 1.0f;
-    }
-    for (int j = w; j < kEnvTile && i0 + j < e.N; j += kEnvWarps) {
-      const int i = i0 + j;
-      float* s = e.s ? e.s + static_cast<int64_t>(i) * e.ld : nullptr;
-      float* nxt = o.next_obs + static_cast<int64_t>(i) * o.ld_obs;
-      float* bt = o.boot + static_cast<int64_t>(i) * o.ld_obs;
-      float* xn = nn.out ? nn.out + static_cast<int64_t>(i) * nn.ld_out : nullptr;
-      auto emit = [&](int d, int c, float ns) {
-        if (s) s[d] = ns;
-        nxt[d] = ns;
-        if (xn) {
-          float z = ns;
-          if (!id) {
-            z = __fmul_rn(__fsub_rn(ns, nm[c]), ni[c]);
-            if (z > 5.0f) z = 5.0f;
-            if (z < -5.0f) z = -5.0f;
-          }
-          xn[d] = z;
-        }
-      };
-      if (sdone[j]) {  // warp-uniform: terminal obs to boot, fresh reset draws
-        const uint64_t st0 = e.rng[i];
-#pragma unroll
-        for (int c = 0; c < kNch; ++c) {
-          const int d = lane + 32 * c;
-          if (d < D) {
-            bt[d] = sv[j * ldv + d];
-            uint64_t st = st0 + static_cast<uint64_t>(d);  // draw d of the reset sequence
-            emit(d, c, rng::env_uniform(st, -1.0f, 1.0f));
-          }
-        }
-        if (lane == 0) e.rng[i] = st0 + static_cast<uint64_t>(D);
-      } else {
-#pragma unroll
-        for (int c = 0; c < kNch; ++c) {
-          const int d = lane + 32 * c;
-          if (d < D) {
-            const float v = sv[j * ldv + d];
-            bt[d] = v;
-            emit(d, c, v);
-          }
-        }
+        o.term[i] = static_cast<uint8_t>(done && !trunc);
+        o.trunc[i] = static_cast<uint8_t>(trunc);
+        if (o.done) o.done[i] = static_cast<uint8_t>(done);
       }
     }
-    // the next tile's phase 1 writes only rows owned by the same warp; saa /
-    // sdone are rewritten after the next barrier
+    // sv / saa / sflag [buf] are rewritten two tiles later, after the next
+    // barrier, which this tile's chain warp reaches only when it is done
   }
 }
 
-inline size_t env_step_smem(int D, int A) {
+// Host: M^T zero padded to [round_up(A, 4)][kMaxD] for the kernel's copy.
+inline std::vector<float> env_transpose_M(const std::vector<float>& M, int D, int A) {
   const int Ap = (A + 3) & ~3;
-  return (static_cast<size_t>(D) * Ap + static_cast<size_t>(kEnvTile) * (D | 1) + 2 * kEnvTile +
-          32 * kEnvTile) *
+  std::vector<float> t(static_cast<size_t>(Ap) * kMaxD, 0.0f);
+  for (int d = 0; d < D; ++d)
+    for (int k = 0; k < A; ++k) t[static_cast<size_t>(k) * kMaxD + d] = M[static_cast<size_t>(d) * A + k];
+  return t;
+}
+
+inline size_t env_step_smem(int D, int A, int slots) {
+  const int Ap = (A + 3) & ~3;
+  return (static_cast<size_t>(Ap) * 128 * slots + 2ull * kEnvTile * (D | 1) + kEnvTile * 32 +
+          4ull * kEnvTile) *
          sizeof(float);
 }
 
@@ -387,101 +446,132 @@ __device__ __forceinline__ void chan_merge(double na, double& mean, double& m2, 
   m2 = m2 + (bm2 + delta * delta * (na * nb / nab));
 }
 
-// RunningNormalizer::update (normalizer.hpp:33-50, :73-83) in one launch,
-// parallel and deterministic.  Grid (ceil(D/32) column strips, kNormGroups
-// row groups), 8 warps: lanes own columns, warp w sums rows r0 + w + 8t of
-// its group with all loads in flight; sums are shifted by the batch's first
-// row (no cancellation for offset data).  The last block of each column strip
-// (atomic ticket) reduces that strip's group partials in fixed order (8
-// threads per column, then the 8 parts in order), forms the batch (mean, M2),
-// merges it into the running stats with Chan's formula and refreshes the
-// fp32 apply constants (normalizer.hpp:62-66); the last strip to finish
-// advances the count.
-constexpr int kNormGroups = 128;  // upper bound (partials buffer)
-// row groups so the (strips x groups) grid is one wave at 4 blocks per SM
-inline int norm_groups(int D) {
-  const int strips = (D + 31) / 32;
-  int g = 4 * 148 / strips;
-  if (g > kNormGroups) g = kNormGroups;
-  if (g < 1) g = 1;
-  return g;
+// RunningNormalizer::update (normalizer.hpp:33-50, :73-83) in two launches,
+// parallel and deterministic:
+//   norm_partial_kernel  one wave of row blocks (kNormBlocks): block g takes a
+//                        contiguous row range; its threads are (row lane,
+//                        column quad) -- float4 loads of whole rows, fp64
+//                        sums of (x - shift) and (x - shift)^2 per column,
+//                        shift = the batch's first row (no cancellation for
+//                        offset data); the row lanes are added in fixed order
+//                        -> partial[g][c] = (s1, s2)
+//   norm_finish_kernel   a block per 32 columns: warp w sums blocks w, w+16,
+//                        ... in order, the 16 warp sums in order; the batch
+//                        (mean, M2) is merged into the running stats with
+//                        Chan's formula and the fp32 apply constants refreshed
+//                        (normalizer.hpp:62-66); the last block advances the
+//                        count (every block read the old one first).
+constexpr int kNormBlocks = 148;      // partial rows (one wave, upper bound)
+constexpr int kNormThreads = 512;     // partial kernel: 8 row lanes x 64 quads
+constexpr int kNormQuads = 64;
+constexpr int kNormLanes = kNormThreads / kNormQuads;
+constexpr int kNormFinishWarps = 16;
+inline int norm_blocks(int N) {
+  // at least ~32 rows per block so the fixed cost amortises
+  int g = (N + 31) / 32;
+  return g < 1 ? 1 : (g > kNormBlocks ? kNormBlocks : g);
 }
-constexpr int kNormRowsPerWarp = 16;  // rows per warp per group (N <= 8*16*kNormGroups in one pass)
-static __global__ void __launch_bounds__(256, 4)
-    norm_update_kernel(const float* __restrict__ x, int64_t ldx, int N, int D, double* partial,
-                       unsigned int* ticket, NormState s) {
+inline int norm_tickets(int) { return 1; }
+
+// vec: x rows are 16-byte aligned (ldx % 4 == 0, 16-byte base); otherwise
+// scalar loads.
+template <bool kVec>
+static __global__ void __launch_bounds__(kNormThreads)
+    norm_partial_kernel(const float* __restrict__ x, int64_t ldx, int N, int D,
+                        double2* __restrict__ partial) {
+  pdl::entry();
+  __shared__ double2 red[kNormLanes][kNormQuads][4];  // 32 KB
+  const int lane_r = threadIdx.x / kNormQuads, q0 = threadIdx.x % kNormQuads;
+  const int g = blockIdx.x;
+  const int per = (N + gridDim.x - 1) / gridDim.x;
+  const int r0 = g * per, r1 = min(r0 + per, N);
+  const int Q = (D + 3) >> 2;
+  for (int qb = 0; qb < Q; qb += kNormQuads) {
+    const int q = qb + q0;
+    double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
+    if (q < Q) {
+      float sh[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) sh[u] = 4 * q + u < D ? x[4 * q + u] : 0.0f;
+      constexpr int kU = 8;  // rows in flight per thread
+      for (int rb = r0 + lane_r; rb < r1; rb += kNormLanes * kU) {
+        float4 v[kU];
+#pragma unroll
+        for (int t = 0; t < kU; ++t) {
+          const int r = rb + kNormLanes * t;
+          v[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (r < r1) {
+            const float* row = x + static_cast<int64_t>(r) * ldx + 4 * q;
+            if constexpr (kVec) {
+              v[t] = __ldg(reinterpret_cast<const float4*>(row));
+            } else {
+              v[t].x = row[0];
+              if (4 * q + 1 < D) v[t].y = row[1];
+              if (4 * q + 2 < D) v[t].z = row[2];
+              if (4 * q + 3 < D) v[t].w = row[3];
+            }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < kU; ++t) {
+          if (rb + kNormLanes * t < r1) {
+            const float e[4] = {v[t].x, v[t].y, v[t].z, v[t].w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double d = static_cast<double>(e[u]) - static_cast<double>(sh[u]);
+              s1[u] += d;
+              s2[u] += d * d;
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) red[lane_r][q0][u] = make_double2(s1[u], s2[u]);
+    __syncthreads();
+    // fixed-order sum of the row lanes; thread (c within this quad block)
+    for (int cc = threadIdx.x; cc < 4 * kNormQuads; cc += blockDim.x) {
+      const int c = 4 * qb + cc;
+      if (c < D) {
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int l = 0; l < kNormLanes; ++l) {
+          const double2 t = red[l][cc >> 2][cc & 3];
+          a += t.x;
+          b += t.y;
+        }
+        partial[static_cast<int64_t>(g) * D + c] = make_double2(a, b);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+static __global__ void __launch_bounds__(32 * kNormFinishWarps)
+    norm_finish_kernel(const float* __restrict__ x, int N, int D, int blocks,
+                       const double2* __restrict__ partial, unsigned int* ticket, NormState s) {
   pdl::entry();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
-  const int g = blockIdx.y;
-  const int per = (N + gridDim.y - 1) / gridDim.y;
-  const int r0 = g * per, r1 = min(r0 + per, N);
-  double s1 = 0.0, s2 = 0.0;
+  __shared__ double2 red[kNormFinishWarps][32];
+  double a1 = 0.0, a2 = 0.0;
   if (c < D) {
-    const double shift = x[c];
-    for (int rb = r0 + w; rb < r1; rb += 8 * kNormRowsPerWarp) {
-      float v[kNormRowsPerWarp];
+    constexpr int kIn = 4;
+    for (int k0 = w; k0 < blocks; k0 += kNormFinishWarps * kIn) {
+      double2 v[kIn];
 #pragma unroll
-      for (int u = 0; u < kNormRowsPerWarp; ++u) {
-        const int r = rb + 8 * u;
-        v[u] = r < r1 ? x[static_cast<int64_t>(r) * ldx + c] : 0.0f;
+      for (int t = 0; t < kIn; ++t) {
+        const int k = k0 + kNormFinishWarps * t;
+        v[t] = k < blocks ? __ldcg(partial + static_cast<int64_t>(k) * D + c) : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int u = 0; u < kNormRowsPerWarp; ++u) {
-        if (rb + 8 * u < r1) {
-          const double t = static_cast<double>(v[u]) - shift;
-          s1 += t;
-          s2 += t * t;
-        }
+      for (int t = 0; t < kIn; ++t) {
+        a1 += v[t].x;
+        a2 += v[t].y;
       }
     }
   }
-  __shared__ double red[8][32][2];
-  red[w][lane][0] = s1;
-  red[w][lane][1] = s2;
-  __syncthreads();
-  if (w == 0 && c < D) {
-    double a = 0.0, b = 0.0;
-    for (int k = 0; k < 8; ++k) {
-      a += red[k][lane][0];
-      b += red[k][lane][1];
-    }
-    partial[(static_cast<int64_t>(g) * D + c) * 2] = a;
-    partial[(static_cast<int64_t>(g) * D + c) * 2 + 1] = b;
-  }
-  __shared__ bool last;
-  if (w == 0) __threadfence();  // only warp 0 wrote partials
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&ticket[1 + blockIdx.x], 1u) == gridDim.y - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  // strip finish: thread (column lane, part w) sums groups w, w+8, ... in order
-  const int groups = gridDim.y;
-  {
-    double a1 = 0.0, a2 = 0.0;
-    if (c < D) {
-      constexpr int kIn = 4;
-      for (int k0 = w; k0 < groups; k0 += 8 * kIn) {
-        double v1[kIn], v2[kIn];
-#pragma unroll
-        for (int q = 0; q < kIn; ++q) {
-          const int k = k0 + 8 * q;
-          const double* src = partial + (static_cast<int64_t>(k) * D + c) * 2;
-          v1[q] = k < groups ? __ldcg(src) : 0.0;
-          v2[q] = k < groups ? __ldcg(src + 1) : 0.0;
-        }
-#pragma unroll
-        for (int q = 0; q < kIn; ++q) {
-          a1 += v1[q];
-          a2 += v2[q];
-        }
-      }
-    }
-    __syncthreads();  // red reuse
-    red[w][lane][0] = a1;
-    red[w][lane][1] = a2;
-  }
+  red[w][lane] = make_double2(a1, a2);
   __syncthreads();
   const int64_t n0i = s.batch ? 0 : *s.count;
   if (w == 0 && c < D) {
@@ -489,9 +579,10 @@ static __global__ void __launch_bounds__(256, 4)
     const double na = static_cast<double>(n0i);
     const int64_t cnt = n0i + N;
     double t1 = 0.0, t2 = 0.0;
-    for (int k = 0; k < 8; ++k) {
-      t1 += red[k][lane][0];
-      t2 += red[k][lane][1];
+#pragma unroll
+    for (int k = 0; k < kNormFinishWarps; ++k) {
+      t1 += red[k][lane].x;
+      t2 += red[k][lane].y;
     }
     const double bmean = static_cast<double>(x[c]) + t1 / nb;
     double bm2 = t2 - t1 * t1 / nb;
@@ -510,19 +601,32 @@ static __global__ void __launch_bounds__(256, 4)
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    ticket[1 + blockIdx.x] = 0u;
     __threadfence();
-    // every strip read the old count before its ticket: the last one advances it
-    if (atomicAdd(&ticket[0], 1u) == gridDim.x - 1) {
+    // every block read the old count before its ticket: the last one advances it
+    if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
       if (s.batch) {
         s.batch[2 * D] = static_cast<double>(N);
       } else {
         *s.count = n0i + N;
         *s.identity = n0i + N <= 1 ? 1 : 0;
       }
-      ticket[0] = 0u;
+      *ticket = 0u;
     }
   }
+}
+
+// Host: both launches of the update (partial buffer: kNormBlocks x D double2).
+inline void norm_update(const float* x, int64_t ldx, int N, int D, double* partial,
+                        unsigned int* ticket, const NormState& ns, cudaStream_t st) {
+  const int g = norm_blocks(N);
+  const bool vec = (ldx % 4) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  double2* part = reinterpret_cast<double2*>(partial);
+  if (vec)
+    launch(norm_partial_kernel<true>, dim3(g), dim3(kNormThreads), 0, st, x, ldx, N, D, part);
+  else
+    launch(norm_partial_kernel<false>, dim3(g), dim3(kNormThreads), 0, st, x, ldx, N, D, part);
+  launch(norm_finish_kernel, dim3((D + 31) / 32), dim3(32 * kNormFinishWarps), 0, st, x, N, D, g,
+         static_cast<const double2*>(part), ticket, ns);
 }
 
 // Sharded actor: after an all-gather of every shard's batch
@@ -561,7 +665,6 @@ static __global__ void norm_merge_kernel(const double* __restrict__ gathered, in
   }
 }
 
-inline int norm_tickets(int D) { return 1 + (D + 31) / 32; }
 
 // Standalone apply_noise (op-level hook): one thread per env row.
 static __global__ void noise_kernel(float* act, int64_t ld, int N, int A, const float* sigma,

@@ -93,7 +93,6 @@ class VLearner {
   int64_t lagged_version_ = 0;
 
   DevBuf<float> q_, qt_, m_, v_, grads_, lagged_;
-  WeightMirror lagged_head_;
   mlp::HeadSplit head_split_;  // split-K lagged-policy head
   std::unique_ptr<DeviceReplay> replay_;
   std::unique_ptr<DeviceNStep> nstep_;

@@ -224,6 +224,80 @@ inline Step head_finish_step(const HeadSplit& hs, head::FinishArgs fin, int M, i
   };
 }
 
+// The narrow head (head::head_mma_kernel): one launch computes x * W and,
+// in squash mode, the finish.  `r` carries the mode and output fields;
+// x/w/M/K/N are set here.
+template <int kNT, bool k3x>
+inline void launch_head(const head::RowsArgs& r, cudaStream_t st) {
+  auto kern = head::head_mma_kernel<kNT, k3x>;
+  const size_t smem = head::head_smem<kNT, k3x>(r.K);
+  static bool configured = false;
+  if (!configured) {
+    PQLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    configured = true;
+  }
+  launch(kern, dim3((r.M + head::kHeadRows - 1) / head::kHeadRows), dim3(32 * head::kHeadWarps),
+         smem, st, r);
+}
+
+template <int kNT>
+inline void pick_head(bool x3, void (*&fn)(const head::RowsArgs&, cudaStream_t)) {
+  fn = x3 ? launch_head<kNT, true> : launch_head<kNT, false>;
+}
+
+inline Step head_rows_step(head::RowsArgs r, const float* x, int64_t ldx, const float* W, int M,
+                           int N, int K) {
+  require(N >= 1 && N <= 8 * head::kHeadMaxNT, "policy head: at most 72 head outputs");
+  require(K % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0,
+          "policy head: activation rows must be 16-byte aligned");
+  r.x = x;
+  r.ldx = ldx;
+  r.w = W;
+  if (r.ldw == 0) r.ldw = N;
+  r.M = M;
+  r.K = K;
+  r.N = N;
+  const bool x3 = gemm::build_x3();
+  const int nt = (N + 7) / 8;
+  void (*fn)(const head::RowsArgs&, cudaStream_t) = nullptr;
+  switch (nt) {
+    case 1: pick_head<1>(x3, fn); break;
+    case 2: pick_head<2>(x3, fn); break;
+    case 3: pick_head<3>(x3, fn); break;
+    case 4: pick_head<4>(x3, fn); break;
+    case 5: pick_head<5>(x3, fn); break;
+    case 6: pick_head<6>(x3, fn); break;
+    case 7: pick_head<7>(x3, fn); break;
+    case 8: pick_head<8>(x3, fn); break;
+    default: pick_head<9>(x3, fn); break;
+  }
+  require(head::head_smem<9, false>(K) <= 200 * 1024 || nt < 9,
+          "policy head: hidden width too large for the head kernel");
+  return [r, fn](cudaStream_t st) { fn(r, st); };
+}
+
+// Raw head sums into hs.part (one "split", row stride round_up(N, 4)) for a
+// finish kernel that adds the bias itself (the SAC Gaussian finish).
+inline Step head_raw_step(HeadSplit& hs, const float* x, int64_t ldx, const float* W, int M,
+                          int N, int K) {
+  hs.splits = 1;
+  hs.ld_part = (N + 3) / 4 * 4;
+  hs.part.alloc(static_cast<size_t>(M) * hs.ld_part);
+  head::RowsArgs r{};
+  r.mode = 0;
+  r.out = hs.part.p;
+  r.ld_out = hs.ld_part;
+  return head_rows_step(r, x, ldx, W, M, N, K);
+}
+
+// DeterministicPolicy::act in one launch: act = mid + half*tanh(x W + b),
+// optional tanh_out and (actor) mixed exploration noise + clamp.
+inline Step head_squash_step(head::RowsArgs r, const float* x, int64_t ldx, const float* W, int M,
+                             int N, int K) {
+  r.mode = 1;
+  return head_rows_step(r, x, ldx, W, M, N, K);
+}
+
 // Bias-correction table bc[t] = (float(1/(1-0.9^t)), float(1/(1-0.999^t)))
 // computed on the host with the same libm pow the reference uses
 // (optim.hpp:35-39).  Beyond t = 32767 both are exactly 1.0f.

@@ -217,11 +217,11 @@ void PLearner::build_update() {
     }
     head_.init(pol_.p + pnet_.w_off[nh], H, Ah_);
     head_.refresh(stream_);
-    steps_.push_back(
-        mlp::head_gemm_step(head_split_, in, ld, head_.ptr(), head_.stride(), B, Ah_, H));
+    const float* Wh = pol_.p + pnet_.w_off[nh];
     if (sac_) {
       // s = policy.sample(states, eps) (sac.hpp:77): actions, log-probs, and
       // tanh(pre) / std kept for the backward
+      steps_.push_back(mlp::head_raw_step(head_split_, in, ld, Wh, B, Ah_, H));
       sac::GaussArgs g{};
       g.bias = pol_.p + pnet_.b_off[nh];
       g.eps = eps_.out.p;
@@ -236,15 +236,15 @@ void PLearner::build_update() {
       steps_.push_back([this](cudaStream_t st) { eps_.join(st); });
       steps_.push_back(gauss_finish_step(head_split_, g, B, A));
     } else {
-      head::FinishArgs ph{};
+      head::RowsArgs ph{};
       ph.bias = pol_.p + pnet_.b_off[nh];
-      ph.act = X_.p + D;  // critic input [norm(s) | pi(s)]
-      ph.ld_act = Kp_;
+      ph.out = X_.p + D;  // critic input [norm(s) | pi(s)]
+      ph.ld_out = Kp_;
       ph.tanh_out = T_.p;
       ph.ld_tanh = Ap_;
       ph.mid = (dims_.low + dims_.high) / 2.0f;
       ph.half = (dims_.high - dims_.low) / 2.0f;
-      steps_.push_back(mlp::head_finish_step(head_split_, ph, B, A));
+      steps_.push_back(mlp::head_squash_step(ph, in, ld, Wh, B, A, H));
     }
   }
 

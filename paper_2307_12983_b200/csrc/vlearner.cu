@@ -225,12 +225,10 @@ void VLearner::build_update() {
       K = H;
     }
     const int hout = sac_ ? 2 * A : A;
-    lagged_head_.init(lagged_.p + pnet_.w_off[nh], H, hout);
-    lagged_head_.refresh(stream_);
-    steps_.push_back(mlp::head_gemm_step(head_split_, in, ld, lagged_head_.ptr(),
-                                         lagged_head_.stride(), B, hout, H));
+    const float* Wh = lagged_.p + pnet_.w_off[nh];
     if (sac_) {
       // next = lagged.sample(boot, eps) (sac.hpp:31): actions + log-probs
+      steps_.push_back(mlp::head_raw_step(head_split_, in, ld, Wh, B, hout, H));
       sac::GaussArgs g{};
       g.bias = lagged_.p + pnet_.b_off[nh];
       g.eps = eps_.out.p;
@@ -242,13 +240,13 @@ void VLearner::build_update() {
       steps_.push_back([this](cudaStream_t st) { eps_.join(st); });
       steps_.push_back(gauss_finish_step(head_split_, g, B, A));
     } else {
-      head::FinishArgs ph{};
+      head::RowsArgs ph{};
       ph.bias = lagged_.p + pnet_.b_off[nh];
-      ph.act = Xtg_.p + D;  // critic target input [norm(boot) | pi(boot)]
-      ph.ld_act = Kp_;
+      ph.out = Xtg_.p + D;  // critic target input [norm(boot) | pi(boot)]
+      ph.ld_out = Kp_;
       ph.mid = (dims_.low + dims_.high) / 2.0f;
       ph.half = (dims_.high - dims_.low) / 2.0f;
-      steps_.push_back(mlp::head_finish_step(head_split_, ph, B, A));
+      steps_.push_back(mlp::head_squash_step(ph, in, ld, Wh, B, A, H));
     }
   }
 
@@ -567,7 +565,6 @@ void VLearner::build_update() {
 void VLearner::adopt_policy(const float* flat, int64_t version) {
   if (version < lagged_version_) return;  // learners.cpp:37-42
   PQLG_CUDA(cudaMemcpyAsync(lagged_.p, flat, pnet_.params * 4, cudaMemcpyHostToDevice, stream_));
-  lagged_head_.refresh(stream_);
   PQLG_CUDA(cudaStreamSynchronize(stream_));
   lagged_version_ = version;
 }
@@ -578,7 +575,6 @@ void VLearner::adopt_policy_sac(const float* flat, float log_alpha, int64_t vers
   PQLG_CUDA(cudaMemcpyAsync(lagged_.p, flat, pnet_.params * 4, cudaMemcpyHostToDevice, stream_));
   PQLG_CUDA(cudaMemcpyAsync(lagged_.p + pnet_.params, &log_alpha, 4, cudaMemcpyHostToDevice,
                             stream_));
-  lagged_head_.refresh(stream_);
   PQLG_CUDA(cudaStreamSynchronize(stream_));
   lagged_version_ = version;
 }
@@ -587,7 +583,6 @@ void VLearner::adopt_policy_device(const float* flat, int64_t version) {
   if (version < lagged_version_) return;  // learners.cpp:37-42
   PQLG_CUDA(cudaMemcpyAsync(lagged_.p, flat, snapshot_len() * 4, cudaMemcpyDeviceToDevice,
                             stream_));
-  lagged_head_.refresh(stream_);
   lagged_version_ = version;
 }
 
@@ -772,7 +767,6 @@ void VLearner::set_params(int which, const float* flat) {
     default: throw Error(PQLG_EINVAL, "set_params: which must be 0..4");
   }
   PQLG_CUDA(cudaMemcpyAsync(dst, flat, n * 4, cudaMemcpyHostToDevice, stream_));
-  if (which == 4) lagged_head_.refresh(stream_);
   PQLG_CUDA(cudaStreamSynchronize(stream_));
 }
 
