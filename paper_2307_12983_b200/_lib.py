@@ -7,10 +7,14 @@ Python mirror classes and the tests call through the exact C ABI.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libpqlg.so"
+# PQLG_LIB_VARIANT=name loads libpqlg_<name>.so (an in-tree A/B build of the
+# same sources with extra nvcc flags, tools/build_variant.sh); default: the product
+_VARIANT = os.environ.get("PQLG_LIB_VARIANT", "")
+LIB_PATH = _PKG / (f"libpqlg_{_VARIANT}.so" if _VARIANT else "libpqlg.so")
 
 PQLG_OK, PQLG_NOT_READY = 0, 1
 PQLG_EINVAL, PQLG_ENONFINITE, PQLG_ECUDA, PQLG_ENCCL = -1, -2, -3, -4

@@ -15,8 +15,12 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-BUILD = PKG / "_build"
-LIB = PKG / "libpqlg.so"
+# PQLG_NVCC_EXTRA: extra nvcc flags for an A/B variant build (tools only),
+# compiled into its own object directory
+EXTRA = os.environ.get("PQLG_NVCC_EXTRA", "").split()
+BUILD = PKG / (f"_build_{os.environ.get('PQLG_VARIANT_NAME', 'variant')}" if EXTRA else "_build")
+LIB = PKG / (f"libpqlg_{os.environ['PQLG_VARIANT_NAME']}.so" if os.environ.get("PQLG_VARIANT_NAME")
+             else "libpqlg.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
@@ -42,7 +46,7 @@ def _compile(src: Path, verbose: bool) -> Path:
     newest_dep = max([src.stat().st_mtime] + [h.stat().st_mtime for h in _headers()])
     if obj.exists() and obj.stat().st_mtime >= newest_dep:
         return obj
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *EXTRA, "-c", str(src), "-o", str(obj)]
     if verbose:
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -7,6 +7,7 @@
 // -> env step kernel (auto-reset, terminal obs, truncation) -> StepSlice
 // views -> running-normalizer update over the step's observations.
 #include <cmath>
+#include <cstdlib>
 #include <memory>
 #include <random>
 #include <vector>
@@ -74,7 +75,46 @@ struct DeviceEnv {
   // persistent grid: as many blocks as fit (occupancy), at most one per tile
   template <int kSlots>
   void step_as(const float* act, int64_t ld_act, const actor::StepOut& o, cudaStream_t st,
-               const actor::NextNorm& nn, const float* cur, int64_t ld_cur) {
+               const actor::NextNorm& nn, const float* cur, int64_t ld_cur,
+               const actor::NormPartialOut& np) {
+    actor::EnvState v = view();
+    if (cur) {  // the caller's obs buffers hold the state: read cur, write next_obs only
+      v.s = nullptr;
+      v.s_in = cur;
+      v.ld_in = ld_cur;
+    }
+    require(v.ld_in % 4 == 0 && (reinterpret_cast<uintptr_t>(v.s_in) & 15) == 0,
+            "env: state rows must be 16-byte aligned");
+    const int tiles = (N + actor::kEnvTile - 1) / actor::kEnvTile;
+    // the bulk path: one 16-byte row stride for state, boot, next obs and
+    // normalised next obs (the actor's Dp-wide buffers)
+    const bool rows16 = o.ld_obs == v.ld_in && (!nn.out || nn.ld_out == v.ld_in) &&
+                        (!v.s || v.ld == v.ld_in) &&
+                        ((reinterpret_cast<uintptr_t>(o.next_obs) | reinterpret_cast<uintptr_t>(o.boot) |
+                          reinterpret_cast<uintptr_t>(nn.out) | reinterpret_cast<uintptr_t>(v.s)) & 15) == 0;
+    if (rows16 && actor::env_tma_ok(act, ld_act, D, A, v.ld_in)) {
+      // TMA-fed persistent kernel, one CTA per SM (tma_grid(): the actor's
+      // normalizer partial count)
+      auto kern = actor::env_step_tma_kernel<kSlots>;
+      const size_t smem = actor::env_tma_smem(A, kSlots, v.ld_in, ld_act);
+      static size_t configured = 0;
+      if (configured < smem) {
+        PQLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+        configured = smem;
+      }
+#ifdef PQLG_ENV_TRACE
+      if (std::getenv("PQLG_ENV_NOPART")) {  // A/B only: no normalizer partials
+        launch(kern, dim3(tma_grid()), dim3(actor::kEnvTmaThreads), smem, st, v, act, ld_act, o, nn,
+               actor::NormPartialOut{});
+        return;
+      }
+#endif
+      launch(kern, dim3(tma_grid()), dim3(actor::kEnvTmaThreads), smem, st, v, act, ld_act, o, nn,
+             np);
+      return;
+    }
+    require(!np.partial, "env: normalizer partials need the TMA step (16-byte rows)");
     auto kern = actor::env_step_kernel<kSlots>;
     const size_t smem = actor::env_step_smem(D, A, kSlots);
     static int per_sm = 0;
@@ -87,27 +127,24 @@ struct DeviceEnv {
       if (per_sm < 1) per_sm = 1;
       per_sm_smem = smem;
     }
-    const int tiles = (N + actor::kEnvTile - 1) / actor::kEnvTile;
     const int blocks = std::min(tiles, per_sm * mlp::kSMs);
-    actor::EnvState v = view();
-    if (cur) {  // the caller's obs buffers hold the state: read cur, write next_obs only
-      v.s = nullptr;
-      v.s_in = cur;
-      v.ld_in = ld_cur;
-    }
-    require(v.ld_in % 4 == 0 && (reinterpret_cast<uintptr_t>(v.s_in) & 15) == 0,
-            "env: state rows must be 16-byte aligned");
     launch(kern, dim3(blocks), dim3(32 * actor::kEnvWarps), smem, st, v, act, ld_act, o, nn);
+  }
+  // blocks of the TMA step = partial sums it writes (one per SM, <= tiles)
+  int tma_grid() const {
+    const int tiles = (N + actor::kEnvTile - 1) / actor::kEnvTile;
+    return std::min(tiles, mlp::kSMs);
   }
   // cur: optional obs buffer holding the current state (the actor's double
   // buffer); then the internal state array is neither read nor written.
+  // np: optional running-normalizer partials of the next observations.
   void step(const float* act, int64_t ld_act, const actor::StepOut& o, cudaStream_t st,
             const actor::NextNorm& nn = actor::NextNorm{}, const float* cur = nullptr,
-            int64_t ld_cur = 0) {
+            int64_t ld_cur = 0, const actor::NormPartialOut& np = actor::NormPartialOut{}) {
     require(A <= actor::kMaxA, "env: act_dim > 32 not supported");
     require(D <= actor::kMaxD, "env: obs_dim > 256 not supported");
-    if ((D + 3) / 4 <= 32) step_as<1>(act, ld_act, o, st, nn, cur, ld_cur);
-    else step_as<2>(act, ld_act, o, st, nn, cur, ld_cur);
+    if ((D + 3) / 4 <= 32) step_as<1>(act, ld_act, o, st, nn, cur, ld_cur, np);
+    else step_as<2>(act, ld_act, o, st, nn, cur, ld_cur, np);
   }
 };
 
@@ -201,7 +238,11 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
     ngather_.alloc(static_cast<size_t>(comm_->world) * (2 * D_ + 1));
   }
   nticket_.alloc(actor::norm_tickets(D_));
+  nshift_.alloc(D_);
   status_.alloc(1);
+  // the first step's normalizer partials (later steps get them from the env
+  // step that produced their observations)
+  actor::norm_partial(obs_[0].p, Dp_, N_, D_, env_->tma_grid(), npart_.p, nshift_.p, stream_);
   // first policy input: apply_stats with count 0 is the identity
   launch(actor::normalize_kernel, dim3(4 * mlp::kSMs), dim3(256), 0, stream_, obs_[0].p, Dp_, Xn_.p, Dp_,
                                                                mean_f_.p, inv_f_.p, identity_.p,
@@ -293,7 +334,8 @@ void Actor::enqueue(int cur) {
   // the next policy input apply(stats_t, obs_{t+1}) directly.
   actor::NormState ns{count_.p, mean_.p, m2_.p, mean_f_.p, inv_f_.p, identity_.p,
                       comm_ ? nbatch_.p : nullptr};
-  actor::norm_update(obs, Dp_, N, D, npart_.p, nticket_.p, ns, st);
+  // the partial sums of obs were written by the env step that produced them
+  actor::norm_finish(nshift_.p, N, D, env_->tma_grid(), npart_.p, nticket_.p, ns, st);
   if (comm_) {
     // sharded: every shard's batch statistics, merged in rank
     // order into identical running stats on all shards (5 KB at config 3)
@@ -307,7 +349,9 @@ void Actor::enqueue(int cur) {
   actor::StepOut o{obs_[nxt].p, boot_[cur].p, rew_[cur].p, term_[cur].p, trunc_[cur].p, nullptr,
                    Dp_, status_.p};
   actor::NextNorm nn{Xn_.p, Dp_, mean_f_.p, inv_f_.p, identity_.p};
-  env_->step(act_[cur].p, Ap_, o, st, nn, obs, Dp_);
+  // ... and the partials of the next observations for the next step's update
+  actor::NormPartialOut np{reinterpret_cast<double2*>(npart_.p), nshift_.p, mean_.p};
+  env_->step(act_[cur].p, Ap_, o, st, nn, obs, Dp_, np);
 }
 
 int Actor::kernels_per_step() {
@@ -740,11 +784,18 @@ int pqlg_k_normalizer_update(int64_t* count_dev, double* mean_dev, double* m2_de
     DevBuf<double> part(static_cast<size_t>(actor::kNormBlocks) * dim * 2);
     DevBuf<int> ident(1);
     DevBuf<unsigned int> ticket(actor::norm_tickets(dim));
+    DevBuf<double> shift(dim);
     const int64_t ldx = ld > 0 ? ld : dim;
     actor::NormState ns{count_dev, mean_dev, m2_dev, mean_f_dev, inv_f_dev, ident.p};
-    actor::norm_update(batch_dev, ldx, rows, dim, part.p, ticket.p, ns, st);
+    actor::norm_update(batch_dev, ldx, rows, dim, part.p, shift.p, ticket.p, ns, st);
     PQLG_CUDA(cudaStreamSynchronize(st));
   });
 }
 
 }  // extern "C"
+
+#ifdef PQLG_ENV_TRACE
+extern "C" __attribute__((visibility("default"))) int pqlg_env_trace_set(unsigned long long* buf) {
+  return pqlg::guarded([&] { PQLG_CUDA(cudaMemcpyToSymbol(pqlg::actor::g_env_trace, &buf, sizeof(buf))); });
+}
+#endif

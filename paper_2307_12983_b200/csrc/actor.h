@@ -87,7 +87,9 @@ class Actor {
   DevBuf<uint64_t> noise_rng_;
   DevBuf<float> sigma_;
   DevBuf<int64_t> count_;
-  DevBuf<double> mean_, m2_, npart_;
+  // npart_/nshift_: running-normalizer partial sums of the current
+  // observations and their shift (written by the previous env step)
+  DevBuf<double> mean_, m2_, npart_, nshift_;
   DevBuf<unsigned int> nticket_;
   DevBuf<float> mean_f_, inv_f_;
   DevBuf<int> identity_;

@@ -61,7 +61,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   do {                                                                                \
     if (g_trace) {                                                                    \
       const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
-      g_trace[bid * 8 + (slot)] = (value);                                            \
+      g_trace[bid * 16 + (slot)] = (value);                                           \
     }                                                                                 \
   } while (0)
 #else
@@ -117,6 +117,7 @@ struct SmemLayout {
   // 3xTF32: [A_hi | B_hi | A_lo | B_lo] per stage
   static constexpr int kStageBytes = k3x ? 2 * kLoadBytes : kLoadBytes;
   // one 4 KB (32 x 32 fp32, 128B-swizzled) TMA-store staging buffer per warp
+  // (a second one per warp was measured slower: tools/gpu_ab2.sh, DESIGN 9c)
   static constexpr int kStagingBytes = Epi::kStoreRank > 0 ? kEpiWarps * 4096 : 0;
   static constexpr int kFixed = kStagingBytes + kScratchBytes + 256;
   static constexpr int kFit = (kMaxDynSmem - kFixed) / kStageBytes;
@@ -439,6 +440,9 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair, k3x>::kThreads, 1)
         }
         if constexpr (kPair) ptx::mma_commit_pair(&tmem_full[a]);
         else ptx::mma_commit(&tmem_full[a]);
+#ifdef PQLG_GEMM_TRACE
+        if (lt == 0) PQLG_TRACE(14, clock64());
+#endif
       }
 #ifdef PQLG_GEMM_TRACE
       PQLG_TRACE(3, clock64());
@@ -502,6 +506,7 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair, k3x>::kThreads, 1)
       ptx::tc_fence_after();
 #ifdef PQLG_GEMM_TRACE
       if (threadIdx.x == 64 && lt == 0) PQLG_TRACE(4, clock64());
+      if (threadIdx.x == 64 && lt == 1) PQLG_TRACE(13, clock64());
 #endif
       const uint32_t t_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + a * BN;
       uint32_t r[32];
@@ -541,6 +546,9 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair, k3x>::kThreads, 1)
             ++nstore;
           }
         }
+#ifdef PQLG_GEMM_TRACE
+        if (threadIdx.x == 64 && lt == 0 && c - c_begin < 4) PQLG_TRACE(8 + c - c_begin, clock64());
+#endif
       }
       // every tcgen05.ld of this warp has completed: release the accumulator
       ptx::tc_fence_before();
@@ -550,6 +558,9 @@ __global__ void __launch_bounds__(SmemLayout<BN, Epi, kPair, k3x>::kThreads, 1)
         else ptx::mbar_arrive(&tmem_empty[a]);
       }
       epi.end(row, ctx);
+#ifdef PQLG_GEMM_TRACE
+      if (threadIdx.x == 64 && lt == 0) PQLG_TRACE(12, clock64());
+#endif
     }
     if constexpr (Epi::kStoreRank > 0) {
       if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
