@@ -316,26 +316,42 @@ void Actor::build() {
   ph.low = dims_.low;
   ph.high = dims_.high;
   const float* W = pol_.p + pnet_.w_off[nh];
+  // the head's W in fragment order, re-packed whenever the policy changes
+  wpack_.alloc(static_cast<size_t>(mlp::head_pack_elems(A, H)) * 4);
+  ph.wpack = reinterpret_cast<const float4*>(wpack_.p);
+  pack_head();
   for (int k = 0; k < kSets; ++k) {
     ph.out = act_[k].p;
     head_steps_[k] = mlp::head_squash_step(ph, in, ld, W, N, A, H);
   }
 }
 
+void Actor::pack_head() {
+  if (!wpack_.p) return;  // (pql_sac: split-K head, no packed weights)
+  mlp::head_pack(pol_.p + pnet_.w_off[nh_], A_, H_, A_, reinterpret_cast<float4*>(wpack_.p),
+                 cfg_.precision == PQLG_PREC_3XTF32, stream_);
+}
+
 void Actor::enqueue(int cur) {
   cudaStream_t st = stream_;
   const int N = N_, D = D_;
   const float* obs = obs_[cur].p;
+  // PQLG_SKIP_STEP=i drops launch i of the step (tools/skip_probe.py: in-situ
+  // marginal costs; the results of such a step are meaningless)
+  const int skip = skip_step();
+  int idx = 0;
+  auto keep = [&] { return idx++ != skip; };
   // actions = pi(obs_norm) + mixed noise; Xn_ holds apply(stats_{t-1}, obs_t)
-  for (auto& s : policy_steps_) s(st);
-  head_steps_[cur](st);
+  for (auto& s : policy_steps_)
+    if (keep()) s(st);
+  if (keep()) head_steps_[cur](st);
   // normalizer_.update(obs_) (learners.cpp:113): it only reads this step's
   // observations, so it runs before the env step and the env kernel can emit
   // the next policy input apply(stats_t, obs_{t+1}) directly.
   actor::NormState ns{count_.p, mean_.p, m2_.p, mean_f_.p, inv_f_.p, identity_.p,
                       comm_ ? nbatch_.p : nullptr};
   // the partial sums of obs were written by the env step that produced them
-  actor::norm_finish(nshift_.p, N, D, env_->tma_grid(), npart_.p, nticket_.p, ns, st);
+  if (keep()) actor::norm_finish(nshift_.p, N, D, env_->tma_grid(), npart_.p, nticket_.p, ns, st);
   if (comm_) {
     // sharded: every shard's batch statistics, merged in rank
     // order into identical running stats on all shards (5 KB at config 3)
@@ -351,7 +367,7 @@ void Actor::enqueue(int cur) {
   actor::NextNorm nn{Xn_.p, Dp_, mean_f_.p, inv_f_.p, identity_.p};
   // ... and the partials of the next observations for the next step's update
   actor::NormPartialOut np{reinterpret_cast<double2*>(npart_.p), nshift_.p, mean_.p};
-  env_->step(act_[cur].p, Ap_, o, st, nn, obs, Dp_, np);
+  if (keep()) env_->step(act_[cur].p, Ap_, o, st, nn, obs, Dp_, np);
 }
 
 int Actor::kernels_per_step() {
@@ -419,6 +435,7 @@ void Actor::adopt_policy(const float* flat, int64_t version, bool device) {
   // device snapshots carry [net | log_alpha]; the host ABI passes the net
   PQLG_CUDA(cudaMemcpyAsync(pol_.p, flat, (device ? snapshot_len() : pnet_.params) * 4,
                             device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream_));
+  pack_head();
   if (!device) PQLG_CUDA(cudaStreamSynchronize(stream_));
   version_ = version;
 }

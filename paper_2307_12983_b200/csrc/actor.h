@@ -83,6 +83,8 @@ class Actor {
   DevBuf<float> obs_[kSets], boot_[kSets], rew_[kSets], act_[kSets], Xn_;
   DevBuf<uint8_t> term_[kSets], trunc_[kSets];
   DevBuf<float> pol_;
+  DevBuf<float> wpack_;  // policy head W in the head kernel's fragment order
+  void pack_head();
   std::vector<DevBuf<float>> pact_;
   DevBuf<uint64_t> noise_rng_;
   DevBuf<float> sigma_;

@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "pdl.cuh"
+#include "ptx.cuh"
 
 namespace pqlg::head {
 
@@ -101,19 +102,49 @@ struct RowsArgs {
   uint64_t* noise_state;  // nullable: per-row SplitMix state (actor exploration)
   const float* sigma;     // [M]
   float low, high;
+  // nullable: W already in the kernel's fragment order ([KB][kNT][32] float4,
+  // head_pack_kernel), copied into shared memory with cp.async instead of
+  // being gathered from W (the actor packs it whenever its policy changes)
+  const float4* wpack;
 };
+
+// W -> the head kernel's B-fragment order (tf32-rounded; raw for 3xTF32):
+// element e = (kb * kNT + nt) * 32 + lane (g, t) holds W[16 kb + 4 t + q][8 nt + g], q = 0..3.
+template <int kNT, bool k3x>
+static __global__ void head_pack_kernel(const float* __restrict__ w, int64_t ldw, int K, int N,
+                                        float4* __restrict__ out) {
+  pdl::entry();
+  const int KB = (K + 15) >> 4;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= KB * kNT * 32) return;
+  const int ln = e & 31, nt = (e >> 5) % kNT, kb = (e >> 5) / kNT;
+  const int g = ln >> 2, t = ln & 3;
+  const int n = 8 * nt + g;
+  float v[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int k = 16 * kb + 4 * t + q;
+    v[q] = (k < K && n < N) ? w[static_cast<int64_t>(k) * ldw + n] : 0.0f;
+    if constexpr (!k3x) {
+      uint32_t r;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v[q]));
+      v[q] = __uint_as_float(r);
+    }
+  }
+  out[e] = make_float4(v[0], v[1], v[2], v[3]);
+}
 
 // The row's A normals (normal_distribution<float> polar pairs over its
 // stream) drawn by the G lanes of its group: candidate pair c of the row uses
 // stream states s0 + 2c, s0 + 2c + 1; accepted candidates are consumed in
 // order.  Lanes of finished groups idle until the warp is done.
 template <int G>
-__device__ __forceinline__ void group_row_normals(uint64_t* state, bool active, int A, int j,
-                                                  float* z) {
+__device__ __forceinline__ void group_row_normals(uint64_t* state, uint64_t s0, bool active, int A,
+                                                  int j, float* z) {
   const int lane = threadIdx.x & 31;
   const int base = lane & ~(G - 1);
   const unsigned gm = (G == 32) ? 0xffffffffu : ((1u << G) - 1u);
-  const uint64_t s0 = active ? *state : 0ull;
+  if (!active) s0 = 0ull;
   const int need = (A + 1) / 2;
   int got = 0;
   bool done = !active;
@@ -182,28 +213,10 @@ static __global__ void __launch_bounds__(32 * kHeadWarps)
   float* xch = reinterpret_cast<float*>(wf + static_cast<int64_t>(KB) * kNT * 32);
   float* sz = xch + 4 * 32 * kNT * 4;                         // [64][kNT * 8]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // stage W fragments.  W is never written by the kernel right before this
-  // one on any stream that runs it (hidden-layer GEMM / activations only),
-  // and under PDL every earlier kernel has completed when this grid starts,
-  // so the staging overlaps the previous kernel's tail.
-  for (int e = tid; e < KB * kNT * 32; e += 32 * kHeadWarps) {
-    const int ln = e & 31, nt = (e >> 5) % kNT, kb = (e >> 5) / kNT;
-    const int g = ln >> 2, t = ln & 3;
-    const int n = 8 * nt + g;
-    float v[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int k = 16 * kb + 4 * t + q;
-      v[q] = (k < K && n < N) ? __ldg(a.w + static_cast<int64_t>(k) * a.ldw + n) : 0.0f;
-    }
-    if constexpr (k3x) {  // raw fp32: split hi / lo where it is used
-      wf[e] = make_float4(v[0], v[1], v[2], v[3]);
-    } else {
-      wf[e] = make_float4(__uint_as_float(tf32_bits(v[0])), __uint_as_float(tf32_bits(v[1])),
-                          __uint_as_float(tf32_bits(v[2])), __uint_as_float(tf32_bits(v[3])));
-    }
-  }
-  __syncthreads();
+  // A loads first (the previous kernel's output), then -- while they are in
+  // flight -- the exploration inputs, the W fragments and the noise draws.
+  // (The previous grid holds every SM until it drains, so staging W before
+  // the PDL wait would not overlap anything.)
   pdl::entry();
   const int mt = warp & 3, kh = warp >> 2;
   const int g = lane >> 2, t = lane & 3;
@@ -225,17 +238,77 @@ static __global__ void __launch_bounds__(32 * kHeadWarps)
     }
   };
   load(kb0);
+  // exploration inputs: the draw rows' sigma and SplitMix state, the finish
+  // rows' sigma
+  float sig_draw[2] = {0.0f, 0.0f}, sig_fin[2] = {0.0f, 0.0f};
+  uint64_t st_draw[2] = {0ull, 0ull};
+  if (a.noise_state) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int m = blockIdx.x * kHeadRows + warp * 8 + c * 4 + (lane >> 3);
+      if (m < a.M) {
+        sig_draw[c] = a.sigma[m];
+        st_draw[c] = a.noise_state[m];
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int m = row0 + g + 8 * h;
+      if (kh == 0 && m < a.M) sig_fin[h] = a.sigma[m];
+    }
+  }
+  if (a.wpack) {
+    // packed fragments: 16-byte cp.async copies, completed before the barrier below
+    for (int e = tid; e < KB * kNT * 32; e += 32 * kHeadWarps)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ptx::smem_u32(wf + e)),
+                   "l"(a.wpack + e)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  // otherwise stage W fragments (kWU fragments' loads in flight per thread
+  // before any is converted)
+  constexpr int kWU = 4;
+  for (int e0 = a.wpack ? KB * kNT * 32 : tid; e0 < KB * kNT * 32; e0 += kWU * 32 * kHeadWarps) {
+    float v[kWU][4];
+#pragma unroll
+    for (int u = 0; u < kWU; ++u) {
+      const int e = e0 + u * 32 * kHeadWarps;
+      const int ln = e & 31, nt = (e >> 5) % kNT, kb = (e >> 5) / kNT;
+      const int gg = ln >> 2, tt = ln & 3;
+      const int n = 8 * nt + gg;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = 16 * kb + 4 * tt + q;
+        v[u][q] = (e < KB * kNT * 32 && k < K && n < N)
+                      ? __ldg(a.w + static_cast<int64_t>(k) * a.ldw + n) : 0.0f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kWU; ++u) {
+      const int e = e0 + u * 32 * kHeadWarps;
+      if (e >= KB * kNT * 32) break;
+      if constexpr (k3x) {  // raw fp32: split hi / lo where it is used
+        wf[e] = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+      } else {
+        wf[e] = make_float4(__uint_as_float(tf32_bits(v[u][0])), __uint_as_float(tf32_bits(v[u][1])),
+                            __uint_as_float(tf32_bits(v[u][2])), __uint_as_float(tf32_bits(v[u][3])));
+      }
+    }
+  }
   // exploration draws for the block's 64 rows (8 lanes per row, 4 rows per
-  // warp per call, 2 calls per warp) while the first loads are in flight
+  // warp per call, 2 calls per warp)
   if (a.noise_state) {
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const int r = warp * 8 + c * 4 + (lane >> 3);  // block row
       const int m = blockIdx.x * kHeadRows + r;
-      const bool on = m < a.M && a.sigma[m < a.M ? m : 0] > 0.0f;
-      group_row_normals<8>(a.noise_state + (m < a.M ? m : 0), on, N, lane & 7, sz + r * kNT * 8);
+      const bool on = m < a.M && sig_draw[c] > 0.0f;
+      group_row_normals<8>(a.noise_state + (m < a.M ? m : 0), st_draw[c], on, N, lane & 7,
+                           sz + r * kNT * 8);
     }
   }
+  if (a.wpack) asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();  // W fragments (and the draws) staged
   float acc[kNT][4];
 #pragma unroll
   for (int nt = 0; nt < kNT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.0f;
@@ -303,7 +376,7 @@ static __global__ void __launch_bounds__(32 * kHeadWarps)
     const int m = row0 + g + 8 * h;
     if (m >= a.M) continue;
     const int br = 16 * mt + g + 8 * h;  // block row
-    const float sig = a.noise_state ? a.sigma[m] : 0.0f;
+    const float sig = sig_fin[h];
 #pragma unroll
     for (int nt = 0; nt < kNT; ++nt)
 #pragma unroll

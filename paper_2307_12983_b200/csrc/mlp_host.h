@@ -276,6 +276,33 @@ inline Step head_rows_step(head::RowsArgs r, const float* x, int64_t ldx, const 
   return [r, fn](cudaStream_t st) { fn(r, st); };
 }
 
+// Packs W [K x ldw] (columns [0, N)) into the head kernel's fragment order
+// (RowsArgs::wpack; head_pack_elems float4).
+inline int64_t head_pack_elems(int N, int K) {
+  return static_cast<int64_t>((K + 15) / 16) * ((N + 7) / 8) * 32;
+}
+template <int kNT>
+inline void launch_head_pack(const float* W, int64_t ldw, int K, int N, float4* out, bool x3,
+                             cudaStream_t st) {
+  const int n = static_cast<int>(head_pack_elems(N, K));
+  if (x3) launch(head::head_pack_kernel<kNT, true>, dim3((n + 255) / 256), dim3(256), 0, st, W, ldw, K, N, out);
+  else launch(head::head_pack_kernel<kNT, false>, dim3((n + 255) / 256), dim3(256), 0, st, W, ldw, K, N, out);
+}
+inline void head_pack(const float* W, int64_t ldw, int K, int N, float4* out, bool x3,
+                      cudaStream_t st) {
+  switch ((N + 7) / 8) {
+    case 1: launch_head_pack<1>(W, ldw, K, N, out, x3, st); break;
+    case 2: launch_head_pack<2>(W, ldw, K, N, out, x3, st); break;
+    case 3: launch_head_pack<3>(W, ldw, K, N, out, x3, st); break;
+    case 4: launch_head_pack<4>(W, ldw, K, N, out, x3, st); break;
+    case 5: launch_head_pack<5>(W, ldw, K, N, out, x3, st); break;
+    case 6: launch_head_pack<6>(W, ldw, K, N, out, x3, st); break;
+    case 7: launch_head_pack<7>(W, ldw, K, N, out, x3, st); break;
+    case 8: launch_head_pack<8>(W, ldw, K, N, out, x3, st); break;
+    default: launch_head_pack<9>(W, ldw, K, N, out, x3, st); break;
+  }
+}
+
 // Raw head sums into hs.part (one "split", row stride round_up(N, 4)) for a
 // finish kernel that adds the bias itself (the SAC Gaussian finish).
 inline Step head_raw_step(HeadSplit& hs, const float* x, int64_t ldx, const float* W, int M,

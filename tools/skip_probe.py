@@ -3,7 +3,7 @@ box): the update graph is rebuilt with PQLG_SKIP_STEP=i (one process per i)
 and replayed; cost(i) = t(full) - t(without step i).  Results of the skipped
 runs are meaningless -- only their time is used.
 
-  python tools/skip_probe.py critic|policy [n_steps]
+  python tools/skip_probe.py critic|policy|actor [n_steps]
 """
 import os
 import subprocess
@@ -24,12 +24,16 @@ if "@WHAT@" == "critic":
     rp = C.c_void_p(); _lib.call("pqlg_vlearner_replay", h, C.byref(rp))
     _lib.call("pqlg_replay_fill_synthetic", rp, 1_000_000, 7, np.float32(0.970299), 200)
     fn = "pqlg_vlearner_update_n"; kfn = "pqlg_vlearner_kernels_per_update"
+elif "@WHAT@" == "actor":
+    _lib.call("pqlg_actor_create", C.byref(cfg), C.byref(dims), sp, C.byref(h))
+    fn = "pqlg_actor_rollout_n"; kfn = None
 else:
     _lib.call("pqlg_plearner_create", C.byref(cfg), C.byref(dims), 1, sp, C.byref(h))
     s = torch.randn(1_000_000, D, device="cuda")
     _lib.call("pqlg_plearner_ingest", h, s.data_ptr(), D, 1_000_000)
     fn = "pqlg_plearner_update_n"; kfn = "pqlg_plearner_kernels_per_update"
-k = C.c_int(); _lib.call(kfn, h, C.byref(k))
+k = C.c_int(6)
+if kfn: _lib.call(kfn, h, C.byref(k))
 _lib.lib()[fn](h, 10); st.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 best = 1e9
