@@ -320,10 +320,20 @@ void Actor::build() {
   wpack_.alloc(static_cast<size_t>(mlp::head_pack_elems(A, H)) * 4);
   ph.wpack = reinterpret_cast<const float4*>(wpack_.p);
   pack_head();
+  // the normalizer update's finish (independent of the policy) rides in the
+  // head launch as extra blocks
+  ph.fin = actor::norm_finish_args(nshift_.p, N, D_, env_->tma_grid(), npart_.p, nticket_.p,
+                                   norm_state());
+  fused_finish_ = true;
   for (int k = 0; k < kSets; ++k) {
     ph.out = act_[k].p;
     head_steps_[k] = mlp::head_squash_step(ph, in, ld, W, N, A, H);
   }
+}
+
+actor::NormState Actor::norm_state() const {
+  return actor::NormState{count_.p, mean_.p, m2_.p, mean_f_.p, inv_f_.p, identity_.p,
+                          comm_ ? nbatch_.p : nullptr};
 }
 
 void Actor::pack_head() {
@@ -348,10 +358,11 @@ void Actor::enqueue(int cur) {
   // normalizer_.update(obs_) (learners.cpp:113): it only reads this step's
   // observations, so it runs before the env step and the env kernel can emit
   // the next policy input apply(stats_t, obs_{t+1}) directly.
-  actor::NormState ns{count_.p, mean_.p, m2_.p, mean_f_.p, inv_f_.p, identity_.p,
-                      comm_ ? nbatch_.p : nullptr};
+  actor::NormState ns = norm_state();
   // the partial sums of obs were written by the env step that produced them
-  if (keep()) actor::norm_finish(nshift_.p, N, D, env_->tma_grid(), npart_.p, nticket_.p, ns, st);
+  // (the finish runs inside the head launch unless the head is pql_sac's)
+  if (!fused_finish_ && keep())
+    actor::norm_finish(nshift_.p, N, D, env_->tma_grid(), npart_.p, nticket_.p, ns, st);
   if (comm_) {
     // sharded: every shard's batch statistics, merged in rank
     // order into identical running stats on all shards (5 KB at config 3)

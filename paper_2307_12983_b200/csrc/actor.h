@@ -85,6 +85,8 @@ class Actor {
   DevBuf<float> pol_;
   DevBuf<float> wpack_;  // policy head W in the head kernel's fragment order
   void pack_head();
+  bool fused_finish_ = false;  // normalizer finish inside the head launch
+  actor::NormState norm_state() const;
   std::vector<DevBuf<float>> pact_;
   DevBuf<uint64_t> noise_rng_;
   DevBuf<float> sigma_;

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "ptx.cuh"
+#include "norm_finish.cuh"
 #include "rng.cuh"
 #include "common.h"
 
@@ -867,28 +868,6 @@ static __global__ void normalize_kernel(const float* __restrict__ x, int64_t ldx
   }
 }
 
-struct NormState {
-  int64_t* count;
-  double* mean;
-  double* m2;
-  float* mean_f;
-  float* inv_f;
-  int* identity;
-  // sharded actor: non-null -> the batch's (mean [D], M2 [D], n) are written
-  // here instead of being merged (norm_merge_kernel merges every shard's)
-  double* batch;
-};
-
-// Chan's parallel merge of (na, mean_a, m2_a) with a batch (nb, mean_b, m2_b)
-// (normalizer.hpp:73-83), fp64, in the reference's operation order.
-__device__ __forceinline__ void chan_merge(double na, double& mean, double& m2, double nb,
-                                           double bmean, double bm2) {
-  const double nab = na + nb;
-  const double delta = bmean - mean;
-  mean = mean + delta * (nb / nab);
-  m2 = m2 + (bm2 + delta * delta * (na * nb / nab));
-}
-
 // RunningNormalizer::update (normalizer.hpp:33-50, :73-83) in two launches,
 // parallel and deterministic:
 //   norm_partial_kernel  one wave of row blocks (kNormBlocks): block g takes a
@@ -908,7 +887,6 @@ constexpr int kNormBlocks = 148;      // partial rows (one wave, upper bound)
 constexpr int kNormThreads = 512;     // partial kernel: 8 row lanes x 64 quads
 constexpr int kNormQuads = 64;
 constexpr int kNormLanes = kNormThreads / kNormQuads;
-constexpr int kNormFinishWarps = 16;
 inline int norm_blocks(int N) {
   // at least ~32 rows per block so the fixed cost amortises
   int g = (N + 31) / 32;
@@ -993,71 +971,10 @@ static __global__ void __launch_bounds__(kNormThreads)
 }
 
 static __global__ void __launch_bounds__(32 * kNormFinishWarps)
-    norm_finish_kernel(const double* __restrict__ shift, int N, int D, int blocks,
-                       const double2* __restrict__ partial, unsigned int* ticket, NormState s) {
+    norm_finish_kernel(const NormFinishArgs f) {
   pdl::entry();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + lane;
-  __shared__ double2 red[kNormFinishWarps][32];
-  double a1 = 0.0, a2 = 0.0;
-  if (c < D) {
-    constexpr int kIn = 4;
-    for (int k0 = w; k0 < blocks; k0 += kNormFinishWarps * kIn) {
-      double2 v[kIn];
-#pragma unroll
-      for (int t = 0; t < kIn; ++t) {
-        const int k = k0 + kNormFinishWarps * t;
-        v[t] = k < blocks ? __ldcg(partial + static_cast<int64_t>(k) * D + c) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int t = 0; t < kIn; ++t) {
-        a1 += v[t].x;
-        a2 += v[t].y;
-      }
-    }
-  }
-  red[w][lane] = make_double2(a1, a2);
-  __syncthreads();
-  const int64_t n0i = s.batch ? 0 : *s.count;
-  if (w == 0 && c < D) {
-    const double nb = static_cast<double>(N);
-    const double na = static_cast<double>(n0i);
-    const int64_t cnt = n0i + N;
-    double t1 = 0.0, t2 = 0.0;
-#pragma unroll
-    for (int k = 0; k < kNormFinishWarps; ++k) {
-      t1 += red[k][lane].x;
-      t2 += red[k][lane].y;
-    }
-    const double bmean = shift[c] + t1 / nb;
-    double bm2 = t2 - t1 * t1 / nb;
-    if (bm2 < 0.0) bm2 = 0.0;
-    if (s.batch) {
-      s.batch[c] = bmean;
-      s.batch[D + c] = bm2;
-    } else {
-      double mean = s.mean[c], m2 = s.m2[c];
-      chan_merge(na, mean, m2, nb, bmean, bm2);
-      s.mean[c] = mean;
-      s.m2[c] = m2;
-      s.mean_f[c] = static_cast<float>(mean);
-      s.inv_f[c] = static_cast<float>(1.0 / sqrt(m2 / static_cast<double>(cnt) + 1e-8));
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    // every block read the old count before its ticket: the last one advances it
-    if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
-      if (s.batch) {
-        s.batch[2 * D] = static_cast<double>(N);
-      } else {
-        *s.count = n0i + N;
-        *s.identity = n0i + N <= 1 ? 1 : 0;
-      }
-      *ticket = 0u;
-    }
-  }
+  __shared__ double2 red[kNormFinishWarps * 32];
+  norm_finish_block(f, blockIdx.x, red);
 }
 
 // Host: the update's two launches (partial buffer: kNormBlocks x D double2,
@@ -1075,10 +992,16 @@ inline void norm_partial(const float* x, int64_t ldx, int N, int D, int blocks, 
     launch(norm_partial_kernel<false>, dim3(blocks), dim3(kNormThreads), 0, st, x, ldx, N, D, part,
            shift);
 }
+inline NormFinishArgs norm_finish_args(const double* shift, int N, int D, int blocks,
+                                       const double* partial, unsigned int* ticket,
+                                       const NormState& ns) {
+  return NormFinishArgs{shift, N, D, blocks, reinterpret_cast<const double2*>(partial), ticket, ns,
+                        norm_finish_blocks(D)};
+}
 inline void norm_finish(const double* shift, int N, int D, int blocks, const double* partial,
                         unsigned int* ticket, const NormState& ns, cudaStream_t st) {
-  launch(norm_finish_kernel, dim3((D + 31) / 32), dim3(32 * kNormFinishWarps), 0, st, shift, N, D,
-         blocks, reinterpret_cast<const double2*>(partial), ticket, ns);
+  launch(norm_finish_kernel, dim3(norm_finish_blocks(D)), dim3(32 * kNormFinishWarps), 0, st,
+         norm_finish_args(shift, N, D, blocks, partial, ticket, ns));
 }
 inline void norm_update(const float* x, int64_t ldx, int N, int D, double* partial, double* shift,
                         unsigned int* ticket, const NormState& ns, cudaStream_t st) {

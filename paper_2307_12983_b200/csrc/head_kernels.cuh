@@ -53,6 +53,7 @@ static __global__ void __launch_bounds__(32 * kFinishWarps)
 
 }  // namespace pqlg::head
 
+#include "norm_finish.cuh"
 #include "rng.cuh"
 
 namespace pqlg::head {
@@ -106,6 +107,9 @@ struct RowsArgs {
   // head_pack_kernel), copied into shared memory with cp.async instead of
   // being gathered from W (the actor packs it whenever its policy changes)
   const float4* wpack;
+  // optional: the actor's running-normalizer finish rides along as
+  // fin.nblk extra blocks after the head's (independent work, one launch)
+  actor::NormFinishArgs fin;
 };
 
 // W -> the head kernel's B-fragment order (tf32-rounded; raw for 3xTF32):
@@ -207,6 +211,12 @@ template <int kNT, bool k3x>
 static __global__ void __launch_bounds__(32 * kHeadWarps)
     head_mma_kernel(const __grid_constant__ RowsArgs a) {
   extern __shared__ float4 smem4[];
+  const int head_blocks = (a.M + kHeadRows - 1) / kHeadRows;
+  if (static_cast<int>(blockIdx.x) >= head_blocks) {  // normalizer finish blocks
+    pdl::entry();
+    actor::norm_finish_block(a.fin, blockIdx.x - head_blocks, reinterpret_cast<double2*>(smem4));
+    return;
+  }
   const int K = a.K, N = a.N;
   const int KB = (K + 15) >> 4;
   float4* wf = smem4;  // [KB][kNT][32]: tf32-rounded, or raw fp32 for 3xTF32

@@ -8,6 +8,8 @@
 //   wgrad  dW = H^T * G       H = [K=B x M=in] (M-major), G = [B x N] (N-major)
 #pragma once
 
+#include <algorithm>
+
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -236,8 +238,11 @@ inline void launch_head(const head::RowsArgs& r, cudaStream_t st) {
     PQLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     configured = true;
   }
-  launch(kern, dim3((r.M + head::kHeadRows - 1) / head::kHeadRows), dim3(32 * head::kHeadWarps),
-         smem, st, r);
+  const int fin = r.fin.partial ? r.fin.nblk : 0;
+  // finish blocks reuse the dynamic shared memory for their [16][32] double2
+  const size_t smem_all = fin ? std::max<size_t>(smem, actor::kNormFinishWarps * 32 * 16) : smem;
+  launch(kern, dim3((r.M + head::kHeadRows - 1) / head::kHeadRows + fin),
+         dim3(32 * head::kHeadWarps), smem_all, st, r);
 }
 
 template <int kNT>
