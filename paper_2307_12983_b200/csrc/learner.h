@@ -93,6 +93,8 @@ class VLearner {
   int64_t lagged_version_ = 0;
 
   DevBuf<float> q_, qt_, m_, v_, grads_, lagged_;
+  DevBuf<float> wpack_;  // lagged policy head W in the head kernel's fragment order
+  void lagged_changed();
   mlp::HeadSplit head_split_;  // split-K lagged-policy head
   std::unique_ptr<DeviceReplay> replay_;
   std::unique_ptr<DeviceNStep> nstep_;

@@ -246,6 +246,11 @@ void VLearner::build_update() {
       ph.ld_out = Kp_;
       ph.mid = (dims_.low + dims_.high) / 2.0f;
       ph.half = (dims_.high - dims_.low) / 2.0f;
+      // W in the head kernel's fragment order, re-packed when the lagged
+      // policy changes (lagged_changed)
+      wpack_.alloc(static_cast<size_t>(mlp::head_pack_elems(A, H)) * 4);
+      ph.wpack = reinterpret_cast<const float4*>(wpack_.p);
+      lagged_changed();
       steps_.push_back(mlp::head_squash_step(ph, in, ld, Wh, B, A, H));
     }
   }
@@ -562,9 +567,17 @@ void VLearner::build_update() {
   }
 }
 
+void VLearner::lagged_changed() {
+  if (!wpack_.p) return;
+  mlp::head_pack(lagged_.p + pnet_.w_off[pnet_.layers() - 1], dims_.act_dim, cfg_.hidden,
+                 dims_.act_dim, reinterpret_cast<float4*>(wpack_.p),
+                 cfg_.precision == PQLG_PREC_3XTF32, stream_);
+}
+
 void VLearner::adopt_policy(const float* flat, int64_t version) {
   if (version < lagged_version_) return;  // learners.cpp:37-42
   PQLG_CUDA(cudaMemcpyAsync(lagged_.p, flat, pnet_.params * 4, cudaMemcpyHostToDevice, stream_));
+  lagged_changed();
   PQLG_CUDA(cudaStreamSynchronize(stream_));
   lagged_version_ = version;
 }
@@ -583,6 +596,7 @@ void VLearner::adopt_policy_device(const float* flat, int64_t version) {
   if (version < lagged_version_) return;  // learners.cpp:37-42
   PQLG_CUDA(cudaMemcpyAsync(lagged_.p, flat, snapshot_len() * 4, cudaMemcpyDeviceToDevice,
                             stream_));
+  lagged_changed();
   lagged_version_ = version;
 }
 
@@ -767,6 +781,7 @@ void VLearner::set_params(int which, const float* flat) {
     default: throw Error(PQLG_EINVAL, "set_params: which must be 0..4");
   }
   PQLG_CUDA(cudaMemcpyAsync(dst, flat, n * 4, cudaMemcpyHostToDevice, stream_));
+  if (which == 4) lagged_changed();
   PQLG_CUDA(cudaStreamSynchronize(stream_));
 }
 
