@@ -936,6 +936,16 @@ def main():
         return
 
     r = run_ours(args, rank, world, local, Bg // world)
+    other_prec = None
+    if world == 1:  # the same update in the other GEMM precision mode, beside the headline
+        import argparse
+        a2 = argparse.Namespace(**vars(args))
+        a2.precision = 1 - args.precision
+        p2 = run_ours(a2, rank, world, local, Bg, timed=False)
+        other_prec = {"precision": ["tf32", "3xtf32"][a2.precision],
+                      "value": 1e3 / p2["ms_step"], "unit": "updates/s",
+                      "ms_per_step": p2["ms_step"],
+                      "note": "3xtf32: the fp32-faithful parity mode (pqlg_config.precision)"}
     weak = None
     if world > 1:  # B = 8192 per GPU beside the strong-scaling headline
         w = run_ours(args, rank, world, local, Bg, timed=False)
@@ -965,6 +975,8 @@ def main():
                batch_per_gpu=r["batch_per_rank"])
     if weak:
         out["weak_scaling"] = weak
+    if other_prec:
+        out["critic_other_precision"] = other_prec
     actor["workload"] = (f"{args.config}: rollout_step + V/P ingest, {N} envs per GPU "
                          f"(scaling: weak)")
     actor_c5["workload"] = (f"c5: rollout_step + V/P ingest, {C5_ENVS} envs over {world} GPU(s) "

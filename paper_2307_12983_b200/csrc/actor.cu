@@ -288,7 +288,17 @@ void Actor::build() {
   if (sac_) {
     // GaussianPolicy::sample with a fresh normal_distribution per env over
     // its noise stream (learners.cpp:87-94): split-K head + sampling finish
-    auto gemm = mlp::head_raw_step(head_split_, in, ld, pol_.p + pnet_.w_off[nh], N, 2 * A, H);
+    // packed head weights and the normalizer finish ride in the head launch
+    // (as for the deterministic head below)
+    head::RowsArgs base{};
+    wpack_.alloc(static_cast<size_t>(mlp::head_pack_elems(2 * A, H)) * 4);
+    base.wpack = reinterpret_cast<const float4*>(wpack_.p);
+    pack_head();
+    base.fin = actor::norm_finish_args(nshift_.p, N, D_, env_->tma_grid(), npart_.p, nticket_.p,
+                                       norm_state());
+    fused_finish_ = true;
+    auto gemm = mlp::head_raw_step(head_split_, in, ld, pol_.p + pnet_.w_off[nh], N, 2 * A, H,
+                                   base);
     sac::GaussArgs g{};
     g.bias = pol_.p + pnet_.b_off[nh];
     g.rng = noise_rng_.p;
@@ -337,8 +347,9 @@ actor::NormState Actor::norm_state() const {
 }
 
 void Actor::pack_head() {
-  if (!wpack_.p) return;  // (pql_sac: split-K head, no packed weights)
-  mlp::head_pack(pol_.p + pnet_.w_off[nh_], A_, H_, A_, reinterpret_cast<float4*>(wpack_.p),
+  if (!wpack_.p) return;
+  const int hout = sac_ ? 2 * A_ : A_;  // GaussianPolicy: [mean | log_std]
+  mlp::head_pack(pol_.p + pnet_.w_off[nh_], hout, H_, hout, reinterpret_cast<float4*>(wpack_.p),
                  cfg_.precision == PQLG_PREC_3XTF32, stream_);
 }
 

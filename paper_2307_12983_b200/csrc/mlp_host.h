@@ -310,12 +310,13 @@ inline void head_pack(const float* W, int64_t ldw, int K, int N, float4* out, bo
 
 // Raw head sums into hs.part (one "split", row stride round_up(N, 4)) for a
 // finish kernel that adds the bias itself (the SAC Gaussian finish).
+// `base` may carry wpack / fin (the actor's packed weights and normalizer finish).
 inline Step head_raw_step(HeadSplit& hs, const float* x, int64_t ldx, const float* W, int M,
-                          int N, int K) {
+                          int N, int K, const head::RowsArgs& base = head::RowsArgs{}) {
   hs.splits = 1;
   hs.ld_part = (N + 3) / 4 * 4;
   hs.part.alloc(static_cast<size_t>(M) * hs.ld_part);
-  head::RowsArgs r{};
+  head::RowsArgs r = base;
   r.mode = 0;
   r.out = hs.part.p;
   r.ld_out = hs.ld_part;
