@@ -36,8 +36,9 @@ struct Ctx {
 // relu(acc + b) -> TMA store (store = 1) and/or a ReLU bitmask (bit t of
 // word n/32 = post[m, n] > 0) used by the backward, stored word-major
 // (mask[(n/32) * ld_mask + m]: a warp's 32 rows write one coalesced 128 B
-// line per word); optional head dot
-// sum_n relu(.)*w_head[n] per n-tile -> partial[(group*n_tiles + n_tile)*ld_part + m].
+// line per word); optional head dot sum_n relu(.)*w_head[n] per 64-column
+// block (min(64, bn) columns; independent of how the epilogue warps split
+// the tile) -> partial[group][(n / unit) * ld_part + m].
 struct Hidden {
   static constexpr int kStoreRank = 2;
   static constexpr bool kSplitCols = true;
@@ -45,9 +46,9 @@ struct Hidden {
   const float* w_head[4];  // null: no head dot
   uint32_t* mask[4];       // null: no bitmask
   int ld_mask;             // word-major: stride between words (>= M rows)
-  float* partial[4];       // per group [slot][ld_part], slot = n_tile * halves + half
+  float* partial[4];       // per group [slot][ld_part], slot = n / min(64, bn)
   int64_t ld_part;
-  int n_slots;             // n_tiles * halves (mlp::hidden_slots)
+  int n_slots;             // ceil(N / min(64, bn)) (mlp::hidden_slots)
   int bn;
   int M, N;
   int store;  // bit g: store group g's activation (0 for the target critics' last layer)
@@ -82,17 +83,18 @@ struct Hidden {
     if (w_head[c.group]) {
 #pragma unroll
       for (int t = 0; t < 32; ++t) r.dot = __fadd_rn(r.dot, __fmul_rn(v[t], scratch[bn + c0 + t]));
+      // a 64-column block (or the tile / matrix edge) is complete: one slot
+      const int unit = bn < 64 ? bn : 64;
+      if ((c0 + 32) % unit == 0 || n0 + 32 >= N) {
+        if (c.m < M) partial[c.group][static_cast<int64_t>(n0 / unit) * ld_part + c.m] = r.dot;
+        r.dot = 0.0f;
+      }
     }
     if (mask[c.group] && c.m < M)
       mask[c.group][static_cast<int64_t>(n0 >> 5) * ld_mask + c.m] = bits;
     return ((store >> c.group) & 1) != 0;
   }
-  __device__ void end(Row& r, const Ctx& c) const {
-    if (c.m < M && w_head[c.group]) {
-      const int slot = c.n_tile * c.halves + c.half;
-      partial[c.group][static_cast<int64_t>(slot) * ld_part + c.m] = r.dot;
-    }
-  }
+  __device__ void end(Row&, const Ctx&) const {}
 };
 
 // Deterministic policy head (policy.hpp:33-38): y = acc + b (identity layer),

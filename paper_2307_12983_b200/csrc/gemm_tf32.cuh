@@ -93,8 +93,9 @@ struct Problem {
 };
 
 // Epilogue warp count: two warps per TMEM lane quadrant (column halves) for
-// tiles >= 128 columns whose epilogue supports it.
-template <int BN, class Epi>
+// tiles >= 128 columns whose epilogue supports it (four per quadrant was
+// measured slower: DESIGN 9c).
+template <int BN, class Epi, bool kPair = false, bool k3x = false>
 constexpr int epi_warps() {
   return (BN >= 128 && Epi::kSplitCols) ? 8 : 4;
 }
@@ -108,7 +109,7 @@ constexpr int kConvWarps = 4;  // 3xTF32 hi/lo converter warps
 // bound at 1 CTA per tile.
 template <int BN, class Epi, bool kPair = false, bool k3x = false>
 struct SmemLayout {
-  static constexpr int kEpiWarps = epi_warps<BN, Epi>();
+  static constexpr int kEpiWarps = epi_warps<BN, Epi, kPair, k3x>();
   static constexpr int kConvWarps3 = k3x ? kConvWarps : 0;
   static constexpr int kThreads = 64 + 32 * kEpiWarps + 32 * kConvWarps3;
   static constexpr int kABytes = kBM * kBK * 4;  // 16 KB

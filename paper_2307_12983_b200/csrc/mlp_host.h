@@ -26,9 +26,12 @@ using Step = std::function<void(cudaStream_t)>;
 
 inline int bn_for(int N) { return N > 128 ? 256 : N > 64 ? 128 : N > 32 ? 64 : 32; }
 inline int n_tiles(int N) { return (N + bn_for(N) - 1) / bn_for(N); }
-// Head-dot partial slots of a Hidden epilogue over N columns: one per n-tile
-// and epilogue column half (gemm::epi_warps).
-inline int hidden_slots(int N) { return n_tiles(N) * (bn_for(N) >= 128 ? 2 : 1); }
+// Head-dot partial slots of a Hidden epilogue over N columns: one per
+// min(64, bn)-column block (epi::Hidden).
+inline int hidden_slots(int N) {
+  const int unit = bn_for(N) < 64 ? bn_for(N) : 64;
+  return (N + unit - 1) / unit;
+}
 constexpr int kSMs = 148;
 
 template <class F>
