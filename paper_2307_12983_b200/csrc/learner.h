@@ -136,7 +136,10 @@ class VLearner {
   int head_splits_ = 0, c51_blocks_ = 0;
 
   std::vector<mlp::Step> steps_;
-  cudaGraphExec_t graph_exec_ = nullptr;
+  // update graphs: one update, and two back to back (update_n replays the
+  // pair, so the second update's sample overlaps the first one's Adam)
+  cudaGraphExec_t graph_exec_ = nullptr, graph2_exec_ = nullptr;
+  bool capture_ = false;  // steps are being captured into an update graph
   bool graph_checked_ = false;
   int kpu_ = 0;
 };
@@ -242,7 +245,8 @@ class PLearner {
   std::array<WeightMirror, 2> heads_;
 
   std::vector<mlp::Step> steps_;
-  cudaGraphExec_t graph_exec_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr, graph2_exec_ = nullptr;  // (as VLearner)
+  bool capture_ = false;
   int kpu_ = 0;
 };
 

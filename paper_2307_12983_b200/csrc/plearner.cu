@@ -120,6 +120,7 @@ PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
 
 PLearner::~PLearner() {
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (graph2_exec_) cudaGraphExecDestroy(graph2_exec_);
   if (owned_stream_) {
     cudaStreamSynchronize(owned_stream_);
     cudaStreamDestroy(owned_stream_);
@@ -186,7 +187,7 @@ void PLearner::build_update() {
   // ------------------------------------------------- sample + normalize
   steps_.push_back([this, B](cudaStream_t st) {
     const uint64_t* idx = mt_mode_ ? idx_.p : nullptr;
-    launch_state_sample(*states_, norm_.view(), X_.p, Kp_, sampler_.p, idx, B, st);
+    launch_state_sample(*states_, norm_.view(), X_.p, Kp_, sampler_.p, idx, B, st, capture_);
   });
   if (sac_) {  // eps of the reparameterised actions (learners.cpp:247-249)
     steps_.push_back([this](cudaStream_t st) {
@@ -716,15 +717,20 @@ void PLearner::update_n(int n) {
     throw Error(PQLG_NOT_READY, "policy update before state warm-up");
   if (!graph_exec_) {
     kernels_per_update();
-    cudaGraph_t g;
-    PQLG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-    enqueue();
-    PQLG_CUDA(cudaStreamEndCapture(stream_, &g));
-    g_launches.fetch_sub(kpu_);
-    PQLG_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
-    cudaGraphDestroy(g);
+    capture_ = true;
+    for (int reps = 1; reps <= 2; ++reps) {
+      cudaGraph_t g;
+      PQLG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+      for (int r = 0; r < reps; ++r) enqueue();
+      PQLG_CUDA(cudaStreamEndCapture(stream_, &g));
+      g_launches.fetch_sub(static_cast<uint64_t>(reps) * kpu_);
+      PQLG_CUDA(cudaGraphInstantiate(reps == 1 ? &graph_exec_ : &graph2_exec_, g, 0));
+      cudaGraphDestroy(g);
+    }
+    capture_ = false;
   }
-  for (int i = 0; i < n; ++i) PQLG_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+  for (int i = 0; i + 1 < n; i += 2) PQLG_CUDA(cudaGraphLaunch(graph2_exec_, stream_));
+  if (n % 2) PQLG_CUDA(cudaGraphLaunch(graph_exec_, stream_));
   count_launch(static_cast<uint64_t>(n) * kpu_);
 }
 

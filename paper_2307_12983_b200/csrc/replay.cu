@@ -31,16 +31,16 @@ void DeviceStates::insert(const float* rows, int64_t ld_rows, uint64_t n, cudaSt
 
 void launch_replay_sample(const DeviceReplay& r, const replay::Norm& norm, const replay::Gather& g,
                           replay::SamplerState* ss, const uint64_t* idx_dev, uint64_t B,
-                          cudaStream_t st) {
+                          cudaStream_t st, bool early) {
   const uint64_t blocks = (B + replay::kSampleRows - 1) / replay::kSampleRows;
-  launch(replay::replay_sample_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kWarpsPerBlock), 0, st, r.view(), norm, g, ss, idx_dev, B);
+  launch(replay::replay_sample_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kWarpsPerBlock), 0, st, r.view(), norm, g, ss, idx_dev, B, early ? 1 : 0);
 }
 
 void launch_state_sample(const DeviceStates& r, const replay::Norm& norm, float* out,
                          int64_t ld_out, replay::SamplerState* ss, const uint64_t* idx_dev,
-                         uint64_t B, cudaStream_t st) {
+                         uint64_t B, cudaStream_t st, bool early) {
   const uint64_t blocks = (B + replay::kSampleRows - 1) / replay::kSampleRows;
-  launch(replay::state_sample_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kWarpsPerBlock), 0, st, r.view(), norm, out, ld_out, ss, idx_dev, B);
+  launch(replay::state_sample_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kWarpsPerBlock), 0, st, r.view(), norm, out, ld_out, ss, idx_dev, B, early ? 1 : 0);
 }
 
 namespace {

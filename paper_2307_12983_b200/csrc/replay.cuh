@@ -541,9 +541,15 @@ static __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 static __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     replay_sample_kernel(const __grid_constant__ Ring ring, const __grid_constant__ Norm norm,
                          const __grid_constant__ Gather g, SamplerState* ss,
-                         const uint64_t* host_idx, uint64_t B) {
+                         const uint64_t* host_idx, uint64_t B, int early) {
   __shared__ uint64_t s_idx[kSampleRows];
-  pdl::entry();
+  // early (inside the learner's update graph, where the preceding kernel is
+  // the previous update's Adam, which touches none of the sampler state, the
+  // ring or the gather buffers): let the next kernel launch and start the
+  // gather at once, overlapping that kernel; wait for it only before exiting,
+  // so this grid's completion still implies its predecessor's
+  if (early) pdl::trigger();
+  else pdl::entry();
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const uint64_t count = ring.state[1];
@@ -619,6 +625,7 @@ static __global__ void __launch_bounds__(32 * kWarpsPerBlock)
   }
   finish_sample(ss, host_idx, count, B,
                 [&](uint64_t i, uint64_t rr, int ln) { gather_row(ring, norm, g, i, rr, ln); });
+  if (early) pdl::wait();
 }
 
 __device__ __forceinline__ void gather_state(const StateRing& ring, const Norm& norm, float* out,
@@ -636,9 +643,10 @@ __device__ __forceinline__ void gather_state(const StateRing& ring, const Norm& 
 // StateBuffer::sample fused with apply_stats (block layout as above).
 static __global__ void __launch_bounds__(32 * kWarpsPerBlock)
     state_sample_kernel(StateRing ring, Norm norm, float* out, int64_t ld_out, SamplerState* ss,
-                        const uint64_t* host_idx, uint64_t B) {
+                        const uint64_t* host_idx, uint64_t B, int early) {
   __shared__ uint64_t s_idx[kSampleRows];
-  pdl::entry();
+  if (early) pdl::trigger();  // as replay_sample_kernel
+  else pdl::entry();
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const uint64_t count = ring.state[1];
@@ -675,6 +683,7 @@ static __global__ void __launch_bounds__(32 * kWarpsPerBlock)
   finish_sample(ss, host_idx, count, B, [&](uint64_t i, uint64_t rr, int ln) {
     gather_state(ring, norm, out, ld_out, i, rr, ln);
   });
+  if (early) pdl::wait();
 }
 
 }  // namespace pqlg::replay

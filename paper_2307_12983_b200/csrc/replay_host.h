@@ -172,10 +172,10 @@ struct DeviceNStep {
 // Sampling into a gather destination; `ss` lives on device.
 void launch_replay_sample(const DeviceReplay& r, const replay::Norm& norm, const replay::Gather& g,
                           replay::SamplerState* ss, const uint64_t* idx_dev, uint64_t B,
-                          cudaStream_t st);
+                          cudaStream_t st, bool early = false);
 void launch_state_sample(const DeviceStates& r, const replay::Norm& norm, float* out,
                          int64_t ld_out, replay::SamplerState* ss, const uint64_t* idx_dev,
-                         uint64_t B, cudaStream_t st);
+                         uint64_t B, cudaStream_t st, bool early = false);
 
 }  // namespace pqlg
 

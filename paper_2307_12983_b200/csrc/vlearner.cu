@@ -129,6 +129,7 @@ VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
 
 VLearner::~VLearner() {
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (graph2_exec_) cudaGraphExecDestroy(graph2_exec_);
   if (owned_stream_) {
     cudaStreamSynchronize(owned_stream_);
     cudaStreamDestroy(owned_stream_);
@@ -196,7 +197,7 @@ void VLearner::build_update() {
   steps_.push_back([this, B](cudaStream_t st) {
     const uint64_t* idx = mt_mode_ ? idx_.p : nullptr;
     replay::Gather g{Xon_.p, Kp_, Xon_.p + D_, Kp_, Xtg_.p, Kp_, ret_.p, eff_.p};
-    launch_replay_sample(*replay_, norm_.view(), g, sampler_.p, idx, B, st);
+    launch_replay_sample(*replay_, norm_.view(), g, sampler_.p, idx, B, st, capture_);
   });
   if (sac_) {  // eps for the reparameterised next actions (learners.cpp:171-173)
     logp_.alloc(B);
@@ -713,17 +714,22 @@ void VLearner::update_n(int n) {
     graph_checked_ = true;
   }
   if (!graph_exec_) {
-    cudaGraph_t g;
-    const uint64_t before = g_launches.load();
-    PQLG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-    enqueue();
-    PQLG_CUDA(cudaStreamEndCapture(stream_, &g));
-    kpu_ = static_cast<int>(g_launches.load() - before);
-    g_launches.fetch_sub(kpu_);  // captured, not launched
-    PQLG_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
-    cudaGraphDestroy(g);
+    capture_ = true;
+    for (int reps = 1; reps <= 2; ++reps) {
+      cudaGraph_t g;
+      const uint64_t before = g_launches.load();
+      PQLG_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+      for (int r = 0; r < reps; ++r) enqueue();
+      PQLG_CUDA(cudaStreamEndCapture(stream_, &g));
+      kpu_ = static_cast<int>(g_launches.load() - before) / reps;
+      g_launches.fetch_sub(static_cast<uint64_t>(reps) * kpu_);  // captured, not launched
+      PQLG_CUDA(cudaGraphInstantiate(reps == 1 ? &graph_exec_ : &graph2_exec_, g, 0));
+      cudaGraphDestroy(g);
+    }
+    capture_ = false;
   }
-  for (int i = 0; i < n; ++i) PQLG_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+  for (int i = 0; i + 1 < n; i += 2) PQLG_CUDA(cudaGraphLaunch(graph2_exec_, stream_));
+  if (n % 2) PQLG_CUDA(cudaGraphLaunch(graph_exec_, stream_));
   count_launch(static_cast<uint64_t>(n) * kpu_);
 }
 
