@@ -408,7 +408,15 @@ int Actor::kernels_per_step() {
 
 void Actor::rollout_step(pqlg_step_slice* out) {
   const int cur = cur_;
-  enqueue(cur);
+  // one replay of the step's captured graph (the same launches as enqueue;
+  // one host call instead of one per kernel); PQLG_EAGER=1 launches eagerly
+  if (eager_updates()) {
+    enqueue(cur);
+  } else {
+    ensure_graphs();
+    PQLG_CUDA(cudaGraphLaunch(graph_[cur], stream_));
+    count_launch(static_cast<uint64_t>(kps_));
+  }
   stepped_ = true;
   if (!step_done_) PQLG_CUDA(cudaEventCreateWithFlags(&step_done_, cudaEventDisableTiming));
   PQLG_CUDA(cudaEventRecord(step_done_, stream_));  // consumers on other streams wait on it
@@ -433,7 +441,7 @@ std::string Actor::time_steps(int reps) {
       stream_, reps);
 }
 
-void Actor::rollout_n(int n) {
+void Actor::ensure_graphs() {
   for (int c = 0; c < kSets; ++c) {
     if (graph_[c]) continue;
     kernels_per_step();
@@ -445,6 +453,10 @@ void Actor::rollout_n(int n) {
     PQLG_CUDA(cudaGraphInstantiate(&graph_[c], g, 0));
     cudaGraphDestroy(g);
   }
+}
+
+void Actor::rollout_n(int n) {
+  ensure_graphs();
   for (int i = 0; i < n; ++i) {
     PQLG_CUDA(cudaGraphLaunch(graph_[cur_], stream_));
     cur_ = (cur_ + 1) % kSets;

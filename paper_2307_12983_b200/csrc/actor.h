@@ -85,6 +85,7 @@ class Actor {
   DevBuf<float> pol_;
   DevBuf<float> wpack_;  // policy head W in the head kernel's fragment order
   void pack_head();
+  void ensure_graphs();  // the per-buffer-set step graphs (rollout_step / rollout_n)
   bool fused_finish_ = false;  // normalizer finish inside the head launch
   actor::NormState norm_state() const;
   std::vector<DevBuf<float>> pact_;
