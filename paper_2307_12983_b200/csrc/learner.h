@@ -244,6 +244,7 @@ class PLearner {
   DevBuf<float> atoms_, probs_, ev_, up51_;  // C51 actor objective
   std::array<WeightMirror, 2> heads_;
 
+  DevBuf<float> wpack_;  // policy head W in the head kernel's fragment order
   std::vector<mlp::Step> steps_;
   cudaGraphExec_t graph_exec_ = nullptr, graph2_exec_ = nullptr;  // (as VLearner)
   bool capture_ = false;

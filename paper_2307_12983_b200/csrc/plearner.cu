@@ -184,6 +184,17 @@ void PLearner::build_update() {
   }
   loss_counter_.alloc(1);
 
+  // the policy head's W in the head kernel's fragment order, packed from the
+  // previous update's Adam result (a tiny launch the early-starting sample
+  // overlaps)
+  if (!sac_) {
+    wpack_.alloc(static_cast<size_t>(mlp::head_pack_elems(A, H)) * 4);
+    const bool x3 = gemm::build_x3();
+    steps_.push_back([this, A, H, nh, x3](cudaStream_t st) {
+      mlp::head_pack(pol_.p + pnet_.w_off[nh], A, H, A, reinterpret_cast<float4*>(wpack_.p), x3,
+                     st);
+    });
+  }
   // ------------------------------------------------- sample + normalize
   steps_.push_back([this, B](cudaStream_t st) {
     const uint64_t* idx = mt_mode_ ? idx_.p : nullptr;
@@ -245,6 +256,7 @@ void PLearner::build_update() {
       ph.ld_tanh = Ap_;
       ph.mid = (dims_.low + dims_.high) / 2.0f;
       ph.half = (dims_.high - dims_.low) / 2.0f;
+      ph.wpack = reinterpret_cast<const float4*>(wpack_.p);
       steps_.push_back(mlp::head_squash_step(ph, in, ld, Wh, B, A, H));
     }
   }
