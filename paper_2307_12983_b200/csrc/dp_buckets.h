@@ -56,6 +56,7 @@ class DpBuckets {
       cudaStream_t s = fork(st);
       launch(optim::finalize_kernel, dim3(dim3(fb, groups)), dim3(optim::kFinalizeThreads), 0, s,
              f);
+      nccl_fence(s);
       PQLG_NCCL(ncclGroupStart());
       for (int k = 0; k < groups; ++k) {
         float* p = g + k * gs + lo;
