@@ -83,8 +83,13 @@ namespace pqlg::head {
 // Rows of the actor additionally draw their exploration normals (8 lanes
 // per row, group_row_normals) while the loads are in flight.
 // ---------------------------------------------------------------------------
-constexpr int kHeadWarps = 8;          // 4 m16 tiles x 2 K halves
-constexpr int kHeadRows = 64;          // rows per block
+constexpr int kHeadWarps = 8;          // kMT m16 tiles x (8 / kMT) K parts
+// Rows per block: 16 kMT.  kMT = 4 (64 rows, K halves) for the actor's
+// 16384 rows; kMT = 2 (32 rows, K quarters: one load round per warp, twice
+// the blocks) for the learners' 8192 (head_mt()).
+template <int kMT>
+constexpr int head_rows() { return 16 * kMT; }
+inline int head_mt(int M) { return M > 8192 ? 4 : 2; }
 constexpr int kHeadMaxNT = 9;          // n8 tiles (N <= 72)
 
 struct RowsArgs {
@@ -198,19 +203,23 @@ __device__ __forceinline__ uint32_t tf32_bits(float x) {
   return r;
 }
 
-// Shared memory: W fragments [KB][kNT][32] float4,
-// the K-half exchange [4 m-tiles][32 lanes][kNT * 4] floats, and the rows'
-// exploration normals [64][kNT * 8].
-template <int kNT, bool k3x>
+// Shared memory: W fragments [KB][kNT][32] float4, the K-part exchange
+// [K parts - 1][kMT m-tiles][32 lanes][kNT * 4] floats, and the rows'
+// exploration normals [rows][kNT * 8].
+template <int kNT, bool k3x, int kMT>
 inline size_t head_smem(int K) {
   const size_t kb = (static_cast<size_t>(K) + 15) / 16;
-  return kb * kNT * 32 * 16 + 4 * 32 * kNT * 4 * 4 + kHeadRows * kNT * 8 * 4;
+  constexpr int kKP = kHeadWarps / kMT;
+  return kb * kNT * 32 * 16 + (kKP - 1) * kMT * 32 * kNT * 4 * 4 + head_rows<kMT>() * kNT * 8 * 4;
 }
 
-template <int kNT, bool k3x>
+template <int kNT, bool k3x, int kMT>
 static __global__ void __launch_bounds__(32 * kHeadWarps)
     head_mma_kernel(const __grid_constant__ RowsArgs a) {
   extern __shared__ float4 smem4[];
+  constexpr int kHeadRows = head_rows<kMT>();
+  constexpr int kKP = kHeadWarps / kMT;      // K parts
+  constexpr int kDrawCalls = kHeadRows / 32;  // 4 rows per warp per draw call
   const int head_blocks = (a.M + kHeadRows - 1) / kHeadRows;
   if (static_cast<int>(blockIdx.x) >= head_blocks) {  // normalizer finish blocks
     pdl::entry();
@@ -221,21 +230,23 @@ static __global__ void __launch_bounds__(32 * kHeadWarps)
   const int KB = (K + 15) >> 4;
   float4* wf = smem4;  // [KB][kNT][32]: tf32-rounded, or raw fp32 for 3xTF32
   float* xch = reinterpret_cast<float*>(wf + static_cast<int64_t>(KB) * kNT * 32);
-  float* sz = xch + 4 * 32 * kNT * 4;                         // [64][kNT * 8]
+  float* sz = xch + (kKP - 1) * kMT * 32 * kNT * 4;  // [rows][kNT * 8]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // A loads first (the previous kernel's output), then -- while they are in
   // flight -- the exploration inputs, the W fragments and the noise draws.
   // (The previous grid holds every SM until it drains, so staging W before
   // the PDL wait would not overlap anything.)
   pdl::entry();
-  const int mt = warp & 3, kh = warp >> 2;
+  const int mt = warp % kMT, kh = warp / kMT;  // m16 tile, K part
   const int g = lane >> 2, t = lane & 3;
   const int row0 = blockIdx.x * kHeadRows + 16 * mt;
   const int ra = row0 + g < a.M ? row0 + g : a.M - 1;   // clamped rows: results discarded
   const int rb = row0 + g + 8 < a.M ? row0 + g + 8 : a.M - 1;
   const float* xa = a.x + static_cast<int64_t>(ra) * a.ldx + 4 * t;
   const float* xb = a.x + static_cast<int64_t>(rb) * a.ldx + 4 * t;
-  const int kb0 = kh * ((KB + 1) >> 1), kb1 = kh ? KB : ((KB + 1) >> 1);
+  const int kp_len = (KB + kKP - 1) / kKP;
+  const int kb0 = kh * kp_len < KB ? kh * kp_len : KB;
+  const int kb1 = kb0 + kp_len < KB ? kb0 + kp_len : KB;
   constexpr int kU = 8;  // k16 blocks with loads in flight
   float4 va[kU], vb[kU];
   auto load = [&](int kb) {
@@ -250,12 +261,12 @@ static __global__ void __launch_bounds__(32 * kHeadWarps)
   load(kb0);
   // exploration inputs: the draw rows' sigma and SplitMix state, the finish
   // rows' sigma
-  float sig_draw[2] = {0.0f, 0.0f}, sig_fin[2] = {0.0f, 0.0f};
-  uint64_t st_draw[2] = {0ull, 0ull};
+  float sig_draw[kDrawCalls] = {}, sig_fin[2] = {0.0f, 0.0f};
+  uint64_t st_draw[kDrawCalls] = {};
   if (a.noise_state) {
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int m = blockIdx.x * kHeadRows + warp * 8 + c * 4 + (lane >> 3);
+    for (int c = 0; c < kDrawCalls; ++c) {
+      const int m = blockIdx.x * kHeadRows + warp * (4 * kDrawCalls) + c * 4 + (lane >> 3);
       if (m < a.M) {
         sig_draw[c] = a.sigma[m];
         st_draw[c] = a.noise_state[m];
@@ -309,8 +320,8 @@ static __global__ void __launch_bounds__(32 * kHeadWarps)
   // warp per call, 2 calls per warp)
   if (a.noise_state) {
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int r = warp * 8 + c * 4 + (lane >> 3);  // block row
+    for (int c = 0; c < kDrawCalls; ++c) {
+      const int r = warp * (4 * kDrawCalls) + c * 4 + (lane >> 3);  // block row
       const int m = blockIdx.x * kHeadRows + r;
       const bool on = m < a.M && sig_draw[c] > 0.0f;
       group_row_normals<8>(a.noise_state + (m < a.M ? m : 0), st_draw[c], on, N, lane & 7,
@@ -366,20 +377,25 @@ static __global__ void __launch_bounds__(32 * kHeadWarps)
       }
     }
   }
-  // K halves: the upper half's partial sums through shared memory, added in
-  // fixed order (lower + upper)
-  if (kh == 1) {
+  // K parts: parts 1.. hand their partial sums over shared memory, part 0
+  // adds them in fixed order
+  if (kh > 0) {
+    float* x = xch + static_cast<int64_t>(((kh - 1) * kMT + mt) * 32 + lane) * kNT * 4;
 #pragma unroll
     for (int nt = 0; nt < kNT; ++nt)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) xch[((mt * 32 + lane) * kNT + nt) * 4 + q] = acc[nt][q];
+      for (int q = 0; q < 4; ++q) x[nt * 4 + q] = acc[nt][q];
   }
   __syncthreads();
-  if (kh == 1) return;
+  if (kh > 0) return;
 #pragma unroll
-  for (int nt = 0; nt < kNT; ++nt)
+  for (int j = 0; j < kKP - 1; ++j) {  // (((p0 + p1) + p2) + ...), fixed order
+    const float* x = xch + static_cast<int64_t>((j * kMT + mt) * 32 + lane) * kNT * 4;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[nt][q] = __fadd_rn(acc[nt][q], xch[((mt * 32 + lane) * kNT + nt) * 4 + q]);
+    for (int nt = 0; nt < kNT; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[nt][q] = __fadd_rn(acc[nt][q], x[nt * 4 + q]);
+  }
   // finish: lane holds rows g / g + 8, columns 8 nt + 2t, + 1
 #pragma unroll
   for (int h = 0; h < 2; ++h) {

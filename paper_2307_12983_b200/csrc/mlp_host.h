@@ -232,10 +232,10 @@ inline Step head_finish_step(const HeadSplit& hs, head::FinishArgs fin, int M, i
 // The narrow head (head::head_mma_kernel): one launch computes x * W and,
 // in squash mode, the finish.  `r` carries the mode and output fields;
 // x/w/M/K/N are set here.
-template <int kNT, bool k3x>
-inline void launch_head(const head::RowsArgs& r, cudaStream_t st) {
-  auto kern = head::head_mma_kernel<kNT, k3x>;
-  const size_t smem = head::head_smem<kNT, k3x>(r.K);
+template <int kNT, bool k3x, int kMT>
+inline void launch_head_mt(const head::RowsArgs& r, cudaStream_t st) {
+  auto kern = head::head_mma_kernel<kNT, k3x, kMT>;
+  const size_t smem = head::head_smem<kNT, k3x, kMT>(r.K);
   static bool configured = false;
   if (!configured) {
     PQLG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -244,8 +244,13 @@ inline void launch_head(const head::RowsArgs& r, cudaStream_t st) {
   const int fin = r.fin.partial ? r.fin.nblk : 0;
   // finish blocks reuse the dynamic shared memory for their [16][32] double2
   const size_t smem_all = fin ? std::max<size_t>(smem, actor::kNormFinishWarps * 32 * 16) : smem;
-  launch(kern, dim3((r.M + head::kHeadRows - 1) / head::kHeadRows + fin),
-         dim3(32 * head::kHeadWarps), smem_all, st, r);
+  constexpr int rows = head::head_rows<kMT>();
+  launch(kern, dim3((r.M + rows - 1) / rows + fin), dim3(32 * head::kHeadWarps), smem_all, st, r);
+}
+template <int kNT, bool k3x>
+inline void launch_head(const head::RowsArgs& r, cudaStream_t st) {
+  if (head::head_mt(r.M) == 4) launch_head_mt<kNT, k3x, 4>(r, st);
+  else launch_head_mt<kNT, k3x, 2>(r, st);
 }
 
 template <int kNT>
@@ -279,7 +284,7 @@ inline Step head_rows_step(head::RowsArgs r, const float* x, int64_t ldx, const 
     case 8: pick_head<8>(x3, fn); break;
     default: pick_head<9>(x3, fn); break;
   }
-  require(head::head_smem<9, false>(K) <= 200 * 1024 || nt < 9,
+  require(head::head_smem<9, false, 4>(K) <= 200 * 1024 || nt < 9,
           "policy head: hidden width too large for the head kernel");
   return [r, fn](cudaStream_t st) { fn(r, st); };
 }
