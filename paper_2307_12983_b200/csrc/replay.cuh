@@ -555,7 +555,95 @@ static __global__ void __launch_bounds__(32 * kWarpsPerBlock)
   const uint64_t count = ring.state[1];
   draw_block_indices(ss, host_idx, count, B, s_idx);
   const uint64_t rb = static_cast<uint64_t>(blockIdx.x) * kSampleRows + w * kRowsPerWarp;
-  if (ring.D <= 256) {
+  const bool vec4 = ring.D <= 256 && (ring.ld_obs & 3) == 0 && (g.ld_obs & 3) == 0 &&
+                    (g.ld_boot & 3) == 0 &&
+                    ((reinterpret_cast<uintptr_t>(ring.obs) | reinterpret_cast<uintptr_t>(ring.boot) |
+                      reinterpret_cast<uintptr_t>(g.obs) | reinterpret_cast<uintptr_t>(g.boot)) & 15) == 0;
+  if (vec4) {
+    // 16-byte rows: lane l gathers quads l and l + 32 of each row (all loads
+    // of the warp's rows in flight before any store); the last, partial quad
+    // is stored element-wise (the critic input's action columns follow the
+    // observation at column D)
+    const bool ident = *norm.identity != 0;
+    const int Q = (ring.D + 3) >> 2;
+    float4 x[kRowsPerWarp][2], y[kRowsPerWarp][2];
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      const uint64_t i = s_idx[w * kRowsPerWarp + k];
+      const float4* so = reinterpret_cast<const float4*>(ring.obs + i * ring.ld_obs);
+      const float4* sb = reinterpret_cast<const float4*>(ring.boot + i * ring.ld_obs);
+      const bool ok = rb + k < B;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int q = lane + 32 * u;
+        x[k][u] = (ok && q < Q) ? __ldg(so + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        y[k][u] = (ok && q < Q) ? __ldg(sb + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    float av[kRowsPerWarp], rv[kRowsPerWarp], ev[kRowsPerWarp];
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      const uint64_t i = s_idx[w * kRowsPerWarp + k];
+      const bool ok = rb + k < B;
+      av[k] = (ok && lane < ring.A) ? __ldg(ring.act + i * ring.ld_act + lane) : 0.0f;
+      rv[k] = (ok && lane == 0) ? __ldg(ring.ret + i) : 0.0f;
+      ev[k] = (ok && lane == 0) ? __ldg(ring.eff + i) : 0.0f;
+    }
+    float mu[2][4], iv[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int d = 4 * (lane + 32 * u) + c;
+        mu[u][c] = (d < ring.D && !ident) ? norm.mean[d] : 0.0f;
+        iv[u][c] = (d < ring.D && !ident) ? norm.inv[d] : 1.0f;
+      }
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+      const uint64_t r = rb + k;
+      if (r >= B) break;
+      float* dobs = g.obs + r * g.ld_obs;
+      float* dboot = g.boot + r * g.ld_boot;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int q = lane + 32 * u;
+        if (q >= Q) continue;
+        float xx[4] = {x[k][u].x, x[k][u].y, x[k][u].z, x[k][u].w};
+        float yy[4] = {y[k][u].x, y[k][u].y, y[k][u].z, y[k][u].w};
+        if (!ident) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            xx[c] = normalize1(xx[c], mu[u][c], iv[u][c]);
+            yy[c] = normalize1(yy[c], mu[u][c], iv[u][c]);
+          }
+        }
+        const int d0 = 4 * q;
+        if (d0 + 4 <= ring.D) {
+          *reinterpret_cast<float4*>(dobs + d0) = make_float4(xx[0], xx[1], xx[2], xx[3]);
+          *reinterpret_cast<float4*>(dboot + d0) = make_float4(yy[0], yy[1], yy[2], yy[3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (d0 + c < ring.D) {
+              dobs[d0 + c] = xx[c];
+              dboot[d0 + c] = yy[c];
+            }
+        }
+      }
+      if (lane < ring.A) g.act[r * g.ld_act + lane] = av[k];
+      if (lane == 0) {
+        g.ret[r] = rv[k];
+        g.eff[r] = ev[k];
+      }
+    }
+    if (ring.A > 32) {  // wide actions: the generic path for the columns >= 32
+      for (int k = 0; k < kRowsPerWarp && rb + k < B; ++k) {
+        const uint64_t i = s_idx[w * kRowsPerWarp + k];
+        for (int d = 32 + lane; d < ring.A; d += 32)
+          g.act[(rb + k) * g.ld_act + d] = ring.act[i * ring.ld_act + d];
+      }
+    }
+  } else if (ring.D <= 256) {
     const bool ident = *norm.identity != 0;
     float x[kRowsPerWarp][8], y[kRowsPerWarp][8];
 #pragma unroll
