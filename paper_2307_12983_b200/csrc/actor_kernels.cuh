@@ -382,19 +382,19 @@ static __global__ void __launch_bounds__(32 * kEnvWarps)
 //   8 step warps     4 envs each (lane = observation quads): clamped actions,
 //                    sum a^2, M a, s' (written back into the stage rows) and
 //                    the done / truncation flags
-//   2 chain warps    alternate tiles, lane = env: the d-ascending s'^2 reward
+//   1 chain warp     lane = env: the d-ascending s'^2 reward
 //                    sum read as float4 from the stage (row stride 212 floats
 //                    puts 8 lanes on 8 distinct bank quads: conflict-free),
 //                    rewards and flags out
-//   4 writer warps   rows w, w+4, ... (lane = quads): next obs (fresh reset
-//                    draws on done rows) and its normalisation into the
-//                    stage's two output blocks, and optionally the fp64
+//   6 writer warps   rows w, w+6, ... (lane = quads): next obs (fresh reset
+//                    draws on done rows) and its normalisation, float4 stores
+//                    straight from registers, and optionally the fp64
 //                    running-normalizer partial sums of the next observations
 //                    (shifted by the running mean), so the next step's
 //                    normalizer update needs no second pass over them; the
-//                    first writer lane then bulk-stores boot (= s', straight
-//                    from the stage rows), next obs and the normalised next
-//                    obs, and releases the stage once the stores have read it
+//                    first writer lane bulk-stores boot (= s') straight from
+//                    the stage rows and releases the stage once that store
+//                    has read it
 // ---------------------------------------------------------------------------
 constexpr int kEnvStages = 4;
 #ifndef PQLG_ENV_STEP_WARPS
@@ -402,9 +402,12 @@ constexpr int kEnvStages = 4;
 #endif
 constexpr int kTStepWarps = PQLG_ENV_STEP_WARPS;   // step warps ...
 constexpr int kTPer = kEnvTile / kTStepWarps;       // ... of kTPer envs each
-constexpr int kEnvChainWarps = 2;
+#ifndef PQLG_ENV_CHAIN
+#define PQLG_ENV_CHAIN 1
+#endif
+constexpr int kEnvChainWarps = PQLG_ENV_CHAIN;
 #ifndef PQLG_ENV_WRITERS
-#define PQLG_ENV_WRITERS 4
+#define PQLG_ENV_WRITERS 6
 #endif
 constexpr int kEnvWriterWarps = PQLG_ENV_WRITERS;
 constexpr int kEnvTmaWarps = kTStepWarps + kEnvChainWarps + kEnvWriterWarps + 1;
