@@ -94,6 +94,7 @@ class VLearner {
 
   DevBuf<float> q_, qt_, m_, v_, grads_, lagged_;
   DevBuf<float> wpack_;  // lagged policy head W in the head kernel's fragment order
+  int wpack_n_ = 0;      // its output columns (act_dim, pql_sac 2 act_dim)
   void lagged_changed();
   mlp::HeadSplit head_split_;  // split-K lagged-policy head
   std::unique_ptr<DeviceReplay> replay_;

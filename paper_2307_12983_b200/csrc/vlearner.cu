@@ -228,8 +228,14 @@ void VLearner::build_update() {
     const int hout = sac_ ? 2 * A : A;
     const float* Wh = lagged_.p + pnet_.w_off[nh];
     if (sac_) {
-      // next = lagged.sample(boot, eps) (sac.hpp:31): actions + log-probs
-      steps_.push_back(mlp::head_raw_step(head_split_, in, ld, Wh, B, hout, H));
+      // next = lagged.sample(boot, eps) (sac.hpp:31): actions + log-probs;
+      // the head's W packed on adopt (lagged_changed)
+      wpack_.alloc(static_cast<size_t>(mlp::head_pack_elems(hout, H)) * 4);
+      wpack_n_ = hout;
+      lagged_changed();
+      head::RowsArgs base{};
+      base.wpack = reinterpret_cast<const float4*>(wpack_.p);
+      steps_.push_back(mlp::head_raw_step(head_split_, in, ld, Wh, B, hout, H, base));
       sac::GaussArgs g{};
       g.bias = lagged_.p + pnet_.b_off[nh];
       g.eps = eps_.out.p;
@@ -250,6 +256,7 @@ void VLearner::build_update() {
       // W in the head kernel's fragment order, re-packed when the lagged
       // policy changes (lagged_changed)
       wpack_.alloc(static_cast<size_t>(mlp::head_pack_elems(A, H)) * 4);
+      wpack_n_ = A;
       ph.wpack = reinterpret_cast<const float4*>(wpack_.p);
       lagged_changed();
       steps_.push_back(mlp::head_squash_step(ph, in, ld, Wh, B, A, H));
@@ -570,9 +577,9 @@ void VLearner::build_update() {
 
 void VLearner::lagged_changed() {
   if (!wpack_.p) return;
-  mlp::head_pack(lagged_.p + pnet_.w_off[pnet_.layers() - 1], dims_.act_dim, cfg_.hidden,
-                 dims_.act_dim, reinterpret_cast<float4*>(wpack_.p),
-                 cfg_.precision == PQLG_PREC_3XTF32, stream_);
+  mlp::head_pack(lagged_.p + pnet_.w_off[pnet_.layers() - 1], wpack_n_, cfg_.hidden, wpack_n_,
+                 reinterpret_cast<float4*>(wpack_.p), cfg_.precision == PQLG_PREC_3XTF32,
+                 stream_);
 }
 
 void VLearner::adopt_policy(const float* flat, int64_t version) {
@@ -589,6 +596,7 @@ void VLearner::adopt_policy_sac(const float* flat, float log_alpha, int64_t vers
   PQLG_CUDA(cudaMemcpyAsync(lagged_.p, flat, pnet_.params * 4, cudaMemcpyHostToDevice, stream_));
   PQLG_CUDA(cudaMemcpyAsync(lagged_.p + pnet_.params, &log_alpha, 4, cudaMemcpyHostToDevice,
                             stream_));
+  lagged_changed();
   PQLG_CUDA(cudaStreamSynchronize(stream_));
   lagged_version_ = version;
 }
