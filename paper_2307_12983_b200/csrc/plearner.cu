@@ -187,11 +187,12 @@ void PLearner::build_update() {
   // the policy head's W in the head kernel's fragment order, packed from the
   // previous update's Adam result (a tiny launch the early-starting sample
   // overlaps)
-  if (!sac_) {
-    wpack_.alloc(static_cast<size_t>(mlp::head_pack_elems(A, H)) * 4);
+  {
+    const int Ah = Ah_;  // A, or 2A ([mean | log_std]) for pql_sac
+    wpack_.alloc(static_cast<size_t>(mlp::head_pack_elems(Ah, H)) * 4);
     const bool x3 = gemm::build_x3();
-    steps_.push_back([this, A, H, nh, x3](cudaStream_t st) {
-      mlp::head_pack(pol_.p + pnet_.w_off[nh], A, H, A, reinterpret_cast<float4*>(wpack_.p), x3,
+    steps_.push_back([this, Ah, H, nh, x3](cudaStream_t st) {
+      mlp::head_pack(pol_.p + pnet_.w_off[nh], Ah, H, Ah, reinterpret_cast<float4*>(wpack_.p), x3,
                      st);
     });
   }
@@ -233,7 +234,9 @@ void PLearner::build_update() {
     if (sac_) {
       // s = policy.sample(states, eps) (sac.hpp:77): actions, log-probs, and
       // tanh(pre) / std kept for the backward
-      steps_.push_back(mlp::head_raw_step(head_split_, in, ld, Wh, B, Ah_, H));
+      head::RowsArgs base{};
+      base.wpack = reinterpret_cast<const float4*>(wpack_.p);
+      steps_.push_back(mlp::head_raw_step(head_split_, in, ld, Wh, B, Ah_, H, base));
       sac::GaussArgs g{};
       g.bias = pol_.p + pnet_.b_off[nh];
       g.eps = eps_.out.p;
