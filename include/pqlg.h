@@ -574,6 +574,15 @@ PQLG_API int pqlg_k_normalizer_update(int64_t* count_dev, double* mean_dev, doub
                                       const float* batch_dev, int64_t ld, int rows, int dim,
                                       float* mean_f_dev, float* inv_f_dev, void* stream);
 
+/* One evaluation context (the metrics loops' reusable Evaluator) run over
+ * n_policies policy vectors in turn, all with `norm`: returns
+ * [n_policies x episodes] and the per-policy mean / stderr, each equal to a
+ * fresh pqlg_evaluate of that policy (test hook).  Synchronizes. */
+PQLG_API int pqlg_k_evaluate_seq(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                                 const float* policies_host, int n_policies,
+                                 const pqlg_norm_stats* norm, int episodes, uint64_t eval_seed,
+                                 double* returns_host, double* mean, double* stderr_out);
+
 /* ------------------------------------------------------------ checkpoints
  * The reference's on-disk format, byte for byte (fa::save_checkpoint /
  * load_checkpoint, src/funcapprox/checkpoint.cpp:35-91): "PQLCKPT\x01",

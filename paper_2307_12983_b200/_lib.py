@@ -226,6 +226,8 @@ SIGNATURES: dict[str, tuple] = {
     "pqlg_env_reset_all": (i32, [vp, vp, i64]),
     "pqlg_env_step": (i32, [vp, vp, i64, vp, vp, vp, vp, vp, i64]),
     "pqlg_k_apply_noise": (i32, [vp, i64, i32, i32, vp, f32, f32, vp, vp]),
+    "pqlg_k_evaluate_seq": (i32, [P(Config), P(TaskDims), vp, i32, P(NormStats), i32, u64, vp,
+                                  vp, vp]),
     "pqlg_k_normalizer_update": (i32, [vp, vp, vp, vp, i64, i32, i32, vp, vp, vp]),
 }
 

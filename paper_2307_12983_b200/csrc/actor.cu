@@ -558,22 +558,45 @@ __global__ void eval_accumulate_kernel(const float* rew, const uint8_t* term,
 }
 }  // namespace
 
-void evaluate_policy(const pqlg_config& cfg, const pqlg_task_dims& dims, const float* policy,
-                     int64_t count, const double* mean, const double* m2, int episodes,
-                     uint64_t eval_seed, double* returns, double* mean_out, double* stderr_out) {
+struct Evaluator::Impl {
+  pqlg_config cfg;
+  int N, D, A;
+  int64_t Dp, Ap;
+  cudaStream_t st = nullptr;
+  NetShape pnet;
+  DevBuf<float> pol;
+  std::unique_ptr<DeviceEnv> env;
+  DevBuf<uint64_t> rng0;  // the env's per-row streams as make_env seeds them
+  DevBuf<float> obs[2], boot, rew, act, Xn;
+  DevBuf<uint8_t> flags;  // term | trunc | finished
+  DevBuf<double> ret;
+  DevBuf<unsigned int> n_fin;
+  DevBuf<uint32_t> status;
+  DeviceNorm norm;
+  std::vector<DevBuf<float>> pact;
+  std::vector<mlp::Step> steps;
+  std::vector<double> r;
+  ~Impl() {
+    if (st) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+  }
+};
+
+Evaluator::Evaluator(const pqlg_config& cfg, const pqlg_task_dims& dims, int episodes,
+                     uint64_t eval_seed)
+    : p_(std::make_unique<Impl>()) {
   require(episodes >= 1, "evaluate: episodes must be >= 1");  // learners.cpp:282
-  const int N = episodes, D = dims.obs_dim, A = dims.act_dim, H = cfg.hidden;
-  const int nh = cfg.hidden_layers;
+  Impl& e = *p_;
+  e.cfg = cfg;
+  const int N = e.N = episodes, D = e.D = dims.obs_dim, A = e.A = dims.act_dim;
+  const int H = cfg.hidden, nh = cfg.hidden_layers;
   require(A <= 32, "evaluate: act_dim > 32 not supported");
   require(cfg.precision == PQLG_PREC_TF32 || cfg.precision == PQLG_PREC_3XTF32,
           "evaluate: unknown precision");
   gemm::PrecisionScope prec(cfg.precision == PQLG_PREC_3XTF32);
-  cudaStream_t st;
-  PQLG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  struct StreamGuard {
-    cudaStream_t s;
-    ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
-  } guard{st};
+  PQLG_CUDA(cudaStreamCreateWithFlags(&e.st, cudaStreamNonBlocking));
   // pql_sac evaluates the squashed mean (GaussianPolicy::mean_act,
   // policy.hpp:110-118): the first A of the 2A head outputs
   const bool sac = cfg.algo == PQLG_ALGO_SAC;
@@ -581,77 +604,97 @@ void evaluate_policy(const pqlg_config& cfg, const pqlg_task_dims& dims, const f
   std::vector<int> ps{D};
   for (int l = 0; l < nh; ++l) ps.push_back(H);
   ps.push_back(hout);
-  const NetShape pnet = NetShape::make(ps);
-  DevBuf<float> pol(pnet.params);
-  PQLG_CUDA(cudaMemcpy(pol.p, policy, pnet.params * 4, cudaMemcpyHostToDevice));
-  DeviceEnv env(N, D, A, eval_seed, cfg.max_episode_len, 0, dims.low, dims.high);
-  const int64_t Dp = round_up(D, 4), Ap = round_up(A, 4);
-  DevBuf<float> obs[2], boot, rew, act, Xn;
-  for (auto& o : obs) o.alloc(static_cast<size_t>(N) * Dp);
-  boot.alloc(static_cast<size_t>(N) * Dp);
-  rew.alloc(N);
-  act.alloc(static_cast<size_t>(N) * Ap);
-  Xn.alloc(static_cast<size_t>(N) * Dp);
-  DevBuf<uint8_t> flags(3ull * N);  // term | trunc | finished
-  DevBuf<double> ret(N);
-  DevBuf<unsigned int> n_fin(1);
-  DevBuf<uint32_t> status(1);
-  DeviceNorm norm;
-  norm.init(D);
-  norm.set(count, mean, m2, st);
-  env.reset(obs[0].p, Dp, st);
-  PQLG_CUDA(cudaMemsetAsync(env.ep.p, 0, N * 8, st));  // make_env: fresh episodes
-  launch(actor::normalize_kernel, dim3(4 * mlp::kSMs), dim3(256), 0, st, obs[0].p, Dp, Xn.p, Dp,
-         norm.mean.p, norm.inv.p, norm.ident.p, N, D);
+  e.pnet = NetShape::make(ps);
+  e.pol.alloc(e.pnet.params);
+  e.env = std::make_unique<DeviceEnv>(N, D, A, eval_seed, cfg.max_episode_len, 0, dims.low,
+                                      dims.high);
+  e.rng0.alloc(N);
+  PQLG_CUDA(cudaMemcpy(e.rng0.p, e.env->rng.p, N * 8, cudaMemcpyDeviceToDevice));
+  e.Dp = round_up(D, 4);
+  e.Ap = round_up(A, 4);
+  for (auto& o : e.obs) o.alloc(static_cast<size_t>(N) * e.Dp);
+  e.boot.alloc(static_cast<size_t>(N) * e.Dp);
+  e.rew.alloc(N);
+  e.act.alloc(static_cast<size_t>(N) * e.Ap);
+  e.Xn.alloc(static_cast<size_t>(N) * e.Dp);
+  e.flags.alloc(3ull * N);
+  e.ret.alloc(N);
+  e.n_fin.alloc(1);
+  e.status.alloc(1);
+  e.norm.init(D);
+  e.r.resize(N);
   // policy forward (hidden layers, squashing head without noise)
-  std::vector<DevBuf<float>> pact(nh);
-  std::vector<mlp::Step> steps;
-  const float* in = Xn.p;
-  int64_t ld = Dp;
+  e.pact.resize(nh);
+  const float* in = e.Xn.p;
+  int64_t ld = e.Dp;
   int K = D;
   for (int l = 0; l < nh; ++l) {
-    pact[l].alloc(static_cast<size_t>(N) * H);
-    epi::Hidden e{};
-    e.bias[0] = pol.p + pnet.b_off[l];
-    e.bn = mlp::bn_for(H);
-    e.M = N;
-    e.N = H;
-    e.store = 1;
-    const float* W = pol.p + pnet.w_off[l];
-    steps.push_back(mlp::fwd(in, in, ld, W, W, N, H, K, 1, e, 0, pact[l].p, pact[l].p, H));
-    in = pact[l].p;
+    e.pact[l].alloc(static_cast<size_t>(N) * H);
+    epi::Hidden h{};
+    h.bias[0] = e.pol.p + e.pnet.b_off[l];
+    h.bn = mlp::bn_for(H);
+    h.M = N;
+    h.N = H;
+    h.store = 1;
+    const float* W = e.pol.p + e.pnet.w_off[l];
+    e.steps.push_back(mlp::fwd(in, in, ld, W, W, N, H, K, 1, h, 0, e.pact[l].p, e.pact[l].p, H));
+    in = e.pact[l].p;
     ld = H;
     K = H;
   }
   head::RowsArgs ph{};
-  ph.bias = pol.p + pnet.b_off[nh];
-  ph.out = act.p;
-  ph.ld_out = Ap;
+  ph.bias = e.pol.p + e.pnet.b_off[nh];
+  ph.out = e.act.p;
+  ph.ld_out = e.Ap;
   ph.ldw = hout;  // pql_sac: the mean columns of [mean | log_std]
   ph.mid = (dims.low + dims.high) / 2.0f;
   ph.half = (dims.high - dims.low) / 2.0f;
-  steps.push_back(mlp::head_squash_step(ph, in, ld, pol.p + pnet.w_off[nh], N, A, H));
+  e.steps.push_back(mlp::head_squash_step(ph, in, ld, e.pol.p + e.pnet.w_off[nh], N, A, H));
+}
+
+Evaluator::~Evaluator() = default;
+
+// Every call starts from make_env's state (the row streams restored from
+// rng0, fresh episodes), so repeated calls equal fresh evaluate_policy calls.
+void Evaluator::run(const float* policy, int64_t count, const double* mean, const double* m2,
+                    double* returns, double* mean_out, double* stderr_out) {
+  Impl& e = *p_;
+  const int N = e.N, D = e.D;
+  cudaStream_t st = e.st;
+  DeviceEnv& env = *e.env;
+  PQLG_CUDA(cudaMemcpyAsync(e.pol.p, policy, e.pnet.params * 4, cudaMemcpyHostToDevice, st));
+  PQLG_CUDA(cudaMemcpyAsync(env.rng.p, e.rng0.p, N * 8, cudaMemcpyDeviceToDevice, st));
+  PQLG_CUDA(cudaMemsetAsync(e.flags.p, 0, 3ull * N, st));
+  PQLG_CUDA(cudaMemsetAsync(e.ret.p, 0, N * 8, st));
+  PQLG_CUDA(cudaMemsetAsync(e.n_fin.p, 0, 4, st));
+  PQLG_CUDA(cudaMemsetAsync(e.status.p, 0, 4, st));
+  e.norm.set(count, mean, m2, st);
+  env.reset(e.obs[0].p, e.Dp, st);
+  PQLG_CUDA(cudaMemsetAsync(env.ep.p, 0, N * 8, st));  // make_env: fresh episodes
+  launch(actor::normalize_kernel, dim3(4 * mlp::kSMs), dim3(256), 0, st, e.obs[0].p, e.Dp, e.Xn.p,
+         e.Dp, e.norm.mean.p, e.norm.inv.p, e.norm.ident.p, N, D);
   const int blocks = std::min((N + 255) / 256, 4 * mlp::kSMs);
   int cur = 0;
-  for (int step = 0; step < cfg.max_episode_len; ++step) {
-    for (auto& s : steps) s(st);
-    actor::StepOut o{obs[1 - cur].p, boot.p, rew.p, flags.p, flags.p + N, nullptr, Dp, status.p};
-    actor::NextNorm nn{Xn.p, Dp, norm.mean.p, norm.inv.p, norm.ident.p};
-    env.step(act.p, Ap, o, st, nn, obs[cur].p, Dp);
-    launch(eval_accumulate_kernel, dim3(blocks), dim3(256), 0, st, rew.p, flags.p, flags.p + N, N,
-           ret.p, flags.p + 2 * N, n_fin.p);
+  for (int step = 0; step < e.cfg.max_episode_len; ++step) {
+    for (auto& s : e.steps) s(st);
+    actor::StepOut o{e.obs[1 - cur].p, e.boot.p, e.rew.p, e.flags.p, e.flags.p + N, nullptr, e.Dp,
+                     e.status.p};
+    actor::NextNorm nn{e.Xn.p, e.Dp, e.norm.mean.p, e.norm.inv.p, e.norm.ident.p};
+    env.step(e.act.p, e.Ap, o, st, nn, e.obs[cur].p, e.Dp);
+    launch(eval_accumulate_kernel, dim3(blocks), dim3(256), 0, st, e.rew.p, e.flags.p,
+           e.flags.p + N, N, e.ret.p, e.flags.p + 2 * N, e.n_fin.p);
     cur = 1 - cur;
-    if ((step & 15) == 15 || step + 1 == cfg.max_episode_len) {  // every row finished?
+    if ((step & 15) == 15 || step + 1 == e.cfg.max_episode_len) {  // every row finished?
       unsigned int fin = 0;
-      PQLG_CUDA(cudaMemcpyAsync(&fin, n_fin.p, 4, cudaMemcpyDeviceToHost, st));
+      PQLG_CUDA(cudaMemcpyAsync(&fin, e.n_fin.p, 4, cudaMemcpyDeviceToHost, st));
       PQLG_CUDA(cudaStreamSynchronize(st));
       if (fin == static_cast<unsigned int>(N)) break;
     }
   }
-  std::vector<double> r(N);
-  PQLG_CUDA(cudaMemcpyAsync(r.data(), ret.p, N * 8, cudaMemcpyDeviceToHost, st));
+  std::vector<double>& r = e.r;
+  PQLG_CUDA(cudaMemcpyAsync(r.data(), e.ret.p, N * 8, cudaMemcpyDeviceToHost, st));
   uint32_t stv = 0;
-  PQLG_CUDA(cudaMemcpyAsync(&stv, status.p, 4, cudaMemcpyDeviceToHost, st));
+  PQLG_CUDA(cudaMemcpyAsync(&stv, e.status.p, 4, cudaMemcpyDeviceToHost, st));
   PQLG_CUDA(cudaStreamSynchronize(st));
   if (stv) throw Error(PQLG_ENONFINITE, "evaluate: non-finite action");
   double mu = 0.0;
@@ -663,6 +706,13 @@ void evaluate_policy(const pqlg_config& cfg, const pqlg_task_dims& dims, const f
   if (returns) std::copy(r.begin(), r.end(), returns);
   *mean_out = mu;
   *stderr_out = std::sqrt(var / static_cast<double>(N));
+}
+
+void evaluate_policy(const pqlg_config& cfg, const pqlg_task_dims& dims, const float* policy,
+                     int64_t count, const double* mean, const double* m2, int episodes,
+                     uint64_t eval_seed, double* returns, double* mean_out, double* stderr_out) {
+  Evaluator(cfg, dims, episodes, eval_seed)
+      .run(policy, count, mean, m2, returns, mean_out, stderr_out);
 }
 
 }  // namespace pqlg
@@ -733,6 +783,25 @@ int pqlg_evaluate(const pqlg_config* cfg, const pqlg_task_dims* dims, const floa
     require(cfg && dims && policy_host && norm && mean && stderr_out, "evaluate: null argument");
     evaluate_policy(*cfg, *dims, policy_host, norm->count, norm->mean, norm->m2, episodes,
                     eval_seed, returns_host, mean, stderr_out);
+  });
+}
+
+int pqlg_k_evaluate_seq(const pqlg_config* cfg, const pqlg_task_dims* dims,
+                        const float* policies_host, int n_policies, const pqlg_norm_stats* norm,
+                        int episodes, uint64_t eval_seed, double* returns_host, double* mean,
+                        double* stderr_out) {
+  return guarded([&] {
+    require(cfg && dims && policies_host && norm && returns_host && mean && stderr_out,
+            "evaluate_seq: null argument");
+    require(n_policies >= 1, "evaluate_seq: n_policies must be >= 1");
+    std::vector<int> ps{dims->obs_dim};
+    for (int l = 0; l < cfg->hidden_layers; ++l) ps.push_back(cfg->hidden);
+    ps.push_back(cfg->algo == PQLG_ALGO_SAC ? 2 * dims->act_dim : dims->act_dim);
+    const int64_t P = NetShape::make(ps).params;
+    Evaluator ev(*cfg, *dims, episodes, eval_seed);
+    for (int k = 0; k < n_policies; ++k)
+      ev.run(policies_host + k * P, norm->count, norm->mean, norm->m2,
+             returns_host + static_cast<int64_t>(k) * episodes, mean + k, stderr_out + k);
   });
 }
 

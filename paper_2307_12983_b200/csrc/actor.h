@@ -106,6 +106,24 @@ class Actor {
 };
 
 // evaluate_policy (learners.cpp:280-325) on the synthetic task (actor.cu).
+// Evaluator owns the device context (env, policy, buffers, stream) for one
+// (config, episodes, eval_seed), allocated once: the metrics loops keep one
+// so an evaluation neither allocates nor frees device memory (cudaFree
+// synchronises the device, stalling the pipeline's streams).
+class Evaluator {
+ public:
+  Evaluator(const pqlg_config& cfg, const pqlg_task_dims& dims, int episodes, uint64_t eval_seed);
+  ~Evaluator();
+  Evaluator(const Evaluator&) = delete;
+  Evaluator& operator=(const Evaluator&) = delete;
+  void run(const float* policy, int64_t count, const double* mean, const double* m2,
+           double* returns, double* mean_out, double* stderr_out);
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> p_;
+};
+// One-shot: a fresh Evaluator.
 void evaluate_policy(const pqlg_config& cfg, const pqlg_task_dims& dims, const float* policy,
                      int64_t count, const double* mean, const double* m2, int episodes,
                      uint64_t eval_seed, double* returns, double* mean_out, double* stderr_out);

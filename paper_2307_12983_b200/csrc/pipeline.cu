@@ -248,6 +248,7 @@ class Pipeline {
     require(!ran_, "pipeline: set_metrics before run()");
     if (!m.path) {
       writer_.reset();
+      evaluator_.reset();
       return;
     }
     require(m.interval_s > 0.0 && m.eval_episodes >= 1 && m.ema >= 0.0 && m.ema < 1.0,
@@ -255,6 +256,7 @@ class Pipeline {
     mcfg_ = m;
     closs_ema_.f = aloss_ema_.f = m.ema;
     writer_ = std::make_unique<MetricsWriter>(m.path);
+    evaluator_ = std::make_unique<Evaluator>(cfg_, dims_, m.eval_episodes, m.eval_seed);
   }
 
   void record_snapshots(bool on) { record_snapshots_ = on; }
@@ -620,8 +622,7 @@ class Pipeline {
   }
   void append_row() {
     double mu = 0.0, se = 0.0;
-    evaluate_policy(cfg_, dims_, ev_pol_.data(), ev_count_, ev_mean_.data(), ev_m2_.data(),
-                    mcfg_.eval_episodes, mcfg_.eval_seed, nullptr, &mu, &se);
+    evaluator_->run(ev_pol_.data(), ev_count_, ev_mean_.data(), ev_m2_.data(), nullptr, &mu, &se);
     pqlg_metrics_row r{};
     r.wall_clock_s =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count();
@@ -683,6 +684,7 @@ class Pipeline {
   // metrics / evaluator
   pqlg_metrics_config mcfg_{};
   std::unique_ptr<MetricsWriter> writer_;
+  std::unique_ptr<Evaluator> evaluator_;  // allocated once at set_metrics
   std::mutex ema_mu_;
   Ema closs_ema_, aloss_ema_;
   std::chrono::steady_clock::time_point t0_;
@@ -716,6 +718,8 @@ pqlg_run_report run_synchronous(const pqlg_config& cfg, const pqlg_task_dims& di
     closs.f = aloss.f = mc->ema;
     writer = std::make_unique<MetricsWriter>(mc->path);
   }
+  std::unique_ptr<Evaluator> evaluator;
+  if (writer) evaluator = std::make_unique<Evaluator>(cfg, dims, mc->eval_episodes, mc->eval_seed);
   cudaStream_t st;
   PQLG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   struct StreamGuard {
@@ -742,8 +746,7 @@ pqlg_run_report run_synchronous(const pqlg_config& cfg, const pqlg_task_dims& di
     PQLG_CUDA(cudaMemcpyAsync(m2.data(), actor.m2_dev(), D * 8, cudaMemcpyDeviceToHost, st));
     PQLG_CUDA(cudaStreamSynchronize(st));
     double mu = 0.0, se = 0.0;
-    evaluate_policy(cfg, dims, pol.data(), count, mean.data(), m2.data(), mc->eval_episodes,
-                    mc->eval_seed, nullptr, &mu, &se);
+    evaluator->run(pol.data(), count, mean.data(), m2.data(), nullptr, &mu, &se);
     pqlg_metrics_row r{};
     r.wall_clock_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     r.env_steps = ca * N;

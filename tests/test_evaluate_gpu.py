@@ -68,3 +68,35 @@ def test_evaluate_vs_reference_golden(k, prec):
           f"stderr {se.value:.8f}/{want_se:.8f}")
     assert abs(mu.value - want_mu) <= bar * abs(want_mu) + 1e-6
     assert abs(se.value - want_se) <= 10 * bar * abs(want_se) + 1e-6
+
+
+@pytest.mark.parametrize("algo", [_lib.ALGO_DDPG, _lib.ALGO_SAC])
+def test_evaluator_reuse_equals_fresh(algo):
+    """The metrics loops keep one Evaluator (env, policy and buffers allocated
+    once) and run it per row: each run must equal a fresh pqlg_evaluate of the
+    same policy, bit for bit (env streams restored, episodes restarted)."""
+    D, A, H, nh, M = 13, 5, 64, 2, 80
+    rng = np.random.default_rng(9)
+    hout = 2 * A if algo == _lib.ALGO_SAC else A
+    ps = [D] + [H] * nh + [hout]
+    P = param_count(ps)
+    pols = f32(rng.standard_normal((3, P)) * 0.1)
+    pols[2] = pols[0]  # a policy seen before returns the same episodes
+    mean = rng.standard_normal(D) * 0.1
+    m2 = np.abs(rng.standard_normal(D)) * 50 + 10
+    cfg = _lib.default_config(hidden=H, hidden_layers=nh, max_episode_len=60, algo=algo)
+    dims = _lib.TaskDims(D, A, -1.0, 1.0)
+    ns = _lib.NormStats(100, ptr(mean), ptr(m2))
+    ret = np.zeros((3, M))
+    mu, se = np.zeros(3), np.zeros(3)
+    _lib.call("pqlg_k_evaluate_seq", C.byref(cfg), C.byref(dims), ptr(pols), 3, C.byref(ns), M, 31,
+              ptr(ret), ptr(mu), ptr(se))
+    for k in range(3):
+        want = np.zeros(M)
+        m1, s1 = C.c_double(), C.c_double()
+        _lib.call("pqlg_evaluate", C.byref(cfg), C.byref(dims), ptr(np.ascontiguousarray(pols[k])),
+                  C.byref(ns), M, 31, ptr(want), C.byref(m1), C.byref(s1))
+        np.testing.assert_array_equal(ret[k], want)
+        assert (mu[k], se[k]) == (m1.value, s1.value)
+    np.testing.assert_array_equal(ret[2], ret[0])
+    assert not np.array_equal(ret[1], ret[0])
