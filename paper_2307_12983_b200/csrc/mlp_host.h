@@ -34,6 +34,35 @@ inline int hidden_slots(int N) {
 }
 constexpr int kSMs = 148;
 
+// Single-net forward layers (the policy MLPs, groups == 1): when twice the
+// 128-row x 256-column tiles still fit in one wave on the SMs, 128-column
+// tiles fill twice as many of them (c2 actor step 41.1 -> 36.9 us, c1 25.8 ->
+// 22.5 us).  At B = 8192 the doubled count would need a second wave (c3
+// critic +1.5 us, 3xTF32 +35 us measured), so 256 stays.  PQLG_BN_FILL=0
+// disables (A/B knob, read once).
+inline bool bn_fill() {
+  static const bool on = [] {
+    const char* e = std::getenv("PQLG_BN_FILL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+inline int fwd_bn(int M, int N, int groups) {
+  const int bn = bn_for(N);
+  if (groups == 1 && bn == 256 && bn_fill() && 2 * ((M + 127) / 128) * ((N + 255) / 256) <= kSMs)
+    return 128;
+  return bn;
+}
+
+template <class F>
+void with_bn_value(int bn, F&& f) {
+  switch (bn) {
+    case 256: f(std::integral_constant<int, 256>{}); break;
+    case 128: f(std::integral_constant<int, 128>{}); break;
+    case 64: f(std::integral_constant<int, 64>{}); break;
+    default: f(std::integral_constant<int, 32>{}); break;
+  }
+}
 template <class F>
 void with_bn(int N, F&& f) {
   switch (bn_for(N)) {
@@ -73,7 +102,12 @@ Step fwd(const float* A0, const float* A1, int64_t lda, const float* W0, const f
   Step step;
   if (ldw == 0) ldw = N;
   if (ldd == 0) ldd = N;
-  with_bn(N, [&](auto bn) {
+  int bn_sel = bn_for(N);
+  if constexpr (std::is_same_v<Epi, epi::Hidden>) {
+    bn_sel = fwd_bn(M, N, groups);
+    epi.bn = bn_sel;
+  }
+  with_bn_value(bn_sel, [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
     gemm::Operands ops;
     ops.a[0] = gemm::map_a(A0, M, K, lda, false, gemm::tf32_maps());
