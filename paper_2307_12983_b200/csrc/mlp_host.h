@@ -34,11 +34,12 @@ inline int hidden_slots(int N) {
 }
 constexpr int kSMs = 148;
 
-// Single-net forward layers (the policy MLPs, groups == 1): when twice the
-// 128-row x 256-column tiles still fit in one wave on the SMs, 128-column
-// tiles fill twice as many of them (c2 actor step 41.1 -> 36.9 us, c1 25.8 ->
-// 22.5 us).  At B = 8192 the doubled count would need a second wave (c3
-// critic +1.5 us, 3xTF32 +35 us measured), so 256 stays.  PQLG_BN_FILL=0
+// Small launches: when twice the 128-row x 256-column tiles (all groups)
+// still fit in one wave on the SMs, 128-column tiles fill twice as many of
+// them (c2 actor step 41.1 -> 36.9 us, c1 25.8 -> 22.6 us).  At B = 8192 the
+// doubled count would need a second wave (c3 critic +1.5 us, 3xTF32 +35 us
+// measured), so 256 stays: c2 / c3 learners are unchanged.  Applies to the
+// epilogues whose tile width is a run-time field (`bn`).  PQLG_BN_FILL=0
 // disables (A/B knob, read once).
 inline bool bn_fill() {
   static const bool on = [] {
@@ -47,11 +48,24 @@ inline bool bn_fill() {
   }();
   return on;
 }
-inline int fwd_bn(int M, int N, int groups) {
+inline int fill_bn(int M, int N, int groups) {
   const int bn = bn_for(N);
-  if (groups == 1 && bn == 256 && bn_fill() && 2 * ((M + 127) / 128) * ((N + 255) / 256) <= kSMs)
+  if (bn == 256 && bn_fill() && 2 * ((M + 127) / 128) * ((N + 255) / 256) * groups <= kSMs)
     return 128;
   return bn;
+}
+template <class E, class = void>
+struct has_bn : std::false_type {};
+template <class E>
+struct has_bn<E, std::void_t<decltype(std::declval<E&>().bn)>> : std::true_type {};
+// The tile width of a launch over [M x N] x groups; sets epi.bn to match.
+template <class Epi>
+int pick_bn(int M, int N, int groups, Epi& epi) {
+  if constexpr (has_bn<Epi>::value) {
+    epi.bn = fill_bn(M, N, groups);
+    return epi.bn;
+  }
+  return bn_for(N);
 }
 
 template <class F>
@@ -102,12 +116,7 @@ Step fwd(const float* A0, const float* A1, int64_t lda, const float* W0, const f
   Step step;
   if (ldw == 0) ldw = N;
   if (ldd == 0) ldd = N;
-  int bn_sel = bn_for(N);
-  if constexpr (std::is_same_v<Epi, epi::Hidden>) {
-    bn_sel = fwd_bn(M, N, groups);
-    epi.bn = bn_sel;
-  }
-  with_bn_value(bn_sel, [&](auto bn) {
+  with_bn_value(pick_bn(M, N, groups, epi), [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
     gemm::Operands ops;
     ops.a[0] = gemm::map_a(A0, M, K, lda, false, gemm::tf32_maps());
@@ -134,7 +143,7 @@ Step fwd_groups(const float* const* A, int64_t lda, const float* const* W, int M
   Step step;
   if (ldw == 0) ldw = N;
   if (ldd == 0) ldd = N;
-  with_bn(N, [&](auto bn) {
+  with_bn_value(pick_bn(M, N, groups, epi), [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
     gemm::Operands ops;
     std::memset(&ops, 0, sizeof(ops));
@@ -159,7 +168,7 @@ Step dgrad(const float* G0, const float* G1, int64_t ldg, const float* W0, const
            const float* D0 = nullptr, const float* D1 = nullptr, int64_t ldd = 0) {
   if (ldd == 0) ldd = N_in;
   Step step;
-  with_bn(N_in, [&](auto bn) {
+  with_bn_value(pick_bn(M, N_in, groups, epi), [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
     gemm::Operands ops;
     ops.a[0] = gemm::map_a(G0, M, N_out, ldg, false, gemm::tf32_maps());
