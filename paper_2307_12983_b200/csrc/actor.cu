@@ -53,17 +53,17 @@ struct DeviceEnv {
     s.alloc(static_cast<size_t>(N) * ld);
     auto m = coupling_matrix(seed, D, A);
     M.alloc(m.size());
-    PQLG_CUDA(cudaMemcpy(M.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice));
+    copy_sync(M.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice);
     if (A <= actor::kMaxA && D <= actor::kMaxD) {
       const auto t = actor::env_transpose_M(m, D, A);
       MT.alloc(t.size());
-      PQLG_CUDA(cudaMemcpy(MT.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+      copy_sync(MT.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice);
     }
     ep.alloc(N);
     std::vector<uint64_t> r(N);
     for (int i = 0; i < N; ++i) r[i] = rng::derive_seed(seed, rng::kEnv, offset + i);
     rng.alloc(N);
-    PQLG_CUDA(cudaMemcpy(rng.p, r.data(), N * 8, cudaMemcpyHostToDevice));
+    copy_sync(rng.p, r.data(), N * 8, cudaMemcpyHostToDevice);
   }
   actor::EnvState view() const {
     return actor::EnvState{s.p, ld, s.p, ld, M.p, reinterpret_cast<const float4*>(MT.p), ep.p, rng.p,
@@ -180,7 +180,7 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
   std::vector<float> pol;
   init_orthogonal(pnet_, pol, prng, static_cast<float>(std::sqrt(2.0)), 1e-2f);
   pol_.alloc(snapshot_len());  // [net | log_alpha] for pql_sac (log_alpha unused here)
-  PQLG_CUDA(cudaMemcpy(pol_.p, pol.data(), pol.size() * 4, cudaMemcpyHostToDevice));
+  copy_sync(pol_.p, pol.data(), pol.size() * 4, cudaMemcpyHostToDevice);
 
   // exploration: build_schedule over the global env count (noise.hpp:23-42;
   // a sharded actor takes its slice of the one global schedule), per-env
@@ -202,11 +202,11 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
     sig[i] = v;
   }
   sigma_.alloc(N_);
-  PQLG_CUDA(cudaMemcpy(sigma_.p, sig.data(), N_ * 4, cudaMemcpyHostToDevice));
+  copy_sync(sigma_.p, sig.data(), N_ * 4, cudaMemcpyHostToDevice);
   std::vector<uint64_t> nr(N_);
   for (int i = 0; i < N_; ++i) nr[i] = rng::derive_seed(cfg.seed, rng::kNoise, cfg.env_offset + i);
   noise_rng_.alloc(N_);
-  PQLG_CUDA(cudaMemcpy(noise_rng_.p, nr.data(), N_ * 8, cudaMemcpyHostToDevice));
+  copy_sync(noise_rng_.p, nr.data(), N_ * 8, cudaMemcpyHostToDevice);
 
   // environment + initial observations (make_env -> reset_all, learners.cpp:66-68)
   env_ = std::make_unique<DeviceEnv>(N_, D_, A_, cfg.seed, cfg.max_episode_len, cfg.env_offset,
@@ -230,7 +230,7 @@ Actor::Actor(const pqlg_config& cfg, const pqlg_task_dims& dims, cudaStream_t st
   inv_f_.alloc(D_);
   identity_.alloc(1);
   const int one = 1;
-  PQLG_CUDA(cudaMemcpy(identity_.p, &one, 4, cudaMemcpyHostToDevice));
+  copy_sync(identity_.p, &one, 4, cudaMemcpyHostToDevice);
   npart_.alloc(static_cast<size_t>(actor::kNormBlocks) * D_ * 2);
   if (comm_) {
     require(D_ <= 1024, "actor: sharded normalizer needs obs_dim <= 1024");
@@ -609,7 +609,7 @@ Evaluator::Evaluator(const pqlg_config& cfg, const pqlg_task_dims& dims, int epi
   e.env = std::make_unique<DeviceEnv>(N, D, A, eval_seed, cfg.max_episode_len, 0, dims.low,
                                       dims.high);
   e.rng0.alloc(N);
-  PQLG_CUDA(cudaMemcpy(e.rng0.p, e.env->rng.p, N * 8, cudaMemcpyDeviceToDevice));
+  copy_sync(e.rng0.p, e.env->rng.p, N * 8, cudaMemcpyDeviceToDevice);
   e.Dp = round_up(D, 4);
   e.Ap = round_up(A, 4);
   for (auto& o : e.obs) o.alloc(static_cast<size_t>(N) * e.Dp);
@@ -882,7 +882,8 @@ int pqlg_env_step(pqlg_env h, const float* act_dev, int64_t ld_act, float* next_
     PQLG_CUDA(cudaMemcpyAsync(&st, h->status.p, 4, cudaMemcpyDeviceToHost, h->stream));
     PQLG_CUDA(cudaStreamSynchronize(h->stream));
     if (st) {
-      PQLG_CUDA(cudaMemset(h->status.p, 0, 4));
+      PQLG_CUDA(cudaMemsetAsync(h->status.p, 0, 4, h->stream));
+      PQLG_CUDA(cudaStreamSynchronize(h->stream));
       throw Error(PQLG_ENONFINITE, "step: non-finite action (upstream divergence)");
     }
   });

@@ -116,7 +116,11 @@ int guarded(F&& f) {
   }
 }
 
-// Owning device allocation (cudaMalloc; zero-initialised).
+// Owning device allocation (cudaMalloc; zero-initialised before alloc()
+// returns: cudaMemset is queued on the legacy stream, which does not order
+// with the library's non-blocking streams, so without the wait a kernel
+// launched right after construction could run before the zeroing lands and
+// have its writes (counters, normalizer state) zeroed after it).
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -137,6 +141,7 @@ struct DevBuf {
     if (count) {
       PQLG_CUDA(cudaMalloc(&p, count * sizeof(T)));
       PQLG_CUDA(cudaMemset(p, 0, count * sizeof(T)));
+      PQLG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
     }
   }
   void release() {
@@ -147,6 +152,14 @@ struct DevBuf {
   size_t bytes() const { return n * sizeof(T); }
   T* get() const { return p; }
 };
+
+// Synchronous copy for construction-time setup: cudaMemcpy can return before
+// an H2D (pageable) or D2D copy has landed, on the legacy stream, which does
+// not order with the library's non-blocking streams; wait for it.
+inline void copy_sync(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  PQLG_CUDA(cudaMemcpy(dst, src, bytes, kind));
+  PQLG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+}
 
 // Owning pinned host allocation (cudaMallocHost): truly asynchronous copies.
 template <class T>

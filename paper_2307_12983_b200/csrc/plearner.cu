@@ -86,9 +86,9 @@ PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   m_.alloc(snapshot_len());
   v_.alloc(snapshot_len());
   grads_.alloc(pnet_.params);
-  PQLG_CUDA(cudaMemcpy(q_.p, q1.data(), q1.size() * 4, cudaMemcpyHostToDevice));
-  PQLG_CUDA(cudaMemcpy(q_.p + Ps_, q2.data(), q2.size() * 4, cudaMemcpyHostToDevice));
-  PQLG_CUDA(cudaMemcpy(pol_.p, pol.data(), pol.size() * 4, cudaMemcpyHostToDevice));
+  copy_sync(q_.p, q1.data(), q1.size() * 4, cudaMemcpyHostToDevice);
+  copy_sync(q_.p + Ps_, q2.data(), q2.size() * 4, cudaMemcpyHostToDevice);
+  copy_sync(pol_.p, pol.data(), pol.size() * 4, cudaMemcpyHostToDevice);
 
   states_ = std::make_unique<DeviceStates>(cfg.buffer_capacity, D_, stream_);
   norm_.init(D_);
@@ -96,7 +96,7 @@ PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   // make_rng(seed, sample, 2) (learners.cpp:212); data-parallel rank r: 2 + 2r
   const uint64_t skey = rng::derive_seed(cfg.seed, rng::kSample, 2 + 2 * static_cast<uint64_t>(rank_));
   replay::SamplerState s0{skey, 0, 0, 0};
-  PQLG_CUDA(cudaMemcpy(sampler_.p, &s0, sizeof(s0), cudaMemcpyHostToDevice));
+  copy_sync(sampler_.p, &s0, sizeof(s0), cudaMemcpyHostToDevice);
   mt_.seed(skey);
   idx_.alloc(B_);
   idx_host_.resize(B_);
@@ -107,7 +107,7 @@ PLearner::PLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   step_.alloc(1);
   auto tab = mlp::adam_bias_table(0.9, 0.999);
   bc_.alloc(tab.size());
-  PQLG_CUDA(cudaMemcpy(bc_.p, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  copy_sync(bc_.p, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice);
   status_.alloc(1);
   hbuf_.alloc(2);
   loss_.alloc(2);  // actor loss (+ pql_sac: mean log-prob for the alpha update)
@@ -173,7 +173,7 @@ void PLearner::build_update() {
   if (dist_) {
     const auto z = c51_atoms(L_, static_cast<float>(cfg_.vmin), static_cast<float>(cfg_.vmax));
     atoms_.alloc(L_);
-    PQLG_CUDA(cudaMemcpy(atoms_.p, z.data(), L_ * 4, cudaMemcpyHostToDevice));
+    copy_sync(atoms_.p, z.data(), L_ * 4, cudaMemcpyHostToDevice);
     probs_.alloc(2ull * B * Lp_);
     ev_.alloc(2ull * B);
     up51_.alloc(2ull * B * Lp_);

@@ -36,13 +36,13 @@ struct EpsStream {
     if (blocks < 1) blocks = 1;
     st.alloc(1);
     const sac::EpsState s0{key, 0};
-    PQLG_CUDA(cudaMemcpy(st.p, &s0, sizeof(s0), cudaMemcpyHostToDevice));
+    copy_sync(st.p, &s0, sizeof(s0), cudaMemcpyHostToDevice);
     out.alloc(static_cast<size_t>(n));
     counts.alloc(blocks);
     ticket.alloc(1);
     last_j.alloc(1);
     const int64_t none = -1;
-    PQLG_CUDA(cudaMemcpy(last_j.p, &none, 8, cudaMemcpyHostToDevice));
+    copy_sync(last_j.p, &none, 8, cudaMemcpyHostToDevice);
     mt.seed(key);
     host.resize(static_cast<size_t>(n));
   }

@@ -88,10 +88,10 @@ VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   v_.alloc(2 * Ps);
   grads_.alloc(2 * Ps);
   lagged_.alloc(snapshot_len());  // [net | log_alpha] for pql_sac
-  PQLG_CUDA(cudaMemcpy(q_.p, q1.data(), P * 4, cudaMemcpyHostToDevice));
-  PQLG_CUDA(cudaMemcpy(q_.p + Ps, q2.data(), P * 4, cudaMemcpyHostToDevice));
-  PQLG_CUDA(cudaMemcpy(qt_.p, q_.p, 2 * Ps * 4, cudaMemcpyDeviceToDevice));
-  PQLG_CUDA(cudaMemcpy(lagged_.p, pol.data(), pnet_.params * 4, cudaMemcpyHostToDevice));
+  copy_sync(q_.p, q1.data(), P * 4, cudaMemcpyHostToDevice);
+  copy_sync(q_.p + Ps, q2.data(), P * 4, cudaMemcpyHostToDevice);
+  copy_sync(qt_.p, q_.p, 2 * Ps * 4, cudaMemcpyDeviceToDevice);
+  copy_sync(lagged_.p, pol.data(), pnet_.params * 4, cudaMemcpyHostToDevice);
 
   // --- replay + n-step (learners.cpp:131-136)
   replay_ = std::make_unique<DeviceReplay>(cfg.buffer_capacity, D_, A_, st);
@@ -102,7 +102,7 @@ VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   // rank r draws from its own stream 1 + 2r (rank 0 = the reference's)
   const uint64_t skey = rng::derive_seed(cfg.seed, rng::kSample, 1 + 2 * static_cast<uint64_t>(rank_));
   replay::SamplerState s0{skey, 0, 0, 0};
-  PQLG_CUDA(cudaMemcpy(sampler_.p, &s0, sizeof(s0), cudaMemcpyHostToDevice));
+  copy_sync(sampler_.p, &s0, sizeof(s0), cudaMemcpyHostToDevice);
   mt_.seed(skey);
   idx_.alloc(B_);
   idx_host_.resize(B_);
@@ -115,7 +115,7 @@ VLearner::VLearner(const pqlg_config& cfg, const pqlg_task_dims& dims, uint64_t 
   step_.alloc(1);
   auto tab = mlp::adam_bias_table(0.9, 0.999);
   bc_.alloc(tab.size());
-  PQLG_CUDA(cudaMemcpy(bc_.p, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  copy_sync(bc_.p, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice);
   status_.alloc(1);
   hbuf_.alloc(2);
   loss_.alloc(1);
@@ -177,7 +177,7 @@ void VLearner::build_update() {
   if (dist_) {
     const auto z = c51_atoms(L_, static_cast<float>(cfg_.vmin), static_cast<float>(cfg_.vmax));
     atoms_.alloc(L_);
-    PQLG_CUDA(cudaMemcpy(atoms_.p, z.data(), L_ * 4, cudaMemcpyHostToDevice));
+    copy_sync(atoms_.p, z.data(), L_ * 4, cudaMemcpyHostToDevice);
     probs_t_.alloc(2ull * B * Lp_);
     probs_o_.alloc(2ull * B * Lp_);
     ev_t_.alloc(2ull * B);
